@@ -1,0 +1,201 @@
+/*
+ * dla.h — C-ABI of the B200-native batched differentiable linear-algebra
+ * operator set (libdla_b200.so).
+ *
+ * This is the drop-in boundary for the reference's operator layer
+ * (/root/reference/proj/include/dlinalg; "dl/" below).  Every entry point is
+ * a batched, stream-ordered replacement of one reference `*_inplace` /
+ * `*_into` / `*_backward_into` function, with the same argument meaning,
+ * flags, aliasing rules and error taxonomy:
+ *
+ *   layout     packed row-major, batch-major: matrix b of an r x c operand
+ *              starts at ptr + b*r*c (dl/matrix.hpp:181-213, BatchTensor).
+ *   pointers   all matrix/vector pointers are DEVICE pointers.
+ *   flags      int 0/1, exactly the reference's bool flags.
+ *   info       optional (nullable) device int32[batch].  0 = slice OK, else
+ *              DLA_INFO(code, index): code is a dla_status, index the
+ *              reference exception's payload (pivot step, zero-diagonal
+ *              index, rank row, QL iteration count).  The first failing
+ *              slice's info is what the reference would have thrown
+ *              (dl/matrix.hpp:232-239); use dla_info_check() to read it.
+ *   workspace  caller-owned device scratch sized by dla_workspace_bytes();
+ *              no entry point allocates device memory.
+ *   stream     cudaStream_t passed as void*; 0 = legacy default stream.
+ *
+ * Host-side validation (shape, aliasing) runs before any launch and
+ * returns a status synchronously; numerical failures are per-slice and
+ * land in info[].  The reference throws for aliasing that it forbids
+ * (dl/blas.hpp:33-38, :58-59, :146, :197): these return DLA_ERR_ALIAS.
+ *
+ * Precision: the f64 path computes in IEEE binary64 end to end (FP64 DMMA
+ * tensor cores for the blocked contractions); the f32 path computes in
+ * binary32 with FFMA (no TF32 rounding), see DESIGN.md "fp32 policy".
+ */
+#ifndef DLA_B200_H_
+#define DLA_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error taxonomy: dl/common.hpp:20-57. */
+typedef enum dla_status {
+  DLA_OK = 0,
+  DLA_ERR_SHAPE = 1,        /* ShapeError: dims / non-square / m > n       */
+  DLA_ERR_NOT_SPD = 2,      /* NotPositiveDefiniteError{step}              */
+  DLA_ERR_SINGULAR = 3,     /* SingularError{index}                        */
+  DLA_ERR_CONVERGENCE = 4,  /* ConvergenceError{iterations}                */
+  DLA_ERR_ALIAS = 5,        /* Error: output must not alias this input     */
+  DLA_ERR_ASYMMETRIC = 6,   /* ShapeError: input is not symmetric          */
+  DLA_ERR_CUDA = 7,         /* launch / runtime failure                    */
+  DLA_ERR_WORKSPACE = 8,    /* workspace missing or too small              */
+  DLA_ERR_INVALID = 9       /* bad argument (negative batch, null pointer) */
+} dla_status;
+
+#define DLA_INFO(code, index) (((int32_t)(code) << 24) | ((int32_t)(index) & 0xFFFFFF))
+#define DLA_INFO_CODE(v) ((int32_t)(v) >> 24)
+#define DLA_INFO_INDEX(v) ((int32_t)(v) & 0xFFFFFF)
+
+typedef enum dla_op {
+  DLA_OP_GEMM = 0, DLA_OP_GEMM2 = 1, DLA_OP_SYRK = 2, DLA_OP_TRMM = 3,
+  DLA_OP_TRSM = 4, DLA_OP_POTRF = 5, DLA_OP_POTRI = 6, DLA_OP_SUMLOGDIAG = 7,
+  DLA_OP_GELQF = 8, DLA_OP_SYEVD = 9
+} dla_op;
+
+typedef enum dla_dtype { DLA_F32 = 0, DLA_F64 = 1 } dla_dtype;
+
+/* dla_workspace_bytes flags */
+#define DLA_WS_BACKWARD 1
+
+const char* dla_status_string(dla_status s);
+const char* dla_version(void);
+
+/* Device scratch (bytes) the op needs for the given problem; 0 = none.
+ * Budgets mirror dl/adjoints.hpp:1-9: gelqf fwd m per slice (tau), gelqf bwd
+ * m*m, syevd fwd/bwd n*n (+ small), everything else 0.  `phase` is 0
+ * (forward) or DLA_WS_BACKWARD. */
+size_t dla_workspace_bytes(dla_op op, dla_dtype dtype, int64_t batch, int64_t m,
+                           int64_t n, int64_t k, int phase);
+
+/* Reads info[0..batch) (synchronises `stream`).  Returns DLA_OK when every
+ * slice is clean, else the first failing slice's code, with *first_bad /
+ * *index set (each nullable). */
+dla_status dla_info_check(const int32_t* info, int64_t batch, void* stream,
+                          int64_t* first_bad, int64_t* index);
+
+/* ---------------------------------------------------------------- macros */
+/* Each operator is declared for f32 and f64 through one prototype list.   */
+
+#define DLA_DECLARE_OPS(T, S)                                                       \
+  /* gemm2: C = alpha op(A) op(B); dl/blas.hpp:119-122 (gemm_accum :43-110).      \
+     A is (ta ? k x m : m x k), B is (tb ? n x k : k x n), C is m x n.           \
+     C must not alias A or B. */                                                    \
+  dla_status dla_gemm2_fwd_##S(int64_t batch, int64_t m, int64_t n, int64_t k,      \
+                               T* c, const T* a, const T* b, int ta, int tb,        \
+                               T alpha, void* stream);                              \
+  /* gemm: C = alpha op(A) op(B) + beta C.  beta = 0 / 1 are the reference's        \
+     gemm_accum(accumulate = false / true) (dl/blas.hpp:43-110); other beta         \
+     scale C first. */                                                              \
+  dla_status dla_gemm_fwd_##S(int64_t batch, int64_t m, int64_t n, int64_t k,       \
+                              T* c, const T* a, const T* b, int ta, int tb,         \
+                              T alpha, T beta, void* stream);                       \
+  /* gemm2 / gemm pullback: dl/adjoints.hpp:36-49 (Abar written before Bbar). */    \
+  dla_status dla_gemm2_bwd_##S(int64_t batch, int64_t m, int64_t n, int64_t k,      \
+                               T* abar, T* bbar, const T* cbar, const T* a,         \
+                               const T* b, int ta, int tb, T alpha, void* stream);  \
+  /* gemm pullback: abar/bbar as gemm2; cbar_io <- beta * cbar_io (the C-input     \
+     cotangent), after abar/bbar are formed. */                                     \
+  dla_status dla_gemm_bwd_##S(int64_t batch, int64_t m, int64_t n, int64_t k,       \
+                              T* abar, T* bbar, T* cbar_io, const T* a,             \
+                              const T* b, int ta, int tb, T alpha, T beta,          \
+                              void* stream);                                        \
+  /* syrk: B = alpha A A^T (ta=0, A n x k) / alpha A^T A (ta=1, A k x n),           \
+     bit-exactly symmetric; dl/blas.hpp:138-169. */                                 \
+  dla_status dla_syrk_fwd_##S(int64_t batch, int64_t n, int64_t k, T* b,            \
+                              const T* a, int ta, T alpha, void* stream);           \
+  /* syrk pullback: dl/adjoints.hpp:69-78. */                                       \
+  dla_status dla_syrk_bwd_##S(int64_t batch, int64_t n, int64_t k, T* abar,         \
+                              const T* bbar, const T* a, int ta, T alpha,           \
+                              void* stream);                                        \
+  /* trmm: X <- alpha op(T) X (right=0) / alpha X op(T) (right=1); X m x n,         \
+     T m x m (left) or n x n (right); dl/blas.hpp:202-291. */                       \
+  dla_status dla_trmm_fwd_##S(int64_t batch, int64_t m, int64_t n, const T* t,      \
+                              T* x, int rightside, int transpose, int lower,        \
+                              T alpha, void* stream);                               \
+  /* trmm pullback (reads the forward INPUT a); abar may alias bbar;                \
+     dl/adjoints.hpp:94-110. */                                                     \
+  dla_status dla_trmm_bwd_##S(int64_t batch, int64_t m, int64_t n, T* abar,         \
+                              T* tbar, const T* bbar, const T* t, const T* a,       \
+                              int rightside, int transpose, int lower, T alpha,     \
+                              void* stream);                                        \
+  /* trsm: X <- alpha op(T)^-1 X / alpha X op(T)^-1; exact zero diagonal =>         \
+     SINGULAR(k) in info and the slice is left untouched; dl/blas.hpp:307-395. */   \
+  dla_status dla_trsm_fwd_##S(int64_t batch, int64_t m, int64_t n, const T* t,      \
+                              T* x, int rightside, int transpose, int lower,        \
+                              T alpha, int32_t* info, void* stream);                \
+  /* trsm pullback (reads the forward OUTPUT b); abar may alias bbar;               \
+     dl/adjoints.hpp:131-153. */                                                    \
+  dla_status dla_trsm_bwd_##S(int64_t batch, int64_t m, int64_t n, T* abar,         \
+                              T* tbar, const T* bbar, const T* t, const T* b,       \
+                              int rightside, int transpose, int lower, T alpha,     \
+                              void* stream);                                        \
+  /* potrf: A = L L^T (lower=1, strict upper zeroed) / A = R^T R (lower=0), in      \
+     place.  Asymmetric input => ASYMMETRIC (slice untouched); failed pivot =>      \
+     NOT_SPD(step); dl/cholesky.hpp:79-88. */                                       \
+  dla_status dla_potrf_fwd_##S(int64_t batch, int64_t n, T* a, int lower,           \
+                               int32_t* info, void* stream);                        \
+  /* potrf pullback: Abar = 1/2 L^-T copyltu(L^T Lbar) L^-1, exactly symmetric;     \
+     abar may alias lbar; dl/adjoints.hpp:175-191. */                               \
+  dla_status dla_potrf_bwd_##S(int64_t batch, int64_t n, T* abar, const T* lbar,    \
+                               const T* l, int lower, void* stream);                \
+  /* potri: B = A^-1 from the Cholesky factor, in place, exactly symmetric;         \
+     zero diagonal => SINGULAR(j); dl/cholesky.hpp:141-147. */                      \
+  dla_status dla_potri_fwd_##S(int64_t batch, int64_t n, T* a, int lower,           \
+                               int32_t* info, void* stream);                        \
+  /* potri pullback: Lbar = -tril((B Bbar + B Bbar^T) L^-T); dl/adjoints.hpp:207. */\
+  dla_status dla_potri_bwd_##S(int64_t batch, int64_t n, T* lbar, const T* bbar,    \
+                               const T* l, const T* b, int lower, void* stream);    \
+  /* sumlogdiag: out[b] = sum_i log A_b(i,i), sequential i order (tape chain        \
+     ExtractDiag->Log->Sum, dl/tape.hpp:789-795, :714, :747-755). */                \
+  dla_status dla_sumlogdiag_fwd_##S(int64_t batch, int64_t n, T* out, const T* a,   \
+                                    void* stream);                                  \
+  /* sumlogdiag pullback: abar(i,i) = gbar[b] / A(i,i), off-diagonal exactly 0      \
+     (accumulate=0) or untouched (accumulate=1: added onto the diagonal). */        \
+  dla_status dla_sumlogdiag_bwd_##S(int64_t batch, int64_t n, T* abar,              \
+                                    const T* gbar, const T* a, int accumulate,      \
+                                    void* stream);                                  \
+  /* gelqf: A (m x n, m <= n) = L Q; q: in A, out Q; l: out L (m x m, positive      \
+     diagonal); rank deficiency => SINGULAR(row); dl/lq.hpp:24-106.                 \
+     workspace: dla_workspace_bytes(DLA_OP_GELQF, ..., 0). */                       \
+  dla_status dla_gelqf_fwd_##S(int64_t batch, int64_t m, int64_t n, T* q, T* l,     \
+                               int32_t* info, void* ws, size_t ws_bytes,            \
+                               void* stream);                                       \
+  /* gelqf pullback: Abar = L^-T (Qbar + copyltu(L^T Lbar - Qbar Q^T) Q);           \
+     one m x m workspace per slice; dl/adjoints.hpp:239-252. */                     \
+  dla_status dla_gelqf_bwd_##S(int64_t batch, int64_t m, int64_t n, T* abar,        \
+                               const T* qbar, const T* lbar, const T* q,            \
+                               const T* l, void* ws, size_t ws_bytes,               \
+                               void* stream);                                       \
+  /* syevd: A = U^T diag(lambda) U, ROWS of U are eigenvectors, lambda              \
+     ascending, sign rule of dl/eigen_sym.hpp:316-333; u: in A, out U;              \
+     dl/eigen_sym.hpp:339-367. */                                                   \
+  dla_status dla_syevd_fwd_##S(int64_t batch, int64_t n, T* u, T* lambda,           \
+                               int32_t* info, void* ws, size_t ws_bytes,            \
+                               void* stream);                                       \
+  /* syevd pullback with the eps_gap guard; one n x n workspace per slice;          \
+     dl/adjoints.hpp:272-295. */                                                    \
+  dla_status dla_syevd_bwd_##S(int64_t batch, int64_t n, T* abar, const T* ubar,    \
+                               const T* lambdabar, const T* u, const T* lambda,     \
+                               T eps_gap, void* ws, size_t ws_bytes, void* stream);
+
+DLA_DECLARE_OPS(float, f32)
+DLA_DECLARE_OPS(double, f64)
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DLA_B200_H_ */

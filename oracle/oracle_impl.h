@@ -1,0 +1,879 @@
+/* CPU oracle — TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain-C restatement of the reference's dense kernels and closed-form
+ * pullbacks (dlinalg, /root/reference/proj/include/dlinalg).  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+ * may load this code, and only as the checker.  The product path
+ * (paper_1710_08717_b200, libdla_b200.so) never links or calls it.
+ *
+ * Parity pinning: every function here is checked against (1) the reference's
+ * own known-answer tests (tests/golden/kat.json, restated from
+ * proj/tests/test_*.cpp) and (2) the real reference compiled from its headers
+ * into oracle/_ref/libdla_ref.so (tests/test_oracle_vs_ref.py).
+ *
+ * This header is instantiated twice by dla_oracle.c: R = double / suffix _f64,
+ * R = float / suffix _f32.  Matrices are packed row-major, element (i, j) of an
+ * r x c matrix at p[i*c + j] — the reference MatrixView layout
+ * (dl/matrix.hpp:64-89).  Return value: a dla status code (include/dla.h);
+ * *idx receives the failing index where the reference exception carries one.
+ */
+
+#define AT(p, ld, i, j) ((p)[(size_t)(i) * (size_t)(ld) + (size_t)(j)])
+
+/* ----------------------------------------------------------------- helpers */
+
+static R FN(absr)(R v) { return v < (R)0 ? -v : v; }
+
+static R FN(max_abs)(const R* a, int64_t count) {
+  R m = (R)0;
+  for (int64_t i = 0; i < count; ++i) {
+    R v = FN(absr)(a[i]);
+    if (v > m) m = v;
+  }
+  return m;
+}
+
+/* dl/transforms.hpp:133-141 + dl/cholesky.hpp:19-25 */
+static int FN(symmetric_ok)(int64_t n, const R* a, R rtol) {
+  R asym = (R)0;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = i + 1; j < n; ++j) {
+      R d = FN(absr)(AT(a, n, i, j) - AT(a, n, j, i));
+      if (d > asym) asym = d;
+    }
+  R scale = FN(max_abs)(a, n * n);
+  return !(asym > rtol * (scale > (R)0 ? scale : (R)1));
+}
+
+static void FN(transpose_sq)(int64_t n, R* a) {
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = i + 1; j < n; ++j) {
+      R t = AT(a, n, i, j);
+      AT(a, n, i, j) = AT(a, n, j, i);
+      AT(a, n, j, i) = t;
+    }
+}
+
+/* dl/transforms.hpp:18-32, 49-61, 78-87 */
+void FN(o_copyltu)(int64_t n, R* a) {
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = i + 1; j < n; ++j) AT(a, n, i, j) = AT(a, n, j, i);
+}
+void FN(o_copyutl)(int64_t n, R* a) {
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = i + 1; j < n; ++j) AT(a, n, j, i) = AT(a, n, i, j);
+}
+void FN(o_tril)(int64_t n, R* a) {
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = i + 1; j < n; ++j) AT(a, n, i, j) = (R)0;
+}
+void FN(o_triu)(int64_t n, R* a) {
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < i; ++j) AT(a, n, i, j) = (R)0;
+}
+void FN(o_sym)(int64_t n, R* a) {
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = i + 1; j < n; ++j) {
+      R v = (AT(a, n, i, j) + AT(a, n, j, i)) / (R)2;
+      AT(a, n, i, j) = v;
+      AT(a, n, j, i) = v;
+    }
+}
+static void FN(scale)(R* a, int64_t count, R s) {
+  for (int64_t i = 0; i < count; ++i) a[i] *= s;
+}
+
+/* ------------------------------------------------------------------- gemm */
+
+/* C (+)= alpha op(A) op(B); dl/blas.hpp:43-110.  A is (ta ? k x m : m x k),
+ * B is (tb ? n x k : k x n), C is m x n.  Same four loop orders as the
+ * reference so rounding matches. */
+int FN(o_gemm)(int64_t m, int64_t n, int64_t k, R* c, const R* a, const R* b,
+               int ta, int tb, R alpha, int accumulate) {
+  if (m < 0 || n < 0 || k < 0) return DLA_ERR_SHAPE;
+  if (c == a || c == b) return DLA_ERR_ALIAS;
+  const int64_t lda = ta ? m : k, ldb = tb ? k : n;
+  if (!accumulate)
+    for (int64_t i = 0; i < m * n; ++i) c[i] = (R)0;
+  if (!ta && !tb) {
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t p = 0; p < k; ++p) {
+        const R av = alpha * AT(a, lda, i, p);
+        for (int64_t j = 0; j < n; ++j) AT(c, n, i, j) += av * AT(b, ldb, p, j);
+      }
+  } else if (ta && !tb) {
+    for (int64_t p = 0; p < k; ++p)
+      for (int64_t i = 0; i < m; ++i) {
+        const R av = alpha * AT(a, lda, p, i);
+        for (int64_t j = 0; j < n; ++j) AT(c, n, i, j) += av * AT(b, ldb, p, j);
+      }
+  } else if (!ta && tb) {
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t j = 0; j < n; ++j) {
+        R acc = (R)0;
+        for (int64_t p = 0; p < k; ++p) acc += AT(a, lda, i, p) * AT(b, ldb, j, p);
+        AT(c, n, i, j) += alpha * acc;
+      }
+  } else {
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t j = 0; j < n; ++j) {
+        R acc = (R)0;
+        for (int64_t p = 0; p < k; ++p) acc += AT(a, lda, p, i) * AT(b, ldb, j, p);
+        AT(c, n, i, j) += alpha * acc;
+      }
+  }
+  return DLA_OK;
+}
+
+/* dl/blas.hpp:119-122 */
+int FN(o_gemm2)(int64_t m, int64_t n, int64_t k, R* c, const R* a, const R* b,
+                int ta, int tb, R alpha) {
+  return FN(o_gemm)(m, n, k, c, a, b, ta, tb, alpha, 0);
+}
+
+/* syrk: B = alpha A A^T (ta=0, A n x k) or alpha A^T A (ta=1, A k x n);
+ * lower triangle computed, then mirrored (bit-exact symmetry);
+ * dl/blas.hpp:138-169. */
+int FN(o_syrk)(int64_t n, int64_t k, R* bo, const R* a, int ta, R alpha) {
+  if (bo == a) return DLA_ERR_ALIAS;
+  for (int64_t i = 0; i < n * n; ++i) bo[i] = (R)0;
+  if (!ta) {
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t j = 0; j <= i; ++j) {
+        R acc = (R)0;
+        for (int64_t p = 0; p < k; ++p) acc += AT(a, k, i, p) * AT(a, k, j, p);
+        AT(bo, n, i, j) = alpha * acc;
+      }
+  } else {
+    for (int64_t p = 0; p < k; ++p)
+      for (int64_t i = 0; i < n; ++i) {
+        const R av = alpha * AT(a, n, p, i);
+        for (int64_t j = 0; j <= i; ++j) AT(bo, n, i, j) += av * AT(a, n, p, j);
+      }
+  }
+  FN(o_copyltu)(n, bo);
+  return DLA_OK;
+}
+
+/* ------------------------------------------------------------- trmm / trsm */
+
+/* Effective element of op(T) restricted to the `lower`-selected triangle. */
+static R FN(tri_at)(const R* t, int64_t ld, int64_t i, int64_t j, int transpose, int lower) {
+  int64_t r = transpose ? j : i, c = transpose ? i : j;
+  if (lower ? (c > r) : (c < r)) return (R)0;
+  return AT(t, ld, r, c);
+}
+
+/* X <- alpha op(T) X (left) or alpha X op(T) (right); dl/blas.hpp:202-291.
+ * X is m x n; T is m x m (left) or n x n (right). */
+int FN(o_trmm)(int64_t m, int64_t n, const R* t, R* x, int rightside, int transpose,
+               int lower, R alpha) {
+  if (x == t) return DLA_ERR_ALIAS;
+  if (!rightside) {
+    /* effective lower => rows bottom-up keep the untouched rows above intact */
+    const int eff_lower = (lower != transpose);
+    for (int64_t s = 0; s < m; ++s) {
+      const int64_t i = eff_lower ? m - 1 - s : s;
+      const R dii = AT(t, m, i, i);
+      for (int64_t j = 0; j < n; ++j) AT(x, n, i, j) *= dii;
+      const int64_t p0 = eff_lower ? 0 : i + 1, p1 = eff_lower ? i : m;
+      for (int64_t p = p0; p < p1; ++p) {
+        const R tv = FN(tri_at)(t, m, i, p, transpose, lower);
+        if (tv == (R)0) continue;
+        for (int64_t j = 0; j < n; ++j) AT(x, n, i, j) += tv * AT(x, n, p, j);
+      }
+      if (alpha != (R)1)
+        for (int64_t j = 0; j < n; ++j) AT(x, n, i, j) *= alpha;
+    }
+    return DLA_OK;
+  }
+  for (int64_t r = 0; r < m; ++r) {
+    R* xr = x + r * n;
+    if (lower && !transpose) {
+      for (int64_t k = 0; k < n; ++k) {
+        const R v = xr[k];
+        for (int64_t j = 0; j < k; ++j) xr[j] += v * AT(t, n, k, j);
+        xr[k] = v * AT(t, n, k, k);
+      }
+    } else if (lower && transpose) {
+      for (int64_t j = n - 1; j >= 0; --j) {
+        R acc = (R)0;
+        for (int64_t k = 0; k <= j; ++k) acc += xr[k] * AT(t, n, j, k);
+        xr[j] = acc;
+      }
+    } else if (!lower && !transpose) {
+      for (int64_t k = n - 1; k >= 0; --k) {
+        const R v = xr[k];
+        for (int64_t j = k + 1; j < n; ++j) xr[j] += v * AT(t, n, k, j);
+        xr[k] = v * AT(t, n, k, k);
+      }
+    } else {
+      for (int64_t j = 0; j < n; ++j) {
+        R acc = (R)0;
+        for (int64_t k = j; k < n; ++k) acc += xr[k] * AT(t, n, j, k);
+        xr[j] = acc;
+      }
+    }
+    if (alpha != (R)1)
+      for (int64_t j = 0; j < n; ++j) xr[j] *= alpha;
+  }
+  return DLA_OK;
+}
+
+/* Solve op(T) Y = alpha X (left) or Y op(T) = alpha X (right), Y over X;
+ * dl/blas.hpp:307-395.  Exact zero diagonal => SINGULAR(k), checked over the
+ * whole diagonal before any write. */
+int FN(o_trsm)(int64_t m, int64_t n, const R* t, R* x, int rightside, int transpose,
+               int lower, R alpha, int64_t* idx) {
+  if (x == t) return DLA_ERR_ALIAS;
+  const int64_t nt = rightside ? n : m;
+  for (int64_t k = 0; k < nt; ++k)
+    if (AT(t, nt, k, k) == (R)0) {
+      if (idx) *idx = k;
+      return DLA_ERR_SINGULAR;
+    }
+  if (alpha != (R)1) FN(scale)(x, m * n, alpha);
+  if (!rightside) {
+    const int forward = (lower != transpose);
+    for (int64_t s = 0; s < m; ++s) {
+      const int64_t i = forward ? s : m - 1 - s;
+      const int64_t p0 = forward ? 0 : i + 1, p1 = forward ? i : m;
+      for (int64_t p = p0; p < p1; ++p) {
+        const R tv = FN(tri_at)(t, m, i, p, transpose, lower);
+        if (tv == (R)0) continue;
+        for (int64_t j = 0; j < n; ++j) AT(x, n, i, j) -= tv * AT(x, n, p, j);
+      }
+      const R inv = (R)1 / AT(t, m, i, i);
+      for (int64_t j = 0; j < n; ++j) AT(x, n, i, j) *= inv;
+    }
+    return DLA_OK;
+  }
+  for (int64_t r = 0; r < m; ++r) {
+    R* xr = x + r * n;
+    if (lower && !transpose) {
+      for (int64_t k = n - 1; k >= 0; --k) {
+        const R yk = xr[k] / AT(t, n, k, k);
+        xr[k] = yk;
+        for (int64_t j = 0; j < k; ++j) xr[j] -= yk * AT(t, n, k, j);
+      }
+    } else if (lower && transpose) {
+      for (int64_t j = 0; j < n; ++j) {
+        R acc = xr[j];
+        for (int64_t k = 0; k < j; ++k) acc -= xr[k] * AT(t, n, j, k);
+        xr[j] = acc / AT(t, n, j, j);
+      }
+    } else if (!lower && !transpose) {
+      for (int64_t k = 0; k < n; ++k) {
+        const R yk = xr[k] / AT(t, n, k, k);
+        xr[k] = yk;
+        for (int64_t j = k + 1; j < n; ++j) xr[j] -= yk * AT(t, n, k, j);
+      }
+    } else {
+      for (int64_t j = n - 1; j >= 0; --j) {
+        R acc = xr[j];
+        for (int64_t k = j + 1; k < n; ++k) acc -= xr[k] * AT(t, n, j, k);
+        xr[j] = acc / AT(t, n, j, j);
+      }
+    }
+  }
+  return DLA_OK;
+}
+
+/* --------------------------------------------------------- potrf / potri */
+
+static R FN(sym_rtol)(void) { return sizeof(R) == 8 ? (R)1e-10 : (R)1e-4; }
+
+/* dl/cholesky.hpp:35-72: nb = 64 panels, left-looking inside the panel,
+ * right-looking lower trailing update; strict upper zeroed at the end. */
+static int FN(potrf_lower)(int64_t n, R* a, int64_t* idx) {
+  const int64_t nb = 64;
+  for (int64_t k0 = 0; k0 < n; k0 += nb) {
+    const int64_t k1 = k0 + nb < n ? k0 + nb : n;
+    for (int64_t j = k0; j < k1; ++j) {
+      for (int64_t i = j; i < n; ++i) {
+        R acc = AT(a, n, i, j);
+        for (int64_t p = k0; p < j; ++p) acc -= AT(a, n, i, p) * AT(a, n, j, p);
+        AT(a, n, i, j) = acc;
+      }
+      const R d = AT(a, n, j, j);
+      if (!(d > (R)0)) {
+        if (idx) *idx = j;
+        return DLA_ERR_NOT_SPD;
+      }
+      const R r = (R)SQRT(d);
+      AT(a, n, j, j) = r;
+      const R inv = (R)1 / r;
+      for (int64_t i = j + 1; i < n; ++i) AT(a, n, i, j) *= inv;
+    }
+    for (int64_t i = k1; i < n; ++i)
+      for (int64_t j = k1; j <= i; ++j) {
+        R acc = (R)0;
+        for (int64_t p = k0; p < k1; ++p) acc += AT(a, n, i, p) * AT(a, n, j, p);
+        AT(a, n, i, j) -= acc;
+      }
+  }
+  FN(o_tril)(n, a);
+  return DLA_OK;
+}
+
+/* dl/cholesky.hpp:79-88 */
+int FN(o_potrf)(int64_t n, R* a, int lower, int64_t* idx) {
+  if (!FN(symmetric_ok)(n, a, FN(sym_rtol)())) return DLA_ERR_ASYMMETRIC;
+  int st = FN(potrf_lower)(n, a, idx);
+  if (st != DLA_OK) return st;
+  if (!lower) FN(transpose_sq)(n, a);
+  return DLA_OK;
+}
+
+/* dl/cholesky.hpp:105-147: trtri (column by column) + lauum + copyltu. */
+int FN(o_potri)(int64_t n, R* a, int lower, int64_t* idx) {
+  if (!lower) FN(transpose_sq)(n, a);
+  for (int64_t j = 0; j < n; ++j) {
+    if (AT(a, n, j, j) == (R)0) {
+      if (idx) *idx = j;
+      return DLA_ERR_SINGULAR;
+    }
+    AT(a, n, j, j) = (R)1 / AT(a, n, j, j);
+    for (int64_t i = j + 1; i < n; ++i) {
+      R acc = (R)0;
+      for (int64_t k = j; k < i; ++k) acc += AT(a, n, i, k) * AT(a, n, k, j);
+      AT(a, n, i, j) = -acc / AT(a, n, i, i);
+    }
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    const R wii = AT(a, n, i, i);
+    for (int64_t j = 0; j <= i; ++j) {
+      R acc = wii * AT(a, n, i, j);
+      for (int64_t k = i + 1; k < n; ++k) acc += AT(a, n, k, i) * AT(a, n, k, j);
+      AT(a, n, i, j) = acc;
+    }
+  }
+  FN(o_copyltu)(n, a);
+  return DLA_OK;
+}
+
+/* ------------------------------------------------------------- sumlogdiag */
+
+/* Tape chain ExtractDiag -> Log -> Sum (dl/tape.hpp:789-795, :714, :747-755):
+ * sequential sum over i = 0..n-1. */
+R FN(o_sumlogdiag)(int64_t n, const R* a) {
+  R acc = (R)0;
+  for (int64_t i = 0; i < n; ++i) acc += (R)LOG(AT(a, n, i, i));
+  return acc;
+}
+
+/* Pullback (dl/tape.hpp:1038-1045, :969-975, :1080-1086): abar zero except
+ * abar_ii = g / a_ii.  accumulate=1 adds onto the diagonal only. */
+void FN(o_sumlogdiag_bwd)(int64_t n, R* abar, R g, const R* a, int accumulate) {
+  if (!accumulate)
+    for (int64_t i = 0; i < n * n; ++i) abar[i] = (R)0;
+  for (int64_t i = 0; i < n; ++i) AT(abar, n, i, i) += g / AT(a, n, i, i);
+}
+
+/* ------------------------------------------------------------------ gelqf */
+
+/* A (m x n, m <= n) = L Q; q: in A, out Q; l: out L (m x m).
+ * dl/lq.hpp:24-106. */
+int FN(o_gelqf)(int64_t m, int64_t n, R* q, R* l, R* tau, int64_t* idx) {
+  if (m > n) return DLA_ERR_SHAPE;
+  const R norm_a = FN(max_abs)(q, m * n);
+  if (norm_a == (R)0) {
+    if (idx) *idx = 0;
+    return DLA_ERR_SINGULAR;
+  }
+  for (int64_t k = 0; k < m; ++k) {
+    R* xk = q + k * n;
+    R sigma = (R)0;
+    for (int64_t j = k + 1; j < n; ++j) sigma += xk[j] * xk[j];
+    const R alpha = xk[k];
+    if (sigma == (R)0) {
+      tau[k] = (R)0;
+      continue;
+    }
+    const R nrm = (R)SQRT(alpha * alpha + sigma);
+    const R beta = alpha >= (R)0 ? -nrm : nrm;
+    tau[k] = (beta - alpha) / beta;
+    const R sc = (R)1 / (alpha - beta);
+    for (int64_t j = k + 1; j < n; ++j) xk[j] *= sc;
+    xk[k] = beta;
+    for (int64_t i = k + 1; i < m; ++i) {
+      R* xi = q + i * n;
+      R w = xi[k];
+      for (int64_t j = k + 1; j < n; ++j) w += xi[j] * xk[j];
+      w *= tau[k];
+      xi[k] -= w;
+      for (int64_t j = k + 1; j < n; ++j) xi[j] -= w * xk[j];
+    }
+  }
+  const R rank_tol = (sizeof(R) == 8 ? (R)1e-12 : (R)1e-5) * norm_a;
+  for (int64_t i = 0; i < m; ++i) {
+    for (int64_t j = 0; j < m; ++j) AT(l, m, i, j) = j <= i ? AT(q, n, i, j) : (R)0;
+    if (FN(absr)(AT(l, m, i, i)) < rank_tol) {
+      if (idx) *idx = i;
+      return DLA_ERR_SINGULAR;
+    }
+  }
+  for (int64_t k = m - 1; k >= 0; --k) {
+    const R* vk = q + k * n;
+    const R tk = tau[k];
+    for (int64_t i = k + 1; i < m; ++i) {
+      R* xi = q + i * n;
+      R w = xi[k];
+      for (int64_t j = k + 1; j < n; ++j) w += xi[j] * vk[j];
+      w *= tk;
+      xi[k] -= w;
+      for (int64_t j = k + 1; j < n; ++j) xi[j] -= w * vk[j];
+    }
+    R* xk = q + k * n;
+    for (int64_t j = 0; j < k; ++j) xk[j] = (R)0;
+    for (int64_t j = k + 1; j < n; ++j) xk[j] = -tk * xk[j];
+    xk[k] = (R)1 - tk;
+  }
+  for (int64_t k = 0; k < m; ++k)
+    if (AT(l, m, k, k) < (R)0) {
+      for (int64_t i = k; i < m; ++i) AT(l, m, i, k) = -AT(l, m, i, k);
+      for (int64_t j = 0; j < n; ++j) AT(q, n, k, j) = -AT(q, n, k, j);
+    }
+  return DLA_OK;
+}
+
+/* ------------------------------------------------------------------ syevd */
+
+static R FN(pythag)(R a, R b) {  /* dl/common.hpp:109-119 */
+  const R aa = FN(absr)(a), ab = FN(absr)(b);
+  if (aa > ab) {
+    const R r = ab / aa;
+    return aa * (R)SQRT((R)1 + r * r);
+  }
+  if (ab == (R)0) return (R)0;
+  const R r = aa / ab;
+  return ab * (R)SQRT((R)1 + r * r);
+}
+
+static R FN(sign_like)(R a, R b) { return b >= (R)0 ? FN(absr)(a) : -FN(absr)(a); }
+
+/* Householder tridiagonalization, reflectors kept (dl/eigen_sym.hpp:34-97). */
+static void FN(tred1)(int64_t n, R* u, R* d, R* e, R* hout, R* v, R* y) {
+  for (int64_t i = n - 1; i >= 1; --i) {
+    const int64_t l = i - 1;
+    R h = (R)0, scale = (R)0;
+    if (l > 0) {
+      for (int64_t k = 0; k <= l; ++k) scale += FN(absr)(AT(u, n, k, i));
+      if (scale == (R)0) {
+        e[i] = AT(u, n, l, i);
+      } else {
+        for (int64_t k = 0; k <= l; ++k) {
+          AT(u, n, k, i) /= scale;
+          v[k] = AT(u, n, k, i);
+          h += v[k] * v[k];
+        }
+        R f = v[l];
+        const R g = f >= (R)0 ? -(R)SQRT(h) : (R)SQRT(h);
+        e[i] = scale * g;
+        h -= f * g;
+        AT(u, n, l, i) = f - g;
+        v[l] = f - g;
+        for (int64_t k = 0; k <= l; ++k) y[k] = (R)0;
+        for (int64_t r = 0; r <= l; ++r) {
+          const R vr = v[r];
+          R acc = AT(u, n, r, r) * vr;
+          for (int64_t c = r + 1; c <= l; ++c) {
+            acc += AT(u, n, r, c) * v[c];
+            y[c] += AT(u, n, r, c) * vr;
+          }
+          y[r] += acc;
+        }
+        f = (R)0;
+        for (int64_t j = 0; j <= l; ++j) {
+          AT(u, n, i, j) = v[j] / h;
+          e[j] = y[j] / h;
+          f += e[j] * v[j];
+        }
+        const R hh = f / (h + h);
+        for (int64_t j = 0; j <= l; ++j) e[j] -= hh * v[j];
+        for (int64_t r = 0; r <= l; ++r) {
+          const R fr = v[r], gr = e[r];
+          for (int64_t c = r; c <= l; ++c) AT(u, n, r, c) -= fr * e[c] + gr * v[c];
+        }
+      }
+    } else {
+      e[i] = AT(u, n, l, i);
+    }
+    hout[i] = h;
+  }
+  hout[0] = (R)0;
+  e[0] = (R)0;
+  for (int64_t i = 0; i < n; ++i) d[i] = AT(u, n, i, i);
+  for (int64_t i = 0; i + 1 < n; ++i) e[i] = e[i + 1];
+  e[n - 1] = (R)0;
+}
+
+static int FN(cmp)(const void* pa, const void* pb) {
+  const R a = *(const R*)pa, b = *(const R*)pb;
+  return a < b ? -1 : (a > b ? 1 : 0);
+}
+
+/* Implicit-shift QL, eigenvalues only, ascending (dl/eigen_sym.hpp:102-150). */
+static int FN(tql1)(int64_t n, R* d, R* e, int64_t cap, int64_t* iters) {
+  const R eps = EPS;
+  int64_t total = 0;
+  for (int64_t l = 0; l < n; ++l) {
+    int64_t m;
+    do {
+      for (m = l; m < n - 1; ++m) {
+        const R dd = FN(absr)(d[m]) + FN(absr)(d[m + 1]);
+        if (FN(absr)(e[m]) <= eps * dd) break;
+      }
+      if (m != l) {
+        if (++total > cap) {
+          if (iters) *iters = total;
+          return DLA_ERR_CONVERGENCE;
+        }
+        R g = (d[l + 1] - d[l]) / ((R)2 * e[l]);
+        R r = FN(pythag)(g, (R)1);
+        g = d[m] - d[l] + e[l] / (g + FN(sign_like)(r, g));
+        R s = (R)1, c = (R)1, p = (R)0;
+        int64_t i;
+        for (i = m - 1; i >= l; --i) {
+          R f = s * e[i];
+          const R b = c * e[i];
+          r = FN(pythag)(f, g);
+          e[i + 1] = r;
+          if (r == (R)0) {
+            d[i + 1] -= p;
+            e[m] = (R)0;
+            break;
+          }
+          s = f / r;
+          c = g / r;
+          g = d[i + 1] - p;
+          r = (d[i] - g) * s + (R)2 * c * b;
+          p = s * r;
+          d[i + 1] = g + p;
+          g = c * r - b;
+        }
+        if (r == (R)0 && i >= l) continue;
+        d[l] -= p;
+        e[l] = g;
+        e[m] = (R)0;
+      }
+    } while (m != l);
+  }
+  qsort(d, (size_t)n, sizeof(R), FN(cmp));
+  return DLA_OK;
+}
+
+/* Deterministic start vector (dl/eigen_sym.hpp:155-162). */
+static R FN(invit_seed)(int64_t salt, int64_t k) {
+  uint64_t x = ((uint64_t)salt + 1) * 0x9E3779B97F4A7C15ull;
+  x ^= ((uint64_t)k + 1) * 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 31;
+  x *= 0x94D049BB133111EBull;
+  x ^= x >> 29;
+  return (R)1 + (R)0.5 * (R)((double)(x >> 11) * 0x1.0p-53);
+}
+
+/* Inverse iteration on the tridiagonal (dl/eigen_sym.hpp:170-275). */
+static void FN(tinvit)(int64_t n, const R* d, const R* e, const R* w, R* z, R* alp,
+                       R* bet, R* gam, R* mul, R* swp) {
+  R norm = FN(absr)(d[0]) + FN(absr)(e[0]);
+  for (int64_t i = 1; i < n; ++i) {
+    R t = FN(absr)(e[i - 1]) + FN(absr)(d[i]) + FN(absr)(e[i]);
+    if (t > norm) norm = t;
+  }
+  if (norm == (R)0) {
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t k = 0; k < n; ++k) AT(z, n, i, k) = k == i ? (R)1 : (R)0;
+    return;
+  }
+  const R eps = EPS;
+  const R eps3 = eps * norm;
+  const R gtol = (R)100 * (R)SQRT(eps) * norm;
+  const R piv_min = RMIN / eps;
+  int64_t gs = 0;
+  R lam_used = (R)0;
+  for (int64_t idx = 0; idx < n; ++idx) {
+    if (idx > 0 && w[idx] - w[idx - 1] > gtol) gs = idx;
+    R lam = w[idx];
+    if (idx > gs && lam < lam_used + eps3) lam = lam_used + eps3;
+    lam_used = lam;
+    R* x = z + idx * n;
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      R a = d[0] - lam;
+      R b = n > 1 ? e[0] : (R)0;
+      for (int64_t i = 0; i + 1 < n; ++i) {
+        const R sub = e[i], dia = d[i + 1] - lam;
+        const R sup = i + 2 < n ? e[i + 1] : (R)0;
+        if (FN(absr)(sub) > FN(absr)(a)) {
+          swp[i] = (R)1;
+          bet[i] = dia;
+          gam[i] = sup;
+          const R mm = a / sub;
+          mul[i] = mm;
+          alp[i] = (R)1 / sub;
+          a = b - mm * dia;
+          b = -mm * sup;
+        } else {
+          swp[i] = (R)0;
+          R piv = a;
+          if (FN(absr)(piv) < piv_min) piv = eps3;
+          bet[i] = b;
+          gam[i] = (R)0;
+          const R mm = sub / piv;
+          mul[i] = mm;
+          alp[i] = (R)1 / piv;
+          a = dia - mm * b;
+          b = sup;
+        }
+      }
+      if (FN(absr)(a) < piv_min) a = eps3;
+      alp[n - 1] = (R)1 / a;
+      for (int64_t k = 0; k < n; ++k) x[k] = FN(invit_seed)(idx + 131 * attempt, k);
+      for (int it = 0; it < 2; ++it) {
+        if (it > 0)
+          for (int64_t i = 0; i + 1 < n; ++i) {
+            if (swp[i] != (R)0) {
+              R t = x[i];
+              x[i] = x[i + 1];
+              x[i + 1] = t;
+            }
+            x[i + 1] -= mul[i] * x[i];
+          }
+        x[n - 1] *= alp[n - 1];
+        if (n >= 2) x[n - 2] = (x[n - 2] - bet[n - 2] * x[n - 1]) * alp[n - 2];
+        for (int64_t i = n - 3; i >= 0; --i)
+          x[i] = (x[i] - bet[i] * x[i + 1] - gam[i] * x[i + 2]) * alp[i];
+        R amax = (R)0;
+        for (int64_t k = 0; k < n; ++k)
+          if (FN(absr)(x[k]) > amax) amax = FN(absr)(x[k]);
+        const R inv = (R)1 / amax;
+        for (int64_t k = 0; k < n; ++k) x[k] *= inv;
+      }
+      R nrm = (R)0;
+      for (int64_t k = 0; k < n; ++k) nrm += x[k] * x[k];
+      nrm = (R)SQRT(nrm);
+      for (int64_t k = 0; k < n; ++k) x[k] /= nrm;
+      R drop = (R)1;
+      for (int pass = 0; pass < 2 && idx > gs; ++pass) {
+        for (int64_t j = gs; j < idx; ++j) {
+          const R* zj = z + j * n;
+          R dot = (R)0;
+          for (int64_t k = 0; k < n; ++k) dot += x[k] * zj[k];
+          for (int64_t k = 0; k < n; ++k) x[k] -= dot * zj[k];
+        }
+        R s = (R)0;
+        for (int64_t k = 0; k < n; ++k) s += x[k] * x[k];
+        s = (R)SQRT(s);
+        if (pass == 0) drop = s;
+        if (s > (R)0)
+          for (int64_t k = 0; k < n; ++k) x[k] /= s;
+      }
+      if (drop >= (R)0.01) break;
+    }
+  }
+}
+
+/* Reflector back-transform onto the rows of z (dl/eigen_sym.hpp:282-310). */
+static void FN(trbak)(int64_t n, const R* refl, const R* h, R* z, R* v) {
+  for (int64_t i = 1; i < n; ++i) {
+    if (h[i] == (R)0) continue;
+    for (int64_t k = 0; k < i; ++k) v[k] = AT(refl, n, k, i);
+    const R* vh = refl + i * n;
+    for (int64_t j = 0; j < n; ++j) {
+      R* zj = z + j * n;
+      R g = (R)0;
+      for (int64_t k = 0; k < i; ++k) g += v[k] * zj[k];
+      for (int64_t k = 0; k < i; ++k) zj[k] -= g * vh[k];
+    }
+  }
+}
+
+/* Sign rule (dl/eigen_sym.hpp:316-333): flip row i when its largest-|.| entry
+ * (first index on ties, strict >) is negative. */
+void FN(o_fix_row_signs)(int64_t rows, int64_t cols, R* u) {
+  for (int64_t i = 0; i < rows; ++i) {
+    R* row = u + i * cols;
+    int64_t kmax = 0;
+    R best = FN(absr)(row[0]);
+    for (int64_t k = 1; k < cols; ++k)
+      if (FN(absr)(row[k]) > best) {
+        best = FN(absr)(row[k]);
+        kmax = k;
+      }
+    if (row[kmax] < (R)0)
+      for (int64_t k = 0; k < cols; ++k) row[k] = -row[k];
+  }
+}
+
+/* A = U^T diag(lambda) U, rows of U eigenvectors, lambda ascending.
+ * dl/eigen_sym.hpp:339-367.  ws: n*n + 9n reals. */
+int FN(o_syevd)(int64_t n, R* u, R* lambda, R* ws, int64_t* idx) {
+  if (!FN(symmetric_ok)(n, u, FN(sym_rtol)())) return DLA_ERR_ASYMMETRIC;
+  if (n == 1) {
+    lambda[0] = u[0];
+    u[0] = (R)1;
+    return DLA_OK;
+  }
+  if (n == 0) return DLA_OK;
+  R* refl = ws;
+  R* d = refl + n * n;
+  R* e = d + n;
+  R* h = e + n;
+  R* v = h + n;
+  R* y = v + n;
+  R* alp = y + n;
+  R* bet = alp + n;
+  R* gam = bet + n;
+  R* mul = gam + n;
+  FN(tred1)(n, u, d, e, h, v, y);
+  memcpy(refl, u, sizeof(R) * (size_t)(n * n));
+  memcpy(lambda, d, sizeof(R) * (size_t)n);
+  memcpy(v, e, sizeof(R) * (size_t)n);
+  int st = FN(tql1)(n, lambda, v, 30 * n, idx);
+  if (st != DLA_OK) return st;
+  FN(tinvit)(n, d, e, lambda, u, alp, bet, gam, mul, y);
+  FN(trbak)(n, refl, h, u, v);
+  FN(o_fix_row_signs)(n, n, u);
+  return DLA_OK;
+}
+
+/* --------------------------------------------------------------- backward */
+
+/* dl/adjoints.hpp:36-49 */
+int FN(o_gemm2_bwd)(int64_t m, int64_t n, int64_t k, R* abar, R* bbar, const R* cbar,
+                    const R* a, const R* b, int ta, int tb, R alpha) {
+  /* A is (ta ? k x m : m x k), B is (tb ? n x k : k x n), C m x n */
+  int st;
+  if (!ta) st = FN(o_gemm)(m, k, n, abar, cbar, b, 0, !tb, alpha, 0);
+  else st = FN(o_gemm)(k, m, n, abar, b, cbar, tb, 1, alpha, 0);
+  if (st) return st;
+  if (!tb) st = FN(o_gemm)(k, n, m, bbar, a, cbar, !ta, 0, alpha, 0);
+  else st = FN(o_gemm)(n, k, m, bbar, cbar, a, 1, ta, alpha, 0);
+  return st;
+}
+
+/* dl/adjoints.hpp:69-78 */
+int FN(o_syrk_bwd)(int64_t n, int64_t k, R* abar, const R* bbar, const R* a, int ta, R alpha) {
+  if (!ta) {  /* A n x k: abar = alpha (Bbar + Bbar^T) A */
+    FN(o_gemm)(n, k, n, abar, bbar, a, 0, 0, alpha, 0);
+    FN(o_gemm)(n, k, n, abar, bbar, a, 1, 0, alpha, 1);
+  } else {    /* A k x n: abar = alpha A (Bbar + Bbar^T) */
+    FN(o_gemm)(k, n, n, abar, a, bbar, 0, 0, alpha, 0);
+    FN(o_gemm)(k, n, n, abar, a, bbar, 0, 1, alpha, 1);
+  }
+  return DLA_OK;
+}
+
+static void FN(mask)(int64_t n, R* x, int lower) {
+  if (lower) FN(o_tril)(n, x);
+  else FN(o_triu)(n, x);
+}
+
+/* dl/adjoints.hpp:94-110.  X/A/Bbar are m x n; T is mt x mt. */
+int FN(o_trmm_bwd)(int64_t m, int64_t n, R* abar, R* tbar, const R* bbar, const R* t,
+                   const R* a, int rightside, int transpose, int lower, R alpha) {
+  const int64_t mt = rightside ? n : m;
+  if (!rightside && !transpose) FN(o_gemm)(m, m, n, tbar, bbar, a, 0, 1, alpha, 0);
+  else if (!rightside && transpose) FN(o_gemm)(m, m, n, tbar, a, bbar, 0, 1, alpha, 0);
+  else if (rightside && !transpose) FN(o_gemm)(n, n, m, tbar, a, bbar, 1, 0, alpha, 0);
+  else FN(o_gemm)(n, n, m, tbar, bbar, a, 1, 0, alpha, 0);
+  FN(mask)(mt, tbar, lower);
+  if (abar != bbar) memcpy(abar, bbar, sizeof(R) * (size_t)(m * n));
+  return FN(o_trmm)(m, n, t, abar, rightside, !transpose, lower, alpha);
+}
+
+/* dl/adjoints.hpp:131-153.  b is the forward OUTPUT. */
+int FN(o_trsm_bwd)(int64_t m, int64_t n, R* abar, R* tbar, const R* bbar, const R* t,
+                   const R* b, int rightside, int transpose, int lower, R alpha,
+                   int64_t* idx) {
+  const int64_t mt = rightside ? n : m;
+  if (abar != bbar) memcpy(abar, bbar, sizeof(R) * (size_t)(m * n));
+  int st = FN(o_trsm)(m, n, t, abar, rightside, !transpose, lower, (R)1, idx);
+  if (st) return st;
+  if (!rightside) {
+    if (!transpose) FN(o_gemm)(m, m, n, tbar, abar, b, 0, 1, (R)-1, 0);
+    else FN(o_gemm)(m, m, n, tbar, b, abar, 0, 1, (R)-1, 0);
+  } else {
+    if (!transpose) FN(o_gemm)(n, n, m, tbar, b, abar, 1, 0, (R)-1, 0);
+    else FN(o_gemm)(n, n, m, tbar, abar, b, 1, 0, (R)-1, 0);
+  }
+  FN(mask)(mt, tbar, lower);
+  if (alpha != (R)1) FN(scale)(abar, m * n, alpha);
+  return DLA_OK;
+}
+
+/* dl/adjoints.hpp:175-191; abar may alias lbar. */
+int FN(o_potrf_bwd)(int64_t n, R* abar, const R* lbar, const R* l, int lower) {
+  if (abar != lbar) memcpy(abar, lbar, sizeof(R) * (size_t)(n * n));
+  if (lower) {
+    FN(o_trmm)(n, n, l, abar, 0, 1, 1, (R)1);
+    FN(o_copyltu)(n, abar);
+    FN(o_trsm)(n, n, l, abar, 0, 1, 1, (R)1, NULL);
+    FN(o_trsm)(n, n, l, abar, 1, 0, 1, (R)1, NULL);
+  } else {
+    FN(o_trmm)(n, n, l, abar, 1, 1, 0, (R)1);
+    FN(o_copyutl)(n, abar);
+    FN(o_trsm)(n, n, l, abar, 0, 0, 0, (R)1, NULL);
+    FN(o_trsm)(n, n, l, abar, 1, 1, 0, (R)1, NULL);
+  }
+  FN(scale)(abar, n * n, (R)0.5);
+  FN(o_sym)(n, abar);
+  return DLA_OK;
+}
+
+/* dl/adjoints.hpp:207-223 */
+int FN(o_potri_bwd)(int64_t n, R* lbar, const R* bbar, const R* l, const R* b, int lower) {
+  if (lower) {
+    FN(o_gemm)(n, n, n, lbar, b, bbar, 0, 0, (R)1, 0);
+    FN(o_gemm)(n, n, n, lbar, b, bbar, 0, 1, (R)1, 1);
+    FN(o_trsm)(n, n, l, lbar, 1, 1, 1, (R)1, NULL);
+    FN(scale)(lbar, n * n, (R)-1);
+    FN(o_tril)(n, lbar);
+  } else {
+    FN(o_gemm)(n, n, n, lbar, bbar, b, 0, 0, (R)1, 0);
+    FN(o_gemm)(n, n, n, lbar, bbar, b, 1, 0, (R)1, 1);
+    FN(o_trsm)(n, n, l, lbar, 0, 1, 0, (R)1, NULL);
+    FN(scale)(lbar, n * n, (R)-1);
+    FN(o_triu)(n, lbar);
+  }
+  return DLA_OK;
+}
+
+/* dl/adjoints.hpp:239-252; work: m*m reals. */
+int FN(o_gelqf_bwd)(int64_t m, int64_t n, R* abar, const R* qbar, const R* lbar,
+                    const R* q, const R* l, R* work) {
+  memcpy(work, lbar, sizeof(R) * (size_t)(m * m));
+  FN(o_trmm)(m, m, l, work, 0, 1, 1, (R)1);
+  FN(o_gemm)(m, m, n, work, qbar, q, 0, 1, (R)-1, 1);
+  FN(o_copyltu)(m, work);
+  if (abar != qbar) memcpy(abar, qbar, sizeof(R) * (size_t)(m * n));
+  FN(o_gemm)(m, n, m, abar, work, q, 0, 0, (R)1, 1);
+  return FN(o_trsm)(m, n, l, abar, 0, 1, 1, (R)1, NULL);
+}
+
+/* dl/adjoints.hpp:272-295; work: n*n reals. */
+int FN(o_syevd_bwd)(int64_t n, R* abar, const R* ubar, const R* lambdabar, const R* u,
+                    const R* lambda, R eps_gap, R* work) {
+  FN(o_gemm)(n, n, n, work, ubar, u, 0, 1, (R)1, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t j = 0; j < i; ++j) {
+      R gap = lambda[i] - lambda[j];
+      if (gap < eps_gap) gap = eps_gap;
+      const R yv = (AT(work, n, i, j) - AT(work, n, j, i)) / ((R)2 * gap);
+      AT(work, n, i, j) = yv;
+      AT(work, n, j, i) = yv;
+    }
+    AT(work, n, i, i) = lambdabar[i];
+  }
+  FN(o_gemm)(n, n, n, abar, u, work, 1, 0, (R)1, 0);
+  FN(o_gemm)(n, n, n, work, abar, u, 0, 0, (R)1, 0);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j <= i; ++j) {
+      const R yv = (AT(work, n, i, j) + AT(work, n, j, i)) / (R)2;
+      AT(abar, n, i, j) = yv;
+      AT(abar, n, j, i) = yv;
+    }
+  return DLA_OK;
+}
+
+#undef AT
