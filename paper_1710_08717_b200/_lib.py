@@ -1,0 +1,94 @@
+"""ctypes binding of the C-ABI (include/dla.h) in libdla_b200.so.
+
+The shared library is built in-tree (``paper_1710_08717_b200/libdla_b200.so``)
+by ``__graft_entry__.build()`` / ``make -C paper_1710_08717_b200/csrc``.
+There is no fallback: if the library is missing or fails to load, importing
+the operator layer raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdla_b200.so")
+
+_i64, _int, _vp, _sz = C.c_int64, C.c_int, C.c_void_p, C.c_size_t
+
+DLA_OK = 0
+STATUS_NAMES = {0: "OK", 1: "SHAPE", 2: "NOT_SPD", 3: "SINGULAR", 4: "CONVERGENCE", 5: "ALIAS",
+                6: "ASYMMETRIC", 7: "CUDA", 8: "WORKSPACE", 9: "INVALID"}
+OPS = {"gemm": 0, "gemm2": 1, "syrk": 2, "trmm": 3, "trsm": 4, "potrf": 5, "potri": 6,
+       "sumlogdiag": 7, "gelqf": 8, "syevd": 9}
+
+# argument kinds: P = device pointer, I = int64, F = flag (int), S = scalar (T), Z = size_t
+_SIGS = {
+    "gemm2_fwd": "IIIIPPPFFSP",
+    "gemm_fwd": "IIIIPPPFFSSP",
+    "gemm2_bwd": "IIIIPPPPPFFSP",
+    "gemm_bwd": "IIIIPPPPPFFSSP",
+    "syrk_fwd": "IIIPPFSP",
+    "syrk_bwd": "IIIPPPFSP",
+    "trmm_fwd": "IIIPPFFFSP",
+    "trmm_bwd": "IIIPPPPPFFFSP",
+    "trsm_fwd": "IIIPPFFFSPP",
+    "trsm_bwd": "IIIPPPPPFFFSP",
+    "potrf_fwd": "IIPFPP",
+    "potrf_bwd": "IIPPPFP",
+    "potri_fwd": "IIPFPP",
+    "potri_bwd": "IIPPPPFP",
+    "sumlogdiag_fwd": "IIPPP",
+    "sumlogdiag_bwd": "IIPPPFP",
+    "gelqf_fwd": "IIIPPPPZP",
+    "gelqf_bwd": "IIIPPPPPPZP",
+    "syevd_fwd": "IIPPPPZP",
+    "syevd_bwd": "IIPPPPPSPZP",
+}
+
+
+class _Lib:
+    def __init__(self, path: str = LIB_PATH):
+        if not os.path.exists(path):
+            raise ImportError(
+                f"libdla_b200.so not found at {path}: build it with "
+                "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+        self.path = path
+        self.lib = C.CDLL(path)
+        L = self.lib
+        L.dla_status_string.restype = C.c_char_p
+        L.dla_status_string.argtypes = [_int]
+        L.dla_version.restype = C.c_char_p
+        L.dla_workspace_bytes.restype = _sz
+        L.dla_workspace_bytes.argtypes = [_int, _int, _i64, _i64, _i64, _i64, _int]
+        L.dla_info_check.restype = _int
+        L.dla_info_check.argtypes = [_vp, _i64, _vp, C.POINTER(_i64), C.POINTER(_i64)]
+        self.fns = {}
+        for name, sig in _SIGS.items():
+            for suffix, scal in (("f32", C.c_float), ("f64", C.c_double)):
+                f = getattr(L, f"dla_{name}_{suffix}")
+                kinds = {"P": _vp, "I": _i64, "F": _int, "S": scal, "Z": _sz}
+                f.argtypes = [kinds[k] for k in sig]
+                f.restype = _int
+                self.fns[(name, suffix)] = f
+
+    def fn(self, name: str, suffix: str):
+        return self.fns[(name, suffix)]
+
+
+_LIB = None
+
+
+def lib() -> _Lib:
+    global _LIB
+    if _LIB is None:
+        _LIB = _Lib()
+    return _LIB
+
+
+def exported_symbols():
+    """Every dla_* symbol include/dla.h declares (used by the CPU symbol test)."""
+    names = ["dla_status_string", "dla_version", "dla_workspace_bytes", "dla_info_check"]
+    for name in _SIGS:
+        for s in ("f32", "f64"):
+            names.append(f"dla_{name}_{s}")
+    return names

@@ -1,0 +1,518 @@
+// extern "C" operator entry points (include/dla.h): host-side validation that
+// mirrors the reference's ShapeError / alias sites, then stream-ordered
+// launches.  Backward ops follow the reference's closed-form compositions
+// (dl/adjoints.hpp) on the batched device kernels.
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "ops.cuh"
+
+namespace dlab {
+
+Ctx make_ctx(void* stream, int32_t* info) {
+  static int sms = 0;
+  static std::once_flag flag;
+  std::call_once(flag, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;  // keep scratch in the pool: no steady-state cudaMalloc
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+  return Ctx{reinterpret_cast<cudaStream_t>(stream), sms, info};
+}
+
+namespace {
+
+bool overlap(const void* a, size_t abytes, const void* b, size_t bbytes) {
+  if (!a || !b || abytes == 0 || bbytes == 0) return false;
+  const char* pa = static_cast<const char*>(a);
+  const char* pb = static_cast<const char*>(b);
+  return pa < pb + bbytes && pb < pa + abytes;
+}
+
+template <typename T>
+size_t bytes(int64_t batch, int64_t r, int64_t c) {
+  return sizeof(T) * (size_t)batch * (size_t)r * (size_t)c;
+}
+
+dla_status reset_info(const Ctx& c, int64_t batch) {
+  if (c.info && batch > 0)
+    if (cudaMemsetAsync(c.info, 0, sizeof(int32_t) * batch, c.stream) != cudaSuccess) return DLA_ERR_CUDA;
+  return DLA_OK;
+}
+
+bool bad_dims(int64_t batch, int64_t a, int64_t b = 0, int64_t c = 0) {
+  return batch < 0 || a < 0 || b < 0 || c < 0 || a > 0xFFFFFF || b > 0x7FFFFFFF;
+}
+
+template <typename T>
+MatB<const T> cpk(const T* p, int64_t r, int64_t c) {
+  return MatB<const T>{p, c, r * c};
+}
+template <typename T>
+MatB<T> pk(T* p, int64_t r, int64_t c) {
+  return MatB<T>{p, c, r * c};
+}
+template <typename T>
+MatB<const T> C_(MatB<T> m) {
+  return MatB<const T>{m.p, m.ld, m.bs};
+}
+
+// ------------------------------------------------------------------- gemm
+template <typename T>
+dla_status gemm_fwd(int64_t batch, int64_t m, int64_t n, int64_t k, T* c, const T* a, const T* b, int ta, int tb,
+                    T alpha, T beta, void* stream) {
+  if (batch < 0 || m < 0 || n < 0 || k < 0) return DLA_ERR_SHAPE;
+  if (overlap(c, bytes<T>(batch, m, n), a, bytes<T>(batch, m, k)) ||
+      overlap(c, bytes<T>(batch, m, n), b, bytes<T>(batch, k, n)))
+    return DLA_ERR_ALIAS;
+  Ctx cx = make_ctx(stream, nullptr);
+  if (beta == T(0)) {  // the reference zero-fills C (gemm_accum accumulate=false)
+    if (k == 0 || alpha == T(0)) {
+      return cudaMemsetAsync(c, 0, bytes<T>(batch, m, n), cx.stream) == cudaSuccess ? DLA_OK : DLA_ERR_CUDA;
+    }
+  }
+  return gemm<T>(cx, batch, m, n, k, alpha, cpk(a, ta ? k : m, ta ? m : k), ta, cpk(b, tb ? n : k, tb ? k : n),
+                 tb, beta, pk(c, m, n));
+}
+
+template <typename T>
+dla_status gemm_bwd(int64_t batch, int64_t m, int64_t n, int64_t k, T* abar, T* bbar, T* cbar_io, const T* a,
+                    const T* b, int ta, int tb, T alpha, T beta, bool has_c, void* stream) {
+  if (batch < 0 || m < 0 || n < 0 || k < 0) return DLA_ERR_SHAPE;
+  const size_t asz = bytes<T>(batch, m, k), bsz = bytes<T>(batch, k, n), csz = bytes<T>(batch, m, n);
+  if (overlap(abar, asz, cbar_io, csz) || overlap(abar, asz, b, bsz) || overlap(bbar, bsz, cbar_io, csz) ||
+      overlap(bbar, bsz, a, asz) || overlap(abar, asz, bbar, bsz))
+    return DLA_ERR_ALIAS;
+  // dl/adjoints.hpp:39-48
+  if (!ta) DLAB_TRY(gemm_fwd<T>(batch, m, k, n, abar, cbar_io, b, 0, !tb, alpha, T(0), stream));
+  else DLAB_TRY(gemm_fwd<T>(batch, k, m, n, abar, b, cbar_io, tb, 1, alpha, T(0), stream));
+  if (!tb) DLAB_TRY(gemm_fwd<T>(batch, k, n, m, bbar, a, cbar_io, !ta, 0, alpha, T(0), stream));
+  else DLAB_TRY(gemm_fwd<T>(batch, n, k, m, bbar, cbar_io, a, 1, ta, alpha, T(0), stream));
+  if (has_c) {
+    Ctx cx = make_ctx(stream, nullptr);
+    if (beta == T(0))
+      return cudaMemsetAsync(cbar_io, 0, csz, cx.stream) == cudaSuccess ? DLA_OK : DLA_ERR_CUDA;
+    return ew_scale<T>(cx, batch, m, n, pk(cbar_io, m, n), beta);
+  }
+  return DLA_OK;
+}
+
+// ------------------------------------------------------------------- syrk
+template <typename T>
+dla_status syrk_fwd(int64_t batch, int64_t n, int64_t k, T* bo, const T* a, int ta, T alpha, void* stream) {
+  if (batch < 0 || n < 0 || k < 0) return DLA_ERR_SHAPE;
+  if (overlap(bo, bytes<T>(batch, n, n), a, bytes<T>(batch, n, k))) return DLA_ERR_ALIAS;
+  Ctx cx = make_ctx(stream, nullptr);
+  if (batch * n == 0) return DLA_OK;
+  if (k == 0 || alpha == T(0))
+    return cudaMemsetAsync(bo, 0, bytes<T>(batch, n, n), cx.stream) == cudaSuccess ? DLA_OK : DLA_ERR_CUDA;
+  MatB<const T> av = cpk(a, ta ? k : n, ta ? n : k);
+  DLAB_TRY(gemm<T>(cx, batch, n, n, k, alpha, av, ta, av, !ta, T(0), pk(bo, n, n), MASK_LOWER));
+  return ew_square<T>(cx, batch, n, pk(bo, n, n), /*copyltu*/ 2);
+}
+
+template <typename T>
+dla_status syrk_bwd(int64_t batch, int64_t n, int64_t k, T* abar, const T* bbar, const T* a, int ta, T alpha,
+                    void* stream) {
+  if (batch < 0 || n < 0 || k < 0) return DLA_ERR_SHAPE;
+  const size_t asz = bytes<T>(batch, n, k);
+  if (overlap(abar, asz, bbar, bytes<T>(batch, n, n)) || overlap(abar, asz, a, asz)) return DLA_ERR_ALIAS;
+  // dl/adjoints.hpp:71-77
+  if (!ta) {
+    DLAB_TRY(gemm_fwd<T>(batch, n, k, n, abar, bbar, a, 0, 0, alpha, T(0), stream));
+    DLAB_TRY(gemm_fwd<T>(batch, n, k, n, abar, bbar, a, 1, 0, alpha, T(1), stream));
+  } else {
+    DLAB_TRY(gemm_fwd<T>(batch, k, n, n, abar, a, bbar, 0, 0, alpha, T(0), stream));
+    DLAB_TRY(gemm_fwd<T>(batch, k, n, n, abar, a, bbar, 0, 1, alpha, T(1), stream));
+  }
+  return DLA_OK;
+}
+
+// ------------------------------------------------------------ trmm / trsm
+template <typename T>
+dla_status trmm_fwd(int64_t batch, int64_t m, int64_t n, const T* t, T* x, int right, int trans, int lower,
+                    T alpha, void* stream) {
+  if (bad_dims(batch, m, n)) return DLA_ERR_SHAPE;
+  const int64_t nt = right ? n : m;
+  if (overlap(x, bytes<T>(batch, m, n), t, bytes<T>(batch, nt, nt))) return DLA_ERR_ALIAS;
+  Ctx cx = make_ctx(stream, nullptr);
+  return trmm<T>(cx, batch, m, n, cpk(t, nt, nt), pk(x, m, n), right, trans, lower, alpha);
+}
+
+template <typename T>
+dla_status trsm_fwd(int64_t batch, int64_t m, int64_t n, const T* t, T* x, int right, int trans, int lower,
+                    T alpha, int32_t* info, void* stream) {
+  if (bad_dims(batch, m, n)) return DLA_ERR_SHAPE;
+  const int64_t nt = right ? n : m;
+  if (overlap(x, bytes<T>(batch, m, n), t, bytes<T>(batch, nt, nt))) return DLA_ERR_ALIAS;
+  Ctx cx = make_ctx(stream, info);
+  DLAB_TRY(reset_info(cx, batch));
+  DLAB_TRY(check_zero_diag<T>(cx, batch, nt, cpk(t, nt, nt), info));
+  return trsm<T>(cx, batch, m, n, cpk(t, nt, nt), pk(x, m, n), right, trans, lower, alpha);
+}
+
+template <typename T>
+dla_status trmm_bwd(int64_t batch, int64_t m, int64_t n, T* abar, T* tbar, const T* bbar, const T* t, const T* a,
+                    int right, int trans, int lower, T alpha, void* stream) {
+  if (bad_dims(batch, m, n)) return DLA_ERR_SHAPE;
+  const int64_t nt = right ? n : m;
+  const size_t xsz = bytes<T>(batch, m, n), tsz = bytes<T>(batch, nt, nt);
+  if (overlap(tbar, tsz, bbar, xsz) || overlap(tbar, tsz, a, xsz) || overlap(abar, xsz, t, tsz) ||
+      overlap(abar, xsz, tbar, tsz) || (abar != bbar && overlap(abar, xsz, bbar, xsz)))
+    return DLA_ERR_ALIAS;
+  Ctx cx = make_ctx(stream, nullptr);
+  if (batch * m * n == 0) {
+    if (batch * nt > 0) cudaMemsetAsync(tbar, 0, tsz, cx.stream);
+    return DLA_OK;
+  }
+  MatB<T> tb = pk(tbar, nt, nt);
+  const int mask = lower ? MASK_LOWER : MASK_UPPER;
+  auto X = [&](const T* p) { return cpk(p, m, n); };
+  // dl/adjoints.hpp:98-107, computed on the kept triangle only
+  if (!right && !trans) DLAB_TRY(gemm<T>(cx, batch, m, m, n, alpha, X(bbar), false, X(a), true, T(0), tb, mask));
+  else if (!right && trans) DLAB_TRY(gemm<T>(cx, batch, m, m, n, alpha, X(a), false, X(bbar), true, T(0), tb, mask));
+  else if (right && !trans) DLAB_TRY(gemm<T>(cx, batch, n, n, m, alpha, X(a), true, X(bbar), false, T(0), tb, mask));
+  else DLAB_TRY(gemm<T>(cx, batch, n, n, m, alpha, X(bbar), true, X(a), false, T(0), tb, mask));
+  DLAB_TRY(ew_square<T>(cx, batch, nt, tb, lower ? 0 : 1));
+  DLAB_TRY(ew_copy<T>(cx, batch, m, n, cpk(bbar, m, n), pk(abar, m, n)));
+  return trmm<T>(cx, batch, m, n, cpk(t, nt, nt), pk(abar, m, n), right, !trans, lower, alpha);
+}
+
+template <typename T>
+dla_status trsm_bwd(int64_t batch, int64_t m, int64_t n, T* abar, T* tbar, const T* bbar, const T* t, const T* b,
+                    int right, int trans, int lower, T alpha, void* stream) {
+  if (bad_dims(batch, m, n)) return DLA_ERR_SHAPE;
+  const int64_t nt = right ? n : m;
+  const size_t xsz = bytes<T>(batch, m, n), tsz = bytes<T>(batch, nt, nt);
+  if (overlap(tbar, tsz, bbar, xsz) || overlap(tbar, tsz, b, xsz) || overlap(abar, xsz, t, tsz) ||
+      overlap(abar, xsz, tbar, tsz) || overlap(abar, xsz, b, xsz) ||
+      (abar != bbar && overlap(abar, xsz, bbar, xsz)))
+    return DLA_ERR_ALIAS;
+  Ctx cx = make_ctx(stream, nullptr);
+  if (batch * m * n == 0) {
+    if (batch * nt > 0) cudaMemsetAsync(tbar, 0, tsz, cx.stream);
+    return DLA_OK;
+  }
+  // dl/adjoints.hpp:136-152: S = op(T)^{-T} Bbar in abar, then Tbar, then alpha.
+  DLAB_TRY(ew_copy<T>(cx, batch, m, n, cpk(bbar, m, n), pk(abar, m, n)));
+  DLAB_TRY(trsm<T>(cx, batch, m, n, cpk(t, nt, nt), pk(abar, m, n), right, !trans, lower, T(1)));
+  MatB<T> tb = pk(tbar, nt, nt);
+  const int mask = lower ? MASK_LOWER : MASK_UPPER;
+  auto X = [&](const T* p) { return cpk(p, m, n); };
+  const T* s = abar;
+  if (!right) {
+    if (!trans) DLAB_TRY(gemm<T>(cx, batch, m, m, n, T(-1), X(s), false, X(b), true, T(0), tb, mask));
+    else DLAB_TRY(gemm<T>(cx, batch, m, m, n, T(-1), X(b), false, X(s), true, T(0), tb, mask));
+  } else {
+    if (!trans) DLAB_TRY(gemm<T>(cx, batch, n, n, m, T(-1), X(b), true, X(s), false, T(0), tb, mask));
+    else DLAB_TRY(gemm<T>(cx, batch, n, n, m, T(-1), X(s), true, X(b), false, T(0), tb, mask));
+  }
+  DLAB_TRY(ew_square<T>(cx, batch, nt, tb, lower ? 0 : 1));
+  return ew_scale<T>(cx, batch, m, n, pk(abar, m, n), alpha);
+}
+
+// ------------------------------------------------------------ potrf / potri
+template <typename T>
+dla_status potrf_fwd(int64_t batch, int64_t n, T* a, int lower, int32_t* info, void* stream) {
+  if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
+  Ctx cx = make_ctx(stream, info);
+  DLAB_TRY(reset_info(cx, batch));
+  if (batch * n == 0) return DLA_OK;
+  if (potrf_small_eligible<T>(n)) return potrf_small<T>(cx, batch, n, pk(a, n, n), lower);
+  DLAB_TRY(check_symmetric<T>(cx, batch, n, cpk(a, n, n), info));
+  DLAB_TRY(potrf_lower<T>(cx, batch, n, pk(a, n, n)));
+  if (!lower) DLAB_TRY(ew_square<T>(cx, batch, n, pk(a, n, n), /*transpose*/ 5, T(1), info));
+  return DLA_OK;
+}
+
+template <typename T>
+dla_status potrf_bwd(int64_t batch, int64_t n, T* abar, const T* lbar, const T* l, int lower, void* stream) {
+  if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
+  const size_t sz = bytes<T>(batch, n, n);
+  if (overlap(abar, sz, l, sz) || (abar != lbar && overlap(abar, sz, lbar, sz))) return DLA_ERR_ALIAS;
+  Ctx cx = make_ctx(stream, nullptr);
+  if (batch * n == 0) return DLA_OK;
+  if (potrf_small_eligible<T>(n)) return potrf_bwd_small<T>(cx, batch, n, pk(abar, n, n), cpk(lbar, n, n),
+                                                            cpk(l, n, n), lower);
+  MatB<T> ab = pk(abar, n, n);
+  MatB<const T> lv = cpk(l, n, n);
+  DLAB_TRY(ew_copy<T>(cx, batch, n, n, cpk(lbar, n, n), ab));
+  if (lower) {  // dl/adjoints.hpp:179-182
+    DLAB_TRY(trmm<T>(cx, batch, n, n, lv, ab, false, true, true, T(1)));
+    DLAB_TRY(ew_square<T>(cx, batch, n, ab, /*copyltu*/ 2));
+    DLAB_TRY(trsm<T>(cx, batch, n, n, lv, ab, false, true, true, T(1)));
+    DLAB_TRY(trsm<T>(cx, batch, n, n, lv, ab, true, false, true, T(1)));
+  } else {      // dl/adjoints.hpp:184-187
+    DLAB_TRY(trmm<T>(cx, batch, n, n, lv, ab, true, true, false, T(1)));
+    DLAB_TRY(ew_square<T>(cx, batch, n, ab, /*copyutl*/ 3));
+    DLAB_TRY(trsm<T>(cx, batch, n, n, lv, ab, false, false, false, T(1)));
+    DLAB_TRY(trsm<T>(cx, batch, n, n, lv, ab, true, true, false, T(1)));
+  }
+  return ew_square<T>(cx, batch, n, ab, /*scaled sym*/ 6, T(0.5));
+}
+
+template <typename T>
+dla_status potri_fwd(int64_t batch, int64_t n, T* a, int lower, int32_t* info, void* stream) {
+  if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
+  Ctx cx = make_ctx(stream, info);
+  DLAB_TRY(reset_info(cx, batch));
+  if (batch * n == 0) return DLA_OK;
+  MatB<T> av = pk(a, n, n);
+  if (!lower) DLAB_TRY(ew_square<T>(cx, batch, n, av, /*transpose*/ 5));
+  DLAB_TRY(check_zero_diag<T>(cx, batch, n, C_(av), info));
+  return potri_lower<T>(cx, batch, n, av);
+}
+
+template <typename T>
+dla_status potri_bwd(int64_t batch, int64_t n, T* lbar, const T* bbar, const T* l, const T* b, int lower,
+                     void* stream) {
+  if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
+  const size_t sz = bytes<T>(batch, n, n);
+  if (overlap(lbar, sz, bbar, sz) || overlap(lbar, sz, l, sz) || overlap(lbar, sz, b, sz)) return DLA_ERR_ALIAS;
+  Ctx cx = make_ctx(stream, nullptr);
+  if (batch * n == 0) return DLA_OK;
+  MatB<T> lb = pk(lbar, n, n);
+  MatB<const T> bv = cpk(b, n, n), bb = cpk(bbar, n, n), lv = cpk(l, n, n);
+  if (lower) {  // dl/adjoints.hpp:211-215
+    DLAB_TRY(gemm<T>(cx, batch, n, n, n, T(1), bv, false, bb, false, T(0), lb));
+    DLAB_TRY(gemm<T>(cx, batch, n, n, n, T(1), bv, false, bb, true, T(1), lb));
+    DLAB_TRY(trsm<T>(cx, batch, n, n, lv, lb, true, true, true, T(-1)));
+    return ew_square<T>(cx, batch, n, lb, /*tril*/ 0);
+  }
+  // dl/adjoints.hpp:217-221
+  DLAB_TRY(gemm<T>(cx, batch, n, n, n, T(1), bb, false, bv, false, T(0), lb));
+  DLAB_TRY(gemm<T>(cx, batch, n, n, n, T(1), bb, true, bv, false, T(1), lb));
+  DLAB_TRY(trsm<T>(cx, batch, n, n, lv, lb, false, true, false, T(-1)));
+  return ew_square<T>(cx, batch, n, lb, /*triu*/ 1);
+}
+
+// ------------------------------------------------------------- sumlogdiag
+template <typename T>
+dla_status sld_fwd(int64_t batch, int64_t n, T* out, const T* a, void* stream) {
+  if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
+  Ctx cx = make_ctx(stream, nullptr);
+  return sumlogdiag_fwd<T>(cx, batch, n, out, cpk(a, n, n));
+}
+
+template <typename T>
+dla_status sld_bwd(int64_t batch, int64_t n, T* abar, const T* g, const T* a, int accumulate, void* stream) {
+  if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
+  const size_t sz = bytes<T>(batch, n, n);
+  if (overlap(abar, sz, a, sz)) return DLA_ERR_ALIAS;
+  Ctx cx = make_ctx(stream, nullptr);
+  return sumlogdiag_bwd<T>(cx, batch, n, pk(abar, n, n), g, cpk(a, n, n), accumulate != 0);
+}
+
+// --------------------------------------------------------------- gelqf
+template <typename T>
+dla_status gelqf_fwd_abi(int64_t batch, int64_t m, int64_t n, T* q, T* l, int32_t* info, void* ws, size_t wsb,
+                         void* stream) {
+  if (bad_dims(batch, m, n) || m > n) return DLA_ERR_SHAPE;
+  if (overlap(q, bytes<T>(batch, m, n), l, bytes<T>(batch, m, m))) return DLA_ERR_ALIAS;
+  Ctx cx = make_ctx(stream, info);
+  DLAB_TRY(reset_info(cx, batch));
+  if (batch * m == 0) return DLA_OK;
+  if (wsb < gelqf_ws_bytes<T>(batch, m, n, false)) return DLA_ERR_WORKSPACE;
+  return gelqf_fwd<T>(cx, batch, m, n, q, l, ws);
+}
+
+template <typename T>
+dla_status gelqf_bwd_abi(int64_t batch, int64_t m, int64_t n, T* abar, const T* qbar, const T* lbar, const T* q,
+                         const T* l, void* ws, size_t wsb, void* stream) {
+  if (bad_dims(batch, m, n) || m > n) return DLA_ERR_SHAPE;
+  const size_t asz = bytes<T>(batch, m, n);
+  if (overlap(abar, asz, q, asz) || overlap(abar, asz, l, bytes<T>(batch, m, m)) ||
+      overlap(abar, asz, lbar, bytes<T>(batch, m, m)) || (abar != qbar && overlap(abar, asz, qbar, asz)))
+    return DLA_ERR_ALIAS;
+  Ctx cx = make_ctx(stream, nullptr);
+  if (batch * m == 0) return DLA_OK;
+  if (wsb < gelqf_ws_bytes<T>(batch, m, n, true) || !ws) return DLA_ERR_WORKSPACE;
+  T* w = static_cast<T*>(ws);
+  MatB<T> wv = pk(w, m, m);
+  MatB<const T> lv = cpk(l, m, m), qv = cpk(q, m, n);
+  // dl/adjoints.hpp:243-251
+  DLAB_TRY(ew_copy<T>(cx, batch, m, m, cpk(lbar, m, m), wv));
+  DLAB_TRY(trmm<T>(cx, batch, m, m, lv, wv, false, true, true, T(1)));
+  DLAB_TRY(gemm<T>(cx, batch, m, m, n, T(-1), cpk(qbar, m, n), false, qv, true, T(1), wv));
+  DLAB_TRY(ew_square<T>(cx, batch, m, wv, /*copyltu*/ 2));
+  DLAB_TRY(ew_copy<T>(cx, batch, m, n, cpk(qbar, m, n), pk(abar, m, n)));
+  DLAB_TRY(gemm<T>(cx, batch, m, n, m, T(1), C_(wv), false, qv, false, T(1), pk(abar, m, n)));
+  return trsm<T>(cx, batch, m, n, lv, pk(abar, m, n), false, true, true, T(1));
+}
+
+// --------------------------------------------------------------- syevd
+template <typename T>
+dla_status syevd_fwd_abi(int64_t batch, int64_t n, T* u, T* lambda, int32_t* info, void* ws, size_t wsb,
+                         void* stream) {
+  if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
+  if (overlap(u, bytes<T>(batch, n, n), lambda, bytes<T>(batch, n, 1))) return DLA_ERR_ALIAS;
+  Ctx cx = make_ctx(stream, info);
+  DLAB_TRY(reset_info(cx, batch));
+  if (batch * n == 0) return DLA_OK;
+  if (wsb < syevd_ws_bytes<T>(batch, n, false)) return DLA_ERR_WORKSPACE;
+  return syevd_fwd<T>(cx, batch, n, u, lambda, ws);
+}
+
+template <typename T>
+dla_status syevd_bwd_abi(int64_t batch, int64_t n, T* abar, const T* ubar, const T* lambdabar, const T* u,
+                         const T* lambda, T eps_gap, void* ws, size_t wsb, void* stream) {
+  if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
+  const size_t sz = bytes<T>(batch, n, n);
+  if (overlap(abar, sz, ubar, sz) || overlap(abar, sz, u, sz)) return DLA_ERR_ALIAS;
+  if (!(eps_gap > T(0))) return DLA_ERR_INVALID;
+  Ctx cx = make_ctx(stream, nullptr);
+  if (batch * n == 0) return DLA_OK;
+  if (wsb < syevd_ws_bytes<T>(batch, n, true) || !ws) return DLA_ERR_WORKSPACE;
+  MatB<T> w = pk(static_cast<T*>(ws), n, n);
+  MatB<const T> uv = cpk(u, n, n);
+  // dl/adjoints.hpp:277-294
+  DLAB_TRY(gemm<T>(cx, batch, n, n, n, T(1), cpk(ubar, n, n), false, uv, true, T(0), w));
+  DLAB_TRY(syevd_gap_kernel<T>(cx, batch, n, w, lambdabar, lambda, eps_gap));
+  DLAB_TRY(gemm<T>(cx, batch, n, n, n, T(1), uv, true, C_(w), false, T(0), pk(abar, n, n)));
+  DLAB_TRY(gemm<T>(cx, batch, n, n, n, T(1), cpk(abar, n, n), false, uv, false, T(0), w));
+  return ew_sym_into<T>(cx, batch, n, C_(w), pk(abar, n, n));
+}
+
+}  // namespace
+}  // namespace dlab
+
+using namespace dlab;
+
+extern "C" {
+
+const char* dla_status_string(dla_status s) {
+  switch (s) {
+    case DLA_OK: return "ok";
+    case DLA_ERR_SHAPE: return "shape error";
+    case DLA_ERR_NOT_SPD: return "matrix is not positive definite";
+    case DLA_ERR_SINGULAR: return "singular";
+    case DLA_ERR_CONVERGENCE: return "did not converge";
+    case DLA_ERR_ALIAS: return "output must not alias this input";
+    case DLA_ERR_ASYMMETRIC: return "input is not symmetric";
+    case DLA_ERR_CUDA: return "CUDA error";
+    case DLA_ERR_WORKSPACE: return "workspace missing or too small";
+    case DLA_ERR_INVALID: return "invalid argument";
+  }
+  return "unknown";
+}
+
+const char* dla_version(void) { return "dla_b200 0.1 (sm_100a)"; }
+
+size_t dla_workspace_bytes(dla_op op, dla_dtype dtype, int64_t batch, int64_t m, int64_t n, int64_t k, int phase) {
+  (void)k;
+  const bool bwd = (phase & DLA_WS_BACKWARD) != 0;
+  if (op == DLA_OP_GELQF)
+    return dtype == DLA_F64 ? gelqf_ws_bytes<double>(batch, m, n, bwd) : gelqf_ws_bytes<float>(batch, m, n, bwd);
+  if (op == DLA_OP_SYEVD)
+    return dtype == DLA_F64 ? syevd_ws_bytes<double>(batch, n, bwd) : syevd_ws_bytes<float>(batch, n, bwd);
+  return 0;
+}
+
+dla_status dla_info_check(const int32_t* info, int64_t batch, void* stream, int64_t* first_bad, int64_t* index) {
+  if (first_bad) *first_bad = -1;
+  if (index) *index = -1;
+  if (!info || batch <= 0) return DLA_OK;
+  std::vector<int32_t> h((size_t)batch);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(h.data(), info, sizeof(int32_t) * batch, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return DLA_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return DLA_ERR_CUDA;
+  for (int64_t b = 0; b < batch; ++b)
+    if (h[(size_t)b] != 0) {
+      if (first_bad) *first_bad = b;
+      if (index) *index = DLA_INFO_INDEX(h[(size_t)b]);
+      return (dla_status)DLA_INFO_CODE(h[(size_t)b]);
+    }
+  return DLA_OK;
+}
+
+#define DLA_DEFINE(T, S)                                                                                          \
+  dla_status dla_gemm2_fwd_##S(int64_t batch, int64_t m, int64_t n, int64_t k, T* c, const T* a, const T* b,      \
+                               int ta, int tb, T alpha, void* stream) {                                          \
+    return gemm_fwd<T>(batch, m, n, k, c, a, b, ta, tb, alpha, T(0), stream);                                    \
+  }                                                                                                               \
+  dla_status dla_gemm_fwd_##S(int64_t batch, int64_t m, int64_t n, int64_t k, T* c, const T* a, const T* b,       \
+                              int ta, int tb, T alpha, T beta, void* stream) {                                   \
+    return gemm_fwd<T>(batch, m, n, k, c, a, b, ta, tb, alpha, beta, stream);                                    \
+  }                                                                                                               \
+  dla_status dla_gemm2_bwd_##S(int64_t batch, int64_t m, int64_t n, int64_t k, T* abar, T* bbar, const T* cbar,   \
+                               const T* a, const T* b, int ta, int tb, T alpha, void* stream) {                  \
+    return gemm_bwd<T>(batch, m, n, k, abar, bbar, const_cast<T*>(cbar), a, b, ta, tb, alpha, T(0), false,       \
+                       stream);                                                                                   \
+  }                                                                                                               \
+  dla_status dla_gemm_bwd_##S(int64_t batch, int64_t m, int64_t n, int64_t k, T* abar, T* bbar, T* cbar_io,       \
+                              const T* a, const T* b, int ta, int tb, T alpha, T beta, void* stream) {           \
+    return gemm_bwd<T>(batch, m, n, k, abar, bbar, cbar_io, a, b, ta, tb, alpha, beta, true, stream);            \
+  }                                                                                                               \
+  dla_status dla_syrk_fwd_##S(int64_t batch, int64_t n, int64_t k, T* b, const T* a, int ta, T alpha,             \
+                              void* stream) {                                                                     \
+    return syrk_fwd<T>(batch, n, k, b, a, ta, alpha, stream);                                                     \
+  }                                                                                                               \
+  dla_status dla_syrk_bwd_##S(int64_t batch, int64_t n, int64_t k, T* abar, const T* bbar, const T* a, int ta,    \
+                              T alpha, void* stream) {                                                            \
+    return syrk_bwd<T>(batch, n, k, abar, bbar, a, ta, alpha, stream);                                            \
+  }                                                                                                               \
+  dla_status dla_trmm_fwd_##S(int64_t batch, int64_t m, int64_t n, const T* t, T* x, int r, int tr, int lo,       \
+                              T alpha, void* stream) {                                                            \
+    return trmm_fwd<T>(batch, m, n, t, x, r, tr, lo, alpha, stream);                                              \
+  }                                                                                                               \
+  dla_status dla_trmm_bwd_##S(int64_t batch, int64_t m, int64_t n, T* abar, T* tbar, const T* bbar, const T* t,   \
+                              const T* a, int r, int tr, int lo, T alpha, void* stream) {                        \
+    return trmm_bwd<T>(batch, m, n, abar, tbar, bbar, t, a, r, tr, lo, alpha, stream);                            \
+  }                                                                                                               \
+  dla_status dla_trsm_fwd_##S(int64_t batch, int64_t m, int64_t n, const T* t, T* x, int r, int tr, int lo,       \
+                              T alpha, int32_t* info, void* stream) {                                             \
+    return trsm_fwd<T>(batch, m, n, t, x, r, tr, lo, alpha, info, stream);                                        \
+  }                                                                                                               \
+  dla_status dla_trsm_bwd_##S(int64_t batch, int64_t m, int64_t n, T* abar, T* tbar, const T* bbar, const T* t,   \
+                              const T* b, int r, int tr, int lo, T alpha, void* stream) {                        \
+    return trsm_bwd<T>(batch, m, n, abar, tbar, bbar, t, b, r, tr, lo, alpha, stream);                            \
+  }                                                                                                               \
+  dla_status dla_potrf_fwd_##S(int64_t batch, int64_t n, T* a, int lower, int32_t* info, void* stream) {         \
+    return potrf_fwd<T>(batch, n, a, lower, info, stream);                                                        \
+  }                                                                                                               \
+  dla_status dla_potrf_bwd_##S(int64_t batch, int64_t n, T* abar, const T* lbar, const T* l, int lower,           \
+                               void* stream) {                                                                    \
+    return potrf_bwd<T>(batch, n, abar, lbar, l, lower, stream);                                                  \
+  }                                                                                                               \
+  dla_status dla_potri_fwd_##S(int64_t batch, int64_t n, T* a, int lower, int32_t* info, void* stream) {         \
+    return potri_fwd<T>(batch, n, a, lower, info, stream);                                                        \
+  }                                                                                                               \
+  dla_status dla_potri_bwd_##S(int64_t batch, int64_t n, T* lbar, const T* bbar, const T* l, const T* b,          \
+                               int lower, void* stream) {                                                         \
+    return potri_bwd<T>(batch, n, lbar, bbar, l, b, lower, stream);                                              \
+  }                                                                                                               \
+  dla_status dla_sumlogdiag_fwd_##S(int64_t batch, int64_t n, T* out, const T* a, void* stream) {                \
+    return sld_fwd<T>(batch, n, out, a, stream);                                                                  \
+  }                                                                                                               \
+  dla_status dla_sumlogdiag_bwd_##S(int64_t batch, int64_t n, T* abar, const T* gbar, const T* a,                 \
+                                    int accumulate, void* stream) {                                               \
+    return sld_bwd<T>(batch, n, abar, gbar, a, accumulate, stream);                                               \
+  }                                                                                                               \
+  dla_status dla_gelqf_fwd_##S(int64_t batch, int64_t m, int64_t n, T* q, T* l, int32_t* info, void* ws,         \
+                               size_t ws_bytes, void* stream) {                                                   \
+    return gelqf_fwd_abi<T>(batch, m, n, q, l, info, ws, ws_bytes, stream);                                       \
+  }                                                                                                               \
+  dla_status dla_gelqf_bwd_##S(int64_t batch, int64_t m, int64_t n, T* abar, const T* qbar, const T* lbar,        \
+                               const T* q, const T* l, void* ws, size_t ws_bytes, void* stream) {                \
+    return gelqf_bwd_abi<T>(batch, m, n, abar, qbar, lbar, q, l, ws, ws_bytes, stream);                           \
+  }                                                                                                               \
+  dla_status dla_syevd_fwd_##S(int64_t batch, int64_t n, T* u, T* lambda, int32_t* info, void* ws,               \
+                               size_t ws_bytes, void* stream) {                                                   \
+    return syevd_fwd_abi<T>(batch, n, u, lambda, info, ws, ws_bytes, stream);                                     \
+  }                                                                                                               \
+  dla_status dla_syevd_bwd_##S(int64_t batch, int64_t n, T* abar, const T* ubar, const T* lambdabar, const T* u,  \
+                               const T* lambda, T eps_gap, void* ws, size_t ws_bytes, void* stream) {            \
+    return syevd_bwd_abi<T>(batch, n, abar, ubar, lambdabar, u, lambda, eps_gap, ws, ws_bytes, stream);           \
+  }
+
+DLA_DEFINE(float, f32)
+DLA_DEFINE(double, f64)
+
+}  // extern "C"

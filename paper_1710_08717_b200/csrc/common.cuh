@@ -1,0 +1,141 @@
+// Shared device/host plumbing for libdla_b200.so (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+
+#include "../../include/dla.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libdla_b200 is built for sm_100a only"
+#endif
+
+namespace dlab {
+
+// Batched strided matrix view: element (b, i, j) at p[b*bs + i*ld + j].
+// Row-major like the reference's MatrixView (dl/matrix.hpp:64-89), with an
+// explicit leading dimension so blocked algorithms address sub-blocks
+// in place.
+template <typename T>
+struct MatB {
+  T* p;
+  int64_t ld;
+  int64_t bs;
+  __host__ __device__ T* at(int64_t b, int64_t i, int64_t j) const {
+    return p + b * bs + i * ld + j;
+  }
+  __host__ __device__ MatB sub(int64_t i, int64_t j) const { return MatB{p + i * ld + j, ld, bs}; }
+};
+
+template <typename T>
+inline MatB<T> packed(T* p, int64_t rows, int64_t cols) {
+  (void)rows;
+  return MatB<T>{p, cols, rows * cols};
+}
+
+// Launch context: stream + device properties + optional per-slice info.
+struct Ctx {
+  cudaStream_t stream;
+  int sms;
+  int32_t* info;  // nullable: device int32[batch]
+};
+
+Ctx make_ctx(void* stream, int32_t* info);
+
+inline unsigned blocks_for(int64_t work, int threads, int64_t cap = 148 * 32) {
+  int64_t b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (unsigned)b;
+}
+
+// Skip rule shared by every kernel: a slice whose info is already set is
+// left untouched (the reference throws before writing, dl/blas.hpp:310-314).
+__device__ __forceinline__ bool slice_failed(const int32_t* info, int64_t b) {
+  return info != nullptr && info[b] != 0;
+}
+
+// First-failure-wins recording (serial block order => lowest index wins).
+__device__ __forceinline__ void record_failure(int32_t* info, int64_t b, int code, int64_t index) {
+  if (info != nullptr) atomicCAS(info + b, 0, DLA_INFO(code, index));
+}
+
+template <typename T>
+struct Num;
+template <>
+struct Num<double> {
+  __device__ static double sqrt_(double x) { return sqrt(x); }
+  __device__ static double log_(double x) { return log(x); }
+  static constexpr double sym_rtol = 1e-10;
+  static constexpr double rank_rtol = 1e-12;
+};
+template <>
+struct Num<float> {
+  __device__ static float sqrt_(float x) { return sqrtf(x); }
+  __device__ static float log_(float x) { return logf(x); }
+  static constexpr float sym_rtol = 1e-4f;
+  static constexpr float rank_rtol = 1e-5f;
+};
+
+#define DLAB_LAUNCH_CHECK()                                  \
+  do {                                                       \
+    cudaError_t e_ = cudaGetLastError();                     \
+    if (e_ != cudaSuccess) {                                 \
+      fprintf(stderr, "dla_b200: %s (%s:%d)\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return DLA_ERR_CUDA;                                   \
+    }                                                        \
+  } while (0)
+
+#define DLAB_TRY(expr)              \
+  do {                              \
+    dla_status s_ = (expr);         \
+    if (s_ != DLA_OK) return s_;    \
+  } while (0)
+
+// Triangle masks for the GEMM epilogue / elementwise kernels.
+enum Mask : int { MASK_FULL = 0, MASK_LOWER = 1, MASK_UPPER = 2 };
+
+// ----------------------------------------------------------------- kernels
+// gemm.cu: C = alpha op(A) op(B) + beta C over a batch (beta == 0 => C is
+// not read).  mask restricts writes to the lower/upper triangle of C
+// (global (i,j) of this C view); masked-out tiles do no math.
+template <typename T>
+dla_status gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T alpha, MatB<const T> a,
+                bool ta, MatB<const T> b, bool tb, T beta, MatB<T> cm, int mask = MASK_FULL,
+                const int32_t* skip = nullptr);
+
+// elementwise.cu
+template <typename T>
+dla_status ew_copy(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> src, MatB<T> dst);
+template <typename T>
+dla_status ew_scale(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<T> x, T alpha,
+                    const int32_t* skip = nullptr);
+// op: 0 tril, 1 triu, 2 copyltu, 3 copyutl, 4 sym, 5 transpose, 6 scaled sym (x*alpha then sym)
+template <typename T>
+dla_status ew_square(const Ctx& c, int64_t batch, int64_t n, MatB<T> x, int op, T alpha = T(1),
+                     const int32_t* skip = nullptr);
+template <typename T>
+dla_status check_symmetric(const Ctx& c, int64_t batch, int64_t n, MatB<const T> a, int32_t* info);
+template <typename T>
+dla_status check_zero_diag(const Ctx& c, int64_t batch, int64_t n, MatB<const T> t, int32_t* info);
+template <typename T>
+dla_status sumlogdiag_fwd(const Ctx& c, int64_t batch, int64_t n, T* out, MatB<const T> a);
+template <typename T>
+dla_status sumlogdiag_bwd(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, const T* g,
+                          MatB<const T> a, bool accumulate);
+
+// tri.cu: blocked triangular algorithms (any n), in place.
+template <typename T>
+dla_status trsm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x,
+                bool right, bool trans, bool lower, T alpha);
+template <typename T>
+dla_status trmm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x,
+                bool right, bool trans, bool lower, T alpha);
+template <typename T>
+dla_status potrf_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a);
+template <typename T>
+dla_status potri_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a);
+
+}  // namespace dlab

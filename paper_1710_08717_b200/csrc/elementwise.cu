@@ -1,0 +1,271 @@
+// Structural / elementwise kernels: the reference's dl/transforms.hpp helpers
+// (tril/triu/copyltu/copyutl/sym/scale, :18-130), the symmetry precheck
+// (dl/cholesky.hpp:19-25), the zero-diagonal precheck (dl/blas.hpp:310-314,
+// dl/cholesky.hpp:108-110) and the sumlogdiag op (tape chain
+// ExtractDiag -> Log -> Sum, dl/tape.hpp:789-795, :714, :747-755, pullbacks
+// :1038-1045, :969-975, :1080-1086).  All HBM-bound; grid-stride loops over
+// (batch x elements) sized to the SM count.
+#include "common.cuh"
+
+namespace dlab {
+namespace {
+
+template <typename T>
+__global__ void k_copy(int64_t batch, int64_t m, int64_t n, MatB<const T> src, MatB<T> dst) {
+  const int64_t total = batch * m * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t / (m * n), r = t % (m * n), i = r / n, j = r % n;
+    *dst.at(b, i, j) = *src.at(b, i, j);
+  }
+}
+
+template <typename T>
+__global__ void k_scale(int64_t batch, int64_t m, int64_t n, MatB<T> x, T alpha, const int32_t* skip) {
+  const int64_t total = batch * m * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t / (m * n), r = t % (m * n), i = r / n, j = r % n;
+    if (slice_failed(skip, b)) continue;
+    *x.at(b, i, j) *= alpha;
+  }
+}
+
+// Square structural ops over (b, i, j).
+template <typename T>
+__global__ void k_square(int64_t batch, int64_t n, MatB<T> x, int op, T alpha, const int32_t* skip) {
+  const int64_t total = batch * n * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t / (n * n), r = t % (n * n), i = r / n, j = r % n;
+    if (slice_failed(skip, b)) continue;
+    T* xij = x.at(b, i, j);
+    switch (op) {
+      case 0:  // tril: zero strict upper
+        if (j > i) *xij = T(0);
+        break;
+      case 1:  // triu: zero strict lower
+        if (j < i) *xij = T(0);
+        break;
+      case 2:  // copyltu: x(i,j) = x(j,i) for j > i
+        if (j > i) *xij = *x.at(b, j, i);
+        break;
+      case 3:  // copyutl: x(i,j) = x(j,i) for j < i
+        if (j < i) *xij = *x.at(b, j, i);
+        break;
+      case 4:    // sym: (x + x^T) / 2, exactly idempotent (dl/transforms.hpp:78-87)
+      case 6: {  // scaled sym: x <- alpha x, then sym
+        if (j < i) {
+          T* xji = x.at(b, j, i);
+          T u = *xij, v = *xji;
+          if (op == 6) {
+            u *= alpha;
+            v *= alpha;
+          }
+          const T s = (v + u) / T(2);  // (x(i',j') + x(j',i'))/2 with i' < j' as the reference
+          *xij = s;
+          *xji = s;
+        } else if (j == i && op == 6) {
+          *xij *= alpha;
+        }
+        break;
+      }
+      case 5:  // in-place transpose
+        if (j < i) {
+          T* xji = x.at(b, j, i);
+          T u = *xij;
+          *xij = *xji;
+          *xji = u;
+        }
+        break;
+    }
+  }
+}
+
+// Symmetry precheck, pass 1: per-slice max|a| and max|a_ij - a_ji| as
+// monotone bit patterns (non-negative IEEE values order as unsigned).
+template <typename T>
+__device__ __forceinline__ unsigned long long ord_bits(T v) {
+  if (!(v == v)) return 0ull;  // NaN ignored, like std::max in max_abs
+  if constexpr (sizeof(T) == 8) return (unsigned long long)__double_as_longlong((double)v);
+  else return (unsigned long long)__float_as_uint((float)v);
+}
+template <typename T>
+__device__ __forceinline__ T from_bits(unsigned long long u) {
+  if constexpr (sizeof(T) == 8) return __longlong_as_double((long long)u);
+  else return __uint_as_float((unsigned)u);
+}
+
+template <typename T>
+__global__ void k_symcheck_reduce(int64_t batch, int64_t n, MatB<const T> a, unsigned long long* red) {
+  // one CTA per (slice, row-chunk)
+  const int64_t chunks = (n + 31) / 32;
+  const int64_t b = blockIdx.x / chunks, c = blockIdx.x % chunks;
+  T mabs = T(0), masym = T(0);
+  const int64_t i0 = c * 32, i1 = min(n, i0 + 32);
+  for (int64_t t = threadIdx.x; t < (i1 - i0) * n; t += blockDim.x) {
+    const int64_t i = i0 + t / n, j = t % n;
+    const T v = *a.at(b, i, j);
+    const T av = fabs(v);
+    if (av > mabs) mabs = av;
+    if (j > i) {
+      const T d = fabs(v - *a.at(b, j, i));
+      if (d > masym) masym = d;
+    }
+  }
+  __shared__ unsigned long long s0[32], s1[32];
+  unsigned long long u0 = ord_bits(mabs), u1 = ord_bits(masym);
+  for (int o = 16; o; o >>= 1) {
+    u0 = max(u0, __shfl_xor_sync(0xffffffffu, u0, o));
+    u1 = max(u1, __shfl_xor_sync(0xffffffffu, u1, o));
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    s0[w] = u0;
+    s1[w] = u1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+      u0 = max(u0, s0[k]);
+      u1 = max(u1, s1[k]);
+    }
+    atomicMax(red + 2 * b, u0);
+    atomicMax(red + 2 * b + 1, u1);
+  }
+}
+
+template <typename T>
+__global__ void k_symcheck_decide(int64_t batch, const unsigned long long* red, int32_t* info) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < batch; b += (int64_t)gridDim.x * blockDim.x) {
+    const T scale = from_bits<T>(red[2 * b]);
+    const T asym = from_bits<T>(red[2 * b + 1]);
+    if (asym > Num<T>::sym_rtol * (scale > T(0) ? scale : T(1))) record_failure(info, b, DLA_ERR_ASYMMETRIC, 0);
+  }
+}
+
+// Exact-zero diagonal => SINGULAR(first k); checked before any write.
+template <typename T>
+__global__ void k_zero_diag(int64_t batch, int64_t n, MatB<const T> t, int32_t* info) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < batch; b += (int64_t)gridDim.x * blockDim.x) {
+    if (info[b] != 0) continue;
+    for (int64_t k = 0; k < n; ++k)
+      if (*t.at(b, k, k) == T(0)) {
+        info[b] = DLA_INFO(DLA_ERR_SINGULAR, k);
+        break;
+      }
+  }
+}
+
+// sumlogdiag forward: logs in parallel, sum strictly in i = 0..n-1 order.
+template <typename T>
+__global__ void k_sumlogdiag(int64_t n, T* out, MatB<const T> a) {
+  __shared__ T logs[1024];
+  const int64_t b = blockIdx.x;
+  T acc = T(0);
+  for (int64_t c0 = 0; c0 < n; c0 += 1024) {
+    const int64_t cn = min((int64_t)1024, n - c0);
+    for (int64_t i = threadIdx.x; i < cn; i += blockDim.x) logs[i] = Num<T>::log_(*a.at(b, c0 + i, c0 + i));
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int64_t i = 0; i < cn; ++i) acc += logs[i];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[b] = acc;
+}
+
+template <typename T>
+__global__ void k_sumlogdiag_bwd(int64_t batch, int64_t n, MatB<T> abar, const T* g, MatB<const T> a, int accumulate) {
+  const int64_t total = batch * n * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t / (n * n), r = t % (n * n), i = r / n, j = r % n;
+    T* p = abar.at(b, i, j);
+    if (i == j) {
+      const T v = g[b] / *a.at(b, i, i);
+      *p = accumulate ? *p + v : v;
+    } else if (!accumulate) {
+      *p = T(0);
+    }
+  }
+}
+
+}  // namespace
+
+template <typename T>
+dla_status ew_copy(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> src, MatB<T> dst) {
+  if (batch * m * n == 0 || src.p == dst.p) return DLA_OK;
+  k_copy<T><<<blocks_for(batch * m * n, 256), 256, 0, c.stream>>>(batch, m, n, src, dst);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+
+template <typename T>
+dla_status ew_scale(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<T> x, T alpha, const int32_t* skip) {
+  if (batch * m * n == 0 || alpha == T(1)) return DLA_OK;
+  k_scale<T><<<blocks_for(batch * m * n, 256), 256, 0, c.stream>>>(batch, m, n, x, alpha, skip);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+
+template <typename T>
+dla_status ew_square(const Ctx& c, int64_t batch, int64_t n, MatB<T> x, int op, T alpha, const int32_t* skip) {
+  if (batch * n == 0) return DLA_OK;
+  k_square<T><<<blocks_for(batch * n * n, 256), 256, 0, c.stream>>>(batch, n, x, op, alpha, skip);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+
+template <typename T>
+dla_status check_symmetric(const Ctx& c, int64_t batch, int64_t n, MatB<const T> a, int32_t* info) {
+  if (info == nullptr || batch * n == 0) return DLA_OK;
+  unsigned long long* red = nullptr;
+  if (cudaMallocAsync(&red, sizeof(unsigned long long) * 2 * batch, c.stream) != cudaSuccess) return DLA_ERR_CUDA;
+  cudaMemsetAsync(red, 0, sizeof(unsigned long long) * 2 * batch, c.stream);
+  const int64_t chunks = (n + 31) / 32;
+  k_symcheck_reduce<T><<<(unsigned)(batch * chunks), 256, 0, c.stream>>>(batch, n, a, red);
+  k_symcheck_decide<T><<<blocks_for(batch, 256), 256, 0, c.stream>>>(batch, red, info);
+  cudaFreeAsync(red, c.stream);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+
+template <typename T>
+dla_status check_zero_diag(const Ctx& c, int64_t batch, int64_t n, MatB<const T> t, int32_t* info) {
+  if (info == nullptr || batch * n == 0) return DLA_OK;
+  k_zero_diag<T><<<blocks_for(batch, 128), 128, 0, c.stream>>>(batch, n, t, info);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+
+template <typename T>
+dla_status sumlogdiag_fwd(const Ctx& c, int64_t batch, int64_t n, T* out, MatB<const T> a) {
+  if (batch == 0) return DLA_OK;
+  if (n == 0) return cudaMemsetAsync(out, 0, sizeof(T) * batch, c.stream) == cudaSuccess ? DLA_OK : DLA_ERR_CUDA;
+  k_sumlogdiag<T><<<(unsigned)batch, 128, 0, c.stream>>>(n, out, a);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+
+template <typename T>
+dla_status sumlogdiag_bwd(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, const T* g, MatB<const T> a,
+                          bool accumulate) {
+  if (batch * n == 0) return DLA_OK;
+  if (accumulate) {  // only the diagonal is touched
+    k_sumlogdiag_bwd<T><<<blocks_for(batch * n * n, 256), 256, 0, c.stream>>>(batch, n, abar, g, a, 1);
+  } else {
+    k_sumlogdiag_bwd<T><<<blocks_for(batch * n * n, 256), 256, 0, c.stream>>>(batch, n, abar, g, a, 0);
+  }
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+
+#define INST(T)                                                                                          \
+  template dla_status ew_copy<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<const T>, MatB<T>);        \
+  template dla_status ew_scale<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<T>, T, const int32_t*);   \
+  template dla_status ew_square<T>(const Ctx&, int64_t, int64_t, MatB<T>, int, T, const int32_t*);      \
+  template dla_status check_symmetric<T>(const Ctx&, int64_t, int64_t, MatB<const T>, int32_t*);        \
+  template dla_status check_zero_diag<T>(const Ctx&, int64_t, int64_t, MatB<const T>, int32_t*);        \
+  template dla_status sumlogdiag_fwd<T>(const Ctx&, int64_t, int64_t, T*, MatB<const T>);               \
+  template dla_status sumlogdiag_bwd<T>(const Ctx&, int64_t, int64_t, MatB<T>, const T*, MatB<const T>, \
+                                        bool);
+INST(double)
+INST(float)
+
+}  // namespace dlab

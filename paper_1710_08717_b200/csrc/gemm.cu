@@ -1,0 +1,337 @@
+// Batched strided GEMM for the blocked factorizations and the backward
+// compositions:  C = alpha op(A) op(B) + beta C  (beta == 0 => C not read),
+// with an optional lower/upper write mask (SYRK-style trailing updates skip
+// the tiles above/below the diagonal entirely).
+//
+// f64: FP64 tensor cores.  Each warp owns a 32x32 output tile built from
+//      4x4 `mma.sync.m8n8k4.f64` (SASS DMMA.8x8x4); tcgen05 has no f64 kind,
+//      and the measured DMMA ceiling on B200 is 37.1 TFLOP/s
+//      (profiles/peaks_fp64_fp32_r01.json).
+// f32: FFMA SIMT (exact binary32, no TF32 rounding), 4x4 register tiles.
+//
+// Operand tiles are staged global->shared with cp.async (zero-filled out of
+// bounds) in a 3-stage pipeline; 16-byte vectors when the leading dimension
+// and the contiguous extent allow, 8/4-byte otherwise, so every shape works.
+// Batch and tiles share a flat grid.x (65536-slice batches exceed gridDim.z).
+#include "common.cuh"
+
+namespace dlab {
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, PAD = 4;
+
+template <typename T>
+struct GemmArgs {
+  int64_t m, n, k;
+  T alpha, beta;
+  MatB<const T> a, b;
+  MatB<T> c;
+  int mask;
+  const int32_t* skip;
+  int64_t tiles_m, tiles_n;
+};
+
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem, bool pred, int bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int src = pred ? bytes : 0;
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src));
+  else if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Shared-memory tile geometry.  A tile (BM x BK logical) is stored [m][k]
+// when !TA (rows of A are contiguous in k) and [k][m] when TA; B likewise
+// [k][n] when !TB and [n][k] when TB.  PAD = 4 elements keeps the 64-bit
+// fragment loads of a half-warp on distinct banks.
+template <typename T, bool TA>
+struct ATile {
+  static constexpr int LD = TA ? (BM + PAD) : (BK + PAD);
+  static constexpr int ELEMS = TA ? BK * LD : BM * LD;
+  __device__ static int idx(int i, int k) { return TA ? k * LD + i : i * LD + k; }
+};
+template <typename T, bool TB>
+struct BTile {
+  static constexpr int LD = TB ? (BK + PAD) : (BN + PAD);
+  static constexpr int ELEMS = TB ? BN * LD : BK * LD;
+  __device__ static int idx(int k, int j) { return TB ? j * LD + k : k * LD + j; }
+};
+
+// Issue the cp.async loads of k-block `kb` into stage buffers sa / sb.
+template <typename T, bool TA, bool TB, int VA, int VB, int NT>
+__device__ __forceinline__ void load_stage(const GemmArgs<T>& g, int64_t bidx, int64_t m0, int64_t n0,
+                                           int64_t k0, T* sa, T* sb) {
+  const T* A = g.a.p + bidx * g.a.bs;
+  const T* B = g.b.p + bidx * g.b.bs;
+  // A: logical tile (i in BM, k in BK), vectors along the contiguous dim.
+  {
+    constexpr int CH = (BM * BK) / VA;
+    for (int c = threadIdx.x; c < CH; c += NT) {
+      int i, k;
+      if (!TA) {  // contiguous along k
+        i = c / (BK / VA);
+        k = (c % (BK / VA)) * VA;
+      } else {    // contiguous along i
+        k = c / (BM / VA);
+        i = (c % (BM / VA)) * VA;
+      }
+      const int64_t gi = m0 + i, gk = k0 + k;
+      const bool ok = gi < g.m && gk < g.k;
+      const T* src = ok ? (TA ? A + gk * g.a.ld + gi : A + gi * g.a.ld + gk) : A;
+      cp_async(sa + ATile<T, TA>::idx(i, k), src, ok, VA * (int)sizeof(T));
+    }
+  }
+  {
+    constexpr int CH = (BN * BK) / VB;
+    for (int c = threadIdx.x; c < CH; c += NT) {
+      int j, k;
+      if (!TB) {  // contiguous along j
+        k = c / (BN / VB);
+        j = (c % (BN / VB)) * VB;
+      } else {    // contiguous along k
+        j = c / (BK / VB);
+        k = (c % (BK / VB)) * VB;
+      }
+      const int64_t gj = n0 + j, gk = k0 + k;
+      const bool ok = gj < g.n && gk < g.k;
+      const T* src = ok ? (TB ? B + gj * g.b.ld + gk : B + gk * g.b.ld + gj) : B;
+      cp_async(sb + BTile<T, TB>::idx(k, j), src, ok, VB * (int)sizeof(T));
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ bool tile_masked_out(int mask, int64_t m0, int64_t n0) {
+  if (mask == MASK_LOWER) return n0 > m0 + BM - 1;
+  if (mask == MASK_UPPER) return m0 > n0 + BN - 1;
+  return false;
+}
+
+template <typename T>
+__device__ __forceinline__ void store_c(const GemmArgs<T>& g, int64_t bidx, int64_t gi, int64_t gj, T v) {
+  if (gi >= g.m || gj >= g.n) return;
+  if (g.mask == MASK_LOWER && gj > gi) return;
+  if (g.mask == MASK_UPPER && gj < gi) return;
+  T* cp = g.c.p + bidx * g.c.bs + gi * g.c.ld + gj;
+  T r = g.alpha * v;
+  if (g.beta != T(0)) r += g.beta * *cp;
+  *cp = r;
+}
+
+// ------------------------------------------------------------------ f64 DMMA
+template <bool TA, bool TB, int VA, int VB>
+__global__ void __launch_bounds__(128) dgemm_dmma(GemmArgs<double> g) {
+  using AT = ATile<double, TA>;
+  using BT = BTile<double, TB>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* smem = reinterpret_cast<double*>(smem_raw);
+  double* sA = smem;
+  double* sB = smem + STAGES * AT::ELEMS;
+
+  int64_t tile = blockIdx.x;
+  const int64_t per = g.tiles_m * g.tiles_n;
+  const int64_t bidx = tile / per;
+  tile -= bidx * per;
+  const int64_t m0 = (tile / g.tiles_n) * BM, n0 = (tile % g.tiles_n) * BN;
+  if (g.skip && g.skip[bidx]) return;
+  if (tile_masked_out<double>(g.mask, m0, n0)) return;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int fr = lane >> 2, fc = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int64_t nk = (g.k + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage<double, TA, TB, VA, VB, 128>(g, bidx, m0, n0, s * BK, sA + s * AT::ELEMS, sB + s * BT::ELEMS);
+    cp_commit();
+  }
+  for (int64_t kb = 0; kb < nk; ++kb) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    const int st = (int)(kb % STAGES);
+    // prefetch kb + STAGES - 1 into the slot freed at kb - 1
+    {
+      const int64_t pf = kb + STAGES - 1;
+      const int ps = (int)(pf % STAGES);
+      if (pf < nk) load_stage<double, TA, TB, VA, VB, 128>(g, bidx, m0, n0, pf * BK, sA + ps * AT::ELEMS, sB + ps * BT::ELEMS);
+      cp_commit();
+    }
+    const double* a = sA + st * AT::ELEMS;
+    const double* b = sB + st * BT::ELEMS;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = a[AT::idx(wm + i * 8 + fr, kk + fc)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = b[BT::idx(kk + fc, wn + j * 8 + fr)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          asm volatile(
+              "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+              : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
+              : "d"(af[i]), "d"(bf[j]));
+    }
+  }
+  cp_wait<0>();
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t gi = m0 + wm + i * 8 + fr;
+      const int64_t gj = n0 + wn + j * 8 + 2 * fc;
+      store_c<double>(g, bidx, gi, gj, acc[i][j][0]);
+      store_c<double>(g, bidx, gi, gj + 1, acc[i][j][1]);
+    }
+}
+
+// ------------------------------------------------------------------ f32 FFMA
+template <bool TA, bool TB, int VA, int VB>
+__global__ void __launch_bounds__(256) sgemm_ffma(GemmArgs<float> g) {
+  using AT = ATile<float, TA>;
+  using BT = BTile<float, TB>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* smem = reinterpret_cast<float*>(smem_raw);
+  float* sA = smem;
+  float* sB = smem + STAGES * AT::ELEMS;
+
+  int64_t tile = blockIdx.x;
+  const int64_t per = g.tiles_m * g.tiles_n;
+  const int64_t bidx = tile / per;
+  tile -= bidx * per;
+  const int64_t m0 = (tile / g.tiles_n) * BM, n0 = (tile % g.tiles_n) * BN;
+  if (g.skip && g.skip[bidx]) return;
+  if (tile_masked_out<float>(g.mask, m0, n0)) return;
+
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 4x4 each
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+  const int64_t nk = (g.k + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage<float, TA, TB, VA, VB, 256>(g, bidx, m0, n0, s * BK, sA + s * AT::ELEMS, sB + s * BT::ELEMS);
+    cp_commit();
+  }
+  for (int64_t kb = 0; kb < nk; ++kb) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    const int st = (int)(kb % STAGES);
+    {
+      const int64_t pf = kb + STAGES - 1;
+      const int ps = (int)(pf % STAGES);
+      if (pf < nk) load_stage<float, TA, TB, VA, VB, 256>(g, bidx, m0, n0, pf * BK, sA + ps * AT::ELEMS, sB + ps * BT::ELEMS);
+      cp_commit();
+    }
+    const float* a = sA + st * AT::ELEMS;
+    const float* b = sB + st * BT::ELEMS;
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = a[AT::idx(ty + 16 * i, kk)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = b[BT::idx(kk, tx + 16 * j)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+  }
+  cp_wait<0>();
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) store_c<float>(g, bidx, m0 + ty + 16 * i, n0 + tx + 16 * j, acc[i][j]);
+}
+
+template <typename T, bool TA, bool TB, int VA, int VB>
+cudaError_t launch_tv(const GemmArgs<T>& g, int64_t batch, cudaStream_t s) {
+  const int64_t grid = batch * g.tiles_m * g.tiles_n;
+  const size_t smem = sizeof(T) * STAGES * (ATile<T, TA>::ELEMS + BTile<T, TB>::ELEMS);
+  if constexpr (sizeof(T) == 8) {
+    auto k = dgemm_dmma<TA, TB, VA, VB>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    k<<<(unsigned)grid, 128, smem, s>>>(g);
+  } else {
+    auto k = sgemm_ffma<TA, TB, VA, VB>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    k<<<(unsigned)grid, 256, smem, s>>>(g);
+  }
+  return cudaGetLastError();
+}
+
+template <typename T, bool TA, bool TB>
+cudaError_t launch_t(const GemmArgs<T>& g, int64_t batch, cudaStream_t s, bool va, bool vb) {
+  constexpr int V = 16 / (int)sizeof(T);
+  if (va && vb) return launch_tv<T, TA, TB, V, V>(g, batch, s);
+  if (va) return launch_tv<T, TA, TB, V, 1>(g, batch, s);
+  if (vb) return launch_tv<T, TA, TB, 1, V>(g, batch, s);
+  return launch_tv<T, TA, TB, 1, 1>(g, batch, s);
+}
+
+// Vector loads need 16-byte aligned rows and a contiguous extent that is a
+// multiple of the vector width.
+template <typename T>
+bool vec_ok(const MatB<const T>& x, int64_t contiguous_extent) {
+  constexpr int V = 16 / (int)sizeof(T);
+  const uintptr_t p = reinterpret_cast<uintptr_t>(x.p);
+  return (p % 16 == 0) && (x.ld % V == 0) && (x.bs % V == 0) && (contiguous_extent % V == 0);
+}
+
+}  // namespace
+
+template <typename T>
+dla_status gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T alpha, MatB<const T> a,
+                bool ta, MatB<const T> b, bool tb, T beta, MatB<T> cm, int mask, const int32_t* skip) {
+  if (batch <= 0 || m <= 0 || n <= 0) return DLA_OK;
+  if (k <= 0) {  // C = beta C
+    if (beta == T(1)) return DLA_OK;
+    if (mask != MASK_FULL) return DLA_ERR_INVALID;
+    return ew_scale<T>(c, batch, m, n, cm, beta, skip);
+  }
+  GemmArgs<T> g{m, n, k, alpha, beta, a, b, cm, mask, skip, (m + BM - 1) / BM, (n + BN - 1) / BN};
+  const bool va = vec_ok<T>(a, ta ? m : k);
+  const bool vb = vec_ok<T>(b, tb ? k : n);
+  cudaError_t e;
+  if (!ta && !tb) e = launch_t<T, false, false>(g, batch, c.stream, va, vb);
+  else if (ta && !tb) e = launch_t<T, true, false>(g, batch, c.stream, va, vb);
+  else if (!ta && tb) e = launch_t<T, false, true>(g, batch, c.stream, va, vb);
+  else e = launch_t<T, true, true>(g, batch, c.stream, va, vb);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "dla_b200 gemm: %s\n", cudaGetErrorString(e));
+    return DLA_ERR_CUDA;
+  }
+  return DLA_OK;
+}
+
+template dla_status gemm<double>(const Ctx&, int64_t, int64_t, int64_t, int64_t, double, MatB<const double>,
+                                 bool, MatB<const double>, bool, double, MatB<double>, int, const int32_t*);
+template dla_status gemm<float>(const Ctx&, int64_t, int64_t, int64_t, int64_t, float, MatB<const float>,
+                                bool, MatB<const float>, bool, float, MatB<float>, int, const int32_t*);
+
+}  // namespace dlab

@@ -1,0 +1,34 @@
+// Internal declarations of the fused / special-purpose operator kernels.
+#pragma once
+
+#include "common.cuh"
+
+namespace dlab {
+
+// small.cu — one CTA per matrix, whole matrix in shared memory (n <= 64).
+template <typename T>
+bool potrf_small_eligible(int64_t n);
+template <typename T>
+dla_status potrf_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool lower);
+template <typename T>
+dla_status potrf_bwd_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> lbar,
+                           MatB<const T> l, bool lower);
+
+// gelqf.cu
+template <typename T>
+size_t gelqf_ws_bytes(int64_t batch, int64_t m, int64_t n, bool backward);
+template <typename T>
+dla_status gelqf_fwd(const Ctx& c, int64_t batch, int64_t m, int64_t n, T* q, T* l, void* ws);
+
+// syevd.cu
+template <typename T>
+size_t syevd_ws_bytes(int64_t batch, int64_t n, bool backward);
+template <typename T>
+dla_status syevd_fwd(const Ctx& c, int64_t batch, int64_t n, T* u, T* lambda, void* ws);
+template <typename T>
+dla_status syevd_gap_kernel(const Ctx& c, int64_t batch, int64_t n, MatB<T> w, const T* lambdabar, const T* lambda,
+                            T eps_gap);
+template <typename T>
+dla_status ew_sym_into(const Ctx& c, int64_t batch, int64_t n, MatB<const T> w, MatB<T> out);
+
+}  // namespace dlab
