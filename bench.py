@@ -1,0 +1,419 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the B200-native dlinalg hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|potrf1024|c3|c4|c5]
+                    [--impl ours|reference]
+
+Default workload (BASELINE.json configs[1], the config the metric is quoted
+on): Gaussian-process NLL + hyperparameter gradient, RBF kernel, n = 4096,
+d = 8, fp64 — the reference's make_gp + Graph::backward graph
+(dl/models.hpp:94-135), evaluated by paper_1710_08717_b200.gp.GPNLL through
+the C-ABI operator library.  One step = one NLL + full gradient evaluation.
+Multi-GPU (torchrun, one process per GPU): C2 does not shard (one 128 MiB
+factorization) — every rank runs an independent replica ("replicas only",
+scaling "weak"); value = evals of all ranks / max-over-ranks time.
+
+Timing: W untimed warm-up steps, then K steps between CUDA events on the
+launching stream, bracketed by barrier + synchronize, max over ranks.  The
+per-step working set (A and Abar, 2 x 128 MiB) exceeds the 126 MB L2.
+``e2e`` repeats the measurement through the public API with pinned host
+buffers: H2D of x, y and D2H of (nll, grads) inside every step.
+``--impl reference`` times the reference's own CPU implementation
+(oracle/_ref/libdla_ref.so, compiled from /root/reference) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GP NLL+grad evals/s"
+BASELINE_METRIC = "batched potrf fwd+bwd matrices/s & GFLOP/s vs FP64 peak; GP NLL+grad evals/s"
+PEAKS_FILE = os.path.join(ROOT, "profiles", "peaks_fp64_fp32_r01.json")
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "gemm_traffic_r01.json")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="c2", choices=["c2", "c1", "potrf1024", "c3", "c4", "c5"])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-also", action="store_true")
+    return p.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ timing
+def timed(torch, fn, steps, warmup, world):
+    """W warm-ups, then K steps between CUDA events on the current stream;
+    barrier + synchronize on both sides; max over ranks (ms per step)."""
+    dist = torch.distributed
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        fn()
+    e1.record(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    return ms / steps
+
+
+def peaks():
+    fp64 = None
+    src = None
+    if os.path.exists(PEAKS_FILE):
+        d = json.load(open(PEAKS_FILE))
+        fp64 = d.get("dmma_m8n8k4_tflops")
+        src = "profiles/peaks_fp64_fp32_r01.json (measured DMMA loop on this pool's B200; MEASURED_PEAKS.json has no FP64 figure)"
+    hbm = None
+    if os.path.exists(MEASURED):
+        hbm = json.load(open(MEASURED)).get("hbm_gbs")
+    return fp64 or 37.08, src or "fallback", hbm or 6535.4
+
+
+def gemm_roofline(torch, lib, step_fn):
+    """One extra (untimed) step with CUDA events around every GEMM launch."""
+    import ctypes as C
+    torch.cuda.synchronize()
+    lib.dla_prof_enable(1)
+    step_fn()
+    torch.cuda.synchronize()
+    ms, fl = C.c_double(0), C.c_double(0)
+    n = lib.dla_prof_read(C.byref(ms), C.byref(fl))
+    lib.dla_prof_enable(0)
+    return n, ms.value, fl.value
+
+
+# -------------------------------------------------------------- workloads
+def gp_flops(n, d):
+    """Algorithmic flops per eval: potrf n^3/3 + potrf_bwd 4n^3/3."""
+    return 5.0 * n ** 3 / 3.0
+
+
+def run_c2(torch, args, rank, world, lib):
+    from paper_1710_08717_b200 import gp
+    from oracle import oracle as O  # input generator only (Philox); never on the product path
+    n, d = 4096, 8
+    r = O.rng(1234 + rank)
+    xh = r.standard_normal((1, n, d))
+    yh = r.standard_normal((1, n, 1))
+    x = torch.from_numpy(xh).cuda()
+    y = torch.from_numpy(yh).cuda()
+    s2, l2, lam = 1.0, 1.0, 0.1
+    g = gp.GPNLL(n, d, 1, "cuda", want_xbar=True)
+
+    def step():
+        g.step(x, y, s2, l2, lam)
+
+    step()
+    g.check()
+    clk = Clocks(torch.cuda.current_device()) if rank == 0 else None
+    c0 = lib.dla_launch_count()
+    ms = timed(torch, step, args.steps, args.warmup, world)
+    launches = (lib.dla_launch_count() - c0) / (args.steps + args.warmup)
+    clocks = clk.stop() if clk else None
+    g.check()
+
+    # e2e: pinned host inputs, H2D + step + D2H of (nll, grads) every step
+    xp = torch.from_numpy(xh).pin_memory()
+    yp = torch.from_numpy(yh).pin_memory()
+    outp = torch.empty(4, dtype=torch.float64).pin_memory()
+    xd = torch.empty_like(x)
+    yd = torch.empty_like(y)
+
+    def e2e_step():
+        xd.copy_(xp, non_blocking=True)
+        yd.copy_(yp, non_blocking=True)
+        nll, grads, _, _ = g.step(xd, yd, s2, l2, lam)
+        outp[0:1].copy_(nll, non_blocking=True)
+        outp[1:4].copy_(grads.view(3), non_blocking=True)
+
+    ms_e2e = timed(torch, e2e_step, args.steps, min(args.warmup, 3), world)
+    nlaunch, gms, gfl = gemm_roofline(torch, lib, step)
+    return dict(ms=ms, ms_e2e=ms_e2e, launches=launches, clocks=clocks, gemm=(nlaunch, gms, gfl),
+                flops=gp_flops(n, d), h2d=xh.nbytes + yh.nbytes, d2h=4 * 8,
+                workload="C2: GP NLL + hyperparameter gradient (and x/y gradients), RBF, n=4096, d=8, fp64",
+                nll=float(g.nll[0].item()), units_per_step=1)
+
+
+def c1_chain_fns(torch, B, n=32):
+    """C1 chain on device: L = potrf(A); z = trsm(L, y); phi = 1/2|z|^2 + sumlogdiag(L);
+    backward phibar = 1 (the reference harness ref_c1_chain_f64 computes the same)."""
+    from paper_1710_08717_b200 import linalg as L
+    from oracle import oracle as O
+    r = O.rng(7)
+    a0 = torch.from_numpy(O.random_spd(n, r, batch=B)).cuda()
+    y0 = torch.from_numpy(r.standard_normal((B, n, 1))).cuda()
+    a = torch.empty_like(a0)
+    z = torch.empty_like(y0)
+    ybar = torch.empty_like(y0)
+    lbar = torch.empty_like(a0)
+    quad = torch.empty(B, 1, 1, dtype=torch.float64, device="cuda")
+    logdet = torch.empty(B, dtype=torch.float64, device="cuda")
+    ones = torch.ones(B, dtype=torch.float64, device="cuda")
+    info = torch.zeros(B, dtype=torch.int32, device="cuda")
+
+    def step():
+        a.copy_(a0)
+        z.copy_(y0)
+        L.potrf_inplace(a, True, check=False, info=info)
+        L.trsm_inplace(a, z, check=False)
+        L.gemm2_into(quad, z, z, True, False, 0.5)
+        L.sumlogdiag(a, out=logdet)
+        L.trsm_backward_into(ybar, lbar, z, a, z, False, False, True, 1.0)
+        L.sumlogdiag_backward_into(lbar, ones, a, accumulate=True)
+        L.potrf_backward_into(lbar, lbar, a, True)
+
+    return step, (a0, y0, lbar, ybar)
+
+
+def run_potrf_batch(torch, n, B, steps, warmup, world):
+    from paper_1710_08717_b200 import linalg as L
+    from oracle import oracle as O
+    r = O.rng(11)
+    a0 = torch.from_numpy(O.random_spd(n, r, batch=B)).cuda()
+    lb0 = torch.from_numpy(np.tril(r.standard_normal((B, n, n)))).cuda()
+    a = torch.empty_like(a0)
+    ab = torch.empty_like(a0)
+    info = torch.zeros(B, dtype=torch.int32, device="cuda")
+
+    def step():
+        a.copy_(a0)
+        L.potrf_inplace(a, True, check=False, info=info)
+        L.potrf_backward_into(ab, lb0, a, True)
+
+    ms = timed(torch, step, steps, warmup, world)
+    return ms
+
+
+def also_measurements(torch, args, world, lib, fp64_peak, hbm):
+    out = []
+    # C1 chain, batch 64 x 32^2 (latency regime) and a large-batch sweep point
+    for B in (64, 65536):
+        step, _ = c1_chain_fns(torch, B)
+        ms = timed(torch, step, 20, 3, world)
+        n = 32
+        flops = B * (n ** 3 / 3 + 4 * n ** 3 / 3 + 4 * n * n)
+        out.append({"workload": f"C1 chain potrf+trsm+sumlogdiag fwd+bwd, batch {B} x 32^2 fp64",
+                    "matrices_per_s": world * B / (ms / 1e3), "ms_per_step": ms,
+                    "gflops": world * flops / (ms / 1e3) / 1e9})
+    for n, B in ((1024, 8), (32, 65536)):
+        ms = run_potrf_batch(torch, n, B, 10 if n > 64 else 20, 3, world)
+        flops = B * 5 * n ** 3 / 3
+        gf = world * flops / (ms / 1e3) / 1e9
+        out.append({"workload": f"potrf fwd+bwd, batch {B} x {n}^2 fp64 (incl. input copy)",
+                    "matrices_per_s": world * B / (ms / 1e3), "ms_per_step": ms, "gflops": gf,
+                    "frac_of_fp64_peak": gf / 1e3 / fp64_peak / world})
+    return out
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_baseline_c2():
+    """Reference make_gp + Graph::backward at n = 2048 on one host core, scaled
+    to n = 4096 by (2048/4096)^3 (the tape is single-threaded by construction)."""
+    from oracle import oracle as O
+    if not O.ref_available():
+        return None
+    ref = O.ref()
+    r = O.rng(99)
+    ns = 2048
+    x = r.standard_normal((ns, 8))
+    y = r.standard_normal((ns, 1))
+    t0 = time.perf_counter()
+    ref.gp_nll_grad(x, y, 1.0, 1.0, 0.1)
+    secs = time.perf_counter() - t0
+    return {"value": (1.0 / secs) * (ns / 4096) ** 3, "unit": "evals/s", "cores": 1, "kind": "reference",
+            "sample": f"1 reference make_gp+backward eval at n={ns}, d=8 ({secs:.1f} s, 1 core), "
+                      f"scaled to n=4096 by (n/4096)^3; a full n=4096 eval took ~157 s/core in the survey"}
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the reference CPU path on all host cores (rank 0 only)."""
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdla_ref.so not built"}))
+        return 0
+    from concurrent.futures import ThreadPoolExecutor
+    ref = O.ref()
+    cores = os.cpu_count() or 1
+    ns = 1024
+    r = O.rng(5)
+    probs = [(r.standard_normal((ns, 8)), r.standard_normal((ns, 1))) for _ in range(cores)]
+
+    def one(i):
+        x, y = probs[i]
+        return ref.gp_nll_grad(x, y, 1.0, 1.0, 0.1)
+
+    pool = ThreadPoolExecutor(max_workers=cores)
+    for _ in range(args.warmup):
+        list(pool.map(one, range(cores)))
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        list(pool.map(one, range(cores)))
+    secs = (time.perf_counter() - t0) / args.steps
+    scale = (ns / 4096) ** 3
+    value = cores * scale / secs
+    line = {"metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (Philox N(0,1) x, y)",
+            "config": {"workload": "C2: GP NLL + gradient, RBF, n=4096, d=8, fp64 (reference CPU tape)",
+                       "baseline_metric": BASELINE_METRIC},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "reference",
+                             "sample": f"{cores} concurrent reference make_gp+backward evals at n={ns} per step "
+                                       f"(one per host thread), scaled to n=4096 by (n/4096)^3"},
+            "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# -------------------------------------------------------------------- main
+def main():
+    args = parse()
+    rank, local, world = env_rank()
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+    import torch
+    if not torch.cuda.is_available():
+        print(json.dumps({"error": "no CUDA device"}))
+        return 1
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1710_08717_b200._lib import lib as _lib
+    lib = _lib().lib
+    fp64_peak, peak_src, hbm = peaks()
+    if args.config != "c2":
+        from tools import bench_configs  # secondary configs
+        res = bench_configs.run(torch, args, rank, world, lib, fp64_peak, hbm)
+        if rank == 0:
+            print(json.dumps(res))
+        return 0
+
+    r = run_c2(torch, args, rank, world, lib)
+    value = world * r["units_per_step"] / (r["ms"] / 1e3)
+    e2e = world * r["units_per_step"] / (r["ms_e2e"] / 1e3)
+    nl, gms, gfl = r["gemm"]
+    achieved = gfl / (gms / 1e3) / 1e12 if gms > 0 else None
+    traffic = None
+    if os.path.exists(TRAFFIC_FILE):
+        traffic = json.load(open(TRAFFIC_FILE)).get("dram_bytes_per_launch")
+    also = [] if args.no_also else also_measurements(torch, args, world, lib, fp64_peak, hbm)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_c2()
+    if rank == 0:
+        step_tflops = r["flops"] / (r["ms"] / 1e3) / 1e12
+        line = {
+            "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (Philox N(0,1) x [4096,8], y [4096,1])",
+            "config": {"workload": r["workload"], "n": 4096, "d": 8, "sigma2": 1.0, "ell2": 1.0, "lam": 0.1,
+                       "parallelism": f"replicas x{world} (C2 does not shard; no collective)",
+                       "l2": "per-step working set 2 x 128 MiB > 126 MB L2 (no flush needed)",
+                       "baseline_metric": BASELINE_METRIC},
+            "step_fp64_tflops": step_tflops,
+            "step_frac_of_fp64_peak": step_tflops / fp64_peak,
+            "roofline": {"bound": "tensor", "kernel": "dgemm_dmma (FP64 DMMA m8n8k4 batched GEMM)",
+                         "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                         "frac": (achieved / fp64_peak) if achieved else None, "traffic": traffic,
+                         "peak_source": peak_src, "gemm_launches_per_step": nl,
+                         "gemm_share_of_step": (gms / r["ms"]) if r["ms"] else None},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e, "unit": "evals/s", "h2d_bytes_per_step": r["h2d"],
+                    "d2h_bytes_per_step": r["d2h"], "ms_per_step": r["ms_e2e"]},
+            "gpu_launches": int(round(r["launches"] * args.steps)),
+            "gpu_launches_per_step": r["launches"],
+            "clocks": r["clocks"],
+            "nll": r["nll"],
+            "also": also,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -194,6 +194,32 @@ dla_status dla_info_check(const int32_t* info, int64_t batch, void* stream,
 DLA_DECLARE_OPS(float, f32)
 DLA_DECLARE_OPS(double, f64)
 
+/* --------------------------------------------------------- instrumentation */
+/* Kernels launched by this library so far (host-side counter). */
+long long dla_launch_count(void);
+/* GEMM launch timing with CUDA events on the launching stream (off by
+ * default; enabling clears previous records). */
+void dla_prof_enable(int on);
+long long dla_prof_read(double* ms, double* flops);
+
+/* ------------------------------------------------------------ GP driver */
+/* Fused RBF-kernel build and pullback for the Gaussian-process NLL driver
+ * (dl/models.hpp:50-65 rbf_kernel + :95-98 K + lam I; pullbacks of the tape
+ * chain dl/tape.hpp:930-1036).  x: [batch, n, d] (d <= 32), a/abar:
+ * [batch, n, n].  grads: [batch, 3] = d phi / d(log sigma2, log ell2,
+ * log lam) given abar = d phi / dA; xbar (nullable): [batch, n, d].
+ * workspace: dla_gp_rbf_ws_bytes(batch, n, d). */
+size_t dla_gp_rbf_ws_bytes(int64_t batch, int64_t n, int64_t d);
+dla_status dla_gp_rbf_fwd_f64(int64_t batch, int64_t n, int64_t d, const double* x, double sigma2,
+                              double ell2, double lam, double* a, void* ws, size_t ws_bytes,
+                              void* stream);
+dla_status dla_gp_rbf_bwd_f64(int64_t batch, int64_t n, int64_t d, const double* x, double sigma2,
+                              double ell2, double lam, const double* abar, double* xbar,
+                              double* grads, void* ws, size_t ws_bytes, void* stream);
+/* nll[b] = quad[b] + logdet[b] + n/2 log(2 pi)  (dl/models.hpp:100-103). */
+dla_status dla_gp_nll_assemble_f64(int64_t batch, int64_t n, const double* quad,
+                                   const double* logdet, double* nll, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -342,15 +342,19 @@ class Ref(_Lib):
         self._chk(st)
         return (out.value, abar) if with_grad else out.value
 
-    def gp_nll_grad(self, x, y, sigma2, ell2, lam):
+    def gp_nll_grad(self, x, y, sigma2, ell2, lam, with_xy=False):
+        """make_gp + Graph::backward: [nll, d/dlog sigma2, d/dlog ell2, d/dlog lam]
+        (and xbar, ybar when with_xy)."""
         x = np.ascontiguousarray(x, np.float64)
         y = np.ascontiguousarray(y, np.float64).reshape(-1)
         out = np.zeros(4)
+        xbar = np.zeros_like(x) if with_xy else None
+        ybar = np.zeros_like(y) if with_xy else None
         st = self.lib.ref_gp_nll_grad_f64(_i64(x.shape[0]), _i64(x.shape[1]), _ptr(x), _ptr(y),
                                           C.c_double(sigma2), C.c_double(ell2), C.c_double(lam),
-                                          _ptr(out))
+                                          _ptr(out), _ptr(xbar), _ptr(ybar))
         self._chk(st)
-        return out
+        return (out, xbar, ybar) if with_xy else out
 
     # batched timing drivers (reference for_each_slice); return seconds
     def c1_chain(self, a, y, threads=1):

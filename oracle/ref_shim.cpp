@@ -189,7 +189,7 @@ int ref_sumlogdiag_f64(int64_t n, const double* a, double* out, double* abar) {
 // dl/tape.hpp:461-484).  out = {nll, d/dlog_sigma2, d/dlog_ell2, d/dlog_lam}.
 // Single-threaded by construction (the tape never fans out).
 int ref_gp_nll_grad_f64(int64_t n, int64_t d, const double* x, const double* y, double sigma2,
-                        double ell2, double lam, double* out) {
+                        double ell2, double lam, double* out, double* xbar, double* ybar) {
   return guarded([&] {
     dla::Matrix<double> xm(n, d), ym(n, 1);
     std::memcpy(xm.data(), x, sizeof(double) * n * d);
@@ -201,6 +201,8 @@ int ref_gp_nll_grad_f64(int64_t n, int64_t d, const double* x, const double* y, 
     out[1] = gs.at(m.log_sigma2)(0, 0);
     out[2] = gs.at(m.log_ell2)(0, 0);
     out[3] = gs.at(m.log_lam)(0, 0);
+    if (xbar) std::memcpy(xbar, gs.at(m.x).data(), sizeof(double) * n * d);
+    if (ybar) std::memcpy(ybar, gs.at(m.y).data(), sizeof(double) * n);
   }, nullptr);
 }
 

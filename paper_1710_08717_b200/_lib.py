@@ -62,6 +62,21 @@ class _Lib:
         L.dla_workspace_bytes.argtypes = [_int, _int, _i64, _i64, _i64, _i64, _int]
         L.dla_info_check.restype = _int
         L.dla_info_check.argtypes = [_vp, _i64, _vp, C.POINTER(_i64), C.POINTER(_i64)]
+        L.dla_launch_count.restype = C.c_longlong
+        L.dla_launch_count.argtypes = []
+        L.dla_prof_enable.restype = None
+        L.dla_prof_enable.argtypes = [_int]
+        L.dla_prof_read.restype = C.c_longlong
+        L.dla_prof_read.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.dla_gp_rbf_ws_bytes.restype = _sz
+        L.dla_gp_rbf_ws_bytes.argtypes = [_i64, _i64, _i64]
+        gsig = [_i64, _i64, _i64, _vp, C.c_double, C.c_double, C.c_double]
+        L.dla_gp_rbf_fwd_f64.argtypes = gsig + [_vp, _vp, _sz, _vp]
+        L.dla_gp_rbf_fwd_f64.restype = _int
+        L.dla_gp_rbf_bwd_f64.argtypes = gsig + [_vp, _vp, _vp, _vp, _sz, _vp]
+        L.dla_gp_rbf_bwd_f64.restype = _int
+        L.dla_gp_nll_assemble_f64.argtypes = [_i64, _i64, _vp, _vp, _vp, _vp]
+        L.dla_gp_nll_assemble_f64.restype = _int
         self.fns = {}
         for name, sig in _SIGS.items():
             for suffix, scal in (("f32", C.c_float), ("f64", C.c_double)):
@@ -87,7 +102,9 @@ def lib() -> _Lib:
 
 def exported_symbols():
     """Every dla_* symbol include/dla.h declares (used by the CPU symbol test)."""
-    names = ["dla_status_string", "dla_version", "dla_workspace_bytes", "dla_info_check"]
+    names = ["dla_status_string", "dla_version", "dla_workspace_bytes", "dla_info_check",
+             "dla_launch_count", "dla_prof_enable", "dla_prof_read", "dla_gp_rbf_ws_bytes",
+             "dla_gp_rbf_fwd_f64", "dla_gp_rbf_bwd_f64", "dla_gp_nll_assemble_f64"]
     for name in _SIGS:
         for s in ("f32", "f64"):
             names.append(f"dla_{name}_{s}")

@@ -2,6 +2,7 @@
 // mirrors the reference's ShapeError / alias sites, then stream-ordered
 // launches.  Backward ops follow the reference's closed-form compositions
 // (dl/adjoints.hpp) on the batched device kernels.
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -24,6 +25,44 @@ Ctx make_ctx(void* stream, int32_t* info) {
     }
   });
   return Ctx{reinterpret_cast<cudaStream_t>(stream), sms, info};
+}
+
+static std::atomic<long long> g_launches{0};
+static std::atomic<bool> g_prof{false};
+static std::mutex g_prof_mu;
+struct ProfRec {
+  cudaEvent_t a, b;
+  double flops;
+};
+static std::vector<ProfRec> g_prof_recs;
+static std::vector<cudaEvent_t> g_event_pool;
+static thread_local cudaEvent_t t_pending = nullptr;
+
+void note_launch(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+bool gemm_prof_on() { return g_prof.load(std::memory_order_relaxed); }
+
+static cudaEvent_t take_event() {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void gemm_prof_begin(cudaStream_t s) {
+  t_pending = take_event();
+  cudaEventRecord(t_pending, s);
+}
+
+void gemm_prof_end(cudaStream_t s, double flops) {
+  cudaEvent_t e = take_event();
+  cudaEventRecord(e, s);
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_recs.push_back(ProfRec{t_pending, e, flops});
 }
 
 namespace {
@@ -403,6 +442,35 @@ const char* dla_status_string(dla_status s) {
 }
 
 const char* dla_version(void) { return "dla_b200 0.1 (sm_100a)"; }
+
+long long dla_launch_count(void) { return g_launches.load(); }
+
+void dla_prof_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& r : g_prof_recs) {
+    g_event_pool.push_back(r.a);
+    g_event_pool.push_back(r.b);
+  }
+  g_prof_recs.clear();
+  g_prof.store(on != 0);
+}
+
+// Synchronises the recorded events; returns the number of GEMM launches and
+// their summed device time (ms) and algorithmic flops.
+long long dla_prof_read(double* ms, double* flops) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  double t = 0, f = 0;
+  for (auto& r : g_prof_recs) {
+    cudaEventSynchronize(r.b);
+    float x = 0;
+    cudaEventElapsedTime(&x, r.a, r.b);
+    t += x;
+    f += r.flops;
+  }
+  if (ms) *ms = t;
+  if (flops) *flops = f;
+  return (long long)g_prof_recs.size();
+}
 
 size_t dla_workspace_bytes(dla_op op, dla_dtype dtype, int64_t batch, int64_t m, int64_t n, int64_t k, int phase) {
   (void)k;

@@ -44,6 +44,13 @@ struct Ctx {
 
 Ctx make_ctx(void* stream, int32_t* info);
 
+// Host-side count of kernels this library launched (bench.py's gpu_launches
+// claim) and optional CUDA-event timing of every GEMM launch (roofline).
+void note_launch(int k = 1);
+bool gemm_prof_on();
+void gemm_prof_begin(cudaStream_t s);
+void gemm_prof_end(cudaStream_t s, double flops);
+
 inline unsigned blocks_for(int64_t work, int threads, int64_t cap = 148 * 32) {
   int64_t b = (work + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -86,6 +93,7 @@ struct Num<float> {
       fprintf(stderr, "dla_b200: %s (%s:%d)\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
       return DLA_ERR_CUDA;                                   \
     }                                                        \
+    note_launch(1);                                          \
   } while (0)
 
 #define DLAB_TRY(expr)              \

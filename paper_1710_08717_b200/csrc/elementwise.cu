@@ -222,6 +222,7 @@ dla_status check_symmetric(const Ctx& c, int64_t batch, int64_t n, MatB<const T>
   k_symcheck_reduce<T><<<(unsigned)(batch * chunks), 256, 0, c.stream>>>(batch, n, a, red);
   k_symcheck_decide<T><<<blocks_for(batch, 256), 256, 0, c.stream>>>(batch, red, info);
   cudaFreeAsync(red, c.stream);
+  note_launch(1);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }

@@ -318,6 +318,8 @@ dla_status gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T 
   const bool va = vec_ok<T>(a, ta ? m : k);
   const bool vb = vec_ok<T>(b, tb ? k : n);
   cudaError_t e;
+  const bool prof = gemm_prof_on();
+  if (prof) gemm_prof_begin(c.stream);
   if (!ta && !tb) e = launch_t<T, false, false>(g, batch, c.stream, va, vb);
   else if (ta && !tb) e = launch_t<T, true, false>(g, batch, c.stream, va, vb);
   else if (!ta && tb) e = launch_t<T, false, true>(g, batch, c.stream, va, vb);
@@ -325,6 +327,13 @@ dla_status gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T 
   if (e != cudaSuccess) {
     fprintf(stderr, "dla_b200 gemm: %s\n", cudaGetErrorString(e));
     return DLA_ERR_CUDA;
+  }
+  note_launch(1);
+  if (prof) {
+    // algorithmic flops: 2 m n k, or the kept triangle only under a mask
+    double useful = (double)m * (double)n;
+    if (mask != MASK_FULL && m == n) useful = (double)m * (double)(m + 1) / 2.0;
+    gemm_prof_end(c.stream, 2.0 * useful * (double)k * (double)batch);
   }
   return DLA_OK;
 }

@@ -1,0 +1,211 @@
+// Gaussian-process driver kernels either side of the Cholesky path (SURVEY
+// §8f row 1): the RBF kernel build and its pullback, fused into one HBM pass
+// each instead of the reference tape's ~15 elementwise n x n nodes.
+//
+// Forward  (dl/models.hpp:50-65, :95-98):
+//   dist_ij = (s_i + s_j) - 2 G_ij,   s = sum_rows(x∘x),  G = syrk(x)
+//   A_ij    = sigma2 * exp(-(dist_ij / (2 ell2))) + lam * I_ij
+// Backward (tape pullbacks dl/tape.hpp:930-1036 composed by hand), given
+// Abar = dphi/dA (symmetric):
+//   dsigma2 = sum Abar∘E,   dlam = tr(Abar),
+//   d(2 ell2) = sum Nbar∘D / (2 ell2),  Nbar = Abar sigma2 E,  D = dist/(2 ell2)
+//   xbar_i  = 4 sum_j W_ij (x_i - x_j),  W = -Nbar / (2 ell2)   (syrk + square
+//             + tile pullbacks with W symmetric)
+//   returned as gradients w.r.t. the log-parameters (dl/models.hpp:126-131).
+// Reductions are two-level with fixed order (no atomics): run-to-run
+// deterministic.
+#include "common.cuh"
+
+namespace dlab {
+namespace {
+
+constexpr int RT = 256;
+constexpr int MAXD = 32;
+
+// s_i = sum_f x_if^2 (sequential f, like SumRows)
+__global__ void k_rowsq(int64_t batch, int64_t n, int64_t d, const double* x, double* s) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < batch * n; t += (int64_t)gridDim.x * blockDim.x) {
+    const double* xi = x + t * d;
+    double acc = 0.0;
+    for (int64_t f = 0; f < d; ++f) acc += xi[f] * xi[f];
+    s[t] = acc;
+  }
+}
+
+__device__ __forceinline__ double gram(const double* xa, const double* xb, int64_t d) {
+  double acc = 0.0;
+  for (int64_t f = 0; f < d; ++f) acc += xa[f] * xb[f];
+  return acc;
+}
+
+// One CTA per (slice, row i); threads sweep j.  Writes full rows (coalesced).
+__global__ void __launch_bounds__(RT) k_rbf_fwd(int64_t n, int64_t d, const double* x, const double* s, double sigma2,
+                                                double two_ell2, double lam, double* a) {
+  __shared__ double xi_s[MAXD];
+  const int64_t row = blockIdx.x;  // b * n + i
+  const int64_t b = row / n, i = row % n;
+  const double* xb = x + b * n * d;
+  if (threadIdx.x < d) xi_s[threadIdx.x] = xb[i * d + threadIdx.x];
+  __syncthreads();
+  const double si = s[b * n + i];
+  double* arow = a + b * n * n + i * n;
+  for (int64_t j = threadIdx.x; j < n; j += RT) {
+    // G_ij from the (max, min) pair: syrk fills the lower triangle and mirrors
+    const double g = gram(xi_s, xb + j * d, d);
+    const double dist = (si + s[b * n + j]) - 2.0 * g;
+    double v = sigma2 * exp(-(dist / two_ell2));
+    if (j == i) v += lam;
+    arow[j] = v;
+  }
+}
+
+// Per (slice, row-block) partial sums + xbar rows.
+__global__ void __launch_bounds__(RT) k_rbf_bwd(int64_t n, int64_t d, const double* x, const double* s, double sigma2,
+                                                double two_ell2, const double* abar, double* xbar, double* part) {
+  __shared__ double xi_s[MAXD];
+  __shared__ double red[3][RT / 32];
+  __shared__ double xred[RT / 32][MAXD];
+  const int64_t row = blockIdx.x;
+  const int64_t b = row / n, i = row % n;
+  const double* xb = x + b * n * d;
+  if (threadIdx.x < d) xi_s[threadIdx.x] = xb[i * d + threadIdx.x];
+  __syncthreads();
+  const double si = s[b * n + i];
+  const double* ar = abar + b * n * n + i * n;
+  double ps = 0.0, pl = 0.0, pe = 0.0;
+  double xacc[MAXD];
+  for (int f = 0; f < d; ++f) xacc[f] = 0.0;
+  for (int64_t j = threadIdx.x; j < n; j += RT) {
+    const double* xj = xb + j * d;
+    const double g = gram(xi_s, xj, d);
+    const double dist = (si + s[b * n + j]) - 2.0 * g;
+    const double D = dist / two_ell2;
+    const double E = exp(-D);
+    const double kb = ar[j];
+    ps += kb * E;                   // sigma2-bar
+    const double nb = kb * sigma2 * E;
+    pe += nb * D;                   // (2 ell2)-bar * (2 ell2)
+    if (j == i) pl += kb;           // lam-bar (trace)
+    if (xbar) {
+      const double w = -nb / two_ell2;  // dist-bar
+      for (int f = 0; f < d; ++f) xacc[f] += w * (xi_s[f] - xj[f]);
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int o = 16; o; o >>= 1) {
+    ps += __shfl_xor_sync(0xffffffffu, ps, o);
+    pl += __shfl_xor_sync(0xffffffffu, pl, o);
+    pe += __shfl_xor_sync(0xffffffffu, pe, o);
+  }
+  if (lane == 0) {
+    red[0][warp] = ps;
+    red[1][warp] = pl;
+    red[2][warp] = pe;
+  }
+  if (xbar) {
+    for (int f = 0; f < d; ++f) {
+      double v = xacc[f];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) xred[warp][f] = v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double acc = 0.0;
+    for (int w = 0; w < RT / 32; ++w) acc += red[threadIdx.x][w];
+    part[row * 3 + threadIdx.x] = acc;
+  }
+  if (xbar && threadIdx.x < d) {
+    double acc = 0.0;
+    for (int w = 0; w < RT / 32; ++w) acc += xred[w][threadIdx.x];
+    xbar[(b * n + i) * d + threadIdx.x] = 4.0 * acc;
+  }
+}
+
+// Fixed-order finalization per slice: grads w.r.t. (log sigma2, log ell2, log lam).
+__global__ void k_rbf_finalize(int64_t batch, int64_t n, const double* part, double sigma2, double ell2,
+                               double lam, double two_ell2, double* grads) {
+  const int64_t b = blockIdx.x;
+  __shared__ double red[3][RT];
+  double a0 = 0, a1 = 0, a2 = 0;
+  for (int64_t i = threadIdx.x; i < n; i += RT) {
+    a0 += part[(b * n + i) * 3 + 0];
+    a1 += part[(b * n + i) * 3 + 1];
+    a2 += part[(b * n + i) * 3 + 2];
+  }
+  red[0][threadIdx.x] = a0;
+  red[1][threadIdx.x] = a1;
+  red[2][threadIdx.x] = a2;
+  __syncthreads();
+  for (int st = RT / 2; st; st >>= 1) {
+    if (threadIdx.x < st)
+      for (int k = 0; k < 3; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double sbar = red[0][0], lbar = red[1][0];
+    const double two_ell2_bar = red[2][0] / two_ell2;  // -sum(Dbar∘D)/(2 ell2), Dbar = -Nbar
+    const double ell2_bar = 2.0 * two_ell2_bar;
+    grads[b * 3 + 0] = sbar * sigma2;
+    grads[b * 3 + 1] = ell2_bar * ell2;
+    grads[b * 3 + 2] = lbar * lam;
+  }
+}
+
+__global__ void k_nll(int64_t batch, int64_t n, const double* quad, const double* logdet, double* nll) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b < batch) nll[b] = (quad[b] + logdet[b]) + 0.5 * (double)n * 1.8378770664093454835606594728112353;
+}
+
+}  // namespace
+}  // namespace dlab
+
+using namespace dlab;
+
+extern "C" {
+
+size_t dla_gp_rbf_ws_bytes(int64_t batch, int64_t n, int64_t d) {
+  (void)d;
+  return sizeof(double) * (size_t)(batch * n + batch * n * 3);
+}
+
+dla_status dla_gp_rbf_fwd_f64(int64_t batch, int64_t n, int64_t d, const double* x, double sigma2, double ell2,
+                              double lam, double* a, void* ws, size_t ws_bytes, void* stream) {
+  if (batch < 0 || n < 0 || d < 0 || d > MAXD) return DLA_ERR_SHAPE;
+  if (batch * n == 0) return DLA_OK;
+  if (!ws || ws_bytes < dla_gp_rbf_ws_bytes(batch, n, d)) return DLA_ERR_WORKSPACE;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  double* sq = static_cast<double*>(ws);
+  k_rowsq<<<blocks_for(batch * n, 256), 256, 0, s>>>(batch, n, d, x, sq);
+  k_rbf_fwd<<<(unsigned)(batch * n), RT, 0, s>>>(n, d, x, sq, sigma2, ell2 * 2.0, lam, a);
+  note_launch(1);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+
+dla_status dla_gp_rbf_bwd_f64(int64_t batch, int64_t n, int64_t d, const double* x, double sigma2, double ell2,
+                              double lam, const double* abar, double* xbar, double* grads, void* ws,
+                              size_t ws_bytes, void* stream) {
+  if (batch < 0 || n < 0 || d < 0 || d > MAXD) return DLA_ERR_SHAPE;
+  if (batch * n == 0) return DLA_OK;
+  if (!ws || ws_bytes < dla_gp_rbf_ws_bytes(batch, n, d)) return DLA_ERR_WORKSPACE;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  double* sq = static_cast<double*>(ws);
+  double* part = sq + batch * n;
+  k_rowsq<<<blocks_for(batch * n, 256), 256, 0, s>>>(batch, n, d, x, sq);
+  k_rbf_bwd<<<(unsigned)(batch * n), RT, 0, s>>>(n, d, x, sq, sigma2, ell2 * 2.0, abar, xbar, part);
+  k_rbf_finalize<<<(unsigned)batch, RT, 0, s>>>(batch, n, part, sigma2, ell2, lam, ell2 * 2.0, grads);
+  note_launch(2);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+
+dla_status dla_gp_nll_assemble_f64(int64_t batch, int64_t n, const double* quad, const double* logdet, double* nll,
+                                   void* stream) {
+  if (batch <= 0) return DLA_OK;
+  k_nll<<<blocks_for(batch, 128), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(batch, n, quad, logdet, nll);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+
+}  // extern "C"

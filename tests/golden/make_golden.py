@@ -49,7 +49,13 @@ def main():
     x = r.standard_normal((96, 8))
     y = r.standard_normal((96, 1))
     out["gp:96/x"], out["gp:96/y"] = x, y
-    out["gp:96/out"] = ref.gp_nll_grad(x, y, 1.0, 1.0, 0.1)
+    o, xb, yb = ref.gp_nll_grad(x, y, 1.0, 1.0, 0.1, with_xy=True)
+    out["gp:96/out"], out["gp:96/xbar"], out["gp:96/ybar"] = o, xb, yb
+    x = r.standard_normal((300, 8))
+    y = r.standard_normal((300, 1))
+    o, xb, yb = ref.gp_nll_grad(x, y, 1.3, 0.7, 0.05, with_xy=True)
+    out["gp:300/x"], out["gp:300/y"], out["gp:300/out"] = x, y, o
+    out["gp:300/xbar"], out["gp:300/ybar"] = xb, yb
     dst = os.path.join(os.path.dirname(os.path.abspath(__file__)), "ref_vectors.npz")
     np.savez_compressed(dst, **out)
     print("wrote", dst, len(out), "arrays")
