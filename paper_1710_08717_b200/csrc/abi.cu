@@ -192,8 +192,7 @@ dla_status trsm_fwd(int64_t batch, int64_t m, int64_t n, const T* t, T* x, int r
   if (overlap(x, bytes<T>(batch, m, n), t, bytes<T>(batch, nt, nt))) return DLA_ERR_ALIAS;
   Ctx cx = make_ctx(stream, info);
   DLAB_TRY(reset_info(cx, batch));
-  DLAB_TRY(check_zero_diag<T>(cx, batch, nt, cpk(t, nt, nt), info));
-  return trsm<T>(cx, batch, m, n, cpk(t, nt, nt), pk(x, m, n), right, trans, lower, alpha);
+  return trsm<T>(cx, batch, m, n, cpk(t, nt, nt), pk(x, m, n), right, trans, lower, alpha, /*check_diag*/ true);
 }
 
 template <typename T>

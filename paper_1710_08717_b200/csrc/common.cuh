@@ -137,7 +137,7 @@ dla_status sumlogdiag_bwd(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, 
 // tri.cu: blocked triangular algorithms (any n), in place.
 template <typename T>
 dla_status trsm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x,
-                bool right, bool trans, bool lower, T alpha);
+                bool right, bool trans, bool lower, T alpha, bool check_diag = false);
 template <typename T>
 dla_status trmm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x,
                 bool right, bool trans, bool lower, T alpha);

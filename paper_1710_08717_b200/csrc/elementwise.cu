@@ -142,16 +142,18 @@ __global__ void k_symcheck_decide(int64_t batch, const unsigned long long* red, 
 }
 
 // Exact-zero diagonal => SINGULAR(first k); checked before any write.
+// One CTA per slice; the smallest zero index wins.
 template <typename T>
 __global__ void k_zero_diag(int64_t batch, int64_t n, MatB<const T> t, int32_t* info) {
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < batch; b += (int64_t)gridDim.x * blockDim.x) {
-    if (info[b] != 0) continue;
-    for (int64_t k = 0; k < n; ++k)
-      if (*t.at(b, k, k) == T(0)) {
-        info[b] = DLA_INFO(DLA_ERR_SINGULAR, k);
-        break;
-      }
-  }
+  __shared__ int first;
+  const int64_t b = blockIdx.x;
+  if (threadIdx.x == 0) first = 0x7fffffff;
+  __syncthreads();
+  if (info[b] != 0) return;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x)
+    if (*t.at(b, k, k) == T(0)) atomicMin(&first, (int)k);
+  __syncthreads();
+  if (threadIdx.x == 0 && first != 0x7fffffff) info[b] = DLA_INFO(DLA_ERR_SINGULAR, first);
 }
 
 // sumlogdiag forward: logs in parallel, sum strictly in i = 0..n-1 order.
@@ -230,7 +232,7 @@ dla_status check_symmetric(const Ctx& c, int64_t batch, int64_t n, MatB<const T>
 template <typename T>
 dla_status check_zero_diag(const Ctx& c, int64_t batch, int64_t n, MatB<const T> t, int32_t* info) {
   if (info == nullptr || batch * n == 0) return DLA_OK;
-  k_zero_diag<T><<<blocks_for(batch, 128), 128, 0, c.stream>>>(batch, n, t, info);
+  k_zero_diag<T><<<(unsigned)batch, 256, 0, c.stream>>>(batch, n, t, info);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }

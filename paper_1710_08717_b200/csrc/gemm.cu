@@ -18,7 +18,18 @@
 namespace dlab {
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, PAD = 4;
+constexpr int BK = 16, STAGES = 3, PAD = 4;
+
+// Tile configurations: CTA tile BM x BN, warp tile WM x WN (FP64 DMMA).
+template <int BM_, int BN_, int WM_, int WN_>
+struct Cfg {
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_;
+  static constexpr int WARPS_N = BN / WN;
+  static constexpr int WARPS = (BM / WM) * (BN / WN);
+  static constexpr int NT = WARPS * 32;
+};
+using CfgS = Cfg<64, 64, 32, 32>;    // 128 threads: small / batched problems
+using CfgL = Cfg<128, 128, 64, 32>;  // 256 threads: large trailing updates
 
 template <typename T>
 struct GemmArgs {
@@ -49,29 +60,32 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 // when !TA (rows of A are contiguous in k) and [k][m] when TA; B likewise
 // [k][n] when !TB and [n][k] when TB.  PAD = 4 elements keeps the 64-bit
 // fragment loads of a half-warp on distinct banks.
-template <typename T, bool TA>
+template <int BM, bool TA>
 struct ATile {
   static constexpr int LD = TA ? (BM + PAD) : (BK + PAD);
   static constexpr int ELEMS = TA ? BK * LD : BM * LD;
   __device__ static int idx(int i, int k) { return TA ? k * LD + i : i * LD + k; }
 };
-template <typename T, bool TB>
+template <int BN, bool TB>
 struct BTile {
   static constexpr int LD = TB ? (BK + PAD) : (BN + PAD);
   static constexpr int ELEMS = TB ? BN * LD : BK * LD;
   __device__ static int idx(int k, int j) { return TB ? j * LD + k : k * LD + j; }
 };
 
-// Issue the cp.async loads of k-block `kb` into stage buffers sa / sb.
-template <typename T, bool TA, bool TB, int VA, int VB, int NT>
+// Issue the cp.async loads of one k-block into stage buffers sa / sb.
+template <typename T, class C, bool TA, bool TB, int VA, int VB>
 __device__ __forceinline__ void load_stage(const GemmArgs<T>& g, int64_t bidx, int64_t m0, int64_t n0,
                                            int64_t k0, T* sa, T* sb) {
   const T* A = g.a.p + bidx * g.a.bs;
   const T* B = g.b.p + bidx * g.b.bs;
-  // A: logical tile (i in BM, k in BK), vectors along the contiguous dim.
+  constexpr int BM = C::BM, BN = C::BN, NT = C::NT;
   {
     constexpr int CH = (BM * BK) / VA;
-    for (int c = threadIdx.x; c < CH; c += NT) {
+#pragma unroll
+    for (int c0 = 0; c0 < CH; c0 += NT) {
+      const int c = c0 + threadIdx.x;
+      if (CH % NT != 0 && c >= CH) break;
       int i, k;
       if (!TA) {  // contiguous along k
         i = c / (BK / VA);
@@ -83,12 +97,15 @@ __device__ __forceinline__ void load_stage(const GemmArgs<T>& g, int64_t bidx, i
       const int64_t gi = m0 + i, gk = k0 + k;
       const bool ok = gi < g.m && gk < g.k;
       const T* src = ok ? (TA ? A + gk * g.a.ld + gi : A + gi * g.a.ld + gk) : A;
-      cp_async(sa + ATile<T, TA>::idx(i, k), src, ok, VA * (int)sizeof(T));
+      cp_async(sa + ATile<BM, TA>::idx(i, k), src, ok, VA * (int)sizeof(T));
     }
   }
   {
     constexpr int CH = (BN * BK) / VB;
-    for (int c = threadIdx.x; c < CH; c += NT) {
+#pragma unroll
+    for (int c0 = 0; c0 < CH; c0 += NT) {
+      const int c = c0 + threadIdx.x;
+      if (CH % NT != 0 && c >= CH) break;
       int j, k;
       if (!TB) {  // contiguous along j
         k = c / (BN / VB);
@@ -100,12 +117,12 @@ __device__ __forceinline__ void load_stage(const GemmArgs<T>& g, int64_t bidx, i
       const int64_t gj = n0 + j, gk = k0 + k;
       const bool ok = gj < g.n && gk < g.k;
       const T* src = ok ? (TB ? B + gj * g.b.ld + gk : B + gk * g.b.ld + gj) : B;
-      cp_async(sb + BTile<T, TB>::idx(k, j), src, ok, VB * (int)sizeof(T));
+      cp_async(sb + BTile<BN, TB>::idx(k, j), src, ok, VB * (int)sizeof(T));
     }
   }
 }
 
-template <typename T>
+template <int BM, int BN>
 __device__ __forceinline__ bool tile_masked_out(int mask, int64_t m0, int64_t n0) {
   if (mask == MASK_LOWER) return n0 > m0 + BM - 1;
   if (mask == MASK_UPPER) return m0 > n0 + BN - 1;
@@ -124,10 +141,11 @@ __device__ __forceinline__ void store_c(const GemmArgs<T>& g, int64_t bidx, int6
 }
 
 // ------------------------------------------------------------------ f64 DMMA
-template <bool TA, bool TB, int VA, int VB>
-__global__ void __launch_bounds__(128) dgemm_dmma(GemmArgs<double> g) {
-  using AT = ATile<double, TA>;
-  using BT = BTile<double, TB>;
+template <class C, bool TA, bool TB, int VA, int VB>
+__global__ void __launch_bounds__(C::NT) dgemm_dmma(GemmArgs<double> g) {
+  using AT = ATile<C::BM, TA>;
+  using BT = BTile<C::BN, TB>;
+  constexpr int MI = C::WM / 8, NI = C::WN / 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* smem = reinterpret_cast<double*>(smem_raw);
   double* sA = smem;
@@ -137,49 +155,50 @@ __global__ void __launch_bounds__(128) dgemm_dmma(GemmArgs<double> g) {
   const int64_t per = g.tiles_m * g.tiles_n;
   const int64_t bidx = tile / per;
   tile -= bidx * per;
-  const int64_t m0 = (tile / g.tiles_n) * BM, n0 = (tile % g.tiles_n) * BN;
+  const int64_t m0 = (tile / g.tiles_n) * C::BM, n0 = (tile % g.tiles_n) * C::BN;
   if (g.skip && g.skip[bidx]) return;
-  if (tile_masked_out<double>(g.mask, m0, n0)) return;
+  if (tile_masked_out<C::BM, C::BN>(g.mask, m0, n0)) return;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int wm = (warp / C::WARPS_N) * C::WM, wn = (warp % C::WARPS_N) * C::WN;
   const int fr = lane >> 2, fc = lane & 3;
-  double acc[4][4][2];
+  double acc[MI][NI][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int64_t nk = (g.k + BK - 1) / BK;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) load_stage<double, TA, TB, VA, VB, 128>(g, bidx, m0, n0, s * BK, sA + s * AT::ELEMS, sB + s * BT::ELEMS);
+    if (s < nk)
+      load_stage<double, C, TA, TB, VA, VB>(g, bidx, m0, n0, s * BK, sA + s * AT::ELEMS, sB + s * BT::ELEMS);
     cp_commit();
   }
   for (int64_t kb = 0; kb < nk; ++kb) {
     cp_wait<STAGES - 2>();
     __syncthreads();
     const int st = (int)(kb % STAGES);
-    // prefetch kb + STAGES - 1 into the slot freed at kb - 1
-    {
+    {  // prefetch kb + STAGES - 1 into the slot freed at kb - 1
       const int64_t pf = kb + STAGES - 1;
       const int ps = (int)(pf % STAGES);
-      if (pf < nk) load_stage<double, TA, TB, VA, VB, 128>(g, bidx, m0, n0, pf * BK, sA + ps * AT::ELEMS, sB + ps * BT::ELEMS);
+      if (pf < nk)
+        load_stage<double, C, TA, TB, VA, VB>(g, bidx, m0, n0, pf * BK, sA + ps * AT::ELEMS, sB + ps * BT::ELEMS);
       cp_commit();
     }
     const double* a = sA + st * AT::ELEMS;
     const double* b = sB + st * BT::ELEMS;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[4], bf[4];
+      double af[MI], bf[NI];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = a[AT::idx(wm + i * 8 + fr, kk + fc)];
+      for (int i = 0; i < MI; ++i) af[i] = a[AT::idx(wm + i * 8 + fr, kk + fc)];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = b[BT::idx(kk + fc, wn + j * 8 + fr)];
+      for (int j = 0; j < NI; ++j) bf[j] = b[BT::idx(kk + fc, wn + j * 8 + fr)];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < NI; ++j)
           asm volatile(
               "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
               : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
@@ -188,9 +207,9 @@ __global__ void __launch_bounds__(128) dgemm_dmma(GemmArgs<double> g) {
   }
   cp_wait<0>();
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NI; ++j) {
       const int64_t gi = m0 + wm + i * 8 + fr;
       const int64_t gj = n0 + wn + j * 8 + 2 * fc;
       store_c<double>(g, bidx, gi, gj, acc[i][j][0]);
@@ -201,8 +220,10 @@ __global__ void __launch_bounds__(128) dgemm_dmma(GemmArgs<double> g) {
 // ------------------------------------------------------------------ f32 FFMA
 template <bool TA, bool TB, int VA, int VB>
 __global__ void __launch_bounds__(256) sgemm_ffma(GemmArgs<float> g) {
-  using AT = ATile<float, TA>;
-  using BT = BTile<float, TB>;
+  using C = Cfg<64, 64, 32, 16>;  // 8 warps -> 256 threads; smem geometry of a 64 x 64 tile
+  static_assert(C::NT == 256, "sgemm thread count");
+  using AT = ATile<64, TA>;
+  using BT = BTile<64, TB>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* smem = reinterpret_cast<float*>(smem_raw);
   float* sA = smem;
@@ -212,9 +233,9 @@ __global__ void __launch_bounds__(256) sgemm_ffma(GemmArgs<float> g) {
   const int64_t per = g.tiles_m * g.tiles_n;
   const int64_t bidx = tile / per;
   tile -= bidx * per;
-  const int64_t m0 = (tile / g.tiles_n) * BM, n0 = (tile % g.tiles_n) * BN;
+  const int64_t m0 = (tile / g.tiles_n) * 64, n0 = (tile % g.tiles_n) * 64;
   if (g.skip && g.skip[bidx]) return;
-  if (tile_masked_out<float>(g.mask, m0, n0)) return;
+  if (tile_masked_out<64, 64>(g.mask, m0, n0)) return;
 
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 4x4 each
   float acc[4][4];
@@ -226,7 +247,7 @@ __global__ void __launch_bounds__(256) sgemm_ffma(GemmArgs<float> g) {
   const int64_t nk = (g.k + BK - 1) / BK;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) load_stage<float, TA, TB, VA, VB, 256>(g, bidx, m0, n0, s * BK, sA + s * AT::ELEMS, sB + s * BT::ELEMS);
+    if (s < nk) load_stage<float, C, TA, TB, VA, VB>(g, bidx, m0, n0, s * BK, sA + s * AT::ELEMS, sB + s * BT::ELEMS);
     cp_commit();
   }
   for (int64_t kb = 0; kb < nk; ++kb) {
@@ -236,7 +257,8 @@ __global__ void __launch_bounds__(256) sgemm_ffma(GemmArgs<float> g) {
     {
       const int64_t pf = kb + STAGES - 1;
       const int ps = (int)(pf % STAGES);
-      if (pf < nk) load_stage<float, TA, TB, VA, VB, 256>(g, bidx, m0, n0, pf * BK, sA + ps * AT::ELEMS, sB + ps * BT::ELEMS);
+      if (pf < nk)
+        load_stage<float, C, TA, TB, VA, VB>(g, bidx, m0, n0, pf * BK, sA + ps * AT::ELEMS, sB + ps * BT::ELEMS);
       cp_commit();
     }
     const float* a = sA + st * AT::ELEMS;
@@ -261,37 +283,62 @@ __global__ void __launch_bounds__(256) sgemm_ffma(GemmArgs<float> g) {
     for (int j = 0; j < 4; ++j) store_c<float>(g, bidx, m0 + ty + 16 * i, n0 + tx + 16 * j, acc[i][j]);
 }
 
+template <typename K>
+void ensure_smem(K k, size_t smem) {
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
 template <typename T, bool TA, bool TB, int VA, int VB>
-cudaError_t launch_tv(const GemmArgs<T>& g, int64_t batch, cudaStream_t s) {
-  const int64_t grid = batch * g.tiles_m * g.tiles_n;
-  const size_t smem = sizeof(T) * STAGES * (ATile<T, TA>::ELEMS + BTile<T, TB>::ELEMS);
+cudaError_t launch_tv(GemmArgs<T> g, int64_t batch, cudaStream_t s, bool large) {
   if constexpr (sizeof(T) == 8) {
-    auto k = dgemm_dmma<TA, TB, VA, VB>;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
+    if (large) {
+      using C = CfgL;
+      g.tiles_m = (g.m + C::BM - 1) / C::BM;
+      g.tiles_n = (g.n + C::BN - 1) / C::BN;
+      const size_t smem = sizeof(T) * STAGES * (ATile<C::BM, TA>::ELEMS + BTile<C::BN, TB>::ELEMS);
+      auto k = dgemm_dmma<C, TA, TB, VA, VB>;
+      static bool attr = false;
+      if (!attr) {
+        ensure_smem(k, smem);
+        attr = true;
+      }
+      k<<<(unsigned)(batch * g.tiles_m * g.tiles_n), C::NT, smem, s>>>(g);
+    } else {
+      using C = CfgS;
+      g.tiles_m = (g.m + C::BM - 1) / C::BM;
+      g.tiles_n = (g.n + C::BN - 1) / C::BN;
+      const size_t smem = sizeof(T) * STAGES * (ATile<C::BM, TA>::ELEMS + BTile<C::BN, TB>::ELEMS);
+      auto k = dgemm_dmma<C, TA, TB, VA, VB>;
+      static bool attr = false;
+      if (!attr) {
+        ensure_smem(k, smem);
+        attr = true;
+      }
+      k<<<(unsigned)(batch * g.tiles_m * g.tiles_n), C::NT, smem, s>>>(g);
     }
-    k<<<(unsigned)grid, 128, smem, s>>>(g);
   } else {
+    (void)large;
+    g.tiles_m = (g.m + 63) / 64;
+    g.tiles_n = (g.n + 63) / 64;
+    const size_t smem = sizeof(T) * STAGES * (ATile<64, TA>::ELEMS + BTile<64, TB>::ELEMS);
     auto k = sgemm_ffma<TA, TB, VA, VB>;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      ensure_smem(k, smem);
       attr = true;
     }
-    k<<<(unsigned)grid, 256, smem, s>>>(g);
+    k<<<(unsigned)(batch * g.tiles_m * g.tiles_n), 256, smem, s>>>(g);
   }
   return cudaGetLastError();
 }
 
 template <typename T, bool TA, bool TB>
-cudaError_t launch_t(const GemmArgs<T>& g, int64_t batch, cudaStream_t s, bool va, bool vb) {
+cudaError_t launch_t(const GemmArgs<T>& g, int64_t batch, cudaStream_t s, bool va, bool vb, bool large) {
   constexpr int V = 16 / (int)sizeof(T);
-  if (va && vb) return launch_tv<T, TA, TB, V, V>(g, batch, s);
-  if (va) return launch_tv<T, TA, TB, V, 1>(g, batch, s);
-  if (vb) return launch_tv<T, TA, TB, 1, V>(g, batch, s);
-  return launch_tv<T, TA, TB, 1, 1>(g, batch, s);
+  if (va && vb) return launch_tv<T, TA, TB, V, V>(g, batch, s, large);
+  if (va) return launch_tv<T, TA, TB, V, 1>(g, batch, s, large);
+  if (vb) return launch_tv<T, TA, TB, 1, V>(g, batch, s, large);
+  return launch_tv<T, TA, TB, 1, 1>(g, batch, s, large);
 }
 
 // Vector loads need 16-byte aligned rows and a contiguous extent that is a
@@ -314,16 +361,19 @@ dla_status gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T 
     if (mask != MASK_FULL) return DLA_ERR_INVALID;
     return ew_scale<T>(c, batch, m, n, cm, beta, skip);
   }
-  GemmArgs<T> g{m, n, k, alpha, beta, a, b, cm, mask, skip, (m + BM - 1) / BM, (n + BN - 1) / BN};
+  GemmArgs<T> g{m, n, k, alpha, beta, a, b, cm, mask, skip, 0, 0};
   const bool va = vec_ok<T>(a, ta ? m : k);
   const bool vb = vec_ok<T>(b, tb ? k : n);
+  // 128 x 128 tiles once they alone fill every SM; 64 x 64 otherwise
+  const int64_t big_tiles = batch * ((m + 127) / 128) * ((n + 127) / 128);
+  const bool large = big_tiles >= c.sms && k >= 64;
   cudaError_t e;
   const bool prof = gemm_prof_on();
   if (prof) gemm_prof_begin(c.stream);
-  if (!ta && !tb) e = launch_t<T, false, false>(g, batch, c.stream, va, vb);
-  else if (ta && !tb) e = launch_t<T, true, false>(g, batch, c.stream, va, vb);
-  else if (!ta && tb) e = launch_t<T, false, true>(g, batch, c.stream, va, vb);
-  else e = launch_t<T, true, true>(g, batch, c.stream, va, vb);
+  if (!ta && !tb) e = launch_t<T, false, false>(g, batch, c.stream, va, vb, large);
+  else if (ta && !tb) e = launch_t<T, true, false>(g, batch, c.stream, va, vb, large);
+  else if (!ta && tb) e = launch_t<T, false, true>(g, batch, c.stream, va, vb, large);
+  else e = launch_t<T, true, true>(g, batch, c.stream, va, vb, large);
   if (e != cudaSuccess) {
     fprintf(stderr, "dla_b200 gemm: %s\n", cudaGetErrorString(e));
     return DLA_ERR_CUDA;

@@ -7,6 +7,7 @@
 //               (dl/cholesky.hpp:35-72) + tril / transpose (:71, :85-86).
 //   potrf bwd : Abar = 1/2 sym(L^-T copyltu(L^T Lbar) L^-1)
 //               (dl/adjoints.hpp:175-191), upper variant by transposition.
+#include "chol64.cuh"
 #include "common.cuh"
 #include "ops.cuh"
 
@@ -32,6 +33,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_potrf_small(int n, MatB<T> a, bool lower, int32_t* info) {
   __shared__ T S[SN * SLD];
   __shared__ T red[8];
+  __shared__ T colbuf[2 * 66];
   const int64_t b = blockIdx.x;
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) S[(e / n) * SLD + e % n] = *a.at(b, e / n, e % n);
   __syncthreads();
@@ -52,38 +54,14 @@ __global__ void __launch_bounds__(256) k_potrf_small(int n, MatB<T> a, bool lowe
     if (threadIdx.x == 0) record_failure(info, b, DLA_ERR_ASYMMETRIC, 0);
     return;
   }
-  for (int j = 0; j < n; ++j) {
-    const T d = S[j * SLD + j];
-    if (!(d > T(0))) {
-      if (threadIdx.x == 0) record_failure(info, b, DLA_ERR_NOT_SPD, j);
-      return;
-    }
-    const T r = Num<T>::sqrt_(d);
-    const T inv = T(1) / r;
-    __syncthreads();
-    if (threadIdx.x == 0) S[j * SLD + j] = r;
-    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) S[i * SLD + j] *= inv;
-    __syncthreads();
-    const int m = n - j - 1;
-    const int tri = m * (m + 1) / 2;
-    for (int e = threadIdx.x; e < tri; e += blockDim.x) {
-      // e -> (ii, jj) with jj <= ii, both in [j+1, n)
-      int ii = (int)((sqrtf(8.f * e + 1.f) - 1.f) * 0.5f);
-      while ((ii + 1) * (ii + 2) / 2 <= e) ++ii;
-      while (ii * (ii + 1) / 2 > e) --ii;
-      const int jj = e - ii * (ii + 1) / 2;
-      const int gi = j + 1 + ii, gj = j + 1 + jj;
-      S[gi * SLD + gj] -= S[gi * SLD + j] * S[gj * SLD + j];
-    }
-    __syncthreads();
+  Chol64<T> ch;
+  ch.load(S, SLD, n);
+  const int failed = ch.factor(n, colbuf);
+  if (failed >= 0) {
+    if (threadIdx.x == 0) record_failure(info, b, DLA_ERR_NOT_SPD, failed);
+    return;
   }
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const int i = e / n, j = e % n;
-    T v;
-    if (lower) v = j <= i ? S[i * SLD + j] : T(0);
-    else v = i <= j ? S[j * SLD + i] : T(0);
-    *a.at(b, i, j) = v;
-  }
+  ch.store(a.at(b, 0, 0), a.ld, n, lower);
 }
 
 template <typename T>

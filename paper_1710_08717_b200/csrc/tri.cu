@@ -11,13 +11,14 @@
 // Reference algorithms these replace (same results up to rounding order):
 //   trsm  dl/blas.hpp:307-395     trmm dl/blas.hpp:202-291
 //   potrf dl/cholesky.hpp:35-88   potri dl/cholesky.hpp:105-147
+#include "chol64.cuh"
 #include "common.cuh"
 
 namespace dlab {
 namespace {
 
 constexpr int NB = 64;        // leaf size
-constexpr int LEAF_VEC = 32;  // vectors per CTA in trsm/trmm leaves
+constexpr int LEAF_VEC = 32;  // vectors per CTA in the trmm leaf
 constexpr int LDS = NB + 1;   // smem row stride (conflict-free column reads)
 
 template <typename T>
@@ -45,57 +46,146 @@ __device__ void load_effective(T* S, MatB<const T> t, int64_t b, int nb, bool s_
   }
 }
 
-// Leaf trsm: solve S y = x for LEAF_VEC vectors per CTA (in place in X).
-//   left : X block is nb x nvec (rows k0.., vectors = columns)
-//   right: X block is nvec x nb (vectors = rows)
+// Blocked leaf trsm (the hot one): 64 vectors per CTA, the effective
+// triangle S re-indexed to lower form (an upper S is solved in reversed
+// order), forward substitution in 8-row blocks: each 8 x 8 diagonal block is
+// solved per vector with precomputed reciprocal pivots (as the reference's
+// left solve multiplies by 1/t_ii, dl/blas.hpp:353-354), then the rows below
+// are updated by an (rows x 8) x (8 x 64) FP64 DMMA product in shared memory.
+// alpha is applied on load; with `check` the CTA first tests the diagonal for
+// an exact zero (SINGULAR, slice left untouched, dl/blas.hpp:310-314).
+constexpr int BV = 64;  // vectors per CTA
+
 template <typename T>
-__global__ void __launch_bounds__(256) k_trsm_leaf(int nb, int64_t nvec, MatB<const T> t, MatB<T> x, bool right,
-                                                   bool s_from_tt, bool slower, const int32_t* skip) {
+__device__ __forceinline__ void mma884(T& c0, T& c1, T a, T b);
+template <>
+__device__ __forceinline__ void mma884<double>(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_trsm_leaf_blk(int nb, int64_t nvec, MatB<const T> t, MatB<T> x, bool right,
+                                                       bool s_tt, bool slower, T alpha, bool check,
+                                                       int32_t* info) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* S = reinterpret_cast<T*>(smem_raw);
-  T* V = S + NB * LDS;
-  const int64_t chunks = (nvec + LEAF_VEC - 1) / LEAF_VEC;
-  const int64_t b = blockIdx.x / chunks, v0 = (blockIdx.x % chunks) * LEAF_VEC;
-  if (slice_failed(skip, b)) return;
-  const int nv = (int)min((int64_t)LEAF_VEC, nvec - v0);
-  load_effective(S, t, b, nb, s_from_tt, slower);
-  for (int e = threadIdx.x; e < nv * nb; e += blockDim.x) {
-    int v, i;
-    if (right) { v = e / nb; i = e % nb; } else { i = e / nv; v = e % nv; }
-    V[v * LDS + i] = right ? *x.at(b, v0 + v, i) : *x.at(b, i, v0 + v);
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int v = warp; v < nv; v += nw) {
-    T* xv = V + v * LDS;
-    T r0 = lane < nb ? xv[lane] : T(0);
-    T r1 = lane + 32 < nb ? xv[lane + 32] : T(0);
-    for (int s = 0; s < nb; ++s) {
-      const int i = slower ? s : nb - 1 - s;
-      const int owner = i & 31;
-      T xi = (i < 32) ? r0 : r1;
-      xi = __shfl_sync(0xffffffffu, xi, owner) / S[i * LDS + i];
-      if (lane == owner) {
-        if (i < 32) r0 = xi; else r1 = xi;
-      }
-      // update the rows still to be solved
-      if (slower) {
-        if (lane > i && lane < nb) r0 -= S[lane * LDS + i] * xi;
-        if (lane + 32 > i && lane + 32 < nb) r1 -= S[(lane + 32) * LDS + i] * xi;
-      } else {
-        if (lane < i) r0 -= S[lane * LDS + i] * xi;
-        if (lane + 32 < i) r1 -= S[(lane + 32) * LDS + i] * xi;
+  T* S = reinterpret_cast<T*>(smem_raw);  // [64][LDS], lower form
+  T* V = S + NB * LDS;                    // [BV][LDS], vector-major
+  T* rd = V + BV * LDS;                   // [64] reciprocal pivots
+  __shared__ int zero_at;
+  const int64_t chunks = (nvec + BV - 1) / BV;
+  const int64_t b = blockIdx.x / chunks, v0 = (blockIdx.x % chunks) * BV;
+  if (slice_failed(info, b)) return;
+  const int nv = (int)min((int64_t)BV, nvec - v0);
+  const int tid = threadIdx.x;
+  // S' (lower): S'[i][j] = S[nb-1-i][nb-1-j] when S is upper; zero padded to 64.
+  // Loads are issued 8 per thread before any shared store (memory-level
+  // parallelism: the leaf is latency bound otherwise).
+  for (int e0 = tid; e0 < NB * NB; e0 += 8 * 128) {
+    T v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 128, i = e / NB, j = e % NB;
+      v[u] = T(0);
+      if (i < nb && j < nb && j <= i) {
+        const int si = slower ? i : nb - 1 - i, sj = slower ? j : nb - 1 - j;
+        v[u] = s_tt ? *t.at(b, sj, si) : *t.at(b, si, sj);
       }
     }
-    if (lane < nb) xv[lane] = r0;
-    if (lane + 32 < nb) xv[lane + 32] = r1;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 128;
+      S[(e / NB) * LDS + e % NB] = v[u];
+    }
+  }
+  for (int e0 = tid; e0 < BV * NB; e0 += 8 * 128) {
+    T val[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 128;
+      int v, i;
+      if (right) { v = e / NB; i = e % NB; } else { i = e / BV; v = e % BV; }
+      val[u] = T(0);
+      if (v < nv && i < nb) {
+        const int si = slower ? i : nb - 1 - i;
+        val[u] = alpha * (right ? *x.at(b, v0 + v, si) : *x.at(b, si, v0 + v));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 128;
+      int v, i;
+      if (right) { v = e / NB; i = e % NB; } else { i = e / BV; v = e % BV; }
+      V[v * LDS + i] = val[u];
+    }
+  }
+  if (tid == 0) zero_at = -1;
+  __syncthreads();
+  if (tid < NB) {
+    const T d = tid < nb ? S[tid * LDS + tid] : T(1);
+    rd[tid] = T(1) / d;
+    if (check && tid < nb && d == T(0)) atomicMax(&zero_at, 0);
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < nv * nb; e += blockDim.x) {
+  if (check && zero_at >= 0) {
+    if (tid == 0) {
+      int first = -1;
+      for (int k = 0; k < nb && first < 0; ++k)
+        if (*t.at(b, k, k) == T(0)) first = k;
+      record_failure(info, b, DLA_ERR_SINGULAR, first);
+    }
+    return;
+  }
+  const int warp = tid >> 5, lane = tid & 31, fr = lane >> 2, fc = lane & 3;
+  for (int c0 = 0; c0 < nb; c0 += 8) {
+    // 1) 8 x 8 diagonal block, one thread per vector
+    if (tid < nv) {
+      T* xv = V + tid * LDS;
+      for (int i = c0; i < c0 + 8 && i < nb; ++i) {
+        T acc = xv[i];
+        for (int p = c0; p < i; ++p) acc -= S[i * LDS + p] * xv[p];
+        xv[i] = acc * rd[i];
+      }
+    }
+    __syncthreads();
+    // 2) rows below: V[:, r] -= S'[r, c0:c0+8] V[:, c0:c0+8]  (DMMA, K = 8)
+    const int r0 = c0 + 8;
+    const int rtiles = (nb - r0 + 7) / 8;
+    const int ntiles = rtiles * (BV / 8);
+    if constexpr (sizeof(T) == 8) {
+      for (int tile = warp; tile < ntiles; tile += 4) {
+        const int rt = r0 + (tile / (BV / 8)) * 8, nt = (tile % (BV / 8)) * 8;
+        T acc0 = T(0), acc1 = T(0);
+#pragma unroll
+        for (int kk = 0; kk < 8; kk += 4) {
+          const T af = S[(rt + fr) * LDS + c0 + kk + fc];
+          const T bf = V[(nt + fr) * LDS + c0 + kk + fc];
+          mma884<T>(acc0, acc1, af, bf);
+        }
+        // accumulator (row fr, vectors 2fc, 2fc+1)
+        V[(nt + 2 * fc) * LDS + rt + fr] -= acc0;
+        V[(nt + 2 * fc + 1) * LDS + rt + fr] -= acc1;
+      }
+    } else {
+      for (int e = tid; e < rtiles * 8 * BV; e += blockDim.x) {
+        const int r = r0 + e / BV, v = e % BV;
+        T acc = T(0);
+#pragma unroll
+        for (int p = 0; p < 8; ++p) acc += S[r * LDS + c0 + p] * V[v * LDS + c0 + p];
+        V[v * LDS + r] -= acc;
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < BV * NB; e += blockDim.x) {
     int v, i;
-    if (right) { v = e / nb; i = e % nb; } else { i = e / nv; v = e % nv; }
-    T* dst = right ? x.at(b, v0 + v, i) : x.at(b, i, v0 + v);
-    *dst = V[v * LDS + i];
+    if (right) { v = e / NB; i = e % NB; } else { i = e / BV; v = e % BV; }
+    if (v < nv && i < nb) {
+      const int si = slower ? i : nb - 1 - i;
+      T* dst = right ? x.at(b, v0 + v, si) : x.at(b, si, v0 + v);
+      *dst = V[v * LDS + i];
+    }
   }
 }
 
@@ -135,44 +225,17 @@ __global__ void __launch_bounds__(256) k_trmm_leaf(int nb, int64_t nvec, MatB<co
 // global offset for the NOT_SPD step index (dl/cholesky.hpp:49-53).
 template <typename T>
 __global__ void __launch_bounds__(256) k_potrf_leaf(int nb, int64_t k0, MatB<T> a, int32_t* info) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* S = reinterpret_cast<T*>(smem_raw);
+  __shared__ T colbuf[2 * 66];
   const int64_t b = blockIdx.x;
   if (slice_failed(info, b)) return;
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-    const int i = e / nb, j = e % nb;
-    if (j <= i) S[i * LDS + j] = *a.at(b, i, j);
-  }
-  __syncthreads();
-  int failed = -1;
-  for (int j = 0; j < nb; ++j) {
-    const T d = S[j * LDS + j];
-    if (!(d > T(0))) {
-      failed = j;
-      break;
-    }
-    const T r = Num<T>::sqrt_(d);
-    const T inv = T(1) / r;
-    __syncthreads();  // everyone has read d
-    if (threadIdx.x == 0) S[j * LDS + j] = r;
-    for (int i = j + 1 + threadIdx.x; i < nb; i += blockDim.x) S[i * LDS + j] *= inv;
-    __syncthreads();
-    // trailing update of the lower triangle
-    const int m = nb - j - 1;
-    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-      const int ii = j + 1 + e / m, jj = j + 1 + e % m;
-      if (jj <= ii) S[ii * LDS + jj] -= S[ii * LDS + j] * S[jj * LDS + j];
-    }
-    __syncthreads();
-  }
+  Chol64<T> ch;
+  ch.load(a.at(b, 0, 0), a.ld, nb);
+  const int failed = ch.factor(nb, colbuf);
   if (failed >= 0) {
     if (threadIdx.x == 0) record_failure(info, b, DLA_ERR_NOT_SPD, k0 + failed);
     return;
   }
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-    const int i = e / nb, j = e % nb;
-    *a.at(b, i, j) = j <= i ? S[i * LDS + j] : T(0);
-  }
+  ch.store(a.at(b, 0, 0), a.ld, nb, true);
 }
 
 // Leaf lower-triangular inverse (in place): column j of W^{-1} solves
@@ -240,22 +303,22 @@ size_t leaf_smem(int vecs) {
 // the other extent nother).  Assumes alpha already applied.
 template <typename T>
 dla_status trsm_core(const Ctx& c, int64_t batch, int64_t nt, int64_t nother, MatB<const T> t, MatB<T> x,
-                     bool right, bool trans, bool lower) {
+                     bool right, bool trans, bool lower, T alpha = T(1), bool check = false) {
   const bool op_lower = (lower != trans);
   if (nt <= NB) {
     // left: S = op(T); right: S = op(T)^T.  S(i,j) = T(j,i) when
     // (left && trans) || (right && !trans).
     const bool s_tt = right ? !trans : trans;
     const bool slower = right ? !op_lower : op_lower;
-    const int64_t chunks = (nother + LEAF_VEC - 1) / LEAF_VEC;
-    const size_t sm = leaf_smem<T>(LEAF_VEC);
+    const int64_t chunks = (nother + BV - 1) / BV;
+    const size_t sm = sizeof(T) * (size_t)(NB * LDS + BV * LDS + NB);
     static bool once = false;
     if (!once) {
-      set_smem(k_trsm_leaf<T>, sm);
+      set_smem(k_trsm_leaf_blk<T>, sm);
       once = true;
     }
-    k_trsm_leaf<T><<<(unsigned)(batch * chunks), 256, sm, c.stream>>>((int)nt, nother, t, x, right, s_tt, slower,
-                                                                       c.info);
+    k_trsm_leaf_blk<T><<<(unsigned)(batch * chunks), 128, sm, c.stream>>>((int)nt, nother, t, x, right, s_tt, slower,
+                                                                          alpha, check, c.info);
     DLAB_LAUNCH_CHECK();
     return DLA_OK;
   }
@@ -351,7 +414,8 @@ template <typename T>
 dla_status potrf_rec(const Ctx& c, int64_t batch, int64_t n, int64_t k0, MatB<T> a) {
   if (n <= NB) {
     const size_t sm = sizeof(T) * NB * LDS;
-    k_potrf_leaf<T><<<(unsigned)batch, 256, sm, c.stream>>>((int)n, k0, a, c.info);
+    (void)sm;
+    k_potrf_leaf<T><<<(unsigned)batch, 256, 0, c.stream>>>((int)n, k0, a, c.info);
     DLAB_LAUNCH_CHECK();
     return DLA_OK;
   }
@@ -411,11 +475,14 @@ dla_status lauum_rec(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
 
 template <typename T>
 dla_status trsm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x, bool right,
-                bool trans, bool lower, T alpha) {
+                bool trans, bool lower, T alpha, bool check_diag) {
   if (batch == 0 || m == 0 || n == 0) return DLA_OK;
+  const int64_t nt = right ? n : m, no = right ? m : n;
+  if (nt <= NB)  // one leaf: alpha and the zero-diagonal test fused into it
+    return trsm_core<T>(c, batch, nt, no, t, x, right, trans, lower, alpha, check_diag && c.info);
+  if (check_diag) DLAB_TRY(check_zero_diag<T>(c, batch, nt, t, c.info));
   DLAB_TRY(ew_scale<T>(c, batch, m, n, x, alpha, c.info));
-  return right ? trsm_core<T>(c, batch, n, m, t, x, right, trans, lower)
-               : trsm_core<T>(c, batch, m, n, t, x, right, trans, lower);
+  return trsm_core<T>(c, batch, nt, no, t, x, right, trans, lower);
 }
 
 template <typename T>
@@ -455,7 +522,7 @@ dla_status potri_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
 
 #define INST(T)                                                                                             \
   template dla_status trsm<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<const T>, MatB<T>, bool, bool, bool, \
-                              T);                                                                           \
+                              T, bool);                                                                     \
   template dla_status trmm<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<const T>, MatB<T>, bool, bool, bool, \
                               T);                                                                           \
   template dla_status potrf_lower<T>(const Ctx&, int64_t, int64_t, MatB<T>);                                \

@@ -1,0 +1,85 @@
+"""CPU-side checks of the C-ABI boundary (no GPU needed).
+
+* libdla_b200.so loads and exports every symbol include/dla.h declares;
+* the header and the Python binding agree on the entry-point list;
+* status strings / workspace queries answer without a device (host-only
+  entry points);
+* the Python operator layer refuses CPU tensors (there is no CPU fallback).
+"""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "dla.h")
+LIB = os.path.join(ROOT, "paper_1710_08717_b200", "libdla_b200.so")
+
+
+def header_symbols():
+    src = open(HEADER).read()
+    names = set(re.findall(r"\b(dla_[a-z0-9_]+)\s*\(", src))
+    # expand the DLA_DECLARE_OPS(T, S) prototype list for f32 / f64
+    macro = re.search(r"#define DLA_DECLARE_OPS\(T, S\)(.*?)\n\n", src, re.S).group(1)
+    for base in re.findall(r"dla_([a-z0-9_]+)_##S\s*\(", macro):
+        names.add(f"dla_{base}_f32")
+        names.add(f"dla_{base}_f64")
+    return {n for n in names if not n.endswith("_")}
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(LIB):
+        import __graft_entry__
+        __graft_entry__.build()
+    return C.CDLL(LIB)
+
+
+def test_every_declared_symbol_is_exported(lib):
+    syms = header_symbols()
+    assert len(syms) >= 44, sorted(syms)
+    missing = [s for s in sorted(syms) if not hasattr(lib, s)]
+    assert not missing, f"declared in include/dla.h but not exported: {missing}"
+
+
+def test_binding_matches_header():
+    from paper_1710_08717_b200 import _lib
+    assert set(_lib.exported_symbols()) <= header_symbols()
+    assert header_symbols() <= set(_lib.exported_symbols())
+
+
+def test_host_only_entry_points(lib):
+    lib.dla_status_string.restype = C.c_char_p
+    assert lib.dla_status_string(2) == b"matrix is not positive definite"
+    lib.dla_version.restype = C.c_char_p
+    assert b"sm_100a" in lib.dla_version()
+    lib.dla_workspace_bytes.restype = C.c_size_t
+    lib.dla_workspace_bytes.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int]
+    # gelqf: m reals per slice forward (tau), m*m backward (dl/adjoints.hpp:1-9)
+    assert lib.dla_workspace_bytes(8, 1, 256, 128, 512, 0, 0) == 256 * 128 * 8
+    assert lib.dla_workspace_bytes(8, 0, 256, 128, 512, 0, 1) == 256 * 128 * 128 * 4
+    assert lib.dla_workspace_bytes(9, 1, 1024, 64, 64, 0, 1) == 1024 * 64 * 64 * 8
+    assert lib.dla_workspace_bytes(5, 1, 1, 64, 64, 0, 0) == 0
+
+
+def test_shape_and_alias_errors_are_host_side(lib):
+    """Validation runs before any launch, so it answers without a GPU."""
+    f = lib.dla_gemm2_fwd_f64
+    f.restype = C.c_int
+    f.argtypes = [C.c_int64] * 4 + [C.c_void_p] * 3 + [C.c_int, C.c_int, C.c_double, C.c_void_p]
+    buf = C.create_string_buffer(1024)
+    p = C.cast(buf, C.c_void_p)
+    assert f(1, 3, 3, 3, p, p, p, 0, 0, 1.0, None) == 5          # DLA_ERR_ALIAS
+    assert f(-1, 3, 3, 3, None, None, None, 0, 0, 1.0, None) == 1  # DLA_ERR_SHAPE
+    g = lib.dla_gelqf_fwd_f64
+    g.restype = C.c_int
+    g.argtypes = [C.c_int64] * 3 + [C.c_void_p] * 4 + [C.c_size_t, C.c_void_p]
+    assert g(1, 3, 2, None, None, None, None, 0, None) == 1        # m > n: ShapeError
+
+
+def test_python_layer_has_no_cpu_path():
+    torch = pytest.importorskip("torch")
+    from paper_1710_08717_b200 import linalg as L
+    with pytest.raises(L.Error):
+        L.potrf(torch.eye(3, dtype=torch.float64))

@@ -1,0 +1,165 @@
+"""Secondary bench lines (bench.py --config c1|potrf1024|c3|c4|c5).
+
+Same JSON contract as the headline line; each config is BASELINE.json's
+configs[i] (SURVEY §8d gives the synthetic inputs and the algorithmic work
+per unit).  CPU baselines run the reference (oracle/_ref) on this host.
+"""
+from __future__ import annotations
+
+import math
+import os
+import time
+
+import numpy as np
+
+
+def _cpu_threads():
+    return os.cpu_count() or 1
+
+
+def _line(args, world, metric, value, unit, ms, workload, dtype="f64", **extra):
+    d = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+         "vs_baseline": None, "dtype": dtype, "data": "synthetic (Philox N(0,1) based)",
+         "config": {"workload": workload}}
+    d.update(extra)
+    return d
+
+
+def run(torch, args, rank, world, lib, fp64_peak, hbm):
+    import bench
+    from oracle import oracle as O
+    from paper_1710_08717_b200 import linalg as L
+    from paper_1710_08717_b200.shard import shard_range
+
+    cfg = args.config
+    ref = O.ref() if O.ref_available() else None
+    if cfg == "c1":
+        B, n = 64, 32
+        step, (a0, y0, _, _) = bench.c1_chain_fns(torch, B, n)
+        c0 = lib.dla_launch_count()
+        step()
+        torch.cuda.synchronize()
+        launches = lib.dla_launch_count() - c0
+        ms = bench.timed(torch, bench.graphed(torch, step), args.steps, args.warmup, world)
+        flops = n ** 3 / 3 + 4 * n ** 3 / 3 + 4 * n * n
+        cpu = None
+        if ref is not None and rank == 0:
+            a = a0.cpu().numpy()
+            y = y0.cpu().numpy()
+            reps, secs = 0, 0.0
+            while secs < 2.0:
+                secs += ref.c1_chain(a, y, 1)[0]
+                reps += 1
+            cpu = {"value": reps * B / secs, "unit": "matrices/s", "cores": 1, "kind": "reference",
+                   "sample": f"{reps} x reference C1 chain over batch {B} (for_each_slice, 1 thread)"}
+        v = world * B / (ms / 1e3)
+        return _line(args, world, "C1 chain matrices/s", v, "matrices/s", ms,
+                     "C1: batch 64 x 32^2 fp64 potrf fwd+bwd + trsm + sumlogdiag (fused small-n kernels)",
+                     gflops=v * flops / 1e9, gpu_launches=launches * args.steps, cpu_baseline=cpu,
+                     roofline={"bound": "latency", "note": "64 x 8 KiB = 512 KiB per step: launch/latency bound"})
+    if cfg == "potrf1024":
+        B, n = 8, 1024
+        ms = bench.run_potrf_batch(torch, n, B, args.steps, args.warmup, world)
+        flops = B * 5 * n ** 3 / 3
+        tf = world * flops / (ms / 1e3) / 1e12
+        cpu = None
+        if ref is not None and rank == 0:
+            r = O.rng(11)
+            a = O.random_spd(n, r, batch=B)
+            lb = np.tril(r.standard_normal((B, n, n)))
+            secs, _ = ref.potrf_fwdbwd_batch(a, lb, min(B, _cpu_threads()))
+            cpu = {"value": B / secs, "unit": "matrices/s", "cores": min(B, _cpu_threads()), "kind": "reference",
+                   "sample": f"reference potrf+potrf_backward over batch {B} x {n}^2, for_each_slice"}
+        return _line(args, world, "potrf fwd+bwd matrices/s (n=1024)", world * B / (ms / 1e3), "matrices/s", ms,
+                     "north star: potrf fwd+bwd, batch 8 x 1024^2 fp64", step_tflops=tf,
+                     roofline={"bound": "tensor", "achieved": tf, "peak": fp64_peak, "unit": "TFLOP/s",
+                               "frac": tf / fp64_peak, "traffic": None}, cpu_baseline=cpu)
+    if cfg == "c3":
+        res = []
+        for dt in (torch.float64, torch.float32):
+            B, m, n = 256, 128, 512
+            r = O.rng(5)
+            x = r.standard_normal((B, m, n - m))
+            a0 = torch.from_numpy(np.concatenate([np.broadcast_to(np.eye(m), (B, m, m)), x], axis=2)).to(dt).cuda()
+            qb = torch.from_numpy(r.standard_normal((B, m, n))).to(dt).cuda()
+            lb = torch.from_numpy(np.tril(r.standard_normal((B, m, m)))).to(dt).cuda()
+            q = torch.empty_like(a0)
+            l = torch.empty(B, m, m, dtype=dt, device="cuda")
+            ab = torch.empty_like(a0)
+
+            def step():
+                q.copy_(a0)
+                L.gelqf_inplace(q, l, check=False)
+                L.gelqf_backward_into(ab, qb, lb, q, l)
+
+            ms = bench.timed(torch, step, args.steps, args.warmup, world)
+            flops = B * (4 * m * m * n - 4 * m ** 3 / 3 + m ** 3 / 3 + 5 * m * m * n)
+            res.append({"dtype": str(dt).split(".")[-1], "matrices_per_s": world * B / (ms / 1e3), "ms": ms,
+                        "tflops": flops / (ms / 1e3) / 1e12})
+        cpu = None
+        if ref is not None and rank == 0:
+            r = O.rng(5)
+            Bc = 32
+            x = r.standard_normal((Bc, m, n - m))
+            a = np.concatenate([np.broadcast_to(np.eye(m), (Bc, m, m)), x], axis=2)
+            secs, _ = ref.gelqf_fwdbwd_batch(a, r.standard_normal((Bc, m, n)),
+                                             np.tril(r.standard_normal((Bc, m, m))), _cpu_threads())
+            cpu = {"value": Bc / secs, "unit": "matrices/s", "cores": _cpu_threads(), "kind": "reference",
+                   "sample": f"reference gelqf+backward over {Bc} of the 256 matrices (fp64, for_each_slice)"}
+        return _line(args, world, "gelqf fwd+bwd matrices/s (128x512)", res[0]["matrices_per_s"], "matrices/s",
+                     res[0]["ms"], "C3: BLR gelqf fwd+bwd, batch 256 of B=[I_128, X] in R^{128x512} (the reference "
+                     "rejects 512x128, dl/lq.hpp:26-29)", per_dtype=res, cpu_baseline=cpu)
+    if cfg == "c4":
+        B, n = 1024, 64
+        r = O.rng(4)
+        a0 = torch.from_numpy(O.random_sym(n, r, batch=B)).cuda()
+        ub = torch.from_numpy(r.standard_normal((B, n, n))).cuda()
+        lb = torch.from_numpy(r.standard_normal((B, n))).cuda()
+        u = torch.empty_like(a0)
+        lam = torch.empty(B, n, dtype=torch.float64, device="cuda")
+        ab = torch.empty_like(a0)
+
+        def step():
+            u.copy_(a0)
+            L.syevd_inplace(u, lam, check=False)
+            L.syevd_backward_into(ab, ub, lb, u, lam)
+
+        ms = bench.timed(torch, step, args.steps, args.warmup, world)
+        flops = B * (10 * n ** 3 / 3 + 6 * n ** 3)
+        cpu = None
+        if ref is not None and rank == 0:
+            Bc = 256
+            secs, _ = ref.syevd_fwdbwd_batch(a0[:Bc].cpu().numpy(), ub[:Bc].cpu().numpy(), lb[:Bc].cpu().numpy(),
+                                             _cpu_threads())
+            cpu = {"value": Bc / secs, "unit": "matrices/s", "cores": _cpu_threads(), "kind": "reference",
+                   "sample": f"reference syevd+backward over {Bc} of the 1024 matrices, for_each_slice"}
+        v = world * B / (ms / 1e3)
+        return _line(args, world, "syevd fwd+bwd matrices/s (64x64)", v, "matrices/s", ms,
+                     "C4: batched syevd fwd+bwd, batch 1024 x 64^2 fp64 (Jacobi, smem-resident)",
+                     gflops=v * flops / B / 1e9, cpu_baseline=cpu)
+    if cfg == "c5":
+        from paper_1710_08717_b200.c5 import MarginalLikelihoods
+        total, n = 65536, 128
+        lo, hi = shard_range(total, rank, world)
+        B = hi - lo
+        r = O.rng(55)
+        s = torch.empty(B, n, n, dtype=torch.float64, device="cuda")
+        chunk = 4096
+        for c0 in range(0, B, chunk):  # per-rank slice of the global synthetic batch
+            cb = min(chunk, B - c0)
+            x = torch.randn(cb, n, n, dtype=torch.float64, device="cuda",
+                            generator=torch.Generator("cuda").manual_seed(lo + c0))
+            s[c0:c0 + cb] = x @ x.transpose(-1, -2) + n * torch.eye(n, dtype=torch.float64, device="cuda")
+        y = torch.randn(B, n, 1, dtype=torch.float64, device="cuda")
+        m = MarginalLikelihoods(B, n)
+        theta = math.log(0.3)
+        ms = bench.timed(torch, lambda: m.step_allreduce(s, y, theta), args.steps, args.warmup, world)
+        m.check()
+        flops = total * 8.33 * n ** 3
+        return _line(args, world, "C5 GP marginal likelihoods items/s", total / (ms / 1e3), "items/s", ms,
+                     "C5: 65536 x 128^2 GP marginal likelihoods (potrf+potri+trmm fwd+bwd), batch sharded over "
+                     f"{world} GPU(s), NCCL all-reduce of (loss, dloss/dtheta)",
+                     step_tflops=flops / (ms / 1e3) / 1e12, loss_grad=m.out.cpu().tolist(),
+                     config_parallelism=f"dp{world} (contiguous batch shards)")
+    raise ValueError(cfg)
