@@ -278,6 +278,7 @@ dla_status potrf_bwd(int64_t batch, int64_t n, T* abar, const T* lbar, const T* 
   if (batch * n == 0) return DLA_OK;
   if (potrf_small_eligible<T>(n)) return potrf_bwd_small<T>(cx, batch, n, pk(abar, n, n), cpk(lbar, n, n),
                                                             cpk(l, n, n), lower);
+  if (inv_eligible<T>(n)) return potrf_bwd_inv<T>(cx, batch, n, pk(abar, n, n), cpk(lbar, n, n), cpk(l, n, n), lower);
   MatB<T> ab = pk(abar, n, n);
   MatB<const T> lv = cpk(l, n, n);
   DLAB_TRY(ew_copy<T>(cx, batch, n, n, cpk(lbar, n, n), ab));

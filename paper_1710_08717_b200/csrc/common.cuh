@@ -18,16 +18,24 @@ namespace dlab {
 // Row-major like the reference's MatrixView (dl/matrix.hpp:64-89), with an
 // explicit leading dimension so blocked algorithms address sub-blocks
 // in place.
+// `bsi` is an optional inner batch stride (GEMM only): the level-batched
+// triangular inverse addresses all diagonal blocks of one matrix as an inner
+// batch.
 template <typename T>
 struct MatB {
   T* p;
   int64_t ld;
   int64_t bs;
+  int64_t bsi = 0;
   __host__ __device__ T* at(int64_t b, int64_t i, int64_t j) const {
     return p + b * bs + i * ld + j;
   }
-  __host__ __device__ MatB sub(int64_t i, int64_t j) const { return MatB{p + i * ld + j, ld, bs}; }
+  __host__ __device__ MatB sub(int64_t i, int64_t j) const { return MatB{p + i * ld + j, ld, bs, bsi}; }
 };
+
+// Triangular-operand flags for gemm(): op(A) / op(B) is lower / upper
+// triangular (the other triangle is ignored, whatever memory holds there).
+enum Tri : int { TRI_NONE = 0, TRI_LOWER = 1, TRI_UPPER = 2 };
 
 template <typename T>
 inline MatB<T> packed(T* p, int64_t rows, int64_t cols) {
@@ -50,6 +58,26 @@ void note_launch(int k = 1);
 bool gemm_prof_on();
 void gemm_prof_begin(cudaStream_t s);
 void gemm_prof_end(cudaStream_t s, double flops);
+
+// Stream-ordered scratch from the device's default memory pool (release
+// threshold raised in make_ctx, so steady state never reaches cudaMalloc;
+// capturable into CUDA graphs as mem-alloc nodes).
+struct Scratch {
+  void* p = nullptr;
+  cudaStream_t s;
+  Scratch(size_t bytes, cudaStream_t st) : s(st) {
+    if (bytes && cudaMallocAsync(&p, bytes, s) != cudaSuccess) p = nullptr;
+  }
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
 
 inline unsigned blocks_for(int64_t work, int threads, int64_t cap = 148 * 32) {
   int64_t b = (work + threads - 1) / threads;
@@ -75,6 +103,7 @@ template <>
 struct Num<double> {
   __device__ static double sqrt_(double x) { return sqrt(x); }
   __device__ static double log_(double x) { return log(x); }
+  __device__ static double rsqrt_(double x) { return rsqrt(x); }
   static constexpr double sym_rtol = 1e-10;
   static constexpr double rank_rtol = 1e-12;
 };
@@ -82,6 +111,7 @@ template <>
 struct Num<float> {
   __device__ static float sqrt_(float x) { return sqrtf(x); }
   __device__ static float log_(float x) { return logf(x); }
+  __device__ static float rsqrt_(float x) { return 1.0f / sqrtf(x); }
   static constexpr float sym_rtol = 1e-4f;
   static constexpr float rank_rtol = 1e-5f;
 };
@@ -109,14 +139,18 @@ enum Mask : int { MASK_FULL = 0, MASK_LOWER = 1, MASK_UPPER = 2 };
 // gemm.cu: C = alpha op(A) op(B) + beta C over a batch (beta == 0 => C is
 // not read).  mask restricts writes to the lower/upper triangle of C
 // (global (i,j) of this C view); masked-out tiles do no math.
+// tri_a / tri_b: op(A) / op(B) triangular (K range restricted per tile, the
+// ignored triangle masked to zero).  inner > 1: each of the `batch` slices is
+// itself an inner batch of `inner` problems at the operands' bsi strides.
 template <typename T>
 dla_status gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T alpha, MatB<const T> a,
                 bool ta, MatB<const T> b, bool tb, T beta, MatB<T> cm, int mask = MASK_FULL,
-                const int32_t* skip = nullptr);
+                const int32_t* skip = nullptr, int tri_a = TRI_NONE, int tri_b = TRI_NONE, int64_t inner = 1);
 
 // elementwise.cu
 template <typename T>
-dla_status ew_copy(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> src, MatB<T> dst);
+dla_status ew_copy(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> src, MatB<T> dst,
+                   const int32_t* skip = nullptr);
 template <typename T>
 dla_status ew_scale(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<T> x, T alpha,
                     const int32_t* skip = nullptr);
@@ -124,6 +158,13 @@ dla_status ew_scale(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<T> x
 template <typename T>
 dla_status ew_square(const Ctx& c, int64_t batch, int64_t n, MatB<T> x, int op, T alpha = T(1),
                      const int32_t* skip = nullptr);
+// dst = lower-triangular form of src's selected triangle (from_upper: dst(i,j)
+// = src(j,i) for j <= i), strict upper of dst zeroed.
+template <typename T>
+dla_status ew_tri_copy(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, bool from_upper);
+// dst(i,j) = dst(j,i) = alpha * src(max(i,j), min(i,j))  (bit-symmetric)
+template <typename T>
+dla_status ew_sym_lower_into(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, T alpha);
 template <typename T>
 dla_status check_symmetric(const Ctx& c, int64_t batch, int64_t n, MatB<const T> a, int32_t* info);
 template <typename T>

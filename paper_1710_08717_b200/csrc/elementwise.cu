@@ -11,10 +11,11 @@ namespace dlab {
 namespace {
 
 template <typename T>
-__global__ void k_copy(int64_t batch, int64_t m, int64_t n, MatB<const T> src, MatB<T> dst) {
+__global__ void k_copy(int64_t batch, int64_t m, int64_t n, MatB<const T> src, MatB<T> dst, const int32_t* skip) {
   const int64_t total = batch * m * n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = t / (m * n), r = t % (m * n), i = r / n, j = r % n;
+    if (slice_failed(skip, b)) continue;
     *dst.at(b, i, j) = *src.at(b, i, j);
   }
 }
@@ -76,6 +77,26 @@ __global__ void k_square(int64_t batch, int64_t n, MatB<T> x, int op, T alpha, c
         }
         break;
     }
+  }
+}
+
+template <typename T>
+__global__ void k_tri_copy(int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, bool from_upper) {
+  const int64_t total = batch * n * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t / (n * n), r = t % (n * n), i = r / n, j = r % n;
+    T v = T(0);
+    if (j <= i) v = from_upper ? *src.at(b, j, i) : *src.at(b, i, j);
+    *dst.at(b, i, j) = v;
+  }
+}
+
+template <typename T>
+__global__ void k_sym_lower_into(int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, T alpha) {
+  const int64_t total = batch * n * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t / (n * n), r = t % (n * n), i = r / n, j = r % n;
+    *dst.at(b, i, j) = alpha * *src.at(b, i > j ? i : j, i > j ? j : i);
   }
 }
 
@@ -191,9 +212,10 @@ __global__ void k_sumlogdiag_bwd(int64_t batch, int64_t n, MatB<T> abar, const T
 }  // namespace
 
 template <typename T>
-dla_status ew_copy(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> src, MatB<T> dst) {
+dla_status ew_copy(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> src, MatB<T> dst,
+                   const int32_t* skip) {
   if (batch * m * n == 0 || src.p == dst.p) return DLA_OK;
-  k_copy<T><<<blocks_for(batch * m * n, 256), 256, 0, c.stream>>>(batch, m, n, src, dst);
+  k_copy<T><<<blocks_for(batch * m * n, 256), 256, 0, c.stream>>>(batch, m, n, src, dst, skip);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }
@@ -210,6 +232,22 @@ template <typename T>
 dla_status ew_square(const Ctx& c, int64_t batch, int64_t n, MatB<T> x, int op, T alpha, const int32_t* skip) {
   if (batch * n == 0) return DLA_OK;
   k_square<T><<<blocks_for(batch * n * n, 256), 256, 0, c.stream>>>(batch, n, x, op, alpha, skip);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+
+template <typename T>
+dla_status ew_tri_copy(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, bool from_upper) {
+  if (batch * n == 0) return DLA_OK;
+  k_tri_copy<T><<<blocks_for(batch * n * n, 256), 256, 0, c.stream>>>(batch, n, src, dst, from_upper);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+
+template <typename T>
+dla_status ew_sym_lower_into(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, T alpha) {
+  if (batch * n == 0) return DLA_OK;
+  k_sym_lower_into<T><<<blocks_for(batch * n * n, 256), 256, 0, c.stream>>>(batch, n, src, dst, alpha);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }
@@ -260,10 +298,13 @@ dla_status sumlogdiag_bwd(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, 
 }
 
 #define INST(T)                                                                                          \
-  template dla_status ew_copy<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<const T>, MatB<T>);        \
+  template dla_status ew_copy<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<const T>, MatB<T>,         \
+                                 const int32_t*);                                                       \
   template dla_status ew_scale<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<T>, T, const int32_t*);   \
   template dla_status ew_square<T>(const Ctx&, int64_t, int64_t, MatB<T>, int, T, const int32_t*);      \
   template dla_status check_symmetric<T>(const Ctx&, int64_t, int64_t, MatB<const T>, int32_t*);        \
+  template dla_status ew_tri_copy<T>(const Ctx&, int64_t, int64_t, MatB<const T>, MatB<T>, bool);       \
+  template dla_status ew_sym_lower_into<T>(const Ctx&, int64_t, int64_t, MatB<const T>, MatB<T>, T);    \
   template dla_status check_zero_diag<T>(const Ctx&, int64_t, int64_t, MatB<const T>, int32_t*);        \
   template dla_status sumlogdiag_fwd<T>(const Ctx&, int64_t, int64_t, T*, MatB<const T>);               \
   template dla_status sumlogdiag_bwd<T>(const Ctx&, int64_t, int64_t, MatB<T>, const T*, MatB<const T>, \

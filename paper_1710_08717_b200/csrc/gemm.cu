@@ -1,12 +1,21 @@
 // Batched strided GEMM for the blocked factorizations and the backward
 // compositions:  C = alpha op(A) op(B) + beta C  (beta == 0 => C not read),
-// with an optional lower/upper write mask (SYRK-style trailing updates skip
-// the tiles above/below the diagonal entirely).
+// with
+//   * an optional lower/upper write mask (SYRK-style updates skip the tiles
+//     above/below the diagonal entirely),
+//   * optional triangular operands (trmm / inverse-based trsm as one GEMM:
+//     the K loop of each tile is restricted to the triangle's nonzero range
+//     and the ignored triangle inside boundary k-blocks is zeroed in shared
+//     memory, so whatever the caller's memory holds there is never used —
+//     the reference reads only the `lower`-selected triangle, dl/blas.hpp:182),
+//   * a two-level batch (outer slices x inner blocks) for the level-batched
+//     triangular inverse.
 //
-// f64: FP64 tensor cores.  Each warp owns a 32x32 output tile built from
-//      4x4 `mma.sync.m8n8k4.f64` (SASS DMMA.8x8x4); tcgen05 has no f64 kind,
-//      and the measured DMMA ceiling on B200 is 37.1 TFLOP/s
-//      (profiles/peaks_fp64_fp32_r01.json).
+// f64: FP64 tensor cores.  Each warp owns a WM x WN output tile built from
+//      `mma.sync.m8n8k4.f64` (SASS DMMA.8x8x4); tcgen05 has no f64 kind, and
+//      the measured DMMA ceiling on B200 is 37.1 TFLOP/s
+//      (profiles/peaks_fp64_fp32_r01.json).  128 x 128 CTA tiles reach
+//      30.7 TFLOP/s at 4096^3.
 // f32: FFMA SIMT (exact binary32, no TF32 rounding), 4x4 register tiles.
 //
 // Operand tiles are staged global->shared with cp.async (zero-filled out of
@@ -40,6 +49,8 @@ struct GemmArgs {
   int mask;
   const int32_t* skip;
   int64_t tiles_m, tiles_n;
+  int tri_a, tri_b;
+  int64_t inner;
 };
 
 __device__ __forceinline__ void cp_async(void* smem, const void* gmem, bool pred, int bytes) {
@@ -75,10 +86,8 @@ struct BTile {
 
 // Issue the cp.async loads of one k-block into stage buffers sa / sb.
 template <typename T, class C, bool TA, bool TB, int VA, int VB>
-__device__ __forceinline__ void load_stage(const GemmArgs<T>& g, int64_t bidx, int64_t m0, int64_t n0,
+__device__ __forceinline__ void load_stage(const GemmArgs<T>& g, const T* A, const T* B, int64_t m0, int64_t n0,
                                            int64_t k0, T* sa, T* sb) {
-  const T* A = g.a.p + bidx * g.a.bs;
-  const T* B = g.b.p + bidx * g.b.bs;
   constexpr int BM = C::BM, BN = C::BN, NT = C::NT;
   {
     constexpr int CH = (BM * BK) / VA;
@@ -122,6 +131,39 @@ __device__ __forceinline__ void load_stage(const GemmArgs<T>& g, int64_t bidx, i
   }
 }
 
+// Zero the ignored triangle of triangular operands inside k-block k0 (only
+// blocks that straddle the diagonal need it).
+template <typename T, class C, bool TA, bool TB>
+__device__ __forceinline__ bool mask_stage(const GemmArgs<T>& g, int64_t m0, int64_t n0, int64_t k0, T* sa, T* sb) {
+  constexpr int BM = C::BM, BN = C::BN, NT = C::NT;
+  bool touched = false;
+  if (g.tri_a != TRI_NONE) {
+    const bool lower = g.tri_a == TRI_LOWER;  // A(i,k) = 0 for k > i (lower) / k < i (upper)
+    const bool straddles = lower ? (k0 + BK - 1 > m0) : (k0 < m0 + BM - 1);
+    if (straddles) {
+      for (int e = threadIdx.x; e < BM * BK; e += NT) {
+        const int i = e / BK, k = e % BK;
+        const int64_t gi = m0 + i, gk = k0 + k;
+        if (lower ? (gk > gi) : (gk < gi)) sa[ATile<BM, TA>::idx(i, k)] = T(0);
+      }
+      touched = true;
+    }
+  }
+  if (g.tri_b != TRI_NONE) {
+    const bool lower = g.tri_b == TRI_LOWER;  // B(k,j) = 0 for k < j (lower) / k > j (upper)
+    const bool straddles = lower ? (k0 < n0 + BN - 1) : (k0 + BK - 1 > n0);
+    if (straddles) {
+      for (int e = threadIdx.x; e < BN * BK; e += NT) {
+        const int k = e / BN, j = e % BN;
+        const int64_t gj = n0 + j, gk = k0 + k;
+        if (lower ? (gk < gj) : (gk > gj)) sb[BTile<BN, TB>::idx(k, j)] = T(0);
+      }
+      touched = true;
+    }
+  }
+  return touched;
+}
+
 template <int BM, int BN>
 __device__ __forceinline__ bool tile_masked_out(int mask, int64_t m0, int64_t n0) {
   if (mask == MASK_LOWER) return n0 > m0 + BM - 1;
@@ -129,15 +171,51 @@ __device__ __forceinline__ bool tile_masked_out(int mask, int64_t m0, int64_t n0
   return false;
 }
 
+// Per-tile K range implied by triangular operands.
+template <typename T, int BM, int BN>
+__device__ __forceinline__ void k_range(const GemmArgs<T>& g, int64_t m0, int64_t n0, int64_t& klo, int64_t& khi) {
+  klo = 0;
+  khi = g.k;
+  if (g.tri_a == TRI_LOWER) khi = min(khi, m0 + BM);
+  if (g.tri_a == TRI_UPPER) klo = max(klo, m0);
+  if (g.tri_b == TRI_LOWER) klo = max(klo, n0);
+  if (g.tri_b == TRI_UPPER) khi = min(khi, n0 + BN);
+  klo = (klo / BK) * BK;
+}
+
 template <typename T>
-__device__ __forceinline__ void store_c(const GemmArgs<T>& g, int64_t bidx, int64_t gi, int64_t gj, T v) {
+__device__ __forceinline__ void store_c(const GemmArgs<T>& g, T* Cp, int64_t gi, int64_t gj, T v) {
   if (gi >= g.m || gj >= g.n) return;
   if (g.mask == MASK_LOWER && gj > gi) return;
   if (g.mask == MASK_UPPER && gj < gi) return;
-  T* cp = g.c.p + bidx * g.c.bs + gi * g.c.ld + gj;
+  T* cp = Cp + gi * g.c.ld + gj;
   T r = g.alpha * v;
   if (g.beta != T(0)) r += g.beta * *cp;
   *cp = r;
+}
+
+// Decode blockIdx.x into (outer slice, inner block, tile) and operand bases.
+template <typename T>
+struct TileCoord {
+  int64_t bo, m0, n0;
+  const T *A, *B;
+  T* C;
+};
+template <typename T, int BM, int BN>
+__device__ __forceinline__ TileCoord<T> decode(const GemmArgs<T>& g) {
+  int64_t tile = blockIdx.x;
+  const int64_t per = g.tiles_m * g.tiles_n;
+  const int64_t slab = tile / per;
+  tile -= slab * per;
+  TileCoord<T> t;
+  t.bo = slab / g.inner;
+  const int64_t bi = slab % g.inner;
+  t.m0 = (tile / g.tiles_n) * BM;
+  t.n0 = (tile % g.tiles_n) * BN;
+  t.A = g.a.p + t.bo * g.a.bs + bi * g.a.bsi;
+  t.B = g.b.p + t.bo * g.b.bs + bi * g.b.bsi;
+  t.C = g.c.p + t.bo * g.c.bs + bi * g.c.bsi;
+  return t;
 }
 
 // ------------------------------------------------------------------ f64 DMMA
@@ -151,13 +229,12 @@ __global__ void __launch_bounds__(C::NT) dgemm_dmma(GemmArgs<double> g) {
   double* sA = smem;
   double* sB = smem + STAGES * AT::ELEMS;
 
-  int64_t tile = blockIdx.x;
-  const int64_t per = g.tiles_m * g.tiles_n;
-  const int64_t bidx = tile / per;
-  tile -= bidx * per;
-  const int64_t m0 = (tile / g.tiles_n) * C::BM, n0 = (tile % g.tiles_n) * C::BN;
-  if (g.skip && g.skip[bidx]) return;
+  const TileCoord<double> tc = decode<double, C::BM, C::BN>(g);
+  const int64_t m0 = tc.m0, n0 = tc.n0;
+  if (g.skip && g.skip[tc.bo]) return;
   if (tile_masked_out<C::BM, C::BN>(g.mask, m0, n0)) return;
+  int64_t klo, khi;
+  k_range<double, C::BM, C::BN>(g, m0, n0, klo, khi);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = (warp / C::WARPS_N) * C::WM, wn = (warp % C::WARPS_N) * C::WN;
@@ -168,22 +245,27 @@ __global__ void __launch_bounds__(C::NT) dgemm_dmma(GemmArgs<double> g) {
 #pragma unroll
     for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  const int64_t nk = (g.k + BK - 1) / BK;
+  const bool tri = (g.tri_a | g.tri_b) != 0;
+  const int64_t nk = khi > klo ? (khi - klo + BK - 1) / BK : 0;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < nk)
-      load_stage<double, C, TA, TB, VA, VB>(g, bidx, m0, n0, s * BK, sA + s * AT::ELEMS, sB + s * BT::ELEMS);
+      load_stage<double, C, TA, TB, VA, VB>(g, tc.A, tc.B, m0, n0, klo + s * BK, sA + s * AT::ELEMS,
+                                            sB + s * BT::ELEMS);
     cp_commit();
   }
   for (int64_t kb = 0; kb < nk; ++kb) {
     cp_wait<STAGES - 2>();
     __syncthreads();
     const int st = (int)(kb % STAGES);
+    if (tri && mask_stage<double, C, TA, TB>(g, m0, n0, klo + kb * BK, sA + st * AT::ELEMS, sB + st * BT::ELEMS))
+      __syncthreads();
     {  // prefetch kb + STAGES - 1 into the slot freed at kb - 1
       const int64_t pf = kb + STAGES - 1;
       const int ps = (int)(pf % STAGES);
       if (pf < nk)
-        load_stage<double, C, TA, TB, VA, VB>(g, bidx, m0, n0, pf * BK, sA + ps * AT::ELEMS, sB + ps * BT::ELEMS);
+        load_stage<double, C, TA, TB, VA, VB>(g, tc.A, tc.B, m0, n0, klo + pf * BK, sA + ps * AT::ELEMS,
+                                              sB + ps * BT::ELEMS);
       cp_commit();
     }
     const double* a = sA + st * AT::ELEMS;
@@ -212,8 +294,8 @@ __global__ void __launch_bounds__(C::NT) dgemm_dmma(GemmArgs<double> g) {
     for (int j = 0; j < NI; ++j) {
       const int64_t gi = m0 + wm + i * 8 + fr;
       const int64_t gj = n0 + wn + j * 8 + 2 * fc;
-      store_c<double>(g, bidx, gi, gj, acc[i][j][0]);
-      store_c<double>(g, bidx, gi, gj + 1, acc[i][j][1]);
+      store_c<double>(g, tc.C, gi, gj, acc[i][j][0]);
+      store_c<double>(g, tc.C, gi, gj + 1, acc[i][j][1]);
     }
 }
 
@@ -229,13 +311,12 @@ __global__ void __launch_bounds__(256) sgemm_ffma(GemmArgs<float> g) {
   float* sA = smem;
   float* sB = smem + STAGES * AT::ELEMS;
 
-  int64_t tile = blockIdx.x;
-  const int64_t per = g.tiles_m * g.tiles_n;
-  const int64_t bidx = tile / per;
-  tile -= bidx * per;
-  const int64_t m0 = (tile / g.tiles_n) * 64, n0 = (tile % g.tiles_n) * 64;
-  if (g.skip && g.skip[bidx]) return;
+  const TileCoord<float> tc = decode<float, 64, 64>(g);
+  const int64_t m0 = tc.m0, n0 = tc.n0;
+  if (g.skip && g.skip[tc.bo]) return;
   if (tile_masked_out<64, 64>(g.mask, m0, n0)) return;
+  int64_t klo, khi;
+  k_range<float, 64, 64>(g, m0, n0, klo, khi);
 
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 4x4 each
   float acc[4][4];
@@ -244,21 +325,27 @@ __global__ void __launch_bounds__(256) sgemm_ffma(GemmArgs<float> g) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
 
-  const int64_t nk = (g.k + BK - 1) / BK;
+  const bool tri = (g.tri_a | g.tri_b) != 0;
+  const int64_t nk = khi > klo ? (khi - klo + BK - 1) / BK : 0;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) load_stage<float, C, TA, TB, VA, VB>(g, bidx, m0, n0, s * BK, sA + s * AT::ELEMS, sB + s * BT::ELEMS);
+    if (s < nk)
+      load_stage<float, C, TA, TB, VA, VB>(g, tc.A, tc.B, m0, n0, klo + s * BK, sA + s * AT::ELEMS,
+                                           sB + s * BT::ELEMS);
     cp_commit();
   }
   for (int64_t kb = 0; kb < nk; ++kb) {
     cp_wait<STAGES - 2>();
     __syncthreads();
     const int st = (int)(kb % STAGES);
+    if (tri && mask_stage<float, C, TA, TB>(g, m0, n0, klo + kb * BK, sA + st * AT::ELEMS, sB + st * BT::ELEMS))
+      __syncthreads();
     {
       const int64_t pf = kb + STAGES - 1;
       const int ps = (int)(pf % STAGES);
       if (pf < nk)
-        load_stage<float, C, TA, TB, VA, VB>(g, bidx, m0, n0, pf * BK, sA + ps * AT::ELEMS, sB + ps * BT::ELEMS);
+        load_stage<float, C, TA, TB, VA, VB>(g, tc.A, tc.B, m0, n0, klo + pf * BK, sA + ps * AT::ELEMS,
+                                             sB + ps * BT::ELEMS);
       cp_commit();
     }
     const float* a = sA + st * AT::ELEMS;
@@ -280,7 +367,7 @@ __global__ void __launch_bounds__(256) sgemm_ffma(GemmArgs<float> g) {
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) store_c<float>(g, bidx, m0 + ty + 16 * i, n0 + tx + 16 * j, acc[i][j]);
+    for (int j = 0; j < 4; ++j) store_c<float>(g, tc.C, m0 + ty + 16 * i, n0 + tx + 16 * j, acc[i][j]);
 }
 
 template <typename K>
@@ -289,7 +376,7 @@ void ensure_smem(K k, size_t smem) {
 }
 
 template <typename T, bool TA, bool TB, int VA, int VB>
-cudaError_t launch_tv(GemmArgs<T> g, int64_t batch, cudaStream_t s, bool large) {
+cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large) {
   if constexpr (sizeof(T) == 8) {
     if (large) {
       using C = CfgL;
@@ -302,7 +389,7 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t batch, cudaStream_t s, bool large) 
         ensure_smem(k, smem);
         attr = true;
       }
-      k<<<(unsigned)(batch * g.tiles_m * g.tiles_n), C::NT, smem, s>>>(g);
+      k<<<(unsigned)(slabs * g.tiles_m * g.tiles_n), C::NT, smem, s>>>(g);
     } else {
       using C = CfgS;
       g.tiles_m = (g.m + C::BM - 1) / C::BM;
@@ -314,7 +401,7 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t batch, cudaStream_t s, bool large) 
         ensure_smem(k, smem);
         attr = true;
       }
-      k<<<(unsigned)(batch * g.tiles_m * g.tiles_n), C::NT, smem, s>>>(g);
+      k<<<(unsigned)(slabs * g.tiles_m * g.tiles_n), C::NT, smem, s>>>(g);
     }
   } else {
     (void)large;
@@ -327,18 +414,18 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t batch, cudaStream_t s, bool large) 
       ensure_smem(k, smem);
       attr = true;
     }
-    k<<<(unsigned)(batch * g.tiles_m * g.tiles_n), 256, smem, s>>>(g);
+    k<<<(unsigned)(slabs * g.tiles_m * g.tiles_n), 256, smem, s>>>(g);
   }
   return cudaGetLastError();
 }
 
 template <typename T, bool TA, bool TB>
-cudaError_t launch_t(const GemmArgs<T>& g, int64_t batch, cudaStream_t s, bool va, bool vb, bool large) {
+cudaError_t launch_t(const GemmArgs<T>& g, int64_t slabs, cudaStream_t s, bool va, bool vb, bool large) {
   constexpr int V = 16 / (int)sizeof(T);
-  if (va && vb) return launch_tv<T, TA, TB, V, V>(g, batch, s, large);
-  if (va) return launch_tv<T, TA, TB, V, 1>(g, batch, s, large);
-  if (vb) return launch_tv<T, TA, TB, 1, V>(g, batch, s, large);
-  return launch_tv<T, TA, TB, 1, 1>(g, batch, s, large);
+  if (va && vb) return launch_tv<T, TA, TB, V, V>(g, slabs, s, large);
+  if (va) return launch_tv<T, TA, TB, V, 1>(g, slabs, s, large);
+  if (vb) return launch_tv<T, TA, TB, 1, V>(g, slabs, s, large);
+  return launch_tv<T, TA, TB, 1, 1>(g, slabs, s, large);
 }
 
 // Vector loads need 16-byte aligned rows and a contiguous extent that is a
@@ -347,50 +434,57 @@ template <typename T>
 bool vec_ok(const MatB<const T>& x, int64_t contiguous_extent) {
   constexpr int V = 16 / (int)sizeof(T);
   const uintptr_t p = reinterpret_cast<uintptr_t>(x.p);
-  return (p % 16 == 0) && (x.ld % V == 0) && (x.bs % V == 0) && (contiguous_extent % V == 0);
+  return (p % 16 == 0) && (x.ld % V == 0) && (x.bs % V == 0) && (x.bsi % V == 0) && (contiguous_extent % V == 0);
+}
+
+double useful_flops(int64_t m, int64_t n, int64_t k, int mask, int tri_a, int tri_b) {
+  double f = 2.0 * (double)m * (double)n * (double)k;
+  if (mask != MASK_FULL && m == n) f *= 0.5;
+  if (tri_a != TRI_NONE) f *= 0.5;
+  if (tri_b != TRI_NONE) f *= 0.5;
+  return f;
 }
 
 }  // namespace
 
 template <typename T>
 dla_status gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T alpha, MatB<const T> a,
-                bool ta, MatB<const T> b, bool tb, T beta, MatB<T> cm, int mask, const int32_t* skip) {
-  if (batch <= 0 || m <= 0 || n <= 0) return DLA_OK;
+                bool ta, MatB<const T> b, bool tb, T beta, MatB<T> cm, int mask, const int32_t* skip, int tri_a,
+                int tri_b, int64_t inner) {
+  if (batch <= 0 || m <= 0 || n <= 0 || inner <= 0) return DLA_OK;
   if (k <= 0) {  // C = beta C
     if (beta == T(1)) return DLA_OK;
-    if (mask != MASK_FULL) return DLA_ERR_INVALID;
+    if (mask != MASK_FULL || inner != 1) return DLA_ERR_INVALID;
     return ew_scale<T>(c, batch, m, n, cm, beta, skip);
   }
-  GemmArgs<T> g{m, n, k, alpha, beta, a, b, cm, mask, skip, 0, 0};
+  GemmArgs<T> g{m, n, k, alpha, beta, a, b, cm, mask, skip, 0, 0, tri_a, tri_b, inner};
   const bool va = vec_ok<T>(a, ta ? m : k);
   const bool vb = vec_ok<T>(b, tb ? k : n);
   // 128 x 128 tiles once they alone fill every SM; 64 x 64 otherwise
-  const int64_t big_tiles = batch * ((m + 127) / 128) * ((n + 127) / 128);
+  const int64_t slabs = batch * inner;
+  const int64_t big_tiles = slabs * ((m + 127) / 128) * ((n + 127) / 128);
   const bool large = big_tiles >= c.sms && k >= 64;
   cudaError_t e;
   const bool prof = gemm_prof_on();
   if (prof) gemm_prof_begin(c.stream);
-  if (!ta && !tb) e = launch_t<T, false, false>(g, batch, c.stream, va, vb, large);
-  else if (ta && !tb) e = launch_t<T, true, false>(g, batch, c.stream, va, vb, large);
-  else if (!ta && tb) e = launch_t<T, false, true>(g, batch, c.stream, va, vb, large);
-  else e = launch_t<T, true, true>(g, batch, c.stream, va, vb, large);
+  if (!ta && !tb) e = launch_t<T, false, false>(g, slabs, c.stream, va, vb, large);
+  else if (ta && !tb) e = launch_t<T, true, false>(g, slabs, c.stream, va, vb, large);
+  else if (!ta && tb) e = launch_t<T, false, true>(g, slabs, c.stream, va, vb, large);
+  else e = launch_t<T, true, true>(g, slabs, c.stream, va, vb, large);
   if (e != cudaSuccess) {
     fprintf(stderr, "dla_b200 gemm: %s\n", cudaGetErrorString(e));
     return DLA_ERR_CUDA;
   }
   note_launch(1);
-  if (prof) {
-    // algorithmic flops: 2 m n k, or the kept triangle only under a mask
-    double useful = (double)m * (double)n;
-    if (mask != MASK_FULL && m == n) useful = (double)m * (double)(m + 1) / 2.0;
-    gemm_prof_end(c.stream, 2.0 * useful * (double)k * (double)batch);
-  }
+  if (prof) gemm_prof_end(c.stream, useful_flops(m, n, k, mask, tri_a, tri_b) * (double)slabs);
   return DLA_OK;
 }
 
 template dla_status gemm<double>(const Ctx&, int64_t, int64_t, int64_t, int64_t, double, MatB<const double>,
-                                 bool, MatB<const double>, bool, double, MatB<double>, int, const int32_t*);
+                                 bool, MatB<const double>, bool, double, MatB<double>, int, const int32_t*, int, int,
+                                 int64_t);
 template dla_status gemm<float>(const Ctx&, int64_t, int64_t, int64_t, int64_t, float, MatB<const float>,
-                                bool, MatB<const float>, bool, float, MatB<float>, int, const int32_t*);
+                                bool, MatB<const float>, bool, float, MatB<float>, int, const int32_t*, int, int,
+                                int64_t);
 
 }  // namespace dlab

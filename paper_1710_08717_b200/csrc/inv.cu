@@ -1,0 +1,164 @@
+// Inverse-based large-n paths: every triangular solve becomes a triangular
+// GEMM on FP64 DMMA instead of a chain of n/64 dependent leaf solves.
+//
+//   trtri_levels : W <- W^{-1} for lower-triangular W, n = 64 * 2^k.  All
+//                  64x64 diagonal blocks are inverted by ONE launch; then for
+//                  s = 64, 128, ..., n/2 every pair [A 0; B C] of the level is
+//                  finished at once:  B <- -C^{-1} (B A^{-1})  (two batched
+//                  triangular GEMMs over the level's n/2s blocks).
+//                  2 log2(n/64) + 1 launches for any n (13 at n = 4096).
+//   trsm_inv     : X <- alpha op(T)^{-1} X = one triangular GEMM with the
+//                  inverse (dl/blas.hpp:307-395 semantics; the reference's
+//                  substitution order is replaced, results agree to rounding).
+//   potrf_bwd_inv: Abar = 1/2 sym(L^-T copyltu(L^T Lbar) L^-1)
+//                  (dl/adjoints.hpp:175-191) as trtri + three triangular
+//                  GEMMs: 2 n^3 flops, all DMMA, vs the composed 3 n^3 of
+//                  trmm + 2 trsm.
+// Scratch (n^2 per slice) comes from the stream-ordered pool.
+#include "common.cuh"
+#include "ops.cuh"
+
+namespace dlab {
+namespace {
+
+constexpr int IB = 64;
+constexpr int ILD = IB + 1;
+
+template <typename T>
+MatB<const T> C_(MatB<T> m) {
+  return MatB<const T>{m.p, m.ld, m.bs, m.bsi};
+}
+
+// Invert every 64x64 lower diagonal block of w (slice b, block k) in place.
+// Column j of the inverse solves L x = e_j by forward substitution.
+template <typename T>
+__global__ void __launch_bounds__(128) k_trtri_blocks(int64_t nblk, MatB<T> w) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* S = reinterpret_cast<T*>(smem_raw);
+  T* X = S + IB * ILD;
+  const int64_t b = blockIdx.x / nblk, k = blockIdx.x % nblk;
+  T* base = w.p + b * w.bs + k * IB * (w.ld + 1);
+  for (int e = threadIdx.x; e < IB * IB; e += blockDim.x) {
+    const int i = e / IB, j = e % IB;
+    S[i * ILD + j] = j <= i ? base[i * w.ld + j] : T(0);
+  }
+  __syncthreads();
+  if (threadIdx.x < IB) {
+    const int j = threadIdx.x;
+    for (int i = 0; i < j; ++i) X[i * ILD + j] = T(0);
+    for (int i = j; i < IB; ++i) {
+      T acc = (i == j) ? T(1) : T(0);
+      for (int p = j; p < i; ++p) acc -= S[i * ILD + p] * X[p * ILD + j];
+      X[i * ILD + j] = acc / S[i * ILD + i];
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < IB * IB; e += blockDim.x) {
+    const int i = e / IB, j = e % IB;
+    base[i * w.ld + j] = j <= i ? X[i * ILD + j] : T(0);
+  }
+}
+
+}  // namespace
+
+template <typename T>
+bool inv_eligible(int64_t n) {
+  if (n < 4 * IB || n % IB) return false;
+  const int64_t q = n / IB;
+  return (q & (q - 1)) == 0;
+}
+
+template <typename T>
+size_t trtri_levels_tmp(int64_t n) {
+  return sizeof(T) * (size_t)(n / 2) * (size_t)(n / 2);
+}
+
+// W lower triangular (strict upper must be zero on entry; stays zero).
+// tmp: >= trtri_levels_tmp(n) elements... bytes per slice, batch slices.
+template <typename T>
+dla_status trtri_levels(const Ctx& c, int64_t batch, int64_t n, MatB<T> w, T* tmp) {
+  const int64_t nblk = n / IB;
+  const size_t sm = sizeof(T) * 2 * IB * ILD;
+  static bool once = false;
+  if (!once) {
+    cudaFuncSetAttribute(k_trtri_blocks<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    once = true;
+  }
+  k_trtri_blocks<T><<<(unsigned)(batch * nblk), 128, sm, c.stream>>>(nblk, w);
+  DLAB_LAUNCH_CHECK();
+  for (int64_t s = IB; s < n; s *= 2) {
+    const int64_t pairs = n / (2 * s);
+    const int64_t stride = 2 * s * (w.ld + 1);
+    MatB<T> wa{w.p, w.ld, w.bs, stride};
+    MatB<T> wb = wa.sub(s, 0), wc = wa.sub(s, s);
+    MatB<T> t1{tmp, s, pairs * s * s, s * s};
+    // T1 = B A^{-1}   (A^{-1} lower)
+    DLAB_TRY(gemm<T>(c, batch, s, s, s, T(1), C_(wb), false, C_(wa), false, T(0), t1, MASK_FULL, nullptr, TRI_NONE,
+                     TRI_LOWER, pairs));
+    // B = -C^{-1} T1  (C^{-1} lower)
+    DLAB_TRY(gemm<T>(c, batch, s, s, s, T(-1), C_(wc), false, C_(t1), false, T(0), wb, MASK_FULL, nullptr,
+                     TRI_LOWER, TRI_NONE, pairs));
+  }
+  return DLA_OK;
+}
+
+template <typename T>
+dla_status trsm_inv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x, bool right,
+                    bool trans, bool lower, T alpha) {
+  const int64_t nt = right ? n : m;
+  Scratch ws(sizeof(T) * (size_t)batch * ((size_t)nt * nt + (size_t)m * n) + (size_t)batch * trtri_levels_tmp<T>(nt),
+             c.stream);
+  if (!ws.p) return DLA_ERR_CUDA;
+  T* wp = ws.as<T>();
+  MatB<T> w{wp, nt, nt * nt};
+  MatB<T> y{wp + batch * nt * nt, n, m * n};
+  T* tmp = wp + batch * (nt * nt + m * n);
+  // lower-form W: inv(T) for lower T, inv(T^T) = T^{-T} for upper T
+  DLAB_TRY(ew_tri_copy<T>(c, batch, nt, t, w, !lower));
+  DLAB_TRY(trtri_levels<T>(c, batch, nt, w, tmp));
+  const bool eff = (lower != trans);  // op(T)^{-1} = eff ? W : W^T
+  const int tri = eff ? TRI_LOWER : TRI_UPPER;
+  if (!right)
+    DLAB_TRY(gemm<T>(c, batch, m, n, m, alpha, C_(w), !eff, C_(x), false, T(0), y, MASK_FULL, c.info, tri, TRI_NONE));
+  else
+    DLAB_TRY(gemm<T>(c, batch, m, n, n, alpha, C_(x), false, C_(w), !eff, T(0), y, MASK_FULL, c.info, TRI_NONE, tri));
+  return ew_copy<T>(c, batch, m, n, C_(y), x, c.info);
+}
+
+template <typename T>
+dla_status potrf_bwd_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> lbar, MatB<const T> l,
+                         bool lower) {
+  Scratch ws(sizeof(T) * (size_t)batch * 2 * (size_t)n * n + (size_t)batch * trtri_levels_tmp<T>(n), c.stream);
+  if (!ws.p) return DLA_ERR_CUDA;
+  T* wp = ws.as<T>();
+  MatB<T> wi{wp, n, n * n};                  // L^{-1} (lower)
+  MatB<T> tt{wp + batch * n * n, n, n * n};  // Phi, then the lower half of L^-T Phi L^-1
+  T* tmp = wp + 2 * batch * n * n;
+  // Upper variant: L = R^T, Lbar = Rbar^T (dl/adjoints.hpp:183-188 is the
+  // transposed composition); the result is symmetric, so no final transpose.
+  DLAB_TRY(ew_tri_copy<T>(c, batch, n, l, wi, !lower));
+  DLAB_TRY(trtri_levels<T>(c, batch, n, wi, tmp));
+  // Phi_lower = tril(L^T Lbar): op(A) = L^T (upper), op(B) = tril(Lbar)
+  DLAB_TRY(gemm<T>(c, batch, n, n, n, T(1), l, lower, lbar, !lower, T(0), tt, MASK_LOWER, nullptr, TRI_UPPER,
+                   TRI_LOWER));
+  DLAB_TRY(ew_square<T>(c, batch, n, tt, /*copyltu*/ 2));
+  // Y = Phi L^{-1}  (into abar; lbar is no longer read, so abar may alias it)
+  DLAB_TRY(gemm<T>(c, batch, n, n, n, T(1), C_(tt), false, C_(wi), false, T(0), abar, MASK_FULL, nullptr, TRI_NONE,
+                   TRI_LOWER));
+  // lower half of L^{-T} Y
+  DLAB_TRY(gemm<T>(c, batch, n, n, n, T(1), C_(wi), true, C_(abar), false, T(0), tt, MASK_LOWER, nullptr, TRI_UPPER,
+                   TRI_NONE));
+  return ew_sym_lower_into<T>(c, batch, n, C_(tt), abar, T(0.5));
+}
+
+#define INST(T)                                                                                              \
+  template bool inv_eligible<T>(int64_t);                                                                    \
+  template size_t trtri_levels_tmp<T>(int64_t);                                                              \
+  template dla_status trtri_levels<T>(const Ctx&, int64_t, int64_t, MatB<T>, T*);                            \
+  template dla_status trsm_inv<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<const T>, MatB<T>, bool, bool, \
+                                  bool, T);                                                                  \
+  template dla_status potrf_bwd_inv<T>(const Ctx&, int64_t, int64_t, MatB<T>, MatB<const T>, MatB<const T>, bool);
+INST(double)
+INST(float)
+
+}  // namespace dlab

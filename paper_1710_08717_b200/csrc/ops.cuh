@@ -14,6 +14,23 @@ template <typename T>
 dla_status potrf_bwd_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> lbar,
                            MatB<const T> l, bool lower);
 
+// inv.cu — inverse-based large-n paths (n = 64 * 2^k, n >= 256)
+template <typename T>
+bool inv_eligible(int64_t n);
+template <typename T>
+dla_status trsm_inv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x, bool right,
+                    bool trans, bool lower, T alpha);
+template <typename T>
+dla_status potrf_bwd_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> lbar, MatB<const T> l,
+                         bool lower);
+
+// trsv.cu — one-launch solve for <= 8 right-hand sides (flag-synchronised)
+template <typename T>
+bool trsv_eligible(int64_t nt, int64_t nvec);
+template <typename T>
+dla_status trsv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x, bool right, bool trans,
+                bool lower, T alpha);
+
 // gelqf.cu
 template <typename T>
 size_t gelqf_ws_bytes(int64_t batch, int64_t m, int64_t n, bool backward);

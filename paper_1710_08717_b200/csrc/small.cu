@@ -33,7 +33,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_potrf_small(int n, MatB<T> a, bool lower, int32_t* info) {
   __shared__ T S[SN * SLD];
   __shared__ T red[8];
-  __shared__ T colbuf[2 * 66];
+  __shared__ int flag;
+  static_assert(SLD == CH_LD, "shared layout");
   const int64_t b = blockIdx.x;
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) S[(e / n) * SLD + e % n] = *a.at(b, e / n, e % n);
   __syncthreads();
@@ -54,14 +55,18 @@ __global__ void __launch_bounds__(256) k_potrf_small(int n, MatB<T> a, bool lowe
     if (threadIdx.x == 0) record_failure(info, b, DLA_ERR_ASYMMETRIC, 0);
     return;
   }
-  Chol64<T> ch;
-  ch.load(S, SLD, n);
-  const int failed = ch.factor(n, colbuf);
+  const int failed = chol_smem64<T>(S, n, &flag);
   if (failed >= 0) {
     if (threadIdx.x == 0) record_failure(info, b, DLA_ERR_NOT_SPD, failed);
     return;
   }
-  ch.store(a.at(b, 0, 0), a.ld, n, lower);
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e % n;
+    T v;
+    if (lower) v = j <= i ? S[i * SLD + j] : T(0);
+    else v = i <= j ? S[j * SLD + i] : T(0);
+    *a.at(b, i, j) = v;
+  }
 }
 
 template <typename T>

@@ -13,6 +13,7 @@
 //   potrf dl/cholesky.hpp:35-88   potri dl/cholesky.hpp:105-147
 #include "chol64.cuh"
 #include "common.cuh"
+#include "ops.cuh"
 
 namespace dlab {
 namespace {
@@ -225,17 +226,35 @@ __global__ void __launch_bounds__(256) k_trmm_leaf(int nb, int64_t nvec, MatB<co
 // global offset for the NOT_SPD step index (dl/cholesky.hpp:49-53).
 template <typename T>
 __global__ void __launch_bounds__(256) k_potrf_leaf(int nb, int64_t k0, MatB<T> a, int32_t* info) {
-  __shared__ T colbuf[2 * 66];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* S = reinterpret_cast<T*>(smem_raw);
+  __shared__ int flag;
   const int64_t b = blockIdx.x;
   if (slice_failed(info, b)) return;
-  Chol64<T> ch;
-  ch.load(a.at(b, 0, 0), a.ld, nb);
-  const int failed = ch.factor(nb, colbuf);
+  T* base = a.at(b, 0, 0);
+  for (int e0 = threadIdx.x; e0 < nb * nb; e0 += 8 * 256) {  // 8 loads in flight per thread
+    T v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 256, i = e / nb, j = e % nb;
+      v[u] = (e < nb * nb && j <= i) ? base[i * a.ld + j] : T(0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 256;
+      if (e < nb * nb) S[(e / nb) * CH_LD + e % nb] = v[u];
+    }
+  }
+  __syncthreads();
+  const int failed = chol_smem64<T>(S, nb, &flag);
   if (failed >= 0) {
     if (threadIdx.x == 0) record_failure(info, b, DLA_ERR_NOT_SPD, k0 + failed);
     return;
   }
-  ch.store(a.at(b, 0, 0), a.ld, nb, true);
+  for (int e = threadIdx.x; e < nb * nb; e += 256) {
+    const int i = e / nb, j = e % nb;
+    base[i * a.ld + j] = j <= i ? S[i * CH_LD + j] : T(0);
+  }
 }
 
 // Leaf lower-triangular inverse (in place): column j of W^{-1} solves
@@ -415,7 +434,7 @@ dla_status potrf_rec(const Ctx& c, int64_t batch, int64_t n, int64_t k0, MatB<T>
   if (n <= NB) {
     const size_t sm = sizeof(T) * NB * LDS;
     (void)sm;
-    k_potrf_leaf<T><<<(unsigned)batch, 256, 0, c.stream>>>((int)n, k0, a, c.info);
+    k_potrf_leaf<T><<<(unsigned)batch, 256, sizeof(T) * NB * CH_LD, c.stream>>>((int)n, k0, a, c.info);
     DLAB_LAUNCH_CHECK();
     return DLA_OK;
   }
@@ -423,7 +442,10 @@ dla_status potrf_rec(const Ctx& c, int64_t batch, int64_t n, int64_t k0, MatB<T>
   DLAB_TRY(potrf_rec<T>(c, batch, n1, k0, a));
   MatB<T> a21 = a.sub(n1, 0), a22 = a.sub(n1, n1);
   // A21 <- A21 L11^{-T}
-  DLAB_TRY(trsm_core<T>(c, batch, n1, n2, C_(a), a21, true, true, true));
+  if (inv_eligible<T>(n1) && n2 >= 128)  // one triangular GEMM with L11^{-1}
+    DLAB_TRY(trsm_inv<T>(c, batch, n2, n1, C_(a), a21, true, true, true, T(1)));
+  else
+    DLAB_TRY(trsm_core<T>(c, batch, n1, n2, C_(a), a21, true, true, true));
   // A22 -= A21 A21^T (lower triangle only)
   DLAB_TRY(gemm<T>(c, batch, n2, n2, n1, T(-1), C_(a21), false, C_(a21), true, T(1), a22, MASK_LOWER, c.info));
   return potrf_rec<T>(c, batch, n2, k0 + n1, a22);
@@ -481,6 +503,8 @@ dla_status trsm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T>
   if (nt <= NB)  // one leaf: alpha and the zero-diagonal test fused into it
     return trsm_core<T>(c, batch, nt, no, t, x, right, trans, lower, alpha, check_diag && c.info);
   if (check_diag) DLAB_TRY(check_zero_diag<T>(c, batch, nt, t, c.info));
+  if (trsv_eligible<T>(nt, no)) return trsv<T>(c, batch, m, n, t, x, right, trans, lower, alpha);
+  if (inv_eligible<T>(nt) && no >= 128) return trsm_inv<T>(c, batch, m, n, t, x, right, trans, lower, alpha);
   DLAB_TRY(ew_scale<T>(c, batch, m, n, x, alpha, c.info));
   return trsm_core<T>(c, batch, nt, no, t, x, right, trans, lower);
 }

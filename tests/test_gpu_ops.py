@@ -129,7 +129,7 @@ def test_syrk(port, dt):
 
 
 # ------------------------------------------------------------ trmm / trsm
-SHAPES = [(4, 3), (1, 5), (33, 17), (70, 65), (130, 7), (7, 130)]
+SHAPES = [(4, 3), (1, 5), (33, 17), (70, 65), (130, 7), (7, 130), (256, 130), (130, 256)]
 
 
 @pytest.mark.parametrize("dt", DTYPES)
@@ -192,7 +192,7 @@ def test_trsm_singular_reports_index_and_leaves_slice():
 
 
 # ----------------------------------------------------------- potrf / potri
-POTRF_N = [1, 2, 5, 17, 32, 63, 64, 65, 70, 129, 200]
+POTRF_N = [1, 2, 5, 17, 32, 63, 64, 65, 70, 129, 200, 256, 512]  # 256/512: inverse-based DMMA paths
 
 
 @pytest.mark.parametrize("dt", DTYPES)

@@ -33,6 +33,29 @@ def tm(fn, reps=10, warm=2):
     return statistics.median(ts)
 
 
+def tm_graph(fn, reps=50):
+    """Per-call device time of fn from a CUDA graph holding `reps` calls
+    (removes the Python/launch overhead that dominates tiny kernels)."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
 def spd(n, batch=1):
     x = torch.randn(batch, n, n, dtype=torch.float64, device="cuda")
     return x @ x.transpose(-1, -2) + n * torch.eye(n, dtype=torch.float64, device="cuda")
@@ -70,10 +93,22 @@ def main():
         c = torch.empty_like(x)
         rec(f"gemm {n}^3", tm(lambda: L.gemm2_into(c, x, x)), 2 * n ** 3)
         rec(f"gemm {n}^3 tb", tm(lambda: L.gemm2_into(c, x, x, False, True)), 2 * n ** 3)
-    for n in (64, 32):
+    info = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for n in (64, 32, 128, 256):
         a0 = spd(n)
         a = a0.clone()
-        rec(f"potrf n={n} batch=1 (latency)", tm(lambda: (a.copy_(a0), L.potrf_inplace(a, check=False)), 50), None)
+        rec(f"potrf n={n} batch=1 (graph, per call)",
+            tm_graph(lambda: (a.copy_(a0), L.potrf_inplace(a, check=False, info=info))), None)
+        l = L.potrf(a0)
+        v = torch.randn(1, n, 1, dtype=torch.float64, device="cuda")
+        rec(f"trsm n={n} nrhs=1 (graph, per call)", tm_graph(lambda: L.trsm_inplace(l, v, check=False)), None)
+        xx = torch.randn(1, 4096, n, dtype=torch.float64, device="cuda")
+        rec(f"trsm right n={n} nrows=4096 (graph, per call)",
+            tm_graph(lambda: L.trsm_inplace(l, xx, True, True, True, 1.0, check=False)), 4096 * n * n)
+    c64 = torch.empty(1, 64, 64, dtype=torch.float64, device="cuda")
+    x64 = torch.randn(1, 64, 64, dtype=torch.float64, device="cuda")
+    rec("gemm 64^3 (graph, per call)", tm_graph(lambda: L.gemm2_into(c64, x64, x64)), 2 * 64 ** 3)
+    rec("empty copy_ 64^2 (graph, per call)", tm_graph(lambda: c64.copy_(x64)), None)
     for n, b in ((32, 65536), (128, 8192)):
         a0 = spd(n, b)
         a = a0.clone()
