@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(128) k_trtri_blocks(int64_t nblk, MatB<T> w) {
 
 template <typename T>
 bool inv_eligible(int64_t n) {
-  if (n < 4 * IB || n % IB) return false;
+  if (n < 2 * IB || n % IB) return false;
   const int64_t q = n / IB;
   return (q & (q - 1)) == 0;
 }
@@ -151,7 +151,43 @@ dla_status potrf_bwd_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, M
   return ew_sym_lower_into<T>(c, batch, n, C_(tt), abar, T(0.5));
 }
 
+// X <- alpha op(T) X / alpha X op(T) as ONE triangular GEMM into scratch plus
+// a copy back (dl/blas.hpp:202-291 semantics; only the `lower`-selected
+// triangle of T is read).
+template <typename T>
+dla_status trmm_gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x, bool right,
+                     bool trans, bool lower, T alpha) {
+  Scratch ws(sizeof(T) * (size_t)batch * (size_t)m * n, c.stream);
+  if (!ws.p) return DLA_ERR_CUDA;
+  MatB<T> y{ws.as<T>(), n, m * n};
+  const int tri = (lower != trans) ? TRI_LOWER : TRI_UPPER;  // op(T)
+  if (!right)
+    DLAB_TRY(gemm<T>(c, batch, m, n, m, alpha, t, trans, C_(x), false, T(0), y, MASK_FULL, c.info, tri, TRI_NONE));
+  else
+    DLAB_TRY(gemm<T>(c, batch, m, n, n, alpha, C_(x), false, t, trans, T(0), y, MASK_FULL, c.info, TRI_NONE, tri));
+  return ew_copy<T>(c, batch, m, n, C_(y), x, c.info);
+}
+
+// potri (lower) via the level-batched inverse: W = L^{-1}, B = W^T W on the
+// lower triangle, mirrored exactly (dl/cholesky.hpp:141-147).  The caller has
+// checked the diagonal for exact zeros.
+template <typename T>
+dla_status potri_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
+  Scratch ws(sizeof(T) * (size_t)batch * (size_t)n * n + (size_t)batch * trtri_levels_tmp<T>(n), c.stream);
+  if (!ws.p) return DLA_ERR_CUDA;
+  MatB<T> b{ws.as<T>(), n, n * n};
+  T* tmp = ws.as<T>() + batch * n * n;
+  DLAB_TRY(ew_square<T>(c, batch, n, a, /*tril*/ 0, T(1), c.info));  // the ignored triangle may hold anything
+  DLAB_TRY(trtri_levels<T>(c, batch, n, a, tmp));
+  DLAB_TRY(gemm<T>(c, batch, n, n, n, T(1), C_(a), true, C_(a), false, T(0), b, MASK_LOWER, c.info, TRI_UPPER,
+                   TRI_LOWER));
+  return ew_sym_lower_into<T>(c, batch, n, C_(b), a, T(1));
+}
+
 #define INST(T)                                                                                              \
+  template dla_status trmm_gemm<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<const T>, MatB<T>, bool, bool, \
+                                   bool, T);                                                                 \
+  template dla_status potri_inv<T>(const Ctx&, int64_t, int64_t, MatB<T>);                                   \
   template bool inv_eligible<T>(int64_t);                                                                    \
   template size_t trtri_levels_tmp<T>(int64_t);                                                              \
   template dla_status trtri_levels<T>(const Ctx&, int64_t, int64_t, MatB<T>, T*);                            \

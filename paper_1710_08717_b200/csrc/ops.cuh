@@ -23,6 +23,11 @@ dla_status trsm_inv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<cons
 template <typename T>
 dla_status potrf_bwd_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> lbar, MatB<const T> l,
                          bool lower);
+template <typename T>
+dla_status trmm_gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x, bool right,
+                     bool trans, bool lower, T alpha);
+template <typename T>
+dla_status potri_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> a);
 
 // trsv.cu — one-launch solve for <= 8 right-hand sides (flag-synchronised)
 template <typename T>

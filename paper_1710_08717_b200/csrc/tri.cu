@@ -430,7 +430,14 @@ dla_status trmm_core(const Ctx& c, int64_t batch, int64_t nt, int64_t nother, Ma
 }
 
 template <typename T>
+dla_status potrf_blocked(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int64_t kbase);
+
+template <typename T>
 dla_status potrf_rec(const Ctx& c, int64_t batch, int64_t n, int64_t k0, MatB<T> a) {
+  // Bottom of the recursion: blocked right-looking with the fused panel
+  // kernel (rank-64 updates are fine at this size; above it, the recursive
+  // split keeps the SYRK/trsm GEMMs at K = n/2).
+  if (n > NB && n <= 512 && batch <= 64) return potrf_blocked<T>(c, batch, n, a, k0);
   if (n <= NB) {
     const size_t sm = sizeof(T) * NB * LDS;
     (void)sm;
@@ -449,6 +456,103 @@ dla_status potrf_rec(const Ctx& c, int64_t batch, int64_t n, int64_t k0, MatB<T>
   // A22 -= A21 A21^T (lower triangle only)
   DLAB_TRY(gemm<T>(c, batch, n2, n2, n1, T(-1), C_(a21), false, C_(a21), true, T(1), a22, MASK_LOWER, c.info));
   return potrf_rec<T>(c, batch, n2, k0 + n1, a22);
+}
+
+// One block column of the right-looking Cholesky in ONE launch: every CTA
+// factors the 64 x 64 diagonal block (redundantly — it is latency, not
+// work), CTA 0 stores L11, and each CTA solves its own 64 rows of the panel
+// A21 <- A21 L11^{-T} in shared memory (blocked substitution + DMMA).
+template <typename T>
+__global__ void __launch_bounds__(256) k_potrf_panel(int nb, int64_t rest, int64_t k0, MatB<T> akk, MatB<T> a21,
+                                                     int32_t* info) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* S = reinterpret_cast<T*>(smem_raw);
+  T* V = S + 64 * CH_LD;
+  T* rd = V + 64 * CH_LD;
+  __shared__ int flag;
+  const int64_t chunks = rest > 0 ? (rest + 63) / 64 : 1;
+  const int64_t b = blockIdx.x / chunks, cid = blockIdx.x % chunks;
+  if (slice_failed(info, b)) return;
+  const int tid = threadIdx.x;
+  T* base = akk.at(b, 0, 0);
+  for (int e0 = tid; e0 < 64 * 64; e0 += 8 * 256) {
+    T v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 256, i = e / 64, j = e % 64;
+      v[u] = (i < nb && j <= i) ? base[i * akk.ld + j] : T(0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 256;
+      S[(e / 64) * CH_LD + e % 64] = v[u];
+    }
+  }
+  const int64_t r0 = cid * 64;
+  const int nv = rest > 0 ? (int)min((int64_t)64, rest - r0) : 0;
+  T* pan = a21.at(b, r0, 0);
+  for (int e0 = tid; e0 < 64 * 64; e0 += 8 * 256) {  // panel rows, loads in flight during the factorization
+    T v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 256, vv = e / 64, i = e % 64;
+      v[u] = (vv < nv && i < nb) ? pan[vv * a21.ld + i] : T(0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 256;
+      V[(e / 64) * CH_LD + e % 64] = v[u];
+    }
+  }
+  __syncthreads();
+  const int failed = chol_smem64<T>(S, nb, &flag);
+  if (failed >= 0) {
+    if (cid == 0 && tid == 0) record_failure(info, b, DLA_ERR_NOT_SPD, k0 + failed);
+    return;
+  }
+  if (cid == 0)
+    for (int e = tid; e < nb * nb; e += 256) {
+      const int i = e / nb, j = e % nb;
+      base[i * akk.ld + j] = j <= i ? S[i * CH_LD + j] : T(0);
+    }
+  if (nv == 0) return;
+  if (tid < 64) rd[tid] = tid < nb ? T(1) / S[tid * CH_LD + tid] : T(1);
+  __syncthreads();
+  blocked_fwd_subst<T>(S, V, rd, nb, nv);  // row v: L11 x = a  <=>  x^T L11^T = a^T
+  for (int e = tid; e < nv * nb; e += 256) {
+    const int vv = e / nb, i = e % nb;
+    pan[vv * a21.ld + i] = V[vv * CH_LD + i];
+  }
+}
+
+// Right-looking blocked Cholesky (the reference's own loop structure,
+// dl/cholesky.hpp:43-70, with nb = 64): per block column one warp-panel leaf
+// factorization, one blocked DMMA panel solve (all rows of the panel in
+// parallel, 64 per CTA) and one masked DMMA SYRK of the trailing matrix.
+// Three launches per 64 columns; used for large single matrices where the
+// recursive variant's deep chain of tiny GEMMs dominates.
+template <typename T>
+dla_status potrf_blocked(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int64_t kbase) {
+  const size_t sm = sizeof(T) * (2 * 64 * CH_LD + 64);
+  static bool once = false;
+  if (!once) {
+    set_smem(k_potrf_panel<T>, sm);
+    once = true;
+  }
+  for (int64_t k0 = 0; k0 < n; k0 += NB) {
+    const int64_t kb = min((int64_t)NB, n - k0);
+    const int64_t rest = n - k0 - kb;
+    MatB<T> akk = a.sub(k0, k0);
+    MatB<T> a21 = a.sub(k0 + kb, k0);
+    const int64_t chunks = rest > 0 ? (rest + 63) / 64 : 1;
+    k_potrf_panel<T><<<(unsigned)(batch * chunks), 256, sm, c.stream>>>((int)kb, rest, kbase + k0, akk, a21,
+                                                                         c.info);
+    DLAB_LAUNCH_CHECK();
+    if (rest == 0) break;
+    DLAB_TRY(gemm<T>(c, batch, rest, rest, kb, T(-1), C_(a21), false, C_(a21), true, T(1), a.sub(k0 + kb, k0 + kb),
+                     MASK_LOWER, c.info));
+  }
+  return DLA_OK;
 }
 
 template <typename T>
@@ -513,6 +617,8 @@ template <typename T>
 dla_status trmm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x, bool right,
                 bool trans, bool lower, T alpha) {
   if (batch == 0 || m == 0 || n == 0) return DLA_OK;
+  const int64_t nt = right ? n : m;
+  if (nt >= 128) return trmm_gemm<T>(c, batch, m, n, t, x, right, trans, lower, alpha);
   return right ? trmm_core<T>(c, batch, n, m, t, x, right, trans, lower, alpha)
                : trmm_core<T>(c, batch, m, n, t, x, right, trans, lower, alpha);
 }
@@ -526,7 +632,13 @@ dla_status potrf_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
     set_smem(k_lauum_leaf<T>, sizeof(T) * NB * LDS);
     once = true;
   }
-  DLAB_TRY(potrf_rec<T>(c, batch, n, 0, a));
+  static const int mode = [] {
+    const char* e = getenv("DLA_POTRF_MODE");  // tuning switch: 0 auto, 1 recursive, 2 blocked
+    return e ? atoi(e) : 0;
+  }();
+  const bool blocked = mode == 2;  // default (auto): recursive with a blocked bottom
+  if (blocked) DLAB_TRY(potrf_blocked<T>(c, batch, n, a, 0));
+  else DLAB_TRY(potrf_rec<T>(c, batch, n, 0, a));
   return ew_square<T>(c, batch, n, a, /*tril*/ 0, T(1), c.info);
 }
 
@@ -539,6 +651,7 @@ dla_status potri_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
     set_smem(k_lauum_leaf<T>, sizeof(T) * NB * LDS);
     once = true;
   }
+  if (inv_eligible<T>(n)) return potri_inv<T>(c, batch, n, a);
   DLAB_TRY(trtri_rec<T>(c, batch, n, a));
   DLAB_TRY(lauum_rec<T>(c, batch, n, a));
   return ew_square<T>(c, batch, n, a, /*copyltu*/ 2, T(1), c.info);

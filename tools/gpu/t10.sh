@@ -1,0 +1,4 @@
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
+bash tools/gpu/t9.sh
+python tools/microbench.py 2>&1 | grep -E "potrf|graph" | head -12
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-also 2> gpurun_out/bench_c2.err | cut -c1-300

@@ -50,7 +50,7 @@ int main() {
     long long* t;
     cudaMalloc(&d, sizeof(h));
     cudaMalloc(&t, 64);
-    for (int threads : {128, 256}) {
+    for (int threads : {32, 64, 128, 256}) {
       cudaMemcpy(d, h, sizeof(double) * n * n, cudaMemcpyHostToDevice);
       k<<<1, threads>>>(d, n, t);
       long long ht[2];
