@@ -165,6 +165,9 @@ dla_status ew_tri_copy(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src
 // dst(i,j) = dst(j,i) = alpha * src(max(i,j), min(i,j))  (bit-symmetric)
 template <typename T>
 dla_status ew_sym_lower_into(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, T alpha);
+// dst = src + src^T
+template <typename T>
+dla_status ew_add_transpose(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst);
 template <typename T>
 dla_status check_symmetric(const Ctx& c, int64_t batch, int64_t n, MatB<const T> a, int32_t* info);
 template <typename T>

@@ -92,6 +92,15 @@ __global__ void k_tri_copy(int64_t batch, int64_t n, MatB<const T> src, MatB<T> 
 }
 
 template <typename T>
+__global__ void k_add_transpose(int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst) {
+  const int64_t total = batch * n * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t / (n * n), r = t % (n * n), i = r / n, j = r % n;
+    *dst.at(b, i, j) = *src.at(b, i, j) + *src.at(b, j, i);
+  }
+}
+
+template <typename T>
 __global__ void k_sym_lower_into(int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, T alpha) {
   const int64_t total = batch * n * n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -245,6 +254,14 @@ dla_status ew_tri_copy(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src
 }
 
 template <typename T>
+dla_status ew_add_transpose(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst) {
+  if (batch * n == 0) return DLA_OK;
+  k_add_transpose<T><<<blocks_for(batch * n * n, 256), 256, 0, c.stream>>>(batch, n, src, dst);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+
+template <typename T>
 dla_status ew_sym_lower_into(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, T alpha) {
   if (batch * n == 0) return DLA_OK;
   k_sym_lower_into<T><<<blocks_for(batch * n * n, 256), 256, 0, c.stream>>>(batch, n, src, dst, alpha);
@@ -305,6 +322,7 @@ dla_status sumlogdiag_bwd(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, 
   template dla_status check_symmetric<T>(const Ctx&, int64_t, int64_t, MatB<const T>, int32_t*);        \
   template dla_status ew_tri_copy<T>(const Ctx&, int64_t, int64_t, MatB<const T>, MatB<T>, bool);       \
   template dla_status ew_sym_lower_into<T>(const Ctx&, int64_t, int64_t, MatB<const T>, MatB<T>, T);    \
+  template dla_status ew_add_transpose<T>(const Ctx&, int64_t, int64_t, MatB<const T>, MatB<T>);        \
   template dla_status check_zero_diag<T>(const Ctx&, int64_t, int64_t, MatB<const T>, int32_t*);        \
   template dla_status sumlogdiag_fwd<T>(const Ctx&, int64_t, int64_t, T*, MatB<const T>);               \
   template dla_status sumlogdiag_bwd<T>(const Ctx&, int64_t, int64_t, MatB<T>, const T*, MatB<const T>, \

@@ -210,8 +210,14 @@ __device__ __forceinline__ TileCoord<T> decode(const GemmArgs<T>& g) {
   TileCoord<T> t;
   t.bo = slab / g.inner;
   const int64_t bi = slab % g.inner;
-  t.m0 = (tile / g.tiles_n) * BM;
-  t.n0 = (tile % g.tiles_n) * BN;
+  int64_t tm = tile / g.tiles_n, tn = tile % g.tiles_n;
+  // Longest-K tiles first (CTAs are dispatched in blockIdx order): a lower
+  // op(A) gives the bottom tile rows the longest K range, an upper op(B) the
+  // right-most tile columns.
+  if (g.tri_a == TRI_LOWER) tm = g.tiles_m - 1 - tm;
+  if (g.tri_b == TRI_UPPER) tn = g.tiles_n - 1 - tn;
+  t.m0 = tm * BM;
+  t.n0 = tn * BN;
   t.A = g.a.p + t.bo * g.a.bs + bi * g.a.bsi;
   t.B = g.b.p + t.bo * g.b.bs + bi * g.b.bsi;
   t.C = g.c.p + t.bo * g.c.bs + bi * g.c.bsi;

@@ -15,6 +15,7 @@
 //                  GEMMs: 2 n^3 flops, all DMMA, vs the composed 3 n^3 of
 //                  trmm + 2 trsm.
 // Scratch (n^2 per slice) comes from the stream-ordered pool.
+#include "chol64.cuh"
 #include "common.cuh"
 #include "ops.cuh"
 
@@ -23,39 +24,45 @@ namespace {
 
 constexpr int IB = 64;
 constexpr int ILD = IB + 1;
+static_assert(ILD == CH_LD, "shared layout shared with chol64.cuh");
 
 template <typename T>
 MatB<const T> C_(MatB<T> m) {
   return MatB<const T>{m.p, m.ld, m.bs, m.bsi};
 }
 
-// Invert every 64x64 lower diagonal block of w (slice b, block k) in place.
-// Column j of the inverse solves L x = e_j by forward substitution.
+// Invert every 64x64 lower diagonal block of w (slice b, block k) in place:
+// L X = I for all 64 columns at once with the blocked substitution (8x8
+// diagonal solves + DMMA updates in shared memory, chol64.cuh).
 template <typename T>
 __global__ void __launch_bounds__(128) k_trtri_blocks(int64_t nblk, MatB<T> w) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* S = reinterpret_cast<T*>(smem_raw);
-  T* X = S + IB * ILD;
+  T* X = S + IB * ILD;  // vector-major: X[v * ILD + i] = Linv(i, v)
+  T* rd = X + IB * ILD;
   const int64_t b = blockIdx.x / nblk, k = blockIdx.x % nblk;
   T* base = w.p + b * w.bs + k * IB * (w.ld + 1);
-  for (int e = threadIdx.x; e < IB * IB; e += blockDim.x) {
-    const int i = e / IB, j = e % IB;
-    S[i * ILD + j] = j <= i ? base[i * w.ld + j] : T(0);
-  }
-  __syncthreads();
-  if (threadIdx.x < IB) {
-    const int j = threadIdx.x;
-    for (int i = 0; i < j; ++i) X[i * ILD + j] = T(0);
-    for (int i = j; i < IB; ++i) {
-      T acc = (i == j) ? T(1) : T(0);
-      for (int p = j; p < i; ++p) acc -= S[i * ILD + p] * X[p * ILD + j];
-      X[i * ILD + j] = acc / S[i * ILD + i];
+  for (int e0 = threadIdx.x; e0 < IB * IB; e0 += 8 * 128) {
+    T v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 128, i = e / IB, j = e % IB;
+      v[u] = j <= i ? base[i * w.ld + j] : T(0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 128, i = e / IB, j = e % IB;
+      S[i * ILD + j] = v[u];
+      X[i * ILD + j] = (i == j) ? T(1) : T(0);
     }
   }
   __syncthreads();
+  if (threadIdx.x < IB) rd[threadIdx.x] = T(1) / S[threadIdx.x * ILD + threadIdx.x];
+  __syncthreads();
+  blocked_fwd_subst<T>(S, X, rd, IB, IB);
   for (int e = threadIdx.x; e < IB * IB; e += blockDim.x) {
     const int i = e / IB, j = e % IB;
-    base[i * w.ld + j] = j <= i ? X[i * ILD + j] : T(0);
+    base[i * w.ld + j] = j <= i ? X[j * ILD + i] : T(0);
   }
 }
 
@@ -78,7 +85,7 @@ size_t trtri_levels_tmp(int64_t n) {
 template <typename T>
 dla_status trtri_levels(const Ctx& c, int64_t batch, int64_t n, MatB<T> w, T* tmp) {
   const int64_t nblk = n / IB;
-  const size_t sm = sizeof(T) * 2 * IB * ILD;
+  const size_t sm = sizeof(T) * (2 * IB * ILD + IB);
   static bool once = false;
   if (!once) {
     cudaFuncSetAttribute(k_trtri_blocks<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
