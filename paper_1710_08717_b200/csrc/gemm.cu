@@ -294,15 +294,60 @@ __global__ void __launch_bounds__(C::NT) dgemm_dmma(GemmArgs<double> g) {
     }
   }
   cp_wait<0>();
-#pragma unroll
-  for (int i = 0; i < MI; ++i)
+  // Epilogue: C rows in groups of 8 (one fragment row i); when beta != 0 the
+  // C values of group i+1 are loaded before group i is stored, so the
+  // read-modify-write of C keeps loads in flight (the rank-64 SYRK updates
+  // of the blocked Cholesky are bound by exactly this C traffic).
+  const bool vec2 = ((g.c.ld & 1) == 0) && ((reinterpret_cast<uintptr_t>(tc.C) & 15) == 0);
+  auto load_group = [&](int i, double (&cv)[NI][2]) {
 #pragma unroll
     for (int j = 0; j < NI; ++j) {
-      const int64_t gi = m0 + wm + i * 8 + fr;
-      const int64_t gj = n0 + wn + j * 8 + 2 * fc;
-      store_c<double>(g, tc.C, gi, gj, acc[i][j][0]);
-      store_c<double>(g, tc.C, gi, gj + 1, acc[i][j][1]);
+      cv[j][0] = cv[j][1] = 0.0;
+      if (g.beta == 0.0) continue;
+      const int64_t gi = m0 + wm + i * 8 + fr, gj = n0 + wn + j * 8 + 2 * fc;
+      if (gi >= g.m) continue;
+      const double* cp = tc.C + gi * g.c.ld + gj;
+      if (vec2 && gj + 1 < g.n) {
+        const double2 v = *reinterpret_cast<const double2*>(cp);
+        cv[j][0] = v.x;
+        cv[j][1] = v.y;
+      } else {
+        if (gj < g.n) cv[j][0] = cp[0];
+        if (gj + 1 < g.n) cv[j][1] = cp[1];
+      }
     }
+  };
+  double cur[NI][2], nxt[NI][2];
+  load_group(0, cur);
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    if (i + 1 < MI) load_group(i + 1, nxt);
+    const int64_t gi = m0 + wm + i * 8 + fr;
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+      const int64_t gj = n0 + wn + j * 8 + 2 * fc;
+      if (gi >= g.m) continue;
+      const double v0 = g.alpha * acc[i][j][0] + g.beta * cur[j][0];
+      const double v1 = g.alpha * acc[i][j][1] + g.beta * cur[j][1];
+      const bool ok0 = gj < g.n && !(g.mask == MASK_LOWER && gj > gi) && !(g.mask == MASK_UPPER && gj < gi);
+      const bool ok1 =
+          gj + 1 < g.n && !(g.mask == MASK_LOWER && gj + 1 > gi) && !(g.mask == MASK_UPPER && gj + 1 < gi);
+      double* cp = tc.C + gi * g.c.ld + gj;
+      if (vec2 && ok0 && ok1) {
+        *reinterpret_cast<double2*>(cp) = make_double2(v0, v1);
+      } else {
+        if (ok0) cp[0] = v0;
+        if (ok1) cp[1] = v1;
+      }
+    }
+    if (i + 1 < MI) {
+#pragma unroll
+      for (int j = 0; j < NI; ++j) {
+        cur[j][0] = nxt[j][0];
+        cur[j][1] = nxt[j][1];
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------------ f32 FFMA
