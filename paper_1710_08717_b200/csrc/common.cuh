@@ -167,7 +167,10 @@ template <typename T>
 dla_status ew_sym_lower_into(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, T alpha);
 // dst = src + src^T
 template <typename T>
-dla_status ew_add_transpose(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst);
+dla_status ew_add_transpose(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, T alpha = T(1));
+// x(i,i) *= alpha
+template <typename T>
+dla_status ew_scale_diag(const Ctx& c, int64_t batch, int64_t n, MatB<T> x, T alpha);
 template <typename T>
 dla_status check_symmetric(const Ctx& c, int64_t batch, int64_t n, MatB<const T> a, int32_t* info);
 template <typename T>

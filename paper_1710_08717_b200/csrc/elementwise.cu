@@ -92,12 +92,20 @@ __global__ void k_tri_copy(int64_t batch, int64_t n, MatB<const T> src, MatB<T> 
 }
 
 template <typename T>
-__global__ void k_add_transpose(int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst) {
+__global__ void k_add_transpose(int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, T alpha) {
   const int64_t total = batch * n * n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = t / (n * n), r = t % (n * n), i = r / n, j = r % n;
-    *dst.at(b, i, j) = *src.at(b, i, j) + *src.at(b, j, i);
+    // (x_ij + x_ji) is the same IEEE sum from either side: bit-symmetric output
+    const T s = (i >= j) ? (*src.at(b, i, j) + *src.at(b, j, i)) : (*src.at(b, j, i) + *src.at(b, i, j));
+    *dst.at(b, i, j) = alpha * s;
   }
+}
+
+template <typename T>
+__global__ void k_scale_diag(int64_t batch, int64_t n, MatB<T> x, T alpha) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < batch * n; t += (int64_t)gridDim.x * blockDim.x)
+    *x.at(t / n, t % n, t % n) *= alpha;
 }
 
 template <typename T>
@@ -254,9 +262,17 @@ dla_status ew_tri_copy(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src
 }
 
 template <typename T>
-dla_status ew_add_transpose(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst) {
+dla_status ew_add_transpose(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, T alpha) {
   if (batch * n == 0) return DLA_OK;
-  k_add_transpose<T><<<blocks_for(batch * n * n, 256), 256, 0, c.stream>>>(batch, n, src, dst);
+  k_add_transpose<T><<<blocks_for(batch * n * n, 256), 256, 0, c.stream>>>(batch, n, src, dst, alpha);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+
+template <typename T>
+dla_status ew_scale_diag(const Ctx& c, int64_t batch, int64_t n, MatB<T> x, T alpha) {
+  if (batch * n == 0) return DLA_OK;
+  k_scale_diag<T><<<blocks_for(batch * n, 256), 256, 0, c.stream>>>(batch, n, x, alpha);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }
@@ -322,7 +338,8 @@ dla_status sumlogdiag_bwd(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, 
   template dla_status check_symmetric<T>(const Ctx&, int64_t, int64_t, MatB<const T>, int32_t*);        \
   template dla_status ew_tri_copy<T>(const Ctx&, int64_t, int64_t, MatB<const T>, MatB<T>, bool);       \
   template dla_status ew_sym_lower_into<T>(const Ctx&, int64_t, int64_t, MatB<const T>, MatB<T>, T);    \
-  template dla_status ew_add_transpose<T>(const Ctx&, int64_t, int64_t, MatB<const T>, MatB<T>);        \
+  template dla_status ew_add_transpose<T>(const Ctx&, int64_t, int64_t, MatB<const T>, MatB<T>, T);     \
+  template dla_status ew_scale_diag<T>(const Ctx&, int64_t, int64_t, MatB<T>, T);                       \
   template dla_status check_zero_diag<T>(const Ctx&, int64_t, int64_t, MatB<const T>, int32_t*);        \
   template dla_status sumlogdiag_fwd<T>(const Ctx&, int64_t, int64_t, T*, MatB<const T>);               \
   template dla_status sumlogdiag_bwd<T>(const Ctx&, int64_t, int64_t, MatB<T>, const T*, MatB<const T>, \

@@ -145,17 +145,20 @@ dla_status potrf_bwd_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, M
   // transposed composition); the result is symmetric, so no final transpose.
   DLAB_TRY(ew_tri_copy<T>(c, batch, n, l, wi, !lower));
   DLAB_TRY(trtri_levels<T>(c, batch, n, wi, tmp));
-  // Phi_lower = tril(L^T Lbar): op(A) = L^T (upper), op(B) = tril(Lbar)
+  // P = tril(L^T Lbar): op(A) = L^T (upper), op(B) = tril(Lbar); then halve
+  // its diagonal so that Phi = copyltu(P) = P' + P'^T exactly.
   DLAB_TRY(gemm<T>(c, batch, n, n, n, T(1), l, lower, lbar, !lower, T(0), tt, MASK_LOWER, nullptr, TRI_UPPER,
                    TRI_LOWER));
-  DLAB_TRY(ew_square<T>(c, batch, n, tt, /*copyltu*/ 2));
-  // Y = Phi L^{-1}  (into abar; lbar is no longer read, so abar may alias it)
-  DLAB_TRY(gemm<T>(c, batch, n, n, n, T(1), C_(tt), false, C_(wi), false, T(0), abar, MASK_FULL, nullptr, TRI_NONE,
+  DLAB_TRY(ew_scale_diag<T>(c, batch, n, tt, T(0.5)));
+  // W = P' L^{-1}: lower x lower = lower  (into abar; lbar is no longer read,
+  // so abar may alias it)
+  DLAB_TRY(gemm<T>(c, batch, n, n, n, T(1), C_(tt), false, C_(wi), false, T(0), abar, MASK_LOWER, nullptr, TRI_LOWER,
                    TRI_LOWER));
-  // lower half of L^{-T} Y
-  DLAB_TRY(gemm<T>(c, batch, n, n, n, T(1), C_(wi), true, C_(abar), false, T(0), tt, MASK_LOWER, nullptr, TRI_UPPER,
-                   TRI_NONE));
-  return ew_sym_lower_into<T>(c, batch, n, C_(tt), abar, T(0.5));
+  // Z = L^{-T} W  (upper x lower, full);  L^-T Phi L^-1 = Z + Z^T
+  DLAB_TRY(gemm<T>(c, batch, n, n, n, T(1), C_(wi), true, C_(abar), false, T(0), tt, MASK_FULL, nullptr, TRI_UPPER,
+                   TRI_LOWER));
+  // Abar = 1/2 (Z + Z^T), bit-symmetric
+  return ew_add_transpose<T>(c, batch, n, C_(tt), abar, T(0.5));
 }
 
 // X <- alpha op(T) X / alpha X op(T) as ONE triangular GEMM into scratch plus
