@@ -11,6 +11,7 @@
 // Semantics are trsm_inplace's (dl/blas.hpp:307-395): S is op(T) (left) or
 // op(T)^T (right, vectors are rows of X); an upper S is handled by reversing
 // the row order so the kernel always runs a forward substitution.
+#include "chol64.cuh"
 #include "common.cuh"
 #include "ops.cuh"
 
@@ -44,9 +45,11 @@ __device__ __forceinline__ T* x_at(const TrsvGeo& g, MatB<T> x, int64_t b, int64
 template <typename T>
 __global__ void __launch_bounds__(TT) k_trsv(TrsvGeo g, MatB<const T> t, MatB<T> x, T alpha, int* flags,
                                              const int32_t* skip) {
-  __shared__ T SP[BR * SLD];    // partial sums P[4][NR][BR], then the diagonal block (lower form)
-  __shared__ T Y[NR][BR];       // solved y_j of the block being applied / result
-  __shared__ T rd[BR];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* SP = reinterpret_cast<T*>(smem_raw);  // diagonal block, then partial sums P[4][NR][BR]
+  T* Xi = SP + BR * SLD;                   // inverse of the diagonal block, vector-major: Xi[v*SLD + r] = Sinv(r, v)
+  T* rd = Xi + BR * SLD;
+  T(*Y)[BR] = reinterpret_cast<T(*)[BR]>(rd + BR);  // [NR][BR]
   T* S = SP;
   const int64_t b = blockIdx.x / g.nblk, i = blockIdx.x % g.nblk;
   if (slice_failed(skip, b)) return;
@@ -54,6 +57,18 @@ __global__ void __launch_bounds__(TT) k_trsv(TrsvGeo g, MatB<const T> t, MatB<T>
   const int64_t r0 = i * BR;
   const int rows = (int)min((int64_t)BR, g.nt - r0);
   const int nv = (int)g.nvec;
+  // Off the critical path (before waiting on any earlier block): invert the
+  // diagonal block, so the dependent step is a 64 x 64 matrix-vector product
+  // instead of a 64-step substitution.
+  for (int e = tid; e < BR * BR; e += TT) {
+    const int rr = e / BR, c = e % BR;
+    S[rr * SLD + c] = (rr < rows && c <= rr) ? s_at(g, t, b, r0 + rr, r0 + c) : (rr == c ? T(1) : T(0));
+    Xi[rr * SLD + c] = (rr == c) ? T(1) : T(0);
+  }
+  __syncthreads();
+  if (tid < BR) rd[tid] = T(1) / S[tid * SLD + tid];
+  __syncthreads();
+  blocked_fwd_subst<T>(S, Xi, rd, BR, BR);
   // (row, 16-column chunk) per thread; lanes walk contiguous memory of T
   const int r = g.s_tt ? tid % BR : tid / 4, cq = g.s_tt ? tid / BR : tid % 4;
   T part[NR];
@@ -61,9 +76,14 @@ __global__ void __launch_bounds__(TT) k_trsv(TrsvGeo g, MatB<const T> t, MatB<T>
   for (int v = 0; v < NR; ++v) part[v] = T(0);
   // off-diagonal blocks j < i, in publication order
   for (int64_t j = 0; j < i; ++j) {
+    // the triangle's block (i, j) does not depend on block j's result:
+    // fetch it before waiting for the flag
+    T s[16];
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) s[cc] = (r < rows) ? s_at(g, t, b, r0 + r, j * BR + cq * 16 + cc) : T(0);
     if (tid == 0) {
       volatile int* f = flags + b * g.nblk + j;
-      while (*f == 0) __nanosleep(64);
+      while (*f == 0) __nanosleep(32);
       __threadfence();
     }
     __syncthreads();
@@ -72,15 +92,12 @@ __global__ void __launch_bounds__(TT) k_trsv(TrsvGeo g, MatB<const T> t, MatB<T>
       Y[v][c] = __ldcg(x_at(g, x, b, j * BR + c, v));  // L2: written by another CTA
     }
     __syncthreads();
-    if (r < rows) {
-#pragma unroll 4
-      for (int cc = 0; cc < 16; ++cc) {
-        const int c = cq * 16 + cc;
-        const T s = s_at(g, t, b, r0 + r, j * BR + c);
 #pragma unroll
-        for (int v = 0; v < NR; ++v)
-          if (v < nv) part[v] += s * Y[v][c];
-      }
+    for (int cc = 0; cc < 16; ++cc) {
+      const int c = cq * 16 + cc;
+#pragma unroll
+      for (int v = 0; v < NR; ++v)
+        if (v < nv) part[v] += s[cc] * Y[v][c];
     }
   }
   // right-hand side: alpha x_i minus the four column-chunk partial sums
@@ -96,35 +113,13 @@ __global__ void __launch_bounds__(TT) k_trsv(TrsvGeo g, MatB<const T> t, MatB<T>
     Y[v][rr] = acc;
   }
   __syncthreads();
-  // diagonal block (over the partial sums) and reciprocal pivots
-  for (int e = tid; e < BR * BR; e += TT) {
-    const int rr = e / BR, c = e % BR;
-    S[rr * SLD + c] = (rr < rows && c <= rr) ? s_at(g, t, b, r0 + rr, r0 + c) : T(0);
-  }
-  __syncthreads();
-  if (tid < BR) rd[tid] = tid < rows ? T(1) / S[tid * SLD + tid] : T(0);
-  __syncthreads();
-  // forward substitution, a warp per vector (lanes own rows l, l + 32)
-  const int warp = tid >> 5, lane = tid & 31;
-  for (int v = warp; v < nv; v += TT / 32) {
-    T y0 = Y[v][lane], y1 = Y[v][lane + 32];
-    for (int c = 0; c < rows; ++c) {
-      const int owner = c & 31;
-      T yc = __shfl_sync(0xffffffffu, c < 32 ? y0 : y1, owner) * rd[c];
-      if (lane == owner) {
-        if (c < 32) y0 = yc;
-        else y1 = yc;
-      }
-      if (lane > c) y0 -= S[lane * SLD + c] * yc;
-      if (lane + 32 > c) y1 -= S[(lane + 32) * SLD + c] * yc;
-    }
-    Y[v][lane] = y0;
-    Y[v][lane + 32] = y1;
-  }
-  __syncthreads();
+  // y_i = S_ii^{-1} rhs: thread (row, vector) dots the lower row of S^{-1}
   for (int e = tid; e < nv * BR; e += TT) {
     const int v = e / BR, rr = e % BR;
-    if (rr < rows) *x_at(g, x, b, r0 + rr, v) = Y[v][rr];
+    if (rr >= rows) continue;
+    T acc = T(0);
+    for (int c = 0; c <= rr; ++c) acc += Xi[c * SLD + rr] * Y[v][c];
+    *x_at(g, x, b, r0 + rr, v) = acc;
   }
   __threadfence();
   __syncthreads();
@@ -152,7 +147,13 @@ dla_status trsv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T>
   Scratch flags(sizeof(int) * (size_t)(batch * g.nblk), c.stream);
   if (!flags.p) return DLA_ERR_CUDA;
   if (cudaMemsetAsync(flags.p, 0, sizeof(int) * batch * g.nblk, c.stream) != cudaSuccess) return DLA_ERR_CUDA;
-  k_trsv<T><<<(unsigned)(batch * g.nblk), TT, 0, c.stream>>>(g, t, x, alpha, flags.as<int>(), c.info);
+  const size_t sm = sizeof(T) * (2 * BR * SLD + BR + NR * BR);
+  static bool once = false;
+  if (!once) {
+    cudaFuncSetAttribute(k_trsv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    once = true;
+  }
+  k_trsv<T><<<(unsigned)(batch * g.nblk), TT, sm, c.stream>>>(g, t, x, alpha, flags.as<int>(), c.info);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }
