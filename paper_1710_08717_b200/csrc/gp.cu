@@ -122,6 +122,132 @@ __global__ void __launch_bounds__(RT) k_rbf_bwd(int64_t n, int64_t d, const doub
   }
 }
 
+// Tiled variants for a compile-time feature count D (the C2 workload has
+// d = 8): a CTA owns 16 rows; warp w handles rows w and w + 8, its lanes
+// stride the columns, so every A / Abar access of a warp is one contiguous
+// 256-byte row segment; x_j tiles are staged in shared memory once per CTA.
+constexpr int TRW = 16;   // rows per CTA
+constexpr int TCJ = 128;  // columns per staged tile
+
+template <int D, bool FWD>
+__global__ void __launch_bounds__(256) k_rbf_tiled(int64_t n, const double* x, const double* s, double sigma2,
+                                                   double two_ell2, double lam, double* a, const double* abar,
+                                                   double* xbar, double* part) {
+  __shared__ double xs[TCJ][D];
+  __shared__ double ss[TCJ];
+  const int64_t rb = (n + TRW - 1) / TRW;
+  const int64_t b = blockIdx.x / rb, i0 = (blockIdx.x % rb) * TRW;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* xb = x + b * n * D;
+  const double* sb = s + b * n;
+  int64_t ii[2] = {i0 + warp, i0 + warp + 8};
+  double xi[2][D], si[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const bool ok = ii[q] < n;
+#pragma unroll
+    for (int f = 0; f < D; ++f) xi[q][f] = ok ? xb[ii[q] * D + f] : 0.0;
+    si[q] = ok ? sb[ii[q]] : 0.0;
+  }
+  double ps[2] = {0, 0}, pl[2] = {0, 0}, pe[2] = {0, 0}, xacc[2][D];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int f = 0; f < D; ++f) xacc[q][f] = 0.0;
+  for (int64_t j0 = 0; j0 < n; j0 += TCJ) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < TCJ * D; e += 256) {
+      const int64_t j = j0 + e / D;
+      xs[e / D][e % D] = j < n ? xb[j * D + e % D] : 0.0;
+    }
+    for (int e = threadIdx.x; e < TCJ; e += 256) ss[e] = (j0 + e < n) ? sb[j0 + e] : 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < TCJ / 32; ++k) {
+      const int jj = lane + 32 * k;
+      const int64_t j = j0 + jj;
+      if (j >= n) continue;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int64_t i = ii[q];
+        if (i >= n) continue;
+        double g = 0.0;
+#pragma unroll
+        for (int f = 0; f < D; ++f) g += xi[q][f] * xs[jj][f];
+        const double dist = (si[q] + ss[jj]) - 2.0 * g;
+        const double Dv = dist / two_ell2;
+        const double E = exp(-Dv);
+        double* ap = a + (b * n + i) * n + j;
+        if constexpr (FWD) {
+          double v = sigma2 * E;
+          if (j == i) v += lam;
+          *ap = v;
+        } else {
+          const double kb = abar[(b * n + i) * n + j];
+          ps[q] += kb * E;
+          const double nb = kb * sigma2 * E;
+          pe[q] += nb * Dv;
+          if (j == i) pl[q] += kb;
+          if (xbar) {
+            const double w = -nb / two_ell2;
+#pragma unroll
+            for (int f = 0; f < D; ++f) xacc[q][f] += w * (xi[q][f] - xs[jj][f]);
+          }
+        }
+      }
+    }
+  }
+  if constexpr (!FWD) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      double v0 = ps[q], v1 = pl[q], v2 = pe[q];
+      for (int o = 16; o; o >>= 1) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+        v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+      }
+      double xv[D];
+#pragma unroll
+      for (int f = 0; f < D; ++f) {
+        double t = xacc[q][f];
+        for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        xv[f] = t;
+      }
+      const int64_t i = ii[q];
+      if (lane == 0 && i < n) {
+        part[(b * n + i) * 3 + 0] = v0;
+        part[(b * n + i) * 3 + 1] = v1;
+        part[(b * n + i) * 3 + 2] = v2;
+        if (xbar)
+#pragma unroll
+          for (int f = 0; f < D; ++f) xbar[(b * n + i) * D + f] = 4.0 * xv[f];
+      }
+    }
+  }
+}
+
+template <bool FWD>
+bool launch_tiled(int64_t d, int64_t batch, int64_t n, const double* x, const double* s, double sigma2,
+                  double two_ell2, double lam, double* a, const double* abar, double* xbar, double* part,
+                  cudaStream_t st) {
+  const unsigned grid = (unsigned)(batch * ((n + TRW - 1) / TRW));
+#define DLAB_RBF_CASE(DD)                                                                                  \
+  case DD:                                                                                                 \
+    k_rbf_tiled<DD, FWD><<<grid, 256, 0, st>>>(n, x, s, sigma2, two_ell2, lam, a, abar, xbar, part);      \
+    return true;
+  switch (d) {
+    DLAB_RBF_CASE(1)
+    DLAB_RBF_CASE(2)
+    DLAB_RBF_CASE(3)
+    DLAB_RBF_CASE(4)
+    DLAB_RBF_CASE(8)
+    DLAB_RBF_CASE(16)
+    default:
+      return false;
+  }
+#undef DLAB_RBF_CASE
+}
+
 // Fixed-order finalization per slice: grads w.r.t. (log sigma2, log ell2, log lam).
 __global__ void k_rbf_finalize(int64_t batch, int64_t n, const double* part, double sigma2, double ell2,
                                double lam, double two_ell2, double* grads) {
@@ -177,7 +303,8 @@ dla_status dla_gp_rbf_fwd_f64(int64_t batch, int64_t n, int64_t d, const double*
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   double* sq = static_cast<double*>(ws);
   k_rowsq<<<blocks_for(batch * n, 256), 256, 0, s>>>(batch, n, d, x, sq);
-  k_rbf_fwd<<<(unsigned)(batch * n), RT, 0, s>>>(n, d, x, sq, sigma2, ell2 * 2.0, lam, a);
+  if (!launch_tiled<true>(d, batch, n, x, sq, sigma2, ell2 * 2.0, lam, a, nullptr, nullptr, nullptr, s))
+    k_rbf_fwd<<<(unsigned)(batch * n), RT, 0, s>>>(n, d, x, sq, sigma2, ell2 * 2.0, lam, a);
   note_launch(1);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
@@ -193,7 +320,8 @@ dla_status dla_gp_rbf_bwd_f64(int64_t batch, int64_t n, int64_t d, const double*
   double* sq = static_cast<double*>(ws);
   double* part = sq + batch * n;
   k_rowsq<<<blocks_for(batch * n, 256), 256, 0, s>>>(batch, n, d, x, sq);
-  k_rbf_bwd<<<(unsigned)(batch * n), RT, 0, s>>>(n, d, x, sq, sigma2, ell2 * 2.0, abar, xbar, part);
+  if (!launch_tiled<false>(d, batch, n, x, sq, sigma2, ell2 * 2.0, lam, nullptr, abar, xbar, part, s))
+    k_rbf_bwd<<<(unsigned)(batch * n), RT, 0, s>>>(n, d, x, sq, sigma2, ell2 * 2.0, abar, xbar, part);
   k_rbf_finalize<<<(unsigned)batch, RT, 0, s>>>(batch, n, part, sigma2, ell2, lam, ell2 * 2.0, grads);
   note_launch(2);
   DLAB_LAUNCH_CHECK();
