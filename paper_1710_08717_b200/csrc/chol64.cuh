@@ -1,13 +1,8 @@
-// Cholesky of one n <= 64 block held in shared memory by a CTA of >= 64
-// threads (dl/cholesky.hpp:35-72 reordered for the GPU).
+// Cholesky of one n <= NMAX (64 or 128) block held in shared memory by a CTA
+// of >= 64 threads (dl/cholesky.hpp:35-72 reordered for the GPU).
 //
 // The pivot chain is the critical path of any Cholesky (n dependent
-// sqrt/div pairs).  Here it never crosses a block barrier: the block is
-// processed in 16-column panels, each factored by ONE warp entirely in
-// registers (lane l holds panel rows l and l + 32; pivots and multipliers move
-// by warp shuffles; every lane takes the sqrt and the reciprocal itself), and
-// the CTA's warps then apply the panel to the trailing lower triangle with
-// plain DFMA.  Two barriers per 16 columns instead of one per column.
+// sqrt/div pairs).  Here it never crosses a block barrier: see chol_smem.
 #pragma once
 
 #include "common.cuh"
@@ -17,12 +12,13 @@ namespace dlab {
 constexpr int CH_LD = 65;  // smem row stride for a 64 x 64 block
 
 // Column J of a W-wide register panel (template recursion keeps every
-// register index a compile-time constant).  Straight-line: a failed pivot is
-// only recorded; the NaNs it creates never leave the CTA.
-template <typename T, int W, int J>
-__device__ __forceinline__ void panel_cols(T (&r0)[W], T (&r1)[W], int lane, int w, int p0, int& failed) {
+// register index a compile-time constant).  Lane l holds panel rows
+// p0 + l + 32 q in slot q.  Straight-line: a failed pivot is only recorded;
+// the NaNs it creates never leave the CTA.
+template <typename T, int W, int Q, int J>
+__device__ __forceinline__ void panel_cols(T (&r)[Q][W], int lane, int w, int p0, int& failed) {
   if constexpr (J < W) {
-    const T d = __shfl_sync(0xffffffffu, r0[J], J);  // pivot row p0 + J lives on lane J
+    const T d = __shfl_sync(0xffffffffu, r[0][J], J);  // pivot row p0 + J lives on lane J
     if (!(d > T(0)) && failed < 0 && J < w) failed = p0 + J;
     // 1/sqrt(d) directly (one MUFU + Newton, ~75 cycles) keeps the serial
     // pivot chain short; L(J,J) = d * (1/sqrt d) is off the chain.  Differs
@@ -30,26 +26,73 @@ __device__ __forceinline__ void panel_cols(T (&r0)[W], T (&r1)[W], int lane, int
     const T inv = Num<T>::rsqrt_(d);
     const T rt = d * inv;
     // column J: L(i, J) = a(i, J) / L(J, J) for rows below the pivot
-    const T l0 = (lane > J) ? r0[J] * inv : (lane == J ? rt : r0[J]);
-    const T l1 = r1[J] * inv;
-    r0[J] = l0;
-    r1[J] = l1;
+    T l[Q];
+    l[0] = (lane > J) ? r[0][J] * inv : (lane == J ? rt : r[0][J]);
+#pragma unroll
+    for (int q = 1; q < Q; ++q) l[q] = r[q][J] * inv;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) r[q][J] = l[q];
 #pragma unroll
     for (int k = J + 1; k < W; ++k) {
-      const T lkj = __shfl_sync(0xffffffffu, l0, k);  // L(p0 + k, J) on lane k
-      if (lane >= k) r0[k] -= l0 * lkj;              // rows at/below the diagonal of col k
-      r1[k] -= l1 * lkj;
+      const T lkj = __shfl_sync(0xffffffffu, l[0], k);  // L(p0 + k, J) on lane k
+      if (lane >= k) r[0][k] -= l[0] * lkj;            // rows at/below the diagonal of col k
+#pragma unroll
+      for (int q = 1; q < Q; ++q) r[q][k] -= l[q] * lkj;
     }
-    panel_cols<T, W, J + 1>(r0, r1, lane, w, p0, failed);
+    panel_cols<T, W, Q, J + 1>(r, lane, w, p0, failed);
   }
 }
 
-// S: n x n block in shared memory (row stride CH_LD), lower triangle valid.
-// On return S holds L in its lower triangle.  Returns the first failing pivot
-// (uniform across the CTA) or -1.  `flag` is one shared int.
-template <typename T>
-__device__ __forceinline__ int chol_smem64(T* S, int n, int* flag) {
-  constexpr int W = 16;
+// One warp factors the W-wide panel at column p0 (rows p0 .. n-1, Q slots of
+// 32 rows per lane) in registers and writes it back.  Returns the failing
+// pivot or -1.
+template <typename T, int LD, int W, int Q>
+__device__ __forceinline__ int panel_warp(T* S, int n, int p0, int w, int lane) {
+  T r[Q][W];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int i = p0 + lane + 32 * q;
+#pragma unroll
+    for (int c = 0; c < W; ++c) r[q][c] = (i < n && c < w) ? S[i * LD + p0 + c] : T(0);
+  }
+  // The padded columns of a narrow last panel factor an identity block.
+#pragma unroll
+  for (int c = 0; c < W; ++c)
+    if (c >= w && lane == c) r[0][c] = T(1);
+  int failed = -1;
+  panel_cols<T, W, Q, 0>(r, lane, w, p0, failed);
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int i = p0 + lane + 32 * q;
+#pragma unroll
+    for (int c = 0; c < W; ++c)
+      if (c < w && i < n && (q > 0 || lane >= c)) S[i * LD + p0 + c] = r[q][c];
+  }
+  return failed;
+}
+
+// Dispatch on the number of live 32-row slots (the panel shrinks as p0
+// advances; dead slots would only burn the serial chain).
+template <typename T, int LD, int W, int Q>
+__device__ __forceinline__ int panel_warp_n(T* S, int n, int p0, int w, int lane, int qa) {
+  if constexpr (Q > 1) {
+    if (qa < Q) return panel_warp_n<T, LD, W, Q - 1>(S, n, p0, w, lane, qa);
+  }
+  return panel_warp<T, LD, W, Q>(S, n, p0, w, lane);
+}
+
+// S: n x n block in shared memory (row stride NMAX + 1), n <= NMAX, lower
+// triangle valid.  On return S holds L in its lower triangle.  Returns the
+// first failing pivot (uniform across the CTA) or -1.  `flag` is one shared
+// int.  Processed in 16-column panels, each factored by ONE warp entirely in
+// registers (pivots and multipliers move by warp shuffles; every lane takes
+// the reciprocal square root itself); the CTA's warps then apply the panel to
+// the trailing lower triangle (8 x 8 DMMA tiles for f64).  Two barriers per
+// 16 columns instead of one per column.
+template <typename T, int NMAX>
+__device__ __forceinline__ int chol_smem(T* S, int n, int* flag) {
+  constexpr int W = 16, LD = NMAX + 1, Q = NMAX / 32;
+  static_assert(NMAX % 32 == 0, "32-row slots");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nthreads = blockDim.x;
   if (threadIdx.x == 0) *flag = -1;
@@ -57,27 +100,7 @@ __device__ __forceinline__ int chol_smem64(T* S, int n, int* flag) {
   for (int p0 = 0; p0 < n; p0 += W) {
     const int w = min(W, n - p0);  // panel width
     if (warp == 0) {
-      // panel rows p0 + lane (slot 0) and p0 + lane + 32 (slot 1)
-      T r0[W], r1[W];
-      const int i0 = p0 + lane, i1 = p0 + lane + 32;
-#pragma unroll
-      for (int c = 0; c < W; ++c) {
-        r0[c] = (i0 < n && c < w) ? S[i0 * CH_LD + p0 + c] : T(0);
-        r1[c] = (i1 < n && c < w) ? S[i1 * CH_LD + p0 + c] : T(0);
-      }
-      int failed = -1;
-      // The padded columns of a narrow last panel factor an identity block.
-#pragma unroll
-      for (int c = 0; c < W; ++c)
-        if (c >= w && lane == c) r0[c] = T(1);
-      panel_cols<T, W, 0>(r0, r1, lane, w, p0, failed);
-#pragma unroll
-      for (int c = 0; c < W; ++c) {
-        if (c < w) {
-          if (i0 < n && lane >= c) S[i0 * CH_LD + p0 + c] = r0[c];
-          if (i1 < n) S[i1 * CH_LD + p0 + c] = r1[c];
-        }
-      }
+      const int failed = panel_warp_n<T, LD, W, Q>(S, n, p0, w, lane, (n - p0 + 31) >> 5);
       if (lane == 0 && failed >= 0) *flag = failed;
     }
     __syncthreads();
@@ -100,13 +123,13 @@ __device__ __forceinline__ int chol_smem64(T* S, int n, int* flag) {
 #pragma unroll
           for (int kk = 0; kk < W; kk += 4) {
             const bool ok = kk + fc < w;
-            const double af = ok ? S[(t0 + 8 * a + fr) * CH_LD + p0 + kk + fc] : 0.0;
-            const double bf = ok ? S[(t0 + 8 * b + fr) * CH_LD + p0 + kk + fc] : 0.0;
+            const double af = ok ? S[(t0 + 8 * a + fr) * LD + p0 + kk + fc] : 0.0;
+            const double bf = ok ? S[(t0 + 8 * b + fr) * LD + p0 + kk + fc] : 0.0;
             asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                          : "+d"(c0), "+d"(c1)
                          : "d"(af), "d"(bf));
           }
-          T* crow = S + (t0 + 8 * a + fr) * CH_LD + t0 + 8 * b + 2 * fc;
+          T* crow = S + (t0 + 8 * a + fr) * LD + t0 + 8 * b + 2 * fc;
           crow[0] -= c0;
           crow[1] -= c1;
         }
@@ -114,13 +137,13 @@ __device__ __forceinline__ int chol_smem64(T* S, int n, int* flag) {
         for (int e = threadIdx.x; e < m * m; e += nthreads) {
           const int i = t0 + e / m, k = t0 + e % m;
           if (k > i) continue;
-          const T* li = S + i * CH_LD + p0;
-          const T* lk = S + k * CH_LD + p0;
-          T acc = S[i * CH_LD + k];
+          const T* li = S + i * LD + p0;
+          const T* lk = S + k * LD + p0;
+          T acc = S[i * LD + k];
 #pragma unroll
           for (int c = 0; c < W; ++c)
             if (c < w) acc -= li[c] * lk[c];
-          S[i * CH_LD + k] = acc;
+          S[i * LD + k] = acc;
         }
       }
     }
@@ -129,23 +152,38 @@ __device__ __forceinline__ int chol_smem64(T* S, int n, int* flag) {
   return -1;
 }
 
+template <typename T>
+__device__ __forceinline__ int chol_smem64(T* S, int n, int* flag) {
+  return chol_smem<T, 64>(S, n, flag);
+}
+
 // Forward substitution S y = v for nv <= 64 vectors held vector-major in
-// shared memory (V[v * CH_LD + i]); S lower triangular, 64 x 64 (zero padded
-// beyond nb), rd[i] = 1 / S(i,i).  8-row blocks: the 8 x 8 diagonal block is
+// shared memory (V[v * LD + i]); S lower triangular, nb x nb at row stride
+// LD, rd[i] = 1 / S(i,i).  8-row blocks: the 8 x 8 diagonal block is
 // solved per vector (one thread per vector), the rows below are updated by an
 // (rows x 8) x (8 x 64) FP64 DMMA product.  Needs >= 64 threads, ends synced.
-template <typename T>
+template <typename T, int LD = CH_LD>
 __device__ __forceinline__ void blocked_fwd_subst(const T* S, T* V, const T* rd, int nb, int nv) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, fr = lane >> 2, fc = lane & 3;
   const int nw = blockDim.x >> 5;
   for (int c0 = 0; c0 < nb; c0 += 8) {
     if (tid < nv) {
-      T* xv = V + tid * CH_LD;
-      for (int i = c0; i < c0 + 8 && i < nb; ++i) {
-        T acc = xv[i];
-        for (int p = c0; p < i; ++p) acc -= S[i * CH_LD + p] * xv[p];
-        xv[i] = acc * rd[i];
+      // right-looking in registers: the serial chain is one multiply and one
+      // FMA per row; the S loads are independent of it
+      T* xv = V + tid * LD;
+      T x[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) x[r] = (c0 + r < nb) ? xv[c0 + r] : T(0);
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        x[p] *= (c0 + p < nb) ? rd[c0 + p] : T(0);
+#pragma unroll
+        for (int i = p + 1; i < 8; ++i)
+          if (c0 + i < nb) x[i] -= S[(c0 + i) * LD + c0 + p] * x[p];
       }
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (c0 + r < nb) xv[c0 + r] = x[r];
     }
     __syncthreads();
     const int r0 = c0 + 8;
@@ -156,22 +194,22 @@ __device__ __forceinline__ void blocked_fwd_subst(const T* S, T* V, const T* rd,
         double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
         for (int kk = 0; kk < 8; kk += 4) {
-          const double af = S[(rt + fr) * CH_LD + c0 + kk + fc];
-          const double bf = V[(nt + fr) * CH_LD + c0 + kk + fc];
+          const double af = S[(rt + fr) * LD + c0 + kk + fc];
+          const double bf = V[(nt + fr) * LD + c0 + kk + fc];
           asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                        : "+d"(acc0), "+d"(acc1)
                        : "d"(af), "d"(bf));
         }
-        V[(nt + 2 * fc) * CH_LD + rt + fr] -= acc0;
-        V[(nt + 2 * fc + 1) * CH_LD + rt + fr] -= acc1;
+        V[(nt + 2 * fc) * LD + rt + fr] -= acc0;
+        V[(nt + 2 * fc + 1) * LD + rt + fr] -= acc1;
       }
     } else {
       for (int e = tid; e < rtiles * 8 * 64; e += blockDim.x) {
         const int r = r0 + e / 64, v = e % 64;
         T acc = T(0);
 #pragma unroll
-        for (int p = 0; p < 8; ++p) acc += S[r * CH_LD + c0 + p] * V[v * CH_LD + c0 + p];
-        V[v * CH_LD + r] -= acc;
+        for (int p = 0; p < 8; ++p) acc += S[r * LD + c0 + p] * V[v * LD + c0 + p];
+        V[v * LD + r] -= acc;
       }
     }
     __syncthreads();

@@ -1,4 +1,5 @@
-// Fused small-matrix kernels (n <= 64): one CTA per matrix, the whole
+// Fused small-matrix kernels (n <= 64): one warp (n <= 32) or one CTA per
+// matrix, the whole
 // operator chain in shared memory, one HBM read of each input and one write
 // of each output.  This is the batched small-n regime of the north star
 // (C1: batch 64 x 32^2; any batch x n <= 64).
@@ -124,6 +125,285 @@ __global__ void __launch_bounds__(256) k_potrf_bwd_small(int n, MatB<T> abar, Ma
   }
 }
 
+// ----------------------------------------------------------- n <= 32: a warp
+// per matrix.  4-8 matrices per CTA, no block barriers: each warp loads its
+// matrix with coalesced 32-lane sweeps into a private shared tile and holds
+// one row (forward) or one column (backward) per lane in registers.  Values
+// every lane needs (a column's multipliers, rows of L) are broadcast from
+// shared memory with 16-byte loads: at 65536 matrices the kernels are bound
+// by shared-memory instruction issue, and one LDS.128 carries 2 doubles where
+// a 64-bit shuffle costs two SHFLs per value.
+constexpr int WN = 32;
+constexpr int WLD = WN + 1;  // column-per-lane tiles: conflict-free rows and columns
+
+template <typename T>
+struct Bc;
+template <>
+struct Bc<double> {
+  static constexpr int N = 2;
+  static constexpr int LLD = 34;  // broadcast tiles: 16-byte aligned rows
+  __device__ static void ld(const double* p, double (&v)[2]) {
+    const double2 t = *reinterpret_cast<const double2*>(p);
+    v[0] = t.x;
+    v[1] = t.y;
+  }
+};
+template <>
+struct Bc<float> {
+  static constexpr int N = 4;
+  static constexpr int LLD = 36;
+  __device__ static void ld(const float* p, float (&v)[4]) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    v[0] = t.x;
+    v[1] = t.y;
+    v[2] = t.z;
+    v[3] = t.w;
+  }
+};
+
+// warps (matrices) per CTA: keeps the per-CTA tile within 70 KB
+template <typename T>
+constexpr int wpc_fwd() { return 8; }
+template <typename T>
+constexpr int wpc_bwd() { return sizeof(T) == 8 ? 4 : 8; }
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Column J of the row-per-lane Cholesky (dl/cholesky.hpp:35-72): the pivot
+// moves by one shuffle, the column's multipliers through a double-buffered
+// shared vector (one __syncwarp per column).
+template <typename T, int J>
+__device__ __forceinline__ void wchol_col(T (&r)[WN], int lane, int n, T* buf, int& failed) {
+  if constexpr (J < WN) {
+    const T d = __shfl_sync(0xffffffffu, r[J], J);
+    if (!(d > T(0)) && failed < 0 && J < n) failed = J;
+    const T inv = Num<T>::rsqrt_(d);
+    const T rt = d * inv;
+    const T l = (lane > J) ? r[J] * inv : (lane == J ? rt : r[J]);
+    r[J] = l;
+    if constexpr (J + 1 < WN) {
+      constexpr int VN = Bc<T>::N;
+      T* cb = buf + (J & 1) * WN;
+      cb[lane] = l;
+      __syncwarp();
+#pragma unroll
+      for (int k0 = ((J + 1) / VN) * VN; k0 < WN; k0 += VN) {
+        T v[VN];
+        Bc<T>::ld(cb + k0, v);
+#pragma unroll
+        for (int u = 0; u < VN; ++u)  // lanes above row k0+u only touch unused upper entries
+          if (k0 + u > J) r[k0 + u] -= l * v[u];
+      }
+    }
+    wchol_col<T, J + 1>(r, lane, n, buf, failed);
+  }
+}
+
+template <typename T, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_potrf_warp(int n, int64_t batch, MatB<T> a, bool lower,
+                                                          int32_t* info) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b = (int64_t)blockIdx.x * wpc_fwd<T>() + warp;
+  if (b >= batch) return;
+  T* S = reinterpret_cast<T*>(smem_raw) + warp * (WN * WLD + 2 * WN + 4);
+  T* buf = S + WN * WLD;  // 16-byte aligned: (WN * WLD) and the per-warp stride are multiples of 16 bytes
+  const T* g = a.at(b, 0, 0);
+  const int ld = (int)a.ld;  // 32-bit in-matrix offsets (64-bit only for the slice base)
+  {
+    T v[WN];  // all rows in flight at once, one coalesced row per load
+#pragma unroll
+    for (int i = 0; i < WN; ++i) v[i] = (i < n && lane < n) ? g[i * ld + lane] : T(0);
+#pragma unroll
+    for (int i = 0; i < WN; ++i)
+      if (i < n) S[i * WLD + lane] = v[i];
+  }
+  __syncwarp();
+  // symmetry precheck (same rule as k_potrf_small): row `lane` against column `lane`
+  T mabs = T(0), masym = T(0);
+  if (lane < n)
+    for (int j = 0; j < n; ++j) {
+      const T v = S[lane * WLD + j];
+      if (fabs(v) > mabs) mabs = fabs(v);
+      if (j > lane) {
+        const T d = fabs(v - S[j * WLD + lane]);
+        if (d > masym) masym = d;
+      }
+    }
+  mabs = warp_max(mabs);
+  masym = warp_max(masym);
+  if (masym > Num<T>::sym_rtol * (mabs > T(0) ? mabs : T(1))) {
+    if (lane == 0) record_failure(info, b, DLA_ERR_ASYMMETRIC, 0);
+    return;
+  }
+  // row `lane` of the lower triangle; rows >= n factor an identity block
+  T r[WN];
+#pragma unroll
+  for (int c = 0; c < WN; ++c) r[c] = (lane < n && c <= lane) ? S[lane * WLD + c] : (c == lane ? T(1) : T(0));
+  int failed = -1;
+  wchol_col<T, 0>(r, lane, n, buf, failed);
+  if (failed >= 0) {
+    if (lane == 0) record_failure(info, b, DLA_ERR_NOT_SPD, failed);
+    return;
+  }
+  T* o = a.at(b, 0, 0);
+  if (!lower) {  // R(i, lane) = L(lane, i): straight from this lane's registers
+#pragma unroll
+    for (int i = 0; i < WN; ++i)
+      if (i < n && lane < n) o[i * ld + lane] = i <= lane ? r[i] : T(0);
+    return;
+  }
+#pragma unroll
+  for (int c = 0; c < WN; ++c)
+    if (c < n && lane < n) S[lane * WLD + c] = r[c];
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < WN; ++i)
+    if (i < n && lane < n) o[i * ld + lane] = lane <= i ? S[i * WLD + lane] : T(0);
+}
+
+// Column `lane` of L^{-T} M held in registers, in unit-diagonal form: the
+// caller has already scaled x by D^{-1} (x_i = m_i / L_ii, off the chain) and
+// Ls holds L with every column divided by its diagonal, so
+// x_m -= Ls(i, m) x_i for m < i, rows i descending, is the whole back
+// substitution — one FMA per row on the serial chain, and row i of Ls is one
+// broadcast sweep.
+template <typename T>
+__device__ __forceinline__ void warp_ltinv_col(const T* Ls, T (&x)[WN], int n) {
+  constexpr int VN = Bc<T>::N, LLD = Bc<T>::LLD;
+#pragma unroll
+  for (int i = WN - 1; i >= 1; --i) {
+    if (i < n) {
+      const T xi = x[i];
+#pragma unroll
+      for (int m0 = 0; m0 < i; m0 += VN) {
+        T v[VN];
+        Bc<T>::ld(Ls + i * LLD + m0, v);
+#pragma unroll
+        for (int u = 0; u < VN; ++u)
+          if (m0 + u < i) x[m0 + u] -= v[u] * xi;
+      }
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(wpc_bwd<T>() * 32, sizeof(T) == 8 ? 3 : 2) k_potrf_bwd_warp(int n, int64_t batch,
+                                                                                      MatB<T> abar,
+                                                                                      MatB<const T> lbar,
+                                                                                      MatB<const T> l, bool lower) {
+  constexpr int VN = Bc<T>::N, LLD = Bc<T>::LLD;
+  constexpr int per_warp = WN * LLD + WN * WLD + 2 * WN + 4;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b = (int64_t)blockIdx.x * wpc_bwd<T>() + warp;
+  if (b >= batch) return;
+  T* L = reinterpret_cast<T*>(smem_raw) + warp * per_warp;  // 16-byte aligned (per_warp * sizeof(T) % 16 == 0)
+  T* W = L + WN * LLD;
+  T* rd = W + WN * WLD;
+  // lower views: L = R^T, Lbar = Rbar^T for the upper variant (dl/adjoints.hpp:183-188)
+  const T* gl = l.at(b, 0, 0);
+  const T* gg = lbar.at(b, 0, 0);
+  const int ldl = (int)l.ld, ldg = (int)lbar.ld, ldo = (int)abar.ld;  // 32-bit in-matrix offsets
+  // Unit-diagonal form: Ls = L D^{-1} (column j divided by L_jj, unit
+  // diagonal), scaled on the way into shared memory; dg / rd keep D and D^{-1}.
+  T* dg = rd + WN;
+  {
+    const T d = lane < n ? gl[lane * ldl + lane] : T(1);
+    dg[lane] = d;
+    rd[lane] = T(1) / d;
+  }
+  __syncwarp();
+  const T r_own = rd[lane];
+#pragma unroll
+  for (int i0 = 0; i0 < WN; i0 += 16) {  // 32 coalesced row loads in flight per lane
+    T lv[16], gv[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int i = i0 + u;
+      lv[u] = (i < n && lane < n) ? gl[i * ldl + lane] : T(0);
+      gv[u] = (i < n && lane < n) ? gg[i * ldg + lane] : T(0);
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int i = i0 + u;
+      if (i < n) {
+        if (lower) {  // element (i, lane) of L, column `lane`
+          L[i * LLD + lane] = lane < i ? lv[u] * r_own : (lane == i ? T(1) : T(0));
+          W[i * WLD + lane] = gv[u];
+        } else {  // element (lane, i) of the lower view, column i
+          L[lane * LLD + i] = i < lane ? lv[u] * rd[i] : (i == lane ? T(1) : T(0));
+          W[lane * WLD + i] = gv[u];
+        }
+      }
+    }
+  }
+  __syncwarp();
+  // Phi = copyltu(L^T Lbar), lower part of column `lane`: Phi_ij = sum_{k>=i} L_ki Lbar_kj
+  // (i >= j = lane) = L_ii (Lbar_ij + sum_{k>i} Ls_ki Lbar_kj), accumulated row by row of Ls
+  T acc[WN];
+#pragma unroll
+  for (int i = 0; i < WN; ++i) acc[i] = T(0);
+#pragma unroll
+  for (int k = 0; k < WN; ++k) {
+    if (k < n) {
+      const T xk = lane < n ? W[k * WLD + lane] : T(0);
+      acc[k] += xk;  // unit diagonal
+#pragma unroll
+      for (int i0 = 0; i0 < k; i0 += VN) {
+        T v[VN];
+        Bc<T>::ld(L + k * LLD + i0, v);
+#pragma unroll
+        for (int u = 0; u < VN; ++u)
+          if (i0 + u < k) acc[i0 + u] += v[u] * xk;
+      }
+    }
+  }
+  __syncwarp();
+  // mirror into W: W(i, j) = W(j, i) = Phi_ij
+#pragma unroll
+  for (int i = 0; i < WN; ++i)
+    if (i < n && lane < n && i >= lane) {
+      const T p = acc[i] * dg[i];
+      W[i * WLD + lane] = p;
+      W[lane * WLD + i] = p;
+    }
+  __syncwarp();
+  T x[WN];
+#pragma unroll
+  for (int i = 0; i < WN; ++i) x[i] = (i < n && lane < n) ? W[i * WLD + lane] * rd[i] : T(0);
+  // X = L^{-T} Phi (column `lane`), then through shared memory X^T = Phi L^{-1}
+  warp_ltinv_col<T>(L, x, n);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < WN; ++i)
+    if (i < n && lane < n) W[i * WLD + lane] = x[i];
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < WN; ++i) x[i] = (i < n && lane < n) ? W[lane * WLD + i] * rd[i] : T(0);
+  // Y = L^{-T} (Phi L^{-1}) = L^{-T} Phi L^{-1}; column `lane`
+  warp_ltinv_col<T>(L, x, n);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < WN; ++i)
+    if (i < n && lane < n) W[i * WLD + lane] = x[i];
+  __syncwarp();
+  // Abar = sym(Y / 2), exactly symmetric: element (i, lane) pairs this lane's
+  // Y(i, lane) with Y(lane, i) from shared memory
+  T* o = abar.at(b, 0, 0);
+#pragma unroll
+  for (int i = 0; i < WN; ++i)
+    if (i < n && lane < n) {
+      const T hi = x[i] * T(0.5), hj = W[lane * WLD + i] * T(0.5);
+      o[i * ldo + lane] = (i == lane) ? hi : (hi + hj) * T(0.5);  // == (hi + hj) / 2 exactly
+    }
+}
+
 }  // namespace
 
 template <typename T>
@@ -133,6 +413,27 @@ bool potrf_small_eligible(int64_t n) {
 
 template <typename T>
 dla_status potrf_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool lower) {
+  if (n <= WN) {
+    constexpr int wpc = wpc_fwd<T>();
+    const size_t sm = sizeof(T) * wpc * (WN * WLD + 2 * WN + 4);
+    static const int minb = [] {
+      const char* e = getenv("DLA_WARP_MINB");  // tuning switch: 1 = no register cap
+      return e ? atoi(e) : 2;
+    }();
+    static bool once = false;
+    if (!once) {
+      cudaFuncSetAttribute(k_potrf_warp<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      cudaFuncSetAttribute(k_potrf_warp<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      once = true;
+    }
+    const unsigned grid = (unsigned)((batch + wpc - 1) / wpc);
+    if (minb == 1)
+      k_potrf_warp<T, 1><<<grid, wpc * 32, sm, c.stream>>>((int)n, batch, a, lower, c.info);
+    else
+      k_potrf_warp<T, 2><<<grid, wpc * 32, sm, c.stream>>>((int)n, batch, a, lower, c.info);
+    DLAB_LAUNCH_CHECK();
+    return DLA_OK;
+  }
   k_potrf_small<T><<<(unsigned)batch, 256, 0, c.stream>>>((int)n, a, lower, c.info);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
@@ -141,6 +442,19 @@ dla_status potrf_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool l
 template <typename T>
 dla_status potrf_bwd_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> lbar,
                            MatB<const T> l, bool lower) {
+  if (n <= WN) {
+    constexpr int wpc = wpc_bwd<T>();
+    const size_t sm = sizeof(T) * wpc * (WN * Bc<T>::LLD + WN * WLD + 2 * WN + 4);
+    static bool once = false;
+    if (!once) {
+      cudaFuncSetAttribute(k_potrf_bwd_warp<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      once = true;
+    }
+    k_potrf_bwd_warp<T><<<(unsigned)((batch + wpc - 1) / wpc), wpc * 32, sm, c.stream>>>((int)n, batch, abar, lbar,
+                                                                                        l, lower);
+    DLAB_LAUNCH_CHECK();
+    return DLA_OK;
+  }
   const size_t sm = sizeof(T) * 3 * SN * SLD;
   static bool once = false;
   if (!once) {

@@ -462,53 +462,54 @@ dla_status potrf_rec(const Ctx& c, int64_t batch, int64_t n, int64_t k0, MatB<T>
 }
 
 // One block column of the right-looking Cholesky in ONE launch: every CTA
-// factors the 64 x 64 diagonal block (redundantly — it is latency, not
+// factors the NBP x NBP diagonal block (redundantly — it is latency, not
 // work), CTA 0 stores L11, and each CTA solves its own 64 rows of the panel
 // A21 <- A21 L11^{-T} in shared memory (blocked substitution + DMMA).
-template <typename T>
-__global__ void __launch_bounds__(256) k_potrf_panel(int nb, int64_t rest, int64_t k0, MatB<T> akk, MatB<T> a21,
+template <typename T, int NBP>
+__global__ void __launch_bounds__(256, 1) k_potrf_panel(int nb, int64_t rest, int64_t k0, MatB<T> akk, MatB<T> a21,
                                                      int32_t* info) {
+  constexpr int LD = NBP + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* S = reinterpret_cast<T*>(smem_raw);
-  T* V = S + 64 * CH_LD;
-  T* rd = V + 64 * CH_LD;
+  T* V = S + NBP * LD;
+  T* rd = V + 64 * LD;
   __shared__ int flag;
   const int64_t chunks = rest > 0 ? (rest + 63) / 64 : 1;
   const int64_t b = blockIdx.x / chunks, cid = blockIdx.x % chunks;
   if (slice_failed(info, b)) return;
   const int tid = threadIdx.x;
   T* base = akk.at(b, 0, 0);
-  for (int e0 = tid; e0 < 64 * 64; e0 += 8 * 256) {
+  for (int e0 = tid; e0 < NBP * NBP; e0 += 8 * 256) {
     T v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int e = e0 + u * 256, i = e / 64, j = e % 64;
+      const int e = e0 + u * 256, i = e / NBP, j = e % NBP;
       v[u] = (i < nb && j <= i) ? base[i * akk.ld + j] : T(0);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int e = e0 + u * 256;
-      S[(e / 64) * CH_LD + e % 64] = v[u];
+      S[(e / NBP) * LD + e % NBP] = v[u];
     }
   }
   const int64_t r0 = cid * 64;
   const int nv = rest > 0 ? (int)min((int64_t)64, rest - r0) : 0;
   T* pan = a21.at(b, r0, 0);
-  for (int e0 = tid; e0 < 64 * 64; e0 += 8 * 256) {  // panel rows, loads in flight during the factorization
+  for (int e0 = tid; e0 < 64 * NBP; e0 += 8 * 256) {  // panel rows, loads in flight during the factorization
     T v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int e = e0 + u * 256, vv = e / 64, i = e % 64;
+      const int e = e0 + u * 256, vv = e / NBP, i = e % NBP;
       v[u] = (vv < nv && i < nb) ? pan[vv * a21.ld + i] : T(0);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int e = e0 + u * 256;
-      V[(e / 64) * CH_LD + e % 64] = v[u];
+      V[(e / NBP) * LD + e % NBP] = v[u];
     }
   }
   __syncthreads();
-  const int failed = chol_smem64<T>(S, nb, &flag);
+  const int failed = chol_smem<T, NBP>(S, nb, &flag);
   if (failed >= 0) {
     if (cid == 0 && tid == 0) record_failure(info, b, DLA_ERR_NOT_SPD, k0 + failed);
     return;
@@ -516,32 +517,38 @@ __global__ void __launch_bounds__(256) k_potrf_panel(int nb, int64_t rest, int64
   if (cid == 0)
     for (int e = tid; e < nb * nb; e += 256) {
       const int i = e / nb, j = e % nb;
-      base[i * akk.ld + j] = j <= i ? S[i * CH_LD + j] : T(0);
+      base[i * akk.ld + j] = j <= i ? S[i * LD + j] : T(0);
     }
   if (nv == 0) return;
-  if (tid < 64) rd[tid] = tid < nb ? T(1) / S[tid * CH_LD + tid] : T(1);
+  for (int i = tid; i < NBP; i += 256) rd[i] = i < nb ? T(1) / S[i * LD + i] : T(1);
   __syncthreads();
-  blocked_fwd_subst<T>(S, V, rd, nb, nv);  // row v: L11 x = a  <=>  x^T L11^T = a^T
+  blocked_fwd_subst<T, LD>(S, V, rd, nb, nv);  // row v: L11 x = a  <=>  x^T L11^T = a^T
   for (int e = tid; e < nv * nb; e += 256) {
     const int vv = e / nb, i = e % nb;
-    pan[vv * a21.ld + i] = V[vv * CH_LD + i];
+    pan[vv * a21.ld + i] = V[vv * LD + i];
   }
 }
 
 // Side stream + event pool for the look-ahead (created once per process;
 // growth happens outside any hot loop).
 struct LookAhead {
-  cudaStream_t side = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaStream_t side = nullptr, crit = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr;
   std::vector<cudaEvent_t> panel, done;
   static LookAhead& get(int64_t steps) {
     static LookAhead la;
     static std::mutex mu;
     std::lock_guard<std::mutex> lk(mu);
     if (!la.side) {
-      cudaStreamCreateWithFlags(&la.side, cudaStreamNonBlocking);
+      // the critical chain gets the highest stream priority so that freed
+      // SMs go to its panel CTAs before the bulk update's next tiles
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      cudaStreamCreateWithPriority(&la.side, cudaStreamNonBlocking, lo);
+      cudaStreamCreateWithPriority(&la.crit, cudaStreamNonBlocking, hi);
       cudaEventCreateWithFlags(&la.fork, cudaEventDisableTiming);
       cudaEventCreateWithFlags(&la.join, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&la.join2, cudaEventDisableTiming);
     }
     while ((int64_t)la.panel.size() < steps) {
       cudaEvent_t a, b;
@@ -555,17 +562,17 @@ struct LookAhead {
 };
 
 // Right-looking blocked Cholesky (the reference's own loop structure,
-// dl/cholesky.hpp:43-70, with nb = 64): per block column one warp-panel leaf
-// factorization, one blocked DMMA panel solve (all rows of the panel in
-// parallel, 64 per CTA) and one masked DMMA SYRK of the trailing matrix.
-// Three launches per 64 columns; used for large single matrices where the
-// recursive variant's deep chain of tiny GEMMs dominates.
-template <typename T>
-dla_status potrf_blocked(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int64_t kbase) {
-  const size_t sm = sizeof(T) * (2 * 64 * CH_LD + 64);
+// dl/cholesky.hpp:43-70, with nb = NBP): per block column one warp-panel leaf
+// factorization and blocked DMMA panel solve (one launch, all rows of the
+// panel in parallel, 64 per CTA) and masked DMMA SYRK updates of the
+// trailing matrix.  Used for large single matrices where the recursive
+// variant's deep chain of tiny GEMMs dominates.
+template <typename T, int NBP>
+dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int64_t kbase) {
+  const size_t sm = sizeof(T) * ((NBP + 64) * (NBP + 1) + NBP);
   static bool once = false;
   if (!once) {
-    set_smem(k_potrf_panel<T>, sm);
+    set_smem(k_potrf_panel<T, NBP>, sm);
     once = true;
   }
   // Look-ahead on two streams: the main stream runs the critical chain
@@ -575,30 +582,36 @@ dla_status potrf_blocked(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int6
   // for it before its own column update of step k (panel k itself only needs
   // side updates <= k-2, already ordered).  Fork/join by events: stream-
   // ordered w.r.t. the caller and capturable into a CUDA graph.
-  const int64_t steps = (n + NB - 1) / NB;
+  const int64_t steps = (n + NBP - 1) / NBP;
   LookAhead& la = LookAhead::get(steps);
-  Ctx side = c;
+  static const bool prio = [] {
+    const char* e = getenv("DLA_POTRF_PRIO");  // tuning switch: 0 keeps the chain on the caller's stream
+    return e ? atoi(e) != 0 : true;
+  }();
+  Ctx side = c, cc = c;
   side.stream = la.side;
+  if (prio) cc.stream = la.crit;
   cudaEventRecord(la.fork, c.stream);
   cudaStreamWaitEvent(la.side, la.fork, 0);
+  if (prio) cudaStreamWaitEvent(cc.stream, la.fork, 0);
   for (int64_t s = 0; s < steps; ++s) {
-    const int64_t k0 = s * NB;
-    const int64_t kb = min((int64_t)NB, n - k0);
+    const int64_t k0 = s * NBP;
+    const int64_t kb = min((int64_t)NBP, n - k0);
     const int64_t rest = n - k0 - kb;
     MatB<T> akk = a.sub(k0, k0);
     MatB<T> a21 = a.sub(k0 + kb, k0);
     const int64_t chunks = rest > 0 ? (rest + 63) / 64 : 1;
-    k_potrf_panel<T><<<(unsigned)(batch * chunks), 256, sm, c.stream>>>((int)kb, rest, kbase + k0, akk, a21,
-                                                                         c.info);
+    k_potrf_panel<T, NBP><<<(unsigned)(batch * chunks), 256, sm, cc.stream>>>((int)kb, rest, kbase + k0, akk, a21,
+                                                                              c.info);
     DLAB_LAUNCH_CHECK();
     if (rest == 0) break;
-    if (s >= 1) cudaStreamWaitEvent(c.stream, la.done[s - 1], 0);
-    const int64_t nb2 = min((int64_t)NB, rest);  // block column k+1
-    DLAB_TRY(gemm<T>(c, batch, rest, nb2, kb, T(-1), C_(a21), false, C_(a21), true, T(1), a.sub(k0 + kb, k0 + kb),
+    if (s >= 1) cudaStreamWaitEvent(cc.stream, la.done[s - 1], 0);
+    const int64_t nb2 = min((int64_t)NBP, rest);  // block column k+1
+    DLAB_TRY(gemm<T>(cc, batch, rest, nb2, kb, T(-1), C_(a21), false, C_(a21), true, T(1), a.sub(k0 + kb, k0 + kb),
                      MASK_LOWER, c.info));
     const int64_t rest2 = rest - nb2;
     if (rest2 > 0) {
-      cudaEventRecord(la.panel[s], c.stream);
+      cudaEventRecord(la.panel[s], cc.stream);
       cudaStreamWaitEvent(la.side, la.panel[s], 0);
       MatB<T> p2 = a.sub(k0 + kb + nb2, k0);
       DLAB_TRY(gemm<T>(side, batch, rest2, rest2, kb, T(-1), C_(p2), false, C_(p2), true, T(1),
@@ -608,7 +621,24 @@ dla_status potrf_blocked(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int6
   }
   cudaEventRecord(la.join, la.side);
   cudaStreamWaitEvent(c.stream, la.join, 0);
+  if (prio) {
+    cudaEventRecord(la.join2, cc.stream);
+    cudaStreamWaitEvent(c.stream, la.join2, 0);
+  }
   return DLA_OK;
+}
+
+// Panel width: 128 halves the serial panel chain of a large matrix (each step
+// costs one launch + one column update regardless of width); 64 keeps more
+// CTAs busy for small n.  DLA_POTRF_NB overrides (tuning switch).
+template <typename T>
+dla_status potrf_blocked(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int64_t kbase) {
+  static const int nbp = [] {
+    const char* e = getenv("DLA_POTRF_NB");
+    return e ? atoi(e) : 0;
+  }();
+  const bool wide = nbp == 128;
+  return wide ? potrf_blocked_nb<T, 128>(c, batch, n, a, kbase) : potrf_blocked_nb<T, 64>(c, batch, n, a, kbase);
 }
 
 template <typename T>

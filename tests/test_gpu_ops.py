@@ -266,6 +266,20 @@ def test_potrf_backward(port, dt):
 
 
 @pytest.mark.parametrize("dt", DTYPES)
+def test_potrf_warp_batches(port, dt):
+    """n <= 32 runs a warp per matrix, 4-8 matrices per CTA: ragged batches."""
+    r = O.rng(18)
+    for n, B in [(32, 13), (9, 17), (1, 9)]:
+        a = O.random_spd(n, r, dt, batch=B)
+        for lower in (1, 0):
+            got = host(L.potrf(dev(a), lower))
+            assert_close(got, batch_apply(lambda x: port.potrf(x, lower), a), dt)
+            lbar = r.standard_normal((B, n, n)).astype(dt)
+            gb = host(L.potrf_backward(dev(lbar), dev(got), lower))
+            assert_close(gb, batch_apply(lambda x, y: port.potrf_bwd(x, y, lower), lbar, got), dt, 10)
+
+
+@pytest.mark.parametrize("dt", DTYPES)
 def test_potri(port, dt):
     r = O.rng(9)
     B = 2

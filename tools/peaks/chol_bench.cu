@@ -9,18 +9,20 @@ namespace dlab {
 void note_launch(int) {}
 }
 
+template <int NMAX>
 __global__ void k(double* a, int n, long long* t) {
-  __shared__ double S[64 * dlab::CH_LD];
+  constexpr int LD = NMAX + 1;
+  extern __shared__ double S[];
   __shared__ int flag;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) S[(e / n) * dlab::CH_LD + e % n] = a[e];
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) S[(e / n) * LD + e % n] = a[e];
   __syncthreads();
   long long t0 = clock64();
-  int f = dlab::chol_smem64<double>(S, n, &flag);
+  int f = dlab::chol_smem<double, NMAX>(S, n, &flag);
   __syncthreads();
   long long t1 = clock64();
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     const int i = e / n, j = e % n;
-    a[e] = j <= i ? S[i * dlab::CH_LD + j] : 0.0;
+    a[e] = j <= i ? S[i * LD + j] : 0.0;
   }
   if (threadIdx.x == 0) {
     t[0] = t1 - t0;
@@ -29,8 +31,8 @@ __global__ void k(double* a, int n, long long* t) {
 }
 
 int main() {
-  for (int n : {64, 32}) {
-    double h[64 * 64], ref[64 * 64];
+  for (int n : {128, 96, 64, 32}) {
+    static double h[128 * 128], ref[128 * 128], out[128 * 128];
     for (int i = 0; i < n; ++i)
       for (int j = 0; j < n; ++j) h[i * n + j] = (i == j ? n + 1.0 : 1.0 / (1 + i + j));
     // host Cholesky for checking
@@ -50,18 +52,21 @@ int main() {
     long long* t;
     cudaMalloc(&d, sizeof(h));
     cudaMalloc(&t, 64);
-    for (int threads : {32, 64, 128, 256}) {
+    cudaFuncSetAttribute(k<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140000);
+    for (int threads : {64, 128, 256, 512}) {
       cudaMemcpy(d, h, sizeof(double) * n * n, cudaMemcpyHostToDevice);
-      k<<<1, threads>>>(d, n, t);
+      if (n <= 64)
+        k<64><<<1, threads, 8 * 64 * 65>>>(d, n, t);
+      else
+        k<128><<<1, threads, 8 * 128 * 129>>>(d, n, t);
       long long ht[2];
-      double out[64 * 64];
       cudaMemcpy(ht, t, sizeof(ht), cudaMemcpyDeviceToHost);
       cudaMemcpy(out, d, sizeof(double) * n * n, cudaMemcpyDeviceToHost);
       double err = 0;
       for (int i = 0; i < n; ++i)
         for (int j = 0; j <= i; ++j) err = fmax(err, fabs(out[i * n + j] - ref[i * n + j]));
-      printf("{\"n\": %d, \"threads\": %d, \"factor_cycles\": %lld, \"per_col\": %.1f, \"fail\": %lld, \"maxerr\": %.2e}\n",
-             n, threads, ht[0], ht[0] / (double)n, ht[1], err);
+      printf("{\"nmax\": %d, \"n\": %d, \"threads\": %d, \"factor_cycles\": %lld, \"per_col\": %.1f, \"fail\": %lld, \"maxerr\": %.2e}\n",
+             n <= 64 ? 64 : 128, n, threads, ht[0], ht[0] / (double)n, ht[1], err);
     }
   }
   return 0;

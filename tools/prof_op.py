@@ -1,6 +1,6 @@
 """Run one operator a few times (for ncu launch lists / captures).
 
-    python tools/prof_op.py potrf 4096 [reps]
+    python tools/prof_op.py potrf 4096 [reps] [batch]
 """
 import os
 import sys
@@ -14,8 +14,9 @@ from paper_1710_08717_b200 import linalg as L  # noqa: E402
 def main():
     op, n = sys.argv[1], int(sys.argv[2])
     reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+    batch = int(sys.argv[4]) if len(sys.argv) > 4 else 1
     torch.manual_seed(0)
-    x = torch.randn(1, n, n, dtype=torch.float64, device="cuda")
+    x = torch.randn(batch, n, n, dtype=torch.float64, device="cuda")
     a0 = x @ x.transpose(-1, -2) + n * torch.eye(n, dtype=torch.float64, device="cuda")
     l = L.potrf(a0)
     lb = torch.tril(torch.randn_like(l))
