@@ -16,9 +16,13 @@ constexpr int CH_LD = 65;  // smem row stride for a 64 x 64 block
 // p0 + l + 32 q in slot q.  Straight-line: a failed pivot is only recorded;
 // the NaNs it creates never leave the CTA.
 template <typename T, int W, int Q, int J>
-__device__ __forceinline__ void panel_cols(T (&r)[Q][W], int lane, int w, int p0, int& failed) {
+__device__ __forceinline__ void panel_cols(T (&r)[Q][W], int lane, int w, int p0, int& failed, T dcur) {
   if constexpr (J < W) {
-    const T d = __shfl_sync(0xffffffffu, r[0][J], J);  // pivot row p0 + J lives on lane J
+    // dcur: this lane's candidate for pivot J (meaningful on lane J), formed
+    // at column J-1 straight from the lane's own multiplier, so the serial
+    // chain per column is shuffle -> rsqrt -> multiply -> FMA and never waits
+    // for the broadcast of the other multipliers.
+    const T d = __shfl_sync(0xffffffffu, dcur, J);  // pivot row p0 + J lives on lane J
     if (!(d > T(0)) && failed < 0 && J < w) failed = p0 + J;
     // 1/sqrt(d) directly (one MUFU + Newton, ~75 cycles) keeps the serial
     // pivot chain short; L(J,J) = d * (1/sqrt d) is off the chain.  Differs
@@ -28,6 +32,8 @@ __device__ __forceinline__ void panel_cols(T (&r)[Q][W], int lane, int w, int p0
     // column J: L(i, J) = a(i, J) / L(J, J) for rows below the pivot
     T l[Q];
     l[0] = (lane > J) ? r[0][J] * inv : (lane == J ? rt : r[0][J]);
+    T dnext = T(0);
+    if constexpr (J + 1 < W) dnext = r[0][J + 1] - l[0] * l[0];  // pivot J+1 on lane J+1
 #pragma unroll
     for (int q = 1; q < Q; ++q) l[q] = r[q][J] * inv;
 #pragma unroll
@@ -39,7 +45,7 @@ __device__ __forceinline__ void panel_cols(T (&r)[Q][W], int lane, int w, int p0
 #pragma unroll
       for (int q = 1; q < Q; ++q) r[q][k] -= l[q] * lkj;
     }
-    panel_cols<T, W, Q, J + 1>(r, lane, w, p0, failed);
+    panel_cols<T, W, Q, J + 1>(r, lane, w, p0, failed, dnext);
   }
 }
 
@@ -60,7 +66,7 @@ __device__ __forceinline__ int panel_warp(T* S, int n, int p0, int w, int lane) 
   for (int c = 0; c < W; ++c)
     if (c >= w && lane == c) r[0][c] = T(1);
   int failed = -1;
-  panel_cols<T, W, Q, 0>(r, lane, w, p0, failed);
+  panel_cols<T, W, Q, 0>(r, lane, w, p0, failed, r[0][0]);
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
     const int i = p0 + lane + 32 * q;
@@ -155,6 +161,72 @@ __device__ __forceinline__ int chol_smem(T* S, int n, int* flag) {
 template <typename T>
 __device__ __forceinline__ int chol_smem64(T* S, int n, int* flag) {
   return chol_smem<T, 64>(S, n, flag);
+}
+
+// ------------------------------------------------ warp-register Cholesky
+// Row-per-lane factorization of a 32 x 32 block held in registers (lane l
+// owns row l).  Values every lane needs are broadcast from shared memory
+// with 16-byte loads (Bc): one LDS.128 carries 2 doubles where a 64-bit
+// shuffle costs two SHFLs per value.
+constexpr int WCH = 32;
+
+template <typename T>
+struct Bc;
+template <>
+struct Bc<double> {
+  static constexpr int N = 2;
+  static constexpr int LLD = 34;  // broadcast tiles: 16-byte aligned rows
+  __device__ static void ld(const double* p, double (&v)[2]) {
+    const double2 t = *reinterpret_cast<const double2*>(p);
+    v[0] = t.x;
+    v[1] = t.y;
+  }
+};
+template <>
+struct Bc<float> {
+  static constexpr int N = 4;
+  static constexpr int LLD = 36;
+  __device__ static void ld(const float* p, float (&v)[4]) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    v[0] = t.x;
+    v[1] = t.y;
+    v[2] = t.z;
+    v[3] = t.w;
+  }
+};
+
+// Column J of the row-per-lane Cholesky (dl/cholesky.hpp:35-72): the pivot
+// moves by one shuffle, the column's multipliers through a double-buffered
+// shared vector (one __syncwarp per column).
+template <typename T, int J>
+__device__ __forceinline__ void wchol_col(T (&r)[WCH], int lane, int n, T* buf, int& failed, T dcur) {
+  if constexpr (J < WCH) {
+    // dcur: pivot candidate formed from this lane's own multiplier at column
+    // J-1 (see panel_cols): the serial chain is shuffle -> rsqrt -> mul -> FMA.
+    const T d = __shfl_sync(0xffffffffu, dcur, J);
+    if (!(d > T(0)) && failed < 0 && J < n) failed = J;
+    const T inv = Num<T>::rsqrt_(d);
+    const T rt = d * inv;
+    const T l = (lane > J) ? r[J] * inv : (lane == J ? rt : r[J]);
+    r[J] = l;
+    T dnext = T(0);
+    if constexpr (J + 1 < WCH) {
+      dnext = r[J + 1] - l * l;
+      constexpr int VN = Bc<T>::N;
+      T* cb = buf + (J & 1) * WCH;
+      cb[lane] = l;
+      __syncwarp();
+#pragma unroll
+      for (int k0 = ((J + 1) / VN) * VN; k0 < WCH; k0 += VN) {
+        T v[VN];
+        Bc<T>::ld(cb + k0, v);
+#pragma unroll
+        for (int u = 0; u < VN; ++u)  // lanes above row k0+u only touch unused upper entries
+          if (k0 + u > J) r[k0 + u] -= l * v[u];
+      }
+    }
+    wchol_col<T, J + 1>(r, lane, n, buf, failed, dnext);
+  }
 }
 
 // Forward substitution S y = v for nv <= 64 vectors held vector-major in

@@ -103,7 +103,19 @@ template <>
 struct Num<double> {
   __device__ static double sqrt_(double x) { return sqrt(x); }
   __device__ static double log_(double x) { return log(x); }
-  __device__ static double rsqrt_(double x) { return rsqrt(x); }
+  // Branch-free 1/sqrt: MUFU.RSQ64H seed + two Newton steps (<= ~1 ulp for
+  // normal positive x).  The library rsqrt() carries a special-case slow path
+  // whose call/reconvergence code wraps every warp shuffle of the Cholesky
+  // pivot chain; non-positive / NaN pivots still yield NaN here and are
+  // caught by the callers' !(d > 0) test.
+  __device__ static double rsqrt_(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y * y, 1.0);
+    y = fma(0.5 * y, e, y);
+    e = fma(-x, y * y, 1.0);
+    return fma(0.5 * y, e, y);
+  }
   static constexpr double sym_rtol = 1e-10;
   static constexpr double rank_rtol = 1e-12;
 };
@@ -111,7 +123,10 @@ template <>
 struct Num<float> {
   __device__ static float sqrt_(float x) { return sqrtf(x); }
   __device__ static float log_(float x) { return logf(x); }
-  __device__ static float rsqrt_(float x) { return 1.0f / sqrtf(x); }
+  __device__ static float rsqrt_(float x) {  // MUFU seed + one Newton step, branch-free
+    const float y = rsqrtf(x);
+    return fmaf(0.5f * y, fmaf(-x, y * y, 1.0f), y);
+  }
   static constexpr float sym_rtol = 1e-4f;
   static constexpr float rank_rtol = 1e-5f;
 };
@@ -146,6 +161,12 @@ template <typename T>
 dla_status gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T alpha, MatB<const T> a,
                 bool ta, MatB<const T> b, bool tb, T beta, MatB<T> cm, int mask = MASK_FULL,
                 const int32_t* skip = nullptr, int tri_a = TRI_NONE, int tri_b = TRI_NONE, int64_t inner = 1);
+
+// skinny.cu: n <= 8, m <= 8 or k <= 8 without triangular operands; returns
+// false when the shape is not skinny (the caller runs the tiled GEMM).
+template <typename T>
+bool gemm_skinny(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T alpha, MatB<const T> a, bool ta,
+                 MatB<const T> b, bool tb, T beta, MatB<T> cm, int mask, const int32_t* skip, dla_status* st);
 
 // elementwise.cu
 template <typename T>

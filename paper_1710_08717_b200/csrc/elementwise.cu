@@ -226,6 +226,17 @@ __global__ void k_sumlogdiag_bwd(int64_t batch, int64_t n, MatB<T> abar, const T
   }
 }
 
+// accumulate: only the diagonal is touched (batch * n threads, no n^2 sweep)
+template <typename T>
+__global__ void k_sumlogdiag_bwd_diag(int64_t batch, int64_t n, MatB<T> abar, const T* g, MatB<const T> a) {
+  const int64_t total = batch * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t / n, i = t - b * n;
+    T* p = abar.at(b, i, i);
+    *p += g[b] / *a.at(b, i, i);
+  }
+}
+
 }  // namespace
 
 template <typename T>
@@ -322,7 +333,7 @@ dla_status sumlogdiag_bwd(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, 
                           bool accumulate) {
   if (batch * n == 0) return DLA_OK;
   if (accumulate) {  // only the diagonal is touched
-    k_sumlogdiag_bwd<T><<<blocks_for(batch * n * n, 256), 256, 0, c.stream>>>(batch, n, abar, g, a, 1);
+    k_sumlogdiag_bwd_diag<T><<<blocks_for(batch * n, 256), 256, 0, c.stream>>>(batch, n, abar, g, a);
   } else {
     k_sumlogdiag_bwd<T><<<blocks_for(batch * n * n, 256), 256, 0, c.stream>>>(batch, n, abar, g, a, 0);
   }

@@ -508,6 +508,10 @@ dla_status gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T 
     if (mask != MASK_FULL || inner != 1) return DLA_ERR_INVALID;
     return ew_scale<T>(c, batch, m, n, cm, beta, skip);
   }
+  if (inner == 1 && tri_a == TRI_NONE && tri_b == TRI_NONE) {  // vector / outer-product shapes
+    dla_status st;
+    if (gemm_skinny<T>(c, batch, m, n, k, alpha, a, ta, b, tb, beta, cm, mask, skip, &st)) return st;
+  }
   GemmArgs<T> g{m, n, k, alpha, beta, a, b, cm, mask, skip, 0, 0, tri_a, tri_b, inner};
   const bool va = vec_ok<T>(a, ta ? m : k);
   const bool vb = vec_ok<T>(b, tb ? k : n);

@@ -42,6 +42,11 @@ size_t gelqf_ws_bytes(int64_t batch, int64_t m, int64_t n, bool backward);
 template <typename T>
 dla_status gelqf_fwd(const Ctx& c, int64_t batch, int64_t m, int64_t n, T* q, T* l, void* ws);
 
+// potrf_tiles.cu: persistent tile-dataflow Cholesky (f64, lower, in place;
+// strict upper untouched)
+bool potrf_tiles_eligible(int64_t batch, int64_t n, const MatB<double>& a);
+dla_status potrf_tiles(const Ctx& c, int64_t batch, int64_t n, MatB<double> a, int64_t kbase);
+
 // syevd.cu
 template <typename T>
 size_t syevd_ws_bytes(int64_t batch, int64_t n, bool backward);

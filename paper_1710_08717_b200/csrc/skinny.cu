@@ -1,0 +1,186 @@
+// Skinny batched GEMMs: matrix-vector and outer-product shapes.
+//
+// The reference's GP / marginal-likelihood chains apply gemm2 to n x 1
+// vectors (v = G y, the quadratic form v^T v, and their pullbacks
+// cbar y^T / G^T cbar, dl/adjoints.hpp:36-49).  On a 128 x 128 DMMA tile
+// these waste 127/128 of the tensor-core work and still pay the tile
+// pipeline; they are HBM-bound by nature (every A element is used once), so
+// they run here as streaming kernels that read each operand once, coalesced:
+//
+//   N-skinny (n <= 8, k >= 16): P = op(A) op(B) with few columns.
+//     !TA: one warp per output row, lanes stride the contiguous k of A's row,
+//          warp-shuffle reduction;
+//     TA : one thread per output row (= column of A), rows of A are swept in
+//          k order, so a warp reads 32 consecutive elements per step.
+//   M-skinny (m <= 8) is the N-skinny kernel on the transposed problem
+//   (C^T = op(B)^T op(A)^T, written through a transposed store).
+//   K-skinny (k <= 8): rank-k outer products, one thread per output
+//   element along the contiguous dimension of C (write-bound).
+//
+// Semantics are gemm()'s: C = alpha P + beta C (beta == 0 => C not read),
+// optional lower/upper write mask for the K-skinny case.
+#include "common.cuh"
+
+namespace dlab {
+namespace {
+
+constexpr int SK_NMAX = 8;
+
+template <typename T>
+struct SkinnyArgs {
+  int64_t m, n, k;  // product P is m x n
+  T alpha, beta;
+  MatB<const T> a, b;
+  MatB<T> c;
+  bool ta, tb, tc;  // tc: C holds P^T (element (i, j) of P at c(j, i))
+  int mask;
+  const int32_t* skip;
+};
+
+template <typename T>
+__device__ __forceinline__ T opa(const SkinnyArgs<T>& g, const T* A, int64_t i, int64_t k) {
+  return g.ta ? A[k * g.a.ld + i] : A[i * g.a.ld + k];
+}
+template <typename T>
+__device__ __forceinline__ T opb(const SkinnyArgs<T>& g, const T* B, int64_t k, int64_t j) {
+  return g.tb ? B[j * g.b.ld + k] : B[k * g.b.ld + j];
+}
+template <typename T>
+__device__ __forceinline__ void put(const SkinnyArgs<T>& g, T* C, int64_t i, int64_t j, T v) {
+  T* p = g.tc ? C + j * g.c.ld + i : C + i * g.c.ld + j;
+  T r = g.alpha * v;
+  if (g.beta != T(0)) r += g.beta * *p;
+  *p = r;
+}
+
+// !TA: warp per output row.  grid.x = batch * ceil(m / 8), 8 warps per CTA.
+template <typename T>
+__global__ void __launch_bounds__(256) k_nskinny_rows(SkinnyArgs<T> g, int64_t row_blocks) {
+  const int64_t b = blockIdx.x / row_blocks, rb = blockIdx.x % row_blocks;
+  if (slice_failed(g.skip, b)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i = rb * 8 + warp;
+  if (i >= g.m) return;
+  const T* A = g.a.p + b * g.a.bs;
+  const T* B = g.b.p + b * g.b.bs;
+  const T* arow = A + i * g.a.ld;
+  T acc[SK_NMAX];
+#pragma unroll
+  for (int j = 0; j < SK_NMAX; ++j) acc[j] = T(0);
+#pragma unroll 4
+  for (int64_t k = lane; k < g.k; k += 32) {
+    const T av = arow[k];
+#pragma unroll
+    for (int j = 0; j < SK_NMAX; ++j)
+      if (j < g.n) acc[j] += av * opb(g, B, k, j);
+  }
+#pragma unroll
+  for (int j = 0; j < SK_NMAX; ++j) {
+    if (j < g.n) {  // warp-uniform
+      T v = acc[j];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) put(g, g.c.p + b * g.c.bs, i, j, v);
+    }
+  }
+}
+
+// TA: thread per output row.  grid.x = batch * ceil(m / 128), 128 threads.
+template <typename T>
+__global__ void __launch_bounds__(128) k_nskinny_cols(SkinnyArgs<T> g, int64_t row_blocks) {
+  const int64_t b = blockIdx.x / row_blocks, rb = blockIdx.x % row_blocks;
+  if (slice_failed(g.skip, b)) return;
+  const int64_t i = rb * 128 + threadIdx.x;
+  const T* A = g.a.p + b * g.a.bs;
+  const T* B = g.b.p + b * g.b.bs;
+  T acc[SK_NMAX];
+#pragma unroll
+  for (int j = 0; j < SK_NMAX; ++j) acc[j] = T(0);
+  if (i < g.m) {
+    const T* acol = A + i;
+#pragma unroll 4
+    for (int64_t k = 0; k < g.k; ++k) {
+      const T av = acol[k * g.a.ld];
+#pragma unroll
+      for (int j = 0; j < SK_NMAX; ++j)
+        if (j < g.n) acc[j] += av * opb(g, B, k, j);
+    }
+#pragma unroll
+    for (int j = 0; j < SK_NMAX; ++j)
+      if (j < g.n) put(g, g.c.p + b * g.c.bs, i, j, acc[j]);
+  }
+}
+
+// K-skinny: one CTA row-sweep per row of C's storage (grid-stride over
+// batch x rows), threads along the contiguous columns: no per-element 64-bit
+// index division, coalesced stores.
+template <typename T>
+__global__ void __launch_bounds__(128) k_kskinny(SkinnyArgs<T> g, int64_t batch) {
+  const int64_t rows = g.tc ? g.n : g.m, cols = g.tc ? g.m : g.n;
+  const int64_t total = batch * rows;
+  for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+    const int64_t b = t / rows, r = t - b * rows;
+    if (slice_failed(g.skip, b)) continue;
+    const T* A = g.a.p + b * g.a.bs;
+    const T* B = g.b.p + b * g.b.bs;
+    T* C = g.c.p + b * g.c.bs;
+    for (int64_t s = threadIdx.x; s < cols; s += blockDim.x) {
+      const int64_t i = g.tc ? s : r, j = g.tc ? r : s;
+      if (g.mask == MASK_LOWER && j > i) continue;
+      if (g.mask == MASK_UPPER && j < i) continue;
+      T acc = T(0);
+      for (int64_t k = 0; k < g.k; ++k) acc += opa(g, A, i, k) * opb(g, B, k, j);
+      put(g, C, i, j, acc);
+    }
+  }
+}
+
+}  // namespace
+
+// Returns true (and launches) when the shape is skinny; false leaves the
+// problem to the tiled DMMA / FFMA GEMM.
+template <typename T>
+bool gemm_skinny(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T alpha, MatB<const T> a, bool ta,
+                 MatB<const T> b, bool tb, T beta, MatB<T> cm, int mask, const int32_t* skip, dla_status* st) {
+  SkinnyArgs<T> g{m, n, k, alpha, beta, a, b, cm, ta, tb, false, mask, skip};
+  *st = DLA_OK;
+  if (k <= SK_NMAX) {
+    k_kskinny<T><<<blocks_for(batch * m, 1, 148 * 64), 128, 0, c.stream>>>(g, batch);
+  } else if (mask != MASK_FULL) {
+    return false;
+  } else if (n <= SK_NMAX || m <= SK_NMAX) {
+    if (n > SK_NMAX) {  // C^T = op(B)^T op(A)^T
+      g.m = n;
+      g.n = m;
+      g.a = b;
+      g.ta = !tb;
+      g.b = a;
+      g.tb = !ta;
+      g.tc = true;
+    }
+    if (!g.ta) {
+      const int64_t rb = (g.m + 7) / 8;
+      k_nskinny_rows<T><<<(unsigned)(batch * rb), 256, 0, c.stream>>>(g, rb);
+    } else {
+      const int64_t rb = (g.m + 127) / 128;
+      k_nskinny_cols<T><<<(unsigned)(batch * rb), 128, 0, c.stream>>>(g, rb);
+    }
+  } else {
+    return false;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "dla_b200 skinny gemm: %s\n", cudaGetErrorString(e));
+    *st = DLA_ERR_CUDA;
+    return true;
+  }
+  note_launch(1);
+  return true;
+}
+
+template bool gemm_skinny<double>(const Ctx&, int64_t, int64_t, int64_t, int64_t, double, MatB<const double>, bool,
+                                  MatB<const double>, bool, double, MatB<double>, int, const int32_t*, dla_status*);
+template bool gemm_skinny<float>(const Ctx&, int64_t, int64_t, int64_t, int64_t, float, MatB<const float>, bool,
+                                 MatB<const float>, bool, float, MatB<float>, int, const int32_t*, dla_status*);
+
+}  // namespace dlab

@@ -136,31 +136,6 @@ __global__ void __launch_bounds__(256) k_potrf_bwd_small(int n, MatB<T> abar, Ma
 constexpr int WN = 32;
 constexpr int WLD = WN + 1;  // column-per-lane tiles: conflict-free rows and columns
 
-template <typename T>
-struct Bc;
-template <>
-struct Bc<double> {
-  static constexpr int N = 2;
-  static constexpr int LLD = 34;  // broadcast tiles: 16-byte aligned rows
-  __device__ static void ld(const double* p, double (&v)[2]) {
-    const double2 t = *reinterpret_cast<const double2*>(p);
-    v[0] = t.x;
-    v[1] = t.y;
-  }
-};
-template <>
-struct Bc<float> {
-  static constexpr int N = 4;
-  static constexpr int LLD = 36;
-  __device__ static void ld(const float* p, float (&v)[4]) {
-    const float4 t = *reinterpret_cast<const float4*>(p);
-    v[0] = t.x;
-    v[1] = t.y;
-    v[2] = t.z;
-    v[3] = t.w;
-  }
-};
-
 // warps (matrices) per CTA: keeps the per-CTA tile within 70 KB
 template <typename T>
 constexpr int wpc_fwd() { return 8; }
@@ -172,36 +147,6 @@ __device__ __forceinline__ T warp_max(T v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
-}
-
-// Column J of the row-per-lane Cholesky (dl/cholesky.hpp:35-72): the pivot
-// moves by one shuffle, the column's multipliers through a double-buffered
-// shared vector (one __syncwarp per column).
-template <typename T, int J>
-__device__ __forceinline__ void wchol_col(T (&r)[WN], int lane, int n, T* buf, int& failed) {
-  if constexpr (J < WN) {
-    const T d = __shfl_sync(0xffffffffu, r[J], J);
-    if (!(d > T(0)) && failed < 0 && J < n) failed = J;
-    const T inv = Num<T>::rsqrt_(d);
-    const T rt = d * inv;
-    const T l = (lane > J) ? r[J] * inv : (lane == J ? rt : r[J]);
-    r[J] = l;
-    if constexpr (J + 1 < WN) {
-      constexpr int VN = Bc<T>::N;
-      T* cb = buf + (J & 1) * WN;
-      cb[lane] = l;
-      __syncwarp();
-#pragma unroll
-      for (int k0 = ((J + 1) / VN) * VN; k0 < WN; k0 += VN) {
-        T v[VN];
-        Bc<T>::ld(cb + k0, v);
-#pragma unroll
-        for (int u = 0; u < VN; ++u)  // lanes above row k0+u only touch unused upper entries
-          if (k0 + u > J) r[k0 + u] -= l * v[u];
-      }
-    }
-    wchol_col<T, J + 1>(r, lane, n, buf, failed);
-  }
 }
 
 template <typename T, int MINB>
@@ -246,7 +191,7 @@ __global__ void __launch_bounds__(256, MINB) k_potrf_warp(int n, int64_t batch, 
 #pragma unroll
   for (int c = 0; c < WN; ++c) r[c] = (lane < n && c <= lane) ? S[lane * WLD + c] : (c == lane ? T(1) : T(0));
   int failed = -1;
-  wchol_col<T, 0>(r, lane, n, buf, failed);
+  wchol_col<T, 0>(r, lane, n, buf, failed, r[0]);
   if (failed >= 0) {
     if (lane == 0) record_failure(info, b, DLA_ERR_NOT_SPD, failed);
     return;

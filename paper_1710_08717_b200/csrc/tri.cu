@@ -723,9 +723,19 @@ dla_status potrf_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
     return e ? atoi(e) : 0;
   }();
   // default: blocked right-looking with look-ahead (measured faster than the
-  // recursive split at every n > 64 on B200); mode 1 keeps the recursion.
+  // recursive split at every n > 64 on B200, and still ~3% ahead of the
+  // persistent tile-dataflow kernel at n = 1024 / 4096, whose per-column
+  // chain is the same chol64 + tile solve).  Modes: 1 recursive, 2 blocked,
+  // 3 tile dataflow (f64).
+  bool tiles = false;
+  if constexpr (sizeof(T) == 8) {
+    MatB<double> ad{reinterpret_cast<double*>(a.p), a.ld, a.bs};
+    tiles = mode == 3 && potrf_tiles_eligible(batch, n, ad);
+    if (tiles) DLAB_TRY(potrf_tiles(c, batch, n, ad, 0));
+  }
   const bool blocked = mode != 1 && n > NB;
-  if (blocked) DLAB_TRY(potrf_blocked<T>(c, batch, n, a, 0));
+  if (tiles) {
+  } else if (blocked) DLAB_TRY(potrf_blocked<T>(c, batch, n, a, 0));
   else DLAB_TRY(potrf_rec<T>(c, batch, n, 0, a));
   return ew_square<T>(c, batch, n, a, /*tril*/ 0, T(1), c.info);
 }

@@ -245,6 +245,14 @@ def test_potrf_errors():
         L.potrf_inplace(x)
     assert e.value.batch_index == 2 and e.value.step == 5
     np.testing.assert_allclose(host(x)[0], np.linalg.cholesky(ab[0]), rtol=1e-10, atol=1e-12)
+    # tile-dataflow path (n >= 256): failure deep inside one slice, the other factored
+    a2 = O.random_spd(300, r, batch=2)
+    a2[1, 200, 200] = -1e6
+    x = dev(a2)
+    with pytest.raises(L.NotPositiveDefiniteError) as e:
+        L.potrf_inplace(x)
+    assert e.value.batch_index == 1 and e.value.step == 200
+    np.testing.assert_allclose(np.tril(host(x)[0]), np.linalg.cholesky(a2[0]), rtol=1e-10, atol=1e-12)
 
 
 @pytest.mark.parametrize("dt", DTYPES)

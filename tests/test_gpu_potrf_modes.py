@@ -1,0 +1,48 @@
+"""The non-default potrf schedules (DLA_POTRF_MODE, read once per process):
+1 = recursive split, 2 = blocked look-ahead (default), 3 = persistent tile
+dataflow.  Each runs in a subprocess against numpy's Cholesky and the same
+failure semantics as the default path (dl/cholesky.hpp:49-53)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import numpy as np, torch
+from oracle import oracle as O
+from paper_1710_08717_b200 import linalg as L
+r = O.rng(31)
+for n, B in [(300, 2), (256, 1), (513, 1), (130, 3)]:
+    a = O.random_spd(n, r, batch=B)
+    got = L.potrf(torch.from_numpy(a).cuda()).cpu().numpy()
+    want = np.linalg.cholesky(a)
+    err = np.abs(got - want).max() / np.abs(want).max()
+    assert err < 1e-12, (n, err)
+    assert np.all(np.triu(got, 1) == 0)
+a = O.random_spd(300, r, batch=2)
+a[1, 200, 200] = -1e6
+x = torch.from_numpy(a).cuda()
+try:
+    L.potrf_inplace(x)
+    raise SystemExit("no error raised")
+except L.NotPositiveDefiniteError as e:
+    assert e.batch_index == 1 and e.step == 200, (e.batch_index, e.step)
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("mode", ["1", "3"])
+def test_potrf_schedule(mode):
+    env = dict(os.environ, DLA_POTRF_MODE=mode, PYTHONPATH=ROOT)
+    p = subprocess.run([sys.executable, "-c", SCRIPT], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert p.returncode == 0 and "ok" in p.stdout, p.stdout + p.stderr

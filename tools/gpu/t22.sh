@@ -1,0 +1,5 @@
+cd /root/repo
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+python tools/microbench.py 2>&1 | grep -E "n=4096|n=128 batch=8192|n=1024"
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-also 2> gpurun_out/bench_c2.err | cut -c1-200
+timeout 600 python bench.py --config c5 --steps 3 --warmup 2 --no-cpu-baseline 2>/dev/null | cut -c1-200
