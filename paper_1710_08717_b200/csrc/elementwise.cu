@@ -132,36 +132,60 @@ __device__ __forceinline__ T from_bits(unsigned long long u) {
 }
 
 template <typename T>
-__global__ void k_symcheck_reduce(int64_t batch, int64_t n, MatB<const T> a, unsigned long long* red) {
-  // one CTA per (slice, row-chunk)
-  const int64_t chunks = (n + 31) / 32;
-  const int64_t b = blockIdx.x / chunks, c = blockIdx.x % chunks;
+__global__ void __launch_bounds__(256) k_symcheck_reduce(int64_t batch, int64_t n, MatB<const T> a,
+                                                         unsigned long long* red) {
+  // one CTA per (slice, 32 x 32 tile pair (ti, tj), ti >= tj): both tiles are
+  // read with coalesced row sweeps and compared through shared memory
+  __shared__ T t1[32][33], t2[32][33];
+  const int64_t nt = (n + 31) / 32, pairs = nt * (nt + 1) / 2;
+  const int64_t b = blockIdx.x / pairs;
+  int64_t p = blockIdx.x % pairs;
+  int64_t ti = (int64_t)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5);
+  while (ti * (ti + 1) / 2 > p) --ti;
+  while ((ti + 1) * (ti + 2) / 2 <= p) ++ti;
+  const int64_t tj = p - ti * (ti + 1) / 2;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   T mabs = T(0), masym = T(0);
-  const int64_t i0 = c * 32, i1 = min(n, i0 + 32);
-  for (int64_t t = threadIdx.x; t < (i1 - i0) * n; t += blockDim.x) {
-    const int64_t i = i0 + t / n, j = t % n;
-    const T v = *a.at(b, i, j);
-    const T av = fabs(v);
-    if (av > mabs) mabs = av;
-    if (j > i) {
-      const T d = fabs(v - *a.at(b, j, i));
-      if (d > masym) masym = d;
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i1 = ti * 32 + r, j1 = tj * 32 + tx;  // tile (ti, tj)
+    const int64_t i2 = tj * 32 + r, j2 = ti * 32 + tx;  // tile (tj, ti)
+    const T v1 = (i1 < n && j1 < n) ? *a.at(b, i1, j1) : T(0);
+    const T v2 = (i2 < n && j2 < n) ? *a.at(b, i2, j2) : T(0);
+    t1[r][tx] = v1;
+    t2[r][tx] = v2;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i = ti * 32 + r, j = tj * 32 + tx;
+    if (i < n && j < n) {
+      const T v = t1[r][tx];
+      if (fabs(v) > mabs) mabs = fabs(v);
+      if (ti != tj) {
+        const T w = t2[r][tx];  // element (tj*32 + r, ti*32 + tx): the other triangle
+        if (fabs(w) > mabs) mabs = fabs(w);
+        const T d = fabs(v - t2[tx][r]);  // a(i, j) vs a(j, i)
+        if (d > masym) masym = d;
+      } else if (tx > r) {
+        const T d = fabs(v - t1[tx][r]);
+        if (d > masym) masym = d;
+      }
     }
   }
-  __shared__ unsigned long long s0[32], s1[32];
+  __shared__ unsigned long long s0[8], s1[8];
   unsigned long long u0 = ord_bits(mabs), u1 = ord_bits(masym);
   for (int o = 16; o; o >>= 1) {
     u0 = max(u0, __shfl_xor_sync(0xffffffffu, u0, o));
     u1 = max(u1, __shfl_xor_sync(0xffffffffu, u1, o));
   }
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) {
-    s0[w] = u0;
-    s1[w] = u1;
+  if (tx == 0) {
+    s0[ty] = u0;
+    s1[ty] = u1;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+    for (int k = 1; k < 8; ++k) {
       u0 = max(u0, s0[k]);
       u1 = max(u1, s1[k]);
     }
@@ -302,8 +326,8 @@ dla_status check_symmetric(const Ctx& c, int64_t batch, int64_t n, MatB<const T>
   unsigned long long* red = nullptr;
   if (cudaMallocAsync(&red, sizeof(unsigned long long) * 2 * batch, c.stream) != cudaSuccess) return DLA_ERR_CUDA;
   cudaMemsetAsync(red, 0, sizeof(unsigned long long) * 2 * batch, c.stream);
-  const int64_t chunks = (n + 31) / 32;
-  k_symcheck_reduce<T><<<(unsigned)(batch * chunks), 256, 0, c.stream>>>(batch, n, a, red);
+  const int64_t nt = (n + 31) / 32;
+  k_symcheck_reduce<T><<<(unsigned)(batch * (nt * (nt + 1) / 2)), 256, 0, c.stream>>>(batch, n, a, red);
   k_symcheck_decide<T><<<blocks_for(batch, 256), 256, 0, c.stream>>>(batch, red, info);
   cudaFreeAsync(red, c.stream);
   note_launch(1);

@@ -128,15 +128,21 @@ __global__ void __launch_bounds__(RT) k_rbf_bwd(int64_t n, int64_t d, const doub
 // 256-byte row segment; x_j tiles are staged in shared memory once per CTA.
 constexpr int TRW = 16;   // rows per CTA
 constexpr int TCJ = 128;  // columns per staged tile
+constexpr int TCS = 512;  // columns per CTA (grid = rows/16 x n/512: enough CTAs to fill 148 SMs at n = 4096)
+
+__host__ __device__ inline int64_t rbf_splits(int64_t n) { return (n + TCS - 1) / TCS; }
 
 template <int D, bool FWD>
 __global__ void __launch_bounds__(256) k_rbf_tiled(int64_t n, const double* x, const double* s, double sigma2,
                                                    double two_ell2, double lam, double* a, const double* abar,
-                                                   double* xbar, double* part) {
+                                                   double* xpart, double* part) {
   __shared__ double xs[TCJ][D];
   __shared__ double ss[TCJ];
-  const int64_t rb = (n + TRW - 1) / TRW;
-  const int64_t b = blockIdx.x / rb, i0 = (blockIdx.x % rb) * TRW;
+  const int64_t rb = (n + TRW - 1) / TRW, splits = rbf_splits(n);
+  const int64_t sp = blockIdx.x % splits, blk = blockIdx.x / splits;
+  const int64_t b = blk / rb, i0 = (blk % rb) * TRW;
+  const int64_t jbeg = sp * TCS, jend = min(n, jbeg + TCS);
+  const double inv2l = 1.0 / two_ell2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double* xb = x + b * n * D;
   const double* sb = s + b * n;
@@ -154,19 +160,19 @@ __global__ void __launch_bounds__(256) k_rbf_tiled(int64_t n, const double* x, c
   for (int q = 0; q < 2; ++q)
 #pragma unroll
     for (int f = 0; f < D; ++f) xacc[q][f] = 0.0;
-  for (int64_t j0 = 0; j0 < n; j0 += TCJ) {
+  for (int64_t j0 = jbeg; j0 < jend; j0 += TCJ) {
     __syncthreads();
     for (int e = threadIdx.x; e < TCJ * D; e += 256) {
       const int64_t j = j0 + e / D;
-      xs[e / D][e % D] = j < n ? xb[j * D + e % D] : 0.0;
+      xs[e / D][e % D] = j < jend ? xb[j * D + e % D] : 0.0;
     }
-    for (int e = threadIdx.x; e < TCJ; e += 256) ss[e] = (j0 + e < n) ? sb[j0 + e] : 0.0;
+    for (int e = threadIdx.x; e < TCJ; e += 256) ss[e] = (j0 + e < jend) ? sb[j0 + e] : 0.0;
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < TCJ / 32; ++k) {
       const int jj = lane + 32 * k;
       const int64_t j = j0 + jj;
-      if (j >= n) continue;
+      if (j >= jend) continue;
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int64_t i = ii[q];
@@ -175,7 +181,7 @@ __global__ void __launch_bounds__(256) k_rbf_tiled(int64_t n, const double* x, c
 #pragma unroll
         for (int f = 0; f < D; ++f) g += xi[q][f] * xs[jj][f];
         const double dist = (si[q] + ss[jj]) - 2.0 * g;
-        const double Dv = dist / two_ell2;
+        const double Dv = dist * inv2l;
         const double E = exp(-Dv);
         double* ap = a + (b * n + i) * n + j;
         if constexpr (FWD) {
@@ -188,8 +194,8 @@ __global__ void __launch_bounds__(256) k_rbf_tiled(int64_t n, const double* x, c
           const double nb = kb * sigma2 * E;
           pe[q] += nb * Dv;
           if (j == i) pl[q] += kb;
-          if (xbar) {
-            const double w = -nb / two_ell2;
+          if (xpart) {
+            const double w = -nb * inv2l;
 #pragma unroll
             for (int f = 0; f < D; ++f) xacc[q][f] += w * (xi[q][f] - xs[jj][f]);
           }
@@ -214,13 +220,14 @@ __global__ void __launch_bounds__(256) k_rbf_tiled(int64_t n, const double* x, c
         xv[f] = t;
       }
       const int64_t i = ii[q];
-      if (lane == 0 && i < n) {
-        part[(b * n + i) * 3 + 0] = v0;
-        part[(b * n + i) * 3 + 1] = v1;
-        part[(b * n + i) * 3 + 2] = v2;
-        if (xbar)
+      if (lane == 0 && i < n) {  // per-(row, column split) partials, reduced in a fixed order later
+        double* pp = part + ((b * n + i) * splits + sp) * 3;
+        pp[0] = v0;
+        pp[1] = v1;
+        pp[2] = v2;
+        if (xpart)
 #pragma unroll
-          for (int f = 0; f < D; ++f) xbar[(b * n + i) * D + f] = 4.0 * xv[f];
+          for (int f = 0; f < D; ++f) xpart[((b * n + i) * splits + sp) * D + f] = xv[f];
       }
     }
   }
@@ -230,7 +237,7 @@ template <bool FWD>
 bool launch_tiled(int64_t d, int64_t batch, int64_t n, const double* x, const double* s, double sigma2,
                   double two_ell2, double lam, double* a, const double* abar, double* xbar, double* part,
                   cudaStream_t st) {
-  const unsigned grid = (unsigned)(batch * ((n + TRW - 1) / TRW));
+  const unsigned grid = (unsigned)(batch * ((n + TRW - 1) / TRW) * rbf_splits(n));
 #define DLAB_RBF_CASE(DD)                                                                                  \
   case DD:                                                                                                 \
     k_rbf_tiled<DD, FWD><<<grid, 256, 0, st>>>(n, x, s, sigma2, two_ell2, lam, a, abar, xbar, part);      \
@@ -248,17 +255,29 @@ bool launch_tiled(int64_t d, int64_t batch, int64_t n, const double* x, const do
 #undef DLAB_RBF_CASE
 }
 
+// xbar rows from the per-split partials (fixed split order).
+__global__ void k_rbf_xbar(int64_t rows, int64_t splits, int d, const double* xpart, double* xbar) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows * d; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / d, f = t % d;
+    double acc = 0.0;
+    for (int64_t sp = 0; sp < splits; ++sp) acc += xpart[(r * splits + sp) * d + f];
+    xbar[t] = 4.0 * acc;
+  }
+}
+
 // Fixed-order finalization per slice: grads w.r.t. (log sigma2, log ell2, log lam).
-__global__ void k_rbf_finalize(int64_t batch, int64_t n, const double* part, double sigma2, double ell2,
-                               double lam, double two_ell2, double* grads) {
+__global__ void k_rbf_finalize(int64_t batch, int64_t n, int64_t splits, const double* part, double sigma2,
+                               double ell2, double lam, double two_ell2, double* grads) {
   const int64_t b = blockIdx.x;
   __shared__ double red[3][RT];
   double a0 = 0, a1 = 0, a2 = 0;
-  for (int64_t i = threadIdx.x; i < n; i += RT) {
-    a0 += part[(b * n + i) * 3 + 0];
-    a1 += part[(b * n + i) * 3 + 1];
-    a2 += part[(b * n + i) * 3 + 2];
-  }
+  for (int64_t i = threadIdx.x; i < n; i += RT)
+    for (int64_t sp = 0; sp < splits; ++sp) {
+      const double* pp = part + ((b * n + i) * splits + sp) * 3;
+      a0 += pp[0];
+      a1 += pp[1];
+      a2 += pp[2];
+    }
   red[0][threadIdx.x] = a0;
   red[1][threadIdx.x] = a1;
   red[2][threadIdx.x] = a2;
@@ -291,8 +310,8 @@ using namespace dlab;
 extern "C" {
 
 size_t dla_gp_rbf_ws_bytes(int64_t batch, int64_t n, int64_t d) {
-  (void)d;
-  return sizeof(double) * (size_t)(batch * n + batch * n * 3);
+  // row norms + per-(row, column split) partials of (s, l, e) and xbar
+  return sizeof(double) * (size_t)(batch * n + batch * n * rbf_splits(n) * (3 + d));
 }
 
 dla_status dla_gp_rbf_fwd_f64(int64_t batch, int64_t n, int64_t d, const double* x, double sigma2, double ell2,
@@ -305,7 +324,7 @@ dla_status dla_gp_rbf_fwd_f64(int64_t batch, int64_t n, int64_t d, const double*
   k_rowsq<<<blocks_for(batch * n, 256), 256, 0, s>>>(batch, n, d, x, sq);
   if (!launch_tiled<true>(d, batch, n, x, sq, sigma2, ell2 * 2.0, lam, a, nullptr, nullptr, nullptr, s))
     k_rbf_fwd<<<(unsigned)(batch * n), RT, 0, s>>>(n, d, x, sq, sigma2, ell2 * 2.0, lam, a);
-  note_launch(1);
+  note_launch(1);  // + 1 in DLAB_LAUNCH_CHECK
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }
@@ -319,11 +338,22 @@ dla_status dla_gp_rbf_bwd_f64(int64_t batch, int64_t n, int64_t d, const double*
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   double* sq = static_cast<double*>(ws);
   double* part = sq + batch * n;
+  const int64_t splits = rbf_splits(n);
+  double* xpart = part + batch * n * splits * 3;
   k_rowsq<<<blocks_for(batch * n, 256), 256, 0, s>>>(batch, n, d, x, sq);
-  if (!launch_tiled<false>(d, batch, n, x, sq, sigma2, ell2 * 2.0, lam, nullptr, abar, xbar, part, s))
+  int launches = 2;  // + 1 in DLAB_LAUNCH_CHECK
+  if (launch_tiled<false>(d, batch, n, x, sq, sigma2, ell2 * 2.0, lam, nullptr, abar, xbar ? xpart : nullptr, part,
+                          s)) {
+    k_rbf_finalize<<<(unsigned)batch, RT, 0, s>>>(batch, n, splits, part, sigma2, ell2, lam, ell2 * 2.0, grads);
+    if (xbar) {
+      k_rbf_xbar<<<blocks_for(batch * n * d, 256), 256, 0, s>>>(batch * n, splits, (int)d, xpart, xbar);
+      ++launches;
+    }
+  } else {  // generic d: one CTA per row, partials already per row
     k_rbf_bwd<<<(unsigned)(batch * n), RT, 0, s>>>(n, d, x, sq, sigma2, ell2 * 2.0, abar, xbar, part);
-  k_rbf_finalize<<<(unsigned)batch, RT, 0, s>>>(batch, n, part, sigma2, ell2, lam, ell2 * 2.0, grads);
-  note_launch(2);
+    k_rbf_finalize<<<(unsigned)batch, RT, 0, s>>>(batch, n, 1, part, sigma2, ell2, lam, ell2 * 2.0, grads);
+  }
+  note_launch(launches);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }

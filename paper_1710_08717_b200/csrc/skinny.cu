@@ -111,6 +111,48 @@ __global__ void __launch_bounds__(128) k_nskinny_cols(SkinnyArgs<T> g, int64_t r
   }
 }
 
+// TA with a tiny product (m * n <= 16, e.g. the quadratic form v^T v): one
+// CTA per slice splits k over its 256 threads (rows of A are contiguous),
+// then a warp-shuffle + shared-memory reduction.
+constexpr int KS_MN = 16;
+template <typename T>
+__global__ void __launch_bounds__(256) k_nskinny_ksplit(SkinnyArgs<T> g) {
+  __shared__ T red[8][KS_MN];
+  const int64_t b = blockIdx.x;
+  if (slice_failed(g.skip, b)) return;
+  const T* A = g.a.p + b * g.a.bs;
+  const T* B = g.b.p + b * g.b.bs;
+  const int mn = (int)(g.m * g.n);
+  T acc[KS_MN];
+#pragma unroll
+  for (int e = 0; e < KS_MN; ++e) acc[e] = T(0);
+  for (int64_t k = threadIdx.x; k < g.k; k += 256) {
+#pragma unroll
+    for (int e = 0; e < KS_MN; ++e)
+      if (e < mn) {
+        const int64_t i = e / g.n, j = e % g.n;
+        acc[e] += A[k * g.a.ld + i] * opb(g, B, k, j);
+      }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int e = 0; e < KS_MN; ++e) {
+    if (e < mn) {
+      T v = acc[e];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[warp][e] = v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < mn) {
+    T v = T(0);
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
+    put(g, g.c.p + b * g.c.bs, threadIdx.x / g.n, threadIdx.x % g.n, v);
+  }
+}
+
 // K-skinny: one CTA row-sweep per row of C's storage (grid-stride over
 // batch x rows), threads along the contiguous columns: no per-element 64-bit
 // index division, coalesced stores.
@@ -161,9 +203,13 @@ bool gemm_skinny(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T
     if (!g.ta) {
       const int64_t rb = (g.m + 7) / 8;
       k_nskinny_rows<T><<<(unsigned)(batch * rb), 256, 0, c.stream>>>(g, rb);
-    } else {
+    } else if (g.m >= 64) {
       const int64_t rb = (g.m + 127) / 128;
       k_nskinny_cols<T><<<(unsigned)(batch * rb), 128, 0, c.stream>>>(g, rb);
+    } else if (g.m * g.n <= KS_MN) {
+      k_nskinny_ksplit<T><<<(unsigned)batch, 256, 0, c.stream>>>(g);
+    } else {
+      return false;  // transposed, mid-sized: the tiled GEMM
     }
   } else {
     return false;

@@ -66,7 +66,9 @@ def tri_factor(r, nt, lower, dt, batch):
 def test_gemm_gemm2(port, dt):
     r = O.rng(1)
     B = 3
-    for m, n, k in [(3, 5, 4), (1, 1, 1), (17, 9, 33), (64, 70, 65), (130, 129, 66)]:
+    # skinny shapes too: vector (n or m <= 8, k > 8) and outer-product (k <= 8) kernels
+    for m, n, k in [(3, 5, 4), (1, 1, 1), (17, 9, 33), (64, 70, 65), (130, 129, 66), (1, 1, 300), (130, 3, 200),
+                    (5, 130, 70), (70, 1, 130), (40, 2, 50), (66, 90, 3)]:
         for ta, tb in itertools.product([0, 1], repeat=2):
             a = r.standard_normal((B,) + ((k, m) if ta else (m, k))).astype(dt)
             b = r.standard_normal((B,) + ((n, k) if tb else (k, n))).astype(dt)
