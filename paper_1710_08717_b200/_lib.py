@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdla_b200.so")
+# DLA_LIB_PATH: an alternative in-tree build of the same library (tuning A/B runs)
+LIB_PATH = os.environ.get("DLA_LIB_PATH") or os.path.join(HERE, "libdla_b200.so")
 
 _i64, _int, _vp, _sz = C.c_int64, C.c_int, C.c_void_p, C.c_size_t
 

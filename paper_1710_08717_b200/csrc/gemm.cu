@@ -24,21 +24,29 @@
 // Batch and tiles share a flat grid.x (65536-slice batches exceed gridDim.z).
 #include "common.cuh"
 
+#ifndef DLAB_GEMM_BKL
+#define DLAB_GEMM_BKL 32  // k-block of the 128 x 128 configuration (3 stages: 212 KB smem)
+#endif
+#ifndef DLAB_GEMM_BKS
+#define DLAB_GEMM_BKS 16  // k-block of the 64 x 64 configuration
+#endif
+
 namespace dlab {
 namespace {
 
-constexpr int BK = 16, STAGES = 3, PAD = 4;
+constexpr int STAGES = 3, PAD = 4;
 
-// Tile configurations: CTA tile BM x BN, warp tile WM x WN (FP64 DMMA).
-template <int BM_, int BN_, int WM_, int WN_>
+// Tile configurations: CTA tile BM x BN, warp tile WM x WN (FP64 DMMA),
+// k-block BK per pipeline stage.
+template <int BM_, int BN_, int WM_, int WN_, int BK_ = 16>
 struct Cfg {
-  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_;
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, BK = BK_;
   static constexpr int WARPS_N = BN / WN;
   static constexpr int WARPS = (BM / WM) * (BN / WN);
   static constexpr int NT = WARPS * 32;
 };
-using CfgS = Cfg<64, 64, 32, 32>;    // 128 threads: small / batched problems
-using CfgL = Cfg<128, 128, 64, 32>;  // 256 threads: large trailing updates
+using CfgS = Cfg<64, 64, 32, 32, DLAB_GEMM_BKS>;  // 128 threads: small / batched problems
+using CfgL = Cfg<128, 128, 64, 32, DLAB_GEMM_BKL>;  // 256 threads: large trailing updates
 
 template <typename T>
 struct GemmArgs {
@@ -71,13 +79,13 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 // when !TA (rows of A are contiguous in k) and [k][m] when TA; B likewise
 // [k][n] when !TB and [n][k] when TB.  PAD = 4 elements keeps the 64-bit
 // fragment loads of a half-warp on distinct banks.
-template <int BM, bool TA>
+template <int BM, int BK, bool TA>
 struct ATile {
   static constexpr int LD = TA ? (BM + PAD) : (BK + PAD);
   static constexpr int ELEMS = TA ? BK * LD : BM * LD;
   __device__ static int idx(int i, int k) { return TA ? k * LD + i : i * LD + k; }
 };
-template <int BN, bool TB>
+template <int BN, int BK, bool TB>
 struct BTile {
   static constexpr int LD = TB ? (BK + PAD) : (BN + PAD);
   static constexpr int ELEMS = TB ? BN * LD : BK * LD;
@@ -88,7 +96,7 @@ struct BTile {
 template <typename T, class C, bool TA, bool TB, int VA, int VB>
 __device__ __forceinline__ void load_stage(const GemmArgs<T>& g, const T* A, const T* B, int64_t m0, int64_t n0,
                                            int64_t k0, T* sa, T* sb) {
-  constexpr int BM = C::BM, BN = C::BN, NT = C::NT;
+  constexpr int BM = C::BM, BN = C::BN, NT = C::NT, BK = C::BK;
   {
     constexpr int CH = (BM * BK) / VA;
 #pragma unroll
@@ -106,7 +114,7 @@ __device__ __forceinline__ void load_stage(const GemmArgs<T>& g, const T* A, con
       const int64_t gi = m0 + i, gk = k0 + k;
       const bool ok = gi < g.m && gk < g.k;
       const T* src = ok ? (TA ? A + gk * g.a.ld + gi : A + gi * g.a.ld + gk) : A;
-      cp_async(sa + ATile<BM, TA>::idx(i, k), src, ok, VA * (int)sizeof(T));
+      cp_async(sa + ATile<BM, BK, TA>::idx(i, k), src, ok, VA * (int)sizeof(T));
     }
   }
   {
@@ -126,7 +134,7 @@ __device__ __forceinline__ void load_stage(const GemmArgs<T>& g, const T* A, con
       const int64_t gj = n0 + j, gk = k0 + k;
       const bool ok = gj < g.n && gk < g.k;
       const T* src = ok ? (TB ? B + gj * g.b.ld + gk : B + gk * g.b.ld + gj) : B;
-      cp_async(sb + BTile<BN, TB>::idx(k, j), src, ok, VB * (int)sizeof(T));
+      cp_async(sb + BTile<BN, BK, TB>::idx(k, j), src, ok, VB * (int)sizeof(T));
     }
   }
 }
@@ -135,7 +143,7 @@ __device__ __forceinline__ void load_stage(const GemmArgs<T>& g, const T* A, con
 // blocks that straddle the diagonal need it).
 template <typename T, class C, bool TA, bool TB>
 __device__ __forceinline__ bool mask_stage(const GemmArgs<T>& g, int64_t m0, int64_t n0, int64_t k0, T* sa, T* sb) {
-  constexpr int BM = C::BM, BN = C::BN, NT = C::NT;
+  constexpr int BM = C::BM, BN = C::BN, NT = C::NT, BK = C::BK;
   bool touched = false;
   if (g.tri_a != TRI_NONE) {
     const bool lower = g.tri_a == TRI_LOWER;  // A(i,k) = 0 for k > i (lower) / k < i (upper)
@@ -144,7 +152,7 @@ __device__ __forceinline__ bool mask_stage(const GemmArgs<T>& g, int64_t m0, int
       for (int e = threadIdx.x; e < BM * BK; e += NT) {
         const int i = e / BK, k = e % BK;
         const int64_t gi = m0 + i, gk = k0 + k;
-        if (lower ? (gk > gi) : (gk < gi)) sa[ATile<BM, TA>::idx(i, k)] = T(0);
+        if (lower ? (gk > gi) : (gk < gi)) sa[ATile<BM, BK, TA>::idx(i, k)] = T(0);
       }
       touched = true;
     }
@@ -156,7 +164,7 @@ __device__ __forceinline__ bool mask_stage(const GemmArgs<T>& g, int64_t m0, int
       for (int e = threadIdx.x; e < BN * BK; e += NT) {
         const int k = e / BN, j = e % BN;
         const int64_t gj = n0 + j, gk = k0 + k;
-        if (lower ? (gk < gj) : (gk > gj)) sb[BTile<BN, TB>::idx(k, j)] = T(0);
+        if (lower ? (gk < gj) : (gk > gj)) sb[BTile<BN, BK, TB>::idx(k, j)] = T(0);
       }
       touched = true;
     }
@@ -172,7 +180,7 @@ __device__ __forceinline__ bool tile_masked_out(int mask, int64_t m0, int64_t n0
 }
 
 // Per-tile K range implied by triangular operands.
-template <typename T, int BM, int BN>
+template <typename T, int BM, int BN, int BK>
 __device__ __forceinline__ void k_range(const GemmArgs<T>& g, int64_t m0, int64_t n0, int64_t& klo, int64_t& khi) {
   klo = 0;
   khi = g.k;
@@ -227,9 +235,9 @@ __device__ __forceinline__ TileCoord<T> decode(const GemmArgs<T>& g) {
 // ------------------------------------------------------------------ f64 DMMA
 template <class C, bool TA, bool TB, int VA, int VB>
 __global__ void __launch_bounds__(C::NT) dgemm_dmma(GemmArgs<double> g) {
-  using AT = ATile<C::BM, TA>;
-  using BT = BTile<C::BN, TB>;
-  constexpr int MI = C::WM / 8, NI = C::WN / 8;
+  using AT = ATile<C::BM, C::BK, TA>;
+  using BT = BTile<C::BN, C::BK, TB>;
+  constexpr int MI = C::WM / 8, NI = C::WN / 8, BK = C::BK;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* smem = reinterpret_cast<double*>(smem_raw);
   double* sA = smem;
@@ -240,7 +248,7 @@ __global__ void __launch_bounds__(C::NT) dgemm_dmma(GemmArgs<double> g) {
   if (g.skip && g.skip[tc.bo]) return;
   if (tile_masked_out<C::BM, C::BN>(g.mask, m0, n0)) return;
   int64_t klo, khi;
-  k_range<double, C::BM, C::BN>(g, m0, n0, klo, khi);
+  k_range<double, C::BM, C::BN, C::BK>(g, m0, n0, klo, khi);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = (warp / C::WARPS_N) * C::WM, wn = (warp % C::WARPS_N) * C::WN;
@@ -355,8 +363,9 @@ template <bool TA, bool TB, int VA, int VB>
 __global__ void __launch_bounds__(256) sgemm_ffma(GemmArgs<float> g) {
   using C = Cfg<64, 64, 32, 16>;  // 8 warps -> 256 threads; smem geometry of a 64 x 64 tile
   static_assert(C::NT == 256, "sgemm thread count");
-  using AT = ATile<64, TA>;
-  using BT = BTile<64, TB>;
+  constexpr int BK = C::BK;
+  using AT = ATile<64, BK, TA>;
+  using BT = BTile<64, BK, TB>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* smem = reinterpret_cast<float*>(smem_raw);
   float* sA = smem;
@@ -367,7 +376,7 @@ __global__ void __launch_bounds__(256) sgemm_ffma(GemmArgs<float> g) {
   if (g.skip && g.skip[tc.bo]) return;
   if (tile_masked_out<64, 64>(g.mask, m0, n0)) return;
   int64_t klo, khi;
-  k_range<float, 64, 64>(g, m0, n0, klo, khi);
+  k_range<float, 64, 64, BK>(g, m0, n0, klo, khi);
 
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 4x4 each
   float acc[4][4];
@@ -433,7 +442,7 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large) 
       using C = CfgL;
       g.tiles_m = (g.m + C::BM - 1) / C::BM;
       g.tiles_n = (g.n + C::BN - 1) / C::BN;
-      const size_t smem = sizeof(T) * STAGES * (ATile<C::BM, TA>::ELEMS + BTile<C::BN, TB>::ELEMS);
+      const size_t smem = sizeof(T) * STAGES * (ATile<C::BM, C::BK, TA>::ELEMS + BTile<C::BN, C::BK, TB>::ELEMS);
       auto k = dgemm_dmma<C, TA, TB, VA, VB>;
       static bool attr = false;
       if (!attr) {
@@ -445,7 +454,7 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large) 
       using C = CfgS;
       g.tiles_m = (g.m + C::BM - 1) / C::BM;
       g.tiles_n = (g.n + C::BN - 1) / C::BN;
-      const size_t smem = sizeof(T) * STAGES * (ATile<C::BM, TA>::ELEMS + BTile<C::BN, TB>::ELEMS);
+      const size_t smem = sizeof(T) * STAGES * (ATile<C::BM, C::BK, TA>::ELEMS + BTile<C::BN, C::BK, TB>::ELEMS);
       auto k = dgemm_dmma<C, TA, TB, VA, VB>;
       static bool attr = false;
       if (!attr) {
@@ -458,7 +467,7 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large) 
     (void)large;
     g.tiles_m = (g.m + 63) / 64;
     g.tiles_n = (g.n + 63) / 64;
-    const size_t smem = sizeof(T) * STAGES * (ATile<64, TA>::ELEMS + BTile<64, TB>::ELEMS);
+    const size_t smem = sizeof(T) * STAGES * (ATile<64, 16, TA>::ELEMS + BTile<64, 16, TB>::ELEMS);
     auto k = sgemm_ffma<TA, TB, VA, VB>;
     static bool attr = false;
     if (!attr) {
