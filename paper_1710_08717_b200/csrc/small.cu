@@ -237,6 +237,73 @@ __device__ __forceinline__ void warp_ltinv_col(const T* Ls, T (&x)[WN], int n) {
   }
 }
 
+// Murray backward of one n <= 32 factor held by a warp, from shared memory:
+// L = unit-diagonal L D^{-1} (LLD rows), dg / rd = D / D^{-1}, W = Lbar
+// (column `lane` per lane; only its lower triangle is used).  Writes
+// Abar = 1/2 sym(L^-T copyltu(L^T Lbar) L^-1) to o (dl/adjoints.hpp:175-191).
+template <typename T>
+__device__ __forceinline__ void warp_potrf_bwd_core(int n, int lane, const T* L, T* W, const T* dg, const T* rd, T* o,
+                                                    int ldo) {
+  constexpr int VN = Bc<T>::N, LLD = Bc<T>::LLD;
+  // Phi = copyltu(L^T Lbar), lower part of column `lane`: Phi_ij = sum_{k>=i} L_ki Lbar_kj
+  // (i >= j = lane) = L_ii (Lbar_ij + sum_{k>i} Ls_ki Lbar_kj), accumulated row by row of Ls
+  T acc[WN];
+#pragma unroll
+  for (int i = 0; i < WN; ++i) acc[i] = T(0);
+#pragma unroll
+  for (int k = 0; k < WN; ++k) {
+    if (k < n) {
+      const T xk = lane < n ? W[k * WLD + lane] : T(0);
+      acc[k] += xk;  // unit diagonal
+#pragma unroll
+      for (int i0 = 0; i0 < k; i0 += VN) {
+        T v[VN];
+        Bc<T>::ld(L + k * LLD + i0, v);
+#pragma unroll
+        for (int u = 0; u < VN; ++u)
+          if (i0 + u < k) acc[i0 + u] += v[u] * xk;
+      }
+    }
+  }
+  __syncwarp();
+  // mirror into W: W(i, j) = W(j, i) = Phi_ij
+#pragma unroll
+  for (int i = 0; i < WN; ++i)
+    if (i < n && lane < n && i >= lane) {
+      const T p = acc[i] * dg[i];
+      W[i * WLD + lane] = p;
+      W[lane * WLD + i] = p;
+    }
+  __syncwarp();
+  T x[WN];
+#pragma unroll
+  for (int i = 0; i < WN; ++i) x[i] = (i < n && lane < n) ? W[i * WLD + lane] * rd[i] : T(0);
+  // X = L^{-T} Phi (column `lane`), then through shared memory X^T = Phi L^{-1}
+  warp_ltinv_col<T>(L, x, n);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < WN; ++i)
+    if (i < n && lane < n) W[i * WLD + lane] = x[i];
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < WN; ++i) x[i] = (i < n && lane < n) ? W[lane * WLD + i] * rd[i] : T(0);
+  // Y = L^{-T} (Phi L^{-1}) = L^{-T} Phi L^{-1}; column `lane`
+  warp_ltinv_col<T>(L, x, n);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < WN; ++i)
+    if (i < n && lane < n) W[i * WLD + lane] = x[i];
+  __syncwarp();
+  // Abar = sym(Y / 2), exactly symmetric: element (i, lane) pairs this lane's
+  // Y(i, lane) with Y(lane, i) from shared memory
+#pragma unroll
+  for (int i = 0; i < WN; ++i)
+    if (i < n && lane < n) {
+      const T hi = x[i] * T(0.5), hj = W[lane * WLD + i] * T(0.5);
+      o[i * ldo + lane] = (i == lane) ? hi : (hi + hj) * T(0.5);  // == (hi + hj) / 2 exactly
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(wpc_bwd<T>() * 32, sizeof(T) == 8 ? 3 : 2) k_potrf_bwd_warp(int n, int64_t batch,
                                                                                       MatB<T> abar,
@@ -289,64 +356,7 @@ __global__ void __launch_bounds__(wpc_bwd<T>() * 32, sizeof(T) == 8 ? 3 : 2) k_p
     }
   }
   __syncwarp();
-  // Phi = copyltu(L^T Lbar), lower part of column `lane`: Phi_ij = sum_{k>=i} L_ki Lbar_kj
-  // (i >= j = lane) = L_ii (Lbar_ij + sum_{k>i} Ls_ki Lbar_kj), accumulated row by row of Ls
-  T acc[WN];
-#pragma unroll
-  for (int i = 0; i < WN; ++i) acc[i] = T(0);
-#pragma unroll
-  for (int k = 0; k < WN; ++k) {
-    if (k < n) {
-      const T xk = lane < n ? W[k * WLD + lane] : T(0);
-      acc[k] += xk;  // unit diagonal
-#pragma unroll
-      for (int i0 = 0; i0 < k; i0 += VN) {
-        T v[VN];
-        Bc<T>::ld(L + k * LLD + i0, v);
-#pragma unroll
-        for (int u = 0; u < VN; ++u)
-          if (i0 + u < k) acc[i0 + u] += v[u] * xk;
-      }
-    }
-  }
-  __syncwarp();
-  // mirror into W: W(i, j) = W(j, i) = Phi_ij
-#pragma unroll
-  for (int i = 0; i < WN; ++i)
-    if (i < n && lane < n && i >= lane) {
-      const T p = acc[i] * dg[i];
-      W[i * WLD + lane] = p;
-      W[lane * WLD + i] = p;
-    }
-  __syncwarp();
-  T x[WN];
-#pragma unroll
-  for (int i = 0; i < WN; ++i) x[i] = (i < n && lane < n) ? W[i * WLD + lane] * rd[i] : T(0);
-  // X = L^{-T} Phi (column `lane`), then through shared memory X^T = Phi L^{-1}
-  warp_ltinv_col<T>(L, x, n);
-  __syncwarp();
-#pragma unroll
-  for (int i = 0; i < WN; ++i)
-    if (i < n && lane < n) W[i * WLD + lane] = x[i];
-  __syncwarp();
-#pragma unroll
-  for (int i = 0; i < WN; ++i) x[i] = (i < n && lane < n) ? W[lane * WLD + i] * rd[i] : T(0);
-  // Y = L^{-T} (Phi L^{-1}) = L^{-T} Phi L^{-1}; column `lane`
-  warp_ltinv_col<T>(L, x, n);
-  __syncwarp();
-#pragma unroll
-  for (int i = 0; i < WN; ++i)
-    if (i < n && lane < n) W[i * WLD + lane] = x[i];
-  __syncwarp();
-  // Abar = sym(Y / 2), exactly symmetric: element (i, lane) pairs this lane's
-  // Y(i, lane) with Y(lane, i) from shared memory
-  T* o = abar.at(b, 0, 0);
-#pragma unroll
-  for (int i = 0; i < WN; ++i)
-    if (i < n && lane < n) {
-      const T hi = x[i] * T(0.5), hj = W[lane * WLD + i] * T(0.5);
-      o[i * ldo + lane] = (i == lane) ? hi : (hi + hj) * T(0.5);  // == (hi + hj) / 2 exactly
-    }
+  warp_potrf_bwd_core<T>(n, lane, L, W, dg, rd, abar.at(b, 0, 0), ldo);
 }
 
 }  // namespace

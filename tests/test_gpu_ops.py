@@ -181,6 +181,18 @@ def test_trmm_trsm_backward(port, dt):
         assert torch.equal(ga2, ga) and torch.equal(gt2, gt)
 
 
+@pytest.mark.parametrize("dt", DTYPES)
+def test_trsv_narrow_large(port, dt):
+    """The one-launch narrow solve (<= 8 vectors, n > 64): every flag set at
+    sizes with a ragged last block, more blocks than SMs, and a batch."""
+    r = O.rng(41)
+    for (nt, nv, B), (right, tr, lo) in itertools.product([(1000, 1, 2), (577, 8, 1), (2112, 3, 3)], FLAGS):
+        t = tri_factor(r, nt, lo, dt, B)
+        x = r.standard_normal((B, nv, nt) if right else (B, nt, nv)).astype(dt)
+        got = host(L.trsm(dev(t), dev(x), right, tr, lo, 0.7))
+        assert_close(got, batch_apply(lambda tt, xx: port.trsm(tt, xx, right, tr, lo, 0.7), t, x), dt, 10)
+
+
 def test_trsm_singular_reports_index_and_leaves_slice():
     t = dev(np.array([[[2.0, 0], [1, 1]], [[1.0, 0], [5, 0]]]))
     x0 = np.array([[[2.0], [3.0]], [[2.0], [3.0]]])
