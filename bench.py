@@ -292,15 +292,31 @@ def run_potrf_batch(torch, n, B, steps, warmup, world):
 
 def also_measurements(torch, args, world, lib, fp64_peak, hbm):
     out = []
-    # C1 chain, batch 64 x 32^2 (latency regime) and a large-batch sweep point
+    # C1 chain, batch 64 x 32^2 (latency regime) and a large-batch point:
+    # the fused one-launch chain (dla_chol_chain_fwdbwd) and, at batch 64, the
+    # same chain through the per-operator C-ABI
+    from paper_1710_08717_b200 import linalg as L
+    from oracle import oracle as O
+    n = 32
+    flops1 = n ** 3 / 3 + 4 * n ** 3 / 3 + 4 * n * n
     for B in (64, 65536):
-        step, _ = c1_chain_fns(torch, B)
-        ms = timed(torch, graphed(torch, step), 20, 3, world)
-        n = 32
-        flops = B * (n ** 3 / 3 + 4 * n ** 3 / 3 + 4 * n * n)
-        out.append({"workload": f"C1 chain potrf+trsm+sumlogdiag fwd+bwd, batch {B} x 32^2 fp64",
+        r = O.rng(7)
+        a0 = torch.from_numpy(O.random_spd(n, r, batch=B)).cuda()
+        y0 = torch.from_numpy(r.standard_normal((B, n, 1))).cuda()
+        phi = torch.empty(B, dtype=torch.float64, device="cuda")
+        ab, yb = torch.empty_like(a0), torch.empty_like(y0)
+        info = torch.zeros(B, dtype=torch.int32, device="cuda")
+        ms = timed(torch, graphed(torch, lambda: L.chol_chain_fwdbwd(a0, y0, phi, ab, yb, check=False, info=info)),
+                   20, 3, world)
+        out.append({"workload": f"C1 chain fused (one launch), batch {B} x 32^2 fp64",
                     "matrices_per_s": world * B / (ms / 1e3), "ms_per_step": ms,
-                    "gflops": world * flops / (ms / 1e3) / 1e9})
+                    "gflops": world * B * flops1 / (ms / 1e3) / 1e9,
+                    "hbm_gb_per_s": B * (2 * n * n + 2 * n + 1) * 8 / (ms / 1e3) / 1e9})
+    step, _ = c1_chain_fns(torch, 64)
+    ms = timed(torch, graphed(torch, step), 20, 3, world)
+    out.append({"workload": "C1 chain via 7 per-operator C-ABI calls, batch 64 x 32^2 fp64",
+                "matrices_per_s": world * 64 / (ms / 1e3), "ms_per_step": ms,
+                "gflops": world * 64 * flops1 / (ms / 1e3) / 1e9})
     for n, B in ((1024, 8), (32, 65536)):
         ms = run_potrf_batch(torch, n, B, 10 if n > 64 else 20, 3, world)
         flops = B * 5 * n ** 3 / 3

@@ -202,6 +202,23 @@ long long dla_launch_count(void);
 void dla_prof_enable(int on);
 long long dla_prof_read(double* ms, double* flops);
 
+/* ----------------------------------------------- fused C1 likelihood chain */
+/* Gaussian log-likelihood chain over a batch of small SPD matrices
+ * (BASELINE config C1; the make_gp graph dl/models.hpp:99-103 given A):
+ *   L = potrf(A);  z = L^-1 y;  phi[b] = 1/2 z^T z + sum_i log L_ii
+ * and its pullback at phibar = 1: ybar = L^-T z and Abar = dphi/dA (trsm,
+ * sumlogdiag and potrf backward: dl/adjoints.hpp:131-153, 175-191,
+ * dl/tape.hpp:1038-1045).  a, abar: [batch, n, n]; y, ybar: [batch, n, 1];
+ * phi: [batch].  n <= 32 runs as ONE launch (one warp per matrix); larger n
+ * composes the operators.  Failures as potrf (info: ASYMMETRIC, NOT_SPD(step));
+ * outputs of a failed slice are untouched.  No output may overlap an input. */
+dla_status dla_chol_chain_fwdbwd_f64(int64_t batch, int64_t n, const double* a, const double* y,
+                                     double* phi, double* abar, double* ybar, int32_t* info,
+                                     void* stream);
+dla_status dla_chol_chain_fwdbwd_f32(int64_t batch, int64_t n, const float* a, const float* y,
+                                     float* phi, float* abar, float* ybar, int32_t* info,
+                                     void* stream);
+
 /* ------------------------------------------------------------ GP driver */
 /* Fused RBF-kernel build and pullback for the Gaussian-process NLL driver
  * (dl/models.hpp:50-65 rbf_kernel + :95-98 K + lam I; pullbacks of the tape

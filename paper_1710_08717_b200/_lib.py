@@ -44,6 +44,7 @@ _SIGS = {
     "gelqf_bwd": "IIIPPPPPPZP",
     "syevd_fwd": "IIPPPPZP",
     "syevd_bwd": "IIPPPPPSPZP",
+    "chol_chain_fwdbwd": "IIPPPPPPP",
 }
 
 

@@ -428,6 +428,52 @@ dla_status syevd_bwd_abi(int64_t batch, int64_t n, T* abar, const T* ubar, const
 
 using namespace dlab;
 
+// ------------------------------------------------- fused C1 chain (GP NLL)
+__global__ void k_fill_ones(int64_t n, double* pd, float* pf) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (pd) pd[i] = 1.0;
+    if (pf) pf[i] = 1.0f;
+  }
+}
+
+// phi = 1/2 |L^-1 y|^2 + sumlogdiag(L), L = potrf(A); ybar, Abar at phibar = 1.
+// n <= 32: one fused warp-per-matrix launch (small.cu); otherwise the
+// operator chain (the reference's own composition) on stream-ordered scratch.
+template <typename T>
+dla_status chol_chain_abi(int64_t batch, int64_t n, const T* a, const T* y, T* phi, T* abar, T* ybar,
+                          int32_t* info, void* stream) {
+  if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
+  const size_t asz = bytes<T>(batch, n, n), ysz = bytes<T>(batch, n, 1), psz = bytes<T>(batch, 1, 1);
+  if (overlap(abar, asz, a, asz) || overlap(abar, asz, y, ysz) || overlap(ybar, ysz, a, asz) ||
+      overlap(ybar, ysz, y, ysz) || overlap(phi, psz, a, asz) || overlap(phi, psz, y, ysz) ||
+      overlap(abar, asz, ybar, ysz) || overlap(phi, psz, abar, asz) || overlap(phi, psz, ybar, ysz))
+    return DLA_ERR_ALIAS;
+  Ctx cx = make_ctx(stream, info);
+  DLAB_TRY(reset_info(cx, batch));
+  if (batch == 0) return DLA_OK;
+  if (n == 0) return cudaMemsetAsync(phi, 0, psz, cx.stream) == cudaSuccess ? DLA_OK : DLA_ERR_CUDA;
+  if (n <= 32) return chol_chain_small<T>(cx, batch, n, cpk(a, n, n), y, phi, pk(abar, n, n), ybar);
+  Scratch ws(asz + ysz + psz, cx.stream);
+  if (!ws.p) return DLA_ERR_CUDA;
+  T* l = ws.as<T>();
+  T* z = l + batch * n * n;
+  T* ones = z + batch * n;
+  k_fill_ones<<<blocks_for(batch, 256), 256, 0, cx.stream>>>(batch, sizeof(T) == 8 ? (double*)ones : nullptr,
+                                                             sizeof(T) == 4 ? (float*)ones : nullptr);
+  DLAB_LAUNCH_CHECK();
+  if (cudaMemcpyAsync(l, a, asz, cudaMemcpyDeviceToDevice, cx.stream) != cudaSuccess ||
+      cudaMemcpyAsync(z, y, ysz, cudaMemcpyDeviceToDevice, cx.stream) != cudaSuccess)
+    return DLA_ERR_CUDA;
+  DLAB_TRY(potrf_fwd<T>(batch, n, l, 1, info, stream));
+  // later ops skip failed slices through info (dl/matrix.hpp:232-239 semantics)
+  DLAB_TRY(trsm<T>(cx, batch, n, 1, cpk(l, n, n), pk(z, n, 1), false, false, true, T(1)));
+  DLAB_TRY(sumlogdiag_fwd<T>(cx, batch, n, phi, cpk(l, n, n)));
+  DLAB_TRY(gemm<T>(cx, batch, 1, 1, n, T(0.5), cpk(z, n, 1), true, cpk(z, n, 1), false, T(1), pk(phi, 1, 1)));
+  DLAB_TRY(trsm_bwd<T>(batch, n, 1, ybar, abar, z, l, z, 0, 0, 1, T(1), stream));
+  DLAB_TRY(sumlogdiag_bwd<T>(cx, batch, n, pk(abar, n, n), ones, cpk(l, n, n), true));
+  return potrf_bwd<T>(batch, n, abar, abar, l, 1, stream);
+}
+
 extern "C" {
 
 const char* dla_status_string(dla_status s) {
@@ -587,5 +633,14 @@ dla_status dla_info_check(const int32_t* info, int64_t batch, void* stream, int6
 
 DLA_DEFINE(float, f32)
 DLA_DEFINE(double, f64)
+
+dla_status dla_chol_chain_fwdbwd_f64(int64_t batch, int64_t n, const double* a, const double* y, double* phi,
+                                     double* abar, double* ybar, int32_t* info, void* stream) {
+  return chol_chain_abi<double>(batch, n, a, y, phi, abar, ybar, info, stream);
+}
+dla_status dla_chol_chain_fwdbwd_f32(int64_t batch, int64_t n, const float* a, const float* y, float* phi,
+                                     float* abar, float* ybar, int32_t* info, void* stream) {
+  return chol_chain_abi<float>(batch, n, a, y, phi, abar, ybar, info, stream);
+}
 
 }  // extern "C"

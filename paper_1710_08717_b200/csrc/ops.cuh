@@ -14,6 +14,12 @@ template <typename T>
 dla_status potrf_bwd_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> lbar,
                            MatB<const T> l, bool lower);
 
+// Fused C1 chain (n <= 32, warp per matrix): phi = 1/2 |L^-1 y|^2 + sumlogdiag(L),
+// L = potrf(A), with ybar and Abar at phibar = 1.
+template <typename T>
+dla_status chol_chain_small(const Ctx& c, int64_t batch, int64_t n, MatB<const T> a, const T* y, T* phi, MatB<T> abar,
+                            T* ybar);
+
 // inv.cu — inverse-based large-n paths (n = 64 * 2^k, n >= 256)
 template <typename T>
 bool inv_eligible(int64_t n);

@@ -359,6 +359,122 @@ __global__ void __launch_bounds__(wpc_bwd<T>() * 32, sizeof(T) == 8 ? 3 : 2) k_p
   warp_potrf_bwd_core<T>(n, lane, L, W, dg, rd, abar.at(b, 0, 0), ldo);
 }
 
+
+// Fused Gaussian log-likelihood chain, one warp per matrix (n <= 32), the
+// whole of BASELINE config C1 in one launch (dl/models.hpp:99-103 given A):
+//   L = potrf(A) (dl/cholesky.hpp:35-72), z = L^-1 y (dl/blas.hpp:307-395),
+//   phi = 1/2 z^T z + sum_i log L_ii (dl/tape.hpp:789-795)
+// and its pullback at phibar = 1: zbar = z; S = L^-T zbar = ybar;
+// Lbar = -tril(S z^T) + diag(1 / L_ii) (dl/adjoints.hpp:136-152,
+// dl/tape.hpp:1038-1045); Abar = potrf pullback (warp_potrf_bwd_core).
+// A and y are read once, Abar / ybar / phi written once.
+template <typename T>
+__global__ void __launch_bounds__(wpc_bwd<T>() * 32) k_chol_chain_warp(int n, int64_t batch, MatB<const T> a,
+                                                                       const T* y, T* phi, MatB<T> abar, T* ybar,
+                                                                       int32_t* info) {
+  constexpr int LLD = Bc<T>::LLD;
+  constexpr int per_warp = WN * LLD + WN * WLD + 6 * WN;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b = (int64_t)blockIdx.x * wpc_bwd<T>() + warp;
+  if (b >= batch) return;
+  T* L = reinterpret_cast<T*>(smem_raw) + warp * per_warp;  // unit-diagonal L D^-1 (LLD rows)
+  T* W = L + WN * LLD;                                       // A, then L (rows), then Lbar (columns)
+  T* buf = W + WN * WLD;
+  T* dg = buf + 2 * WN;
+  T* rd = dg + WN;
+  T* sv = rd + WN;
+  T* lg = sv + WN;
+  const T* ga = a.at(b, 0, 0);
+  const int ld = (int)a.ld;
+  {
+    T v[WN];
+#pragma unroll
+    for (int i = 0; i < WN; ++i) v[i] = (i < n && lane < n) ? ga[i * ld + lane] : T(0);
+#pragma unroll
+    for (int i = 0; i < WN; ++i)
+      if (i < n) W[i * WLD + lane] = v[i];
+  }
+  T yv = lane < n ? y[b * n + lane] : T(0);
+  __syncwarp();
+  // symmetry precheck (dl/cholesky.hpp:19-25), as k_potrf_warp
+  T mabs = T(0), masym = T(0);
+  if (lane < n)
+    for (int j = 0; j < n; ++j) {
+      const T v = W[lane * WLD + j];
+      if (fabs(v) > mabs) mabs = fabs(v);
+      if (j > lane) {
+        const T d = fabs(v - W[j * WLD + lane]);
+        if (d > masym) masym = d;
+      }
+    }
+  mabs = warp_max(mabs);
+  masym = warp_max(masym);
+  if (masym > Num<T>::sym_rtol * (mabs > T(0) ? mabs : T(1))) {
+    if (lane == 0) record_failure(info, b, DLA_ERR_ASYMMETRIC, 0);
+    return;
+  }
+  T r[WN];
+#pragma unroll
+  for (int c = 0; c < WN; ++c) r[c] = (lane < n && c <= lane) ? W[lane * WLD + c] : (c == lane ? T(1) : T(0));
+  int failed = -1;
+  wchol_col<T, 0>(r, lane, n, buf, failed, r[0]);
+  if (failed >= 0) {
+    if (lane == 0) record_failure(info, b, DLA_ERR_NOT_SPD, failed);
+    return;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < WN; ++c)
+    if (c < n && lane < n) W[lane * WLD + c] = c <= lane ? r[c] : T(0);
+  __syncwarp();
+  const T d = lane < n ? W[lane * WLD + lane] : T(1);
+  const T rinv = T(1) / d;
+  dg[lane] = d;
+  rd[lane] = rinv;
+#pragma unroll
+  for (int i = 0; i < WN; ++i)
+    if (i < n) L[i * LLD + lane] = lane < i ? (lane < n ? W[i * WLD + lane] * rinv : T(0)) : (lane == i ? T(1) : T(0));
+  // z = L^-1 y, column-oriented: z_j = y_j / L_jj moves by one shuffle
+  T z = T(0);
+#pragma unroll
+  for (int j = 0; j < WN; ++j) {
+    if (j < n) {
+      const T zj = __shfl_sync(0xffffffffu, yv * rinv, j);
+      if (lane == j) z = zj;
+      if (lane > j) yv -= r[j] * zj;
+    }
+  }
+  sv[lane] = lane < n ? z : T(0);
+  lg[lane] = lane < n ? Num<T>::log_(d) : T(0);
+  __syncwarp();
+  if (lane == 0) {  // sequential i order, as the tape's Sum node
+    T q = T(0), ldt = T(0);
+    for (int i = 0; i < n; ++i) q += sv[i] * sv[i];
+    for (int i = 0; i < n; ++i) ldt += lg[i];
+    phi[b] = T(0.5) * q + ldt;
+  }
+  // S = L^-T z (zbar = z), row k of L read from W
+  T zb = z, s_own = T(0);
+#pragma unroll
+  for (int k = WN - 1; k >= 0; --k) {
+    if (k < n) {
+      const T sk = __shfl_sync(0xffffffffu, zb * rinv, k);
+      if (lane == k) s_own = sk;
+      if (lane < k) zb -= W[k * WLD + lane] * sk;
+    }
+  }
+  if (lane < n) ybar[b * n + lane] = s_own;
+  __syncwarp();
+  sv[lane] = lane < n ? s_own : T(0);
+  __syncwarp();
+  // Lbar, column `lane`: -s_i z_lane (i >= lane) + 1 / L_ii on the diagonal
+#pragma unroll
+  for (int i = 0; i < WN; ++i)
+    if (i < n) W[i * WLD + lane] = (i >= lane && lane < n) ? -sv[i] * z + (i == lane ? rinv : T(0)) : T(0);
+  __syncwarp();
+  warp_potrf_bwd_core<T>(n, lane, L, W, dg, rd, abar.at(b, 0, 0), (int)abar.ld);
+}
 }  // namespace
 
 template <typename T>
@@ -421,10 +537,28 @@ dla_status potrf_bwd_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar,
   return DLA_OK;
 }
 
+
+template <typename T>
+dla_status chol_chain_small(const Ctx& c, int64_t batch, int64_t n, MatB<const T> a, const T* y, T* phi, MatB<T> abar,
+                            T* ybar) {
+  constexpr int wpc = wpc_bwd<T>();
+  const size_t sm = sizeof(T) * wpc * (WN * Bc<T>::LLD + WN * WLD + 6 * WN);
+  static bool once = false;
+  if (!once) {
+    cudaFuncSetAttribute(k_chol_chain_warp<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    once = true;
+  }
+  k_chol_chain_warp<T><<<(unsigned)((batch + wpc - 1) / wpc), wpc * 32, sm, c.stream>>>((int)n, batch, a, y, phi,
+                                                                                       abar, ybar, c.info);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+
 #define INST(T)                                                                                     \
   template bool potrf_small_eligible<T>(int64_t);                                                   \
   template dla_status potrf_small<T>(const Ctx&, int64_t, int64_t, MatB<T>, bool);                  \
-  template dla_status potrf_bwd_small<T>(const Ctx&, int64_t, int64_t, MatB<T>, MatB<const T>, MatB<const T>, bool);
+  template dla_status potrf_bwd_small<T>(const Ctx&, int64_t, int64_t, MatB<T>, MatB<const T>, MatB<const T>, bool); \
+  template dla_status chol_chain_small<T>(const Ctx&, int64_t, int64_t, MatB<const T>, const T*, T*, MatB<T>, T*);
 INST(double)
 INST(float)
 

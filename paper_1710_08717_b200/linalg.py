@@ -302,6 +302,24 @@ def sumlogdiag(a, out=None):
     return out
 
 
+def chol_chain_fwdbwd(a, y, phi=None, abar=None, ybar=None, check=True, info=None):
+    """Fused C1 chain: phi = 1/2 |L^-1 y|^2 + sumlogdiag(L), L = potrf(A), with
+    (ybar, Abar) at phibar = 1 -- the make_gp graph of dl/models.hpp:99-103
+    given A.  a: [B, n, n], y: [B, n, 1].  One launch for n <= 32."""
+    batch = _prep("chol_chain", a, y)
+    n = _square(a, "chol_chain")
+    if tuple(y.shape[-2:]) != (n, 1):
+        raise ShapeError(f"chol_chain: y must be [.., {n}, 1], got {tuple(y.shape)}")
+    phi = torch.empty(batch, dtype=a.dtype, device=a.device) if phi is None else phi
+    abar = torch.empty_like(a) if abar is None else abar
+    ybar = torch.empty_like(y) if ybar is None else ybar
+    info = _info(batch, a.device) if info is None else info
+    _call("chol_chain_fwdbwd", a, batch, n, _p(a), _p(y), _p(phi), _p(abar), _p(ybar), _p(info), _stream(a))
+    if check:
+        _check(info, batch, a, "chol_chain")
+    return phi, abar, ybar
+
+
 def gelqf_inplace(q, l, check=True):
     """dl/lq.hpp:24-106: q in = A (m x n, m <= n), out = Q; l out = L."""
     batch = _prep("gelqf", q, l)

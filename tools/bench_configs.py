@@ -36,13 +36,43 @@ def run(torch, args, rank, world, lib, fp64_peak, hbm):
     ref = O.ref() if O.ref_available() else None
     if cfg == "c1":
         B, n = 64, 32
-        step, (a0, y0, _, _) = bench.c1_chain_fns(torch, B, n)
+        # (1) the fused chain (dla_chol_chain_fwdbwd: ONE launch) -- the value
+        r = O.rng(7)
+        a0 = torch.from_numpy(O.random_spd(n, r, batch=B)).cuda()
+        y0 = torch.from_numpy(r.standard_normal((B, n, 1))).cuda()
+        phi = torch.empty(B, dtype=torch.float64, device="cuda")
+        abar, ybar = torch.empty_like(a0), torch.empty_like(y0)
+        info = torch.zeros(B, dtype=torch.int32, device="cuda")
+
+        def fused():
+            L.chol_chain_fwdbwd(a0, y0, phi, abar, ybar, check=False, info=info)
+
         c0 = lib.dla_launch_count()
-        step()
+        fused()
         torch.cuda.synchronize()
         launches = lib.dla_launch_count() - c0
-        ms = bench.timed(torch, bench.graphed(torch, step), args.steps, args.warmup, world)
+        ms = bench.timed(torch, bench.graphed(torch, fused), args.steps, args.warmup, world)
+        # (2) the same chain through the per-operator C-ABI (potrf, trsm, gemm2,
+        #     sumlogdiag, trsm_bwd, sumlogdiag_bwd, potrf_bwd)
+        step, _ = bench.c1_chain_fns(torch, B, n)
+        ms_ops = bench.timed(torch, bench.graphed(torch, step), args.steps, args.warmup, world)
         flops = n ** 3 / 3 + 4 * n ** 3 / 3 + 4 * n * n
+        bytes_per = (2 * n * n + 2 * n + 1) * 8  # read A, y; write Abar, ybar, phi
+        # batch sweep of the fused chain (HBM regime), L2 flushed by size
+        sweep = []
+        for Bs in (1024, 65536, 1 << 20):
+            if Bs * n * n * 8 * 2 > 0.5 * torch.cuda.get_device_properties(0).total_memory:
+                continue
+            a1 = torch.from_numpy(O.random_spd(n, O.rng(3), batch=1)).cuda().expand(Bs, n, n).contiguous()
+            y1 = torch.randn(Bs, n, 1, dtype=torch.float64, device="cuda")
+            p1, ab1, yb1 = torch.empty(Bs, dtype=torch.float64, device="cuda"), torch.empty_like(a1), torch.empty_like(y1)
+            i1 = torch.zeros(Bs, dtype=torch.int32, device="cuda")
+            f1 = lambda: L.chol_chain_fwdbwd(a1, y1, p1, ab1, yb1, check=False, info=i1)  # noqa: E731
+            ms1 = bench.timed(torch, bench.graphed(torch, f1), 5, 3, world)
+            sweep.append({"batch": Bs, "ms": ms1, "matrices_per_s": world * Bs / (ms1 / 1e3),
+                          "gb_per_s": Bs * bytes_per / (ms1 / 1e3) / 1e9,
+                          "frac_of_hbm": Bs * bytes_per / (ms1 / 1e3) / 1e9 / hbm})
+            del a1, y1, p1, ab1, yb1, i1
         cpu = None
         if ref is not None and rank == 0:
             a = a0.cpu().numpy()
@@ -54,10 +84,19 @@ def run(torch, args, rank, world, lib, fp64_peak, hbm):
             cpu = {"value": reps * B / secs, "unit": "matrices/s", "cores": 1, "kind": "reference",
                    "sample": f"{reps} x reference C1 chain over batch {B} (for_each_slice, 1 thread)"}
         v = world * B / (ms / 1e3)
+        big = sweep[-1] if sweep else None
         return _line(args, world, "C1 chain matrices/s", v, "matrices/s", ms,
-                     "C1: batch 64 x 32^2 fp64 potrf fwd+bwd + trsm + sumlogdiag (fused small-n kernels)",
+                     "C1: batch 64 x 32^2 fp64 potrf fwd+bwd + trsm + sumlogdiag (fused one-launch chain, "
+                     "dla_chol_chain_fwdbwd_f64)",
                      gflops=v * flops / 1e9, gpu_launches=launches * args.steps, cpu_baseline=cpu,
-                     roofline={"bound": "latency", "note": "64 x 8 KiB = 512 KiB per step: launch/latency bound"})
+                     operator_chain={"ms_per_step": ms_ops, "matrices_per_s": world * B / (ms_ops / 1e3),
+                                     "note": "same chain via 7 per-operator C-ABI calls (graph-replayed)"},
+                     batch_sweep=sweep,
+                     roofline={"bound": "hbm", "kernel": "k_chol_chain_warp",
+                               "achieved": big["gb_per_s"] if big else None, "peak": hbm, "unit": "GB/s",
+                               "frac": big["frac_of_hbm"] if big else None, "traffic": None,
+                               "note": f"at batch {big['batch'] if big else '-'} (batch 64 = 1 MiB per step is "
+                                       f"launch/latency bound); algorithmic bytes (2n^2+2n+1)*8 per matrix"})
     if cfg == "potrf1024":
         B, n = 8, 1024
         ms = bench.run_potrf_batch(torch, n, B, args.steps, args.warmup, world)
