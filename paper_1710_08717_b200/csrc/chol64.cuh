@@ -11,12 +11,16 @@ namespace dlab {
 
 constexpr int CH_LD = 65;  // smem row stride for a 64 x 64 block
 
+#ifndef DLAB_CHOL_W
+#define DLAB_CHOL_W(NMAX) 16  // warp-panel width of chol_smem
+#endif
+
 // Column J of a W-wide register panel (template recursion keeps every
 // register index a compile-time constant).  Lane l holds panel rows
 // p0 + l + 32 q in slot q.  Straight-line: a failed pivot is only recorded;
 // the NaNs it creates never leave the CTA.
 template <typename T, int W, int Q, int J>
-__device__ __forceinline__ void panel_cols(T (&r)[Q][W], int lane, int w, int p0, int& failed, T dcur) {
+__device__ __forceinline__ void panel_cols(T (&r)[Q][W], int lane, int w, int p0, int& failed, T dcur, T* cbuf) {
   if constexpr (J < W) {
     // dcur: this lane's candidate for pivot J (meaningful on lane J), formed
     // at column J-1 straight from the lane's own multiplier, so the serial
@@ -38,6 +42,7 @@ __device__ __forceinline__ void panel_cols(T (&r)[Q][W], int lane, int w, int p0
     for (int q = 1; q < Q; ++q) l[q] = r[q][J] * inv;
 #pragma unroll
     for (int q = 0; q < Q; ++q) r[q][J] = l[q];
+#ifdef DLAB_PANEL_SHFL
 #pragma unroll
     for (int k = J + 1; k < W; ++k) {
       const T lkj = __shfl_sync(0xffffffffu, l[0], k);  // L(p0 + k, J) on lane k
@@ -45,7 +50,42 @@ __device__ __forceinline__ void panel_cols(T (&r)[Q][W], int lane, int w, int p0
 #pragma unroll
       for (int q = 1; q < Q; ++q) r[q][k] -= l[q] * lkj;
     }
-    panel_cols<T, W, Q, J + 1>(r, lane, w, p0, failed, dnext);
+#else
+    // the column's panel multipliers L(p0 + k, J), k > J, are broadcast
+    // through a double-buffered shared vector: one STS + vector LDS per pair
+    // instead of two SHFLs per value
+    if constexpr (J + 1 < W) {
+      T* cb = cbuf + (J & 1) * 32;
+      if (lane < W) cb[lane] = l[0];
+      __syncwarp();
+      constexpr int VN = 16 / sizeof(T);
+#pragma unroll
+      for (int k0 = ((J + 1) / VN) * VN; k0 < W; k0 += VN) {
+        T v[VN];
+        if constexpr (VN == 2) {
+          const double2 t2 = *reinterpret_cast<const double2*>(cb + k0);
+          v[0] = t2.x;
+          v[1] = t2.y;
+        } else {
+          const float4 t4 = *reinterpret_cast<const float4*>(cb + k0);
+          v[0] = t4.x;
+          v[1] = t4.y;
+          v[2] = t4.z;
+          v[3] = t4.w;
+        }
+#pragma unroll
+        for (int u = 0; u < VN; ++u) {
+          const int k = k0 + u;
+          if (k > J) {
+            if (lane >= k) r[0][k] -= l[0] * v[u];
+#pragma unroll
+            for (int q = 1; q < Q; ++q) r[q][k] -= l[q] * v[u];
+          }
+        }
+      }
+    }
+#endif
+    panel_cols<T, W, Q, J + 1>(r, lane, w, p0, failed, dnext, cbuf);
   }
 }
 
@@ -66,7 +106,8 @@ __device__ __forceinline__ int panel_warp(T* S, int n, int p0, int w, int lane) 
   for (int c = 0; c < W; ++c)
     if (c >= w && lane == c) r[0][c] = T(1);
   int failed = -1;
-  panel_cols<T, W, Q, 0>(r, lane, w, p0, failed, r[0][0]);
+  __shared__ __align__(16) T cbuf[64];
+  panel_cols<T, W, Q, 0>(r, lane, w, p0, failed, r[0][0], cbuf);
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
     const int i = p0 + lane + 32 * q;
@@ -97,7 +138,7 @@ __device__ __forceinline__ int panel_warp_n(T* S, int n, int p0, int w, int lane
 // 16 columns instead of one per column.
 template <typename T, int NMAX>
 __device__ __forceinline__ int chol_smem(T* S, int n, int* flag) {
-  constexpr int W = 16, LD = NMAX + 1, Q = NMAX / 32;
+  constexpr int W = DLAB_CHOL_W(NMAX), LD = NMAX + 1, Q = NMAX / 32;
   static_assert(NMAX % 32 == 0, "32-row slots");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nthreads = blockDim.x;

@@ -47,7 +47,8 @@ inline MatB<T> packed(T* p, int64_t rows, int64_t cols) {
 struct Ctx {
   cudaStream_t stream;
   int sms;
-  int32_t* info;  // nullable: device int32[batch]
+  int32_t* info;       // nullable: device int32[batch]
+  int gemm_ctas = 0;   // > 0: DMMA GEMMs run persistent on at most this many CTAs
 };
 
 Ctx make_ctx(void* stream, int32_t* info);

@@ -27,6 +27,9 @@
 #ifndef DLAB_GEMM_BKL
 #define DLAB_GEMM_BKL 32  // k-block of the 128 x 128 configuration (3 stages: 212 KB smem)
 #endif
+#ifndef DLAB_SHORTK
+#define DLAB_SHORTK 128  // K up to which the 128 x 128 tiles use the 16-deep k-block
+#endif
 #ifndef DLAB_GEMM_BKS
 #define DLAB_GEMM_BKS 16  // k-block of the 64 x 64 configuration
 #endif
@@ -47,6 +50,10 @@ struct Cfg {
 };
 using CfgS = Cfg<64, 64, 32, 32, DLAB_GEMM_BKS>;  // 128 threads: small / batched problems
 using CfgL = Cfg<128, 128, 64, 32, DLAB_GEMM_BKL>;  // 256 threads: large trailing updates
+// short-K (rank <= 128 updates: the blocked Cholesky's trailing SYRKs): a
+// 16-deep k-block keeps 3 stages in 71 KB, so 3 CTAs share an SM and one
+// CTA's C read-modify-write epilogue overlaps another's operand loads
+using CfgK = Cfg<128, 128, 64, 32, 16>;
 
 template <typename T>
 struct GemmArgs {
@@ -59,6 +66,7 @@ struct GemmArgs {
   int64_t tiles_m, tiles_n;
   int tri_a, tri_b;
   int64_t inner;
+  int64_t total;  // tiles over all slabs; CTAs loop tile = blockIdx.x, += gridDim.x
 };
 
 __device__ __forceinline__ void cp_async(void* smem, const void* gmem, bool pred, int bytes) {
@@ -210,8 +218,7 @@ struct TileCoord {
   T* C;
 };
 template <typename T, int BM, int BN>
-__device__ __forceinline__ TileCoord<T> decode(const GemmArgs<T>& g) {
-  int64_t tile = blockIdx.x;
+__device__ __forceinline__ TileCoord<T> decode(const GemmArgs<T>& g, int64_t tile) {
   const int64_t per = g.tiles_m * g.tiles_n;
   const int64_t slab = tile / per;
   tile -= slab * per;
@@ -243,10 +250,12 @@ __global__ void __launch_bounds__(C::NT) dgemm_dmma(GemmArgs<double> g) {
   double* sA = smem;
   double* sB = smem + STAGES * AT::ELEMS;
 
-  const TileCoord<double> tc = decode<double, C::BM, C::BN>(g);
+  for (int64_t tile = blockIdx.x; tile < g.total; tile += gridDim.x) {
+  __syncthreads();  // the previous tile's warps are done with the stage buffers
+  const TileCoord<double> tc = decode<double, C::BM, C::BN>(g, tile);
   const int64_t m0 = tc.m0, n0 = tc.n0;
-  if (g.skip && g.skip[tc.bo]) return;
-  if (tile_masked_out<C::BM, C::BN>(g.mask, m0, n0)) return;
+  if (g.skip && g.skip[tc.bo]) continue;
+  if (tile_masked_out<C::BM, C::BN>(g.mask, m0, n0)) continue;
   int64_t klo, khi;
   k_range<double, C::BM, C::BN, C::BK>(g, m0, n0, klo, khi);
 
@@ -356,6 +365,7 @@ __global__ void __launch_bounds__(C::NT) dgemm_dmma(GemmArgs<double> g) {
       }
     }
   }
+  }  // tile loop
 }
 
 // ------------------------------------------------------------------ f32 FFMA
@@ -371,7 +381,7 @@ __global__ void __launch_bounds__(256) sgemm_ffma(GemmArgs<float> g) {
   float* sA = smem;
   float* sB = smem + STAGES * AT::ELEMS;
 
-  const TileCoord<float> tc = decode<float, 64, 64>(g);
+  const TileCoord<float> tc = decode<float, 64, 64>(g, blockIdx.x);
   const int64_t m0 = tc.m0, n0 = tc.n0;
   if (g.skip && g.skip[tc.bo]) return;
   if (tile_masked_out<64, 64>(g.mask, m0, n0)) return;
@@ -436,9 +446,26 @@ void ensure_smem(K k, size_t smem) {
 }
 
 template <typename T, bool TA, bool TB, int VA, int VB>
-cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large) {
+cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large, int max_ctas) {
+  auto grid = [&](int64_t tiles) {
+    g.total = tiles;
+    return (unsigned)(max_ctas > 0 && tiles > max_ctas ? max_ctas : tiles);
+  };
   if constexpr (sizeof(T) == 8) {
-    if (large) {
+    if (large && g.k <= DLAB_SHORTK) {
+      using C = CfgK;
+      g.tiles_m = (g.m + C::BM - 1) / C::BM;
+      g.tiles_n = (g.n + C::BN - 1) / C::BN;
+      const size_t smem = sizeof(T) * STAGES * (ATile<C::BM, C::BK, TA>::ELEMS + BTile<C::BN, C::BK, TB>::ELEMS);
+      auto k = dgemm_dmma<C, TA, TB, VA, VB>;
+      static bool attr = false;
+      if (!attr) {
+        ensure_smem(k, smem);
+        attr = true;
+      }
+      const unsigned nb = grid(slabs * g.tiles_m * g.tiles_n);
+      k<<<nb, C::NT, smem, s>>>(g);
+    } else if (large) {
       using C = CfgL;
       g.tiles_m = (g.m + C::BM - 1) / C::BM;
       g.tiles_n = (g.n + C::BN - 1) / C::BN;
@@ -449,7 +476,8 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large) 
         ensure_smem(k, smem);
         attr = true;
       }
-      k<<<(unsigned)(slabs * g.tiles_m * g.tiles_n), C::NT, smem, s>>>(g);
+      const unsigned nb = grid(slabs * g.tiles_m * g.tiles_n);
+      k<<<nb, C::NT, smem, s>>>(g);
     } else {
       using C = CfgS;
       g.tiles_m = (g.m + C::BM - 1) / C::BM;
@@ -461,7 +489,8 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large) 
         ensure_smem(k, smem);
         attr = true;
       }
-      k<<<(unsigned)(slabs * g.tiles_m * g.tiles_n), C::NT, smem, s>>>(g);
+      const unsigned nb = grid(slabs * g.tiles_m * g.tiles_n);
+      k<<<nb, C::NT, smem, s>>>(g);
     }
   } else {
     (void)large;
@@ -474,18 +503,19 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large) 
       ensure_smem(k, smem);
       attr = true;
     }
-    k<<<(unsigned)(slabs * g.tiles_m * g.tiles_n), 256, smem, s>>>(g);
+    g.total = slabs * g.tiles_m * g.tiles_n;
+    k<<<(unsigned)g.total, 256, smem, s>>>(g);
   }
   return cudaGetLastError();
 }
 
 template <typename T, bool TA, bool TB>
-cudaError_t launch_t(const GemmArgs<T>& g, int64_t slabs, cudaStream_t s, bool va, bool vb, bool large) {
+cudaError_t launch_t(const GemmArgs<T>& g, int64_t slabs, cudaStream_t s, bool va, bool vb, bool large, int mc) {
   constexpr int V = 16 / (int)sizeof(T);
-  if (va && vb) return launch_tv<T, TA, TB, V, V>(g, slabs, s, large);
-  if (va) return launch_tv<T, TA, TB, V, 1>(g, slabs, s, large);
-  if (vb) return launch_tv<T, TA, TB, 1, V>(g, slabs, s, large);
-  return launch_tv<T, TA, TB, 1, 1>(g, slabs, s, large);
+  if (va && vb) return launch_tv<T, TA, TB, V, V>(g, slabs, s, large, mc);
+  if (va) return launch_tv<T, TA, TB, V, 1>(g, slabs, s, large, mc);
+  if (vb) return launch_tv<T, TA, TB, 1, V>(g, slabs, s, large, mc);
+  return launch_tv<T, TA, TB, 1, 1>(g, slabs, s, large, mc);
 }
 
 // Vector loads need 16-byte aligned rows and a contiguous extent that is a
@@ -521,7 +551,7 @@ dla_status gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T 
     dla_status st;
     if (gemm_skinny<T>(c, batch, m, n, k, alpha, a, ta, b, tb, beta, cm, mask, skip, &st)) return st;
   }
-  GemmArgs<T> g{m, n, k, alpha, beta, a, b, cm, mask, skip, 0, 0, tri_a, tri_b, inner};
+  GemmArgs<T> g{m, n, k, alpha, beta, a, b, cm, mask, skip, 0, 0, tri_a, tri_b, inner, 0};
   const bool va = vec_ok<T>(a, ta ? m : k);
   const bool vb = vec_ok<T>(b, tb ? k : n);
   // 128 x 128 tiles once they alone fill every SM; 64 x 64 otherwise
@@ -531,10 +561,10 @@ dla_status gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T 
   cudaError_t e;
   const bool prof = gemm_prof_on();
   if (prof) gemm_prof_begin(c.stream);
-  if (!ta && !tb) e = launch_t<T, false, false>(g, slabs, c.stream, va, vb, large);
-  else if (ta && !tb) e = launch_t<T, true, false>(g, slabs, c.stream, va, vb, large);
-  else if (!ta && tb) e = launch_t<T, false, true>(g, slabs, c.stream, va, vb, large);
-  else e = launch_t<T, true, true>(g, slabs, c.stream, va, vb, large);
+  if (!ta && !tb) e = launch_t<T, false, false>(g, slabs, c.stream, va, vb, large, c.gemm_ctas);
+  else if (ta && !tb) e = launch_t<T, true, false>(g, slabs, c.stream, va, vb, large, c.gemm_ctas);
+  else if (!ta && tb) e = launch_t<T, false, true>(g, slabs, c.stream, va, vb, large, c.gemm_ctas);
+  else e = launch_t<T, true, true>(g, slabs, c.stream, va, vb, large, c.gemm_ctas);
   if (e != cudaSuccess) {
     fprintf(stderr, "dla_b200 gemm: %s\n", cudaGetErrorString(e));
     return DLA_ERR_CUDA;

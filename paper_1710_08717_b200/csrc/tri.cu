@@ -1,3 +1,4 @@
+#include <algorithm>
 // Recursive (divide-and-conquer) triangular algorithms over a batch:
 // trsm, trmm, potrf (lower), potri (trtri + lauum, lower), all in place.
 //
@@ -467,7 +468,7 @@ dla_status potrf_rec(const Ctx& c, int64_t batch, int64_t n, int64_t k0, MatB<T>
 // A21 <- A21 L11^{-T} in shared memory (blocked substitution + DMMA).
 template <typename T, int NBP>
 __global__ void __launch_bounds__(256, 1) k_potrf_panel(int nb, int64_t rest, int64_t k0, MatB<T> akk, MatB<T> a21,
-                                                     int32_t* info) {
+                                                     int32_t* info, int* arrive) {
   constexpr int LD = NBP + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* S = reinterpret_cast<T*>(smem_raw);
@@ -509,16 +510,23 @@ __global__ void __launch_bounds__(256, 1) k_potrf_panel(int nb, int64_t rest, in
     }
   }
   __syncthreads();
-  const int failed = chol_smem<T, NBP>(S, nb, &flag);
+  // Every CTA reads A11 from global memory; the CTA that arrives LAST (all
+  // others have their copy in shared memory by then) writes L11 back over it
+  // and re-arms the slice's counter for the next panel launch.
+  __shared__ int last;
+  if (tid == 0) last = atomicAdd(arrive + b, 1) == (int)chunks - 1;
+  const int failed = chol_smem<T, NBP>(S, nb, &flag);  // (its first barrier publishes `last`)
   if (failed >= 0) {
     if (cid == 0 && tid == 0) record_failure(info, b, DLA_ERR_NOT_SPD, k0 + failed);
     return;
   }
-  if (cid == 0)
+  if (last) {
+    if (tid == 0) arrive[b] = 0;
     for (int e = tid; e < nb * nb; e += 256) {
       const int i = e / nb, j = e % nb;
       base[i * akk.ld + j] = j <= i ? S[i * LD + j] : T(0);
     }
+  }
   if (nv == 0) return;
   for (int i = tid; i < NBP; i += 256) rd[i] = i < nb ? T(1) / S[i * LD + i] : T(1);
   __syncthreads();
@@ -584,41 +592,84 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
   // ordered w.r.t. the caller and capturable into a CUDA graph.
   const int64_t steps = (n + NBP - 1) / NBP;
   LookAhead& la = LookAhead::get(steps);
+  Scratch arrive(sizeof(int) * (size_t)batch, c.stream);
+  if (!arrive.p) return DLA_ERR_CUDA;
+  if (cudaMemsetAsync(arrive.p, 0, sizeof(int) * (size_t)batch, c.stream) != cudaSuccess) return DLA_ERR_CUDA;
   static const bool prio = [] {
     const char* e = getenv("DLA_POTRF_PRIO");  // tuning switch: 0 keeps the chain on the caller's stream
     return e ? atoi(e) != 0 : true;
   }();
   Ctx side = c, cc = c;
   side.stream = la.side;
+  // The bulk update runs persistent on sms - reserve CTAs: a 128 x 128 GEMM
+  // CTA (212 KB smem) cannot share an SM with a panel CTA, so without a
+  // reserve every panel launch of the critical chain first waits for update
+  // tiles to drain.  Measured: the bulk update is the scarcer resource, so
+  // the default reserve is 0; DLA_POTRF_RESERVE sets one (tuning switch).
+  static const int reserve_env = [] {
+    const char* e = getenv("DLA_POTRF_RESERVE");
+    return e ? atoi(e) : -1;
+  }();
+  {
+    const int64_t chunks0 = batch * ((n - NBP + 63) / 64);
+    const int reserve = reserve_env > 0 ? (int)std::min<int64_t>(reserve_env, chunks0) : 0;
+    if (reserve > 0 && reserve < c.sms) side.gemm_ctas = c.sms - reserve;
+  }
   if (prio) cc.stream = la.crit;
   cudaEventRecord(la.fork, c.stream);
   cudaStreamWaitEvent(la.side, la.fork, 0);
   if (prio) cudaStreamWaitEvent(cc.stream, la.fork, 0);
-  for (int64_t s = 0; s < steps; ++s) {
-    const int64_t k0 = s * NBP;
+  // Look-ahead with (optionally) grouped trailing updates.  Panels are taken in
+  // groups of G.  After the last panel of group g the side stream applies
+  // the whole group to every column >= (g+2) G NBP in ONE masked SYRK with
+  // K = G NBP (a rank-64 update re-reads and re-writes the trailing triangle
+  // for only 64 flops per element; grouping amortises that C traffic G-fold).
+  // Before panel p (group g) the critical stream brings block column p up to
+  // date with the panels the side updates have not covered — group g-1 and
+  // the earlier panels of group g, contiguous in L, K <= (2G-1) NBP — after
+  // waiting for side update g-2, the last one that writes column p.
+  // Measured on B200 (tools/timeline.py): G = 1 is fastest at n = 1024 and
+  // 4096 — the longer critical-path GEMM of G > 1 costs what the cheaper
+  // bulk updates save — so DLA_POTRF_GROUP defaults to 1.
+  static const int group = [] {
+    const char* e = getenv("DLA_POTRF_GROUP");  // tuning switch
+    const int gsz = e ? atoi(e) : 1;
+    return gsz < 1 ? 1 : gsz;
+  }();
+  const int64_t G = group;
+  const int64_t ngroups = (steps + G - 1) / G;
+  for (int64_t p = 0; p < steps; ++p) {
+    const int64_t k0 = p * NBP;
     const int64_t kb = min((int64_t)NBP, n - k0);
     const int64_t rest = n - k0 - kb;
-    MatB<T> akk = a.sub(k0, k0);
-    MatB<T> a21 = a.sub(k0 + kb, k0);
+    const int64_t g = p / G;
+    if (p > 0) {  // column p: panels [max(0, (g-1) G), p)
+      if (g >= 2) cudaStreamWaitEvent(cc.stream, la.done[g - 2], 0);
+      const int64_t kk0 = std::max<int64_t>(0, (g - 1) * G) * NBP;
+      MatB<T> lrows = a.sub(k0, kk0);
+      DLAB_TRY(gemm<T>(cc, batch, n - k0, kb, k0 - kk0, T(-1), C_(lrows), false, C_(lrows), true, T(1), a.sub(k0, k0),
+                       MASK_LOWER, c.info));
+    }
     const int64_t chunks = rest > 0 ? (rest + 63) / 64 : 1;
-    k_potrf_panel<T, NBP><<<(unsigned)(batch * chunks), 256, sm, cc.stream>>>((int)kb, rest, kbase + k0, akk, a21,
-                                                                              c.info);
+    k_potrf_panel<T, NBP><<<(unsigned)(batch * chunks), 256, sm, cc.stream>>>((int)kb, rest, kbase + k0, a.sub(k0, k0),
+                                                                              a.sub(k0 + kb, k0), c.info,
+                                                                              arrive.as<int>());
     DLAB_LAUNCH_CHECK();
     if (rest == 0) break;
-    if (s >= 1) cudaStreamWaitEvent(cc.stream, la.done[s - 1], 0);
-    const int64_t nb2 = min((int64_t)NBP, rest);  // block column k+1
-    DLAB_TRY(gemm<T>(cc, batch, rest, nb2, kb, T(-1), C_(a21), false, C_(a21), true, T(1), a.sub(k0 + kb, k0 + kb),
-                     MASK_LOWER, c.info));
-    const int64_t rest2 = rest - nb2;
-    if (rest2 > 0) {
-      cudaEventRecord(la.panel[s], cc.stream);
-      cudaStreamWaitEvent(la.side, la.panel[s], 0);
-      MatB<T> p2 = a.sub(k0 + kb + nb2, k0);
-      DLAB_TRY(gemm<T>(side, batch, rest2, rest2, kb, T(-1), C_(p2), false, C_(p2), true, T(1),
-                       a.sub(k0 + kb + nb2, k0 + kb + nb2), MASK_LOWER, c.info));
+    if (p % G == G - 1 || p == steps - 1) {  // last panel of group g: side update U(g)
+      const int64_t c0 = (g + 2) * G * NBP;
+      if (c0 < n) {
+        cudaEventRecord(la.panel[g], cc.stream);
+        cudaStreamWaitEvent(la.side, la.panel[g], 0);
+        const int64_t gk0 = g * G * NBP;
+        MatB<T> p2 = a.sub(c0, gk0);
+        DLAB_TRY(gemm<T>(side, batch, n - c0, n - c0, k0 + kb - gk0, T(-1), C_(p2), false, C_(p2), true, T(1),
+                         a.sub(c0, c0), MASK_LOWER, c.info));
+      }
+      cudaEventRecord(la.done[g], la.side);
     }
-    cudaEventRecord(la.done[s], la.side);
   }
+  (void)ngroups;
   cudaEventRecord(la.join, la.side);
   cudaStreamWaitEvent(c.stream, la.join, 0);
   if (prio) {

@@ -209,6 +209,19 @@ def test_trsm_singular_reports_index_and_leaves_slice():
 POTRF_N = [1, 2, 5, 17, 32, 63, 64, 65, 70, 129, 200, 256, 512]  # 256/512: inverse-based DMMA paths
 
 
+def test_potrf_large_blocked_lookahead():
+    """Blocked look-ahead path at sizes with many panel CTAs per launch (the
+    panel kernel's redundant A11 reads must never see the written L11)."""
+    r = O.rng(77)
+    for n, B in ((1024, 6), (2112, 1)):
+        a = O.random_spd(n, r, batch=B)
+        for _ in range(3):
+            got = host(L.potrf(dev(a)))
+            want = np.linalg.cholesky(a)
+            assert np.abs(got - want).max() / np.abs(want).max() < 1e-12
+            assert np.all(np.triu(got, 1) == 0)
+
+
 @pytest.mark.parametrize("dt", DTYPES)
 def test_potrf_forward(port, dt):
     r = O.rng(6)

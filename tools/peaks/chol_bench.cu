@@ -55,10 +55,13 @@ int main() {
     cudaFuncSetAttribute(k<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140000);
     for (int threads : {64, 128, 256, 512}) {
       cudaMemcpy(d, h, sizeof(double) * n * n, cudaMemcpyHostToDevice);
-      if (n <= 64)
-        k<64><<<1, threads, 8 * 64 * 65>>>(d, n, t);
-      else
-        k<128><<<1, threads, 8 * 128 * 129>>>(d, n, t);
+      for (int rep = 0; rep < 2; ++rep) {
+        cudaMemcpy(d, h, sizeof(double) * n * n, cudaMemcpyHostToDevice);
+        if (n <= 64)
+          k<64><<<1, threads, 8 * 64 * 65>>>(d, n, t);
+        else
+          k<128><<<1, threads, 8 * 128 * 129>>>(d, n, t);
+      }
       long long ht[2];
       cudaMemcpy(ht, t, sizeof(ht), cudaMemcpyDeviceToHost);
       cudaMemcpy(out, d, sizeof(double) * n * n, cudaMemcpyDeviceToHost);
