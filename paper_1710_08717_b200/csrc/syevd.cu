@@ -269,6 +269,216 @@ __global__ void __launch_bounds__(ET) k_syevd(int n, T* uall, T* lamall, T* wsal
   }
 }
 
+
+// ---------------------------------------------------- n <= 64: one pass/round
+// The same cyclic Jacobi (round-robin ordering, Rutishauser rotations), with
+// each round applied as ONE pass over 2 x 2 blocks: rows {p_a, q_a} x columns
+// {p_b, q_b} of A become J_a^T A_blk J_b, so a thread owns every element it
+// reads and writes (no row pass / column pass / zeroing pass, 2 barriers per
+// round instead of 4).  Only blocks a <= b are computed and mirrored, so A
+// stays exactly symmetric.  The eigenvector accumulator is kept transposed
+// (Vt = V^T, rotated by rows), which makes the output rows contiguous.
+constexpr int SP = 32;                 // max pairs
+constexpr int NUB = SP * (SP + 1) / 2;  // upper 2x2 blocks
+static_assert(ET == 8 * SP, "Vt pass: 8 threads per pair");
+
+struct BlkTab {  // (a, b), a <= b, packed a << 8 | b
+  unsigned short v[NUB];
+  constexpr BlkTab() : v() {
+    int e = 0;
+    for (int a = 0; a < SP; ++a)
+      for (int b = a; b < SP; ++b) v[e++] = (unsigned short)(a << 8 | b);
+  }
+};
+__device__ const BlkTab kBlkTab = BlkTab();
+
+template <typename T>
+__global__ void __launch_bounds__(ET) k_syevd_small(int n, T* uall, T* lamall, int32_t* info) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* A = reinterpret_cast<T*>(smem_raw);  // EN x (EN+1)
+  T* Vt = A + EN * (EN + 1);
+  __shared__ T red[ET / 32];
+  __shared__ T cs[2 * SP];
+  __shared__ int pq[2 * SP];
+  __shared__ unsigned short blk[NUB];
+  __shared__ int order[EN];
+  __shared__ int done;
+  constexpr int ld = EN + 1;
+  const int64_t b = blockIdx.x;
+  T* u = uall + b * (int64_t)n * n;
+  T* lam = lamall + b * (int64_t)n;
+  const int tid = threadIdx.x;
+  const int N = n + (n & 1), half = N / 2;
+  for (int e = tid; e < n * n; e += ET) A[(e / n) * ld + e % n] = u[e];
+  for (int e = tid; e < NUB; e += ET) blk[e] = kBlkTab.v[e];
+  __syncthreads();
+  T mabs = T(0), masym = T(0);
+  for (int e = tid; e < n * n; e += ET) {
+    const int i = e / n, j = e % n;
+    const T v = A[i * ld + j];
+    if (fabs(v) > mabs) mabs = fabs(v);
+    if (j > i) masym = fmax(masym, fabs(v - A[j * ld + i]));
+  }
+  mabs = bmax(mabs, red);
+  masym = bmax(masym, red);
+  if (masym > Num<T>::sym_rtol * (mabs > T(0) ? mabs : T(1))) {
+    if (tid == 0) record_failure(info, b, DLA_ERR_ASYMMETRIC, 0);
+    return;
+  }
+  if (n == 1) {
+    if (tid == 0) {
+      lam[0] = u[0];
+      u[0] = T(1);
+    }
+    return;
+  }
+  int ex = 0;
+  if (mabs > T(0)) frexp(mabs, &ex);
+  for (int e = tid; e < EN * EN; e += ET) {
+    const int i = e / EN, j = e % EN;
+    if (i < n && j < n) {
+      if (j <= i) {
+        const T v = ldexp(A[i * ld + j], -ex);
+        A[i * ld + j] = v;
+        A[j * ld + i] = v;
+      }
+    } else if (i < N && j < N) {
+      A[i * ld + j] = T(0);  // padding row / column of an odd n
+    }
+    Vt[i * ld + j] = (i == j) ? T(1) : T(0);
+  }
+  __syncthreads();
+  int sweep = 0;
+  for (; sweep < MAX_SWEEPS; ++sweep) {
+    T off = T(0), dia = T(0);
+    for (int e = tid; e < n * n; e += ET) {
+      const int i = e / n, j = e % n;
+      const T v = fabs(A[i * ld + j]);
+      if (i != j) off = fmax(off, v);
+      else dia = fmax(dia, v);
+    }
+    off = bmax(off, red);
+    dia = bmax(dia, red);
+    if (off <= Eps<T>::v * dia || off == T(0)) break;
+    for (int r = 0; r < N - 1; ++r) {
+      if (tid < half) {
+        int p, q;
+        rr_pair(N, r, tid, p, q);
+        T c = T(1), s = T(0);
+        if (q < n) {
+          const T apq = A[p * ld + q];
+          if (apq != T(0)) {
+            const T theta = (A[q * ld + q] - A[p * ld + p]) / (T(2) * apq);
+            T t;
+            if (fabs(theta) > (sizeof(T) == 8 ? T(1e150) : T(1e15))) t = T(0.5) / theta;
+            else t = (theta >= T(0) ? T(1) : T(-1)) / (fabs(theta) + sqrt(theta * theta + T(1)));
+            c = T(1) / sqrt(t * t + T(1));
+            s = t * c;
+          }
+        }
+        cs[2 * tid] = c;
+        cs[2 * tid + 1] = s;
+        pq[2 * tid] = p;
+        pq[2 * tid + 1] = q;
+      }
+      __syncthreads();
+      // A <- J^T A J on the upper 2x2 blocks, mirrored
+      for (int e = tid; e < NUB; e += ET) {
+        const int ba = blk[e] >> 8, bb = blk[e] & 255;
+        if (bb >= half) continue;
+        const int pa = pq[2 * ba], qa = pq[2 * ba + 1], pb = pq[2 * bb], qb = pq[2 * bb + 1];
+        const T ca = cs[2 * ba], sa = cs[2 * ba + 1], cb = cs[2 * bb], sb = cs[2 * bb + 1];
+        if (ba == bb) {
+          if (sa == T(0)) continue;
+          const T x = A[pa * ld + pa], y = A[pa * ld + qa], w = A[qa * ld + qa];
+          // rows, then columns (the order of the former row / column passes)
+          const T x1 = ca * x - sa * y, y1 = ca * y - sa * w;
+          const T z1 = sa * x + ca * y, w1 = sa * y + ca * w;
+          A[pa * ld + pa] = ca * x1 - sa * y1;
+          A[qa * ld + qa] = sa * z1 + ca * w1;
+          A[pa * ld + qa] = T(0);  // the annihilated pair is exactly zero
+          A[qa * ld + pa] = T(0);
+          continue;
+        }
+        if (sa == T(0) && sb == T(0)) continue;
+        const T x = A[pa * ld + pb], y = A[pa * ld + qb], z = A[qa * ld + pb], w = A[qa * ld + qb];
+        const T x1 = ca * x - sa * z, y1 = ca * y - sa * w;
+        const T z1 = sa * x + ca * z, w1 = sa * y + ca * w;
+        const T x2 = cb * x1 - sb * y1, y2 = sb * x1 + cb * y1;
+        const T z2 = cb * z1 - sb * w1, w2 = sb * z1 + cb * w1;
+        A[pa * ld + pb] = x2;
+        A[pa * ld + qb] = y2;
+        A[qa * ld + pb] = z2;
+        A[qa * ld + qb] = w2;
+        A[pb * ld + pa] = x2;
+        A[qb * ld + pa] = y2;
+        A[pb * ld + qa] = z2;
+        A[qb * ld + qa] = w2;
+      }
+      // Vt <- J^T Vt (rows p, q of Vt = columns of V): thread -> one pair,
+      // every 8th element of its two rows
+      {
+        const int k = tid >> 3, i0 = tid & 7;
+        const T s = k < half ? cs[2 * k + 1] : T(0);
+        if (s != T(0)) {
+          const int p = pq[2 * k], q = pq[2 * k + 1];
+          const T c = cs[2 * k];
+          T* vp = Vt + p * ld;
+          T* vq = Vt + q * ld;
+#pragma unroll
+          for (int v = 0; v < EN / 8; ++v) {
+            const int i = i0 + 8 * v;
+            const T a0 = vp[i], a1 = vq[i];
+            vp[i] = c * a0 - s * a1;
+            vq[i] = s * a0 + c * a1;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (sweep >= MAX_SWEEPS) {
+    if (tid == 0) record_failure(info, b, DLA_ERR_CONVERGENCE, sweep);
+    return;
+  }
+  (void)done;
+  for (int i = tid; i < n; i += ET) {
+    const T di = A[i * ld + i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const T dj = A[j * ld + j];
+      rank += (dj < di) || (dj == di && j < i);
+    }
+    order[rank] = i;
+  }
+  __syncthreads();
+  for (int r = tid >> 5; r < n; r += ET / 32) {
+    const int lane = tid & 31;
+    const int col = order[r];
+    const T* vr = Vt + col * ld;
+    T best = T(-1);
+    int kbest = 0;
+    for (int k = lane; k < n; k += 32) {
+      const T v = fabs(vr[k]);
+      if (v > best) {
+        best = v;
+        kbest = k;
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const T ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int ok = __shfl_xor_sync(0xffffffffu, kbest, o);
+      if (ob > best || (ob == best && ok < kbest)) {
+        best = ob;
+        kbest = ok;
+      }
+    }
+    const T sgn = vr[kbest] < T(0) ? T(-1) : T(1);
+    for (int k = lane; k < n; k += 32) u[(int64_t)r * n + k] = sgn * vr[k];
+    if (lane == 0) lam[r] = ldexp(A[col * ld + col], ex);
+  }
+}
+
 template <typename T>
 __global__ void k_gap(int64_t batch, int64_t n, MatB<T> w, const T* lambdabar, const T* lambda, T eps_gap) {
   const int64_t total = batch * n * n;
@@ -309,7 +519,18 @@ size_t syevd_ws_bytes(int64_t batch, int64_t n, bool backward) {
 template <typename T>
 dla_status syevd_fwd(const Ctx& c, int64_t batch, int64_t n, T* u, T* lambda, void* ws) {
   const bool sm = n <= EN;
-  if (!sm && !ws) return DLA_ERR_WORKSPACE;
+  if (sm) {
+    const size_t smem = sizeof(T) * 2 * EN * (EN + 1);
+    static bool once = false;
+    if (!once) {
+      cudaFuncSetAttribute(k_syevd_small<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      once = true;
+    }
+    k_syevd_small<T><<<(unsigned)batch, ET, smem, c.stream>>>((int)n, u, lambda, c.info);
+    DLAB_LAUNCH_CHECK();
+    return DLA_OK;
+  }
+  if (!ws) return DLA_ERR_WORKSPACE;
   const int64_t npairs = (n + 1) / 2;
   const size_t smem = (sm ? sizeof(T) * 2 * EN * (EN + 1) : 0) + npairs * 2 * (sizeof(T) + sizeof(int));
   if (smem > 200 * 1024) return DLA_ERR_SHAPE;  // n > ~8000: out of the supported range
