@@ -237,6 +237,18 @@ dla_status dla_gp_rbf_bwd_f64(int64_t batch, int64_t n, int64_t d, const double*
 dla_status dla_gp_nll_assemble_f64(int64_t batch, int64_t n, const double* quad,
                                    const double* logdet, double* nll, void* stream);
 
+/* ------------------------------------- batched marginal-likelihood driver */
+/* Helpers of the C5 driver (batched GP marginal likelihoods; the graph is
+ * SURVEY §8d's, built from reference ops): a = s + lam I (batch of n x n);
+ * y += alpha x (count elements); out[0] = sum_b (quad_b + logdet_b) +
+ * batch n/2 log 2 pi and out[1] = lam sum_b tr(abar_b), summed in a fixed
+ * order (deterministic). */
+dla_status dla_ml_shift_copy_f64(int64_t batch, int64_t n, const double* s, double* a, double lam,
+                                 void* stream);
+dla_status dla_axpy_f64(int64_t count, double alpha, const double* x, double* y, void* stream);
+dla_status dla_ml_reduce_f64(int64_t batch, int64_t n, const double* quad, const double* logdet,
+                             const double* abar, double lam, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

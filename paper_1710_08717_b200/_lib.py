@@ -79,6 +79,12 @@ class _Lib:
         L.dla_gp_rbf_bwd_f64.restype = _int
         L.dla_gp_nll_assemble_f64.argtypes = [_i64, _i64, _vp, _vp, _vp, _vp]
         L.dla_gp_nll_assemble_f64.restype = _int
+        L.dla_ml_shift_copy_f64.argtypes = [_i64, _i64, _vp, _vp, C.c_double, _vp]
+        L.dla_ml_shift_copy_f64.restype = _int
+        L.dla_axpy_f64.argtypes = [_i64, C.c_double, _vp, _vp, _vp]
+        L.dla_axpy_f64.restype = _int
+        L.dla_ml_reduce_f64.argtypes = [_i64, _i64, _vp, _vp, _vp, C.c_double, _vp, _vp]
+        L.dla_ml_reduce_f64.restype = _int
         self.fns = {}
         for name, sig in _SIGS.items():
             for suffix, scal in (("f32", C.c_float), ("f64", C.c_double)):
@@ -106,7 +112,8 @@ def exported_symbols():
     """Every dla_* symbol include/dla.h declares (used by the CPU symbol test)."""
     names = ["dla_status_string", "dla_version", "dla_workspace_bytes", "dla_info_check",
              "dla_launch_count", "dla_prof_enable", "dla_prof_read", "dla_gp_rbf_ws_bytes",
-             "dla_gp_rbf_fwd_f64", "dla_gp_rbf_bwd_f64", "dla_gp_nll_assemble_f64"]
+             "dla_gp_rbf_fwd_f64", "dla_gp_rbf_bwd_f64", "dla_gp_nll_assemble_f64",
+             "dla_ml_shift_copy_f64", "dla_axpy_f64", "dla_ml_reduce_f64"]
     for name in _SIGS:
         for s in ("f32", "f64"):
             names.append(f"dla_{name}_{s}")

@@ -26,6 +26,7 @@ import math
 import torch
 
 from . import linalg as L
+from ._lib import lib
 from .shard import allreduce_loss_grad
 
 LOG_2PI = 1.8378770664093454835606594728112353
@@ -52,16 +53,20 @@ class MarginalLikelihoods:
         self.info = torch.zeros(batch, dtype=torch.int32, device=device)
         self.out = torch.empty(2, **f)  # [loss, dloss/dtheta] of this shard
 
+    def _st(self):
+        return C.c_void_p(torch.cuda.current_stream(self.l.device).cuda_stream)
+
     def step(self, s: torch.Tensor, y: torch.Tensor, theta: float):
         lam = math.exp(theta)
         B, n = self.batch, self.n
-        # forward
-        self.l.copy_(s)
-        self.l.diagonal(dim1=-2, dim2=-1).add_(lam)
+        lib_ = lib().lib
+        P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+        # forward: every kernel below is libdla_b200's (copies included)
+        self._ok(lib_.dla_ml_shift_copy_f64(B, n, P(s), P(self.l), lam, self._st()))  # A = S + lam I
         L.potrf_inplace(self.l, True, check=False, info=self.info)
-        self.b.copy_(self.l)
+        self._ok(lib_.dla_ml_shift_copy_f64(B, n, P(self.l), P(self.b), 0.0, self._st()))
         L.potri_inplace(self.b, True, check=False)
-        self.g.copy_(self.b)
+        self._ok(lib_.dla_ml_shift_copy_f64(B, n, P(self.b), P(self.g), 0.0, self._st()))
         L.trmm_inplace(self.l, self.g, False, True, True)
         L.gemm2_into(self.v, self.g, y)
         L.gemm2_into(self.quad, self.v, self.v, True, False, 0.5)
@@ -70,13 +75,18 @@ class MarginalLikelihoods:
         L.gemm2_backward_into(self.gbar, self.ybar, self.v, self.g, y, False, False)
         L.trmm_backward_into(self.bbar, self.tbar, self.gbar, self.l, self.b, False, True, True)
         L.potri_backward_into(self.lbar, self.bbar, self.l, self.b, True)
-        self.lbar.add_(self.tbar)
+        self._ok(lib_.dla_axpy_f64(B * n * n, 1.0, P(self.tbar), P(self.lbar), self._st()))
         L.sumlogdiag_backward_into(self.lbar, self.ones, self.l, accumulate=True)
         L.potrf_backward_into(self.lbar, self.lbar, self.l, True)  # lbar now holds Abar
-        # shard reduction: loss and dloss/dtheta
-        self.out[0] = (self.quad.view(B) + self.logdet).sum() + B * 0.5 * n * LOG_2PI
-        self.out[1] = self.lbar.diagonal(dim1=-2, dim2=-1).sum() * lam
+        # shard reduction: [loss, dloss/dtheta] (fixed order, on device)
+        self._ok(lib_.dla_ml_reduce_f64(B, n, P(self.quad), P(self.logdet), P(self.lbar), lam, P(self.out),
+                                        self._st()))
         return self.out
+
+    @staticmethod
+    def _ok(st):
+        if st:
+            L._raise_status(st, "c5 driver")
 
     def step_allreduce(self, s, y, theta):
         return allreduce_loss_grad(self.step(s, y, theta))

@@ -149,13 +149,15 @@ __global__ void __launch_bounds__(GT) k_gelqf(int64_t m, int64_t n, T* qall, T* 
 
 template <typename T>
 size_t gelqf_ws_bytes(int64_t batch, int64_t m, int64_t n, bool backward) {
-  (void)n;
-  return backward ? sizeof(T) * (size_t)(batch * m * m) : sizeof(T) * (size_t)(batch * m);
+  if (backward) return sizeof(T) * (size_t)(batch * m * m);
+  if (gelqf_blocked_eligible<T>(m, n)) return gelqf_blocked_ws_bytes<T>(batch, m, n);
+  return sizeof(T) * (size_t)(batch * m);
 }
 
 template <typename T>
 dla_status gelqf_fwd(const Ctx& c, int64_t batch, int64_t m, int64_t n, T* q, T* l, void* ws) {
   if (!ws) return DLA_ERR_WORKSPACE;
+  if (gelqf_blocked_eligible<T>(m, n)) return gelqf_blocked<T>(c, batch, m, n, q, l, ws);
   k_gelqf<T><<<(unsigned)batch, GT, 0, c.stream>>>(m, n, q, l, static_cast<T*>(ws), c.info);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;

@@ -54,6 +54,8 @@ using CfgL = Cfg<128, 128, 64, 32, DLAB_GEMM_BKL>;  // 256 threads: large traili
 // 16-deep k-block keeps 3 stages in 71 KB, so 3 CTAs share an SM and one
 // CTA's C read-modify-write epilogue overlaps another's operand loads
 using CfgK = Cfg<128, 128, 64, 32, 16>;
+// narrow N (<= 32, deep K): the blocked LQ's W = R Yc^T (rows x 32 x n)
+using CfgN = Cfg<64, 32, 32, 16, 16>;
 
 template <typename T>
 struct GemmArgs {
@@ -452,7 +454,20 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large, 
     return (unsigned)(max_ctas > 0 && tiles > max_ctas ? max_ctas : tiles);
   };
   if constexpr (sizeof(T) == 8) {
-    if (large && g.k <= DLAB_SHORTK) {
+    if (g.n <= 32 && g.k >= 128 && g.m >= 64) {
+      using C = CfgN;
+      g.tiles_m = (g.m + C::BM - 1) / C::BM;
+      g.tiles_n = (g.n + C::BN - 1) / C::BN;
+      const size_t smem = sizeof(T) * STAGES * (ATile<C::BM, C::BK, TA>::ELEMS + BTile<C::BN, C::BK, TB>::ELEMS);
+      auto k = dgemm_dmma<C, TA, TB, VA, VB>;
+      static bool attr = false;
+      if (!attr) {
+        ensure_smem(k, smem);
+        attr = true;
+      }
+      const unsigned nb = grid(slabs * g.tiles_m * g.tiles_n);
+      k<<<nb, C::NT, smem, s>>>(g);
+    } else if (large && g.k <= DLAB_SHORTK) {
       using C = CfgK;
       g.tiles_m = (g.m + C::BM - 1) / C::BM;
       g.tiles_n = (g.n + C::BN - 1) / C::BN;

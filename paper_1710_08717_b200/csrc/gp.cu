@@ -302,6 +302,53 @@ __global__ void k_nll(int64_t batch, int64_t n, const double* quad, const double
   if (b < batch) nll[b] = (quad[b] + logdet[b]) + 0.5 * (double)n * 1.8378770664093454835606594728112353;
 }
 
+
+// ---- batched marginal-likelihood driver helpers (BASELINE config C5) ----
+// dst = src + lam I over a batch of n x n matrices (copy with diagonal shift)
+__global__ void k_shift_copy(int64_t total, int64_t n, const double* src, double* dst, double lam) {
+  const int64_t nn = n * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t % nn;
+    const double v = src[t];
+    dst[t] = (r / n == r % n) ? v + lam : v;
+  }
+}
+
+__global__ void k_axpy(int64_t count, double alpha, const double* x, double* y) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x)
+    y[t] += alpha * x[t];
+}
+
+// out[0] = sum_b (quad_b + logdet_b) + batch n/2 log 2 pi, out[1] = lam sum_b tr(abar_b):
+// one CTA, fixed summation order (deterministic; no atomics)
+constexpr int MLT = 1024;
+__global__ void __launch_bounds__(MLT) k_ml_reduce(int64_t batch, int64_t n, const double* quad, const double* logdet,
+                                                    const double* abar, double lam, double* out) {
+  __shared__ double r0[MLT], r1[MLT];
+  double a = 0.0, g = 0.0;
+  for (int64_t b = threadIdx.x; b < batch; b += MLT) {
+    a += quad[b] + logdet[b];
+    const double* ab = abar + b * n * n;
+    double tr = 0.0;
+    for (int64_t i = 0; i < n; ++i) tr += ab[i * (n + 1)];
+    g += tr;
+  }
+  r0[threadIdx.x] = a;
+  r1[threadIdx.x] = g;
+  __syncthreads();
+  for (int st = MLT / 2; st; st >>= 1) {
+    if (threadIdx.x < st) {
+      r0[threadIdx.x] += r0[threadIdx.x + st];
+      r1[threadIdx.x] += r1[threadIdx.x + st];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = r0[0] + (double)batch * 0.5 * (double)n * 1.8378770664093454835606594728112353;
+    out[1] = lam * r1[0];
+  }
+}
+
 }  // namespace
 }  // namespace dlab
 
@@ -362,6 +409,31 @@ dla_status dla_gp_nll_assemble_f64(int64_t batch, int64_t n, const double* quad,
                                    void* stream) {
   if (batch <= 0) return DLA_OK;
   k_nll<<<blocks_for(batch, 128), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(batch, n, quad, logdet, nll);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+
+dla_status dla_ml_shift_copy_f64(int64_t batch, int64_t n, const double* s, double* a, double lam, void* stream) {
+  if (batch < 0 || n < 0) return DLA_ERR_SHAPE;
+  if (batch * n == 0) return DLA_OK;
+  const int64_t total = batch * n * n;
+  k_shift_copy<<<blocks_for(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(total, n, s, a, lam);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+
+dla_status dla_axpy_f64(int64_t count, double alpha, const double* x, double* y, void* stream) {
+  if (count < 0) return DLA_ERR_SHAPE;
+  if (count == 0) return DLA_OK;
+  k_axpy<<<blocks_for(count, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(count, alpha, x, y);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+
+dla_status dla_ml_reduce_f64(int64_t batch, int64_t n, const double* quad, const double* logdet, const double* abar,
+                             double lam, double* out, void* stream) {
+  if (batch < 0 || n < 0) return DLA_ERR_SHAPE;
+  k_ml_reduce<<<1, MLT, 0, reinterpret_cast<cudaStream_t>(stream)>>>(batch, n, quad, logdet, abar, lam, out);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }

@@ -42,6 +42,14 @@ template <typename T>
 dla_status trsv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x, bool right, bool trans,
                 bool lower, T alpha);
 
+// gelqf_blk.cu: blocked (compact WY) LQ, m >= 64
+template <typename T>
+bool gelqf_blocked_eligible(int64_t m, int64_t n);
+template <typename T>
+size_t gelqf_blocked_ws_bytes(int64_t batch, int64_t m, int64_t n);
+template <typename T>
+dla_status gelqf_blocked(const Ctx& c, int64_t batch, int64_t m, int64_t n, T* q, T* l, void* ws);
+
 // gelqf.cu
 template <typename T>
 size_t gelqf_ws_bytes(int64_t batch, int64_t m, int64_t n, bool backward);

@@ -365,7 +365,7 @@ def test_sumlogdiag(port, dt):
 def test_gelqf(port, dt):
     r = O.rng(11)
     B = 2
-    for m, n in [(1, 1), (2, 5), (4, 4), (7, 11), (16, 16), (32, 128), (128, 512)]:
+    for m, n in [(1, 1), (2, 5), (4, 4), (7, 11), (16, 16), (32, 128), (128, 512), (70, 300), (96, 96), (64, 65)]:
         a = r.standard_normal((B, m, n)).astype(dt)
         q, l = L.gelqf(dev(a))
         q, l = host(q), host(l)
@@ -388,6 +388,17 @@ def test_gelqf(port, dt):
         L.gelqf(dev(np.array([[1.0, 2, 3], [2, 4, 6]])))
     with pytest.raises(L.ShapeError):
         L.gelqf(dev(np.zeros((3, 2))))
+    # blocked path (m >= 64): rank deficiency and an all-zero slice, with a
+    # healthy slice beside them left exactly as the unbatched call computes it
+    a = r.standard_normal((3, 80, 120)).astype(dt)
+    a[1, 50] = 2 * a[1, 7]
+    a[2] = 0
+    ok_q, ok_l = L.gelqf(dev(a[:1]))
+    qd, ld = dev(a), torch.empty(3, 80, 80, dtype=dev(a).dtype, device="cuda")
+    with pytest.raises(L.SingularError) as e:
+        L.gelqf_inplace(qd, ld)
+    assert e.value.batch_index == 1 and e.value.index == 50
+    assert torch.equal(qd[0], ok_q[0]) and torch.equal(ld[0], ok_l[0])
 
 
 # ------------------------------------------------------------------ syevd
