@@ -169,7 +169,8 @@ dla_status dla_info_check(const int32_t* info, int64_t batch, void* stream,
                                     void* stream);                                  \
   /* gelqf: A (m x n, m <= n) = L Q; q: in A, out Q; l: out L (m x m, positive      \
      diagonal); rank deficiency => SINGULAR(row); dl/lq.hpp:24-106.                 \
-     workspace: dla_workspace_bytes(DLA_OP_GELQF, ..., 0). */                       \
+     workspace: dla_workspace_bytes(DLA_OP_GELQF, ..., 0) (m reals per slice;       \
+     m >= 64 runs the blocked compact-WY path: 2mn + 64m + m + 1 reals). */         \
   dla_status dla_gelqf_fwd_##S(int64_t batch, int64_t m, int64_t n, T* q, T* l,     \
                                int32_t* info, void* ws, size_t ws_bytes,            \
                                void* stream);                                       \

@@ -56,8 +56,11 @@ def test_host_only_entry_points(lib):
     assert b"sm_100a" in lib.dla_version()
     lib.dla_workspace_bytes.restype = C.c_size_t
     lib.dla_workspace_bytes.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int]
-    # gelqf: m reals per slice forward (tau), m*m backward (dl/adjoints.hpp:1-9)
-    assert lib.dla_workspace_bytes(8, 1, 256, 128, 512, 0, 0) == 256 * 128 * 8
+    # gelqf forward: m reals per slice (tau) on the unblocked path (m < 64);
+    # the blocked compact-WY path (m >= 64) also keeps Yc, Z (m x n each),
+    # T and W (m x 32 each) and the norm; backward: m*m (dl/adjoints.hpp:1-9)
+    assert lib.dla_workspace_bytes(8, 1, 256, 32, 512, 0, 0) == 256 * 32 * 8
+    assert lib.dla_workspace_bytes(8, 1, 256, 128, 512, 0, 0) == 256 * (2 * 128 * 512 + 2 * 128 * 32 + 128 + 1) * 8
     assert lib.dla_workspace_bytes(8, 0, 256, 128, 512, 0, 1) == 256 * 128 * 128 * 4
     assert lib.dla_workspace_bytes(9, 1, 1024, 64, 64, 0, 1) == 1024 * 64 * 64 * 8
     assert lib.dla_workspace_bytes(5, 1, 1, 64, 64, 0, 0) == 0
