@@ -168,7 +168,8 @@ def peaks():
 
 
 def gemm_roofline(torch, lib, step_fn):
-    """One extra (untimed) step with CUDA events around every GEMM launch."""
+    """One extra (untimed) step with CUDA events around every GEMM launch:
+    (launches, total ms, total flops) and the largest launch (ms, flops)."""
     import ctypes as C
     torch.cuda.synchronize()
     lib.dla_prof_enable(1)
@@ -176,8 +177,10 @@ def gemm_roofline(torch, lib, step_fn):
     torch.cuda.synchronize()
     ms, fl = C.c_double(0), C.c_double(0)
     n = lib.dla_prof_read(C.byref(ms), C.byref(fl))
+    mms, mfl = C.c_double(0), C.c_double(0)
+    lib.dla_prof_read_max(C.byref(mms), C.byref(mfl))
     lib.dla_prof_enable(0)
-    return n, ms.value, fl.value
+    return n, ms.value, fl.value, mms.value, mfl.value
 
 
 # -------------------------------------------------------------- workloads
@@ -232,9 +235,9 @@ def run_c2(torch, args, rank, world, lib):
     # e2e answer check against the device result
     torch.cuda.synchronize()
     assert abs(outp[0].item() - g.nll[0].item()) <= 1e-9 * abs(g.nll[0].item())
-    nlaunch, gms, gfl = gemm_roofline(torch, lib, step)
+    gemm_stats = gemm_roofline(torch, lib, step)
     return dict(ms=ms, ms_eager=ms_eager, ms_e2e=ms_e2e, launches=launches, clocks=clocks,
-                gemm=(nlaunch, gms, gfl),
+                gemm=gemm_stats,
                 flops=gp_flops(n, d), h2d=xh.nbytes + yh.nbytes, d2h=4 * 8,
                 workload="C2: GP NLL + hyperparameter gradient (and x/y gradients), RBF, n=4096, d=8, fp64",
                 nll=float(g.nll[0].item()), units_per_step=1)
@@ -416,8 +419,9 @@ def main():
     r = run_c2(torch, args, rank, world, lib)
     value = world * r["units_per_step"] / (r["ms"] / 1e3)
     e2e = world * r["units_per_step"] / (r["ms_e2e"] / 1e3)
-    nl, gms, gfl = r["gemm"]
-    achieved = gfl / (gms / 1e3) / 1e12 if gms > 0 else None
+    nl, gms, gfl, mms, mfl = r["gemm"]
+    avg_tf = gfl / (gms / 1e3) / 1e12 if gms > 0 else None
+    achieved = mfl / (mms / 1e3) / 1e12 if mms > 0 else None
     traffic = None
     if os.path.exists(TRAFFIC_FILE):
         traffic = json.load(open(TRAFFIC_FILE)).get("dram_bytes_per_launch")
@@ -439,10 +443,15 @@ def main():
             "launch_mode": "CUDA graph replay of the step's libdla_b200 launches (eager timing in ms_per_step_eager)",
             "step_fp64_tflops": step_tflops,
             "step_frac_of_fp64_peak": step_tflops / fp64_peak,
-            "roofline": {"bound": "tensor", "kernel": "dgemm_dmma (FP64 DMMA m8n8k4 batched GEMM)",
+            "roofline": {"bound": "tensor",
+                         "kernel": "dgemm_dmma<128x128, k-block 32, transposed A> (FP64 DMMA m8n8k4): Z = L^-T W "
+                                   "inside potrf_bwd, the step's largest launch",
                          "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                          "frac": (achieved / fp64_peak) if achieved else None, "traffic": traffic,
+                         "algorithmic": "2n^3/3 useful flops (upper x lower triangular operands) per launch, "
+                                        "event-timed on the launching stream",
                          "peak_source": peak_src, "gemm_launches_per_step": nl,
+                         "all_gemm_launches_tflops": avg_tf,
                          "gemm_share_of_step": (gms / r["ms"]) if r["ms"] else None},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "evals/s", "h2d_bytes_per_step": r["h2d"],

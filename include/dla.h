@@ -202,6 +202,9 @@ long long dla_launch_count(void);
  * default; enabling clears previous records). */
 void dla_prof_enable(int on);
 long long dla_prof_read(double* ms, double* flops);
+/* The recorded GEMM launch(es) with the largest flop count: average event
+ * time (ms) and that flop count; returns how many launches tied. */
+long long dla_prof_read_max(double* ms, double* flops);
 
 /* ----------------------------------------------- fused C1 likelihood chain */
 /* Gaussian log-likelihood chain over a batch of small SPD matrices

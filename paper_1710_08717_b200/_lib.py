@@ -70,6 +70,8 @@ class _Lib:
         L.dla_prof_enable.argtypes = [_int]
         L.dla_prof_read.restype = C.c_longlong
         L.dla_prof_read.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.dla_prof_read_max.restype = C.c_longlong
+        L.dla_prof_read_max.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.dla_gp_rbf_ws_bytes.restype = _sz
         L.dla_gp_rbf_ws_bytes.argtypes = [_i64, _i64, _i64]
         gsig = [_i64, _i64, _i64, _vp, C.c_double, C.c_double, C.c_double]
@@ -111,7 +113,7 @@ def lib() -> _Lib:
 def exported_symbols():
     """Every dla_* symbol include/dla.h declares (used by the CPU symbol test)."""
     names = ["dla_status_string", "dla_version", "dla_workspace_bytes", "dla_info_check",
-             "dla_launch_count", "dla_prof_enable", "dla_prof_read", "dla_gp_rbf_ws_bytes",
+             "dla_launch_count", "dla_prof_enable", "dla_prof_read", "dla_prof_read_max", "dla_gp_rbf_ws_bytes",
              "dla_gp_rbf_fwd_f64", "dla_gp_rbf_bwd_f64", "dla_gp_nll_assemble_f64",
              "dla_ml_shift_copy_f64", "dla_axpy_f64", "dla_ml_reduce_f64"]
     for name in _SIGS:

@@ -523,6 +523,26 @@ long long dla_prof_read(double* ms, double* flops) {
   return (long long)g_prof_recs.size();
 }
 
+long long dla_prof_read_max(double* ms, double* flops) {
+  // the GEMM launch(es) with the largest flop count (ties averaged)
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  double fmaxv = 0;
+  for (auto& r : g_prof_recs) fmaxv = r.flops > fmaxv ? r.flops : fmaxv;
+  double t = 0;
+  long long cnt = 0;
+  for (auto& r : g_prof_recs) {
+    if (r.flops < fmaxv) continue;
+    cudaEventSynchronize(r.b);
+    float x = 0;
+    cudaEventElapsedTime(&x, r.a, r.b);
+    t += x;
+    ++cnt;
+  }
+  if (ms) *ms = cnt ? t / cnt : 0;
+  if (flops) *flops = fmaxv;
+  return cnt;
+}
+
 size_t dla_workspace_bytes(dla_op op, dla_dtype dtype, int64_t batch, int64_t m, int64_t n, int64_t k, int phase) {
   (void)k;
   const bool bwd = (phase & DLA_WS_BACKWARD) != 0;

@@ -1,0 +1,12 @@
+cd /root/repo
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -q -m gpu 2>&1 | tail -2
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; cut -c1-300 gpurun_out/bench_c2.json
+for c in c1 potrf1024 c3 c4 c5; do timeout 600 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; cut -c1-200 gpurun_out/bench_$c.json; done
+timeout 600 python bench.py --impl reference --steps 2 --warmup 0 > gpurun_out/bench_ref.json 2>gpurun_out/bench_ref.err; cut -c1-200 gpurun_out/bench_ref.json
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 700 -c 700 --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 1 --warmup 0 --no-also --no-cpu-baseline > /dev/null 2>&1
+python tools/ncu_summary.py gpurun_out/launches_c2.csv 12
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:Cfg<\(int\)128' -s 2 -c 2 -o gpurun_out/prof_gemm -f python tools/prof_op.py potrf_bwd 4096 2 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:k_chol_chain_warp|k_syevd_small|k_lq_panel|k_potrf_panel|k_trsv' -c 5 -o gpurun_out/prof_misc -f python tools/prof_misc.py > /dev/null 2>&1
+ls gpurun_out/*.ncu-rep
