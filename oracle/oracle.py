@@ -432,3 +432,27 @@ def random_sym(n, r, dtype=np.float64, batch=None):
     shape = (n, n) if batch is None else (batch, n, n)
     x = r.standard_normal(shape)
     return (0.5 * (x + np.swapaxes(x, -1, -2))).astype(dtype)
+
+
+LOG_2PI = 1.8378770664093454835606594728112353
+
+
+def c5_item(p, s, y, theta):
+    """TEST INFRASTRUCTURE: phi and dphi/dtheta of one C5 item (SURVEY §8d's
+    graph: A = S + e^theta I, L = potrf, B = potri, G = trmm(L, B, left, T),
+    v = G y, phi = 1/2 v^T v + sumlogdiag(L) + n/2 log 2 pi) through the
+    oracle's per-op pullbacks (dl/adjoints.hpp)."""
+    import math
+    n = s.shape[0]
+    lam = math.exp(theta)
+    a = s + lam * np.eye(n)
+    l = p.potrf(a)
+    b = p.potri(l)
+    g = p.trmm(l, b, False, True, True)
+    v = p.gemm(g, y)
+    phi = 0.5 * float((v.T @ v)[0, 0]) + p.sumlogdiag(l) + 0.5 * n * LOG_2PI
+    gbar, _ = p.gemm2_bwd(v, g, y)
+    bbar, tbar = p.trmm_bwd(gbar, l, b, False, True, True)
+    lbar = p.potri_bwd(bbar, l, b) + tbar + np.diag(1.0 / np.diag(l))
+    abar = p.potrf_bwd(lbar, l)
+    return phi, lam * np.trace(abar)

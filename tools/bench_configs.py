@@ -148,7 +148,12 @@ def run(torch, args, rank, world, lib, fp64_peak, hbm):
                    "sample": f"reference gelqf+backward over {Bc} of the 256 matrices (fp64, for_each_slice)"}
         return _line(args, world, "gelqf fwd+bwd matrices/s (128x512)", res[0]["matrices_per_s"], "matrices/s",
                      res[0]["ms"], "C3: BLR gelqf fwd+bwd, batch 256 of B=[I_128, X] in R^{128x512} (the reference "
-                     "rejects 512x128, dl/lq.hpp:26-29)", per_dtype=res, cpu_baseline=cpu)
+                     "rejects 512x128, dl/lq.hpp:26-29)", per_dtype=res, cpu_baseline=cpu,
+                     roofline={"bound": "tensor", "achieved": res[0]["tflops"], "peak": fp64_peak, "unit": "TFLOP/s",
+                               "frac": res[0]["tflops"] / fp64_peak, "traffic": None,
+                               "note": "fp64 step: blocked compact-WY LQ (panel kernels latency-bound, trailing "
+                                       "updates on FP64 DMMA) + backward GEMMs; algorithmic flops "
+                                       "4m^2n - 4m^3/3 + m^3/3 + 5m^2n per matrix (SURVEY 8d)"})
     if cfg == "c4":
         B, n = 1024, 64
         r = O.rng(4)
@@ -176,7 +181,11 @@ def run(torch, args, rank, world, lib, fp64_peak, hbm):
         v = world * B / (ms / 1e3)
         return _line(args, world, "syevd fwd+bwd matrices/s (64x64)", v, "matrices/s", ms,
                      "C4: batched syevd fwd+bwd, batch 1024 x 64^2 fp64 (Jacobi, smem-resident)",
-                     gflops=v * flops / B / 1e9, cpu_baseline=cpu)
+                     gflops=v * flops / B / 1e9, cpu_baseline=cpu,
+                     roofline={"bound": "latency", "achieved": v * flops / B / 1e12, "peak": fp64_peak,
+                               "unit": "TFLOP/s", "frac": v * flops / B / 1e12 / fp64_peak, "traffic": None,
+                               "note": "count-convention flops 10n^3/3 + 6n^3 per matrix; the smem Jacobi does "
+                                       "~20x that in FP64 FMA and is bound by its per-round barrier chain"})
     if cfg == "c5":
         from paper_1710_08717_b200.c5 import MarginalLikelihoods
         total, n = 65536, 128
@@ -196,9 +205,28 @@ def run(torch, args, rank, world, lib, fp64_peak, hbm):
         ms = bench.timed(torch, lambda: m.step_allreduce(s, y, theta), args.steps, args.warmup, world)
         m.check()
         flops = total * 8.33 * n ** 3
+        cpu = None
+        if rank == 0 and world == 1 and not getattr(args, "no_cpu_baseline", False):
+            import time as _t
+            port = O.port()
+            sc = s[:1].cpu().numpy()[0]
+            yc = y[:1].cpu().numpy()[0]
+            reps, t0 = 0, _t.perf_counter()
+            while _t.perf_counter() - t0 < 3.0:
+                O.c5_item(port, sc, yc, theta)
+                reps += 1
+            secs = (_t.perf_counter() - t0) / reps
+            cpu = {"value": 1.0 / secs, "unit": "items/s", "cores": 1, "kind": "port",
+                   "sample": f"{reps} C5 items through the oracle port's per-op chain (C restatement of the "
+                             f"reference ops, 1 thread); the reference has no C5 driver"}
         return _line(args, world, "C5 GP marginal likelihoods items/s", total / (ms / 1e3), "items/s", ms,
                      "C5: 65536 x 128^2 GP marginal likelihoods (potrf+potri+trmm fwd+bwd), batch sharded over "
                      f"{world} GPU(s), NCCL all-reduce of (loss, dloss/dtheta)",
                      step_tflops=flops / (ms / 1e3) / 1e12, loss_grad=m.out.cpu().tolist(),
-                     config_parallelism=f"dp{world} (contiguous batch shards)")
+                     config_parallelism=f"dp{world} (contiguous batch shards)", cpu_baseline=cpu,
+                     roofline={"bound": "tensor", "achieved": flops / (ms / 1e3) / 1e12 / world, "peak": fp64_peak,
+                               "unit": "TFLOP/s", "frac": flops / (ms / 1e3) / 1e12 / world / fp64_peak,
+                               "traffic": None,
+                               "note": "per GPU, minimal flops 8.33 n^3 per item (SURVEY 8d); the operator "
+                                       "composition executes ~11 n^3 in 128-wide batched DMMA tiles"})
     raise ValueError(cfg)
