@@ -28,7 +28,10 @@
 #define DLAB_GEMM_BKL 32  // k-block of the 128 x 128 configuration (3 stages: 212 KB smem)
 #endif
 #ifndef DLAB_SHORTK
-#define DLAB_SHORTK 128  // K up to which the 128 x 128 tiles use the 16-deep k-block
+#define DLAB_SHORTK 1024  // K up to which large GEMMs use the two-CTA 128 x 64 tiles
+#endif
+#ifndef DLAB_SHORTK_CFG
+#define DLAB_SHORTK_CFG 1
 #endif
 #ifndef DLAB_GEMM_BKS
 #define DLAB_GEMM_BKS 16  // k-block of the 64 x 64 configuration
@@ -41,19 +44,33 @@ constexpr int STAGES = 3, PAD = 4;
 
 // Tile configurations: CTA tile BM x BN, warp tile WM x WN (FP64 DMMA),
 // k-block BK per pipeline stage.
-template <int BM_, int BN_, int WM_, int WN_, int BK_ = 16>
+template <int BM_, int BN_, int WM_, int WN_, int BK_ = 16, int MINB_ = 1>
 struct Cfg {
-  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, BK = BK_;
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, BK = BK_, MINB = MINB_;
   static constexpr int WARPS_N = BN / WN;
   static constexpr int WARPS = (BM / WM) * (BN / WN);
   static constexpr int NT = WARPS * 32;
 };
-using CfgS = Cfg<64, 64, 32, 32, DLAB_GEMM_BKS>;  // 128 threads: small / batched problems
+#ifndef DLAB_CFGS_MINB
+#define DLAB_CFGS_MINB 4
+#endif
+using CfgS = Cfg<64, 64, 32, 32, DLAB_GEMM_BKS, DLAB_CFGS_MINB>;  // 128 threads: small / batched problems
 using CfgL = Cfg<128, 128, 64, 32, DLAB_GEMM_BKL>;  // 256 threads: large trailing updates
 // short-K (rank <= 128 updates: the blocked Cholesky's trailing SYRKs): a
 // 16-deep k-block keeps 3 stages in 71 KB, so 3 CTAs share an SM and one
 // CTA's C read-modify-write epilogue overlaps another's operand loads
+// Large GEMMs with K <= DLAB_SHORTK, a write mask or a triangular operand:
+// 128 x 64 tiles at two CTAs per SM (110-128 registers), so one CTA's
+// operand prologue and C read-modify-write epilogue overlap the other's DMMA
+// main loop, and the finer tiles balance triangular K ranges.  Measured on
+// B200: the blocked Cholesky's rank-64 SYRKs, the 128^3 batched products of
+// C5 and potrf_bwd's triangular products all gain (C5 -16 %); plain deep-K
+// GEMMs keep the 128 x 128, k-block 32 tiles (31.5 TF/s at 4096^3).
+#if DLAB_SHORTK_CFG == 1
+using CfgK = Cfg<128, 64, 32, 32, 16, 2>;
+#else
 using CfgK = Cfg<128, 128, 64, 32, 16>;
+#endif
 // narrow N (<= 32, deep K): the blocked LQ's W = R Yc^T (rows x 32 x n)
 using CfgN = Cfg<64, 32, 32, 16, 16>;
 
@@ -243,7 +260,7 @@ __device__ __forceinline__ TileCoord<T> decode(const GemmArgs<T>& g, int64_t til
 
 // ------------------------------------------------------------------ f64 DMMA
 template <class C, bool TA, bool TB, int VA, int VB>
-__global__ void __launch_bounds__(C::NT) dgemm_dmma(GemmArgs<double> g) {
+__global__ void __launch_bounds__(C::NT, C::MINB) dgemm_dmma(GemmArgs<double> g) {
   using AT = ATile<C::BM, C::BK, TA>;
   using BT = BTile<C::BN, C::BK, TB>;
   constexpr int MI = C::WM / 8, NI = C::WN / 8, BK = C::BK;
@@ -467,7 +484,7 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large, 
       }
       const unsigned nb = grid(slabs * g.tiles_m * g.tiles_n);
       k<<<nb, C::NT, smem, s>>>(g);
-    } else if (large && g.k <= DLAB_SHORTK) {
+    } else if (large && (g.k <= DLAB_SHORTK || g.mask != MASK_FULL || g.tri_a != TRI_NONE || g.tri_b != TRI_NONE)) {
       using C = CfgK;
       g.tiles_m = (g.m + C::BM - 1) / C::BM;
       g.tiles_n = (g.n + C::BN - 1) / C::BN;
