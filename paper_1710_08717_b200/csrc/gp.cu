@@ -319,19 +319,49 @@ __global__ void k_axpy(int64_t count, double alpha, const double* x, double* y) 
     y[t] += alpha * x[t];
 }
 
-// out[0] = sum_b (quad_b + logdet_b) + batch n/2 log 2 pi, out[1] = lam sum_b tr(abar_b):
-// one CTA, fixed summation order (deterministic; no atomics)
+// out[0] = sum_b (quad_b + logdet_b) + batch n/2 log 2 pi, out[1] = lam sum_b tr(abar_b).
+// Two fixed-order passes (deterministic; no atomics):
+// k_ml_partial — one warp per slice computes the slice's (phi_b, tr_b), CTAs
+// reduce 64 consecutive slices each into part[]; k_ml_final — one CTA sums
+// the parts in order.
 constexpr int MLT = 1024;
-__global__ void __launch_bounds__(MLT) k_ml_reduce(int64_t batch, int64_t n, const double* quad, const double* logdet,
-                                                    const double* abar, double lam, double* out) {
+constexpr int MLS = 64;  // slices per partial CTA (2 per warp)
+__global__ void __launch_bounds__(MLT) k_ml_partial(int64_t batch, int64_t n, const double* quad,
+                                                     const double* logdet, const double* abar, double* part) {
+  __shared__ double s0[MLS], s1[MLS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int q = warp; q < MLS; q += MLT / 32) {
+    const int64_t b = blockIdx.x * (int64_t)MLS + q;
+    double tr = 0.0;
+    if (b < batch) {
+      const double* ab = abar + b * n * n;
+      for (int64_t i = lane; i < n; i += 32) tr += ab[i * (n + 1)];
+    }
+    for (int o = 16; o; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    if (lane == 0) {
+      s0[q] = b < batch ? quad[b] + logdet[b] : 0.0;
+      s1[q] = tr;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, g = 0.0;
+    for (int q = 0; q < MLS; ++q) {
+      a += s0[q];
+      g += s1[q];
+    }
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = g;
+  }
+}
+
+__global__ void __launch_bounds__(MLT) k_ml_final(int64_t nparts, int64_t batch, int64_t n, const double* part,
+                                                   double lam, double* out) {
   __shared__ double r0[MLT], r1[MLT];
   double a = 0.0, g = 0.0;
-  for (int64_t b = threadIdx.x; b < batch; b += MLT) {
-    a += quad[b] + logdet[b];
-    const double* ab = abar + b * n * n;
-    double tr = 0.0;
-    for (int64_t i = 0; i < n; ++i) tr += ab[i * (n + 1)];
-    g += tr;
+  for (int64_t p = threadIdx.x; p < nparts; p += MLT) {
+    a += part[2 * p];
+    g += part[2 * p + 1];
   }
   r0[threadIdx.x] = a;
   r1[threadIdx.x] = g;
@@ -433,7 +463,15 @@ dla_status dla_axpy_f64(int64_t count, double alpha, const double* x, double* y,
 dla_status dla_ml_reduce_f64(int64_t batch, int64_t n, const double* quad, const double* logdet, const double* abar,
                              double lam, double* out, void* stream) {
   if (batch < 0 || n < 0) return DLA_ERR_SHAPE;
-  k_ml_reduce<<<1, MLT, 0, reinterpret_cast<cudaStream_t>(stream)>>>(batch, n, quad, logdet, abar, lam, out);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t nparts = batch > 0 ? (batch + MLS - 1) / MLS : 0;
+  Scratch part(sizeof(double) * (size_t)(2 * (nparts > 0 ? nparts : 1)), s);
+  if (!part.p) return DLA_ERR_CUDA;
+  if (nparts > 0) {
+    k_ml_partial<<<(unsigned)nparts, MLT, 0, s>>>(batch, n, quad, logdet, abar, part.as<double>());
+    DLAB_LAUNCH_CHECK();
+  }
+  k_ml_final<<<1, MLT, 0, s>>>(nparts, batch, n, part.as<double>(), lam, out);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }
