@@ -136,7 +136,7 @@ template <int D, bool FWD>
 __global__ void __launch_bounds__(256) k_rbf_tiled(int64_t n, const double* x, const double* s, double sigma2,
                                                    double two_ell2, double lam, double* a, const double* abar,
                                                    double* xpart, double* part) {
-  __shared__ double xs[TCJ][D];
+  __shared__ double xs[TCJ][D + 1];  // odd row stride: lane-strided reads are conflict-free
   __shared__ double ss[TCJ];
   const int64_t rb = (n + TRW - 1) / TRW, splits = rbf_splits(n);
   const int64_t sp = blockIdx.x % splits, blk = blockIdx.x / splits;
