@@ -206,6 +206,20 @@ long long dla_prof_read(double* ms, double* flops);
  * time (ms) and that flop count; returns how many launches tied. */
 long long dla_prof_read_max(double* ms, double* flops);
 
+/* --------------------------------------------- split potrf pullback (driver) */
+/* dla_potrf_bwd_f64 in two stream-ordered halves so a driver can overlap the
+ * factor's inverse with work that only reads L (the GP driver's solves):
+ * _begin forks L^-1 onto an internal side stream; _end joins and produces
+ * Abar bitwise identical to dla_potrf_bwd_f64 (dl/adjoints.hpp:175-191).  L
+ * must not change in between; one begin/end pair in flight per process.
+ * Sizes where the inverse path does not apply (n != 64 * 2^k) make _begin a
+ * no-op and _end the plain pullback.  Workspace: dla_potrf_bwd_ws_bytes_f64. */
+size_t dla_potrf_bwd_ws_bytes_f64(int64_t batch, int64_t n);
+dla_status dla_potrf_bwd_begin_f64(int64_t batch, int64_t n, const double* l, int lower, void* ws,
+                                   size_t ws_bytes, void* stream);
+dla_status dla_potrf_bwd_end_f64(int64_t batch, int64_t n, double* abar, const double* lbar,
+                                 const double* l, int lower, void* ws, size_t ws_bytes, void* stream);
+
 /* ----------------------------------------------- fused C1 likelihood chain */
 /* Gaussian log-likelihood chain over a batch of small SPD matrices
  * (BASELINE config C1; the make_gp graph dl/models.hpp:99-103 given A):

@@ -81,6 +81,12 @@ class _Lib:
         L.dla_gp_rbf_bwd_f64.restype = _int
         L.dla_gp_nll_assemble_f64.argtypes = [_i64, _i64, _vp, _vp, _vp, _vp]
         L.dla_gp_nll_assemble_f64.restype = _int
+        L.dla_potrf_bwd_ws_bytes_f64.restype = _sz
+        L.dla_potrf_bwd_ws_bytes_f64.argtypes = [_i64, _i64]
+        L.dla_potrf_bwd_begin_f64.argtypes = [_i64, _i64, _vp, _int, _vp, _sz, _vp]
+        L.dla_potrf_bwd_begin_f64.restype = _int
+        L.dla_potrf_bwd_end_f64.argtypes = [_i64, _i64, _vp, _vp, _vp, _int, _vp, _sz, _vp]
+        L.dla_potrf_bwd_end_f64.restype = _int
         L.dla_ml_shift_copy_f64.argtypes = [_i64, _i64, _vp, _vp, C.c_double, _vp]
         L.dla_ml_shift_copy_f64.restype = _int
         L.dla_axpy_f64.argtypes = [_i64, C.c_double, _vp, _vp, _vp]
@@ -115,7 +121,8 @@ def exported_symbols():
     names = ["dla_status_string", "dla_version", "dla_workspace_bytes", "dla_info_check",
              "dla_launch_count", "dla_prof_enable", "dla_prof_read", "dla_prof_read_max", "dla_gp_rbf_ws_bytes",
              "dla_gp_rbf_fwd_f64", "dla_gp_rbf_bwd_f64", "dla_gp_nll_assemble_f64",
-             "dla_ml_shift_copy_f64", "dla_axpy_f64", "dla_ml_reduce_f64"]
+             "dla_ml_shift_copy_f64", "dla_axpy_f64", "dla_ml_reduce_f64", "dla_potrf_bwd_ws_bytes_f64",
+             "dla_potrf_bwd_begin_f64", "dla_potrf_bwd_end_f64"]
     for name in _SIGS:
         for s in ("f32", "f64"):
             names.append(f"dla_{name}_{s}")

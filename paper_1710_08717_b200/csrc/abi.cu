@@ -474,6 +474,65 @@ dla_status chol_chain_abi(int64_t batch, int64_t n, const T* a, const T* y, T* p
   return potrf_bwd<T>(batch, n, abar, abar, l, 1, stream);
 }
 
+// ------------------------------------------- split potrf pullback (drivers)
+// L^{-1} for the inverse-based potrf pullback computed on a side stream
+// forked from the caller's stream, so a driver can overlap it with work
+// that only needs L (the GP driver's solves).  One begin/end pair in flight
+// per process; both halves are stream-ordered and graph-capturable.
+struct InvFork {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, done = nullptr;
+  static InvFork& get() {
+    static InvFork f;
+    static std::once_flag once;
+    std::call_once(once, [] {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      cudaStreamCreateWithPriority(&f.side, cudaStreamNonBlocking, lo);
+      cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&f.done, cudaEventDisableTiming);
+    });
+    return f;
+  }
+};
+
+template <typename T>
+size_t potrf_inv_ws(int64_t batch, int64_t n) {
+  return sizeof(T) * (size_t)batch * 2 * (size_t)n * n + (size_t)batch * trtri_levels_tmp<T>(n);
+}
+
+template <typename T>
+dla_status potrf_bwd_begin(int64_t batch, int64_t n, const T* l, int lower, void* ws, size_t wsb, void* stream) {
+  if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
+  if (batch * n == 0 || !inv_eligible<T>(n)) return DLA_OK;  // end() takes the direct path
+  if (!ws || wsb < potrf_inv_ws<T>(batch, n)) return DLA_ERR_WORKSPACE;
+  Ctx cx = make_ctx(stream, nullptr);
+  InvFork& f = InvFork::get();
+  Ctx side = cx;
+  side.stream = f.side;
+  cudaEventRecord(f.fork, cx.stream);
+  cudaStreamWaitEvent(f.side, f.fork, 0);
+  T* wp = static_cast<T*>(ws);
+  DLAB_TRY(potrf_inv_prepare<T>(side, batch, n, cpk(l, n, n), lower != 0, pk(wp, n, n), wp + 2 * batch * n * n));
+  cudaEventRecord(f.done, f.side);
+  return DLA_OK;
+}
+
+template <typename T>
+dla_status potrf_bwd_end(int64_t batch, int64_t n, T* abar, const T* lbar, const T* l, int lower, void* ws,
+                         size_t wsb, void* stream) {
+  if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
+  if (batch * n == 0 || !inv_eligible<T>(n)) return potrf_bwd<T>(batch, n, abar, lbar, l, lower, stream);
+  const size_t sz = bytes<T>(batch, n, n);
+  if (overlap(abar, sz, l, sz) || (abar != lbar && overlap(abar, sz, lbar, sz))) return DLA_ERR_ALIAS;
+  if (!ws || wsb < potrf_inv_ws<T>(batch, n)) return DLA_ERR_WORKSPACE;
+  Ctx cx = make_ctx(stream, nullptr);
+  cudaStreamWaitEvent(cx.stream, InvFork::get().done, 0);
+  T* wp = static_cast<T*>(ws);
+  return potrf_bwd_from_inv<T>(cx, batch, n, pk(abar, n, n), cpk(lbar, n, n), cpk(l, n, n), lower != 0,
+                               cpk(wp, n, n), pk(wp + batch * n * n, n, n));
+}
+
 extern "C" {
 
 const char* dla_status_string(dla_status s) {
@@ -653,6 +712,18 @@ dla_status dla_info_check(const int32_t* info, int64_t batch, void* stream, int6
 
 DLA_DEFINE(float, f32)
 DLA_DEFINE(double, f64)
+
+size_t dla_potrf_bwd_ws_bytes_f64(int64_t batch, int64_t n) {
+  return inv_eligible<double>(n) ? potrf_inv_ws<double>(batch, n) : 0;
+}
+dla_status dla_potrf_bwd_begin_f64(int64_t batch, int64_t n, const double* l, int lower, void* ws, size_t ws_bytes,
+                                   void* stream) {
+  return potrf_bwd_begin<double>(batch, n, l, lower, ws, ws_bytes, stream);
+}
+dla_status dla_potrf_bwd_end_f64(int64_t batch, int64_t n, double* abar, const double* lbar, const double* l,
+                                 int lower, void* ws, size_t ws_bytes, void* stream) {
+  return potrf_bwd_end<double>(batch, n, abar, lbar, l, lower, ws, ws_bytes, stream);
+}
 
 dla_status dla_chol_chain_fwdbwd_f64(int64_t batch, int64_t n, const double* a, const double* y, double* phi,
                                      double* abar, double* ybar, int32_t* info, void* stream) {

@@ -132,6 +132,37 @@ dla_status trsm_inv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<cons
   return ew_copy<T>(c, batch, m, n, C_(y), x, c.info);
 }
 
+// L^{-1} (lower form) of the factor into wi, with tmp >= trtri_levels_tmp(n)
+// per slice: the first half of potrf_bwd_inv, callable ahead of time.
+template <typename T>
+dla_status potrf_inv_prepare(const Ctx& c, int64_t batch, int64_t n, MatB<const T> l, bool lower, MatB<T> wi, T* tmp) {
+  DLAB_TRY(ew_tri_copy<T>(c, batch, n, l, wi, !lower));
+  return trtri_levels<T>(c, batch, n, wi, tmp);
+}
+
+// The second half: Abar from Lbar, L and the prepared wi = L^{-1}; tt is n^2
+// scratch per slice.
+template <typename T>
+dla_status potrf_bwd_from_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> lbar, MatB<const T> l,
+                              bool lower, MatB<const T> wi, MatB<T> tt) {
+  // Upper variant: L = R^T, Lbar = Rbar^T (dl/adjoints.hpp:183-188 is the
+  // transposed composition); the result is symmetric, so no final transpose.
+  // P = tril(L^T Lbar): op(A) = L^T (upper), op(B) = tril(Lbar); then halve
+  // its diagonal so that Phi = copyltu(P) = P' + P'^T exactly.
+  DLAB_TRY(gemm<T>(c, batch, n, n, n, T(1), l, lower, lbar, !lower, T(0), tt, MASK_LOWER, nullptr, TRI_UPPER,
+                   TRI_LOWER));
+  DLAB_TRY(ew_scale_diag<T>(c, batch, n, tt, T(0.5)));
+  // W = P' L^{-1}: lower x lower = lower  (into abar; lbar is no longer read,
+  // so abar may alias it)
+  DLAB_TRY(gemm<T>(c, batch, n, n, n, T(1), C_(tt), false, wi, false, T(0), abar, MASK_LOWER, nullptr, TRI_LOWER,
+                   TRI_LOWER));
+  // Z = L^{-T} W  (upper x lower, full);  L^-T Phi L^-1 = Z + Z^T
+  DLAB_TRY(gemm<T>(c, batch, n, n, n, T(1), wi, true, C_(abar), false, T(0), tt, MASK_FULL, nullptr, TRI_UPPER,
+                   TRI_LOWER));
+  // Abar = 1/2 (Z + Z^T), bit-symmetric
+  return ew_add_transpose<T>(c, batch, n, C_(tt), abar, T(0.5));
+}
+
 template <typename T>
 dla_status potrf_bwd_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> lbar, MatB<const T> l,
                          bool lower) {
@@ -141,24 +172,8 @@ dla_status potrf_bwd_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, M
   MatB<T> wi{wp, n, n * n};                  // L^{-1} (lower)
   MatB<T> tt{wp + batch * n * n, n, n * n};  // Phi, then the lower half of L^-T Phi L^-1
   T* tmp = wp + 2 * batch * n * n;
-  // Upper variant: L = R^T, Lbar = Rbar^T (dl/adjoints.hpp:183-188 is the
-  // transposed composition); the result is symmetric, so no final transpose.
-  DLAB_TRY(ew_tri_copy<T>(c, batch, n, l, wi, !lower));
-  DLAB_TRY(trtri_levels<T>(c, batch, n, wi, tmp));
-  // P = tril(L^T Lbar): op(A) = L^T (upper), op(B) = tril(Lbar); then halve
-  // its diagonal so that Phi = copyltu(P) = P' + P'^T exactly.
-  DLAB_TRY(gemm<T>(c, batch, n, n, n, T(1), l, lower, lbar, !lower, T(0), tt, MASK_LOWER, nullptr, TRI_UPPER,
-                   TRI_LOWER));
-  DLAB_TRY(ew_scale_diag<T>(c, batch, n, tt, T(0.5)));
-  // W = P' L^{-1}: lower x lower = lower  (into abar; lbar is no longer read,
-  // so abar may alias it)
-  DLAB_TRY(gemm<T>(c, batch, n, n, n, T(1), C_(tt), false, C_(wi), false, T(0), abar, MASK_LOWER, nullptr, TRI_LOWER,
-                   TRI_LOWER));
-  // Z = L^{-T} W  (upper x lower, full);  L^-T Phi L^-1 = Z + Z^T
-  DLAB_TRY(gemm<T>(c, batch, n, n, n, T(1), C_(wi), true, C_(abar), false, T(0), tt, MASK_FULL, nullptr, TRI_UPPER,
-                   TRI_LOWER));
-  // Abar = 1/2 (Z + Z^T), bit-symmetric
-  return ew_add_transpose<T>(c, batch, n, C_(tt), abar, T(0.5));
+  DLAB_TRY(potrf_inv_prepare<T>(c, batch, n, l, lower, wi, tmp));
+  return potrf_bwd_from_inv<T>(c, batch, n, abar, lbar, l, lower, C_(wi), tt);
 }
 
 // X <- alpha op(T) X / alpha X op(T) as ONE triangular GEMM into scratch plus
@@ -203,7 +218,10 @@ dla_status potri_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
   template dla_status trtri_levels<T>(const Ctx&, int64_t, int64_t, MatB<T>, T*);                            \
   template dla_status trsm_inv<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<const T>, MatB<T>, bool, bool, \
                                   bool, T);                                                                  \
-  template dla_status potrf_bwd_inv<T>(const Ctx&, int64_t, int64_t, MatB<T>, MatB<const T>, MatB<const T>, bool);
+  template dla_status potrf_bwd_inv<T>(const Ctx&, int64_t, int64_t, MatB<T>, MatB<const T>, MatB<const T>, bool); \
+  template dla_status potrf_inv_prepare<T>(const Ctx&, int64_t, int64_t, MatB<const T>, bool, MatB<T>, T*);      \
+  template dla_status potrf_bwd_from_inv<T>(const Ctx&, int64_t, int64_t, MatB<T>, MatB<const T>, MatB<const T>, \
+                                            bool, MatB<const T>, MatB<T>);
 INST(double)
 INST(float)
 

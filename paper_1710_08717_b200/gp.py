@@ -11,7 +11,9 @@ of independent GP problems:
   backward, phibar = 1:
     zbar = z;  (ybar, Lbar) = trsm_backward(zbar, L, z)   (C-ABI op)
     Lbar += diag(1 / L_ii)                                (sumlogdiag_backward)
-    Abar = potrf_backward(Lbar, L)  (in place)            (C-ABI op)
+    Abar = potrf_backward(Lbar, L)  (in place)            (C-ABI op, split:
+           L^-1 forms on a side stream from right after potrf, overlapping
+           the solves; dla_potrf_bwd_{begin,end}_f64, bitwise = the op)
     (d/dlog sigma2, d/dlog ell2, d/dlog lam, xbar) = RBF pullback(Abar)
 
 Every step is a libdla_b200.so call on torch's current stream; the driver
@@ -51,6 +53,11 @@ class GPNLL:
         nb = int(lib().lib.dla_gp_rbf_ws_bytes(batch, n, d))
         self.ws = torch.empty(max(nb, 8), dtype=torch.uint8, device=self.device)
         self.ws_bytes = nb
+        # split potrf pullback: L^-1 is formed on a side stream while the
+        # solves (which only read L) run on the caller's stream
+        nbi = int(lib().lib.dla_potrf_bwd_ws_bytes_f64(batch, n))
+        self.iws = torch.empty(max(nbi, 8), dtype=torch.uint8, device=self.device)
+        self.iws_bytes = nbi
 
     def _stream(self):
         return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
@@ -70,6 +77,11 @@ class GPNLL:
         if st:
             L._raise_status(st, "gp_rbf_fwd")
         L.potrf_inplace(self.a, True, check=False, info=self.info)
+        lib_ = lib().lib
+        st = lib_.dla_potrf_bwd_begin_f64(B, n, C.c_void_p(self.a.data_ptr()), 1, C.c_void_p(self.iws.data_ptr()),
+                                          self.iws_bytes, self._stream())
+        if st:
+            L._raise_status(st, "potrf_bwd_begin")
         self.z.copy_(y)
         L.trsm_inplace(self.a, self.z, False, False, True, 1.0, check=False)
         L.gemm2_into(self.quad, self.z, self.z, True, False, 0.5)
@@ -82,7 +94,11 @@ class GPNLL:
         # backward (phibar = 1): zbar = z
         L.trsm_backward_into(self.ybar, self.lbar, self.z, self.a, self.z, False, False, True, 1.0)
         L.sumlogdiag_backward_into(self.lbar, self.ones, self.a, accumulate=True)
-        L.potrf_backward_into(self.lbar, self.lbar, self.a, True)
+        st = lib_.dla_potrf_bwd_end_f64(B, n, C.c_void_p(self.lbar.data_ptr()), C.c_void_p(self.lbar.data_ptr()),
+                                        C.c_void_p(self.a.data_ptr()), 1, C.c_void_p(self.iws.data_ptr()),
+                                        self.iws_bytes, self._stream())
+        if st:
+            L._raise_status(st, "potrf_bwd_end")
         st = lib().lib.dla_gp_rbf_bwd_f64(B, n, d, C.c_void_p(x.data_ptr()), sigma2, ell2, lam,
                                           C.c_void_p(self.lbar.data_ptr()),
                                           C.c_void_p(self.xbar.data_ptr()) if self.xbar is not None else None,

@@ -209,6 +209,28 @@ def test_trsm_singular_reports_index_and_leaves_slice():
 POTRF_N = [1, 2, 5, 17, 32, 63, 64, 65, 70, 129, 200, 256, 512]  # 256/512: inverse-based DMMA paths
 
 
+def test_potrf_bwd_split_is_bitwise_the_op():
+    """dla_potrf_bwd_{begin,end}_f64 (L^-1 on a side stream, used by the GP
+    driver) must reproduce dla_potrf_bwd_f64 bit for bit."""
+    import ctypes as C
+    from paper_1710_08717_b200._lib import lib
+    lb = lib().lib
+    r = O.rng(78)
+    for n, B in ((256, 2), (512, 1), (300, 2)):
+        l = dev(np.linalg.cholesky(O.random_spd(n, r, batch=B)))
+        lbar = dev(np.tril(r.standard_normal((B, n, n))))
+        want = L.potrf_backward(lbar, l)
+        nb = int(lb.dla_potrf_bwd_ws_bytes_f64(B, n))
+        ws = torch.empty(max(nb, 8), dtype=torch.uint8, device="cuda")
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        got = torch.empty_like(l)
+        assert lb.dla_potrf_bwd_begin_f64(B, n, C.c_void_p(l.data_ptr()), 1, C.c_void_p(ws.data_ptr()), nb, st) == 0
+        assert lb.dla_potrf_bwd_end_f64(B, n, C.c_void_p(got.data_ptr()), C.c_void_p(lbar.data_ptr()),
+                                        C.c_void_p(l.data_ptr()), 1, C.c_void_p(ws.data_ptr()), nb, st) == 0
+        torch.cuda.synchronize()
+        assert torch.equal(got, want)
+
+
 def test_potrf_large_blocked_lookahead():
     """Blocked look-ahead path at sizes with many panel CTAs per launch (the
     panel kernel's redundant A11 reads must never see the written L11)."""
