@@ -527,10 +527,12 @@ dla_status potrf_bwd_end(int64_t batch, int64_t n, T* abar, const T* lbar, const
   if (overlap(abar, sz, l, sz) || (abar != lbar && overlap(abar, sz, lbar, sz))) return DLA_ERR_ALIAS;
   if (!ws || wsb < potrf_inv_ws<T>(batch, n)) return DLA_ERR_WORKSPACE;
   Ctx cx = make_ctx(stream, nullptr);
-  cudaStreamWaitEvent(cx.stream, InvFork::get().done, 0);
   T* wp = static_cast<T*>(ws);
-  return potrf_bwd_from_inv<T>(cx, batch, n, pk(abar, n, n), cpk(lbar, n, n), cpk(l, n, n), lower != 0,
-                               cpk(wp, n, n), pk(wp + batch * n * n, n, n));
+  MatB<T> tt = pk(wp + batch * n * n, n, n);
+  // P' needs only L and Lbar: it overlaps the inverse still running on the side stream
+  DLAB_TRY(potrf_bwd_phi<T>(cx, batch, n, cpk(lbar, n, n), cpk(l, n, n), lower != 0, tt));
+  cudaStreamWaitEvent(cx.stream, InvFork::get().done, 0);
+  return potrf_bwd_finish<T>(cx, batch, n, pk(abar, n, n), cpk(wp, n, n), tt);
 }
 
 extern "C" {

@@ -142,16 +142,22 @@ dla_status potrf_inv_prepare(const Ctx& c, int64_t batch, int64_t n, MatB<const 
 
 // The second half: Abar from Lbar, L and the prepared wi = L^{-1}; tt is n^2
 // scratch per slice.
+// P' = tril(L^T Lbar) with a halved diagonal into tt (needs L and Lbar only).
 template <typename T>
-dla_status potrf_bwd_from_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> lbar, MatB<const T> l,
-                              bool lower, MatB<const T> wi, MatB<T> tt) {
+dla_status potrf_bwd_phi(const Ctx& c, int64_t batch, int64_t n, MatB<const T> lbar, MatB<const T> l, bool lower,
+                         MatB<T> tt) {
   // Upper variant: L = R^T, Lbar = Rbar^T (dl/adjoints.hpp:183-188 is the
   // transposed composition); the result is symmetric, so no final transpose.
   // P = tril(L^T Lbar): op(A) = L^T (upper), op(B) = tril(Lbar); then halve
   // its diagonal so that Phi = copyltu(P) = P' + P'^T exactly.
   DLAB_TRY(gemm<T>(c, batch, n, n, n, T(1), l, lower, lbar, !lower, T(0), tt, MASK_LOWER, nullptr, TRI_UPPER,
                    TRI_LOWER));
-  DLAB_TRY(ew_scale_diag<T>(c, batch, n, tt, T(0.5)));
+  return ew_scale_diag<T>(c, batch, n, tt, T(0.5));
+}
+
+// The rest once wi = L^{-1} is ready: tt holds P' on entry.
+template <typename T>
+dla_status potrf_bwd_finish(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> wi, MatB<T> tt) {
   // W = P' L^{-1}: lower x lower = lower  (into abar; lbar is no longer read,
   // so abar may alias it)
   DLAB_TRY(gemm<T>(c, batch, n, n, n, T(1), C_(tt), false, wi, false, T(0), abar, MASK_LOWER, nullptr, TRI_LOWER,
@@ -161,6 +167,13 @@ dla_status potrf_bwd_from_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> ab
                    TRI_LOWER));
   // Abar = 1/2 (Z + Z^T), bit-symmetric
   return ew_add_transpose<T>(c, batch, n, C_(tt), abar, T(0.5));
+}
+
+template <typename T>
+dla_status potrf_bwd_from_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> lbar, MatB<const T> l,
+                              bool lower, MatB<const T> wi, MatB<T> tt) {
+  DLAB_TRY(potrf_bwd_phi<T>(c, batch, n, lbar, l, lower, tt));
+  return potrf_bwd_finish<T>(c, batch, n, abar, wi, tt);
 }
 
 template <typename T>
@@ -221,7 +234,9 @@ dla_status potri_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
   template dla_status potrf_bwd_inv<T>(const Ctx&, int64_t, int64_t, MatB<T>, MatB<const T>, MatB<const T>, bool); \
   template dla_status potrf_inv_prepare<T>(const Ctx&, int64_t, int64_t, MatB<const T>, bool, MatB<T>, T*);      \
   template dla_status potrf_bwd_from_inv<T>(const Ctx&, int64_t, int64_t, MatB<T>, MatB<const T>, MatB<const T>, \
-                                            bool, MatB<const T>, MatB<T>);
+                                            bool, MatB<const T>, MatB<T>);                                         \
+  template dla_status potrf_bwd_phi<T>(const Ctx&, int64_t, int64_t, MatB<const T>, MatB<const T>, bool, MatB<T>); \
+  template dla_status potrf_bwd_finish<T>(const Ctx&, int64_t, int64_t, MatB<T>, MatB<const T>, MatB<T>);
 INST(double)
 INST(float)
 

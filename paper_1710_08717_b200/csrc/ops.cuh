@@ -37,6 +37,11 @@ template <typename T>
 dla_status potrf_bwd_from_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> lbar, MatB<const T> l,
                               bool lower, MatB<const T> wi, MatB<T> tt);
 template <typename T>
+dla_status potrf_bwd_phi(const Ctx& c, int64_t batch, int64_t n, MatB<const T> lbar, MatB<const T> l, bool lower,
+                         MatB<T> tt);
+template <typename T>
+dla_status potrf_bwd_finish(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> wi, MatB<T> tt);
+template <typename T>
 dla_status trmm_gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x, bool right,
                      bool trans, bool lower, T alpha);
 template <typename T>
