@@ -15,6 +15,8 @@
 //                  GEMMs: 2 n^3 flops, all DMMA, vs the composed 3 n^3 of
 //                  trmm + 2 trsm.
 // Scratch (n^2 per slice) comes from the stream-ordered pool.
+#include <mutex>
+
 #include "chol64.cuh"
 #include "common.cuh"
 #include "ops.cuh"
@@ -185,8 +187,28 @@ dla_status potrf_bwd_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, M
   MatB<T> wi{wp, n, n * n};                  // L^{-1} (lower)
   MatB<T> tt{wp + batch * n * n, n, n * n};  // Phi, then the lower half of L^-T Phi L^-1
   T* tmp = wp + 2 * batch * n * n;
-  DLAB_TRY(potrf_inv_prepare<T>(c, batch, n, l, lower, wi, tmp));
-  return potrf_bwd_from_inv<T>(c, batch, n, abar, lbar, l, lower, C_(wi), tt);
+  // L^-1 (trtri) and P' = tril(L^T Lbar) are independent: the inverse runs
+  // on a side stream (event fork/join: stream-ordered, graph-capturable)
+  // while P' runs on the caller's stream.
+  static cudaStream_t side = nullptr;
+  static cudaEvent_t fork = nullptr, join = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+  });
+  static std::mutex mu;  // one fork in flight per process
+  std::lock_guard<std::mutex> lk(mu);
+  Ctx sc = c;
+  sc.stream = side;
+  cudaEventRecord(fork, c.stream);
+  cudaStreamWaitEvent(side, fork, 0);
+  DLAB_TRY(potrf_inv_prepare<T>(sc, batch, n, l, lower, wi, tmp));
+  cudaEventRecord(join, side);
+  DLAB_TRY(potrf_bwd_phi<T>(c, batch, n, lbar, l, lower, tt));
+  cudaStreamWaitEvent(c.stream, join, 0);
+  return potrf_bwd_finish<T>(c, batch, n, abar, C_(wi), tt);
 }
 
 // X <- alpha op(T) X / alpha X op(T) as ONE triangular GEMM into scratch plus
