@@ -1,0 +1,31 @@
+"""Small invocations of every kernel family for compute-sanitizer runs."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from oracle import oracle as O  # noqa: E402  (input generator only)
+from paper_1710_08717_b200 import gp  # noqa: E402
+from paper_1710_08717_b200 import linalg as L  # noqa: E402
+
+r = O.rng(1)
+f = dict(dtype=torch.float64, device="cuda")
+for n, B in ((16, 3), (40, 2), (200, 2), (256, 1)):
+    a = torch.from_numpy(O.random_spd(n, r, batch=B)).cuda()
+    l = L.potrf(a)
+    L.potrf_backward(torch.tril(torch.randn_like(l)), l)
+    L.potri(l)
+    y = torch.randn(B, n, 1, **f)
+    L.trsm(l, y)
+    L.trsm(l, y, False, True, True)
+    L.chol_chain_fwdbwd(a, y)
+x = torch.randn(2, 64, 64, **f)
+L.syevd(0.5 * (x + x.transpose(-1, -2)))
+q = torch.randn(2, 80, 120, **f)
+L.gelqf(q)
+L.gemm2(torch.randn(2, 130, 70, **f), torch.randn(2, 70, 90, **f))
+gp.gp_nll_grad(torch.randn(256, 8, **f), torch.randn(256, 1, **f), 1.0, 1.0, 0.1)
+torch.cuda.synchronize()
+print("sanitize cases done")
