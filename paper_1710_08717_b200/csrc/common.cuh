@@ -163,6 +163,11 @@ dla_status gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T 
                 bool ta, MatB<const T> b, bool tb, T beta, MatB<T> cm, int mask = MASK_FULL,
                 const int32_t* skip = nullptr, int tri_a = TRI_NONE, int tri_b = TRI_NONE, int64_t inner = 1);
 
+// gemm_tc.cu: fp32 on tcgen05 (3xTF32); false = not handled
+bool sgemm_tc(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, float alpha, MatB<const float> a, bool ta,
+              MatB<const float> b, bool tb, float beta, MatB<float> cm, int mask, const int32_t* skip, int tri_a,
+              int tri_b, int64_t inner, dla_status* st);
+
 // skinny.cu: n <= 8, m <= 8 or k <= 8 without triangular operands; returns
 // false when the shape is not skinny (the caller runs the tiled GEMM).
 template <typename T>

@@ -583,6 +583,21 @@ dla_status gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T 
     dla_status st;
     if (gemm_skinny<T>(c, batch, m, n, k, alpha, a, ta, b, tb, beta, cm, mask, skip, &st)) return st;
   }
+  if constexpr (sizeof(T) == 4) {  // large fp32 products: tcgen05 3xTF32 (gemm_tc.cu)
+    static const bool tc = [] {
+      const char* e = getenv("DLA_SGEMM_TC");  // tuning switch: 0 keeps every fp32 GEMM on FFMA
+      return e ? atoi(e) != 0 : true;
+    }();
+    if (tc && inner == 1 && m >= 256 && n >= 256 && k >= 128) {  // big products: the packing pass pays off
+      dla_status st;
+      const bool prof = gemm_prof_on();
+      if (prof) gemm_prof_begin(c.stream);
+      if (sgemm_tc(c, batch, m, n, k, alpha, a, ta, b, tb, beta, cm, mask, skip, tri_a, tri_b, inner, &st)) {
+        if (prof) gemm_prof_end(c.stream, useful_flops(m, n, k, mask, tri_a, tri_b) * (double)batch);
+        return st;
+      }
+    }
+  }
   GemmArgs<T> g{m, n, k, alpha, beta, a, b, cm, mask, skip, 0, 0, tri_a, tri_b, inner, 0};
   const bool va = vec_ok<T>(a, ta ? m : k);
   const bool vb = vec_ok<T>(b, tb ? k : n);

@@ -104,6 +104,30 @@ def test_gemm_backward(port, dt):
         assert_close(host(cio), 0.5 * cb, dt)
 
 
+def test_sgemm_tcgen05_3xtf32():
+    """Large fp32 products run on tcgen05 (kind::tf32, 3xTF32 split, packed
+    tiles moved by bulk async copies): fp32-level accuracy on every
+    transposition, ragged edges, batch, alpha / beta, masks and triangular
+    operands (through trmm)."""
+    torch.manual_seed(3)
+    for (B, m, n, k) in ((1, 256, 256, 128), (2, 300, 270, 333)):
+        for ta, tb in itertools.product([False, True], repeat=2):
+            a = torch.randn(B, *((k, m) if ta else (m, k)), device="cuda")
+            b = torch.randn(B, *((n, k) if tb else (k, n)), device="cuda")
+            c0 = torch.randn(B, m, n, device="cuda")
+            c = c0.clone()
+            L.gemm_into(c, a, b, ta, tb, 0.7, 0.3)
+            ad, bd = a.double(), b.double()
+            want = 0.7 * (ad.transpose(-1, -2) if ta else ad) @ (bd.transpose(-1, -2) if tb else bd) + 0.3 * c0.double()
+            assert ((c.double() - want).abs().max() / want.abs().max()).item() < 1e-5  # fp32-level (k <= 333)
+    r = O.rng(12)
+    t = tri_factor(r, 384, True, np.float32, 2)
+    x = r.standard_normal((2, 384, 300)).astype(np.float32)
+    got = host(L.trmm(dev(t), dev(x), False, True, True, 1.0))
+    want = np.einsum("bki,bkj->bij", t.astype(np.float64), x.astype(np.float64))
+    assert np.abs(got - want).max() / np.abs(want).max() < 1e-5
+
+
 def test_gemm_rejects_alias_and_shape():
     a = torch.zeros(3, 3, dtype=torch.float64, device="cuda")
     with pytest.raises(L.Error):
