@@ -110,8 +110,14 @@ def run(torch, args, rank, world, lib, fp64_peak, hbm):
             secs, _ = ref.potrf_fwdbwd_batch(a, lb, min(B, _cpu_threads()))
             cpu = {"value": B / secs, "unit": "matrices/s", "cores": min(B, _cpu_threads()), "kind": "reference",
                    "sample": f"reference potrf+potrf_backward over batch {B} x {n}^2, for_each_slice"}
+        sweep = []
+        for Bs in (32, 128):  # the per-panel chain is batch-independent: larger batches amortise it
+            mss = bench.run_potrf_batch(torch, n, Bs, 5, 2, world)
+            tfs = world * Bs * 5 * n ** 3 / 3 / (mss / 1e3) / 1e12
+            sweep.append({"batch": Bs, "ms": mss, "matrices_per_s": world * Bs / (mss / 1e3), "tflops": tfs,
+                          "frac_of_fp64_peak": tfs / fp64_peak / world})
         return _line(args, world, "potrf fwd+bwd matrices/s (n=1024)", world * B / (ms / 1e3), "matrices/s", ms,
-                     "north star: potrf fwd+bwd, batch 8 x 1024^2 fp64", step_tflops=tf,
+                     "north star: potrf fwd+bwd, batch 8 x 1024^2 fp64", step_tflops=tf, batch_sweep=sweep,
                      roofline={"bound": "tensor", "achieved": tf, "peak": fp64_peak, "unit": "TFLOP/s",
                                "frac": tf / fp64_peak, "traffic": None}, cpu_baseline=cpu)
     if cfg == "c3":
