@@ -537,6 +537,46 @@ __global__ void __launch_bounds__(256, 1) k_potrf_panel(int nb, int64_t rest, in
   }
 }
 
+// Throughput variant of the panel step for large batches (batch x chunks
+// above the SM count, where the panel kernel's redundant per-CTA A11
+// factorization would cost real throughput): ONE CTA per slice factors A11,
+// writes L11 and L11^{-1} (into linv), and the panel solve becomes the
+// batched DMMA GEMM A21 <- A21 L11^{-T} (in place: N = nb fits one tile).
+template <typename T>
+__global__ void __launch_bounds__(256) k_potrf_diag_inv(int nb, int64_t k0, MatB<T> akk, T* linv, int32_t* info) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* S = reinterpret_cast<T*>(smem_raw);
+  T* X = S + 64 * CH_LD;  // vector-major: X[v * CH_LD + i] = L11^{-1}(i, v)
+  T* rd = X + 64 * CH_LD;
+  __shared__ int flag;
+  const int64_t b = blockIdx.x;
+  if (slice_failed(info, b)) return;
+  T* base = akk.at(b, 0, 0);
+  for (int e = threadIdx.x; e < 64 * 64; e += 256) {
+    const int i = e / 64, j = e % 64;
+    S[i * CH_LD + j] = (i < nb && j <= i) ? base[i * akk.ld + j] : T(0);
+    X[i * CH_LD + j] = (i == j) ? T(1) : T(0);
+  }
+  __syncthreads();
+  const int failed = chol_smem64<T>(S, nb, &flag);
+  if (failed >= 0) {
+    if (threadIdx.x == 0) record_failure(info, b, DLA_ERR_NOT_SPD, k0 + failed);
+    return;
+  }
+  for (int e = threadIdx.x; e < nb * nb; e += 256) {
+    const int i = e / nb, j = e % nb;
+    base[i * akk.ld + j] = j <= i ? S[i * CH_LD + j] : T(0);
+  }
+  for (int i = threadIdx.x; i < 64; i += 256) rd[i] = i < nb ? T(1) / S[i * CH_LD + i] : T(1);
+  __syncthreads();
+  blocked_fwd_subst<T>(S, X, rd, nb, nb);  // X rows v: L11 x = e_v
+  T* out = linv + b * 64 * 64;
+  for (int e = threadIdx.x; e < 64 * 64; e += 256) {
+    const int i = e / 64, j = e % 64;
+    out[e] = (i < nb && j < nb && j <= i) ? X[j * CH_LD + i] : T(0);  // L11^{-1}(i, j), lower
+  }
+}
+
 // Side stream + event pool for the look-ahead (created once per process;
 // growth happens outside any hot loop).
 struct LookAhead {
@@ -594,6 +634,7 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
   LookAhead& la = LookAhead::get(steps);
   Scratch arrive(sizeof(int) * (size_t)batch, c.stream);
   if (!arrive.p) return DLA_ERR_CUDA;
+  Scratch linv(NBP == 64 && batch * ((n + 63) / 64) > c.sms ? sizeof(T) * (size_t)batch * 64 * 64 : 0, c.stream);
   if (cudaMemsetAsync(arrive.p, 0, sizeof(int) * (size_t)batch, c.stream) != cudaSuccess) return DLA_ERR_CUDA;
   static const bool prio = [] {
     const char* e = getenv("DLA_POTRF_PRIO");  // tuning switch: 0 keeps the chain on the caller's stream
@@ -651,10 +692,26 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
                        MASK_LOWER, c.info));
     }
     const int64_t chunks = rest > 0 ? (rest + 63) / 64 : 1;
-    k_potrf_panel<T, NBP><<<(unsigned)(batch * chunks), 256, sm, cc.stream>>>((int)kb, rest, kbase + k0, a.sub(k0, k0),
-                                                                              a.sub(k0 + kb, k0), c.info,
-                                                                              arrive.as<int>());
-    DLAB_LAUNCH_CHECK();
+    if (NBP == 64 && chunks > 1 && batch * chunks > c.sms) {  // redundancy (chunks > 1) would cost throughput
+      // throughput path: one diagonal factorization per slice + a batched GEMM solve
+      const size_t smd = sizeof(T) * (2 * 64 * CH_LD + 64);
+      static bool once_d = false;
+      if (!once_d) {
+        set_smem(k_potrf_diag_inv<T>, smd);
+        once_d = true;
+      }
+      k_potrf_diag_inv<T><<<(unsigned)batch, 256, smd, cc.stream>>>((int)kb, kbase + k0, a.sub(k0, k0), linv.as<T>(),
+                                                                     c.info);
+      DLAB_LAUNCH_CHECK();
+      MatB<T> a21 = a.sub(k0 + kb, k0);
+      DLAB_TRY(gemm<T>(cc, batch, rest, kb, kb, T(1), C_(a21), false, MatB<const T>{linv.as<T>(), 64, 64 * 64}, true,
+                       T(0), a21, MASK_FULL, c.info, TRI_NONE, TRI_UPPER));
+    } else {
+      k_potrf_panel<T, NBP><<<(unsigned)(batch * chunks), 256, sm, cc.stream>>>((int)kb, rest, kbase + k0,
+                                                                                a.sub(k0, k0), a.sub(k0 + kb, k0),
+                                                                                c.info, arrive.as<int>());
+      DLAB_LAUNCH_CHECK();
+    }
     if (rest == 0) break;
     if (p % G == G - 1 || p == steps - 1) {  // last panel of group g: side update U(g)
       const int64_t c0 = (g + 2) * G * NBP;
