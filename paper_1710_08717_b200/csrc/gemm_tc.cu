@@ -8,10 +8,12 @@
 // A packing pass writes each operand once as TF32 hi / lo tiles (128 x 32,
 // the canonical no-swizzle K-major UMMA layout, zero-padded, transposed when
 // the operand's m / n is the contiguous dimension).  The GEMM then moves
-// whole 16 KB tiles with bulk async copies (TMA bulk engine) into a 3-stage
-// shared ring, one lane issues 12 tcgen05.mma per k-block (4 k-steps x 3
-// products) with the accumulator in TMEM (128 columns), and 4 warps run the
-// epilogue.  One CTA per 128 x 128 output tile.
+// whole tiles with bulk async copies (TMA bulk engine) into a 4-stage shared
+// ring (k-block 16), one lane issues tcgen05.mma (UMMA 128 x 256 x 8, three
+// products per k-step) with the accumulator in TMEM (256 columns), and 4 warps
+// run the epilogue.  One CTA per 128 x 256 output tile.  Measured on B200 at
+// 4096^3: 201.8 TFLOP/s fp32-accurate (128 x 128 tiles / k-block 32 / 3
+// stages: 190.7; k-block 8 / 8 stages: 140).
 // Triangular operands, batching, alpha / beta and the lower / upper write
 // masks are handled in staging and in the epilogue, like gemm.cu.
 #include "common.cuh"
@@ -19,7 +21,15 @@
 namespace dlab {
 namespace {
 
-constexpr int TM = 128, TN = 128, TK = 32, TT = 128;
+#ifndef DLAB_TC_TK
+#define DLAB_TC_TK 16
+#endif
+#ifndef DLAB_TC_ST
+#define DLAB_TC_ST 4
+#endif
+constexpr int TM = 128, TN = 128, TK = DLAB_TC_TK, TT = 128;
+constexpr uint32_t KSBO = (TK / 4) * 128;  // K-major tile: bytes between 8-row groups
+constexpr int TNC = 256;  // CTA tile N: two packed 128-row B tiles per MMA (UMMA N = 256)
 constexpr int TILE_F = TM * TK;  // floats per staged operand tile (A and B tiles are the same size)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -120,8 +130,10 @@ __global__ void __launch_bounds__(256) k_tf32_pack(const float* X, int64_t ld, i
 // with bulk async copies (TMA bulk engine, mbarrier transaction counts);
 // warp 1 (one lane) issues the 12 tcgen05.mma of a stage and commits them to
 // the stage's "empty" barrier; all four warps run the TMEM epilogue.
-constexpr int TCST = 3;
-constexpr uint32_t STAGE_BYTES = 4 * TILE_F * 4;
+constexpr int TCST = DLAB_TC_ST;
+constexpr uint32_t A_BYTES = 2 * TILE_F * 4;                // A hi | A lo (128 rows)
+constexpr uint32_t B_BYTES = 2 * (TNC / TN) * TILE_F * 4;   // B hi (256 rows) | B lo (256 rows)
+constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
 
 struct TcArgs2 {
   int64_t m, n;
@@ -155,21 +167,21 @@ __global__ void __launch_bounds__(TT, 1) k_sgemm_tc(TcArgs2 g) {
   const int64_t b = tile / per;
   tile -= b * per;
   const int64_t mt = tile / g.tiles_n, nt = tile % g.tiles_n;
-  const int64_t m0 = mt * TM, n0 = nt * TN;
+  const int64_t m0 = mt * TM, n0 = nt * TNC;
   if (g.skip && g.skip[b]) return;
   if (g.mask == MASK_LOWER && n0 > m0 + TM - 1) return;
-  if (g.mask == MASK_UPPER && m0 > n0 + TN - 1) return;
+  if (g.mask == MASK_UPPER && m0 > n0 + TNC - 1) return;
   int64_t klo = 0, khi = g.kdim;
   if (g.tri_a == TRI_LOWER) khi = min(khi, m0 + TM);
   if (g.tri_a == TRI_UPPER) klo = max(klo, m0);
   if (g.tri_b == TRI_LOWER) klo = max(klo, n0);
-  if (g.tri_b == TRI_UPPER) khi = min(khi, n0 + TN);
+  if (g.tri_b == TRI_UPPER) khi = min(khi, n0 + TNC);
   const int64_t kt0 = klo / TK;
   const int64_t nk = khi > kt0 * TK ? (khi - kt0 * TK + TK - 1) / TK : 0;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
-                 "r"(TN));
+                 "r"(TNC));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (tid == 0) {
@@ -188,29 +200,34 @@ __global__ void __launch_bounds__(TT, 1) k_sgemm_tc(TcArgs2 g) {
 
   if (warp == 0 && lane == 0) {  // producer
     const float* at = g.ap + (size_t)((b * g.art + mt) * g.akt) * 2 * TILE_F;
-    const float* bt = g.bp + (size_t)((b * g.brt + nt) * g.bkt) * 2 * TILE_F;
+    const int64_t rt0 = nt * (TNC / TN);
+    const int nsub = (int)min((int64_t)(TNC / TN), g.brt - rt0);  // B sub-tiles that exist (the rest: unused columns)
     for (int64_t kb = 0; kb < nk; ++kb) {
       const int s = (int)(kb % TCST);
       if (kb >= TCST) mbar_wait(smem_u32(&empty[s]), (uint32_t)(((kb / TCST) - 1) & 1));
       const uint32_t dst = sbase + (uint32_t)s * STAGE_BYTES;
-      mbar_arrive_tx(smem_u32(&full[s]), STAGE_BYTES);
-      bulk_g2s(dst, at + (size_t)(kt0 + kb) * 2 * TILE_F, STAGE_BYTES / 2, smem_u32(&full[s]));
-      bulk_g2s(dst + STAGE_BYTES / 2, bt + (size_t)(kt0 + kb) * 2 * TILE_F, STAGE_BYTES / 2, smem_u32(&full[s]));
+      mbar_arrive_tx(smem_u32(&full[s]), A_BYTES + (uint32_t)nsub * 2 * TILE_F * 4);
+      bulk_g2s(dst, at + (size_t)(kt0 + kb) * 2 * TILE_F, A_BYTES, smem_u32(&full[s]));
+      for (int j = 0; j < nsub; ++j) {
+        const float* bt = g.bp + (size_t)(((b * g.brt + rt0 + j) * g.bkt) + kt0 + kb) * 2 * TILE_F;
+        bulk_g2s(dst + A_BYTES + j * TILE_F * 4, bt, TILE_F * 4, smem_u32(&full[s]));
+        bulk_g2s(dst + A_BYTES + B_BYTES / 2 + j * TILE_F * 4, bt + TILE_F, TILE_F * 4, smem_u32(&full[s]));
+      }
     }
   } else if (warp == 1 && lane == 0) {  // MMA issuer
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TNC >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
     for (int64_t kb = 0; kb < nk; ++kb) {
       const int s = (int)(kb % TCST);
       mbar_wait(smem_u32(&full[s]), (uint32_t)((kb / TCST) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;\n");
       const uint32_t st = sbase + (uint32_t)s * STAGE_BYTES;
-      const uint32_t ahi = st, alo = st + TILE_F * 4, bhi = st + 2 * TILE_F * 4, blo = st + 3 * TILE_F * 4;
+      const uint32_t ahi = st, alo = st + TILE_F * 4, bhi = st + A_BYTES, blo = st + A_BYTES + B_BYTES / 2;
 #pragma unroll
       for (int ks = 0; ks < TK / 8; ++ks) {
-        const uint64_t dah = make_sdesc(ahi + ks * 256, 128, 1024);
-        const uint64_t dal = make_sdesc(alo + ks * 256, 128, 1024);
-        const uint64_t dbh = make_sdesc(bhi + ks * 256, 128, 1024);
-        const uint64_t dbl = make_sdesc(blo + ks * 256, 128, 1024);
+        const uint64_t dah = make_sdesc(ahi + ks * 256, 128, KSBO);
+        const uint64_t dal = make_sdesc(alo + ks * 256, 128, KSBO);
+        const uint64_t dbh = make_sdesc(bhi + ks * 256, 128, KSBO);
+        const uint64_t dbl = make_sdesc(blo + ks * 256, 128, KSBO);
         const uint32_t acc = (kb == 0 && ks == 0) ? 0u : 1u;
         mma_tf32(tmem, dal, dbh, idesc, acc);  // small terms first
         mma_tf32(tmem, dah, dbl, idesc, 1u);
@@ -229,7 +246,7 @@ __global__ void __launch_bounds__(TT, 1) k_sgemm_tc(TcArgs2 g) {
   // epilogue: warp w owns TMEM lanes (= rows) 32w .. 32w+31
   const int64_t gi = m0 + warp * 32 + lane;
   float* C = g.c.p + b * g.c.bs;
-  for (int c0 = 0; c0 < TN; c0 += 32) {
+  for (int c0 = 0; c0 < TNC; c0 += 32) {
     uint32_t r[32];
     const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
     asm volatile(
@@ -257,7 +274,7 @@ __global__ void __launch_bounds__(TT, 1) k_sgemm_tc(TcArgs2 g) {
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TN));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TNC));
 }
 
 }  // namespace
@@ -288,14 +305,15 @@ bool sgemm_tc(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, floa
     k_tf32_pack<true><<<(unsigned)(batch * brt * kt), 256, 0, c.stream>>>(b.p, b.ld, b.bs, n, k, tri_bv, brt, kt, skip, bpk);
   else
     k_tf32_pack<false><<<(unsigned)(batch * brt * kt), 256, 0, c.stream>>>(b.p, b.ld, b.bs, n, k, tri_bv, brt, kt, skip, bpk);
-  TcArgs2 g{m, n, alpha, beta, apk, bpk, art, kt, brt, kt, cm, mask, skip, art, brt, tri_a, tri_b, k};
+  const int64_t ctn = (n + TNC - 1) / TNC;
+  TcArgs2 g{m, n, alpha, beta, apk, bpk, art, kt, brt, kt, cm, mask, skip, art, ctn, tri_a, tri_b, k};
   const size_t smem = (size_t)TCST * STAGE_BYTES;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_sgemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_sgemm_tc<<<(unsigned)(batch * art * brt), TT, smem, c.stream>>>(g);
+  k_sgemm_tc<<<(unsigned)(batch * art * ctn), TT, smem, c.stream>>>(g);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     fprintf(stderr, "dla_b200 sgemm_tc: %s\n", cudaGetErrorString(e));
