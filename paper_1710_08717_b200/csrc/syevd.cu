@@ -292,32 +292,40 @@ struct BlkTab {  // (a, b), a <= b, packed a << 8 | b
 };
 __device__ const BlkTab kBlkTab = BlkTab();
 
+// Packed upper triangle of the symmetric A: (i, j), i <= j, at i (129 - i) / 2 + j - i
+// (row i starts after rows 0 .. i-1 of lengths 64, 63, ...): 2080 doubles.
+// With the transposed eigenvector accumulator (64 x 65) the CTA needs 50 KB,
+// so four matrices share an SM (full storage: three).
+constexpr int PK = EN * (EN + 1) / 2;
+__device__ __forceinline__ int pidx(int i, int j) {
+  const int lo = i < j ? i : j, hi = i < j ? j : i;
+  return (lo * (2 * EN + 1 - lo)) / 2 + hi - lo;
+}
+
 template <typename T>
-__global__ void __launch_bounds__(ET) k_syevd_small(int n, T* uall, T* lamall, int32_t* info) {
+__global__ void __launch_bounds__(ET, 4) k_syevd_small(int n, T* uall, T* lamall, int32_t* info) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* A = reinterpret_cast<T*>(smem_raw);  // EN x (EN+1)
-  T* Vt = A + EN * (EN + 1);
+  T* A = reinterpret_cast<T*>(smem_raw);  // packed upper triangle, PK
+  T* Vt = A + PK + (PK & 1);              // EN x (EN+1)
   __shared__ T red[ET / 32];
   __shared__ T cs[2 * SP];
   __shared__ int pq[2 * SP];
   __shared__ unsigned short blk[NUB];
   __shared__ int order[EN];
-  __shared__ int done;
   constexpr int ld = EN + 1;
   const int64_t b = blockIdx.x;
   T* u = uall + b * (int64_t)n * n;
   T* lam = lamall + b * (int64_t)n;
   const int tid = threadIdx.x;
   const int N = n + (n & 1), half = N / 2;
-  for (int e = tid; e < n * n; e += ET) A[(e / n) * ld + e % n] = u[e];
   for (int e = tid; e < NUB; e += ET) blk[e] = kBlkTab.v[e];
-  __syncthreads();
+  // symmetry precheck straight from global memory (both triangles)
   T mabs = T(0), masym = T(0);
   for (int e = tid; e < n * n; e += ET) {
     const int i = e / n, j = e % n;
-    const T v = A[i * ld + j];
+    const T v = u[e];
     if (fabs(v) > mabs) mabs = fabs(v);
-    if (j > i) masym = fmax(masym, fabs(v - A[j * ld + i]));
+    if (j > i) masym = fmax(masym, fabs(v - u[j * n + i]));
   }
   mabs = bmax(mabs, red);
   masym = bmax(masym, red);
@@ -334,26 +342,29 @@ __global__ void __launch_bounds__(ET) k_syevd_small(int n, T* uall, T* lamall, i
   }
   int ex = 0;
   if (mabs > T(0)) frexp(mabs, &ex);
+  // exact power-of-two pre-scaling; the symmetric matrix from the lower triangle
+  for (int e = tid; e < PK; e += ET) A[e] = T(0);
   for (int e = tid; e < EN * EN; e += ET) {
     const int i = e / EN, j = e % EN;
-    if (i < n && j < n) {
-      if (j <= i) {
-        const T v = ldexp(A[i * ld + j], -ex);
-        A[i * ld + j] = v;
-        A[j * ld + i] = v;
-      }
-    } else if (i < N && j < N) {
-      A[i * ld + j] = T(0);  // padding row / column of an odd n
-    }
     Vt[i * ld + j] = (i == j) ? T(1) : T(0);
+  }
+  __syncthreads();
+  for (int e = tid; e < n * n; e += ET) {
+    const int i = e / n, j = e % n;
+    if (j <= i) A[pidx(j, i)] = ldexp(u[e], -ex);
   }
   __syncthreads();
   int sweep = 0;
   for (; sweep < MAX_SWEEPS; ++sweep) {
     T off = T(0), dia = T(0);
-    for (int e = tid; e < n * n; e += ET) {
-      const int i = e / n, j = e % n;
-      const T v = fabs(A[i * ld + j]);
+    for (int e = tid; e < PK; e += ET) {
+      // row i of the packed triangle: e in [i (129 - i) / 2, ...)
+      int i = (int)((2 * EN + 1 - sqrtf((float)((2 * EN + 1) * (2 * EN + 1) - 8 * e))) * 0.5f);
+      while (i > 0 && (i * (2 * EN + 1 - i)) / 2 > e) --i;
+      while ((i + 1) * (2 * EN + 1 - (i + 1)) / 2 <= e) ++i;
+      const int j = i + e - (i * (2 * EN + 1 - i)) / 2;
+      if (i >= n || j >= n) continue;
+      const T v = fabs(A[e]);
       if (i != j) off = fmax(off, v);
       else dia = fmax(dia, v);
     }
@@ -364,25 +375,26 @@ __global__ void __launch_bounds__(ET) k_syevd_small(int n, T* uall, T* lamall, i
       if (tid < half) {
         int p, q;
         rr_pair(N, r, tid, p, q);
-        T c = T(1), s = T(0);
+        T c = T(1), sn = T(0);
         if (q < n) {
-          const T apq = A[p * ld + q];
+          const T apq = A[pidx(p, q)];
           if (apq != T(0)) {
-            const T theta = (A[q * ld + q] - A[p * ld + p]) / (T(2) * apq);
+            const T theta = (A[pidx(q, q)] - A[pidx(p, p)]) / (T(2) * apq);
             T t;
             if (fabs(theta) > (sizeof(T) == 8 ? T(1e150) : T(1e15))) t = T(0.5) / theta;
             else t = (theta >= T(0) ? T(1) : T(-1)) / (fabs(theta) + sqrt(theta * theta + T(1)));
             c = T(1) / sqrt(t * t + T(1));
-            s = t * c;
+            sn = t * c;
           }
         }
         cs[2 * tid] = c;
-        cs[2 * tid + 1] = s;
+        cs[2 * tid + 1] = sn;
         pq[2 * tid] = p;
         pq[2 * tid + 1] = q;
       }
       __syncthreads();
-      // A <- J^T A J on the upper 2x2 blocks, mirrored
+      // A <- J^T A J on the 2x2 blocks {p_a, q_a} x {p_b, q_b}, a <= b (each
+      // packed element is owned by exactly one block)
       for (int e = tid; e < NUB; e += ET) {
         const int ba = blk[e] >> 8, bb = blk[e] & 255;
         if (bb >= half) continue;
@@ -390,37 +402,31 @@ __global__ void __launch_bounds__(ET) k_syevd_small(int n, T* uall, T* lamall, i
         const T ca = cs[2 * ba], sa = cs[2 * ba + 1], cb = cs[2 * bb], sb = cs[2 * bb + 1];
         if (ba == bb) {
           if (sa == T(0)) continue;
-          const T x = A[pa * ld + pa], y = A[pa * ld + qa], w = A[qa * ld + qa];
-          // rows, then columns (the order of the former row / column passes)
+          const int ipp = pidx(pa, pa), ipq = pidx(pa, qa), iqq = pidx(qa, qa);
+          const T x = A[ipp], y = A[ipq], w = A[iqq];
           const T x1 = ca * x - sa * y, y1 = ca * y - sa * w;
           const T z1 = sa * x + ca * y, w1 = sa * y + ca * w;
-          A[pa * ld + pa] = ca * x1 - sa * y1;
-          A[qa * ld + qa] = sa * z1 + ca * w1;
-          A[pa * ld + qa] = T(0);  // the annihilated pair is exactly zero
-          A[qa * ld + pa] = T(0);
+          A[ipp] = ca * x1 - sa * y1;
+          A[iqq] = sa * z1 + ca * w1;
+          A[ipq] = T(0);  // the annihilated pair is exactly zero
           continue;
         }
         if (sa == T(0) && sb == T(0)) continue;
-        const T x = A[pa * ld + pb], y = A[pa * ld + qb], z = A[qa * ld + pb], w = A[qa * ld + qb];
+        const int i0 = pidx(pa, pb), i1 = pidx(pa, qb), i2 = pidx(qa, pb), i3 = pidx(qa, qb);
+        const T x = A[i0], y = A[i1], z = A[i2], w = A[i3];
         const T x1 = ca * x - sa * z, y1 = ca * y - sa * w;
         const T z1 = sa * x + ca * z, w1 = sa * y + ca * w;
-        const T x2 = cb * x1 - sb * y1, y2 = sb * x1 + cb * y1;
-        const T z2 = cb * z1 - sb * w1, w2 = sb * z1 + cb * w1;
-        A[pa * ld + pb] = x2;
-        A[pa * ld + qb] = y2;
-        A[qa * ld + pb] = z2;
-        A[qa * ld + qb] = w2;
-        A[pb * ld + pa] = x2;
-        A[qb * ld + pa] = y2;
-        A[pb * ld + qa] = z2;
-        A[qb * ld + qa] = w2;
+        A[i0] = cb * x1 - sb * y1;
+        A[i1] = sb * x1 + cb * y1;
+        A[i2] = cb * z1 - sb * w1;
+        A[i3] = sb * z1 + cb * w1;
       }
       // Vt <- J^T Vt (rows p, q of Vt = columns of V): thread -> one pair,
       // every 8th element of its two rows
       {
         const int k = tid >> 3, i0 = tid & 7;
-        const T s = k < half ? cs[2 * k + 1] : T(0);
-        if (s != T(0)) {
+        const T sn = k < half ? cs[2 * k + 1] : T(0);
+        if (sn != T(0)) {
           const int p = pq[2 * k], q = pq[2 * k + 1];
           const T c = cs[2 * k];
           T* vp = Vt + p * ld;
@@ -429,8 +435,8 @@ __global__ void __launch_bounds__(ET) k_syevd_small(int n, T* uall, T* lamall, i
           for (int v = 0; v < EN / 8; ++v) {
             const int i = i0 + 8 * v;
             const T a0 = vp[i], a1 = vq[i];
-            vp[i] = c * a0 - s * a1;
-            vq[i] = s * a0 + c * a1;
+            vp[i] = c * a0 - sn * a1;
+            vq[i] = sn * a0 + c * a1;
           }
         }
       }
@@ -441,12 +447,11 @@ __global__ void __launch_bounds__(ET) k_syevd_small(int n, T* uall, T* lamall, i
     if (tid == 0) record_failure(info, b, DLA_ERR_CONVERGENCE, sweep);
     return;
   }
-  (void)done;
   for (int i = tid; i < n; i += ET) {
-    const T di = A[i * ld + i];
+    const T di = A[pidx(i, i)];
     int rank = 0;
     for (int j = 0; j < n; ++j) {
-      const T dj = A[j * ld + j];
+      const T dj = A[pidx(j, j)];
       rank += (dj < di) || (dj == di && j < i);
     }
     order[rank] = i;
@@ -475,7 +480,7 @@ __global__ void __launch_bounds__(ET) k_syevd_small(int n, T* uall, T* lamall, i
     }
     const T sgn = vr[kbest] < T(0) ? T(-1) : T(1);
     for (int k = lane; k < n; k += 32) u[(int64_t)r * n + k] = sgn * vr[k];
-    if (lane == 0) lam[r] = ldexp(A[col * ld + col], ex);
+    if (lane == 0) lam[r] = ldexp(A[pidx(col, col)], ex);
   }
 }
 
@@ -520,7 +525,7 @@ template <typename T>
 dla_status syevd_fwd(const Ctx& c, int64_t batch, int64_t n, T* u, T* lambda, void* ws) {
   const bool sm = n <= EN;
   if (sm) {
-    const size_t smem = sizeof(T) * 2 * EN * (EN + 1);
+    const size_t smem = sizeof(T) * (PK + (PK & 1) + EN * (EN + 1));
     static bool once = false;
     if (!once) {
       cudaFuncSetAttribute(k_syevd_small<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
