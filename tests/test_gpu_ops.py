@@ -233,6 +233,24 @@ def test_trsm_singular_reports_index_and_leaves_slice():
 POTRF_N = [1, 2, 5, 17, 32, 63, 64, 65, 70, 129, 200, 256, 512]  # 256/512: inverse-based DMMA paths
 
 
+def test_potrf_throughput_panel_path():
+    """Large batches of multi-chunk panels take the one-factorization-per-slice
+    path (diagonal block + inverse, then an in-place batched DMMA panel
+    solve); same answer as LAPACK, failures still reported per slice."""
+    r = O.rng(79)
+    for n, B in ((256, 64), (1024, 12)):
+        a = O.random_spd(n, r, batch=B)
+        got = host(L.potrf(dev(a)))
+        want = np.linalg.cholesky(a)
+        assert np.abs(got - want).max() / np.abs(want).max() < 1e-12
+        assert np.all(np.triu(got, 1) == 0)
+    a = O.random_spd(256, r, batch=64)
+    a[17, 130, 130] = -1e4
+    with pytest.raises(L.NotPositiveDefiniteError) as e:
+        L.potrf(dev(a))
+    assert e.value.batch_index == 17 and e.value.step == 130
+
+
 def test_potrf_bwd_split_is_bitwise_the_op():
     """dla_potrf_bwd_{begin,end}_f64 (L^-1 on a side stream, used by the GP
     driver) must reproduce dla_potrf_bwd_f64 bit for bit."""
