@@ -136,8 +136,15 @@ __device__ __forceinline__ int panel_warp_n(T* S, int n, int p0, int w, int lane
 // the reciprocal square root itself); the CTA's warps then apply the panel to
 // the trailing lower triangle (8 x 8 DMMA tiles for f64).  Two barriers per
 // 16 columns instead of one per column.
-template <typename T, int NMAX>
-__device__ __forceinline__ int chol_smem(T* S, int n, int* flag) {
+struct NoSide {
+  __device__ void operator()(int) const {}
+};
+
+// `side(warp)` runs on warps 1.. while warp 0 factors the first 16-column
+// panel (the only phase in which they would otherwise wait at a barrier);
+// it must not touch S.
+template <typename T, int NMAX, typename F = NoSide>
+__device__ __forceinline__ int chol_smem(T* S, int n, int* flag, F side = F()) {
   constexpr int W = DLAB_CHOL_W(NMAX), LD = NMAX + 1, Q = NMAX / 32;
   static_assert(NMAX % 32 == 0, "32-row slots");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -149,6 +156,8 @@ __device__ __forceinline__ int chol_smem(T* S, int n, int* flag) {
     if (warp == 0) {
       const int failed = panel_warp_n<T, LD, W, Q>(S, n, p0, w, lane, (n - p0 + 31) >> 5);
       if (lane == 0 && failed >= 0) *flag = failed;
+    } else if (p0 == 0) {
+      side(warp);
     }
     __syncthreads();
     if (*flag >= 0) return *flag;

@@ -468,12 +468,13 @@ dla_status potrf_rec(const Ctx& c, int64_t batch, int64_t n, int64_t k0, MatB<T>
 // A21 <- A21 L11^{-T} in shared memory (blocked substitution + DMMA).
 template <typename T, int NBP>
 __global__ void __launch_bounds__(256, 1) k_potrf_panel(int nb, int64_t rest, int64_t k0, MatB<T> akk, MatB<T> a21,
-                                                     int32_t* info, int* arrive) {
+                                                     int32_t* info, int* arrive, MatB<const T> lp, int kp) {
   constexpr int LD = NBP + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* S = reinterpret_cast<T*>(smem_raw);
   T* V = S + NBP * LD;
   T* rd = V + 64 * LD;
+  T* P = rd + NBP;  // kp > 0: the previous panel's columns at this block's diagonal rows (64 x kp)
   __shared__ int flag;
   const int64_t chunks = rest > 0 ? (rest + 63) / 64 : 1;
   const int64_t b = blockIdx.x / chunks, cid = blockIdx.x % chunks;
@@ -509,13 +510,117 @@ __global__ void __launch_bounds__(256, 1) k_potrf_panel(int nb, int64_t rest, in
       V[(e / NBP) * LD + e % NBP] = v[u];
     }
   }
+  if constexpr (NBP == 64) {
+    if (kp > 0) {
+      // Fused look-ahead column update: this block column still lacks the
+      // previous panel's rank-kp update, A11 -= Pd Pd^T (lower) and
+      // A21 -= Pc Pd^T, applied here on FP64 DMMA instead of by a separate
+      // GEMM launch on the critical chain.  Pd is staged in shared memory;
+      // each warp streams its 8 Pc rows' fragments from L2 once per k-step
+      // and reuses them across all 8 column tiles.
+      const T* gp = lp.at(b, 0, 0);
+      {  // all 16 loads of a thread in flight before the stores
+        T v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int e = tid + u * 256, i = e / 64, k = e % 64;
+          v[u] = (i < nb && k < kp) ? gp[i * lp.ld + k] : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int e = tid + u * 256;
+          P[(e / 64) * LD + e % 64] = v[u];
+        }
+      }
+      __syncthreads();
+      const int warp = tid >> 5, lane = tid & 31, fr = lane >> 2, fc = lane & 3;
+      if constexpr (sizeof(T) == 8) {
+        // A11 lower tiles of row tile `warp` first (the factorization needs them)
+        double acc[8][2];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = 0.0;
+        for (int kk = 0; kk < kp; kk += 4) {
+          const double af = P[(8 * warp + fr) * LD + kk + fc];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            if (t > warp) break;
+            const double bf = P[(8 * t + fr) * LD + kk + fc];
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(acc[t][0]), "+d"(acc[t][1])
+                         : "d"(af), "d"(bf));
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (t > warp) break;
+          S[(8 * warp + fr) * LD + 8 * t + 2 * fc] -= acc[t][0];  // entries above the diagonal are scratch
+          S[(8 * warp + fr) * LD + 8 * t + 2 * fc + 1] -= acc[t][1];
+        }
+      } else {
+        for (int e = tid; e < 64 * 64; e += 256) {
+          const int i = e / 64, j = e % 64;
+          if (j > i) continue;
+          T acc = T(0);
+          for (int k = 0; k < kp; ++k) acc += P[i * LD + k] * P[j * LD + k];
+          S[i * LD + j] -= acc;
+        }
+      }
+    }
+  }
   __syncthreads();
+  // A21 -= Pc Pd^T (the chunk rows) runs on warps 1-7 while warp 0 factors
+  // the first 16 columns of A11 (chol_smem's side task)
+  auto v_update = [&](int warp) {
+    if constexpr (NBP == 64 && sizeof(T) == 8) {
+      if (kp == 0) return;
+      const int lane = tid & 31, fr = lane >> 2, fc = lane & 3;
+      const T* gp = lp.at(b, 0, 0);
+      for (int rt = warp - 1; rt < 8; rt += 7) {  // warp 1: row tiles 0, 7; warps 2..7: 1..6
+        double acc[8][2];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = 0.0;
+        const int vr = 8 * rt + fr;
+        const T* arow = gp + (int64_t)(nb + r0 + vr) * lp.ld;
+        const bool okr = vr < nv;
+        double afv[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) afv[q] = (okr && 4 * q < kp) ? arow[4 * q + fc] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const double af = afv[q];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const double bf = P[(8 * t + fr) * LD + 4 * q + fc];
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(acc[t][0]), "+d"(acc[t][1])
+                         : "d"(af), "d"(bf));
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          V[vr * LD + 8 * t + 2 * fc] -= acc[t][0];
+          V[vr * LD + 8 * t + 2 * fc + 1] -= acc[t][1];
+        }
+      }
+    } else {
+      if (kp == 0 || warp != 1) return;
+      const T* gp = lp.at(b, 0, 0);
+      for (int e = tid - 32; e < 64 * 64; e += 32) {
+        const int vv = e / 64, j = e % 64;
+        if (vv >= nv) continue;
+        const T* ga = gp + (int64_t)(nb + r0 + vv) * lp.ld;
+        T acc = T(0);
+        for (int k = 0; k < kp; ++k) acc += ga[k] * P[j * LD + k];
+        V[vv * LD + j] -= acc;
+      }
+    }
+  };
   // Every CTA reads A11 from global memory; the CTA that arrives LAST (all
   // others have their copy in shared memory by then) writes L11 back over it
   // and re-arms the slice's counter for the next panel launch.
   __shared__ int last;
   if (tid == 0) last = atomicAdd(arrive + b, 1) == (int)chunks - 1;
-  const int failed = chol_smem<T, NBP>(S, nb, &flag);  // (its first barrier publishes `last`)
+  const int failed = chol_smem<T, NBP>(S, nb, &flag, v_update);  // (its first barrier publishes `last`)
   if (failed >= 0) {
     if (cid == 0 && tid == 0) record_failure(info, b, DLA_ERR_NOT_SPD, k0 + failed);
     return;
@@ -617,7 +722,7 @@ struct LookAhead {
 // variant's deep chain of tiny GEMMs dominates.
 template <typename T, int NBP>
 dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int64_t kbase) {
-  const size_t sm = sizeof(T) * ((NBP + 64) * (NBP + 1) + NBP);
+  const size_t sm = sizeof(T) * ((NBP + 64) * (NBP + 1) + NBP + (NBP == 64 ? 64 * (NBP + 1) : 0));
   static bool once = false;
   if (!once) {
     set_smem(k_potrf_panel<T, NBP>, sm);
@@ -679,20 +784,32 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
   }();
   const int64_t G = group;
   const int64_t ngroups = (steps + G - 1) / G;
+  // Step p's panel either runs the fused panel kernel (which, for NBP = 64,
+  // also applies panel p-1's update to its own block column) or, for large
+  // batches of multi-chunk panels, the per-slice factorization + batched
+  // GEMM solve (then panel p-1's column update is a separate GEMM).
+  auto chunks_of = [&](int64_t p) {
+    const int64_t r = n - p * NBP - min((int64_t)NBP, n - p * NBP);
+    return r > 0 ? (r + 63) / 64 : (int64_t)1;
+  };
+  auto throughput = [&](int64_t p) { return NBP == 64 && chunks_of(p) > 1 && batch * chunks_of(p) > c.sms; };
+  auto fused = [&](int64_t p) { return NBP == 64 && G == 1 && p >= 1 && !throughput(p); };
   for (int64_t p = 0; p < steps; ++p) {
     const int64_t k0 = p * NBP;
     const int64_t kb = min((int64_t)NBP, n - k0);
     const int64_t rest = n - k0 - kb;
     const int64_t g = p / G;
-    if (p > 0) {  // column p: panels [max(0, (g-1) G), p)
+    if (p > 0 && !fused(p)) {  // column p: panels [max(0, (g-1) G), p)
       if (g >= 2) cudaStreamWaitEvent(cc.stream, la.done[g - 2], 0);
       const int64_t kk0 = std::max<int64_t>(0, (g - 1) * G) * NBP;
       MatB<T> lrows = a.sub(k0, kk0);
       DLAB_TRY(gemm<T>(cc, batch, n - k0, kb, k0 - kk0, T(-1), C_(lrows), false, C_(lrows), true, T(1), a.sub(k0, k0),
                        MASK_LOWER, c.info));
+    } else if (p >= 2) {
+      cudaStreamWaitEvent(cc.stream, la.done[p - 2], 0);  // the last side update that wrote column p
     }
-    const int64_t chunks = rest > 0 ? (rest + 63) / 64 : 1;
-    if (NBP == 64 && chunks > 1 && batch * chunks > c.sms) {  // redundancy (chunks > 1) would cost throughput
+    const int64_t chunks = chunks_of(p);
+    if (throughput(p) && rest > 0) {
       // throughput path: one diagonal factorization per slice + a batched GEMM solve
       const size_t smd = sizeof(T) * (2 * 64 * CH_LD + 64);
       static bool once_d = false;
@@ -707,9 +824,11 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
       DLAB_TRY(gemm<T>(cc, batch, rest, kb, kb, T(1), C_(a21), false, MatB<const T>{linv.as<T>(), 64, 64 * 64}, true,
                        T(0), a21, MASK_FULL, c.info, TRI_NONE, TRI_UPPER));
     } else {
+      const int kp = fused(p) ? (int)NBP : 0;
+      MatB<const T> lp = C_(p >= 1 ? a.sub(k0, k0 - NBP) : a);
       k_potrf_panel<T, NBP><<<(unsigned)(batch * chunks), 256, sm, cc.stream>>>((int)kb, rest, kbase + k0,
                                                                                 a.sub(k0, k0), a.sub(k0 + kb, k0),
-                                                                                c.info, arrive.as<int>());
+                                                                                c.info, arrive.as<int>(), lp, kp);
       DLAB_LAUNCH_CHECK();
     }
     if (rest == 0) break;
