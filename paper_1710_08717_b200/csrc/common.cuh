@@ -49,6 +49,7 @@ struct Ctx {
   int sms;
   int32_t* info;       // nullable: device int32[batch]
   int gemm_ctas = 0;   // > 0: DMMA GEMMs run persistent on at most this many CTAs
+  int gemm_rowtile = 0;  // 1: (f64, m <= 128) one 128-row tile per column block, so C may alias op(B)
 };
 
 Ctx make_ctx(void* stream, int32_t* info);

@@ -465,13 +465,13 @@ void ensure_smem(K k, size_t smem) {
 }
 
 template <typename T, bool TA, bool TB, int VA, int VB>
-cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large, int max_ctas) {
+cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large, int max_ctas, bool rowtile) {
   auto grid = [&](int64_t tiles) {
     g.total = tiles;
     return (unsigned)(max_ctas > 0 && tiles > max_ctas ? max_ctas : tiles);
   };
   if constexpr (sizeof(T) == 8) {
-    if (g.n <= 32 && g.k >= 128 && g.m >= 64) {
+    if (g.n <= 32 && g.k >= 128 && g.m >= 64 && !rowtile) {
       using C = CfgN;
       g.tiles_m = (g.m + C::BM - 1) / C::BM;
       g.tiles_n = (g.n + C::BN - 1) / C::BN;
@@ -484,7 +484,8 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large, 
       }
       const unsigned nb = grid(slabs * g.tiles_m * g.tiles_n);
       k<<<nb, C::NT, smem, s>>>(g);
-    } else if (large && (g.k <= DLAB_SHORTK || g.mask != MASK_FULL || g.tri_a != TRI_NONE || g.tri_b != TRI_NONE)) {
+    } else if (rowtile || (large && (g.k <= DLAB_SHORTK || g.mask != MASK_FULL || g.tri_a != TRI_NONE ||
+                                      g.tri_b != TRI_NONE))) {
       using C = CfgK;
       g.tiles_m = (g.m + C::BM - 1) / C::BM;
       g.tiles_n = (g.n + C::BN - 1) / C::BN;
@@ -542,12 +543,13 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large, 
 }
 
 template <typename T, bool TA, bool TB>
-cudaError_t launch_t(const GemmArgs<T>& g, int64_t slabs, cudaStream_t s, bool va, bool vb, bool large, int mc) {
+cudaError_t launch_t(const GemmArgs<T>& g, int64_t slabs, cudaStream_t s, bool va, bool vb, bool large, int mc,
+                     bool rt) {
   constexpr int V = 16 / (int)sizeof(T);
-  if (va && vb) return launch_tv<T, TA, TB, V, V>(g, slabs, s, large, mc);
-  if (va) return launch_tv<T, TA, TB, V, 1>(g, slabs, s, large, mc);
-  if (vb) return launch_tv<T, TA, TB, 1, V>(g, slabs, s, large, mc);
-  return launch_tv<T, TA, TB, 1, 1>(g, slabs, s, large, mc);
+  if (va && vb) return launch_tv<T, TA, TB, V, V>(g, slabs, s, large, mc, rt);
+  if (va) return launch_tv<T, TA, TB, V, 1>(g, slabs, s, large, mc, rt);
+  if (vb) return launch_tv<T, TA, TB, 1, V>(g, slabs, s, large, mc, rt);
+  return launch_tv<T, TA, TB, 1, 1>(g, slabs, s, large, mc, rt);
 }
 
 // Vector loads need 16-byte aligned rows and a contiguous extent that is a
@@ -579,7 +581,8 @@ dla_status gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T 
     if (mask != MASK_FULL || inner != 1) return DLA_ERR_INVALID;
     return ew_scale<T>(c, batch, m, n, cm, beta, skip);
   }
-  if (inner == 1 && tri_a == TRI_NONE && tri_b == TRI_NONE) {  // vector / outer-product shapes
+  const bool rowtile = sizeof(T) == 8 && c.gemm_rowtile != 0 && m <= 128;
+  if (inner == 1 && tri_a == TRI_NONE && tri_b == TRI_NONE && !rowtile) {  // vector / outer-product shapes
     dla_status st;
     if (gemm_skinny<T>(c, batch, m, n, k, alpha, a, ta, b, tb, beta, cm, mask, skip, &st)) return st;
   }
@@ -608,10 +611,10 @@ dla_status gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T 
   cudaError_t e;
   const bool prof = gemm_prof_on();
   if (prof) gemm_prof_begin(c.stream);
-  if (!ta && !tb) e = launch_t<T, false, false>(g, slabs, c.stream, va, vb, large, c.gemm_ctas);
-  else if (ta && !tb) e = launch_t<T, true, false>(g, slabs, c.stream, va, vb, large, c.gemm_ctas);
-  else if (!ta && tb) e = launch_t<T, false, true>(g, slabs, c.stream, va, vb, large, c.gemm_ctas);
-  else e = launch_t<T, true, true>(g, slabs, c.stream, va, vb, large, c.gemm_ctas);
+  if (!ta && !tb) e = launch_t<T, false, false>(g, slabs, c.stream, va, vb, large, c.gemm_ctas, rowtile);
+  else if (ta && !tb) e = launch_t<T, true, false>(g, slabs, c.stream, va, vb, large, c.gemm_ctas, rowtile);
+  else if (!ta && tb) e = launch_t<T, false, true>(g, slabs, c.stream, va, vb, large, c.gemm_ctas, rowtile);
+  else e = launch_t<T, true, true>(g, slabs, c.stream, va, vb, large, c.gemm_ctas, rowtile);
   if (e != cudaSuccess) {
     fprintf(stderr, "dla_b200 gemm: %s\n", cudaGetErrorString(e));
     return DLA_ERR_CUDA;

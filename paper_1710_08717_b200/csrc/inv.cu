@@ -217,6 +217,15 @@ dla_status potrf_bwd_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, M
 template <typename T>
 dla_status trmm_gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x, bool right,
                      bool trans, bool lower, T alpha) {
+  if (sizeof(T) == 8 && !right && m <= 128) {
+    // X <- op(T) X in place: with one 128-row tile per column block every CTA
+    // reads the whole of its X columns (the K range) before writing them, and
+    // no other CTA reads those columns -- no scratch copy back
+    Ctx cr = c;
+    cr.gemm_rowtile = 1;
+    const int tri = (lower != trans) ? TRI_LOWER : TRI_UPPER;
+    return gemm<T>(cr, batch, m, n, m, alpha, t, trans, C_(x), false, T(0), x, MASK_FULL, c.info, tri, TRI_NONE);
+  }
   Scratch ws(sizeof(T) * (size_t)batch * (size_t)m * n, c.stream);
   if (!ws.p) return DLA_ERR_CUDA;
   MatB<T> y{ws.as<T>(), n, m * n};

@@ -155,7 +155,7 @@ def test_syrk(port, dt):
 
 
 # ------------------------------------------------------------ trmm / trsm
-SHAPES = [(4, 3), (1, 5), (33, 17), (70, 65), (130, 7), (7, 130), (256, 130), (130, 256)]
+SHAPES = [(4, 3), (1, 5), (33, 17), (70, 65), (130, 7), (7, 130), (256, 130), (130, 256), (128, 70), (128, 200)]
 
 
 @pytest.mark.parametrize("dt", DTYPES)
