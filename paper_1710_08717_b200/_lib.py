@@ -83,6 +83,8 @@ class _Lib:
         L.dla_gp_nll_assemble_f64.restype = _int
         L.dla_potrf_bwd_ws_bytes_f64.restype = _sz
         L.dla_potrf_bwd_ws_bytes_f64.argtypes = [_i64, _i64]
+        L.dla_gp_potrf_inv_f64.argtypes = [_i64, _i64, _vp, _vp, _vp, _sz, _vp]
+        L.dla_gp_potrf_inv_f64.restype = _int
         L.dla_potrf_bwd_begin_f64.argtypes = [_i64, _i64, _vp, _int, _vp, _sz, _vp]
         L.dla_potrf_bwd_begin_f64.restype = _int
         L.dla_potrf_bwd_end_f64.argtypes = [_i64, _i64, _vp, _vp, _vp, _int, _vp, _sz, _vp]
@@ -122,7 +124,7 @@ def exported_symbols():
              "dla_launch_count", "dla_prof_enable", "dla_prof_read", "dla_prof_read_max", "dla_gp_rbf_ws_bytes",
              "dla_gp_rbf_fwd_f64", "dla_gp_rbf_bwd_f64", "dla_gp_nll_assemble_f64",
              "dla_ml_shift_copy_f64", "dla_axpy_f64", "dla_ml_reduce_f64", "dla_potrf_bwd_ws_bytes_f64",
-             "dla_potrf_bwd_begin_f64", "dla_potrf_bwd_end_f64"]
+             "dla_potrf_bwd_begin_f64", "dla_potrf_bwd_end_f64", "dla_gp_potrf_inv_f64"]
     for name in _SIGS:
         for s in ("f32", "f64"):
             names.append(f"dla_{name}_{s}")

@@ -498,7 +498,9 @@ struct InvFork {
 
 template <typename T>
 size_t potrf_inv_ws(int64_t batch, int64_t n) {
-  return sizeof(T) * (size_t)batch * 2 * (size_t)n * n + (size_t)batch * trtri_levels_tmp<T>(n);
+  // wi (n^2) | tt (n^2) | tmp (trtri_levels_tmp(n) bytes) | tmp2 (trtri_levels_tmp(n / 2) bytes)
+  return sizeof(T) * (size_t)batch * 2 * (size_t)n * n + (size_t)batch * trtri_levels_tmp<T>(n) +
+         (size_t)batch * trtri_levels_tmp<T>(n / 2);
 }
 
 template <typename T>
@@ -534,6 +536,88 @@ dla_status potrf_bwd_end(int64_t batch, int64_t n, T* abar, const T* lbar, const
   cudaStreamWaitEvent(cx.stream, InvFork::get().done, 0);
   return potrf_bwd_finish<T>(cx, batch, n, pk(abar, n, n), cpk(wp, n, n), tt);
 }
+
+// Factorization + early inverse for drivers (the GP step): the blocked
+// Cholesky signals once block columns [0, n/2) are final; from then on the
+// side stream forms L11^{-1} and T1 = L21 L11^{-1} (half of the inverse's
+// flops) while the factorization's chain-bound second half runs; after it,
+// L22^{-1} and W21 = -L22^{-1} T1 complete L^{-1} into the workspace that
+// dla_potrf_bwd_end_f64 consumes.  Same operations as trtri_levels on the
+// whole matrix (its top level is exactly T1 and W21).
+template <typename T>
+struct EarlyInv {
+  int64_t batch, n;
+  const T* l;
+  T* wp;
+  cudaStream_t side;
+  cudaEvent_t ev;
+  bool fired;
+};
+
+template <typename T>
+void early_inv_first(void* user, cudaStream_t crit) {
+  EarlyInv<T>& e = *static_cast<EarlyInv<T>*>(user);
+  e.fired = true;
+  const int64_t n = e.n, h = n / 2, B = e.batch;
+  cudaEventRecord(e.ev, crit);
+  cudaStreamWaitEvent(e.side, e.ev, 0);
+  Ctx sc = make_ctx(e.side, nullptr);
+  MatB<T> wi{e.wp, n, n * n};
+  T* tmp = e.wp + 2 * B * n * n;
+  MatB<const T> lv{e.l, n, n * n};
+  // W11 = tril(L11), W21 = L21; L11^{-1} in place; T1 = W21 W11^{-1} into tmp
+  if (ew_tri_copy<T>(sc, B, h, lv, wi, false) != DLA_OK) return;
+  if (ew_copy<T>(sc, B, h, h, MatB<const T>{e.l + h * n, n, n * n}, wi.sub(h, 0)) != DLA_OK) return;
+  T* tmp2 = tmp + B * (trtri_levels_tmp<T>(n) / sizeof(T));
+  if (trtri_levels<T>(sc, B, h, wi, tmp2) != DLA_OK) return;
+  MatB<T> t1{tmp, h, h * h};
+  gemm<T>(sc, B, h, h, h, T(1), MatB<const T>{wi.p + h * n, n, n * n}, false, MatB<const T>{wi.p, n, n * n}, false,
+          T(0), t1, MASK_FULL, nullptr, TRI_NONE, TRI_LOWER);
+}
+
+template <typename T>
+dla_status gp_potrf_inv(int64_t batch, int64_t n, T* a, int32_t* info, void* ws, size_t wsb, void* stream) {
+  if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
+  if (!inv_eligible<T>(n) || batch * n == 0) {  // no early path: factorization, then the plain begin
+    DLAB_TRY(potrf_fwd<T>(batch, n, a, 1, info, stream));
+    return potrf_bwd_begin<T>(batch, n, a, 1, ws, wsb, stream);
+  }
+  if (!ws || wsb < potrf_inv_ws<T>(batch, n)) return DLA_ERR_WORKSPACE;
+  Ctx cx = make_ctx(stream, info);
+  DLAB_TRY(reset_info(cx, batch));
+  DLAB_TRY(check_symmetric<T>(cx, batch, n, cpk(a, n, n), info));
+  InvFork& f = InvFork::get();
+  static cudaEvent_t mid = nullptr, fin = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaEventCreateWithFlags(&mid, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&fin, cudaEventDisableTiming);
+  });
+  EarlyInv<T> e{batch, n, a, static_cast<T*>(ws), f.side, mid, false};
+  PotrfHook hook{n / 2, early_inv_first<T>, &e};
+  Ctx hc = cx;
+  hc.potrf_hook = &hook;
+  DLAB_TRY(potrf_lower<T>(hc, batch, n, pk(a, n, n)));
+  if (!e.fired) early_inv_first<T>(&e, cx.stream);  // a schedule without the hook point (tuning modes)
+  const int64_t h = n / 2;
+  T* wp = static_cast<T*>(ws);
+  MatB<T> wi{wp, n, n * n};
+  T* tmp = wp + 2 * batch * n * n;
+  T* tmp2 = tmp + batch * (trtri_levels_tmp<T>(n) / sizeof(T));
+  cudaEventRecord(fin, cx.stream);
+  cudaStreamWaitEvent(f.side, fin, 0);
+  Ctx sc = make_ctx(f.side, nullptr);
+  // W22 = tril(L22); L22^{-1} in place; W21 = -W22^{-1} T1
+  DLAB_TRY(ew_tri_copy<T>(sc, batch, h, MatB<const T>{a + h * n + h, n, n * n}, wi.sub(h, h), false));
+  DLAB_TRY(trtri_levels<T>(sc, batch, h, wi.sub(h, h), tmp2));
+  DLAB_TRY(gemm<T>(sc, batch, h, h, h, T(-1), MatB<const T>{wi.p + h * n + h, n, n * n}, false,
+                   MatB<const T>{tmp, h, h * h}, false, T(0), wi.sub(h, 0), MASK_FULL, nullptr, TRI_LOWER,
+                   TRI_NONE));
+  cudaEventRecord(f.done, f.side);
+  return DLA_OK;
+}
+
+
 
 extern "C" {
 
@@ -717,6 +801,10 @@ DLA_DEFINE(double, f64)
 
 size_t dla_potrf_bwd_ws_bytes_f64(int64_t batch, int64_t n) {
   return inv_eligible<double>(n) ? potrf_inv_ws<double>(batch, n) : 0;
+}
+dla_status dla_gp_potrf_inv_f64(int64_t batch, int64_t n, double* a, int32_t* info, void* ws, size_t ws_bytes,
+                                void* stream) {
+  return gp_potrf_inv<double>(batch, n, a, info, ws, ws_bytes, stream);
 }
 dla_status dla_potrf_bwd_begin_f64(int64_t batch, int64_t n, const double* l, int lower, void* ws, size_t ws_bytes,
                                    void* stream) {

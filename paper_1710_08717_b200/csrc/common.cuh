@@ -43,6 +43,15 @@ inline MatB<T> packed(T* p, int64_t rows, int64_t cols) {
   return MatB<T>{p, cols, rows * cols};
 }
 
+// Optional hook into the blocked Cholesky: fn(user, crit) is called once,
+// right after the panel launch that completes block columns [0, col), with
+// the critical stream (so `user` can order work after that point).
+struct PotrfHook {
+  int64_t col;
+  void (*fn)(void* user, cudaStream_t crit);
+  void* user;
+};
+
 // Launch context: stream + device properties + optional per-slice info.
 struct Ctx {
   cudaStream_t stream;
@@ -50,6 +59,7 @@ struct Ctx {
   int32_t* info;       // nullable: device int32[batch]
   int gemm_ctas = 0;   // > 0: DMMA GEMMs run persistent on at most this many CTAs
   int gemm_rowtile = 0;  // 1: (f64, m <= 128) one 128-row tile per column block, so C may alias op(B)
+  const PotrfHook* potrf_hook = nullptr;
 };
 
 Ctx make_ctx(void* stream, int32_t* info);

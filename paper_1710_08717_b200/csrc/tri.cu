@@ -794,6 +794,7 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
   };
   auto throughput = [&](int64_t p) { return NBP == 64 && chunks_of(p) > 1 && batch * chunks_of(p) > c.sms; };
   auto fused = [&](int64_t p) { return NBP == 64 && G == 1 && p >= 1 && !throughput(p); };
+  bool hook_fired = false;
   for (int64_t p = 0; p < steps; ++p) {
     const int64_t k0 = p * NBP;
     const int64_t kb = min((int64_t)NBP, n - k0);
@@ -830,6 +831,10 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
                                                                                 a.sub(k0, k0), a.sub(k0 + kb, k0),
                                                                                 c.info, arrive.as<int>(), lp, kp);
       DLAB_LAUNCH_CHECK();
+    }
+    if (c.potrf_hook && !hook_fired && kbase == 0 && k0 + kb >= c.potrf_hook->col) {
+      c.potrf_hook->fn(c.potrf_hook->user, cc.stream);  // block columns [0, col) are final from here on
+      hook_fired = true;
     }
     if (rest == 0) break;
     if (p % G == G - 1 || p == steps - 1) {  // last panel of group g: side update U(g)

@@ -30,6 +30,7 @@ from . import linalg as L
 from ._lib import lib
 
 LOG_2PI = 1.8378770664093454835606594728112353
+_EARLY = __import__("os").environ.get("DLA_GP_EARLY", "1") != "0"
 
 
 class GPNLL:
@@ -76,12 +77,18 @@ class GPNLL:
                                           self.ws_bytes, self._stream())
         if st:
             L._raise_status(st, "gp_rbf_fwd")
-        L.potrf_inplace(self.a, True, check=False, info=self.info)
+        # potrf (lower, in place) + the pullback's L^-1, half of it formed
+        # during the factorization's chain-bound second half
         lib_ = lib().lib
-        st = lib_.dla_potrf_bwd_begin_f64(B, n, C.c_void_p(self.a.data_ptr()), 1, C.c_void_p(self.iws.data_ptr()),
-                                          self.iws_bytes, self._stream())
+        if _EARLY:
+            st = lib_.dla_gp_potrf_inv_f64(B, n, C.c_void_p(self.a.data_ptr()), C.c_void_p(self.info.data_ptr()),
+                                           C.c_void_p(self.iws.data_ptr()), self.iws_bytes, self._stream())
+        else:
+            L.potrf_inplace(self.a, True, check=False, info=self.info)
+            st = lib_.dla_potrf_bwd_begin_f64(B, n, C.c_void_p(self.a.data_ptr()), 1,
+                                              C.c_void_p(self.iws.data_ptr()), self.iws_bytes, self._stream())
         if st:
-            L._raise_status(st, "potrf_bwd_begin")
+            L._raise_status(st, "gp_potrf_inv")
         self.z.copy_(y)
         L.trsm_inplace(self.a, self.z, False, False, True, 1.0, check=False)
         L.gemm2_into(self.quad, self.z, self.z, True, False, 0.5)

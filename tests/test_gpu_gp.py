@@ -65,3 +65,21 @@ def test_gp_matches_live_reference_n512():
     assert abs(nll.item() - out[0]) / abs(out[0]) < 1e-10
     assert rel(grads.cpu().numpy(), out[1:]) < 1e-8
     assert rel(xbar.cpu().numpy(), xb) < 1e-8
+
+
+@pytest.mark.parametrize("n,batch", [(1024, 1), (1536, 2), (4096, 1)])
+def test_gp_early_inverse_matches_split(monkeypatch, n, batch):
+    # dla_gp_potrf_inv_f64 (L11^-1 and L21 L11^-1 formed while the blocked
+    # factorization's second half runs) vs potrf + dla_potrf_bwd_begin_f64
+    r = O.rng(n)
+    x = torch.from_numpy(r.standard_normal((batch, n, 8))).cuda()
+    y = torch.from_numpy(r.standard_normal((batch, n, 1))).cuda()
+    outs = []
+    for early in (False, True):
+        monkeypatch.setattr(gp, "_EARLY", early)
+        g = gp.GPNLL(n, 8, batch, "cuda")
+        outs.append([t.clone() for t in g.step(x, y, 1.0, 1.0, 0.1)])
+        g.check()
+    # same kernels on the same blocks in a different order: bitwise equal
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
