@@ -136,6 +136,19 @@ __device__ __forceinline__ int panel_warp_n(T* S, int n, int p0, int w, int lane
 // the reciprocal square root itself); the CTA's warps then apply the panel to
 // the trailing lower triangle (8 x 8 DMMA tiles for f64).  Two barriers per
 // 16 columns instead of one per column.
+#ifdef DLAB_PANEL_PROF
+__device__ unsigned long long g_cprof[16];
+#define CSTAMP(i)                                                                     \
+  do {                                                                                \
+    if (gridDim.x >= 16 && blockIdx.x == 0 && threadIdx.x == 0) {                     \
+      unsigned long long t_;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
+      g_cprof[i] = t_;                                                                \
+    }                                                                                 \
+  } while (0)
+#else
+#define CSTAMP(i)
+#endif
 struct NoSide {
   __device__ void operator()(int) const {}
 };
@@ -151,15 +164,18 @@ __device__ __forceinline__ int chol_smem(T* S, int n, int* flag, F side = F()) {
   const int nthreads = blockDim.x;
   if (threadIdx.x == 0) *flag = -1;
   __syncthreads();
+  CSTAMP(0);
   for (int p0 = 0; p0 < n; p0 += W) {
     const int w = min(W, n - p0);  // panel width
     if (warp == 0) {
       const int failed = panel_warp_n<T, LD, W, Q>(S, n, p0, w, lane, (n - p0 + 31) >> 5);
       if (lane == 0 && failed >= 0) *flag = failed;
+      if (p0 == 0) CSTAMP(9);
     } else if (p0 == 0) {
       side(warp);
     }
     __syncthreads();
+    CSTAMP(1 + 2 * (p0 / W));
     if (*flag >= 0) return *flag;
     // trailing update: A(i, k) -= sum_c L(i, p0+c) L(k, p0+c) for p0+w <= k <= i < n
     const int t0 = p0 + w;
@@ -204,6 +220,113 @@ __device__ __forceinline__ int chol_smem(T* S, int n, int* flag, F side = F()) {
       }
     }
     __syncthreads();
+    CSTAMP(2 + 2 * (p0 / W));
+  }
+  return -1;
+}
+
+// Blocked-potrf panel step, fp64: factor A11 (S, nb x nb, nb <= 64) AND
+// solve the CTA's chunk rows V <- V L11^{-T} (nv <= 64 rows, stride LD) in
+// one interleaved pass.  While warp 0 factors 16-column panel j of A11 (the
+// pivot chain), warps {1,2,3,5,6,7} (not warp 4: it shares warp 0's issue
+// slots) solve V's columns of panel j-1 against its 16 x 16 diagonal block
+// and apply them to V's later columns (DMMA) -- so the chunk solve rides
+// under the factorization instead of following it.  `pre(warp)` (the fused
+// look-ahead update of V) runs in that slot for j = 0.  Returns the failing
+// pivot (uniform) or -1; on success V holds L21's rows.
+template <int LD, typename F>
+__device__ __forceinline__ int chol_tall64(double* S, double* V, int nb, int nv, int* flag, F pre) {
+  constexpr int W = 16, Q = 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, fr = lane >> 2, fc = lane & 3;
+  if (threadIdx.x == 0) *flag = -1;
+  __syncthreads();
+  CSTAMP(0);
+  const int np = (nb + W - 1) / W;
+  // V work group: 6 warps, a named barrier of 192 threads
+  const int vw = warp < 4 ? warp - 1 : warp - 2;  // 0..5 for warps 1-3, 5-7
+  for (int j = 0; j <= np; ++j) {
+    const int p0 = j * W;
+    if (warp == 0) {
+      if (j < np) {
+        const int failed = panel_warp_n<double, LD, W, Q>(S, nb, p0, min(W, nb - p0), lane, (nb - p0 + 31) >> 5);
+        if (lane == 0 && failed >= 0) *flag = failed;
+      }
+    } else if (j == 0) {
+      pre(warp);
+    } else if (warp != 4 && nv > 0) {
+      const int c0 = p0 - W, w = min(W, nb - c0);
+      // (1) rows of V: x L(c0.., c0..)^T = v on the 16 x 16 diagonal block
+      const int v = threadIdx.x - 32;  // warps 1, 2
+      if (v < nv && v >= 0) {
+        double x[W], rdl[W];
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+          x[i] = i < w ? V[v * LD + c0 + i] : 0.0;
+          rdl[i] = i < w ? 1.0 / S[(c0 + i) * LD + c0 + i] : 0.0;
+        }
+#pragma unroll
+        for (int p = 0; p < W; ++p) {
+          x[p] *= rdl[p];
+#pragma unroll
+          for (int i = p + 1; i < W; ++i)
+            if (i < w) x[i] -= S[(c0 + i) * LD + c0 + p] * x[p];
+        }
+#pragma unroll
+        for (int i = 0; i < W; ++i)
+          if (i < w) V[v * LD + c0 + i] = x[i];
+      }
+      asm volatile("bar.sync 1, 192;" ::: "memory");
+      // (2) V(:, c0+W .. nb) -= X L(c0+W .. nb, c0 .. c0+W)^T  (8 x 8 DMMA tiles)
+      const int t0 = c0 + W;
+      if (t0 < nb) {
+        const int rts = (nv + 7) / 8, cts = (nb - t0 + 7) / 8;
+        for (int tile = vw; tile < rts * cts; tile += 6) {
+          const int rt = tile / cts, ct = t0 / 8 + tile % cts;
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {  // k-column 4 fc + s: conflict-free with stride 65
+            const bool ok = 4 * fc + s < w;
+            const double af = ok ? V[(8 * rt + fr) * LD + c0 + 4 * fc + s] : 0.0;
+            const double bf = ok ? S[(8 * ct + fr) * LD + c0 + 4 * fc + s] : 0.0;
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(a0), "+d"(a1)
+                         : "d"(af), "d"(bf));
+          }
+          double* crow = V + (8 * rt + fr) * LD + 8 * ct + 2 * fc;
+          crow[0] -= a0;
+          crow[1] -= a1;
+        }
+      }
+    }
+    __syncthreads();
+    CSTAMP(1 + 2 * j);
+    if (*flag >= 0) return *flag;
+    if (j == np) break;
+    // A11 trailing update with panel j: A(i, k) -= L(i, p0..) L(k, p0..), t0 <= k <= i < nb
+    const int w = min(W, nb - p0), t0 = p0 + w, m = nb - t0;
+    if (m > 0) {
+      const int mt = (m + 7) / 8, ntiles = mt * (mt + 1) / 2;
+      for (int tile = warp; tile < ntiles; tile += 8) {
+        int a = 0;
+        while ((a + 1) * (a + 2) / 2 <= tile) ++a;
+        const int b = tile - a * (a + 1) / 2;
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          const bool ok = 4 * fc + s < w;
+          const double af = ok ? S[(t0 + 8 * a + fr) * LD + p0 + 4 * fc + s] : 0.0;
+          const double bf = ok ? S[(t0 + 8 * b + fr) * LD + p0 + 4 * fc + s] : 0.0;
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(c0), "+d"(c1)
+                       : "d"(af), "d"(bf));
+        }
+        double* crow = S + (t0 + 8 * a + fr) * LD + t0 + 8 * b + 2 * fc;
+        crow[0] -= c0;
+        crow[1] -= c1;
+      }
+      __syncthreads();
+      CSTAMP(2 + 2 * j);
+    }
   }
   return -1;
 }

@@ -462,6 +462,34 @@ dla_status potrf_rec(const Ctx& c, int64_t batch, int64_t n, int64_t k0, MatB<T>
   return potrf_rec<T>(c, batch, n2, k0 + n1, a22);
 }
 
+// k-column of DMMA k-step s for fragment column fc (see k_potrf_panel)
+__device__ __forceinline__ int kcol(int s, int fc) { return ((s & ~3) << 2) + 4 * fc + (s & 3); }
+
+// 8-byte cp.async global -> shared, zero-filled when !pred
+__device__ __forceinline__ void st_async8(void* smem, const void* gmem, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(pred ? 8 : 0));
+}
+
+#ifndef DLAB_PANEL_TALL
+#define DLAB_PANEL_TALL 1  // fp64 panel: chunk solve interleaved with the factorization
+#endif
+
+#ifdef DLAB_PANEL_PROF
+// tuning build only: %globaltimer stamps of CTA 0's phases per panel step
+__device__ unsigned long long g_pprof[128][8];
+#define PSTAMP(i)                                                   \
+  do {                                                              \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                      \
+      unsigned long long t_;                                        \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));        \
+      g_pprof[(k0 / 64) & 127][i] = t_;                             \
+    }                                                               \
+  } while (0)
+#else
+#define PSTAMP(i)
+#endif
+
 // One block column of the right-looking Cholesky in ONE launch: every CTA
 // factors the NBP x NBP diagonal block (redundantly — it is latency, not
 // work), CTA 0 stores L11, and each CTA solves its own 64 rows of the panel
@@ -469,6 +497,10 @@ dla_status potrf_rec(const Ctx& c, int64_t batch, int64_t n, int64_t k0, MatB<T>
 template <typename T, int NBP>
 __global__ void __launch_bounds__(256, 1) k_potrf_panel(int nb, int64_t rest, int64_t k0, MatB<T> akk, MatB<T> a21,
                                                      int32_t* info, int* arrive, MatB<const T> lp, int kp) {
+  // Row stride 65: row-per-lane accesses are conflict-free.  The DMMA
+  // fragments (8 rows x 4 k) of the fp64 path take k-column 4 fc + s within
+  // each 16-column group (kcol) instead of fc + 4 s: with stride 65 the
+  // fr + fc pattern is a 4-way bank conflict, fr + 4 fc a 2-wavefront load.
   constexpr int LD = NBP + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* S = reinterpret_cast<T*>(smem_raw);
@@ -480,8 +512,31 @@ __global__ void __launch_bounds__(256, 1) k_potrf_panel(int nb, int64_t rest, in
   const int64_t b = blockIdx.x / chunks, cid = blockIdx.x % chunks;
   if (slice_failed(info, b)) return;
   const int tid = threadIdx.x;
+  PSTAMP(0);
   T* base = akk.at(b, 0, 0);
-  for (int e0 = tid; e0 < NBP * NBP; e0 += 8 * 256) {
+  constexpr bool tall = NBP == 64 && sizeof(T) == 8 && DLAB_PANEL_TALL;
+  const int64_t r0 = cid * 64;
+  const int nv = rest > 0 ? (int)min((int64_t)64, rest - r0) : 0;
+  T* pan = a21.at(b, r0, 0);
+  T* PC = P + 64 * LD;  // tall: the previous panel's columns at the chunk rows (nv x kp)
+  if constexpr (tall) {
+    // every operand of the step in flight at once: A11 (lower), the chunk
+    // rows, and the previous panel's rows Pd (diagonal) and Pc (chunk)
+    const T* gp = lp.at(b, 0, 0);
+#pragma unroll 4
+    for (int u = 0; u < 16; ++u) {
+      const int e = tid + u * 256, i = e / 64, j = e % 64;
+      st_async8(S + i * LD + j, base + (i < nb && j <= i ? i * akk.ld + j : 0), i < nb && j <= i);
+      st_async8(V + i * LD + j, pan + (i < nv && j < nb ? i * a21.ld + j : 0), i < nv && j < nb);
+      if (kp > 0) {
+        st_async8(P + i * LD + j, gp + (i < nb && j < kp ? i * lp.ld + j : 0), i < nb && j < kp);
+        st_async8(PC + i * LD + j, gp + (i < nv && j < kp ? (nb + r0 + i) * lp.ld + j : 0), i < nv && j < kp);
+      }
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+  }
+  for (int e0 = tid; !tall && e0 < NBP * NBP; e0 += 8 * 256) {
     T v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -494,10 +549,7 @@ __global__ void __launch_bounds__(256, 1) k_potrf_panel(int nb, int64_t rest, in
       S[(e / NBP) * LD + e % NBP] = v[u];
     }
   }
-  const int64_t r0 = cid * 64;
-  const int nv = rest > 0 ? (int)min((int64_t)64, rest - r0) : 0;
-  T* pan = a21.at(b, r0, 0);
-  for (int e0 = tid; e0 < 64 * NBP; e0 += 8 * 256) {  // panel rows, loads in flight during the factorization
+  for (int e0 = tid; !tall && e0 < 64 * NBP; e0 += 8 * 256) {  // panel rows, loads in flight during the factorization
     T v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -510,6 +562,7 @@ __global__ void __launch_bounds__(256, 1) k_potrf_panel(int nb, int64_t rest, in
       V[(e / NBP) * LD + e % NBP] = v[u];
     }
   }
+  PSTAMP(1);
   if constexpr (NBP == 64) {
     if (kp > 0) {
       // Fused look-ahead column update: this block column still lacks the
@@ -519,7 +572,7 @@ __global__ void __launch_bounds__(256, 1) k_potrf_panel(int nb, int64_t rest, in
       // each warp streams its 8 Pc rows' fragments from L2 once per k-step
       // and reuses them across all 8 column tiles.
       const T* gp = lp.at(b, 0, 0);
-      {  // all 16 loads of a thread in flight before the stores
+      if constexpr (!tall) {  // all 16 loads of a thread in flight before the stores
         T v[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
@@ -540,11 +593,12 @@ __global__ void __launch_bounds__(256, 1) k_potrf_panel(int nb, int64_t rest, in
 #pragma unroll
         for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = 0.0;
         for (int kk = 0; kk < kp; kk += 4) {
-          const double af = P[(8 * warp + fr) * LD + kk + fc];
+          const int kc = tall ? kcol(kk >> 2, fc) : kk + fc;
+          const double af = P[(8 * warp + fr) * LD + kc];
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
             if (t > warp) break;
-            const double bf = P[(8 * t + fr) * LD + kk + fc];
+            const double bf = P[(8 * t + fr) * LD + kc];
             asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                          : "+d"(acc[t][0]), "+d"(acc[t][1])
                          : "d"(af), "d"(bf));
@@ -568,6 +622,7 @@ __global__ void __launch_bounds__(256, 1) k_potrf_panel(int nb, int64_t rest, in
     }
   }
   __syncthreads();
+  PSTAMP(2);
   // A21 -= Pc Pd^T (the chunk rows) runs on warps 1-7 while warp 0 factors
   // the first 16 columns of A11 (chol_smem's side task)
   auto v_update = [&](int warp) {
@@ -584,13 +639,14 @@ __global__ void __launch_bounds__(256, 1) k_potrf_panel(int nb, int64_t rest, in
         const bool okr = vr < nv;
         double afv[16];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) afv[q] = (okr && 4 * q < kp) ? arow[4 * q + fc] : 0.0;
+        for (int q = 0; q < 16; ++q)
+          afv[q] = tall ? PC[vr * LD + kcol(q, fc)] : (okr && 4 * q < kp) ? arow[4 * q + fc] : 0.0;
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
           const double af = afv[q];
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
-            const double bf = P[(8 * t + fr) * LD + 4 * q + fc];
+            const double bf = P[(8 * t + fr) * LD + (tall ? kcol(q, fc) : 4 * q + fc)];
             asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                          : "+d"(acc[t][0]), "+d"(acc[t][1])
                          : "d"(af), "d"(bf));
@@ -619,8 +675,21 @@ __global__ void __launch_bounds__(256, 1) k_potrf_panel(int nb, int64_t rest, in
   // others have their copy in shared memory by then) writes L11 back over it
   // and re-arms the slice's counter for the next panel launch.
   __shared__ int last;
-  if (tid == 0) last = atomicAdd(arrive + b, 1) == (int)chunks - 1;
-  const int failed = chol_smem<T, NBP>(S, nb, &flag, v_update);  // (its first barrier publishes `last`)
+  int failed;
+  if constexpr (tall) {
+    // factor + chunk solve interleaved (V holds L21's rows after).  The
+    // arrival (after the barrier above: this CTA's A11 copy is complete) is
+    // issued now and its result consumed only after the factorization.
+    int my = 0;
+    if (tid == 0) my = atomicAdd(arrive + b, 1);
+    failed = chol_tall64<LD>(reinterpret_cast<double*>(S), reinterpret_cast<double*>(V), nb, nv, &flag, v_update);
+    if (tid == 0) last = my == (int)chunks - 1;
+    __syncthreads();
+  } else {
+    if (tid == 0) last = atomicAdd(arrive + b, 1) == (int)chunks - 1;
+    failed = chol_smem<T, NBP>(S, nb, &flag, v_update);  // (its first barrier publishes `last`)
+  }
+  PSTAMP(3);
   if (failed >= 0) {
     if (cid == 0 && tid == 0) record_failure(info, b, DLA_ERR_NOT_SPD, k0 + failed);
     return;
@@ -633,13 +702,18 @@ __global__ void __launch_bounds__(256, 1) k_potrf_panel(int nb, int64_t rest, in
     }
   }
   if (nv == 0) return;
-  for (int i = tid; i < NBP; i += 256) rd[i] = i < nb ? T(1) / S[i * LD + i] : T(1);
-  __syncthreads();
-  blocked_fwd_subst<T, LD>(S, V, rd, nb, nv);  // row v: L11 x = a  <=>  x^T L11^T = a^T
+  if constexpr (!tall) {
+    for (int i = tid; i < NBP; i += 256) rd[i] = i < nb ? T(1) / S[i * LD + i] : T(1);
+    __syncthreads();
+    PSTAMP(4);
+    blocked_fwd_subst<T, LD>(S, V, rd, nb, nv);  // row v: L11 x = a  <=>  x^T L11^T = a^T
+    PSTAMP(5);
+  }
   for (int e = tid; e < nv * nb; e += 256) {
     const int vv = e / nb, i = e % nb;
     pan[vv * a21.ld + i] = V[vv * LD + i];
   }
+  PSTAMP(6);
 }
 
 // Throughput variant of the panel step for large batches (batch x chunks
@@ -722,7 +796,7 @@ struct LookAhead {
 // variant's deep chain of tiny GEMMs dominates.
 template <typename T, int NBP>
 dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int64_t kbase) {
-  const size_t sm = sizeof(T) * ((NBP + 64) * (NBP + 1) + NBP + (NBP == 64 ? 64 * (NBP + 1) : 0));
+  const size_t sm = sizeof(T) * ((NBP + 64) * (NBP + 1) + NBP + (NBP == 64 ? 2 * 64 * (NBP + 1) : 0));
   static bool once = false;
   if (!once) {
     set_smem(k_potrf_panel<T, NBP>, sm);
@@ -998,3 +1072,12 @@ INST(double)
 INST(float)
 
 }  // namespace dlab
+
+#ifdef DLAB_PANEL_PROF
+extern "C" int dla_panel_prof_read(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, dlab::g_pprof, sizeof(dlab::g_pprof)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int dla_chol_prof_read(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, dlab::g_cprof, sizeof(dlab::g_cprof)) == cudaSuccess ? 0 : 1;
+}
+#endif
