@@ -137,13 +137,14 @@ __device__ __forceinline__ int panel_warp_n(T* S, int n, int p0, int w, int lane
 // the trailing lower triangle (8 x 8 DMMA tiles for f64).  Two barriers per
 // 16 columns instead of one per column.
 #ifdef DLAB_PANEL_PROF
-__device__ unsigned long long g_cprof[16];
+__device__ unsigned long long g_cprof[128][16];
+__device__ int g_prof_row;
 #define CSTAMP(i)                                                                     \
   do {                                                                                \
     if (gridDim.x >= 16 && blockIdx.x == 0 && threadIdx.x == 0) {                     \
       unsigned long long t_;                                                          \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
-      g_cprof[i] = t_;                                                                \
+      g_cprof[g_prof_row & 127][i] = t_;                                              \
     }                                                                                 \
   } while (0)
 #else

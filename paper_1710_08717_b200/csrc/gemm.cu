@@ -41,6 +41,9 @@ namespace dlab {
 namespace {
 
 constexpr int STAGES = 3, PAD = 4;
+#ifndef DLAB_GEMM_CPF
+#define DLAB_GEMM_CPF 2  // C row groups prefetched before the main loop (the MINB == 2 configuration)
+#endif
 
 // Tile configurations: CTA tile BM x BN, warp tile WM x WN (FP64 DMMA),
 // k-block BK per pipeline stage.
@@ -296,6 +299,33 @@ __global__ void __launch_bounds__(C::NT, C::MINB) dgemm_dmma(GemmArgs<double> g)
                                             sB + s * BT::ELEMS);
     cp_commit();
   }
+  const bool vec2 = ((g.c.ld & 1) == 0) && ((reinterpret_cast<uintptr_t>(tc.C) & 15) == 0);
+  auto load_group = [&](int i, double (&cv)[NI][2]) {
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+      cv[j][0] = cv[j][1] = 0.0;
+      if (g.beta == 0.0) continue;
+      const int64_t gi = m0 + wm + i * 8 + fr, gj = n0 + wn + j * 8 + 2 * fc;
+      if (gi >= g.m) continue;
+      const double* cp = tc.C + gi * g.c.ld + gj;
+      if (vec2 && gj + 1 < g.n) {
+        const double2 v = *reinterpret_cast<const double2*>(cp);
+        cv[j][0] = v.x;
+        cv[j][1] = v.y;
+      } else {
+        if (gj < g.n) cv[j][0] = cp[0];
+        if (gj + 1 < g.n) cv[j][1] = cp[1];
+      }
+    }
+  };
+  // short-K configurations: the first CPF C row groups load now, in flight
+  // under the main loop instead of exposed at the epilogue
+  constexpr int CPF = C::MINB == 2 ? DLAB_GEMM_CPF : 0, CPF1 = CPF > 0 ? CPF : 1;
+  double cpf[CPF1][NI][2];
+  if constexpr (CPF > 0) {
+#pragma unroll
+    for (int i = 0; i < CPF; ++i) load_group(i, cpf[i]);
+  }
   for (int64_t kb = 0; kb < nk; ++kb) {
     cp_wait<STAGES - 2>();
     __syncthreads();
@@ -333,31 +363,25 @@ __global__ void __launch_bounds__(C::NT, C::MINB) dgemm_dmma(GemmArgs<double> g)
   // Epilogue: C rows in groups of 8 (one fragment row i); when beta != 0 the
   // C values of group i+1 are loaded before group i is stored, so the
   // read-modify-write of C keeps loads in flight (the rank-64 SYRK updates
-  // of the blocked Cholesky are bound by exactly this C traffic).
-  const bool vec2 = ((g.c.ld & 1) == 0) && ((reinterpret_cast<uintptr_t>(tc.C) & 15) == 0);
-  auto load_group = [&](int i, double (&cv)[NI][2]) {
-#pragma unroll
-    for (int j = 0; j < NI; ++j) {
-      cv[j][0] = cv[j][1] = 0.0;
-      if (g.beta == 0.0) continue;
-      const int64_t gi = m0 + wm + i * 8 + fr, gj = n0 + wn + j * 8 + 2 * fc;
-      if (gi >= g.m) continue;
-      const double* cp = tc.C + gi * g.c.ld + gj;
-      if (vec2 && gj + 1 < g.n) {
-        const double2 v = *reinterpret_cast<const double2*>(cp);
-        cv[j][0] = v.x;
-        cv[j][1] = v.y;
-      } else {
-        if (gj < g.n) cv[j][0] = cp[0];
-        if (gj + 1 < g.n) cv[j][1] = cp[1];
-      }
-    }
-  };
+  // of the blocked Cholesky are bound by exactly this C traffic).  The first
+  // CPF groups were loaded before the main loop (short-K configurations).
   double cur[NI][2], nxt[NI][2];
-  load_group(0, cur);
+  if constexpr (CPF > 0) {
+#pragma unroll
+    for (int j = 0; j < NI; ++j) cur[j][0] = cpf[0][j][0], cur[j][1] = cpf[0][j][1];
+  } else {
+    load_group(0, cur);
+  }
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
-    if (i + 1 < MI) load_group(i + 1, nxt);
+    if (i + 1 < MI) {
+      if (i + 1 < CPF) {
+#pragma unroll
+        for (int j = 0; j < NI; ++j) nxt[j][0] = cpf[(i + 1) % CPF1][j][0], nxt[j][1] = cpf[(i + 1) % CPF1][j][1];
+      } else {
+        load_group(i + 1, nxt);
+      }
+    }
     const int64_t gi = m0 + wm + i * 8 + fr;
 #pragma unroll
     for (int j = 0; j < NI; ++j) {

@@ -484,6 +484,7 @@ __device__ unsigned long long g_pprof[128][8];
       unsigned long long t_;                                        \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));        \
       g_pprof[(k0 / 64) & 127][i] = t_;                             \
+      g_prof_row = (int)(k0 / 64);                                  \
     }                                                               \
   } while (0)
 #else

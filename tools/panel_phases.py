@@ -45,9 +45,11 @@ for rep in acc[-1:]:
     for p in (1, 2, 8, 16, 32, 48, 60, 62):
         if p < len(rep):
             print(f"  p={p:2d}", "  ".join(f"{v:6.2f}" for v in d[p]), f"  gap-before {gaps[p - 1]:6.2f}")
-cb = (C.c_ulonglong * 16)()
+cb = (C.c_ulonglong * (128 * 16))()
 if hasattr(L, "dla_chol_prof_read") and L.dla_chol_prof_read(cb) == 0:
-    c = np.frombuffer(cb, dtype=np.uint64).astype(np.int64)
-    print("chol_smem (last panel with >= 16 CTAs): warp0 panel0 %.2f us" % ((c[9] - c[0]) / 1e3))
-    print("  ", "  ".join(f"{(c[i] - c[i - 1]) / 1e3:.2f}" for i in range(1, 9)),
-          " (panel0+side | trail0 | panel1 | trail1 | ...)")
+    c = np.frombuffer(cb, dtype=np.uint64).reshape(128, 16).astype(np.int64)
+    rows = [r for r in range(1, 48) if c[r, 0] > 0 and c[r, 7] > c[r, 0]]
+    d = np.array([[(c[r, i] - c[r, i - 1]) / 1e3 for i in range(1, 8)] + [(c[r, 9] - c[r, 7]) / 1e3] for r in rows])
+    print("chol phases, mean over panels", rows[0], "..", rows[-1], "(A_j = warp-0 panel j || off-chain work; T_j = trail):")
+    print("  ", "  ".join(f"{nm} {v:.2f}" for nm, v in zip(["A0", "T0", "A1", "T1", "A2", "T2", "A3", "tail"], d.mean(0))))
+    print("   min", "  ".join(f"{v:.2f}" for v in d.min(0)))
