@@ -31,11 +31,29 @@ __global__ void k_scale(int64_t batch, int64_t m, int64_t n, MatB<T> x, T alpha,
 }
 
 // Square structural ops over (b, i, j).
+// Row-mapped square kernels: blockIdx.y walks the batch * n rows, blockIdx.x
+// and the threads the columns -- one division per row instead of four 64-bit
+// div/mods per element (which made these HBM-trivial kernels ALU-bound).
+#define DLAB_ROWS_BEGIN(batch, n)                                                   \
+  for (int64_t row_ = blockIdx.y; row_ < (batch) * (n); row_ += gridDim.y) {       \
+    const int64_t b = row_ / (n), i = row_ - b * (n);                               \
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < (n); j += (int64_t)gridDim.x * blockDim.x) {
+#define DLAB_ROWS_END \
+  }                   \
+  }
+
+inline dim3 row_grid(int64_t batch, int64_t n) {
+  // ~32 CTAs per SM in total (the rows loop covers the rest): one CTA per
+  // row-segment would be CTA-launch bound
+  const int64_t rows = batch * n, gx = (n + 255) / 256;
+  int64_t gy = std::max<int64_t>(1, (148 * 32) / gx);
+  gy = std::min<int64_t>(std::min<int64_t>(gy, std::max<int64_t>(rows, 1)), 65535);
+  return dim3((unsigned)gx, (unsigned)gy);
+}
+
 template <typename T>
 __global__ void k_square(int64_t batch, int64_t n, MatB<T> x, int op, T alpha, const int32_t* skip) {
-  const int64_t total = batch * n * n;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = t / (n * n), r = t % (n * n), i = r / n, j = r % n;
+  DLAB_ROWS_BEGIN(batch, n)
     if (slice_failed(skip, b)) continue;
     T* xij = x.at(b, i, j);
     switch (op) {
@@ -77,28 +95,44 @@ __global__ void k_square(int64_t batch, int64_t n, MatB<T> x, int op, T alpha, c
         }
         break;
     }
-  }
+  DLAB_ROWS_END
 }
 
 template <typename T>
 __global__ void k_tri_copy(int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, bool from_upper) {
-  const int64_t total = batch * n * n;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = t / (n * n), r = t % (n * n), i = r / n, j = r % n;
+  DLAB_ROWS_BEGIN(batch, n)
     T v = T(0);
     if (j <= i) v = from_upper ? *src.at(b, j, i) : *src.at(b, i, j);
     *dst.at(b, i, j) = v;
-  }
+  DLAB_ROWS_END
 }
 
+// dst = alpha (src + src^T) by 32 x 32 tile PAIRS: the block of tile (I, J),
+// I >= J, reads tiles (I, J) and (J, I) with coalesced rows, writes both
+// (in-place safe: no other block touches them).  IEEE addition commutes, so
+// the two mirrored sums are the same bits: bit-symmetric output.
 template <typename T>
-__global__ void k_add_transpose(int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, T alpha) {
-  const int64_t total = batch * n * n;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = t / (n * n), r = t % (n * n), i = r / n, j = r % n;
-    // (x_ij + x_ji) is the same IEEE sum from either side: bit-symmetric output
-    const T s = (i >= j) ? (*src.at(b, i, j) + *src.at(b, j, i)) : (*src.at(b, j, i) + *src.at(b, i, j));
-    *dst.at(b, i, j) = alpha * s;
+__global__ void __launch_bounds__(256) k_add_transpose(int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst,
+                                                       T alpha) {
+  __shared__ T ta[32][33], tb[32][33];
+  const int64_t I = blockIdx.x, J = blockIdx.y;
+  if (J > I) return;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int64_t b = blockIdx.z; b < batch; b += gridDim.z) {
+#pragma unroll
+    for (int r = ty; r < 32; r += 8) {
+      const int64_t i = I * 32 + r, j = J * 32 + tx, i2 = J * 32 + r, j2 = I * 32 + tx;
+      ta[r][tx] = (i < n && j < n) ? *src.at(b, i, j) : T(0);
+      tb[r][tx] = (i2 < n && j2 < n) ? *src.at(b, i2, j2) : T(0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = ty; r < 32; r += 8) {
+      const int64_t i = I * 32 + r, j = J * 32 + tx, i2 = J * 32 + r, j2 = I * 32 + tx;
+      if (i < n && j < n) *dst.at(b, i, j) = alpha * (ta[r][tx] + tb[tx][r]);
+      if (I != J && i2 < n && j2 < n) *dst.at(b, i2, j2) = alpha * (tb[r][tx] + ta[tx][r]);
+    }
+    __syncthreads();
   }
 }
 
@@ -221,18 +255,19 @@ __global__ void k_zero_diag(int64_t batch, int64_t n, MatB<const T> t, int32_t* 
 // sumlogdiag forward: logs in parallel, sum strictly in i = 0..n-1 order.
 template <typename T>
 __global__ void k_sumlogdiag(int64_t n, T* out, MatB<const T> a) {
-  __shared__ T logs[1024];
+  // per-thread strided partial sums, then a fixed-order tree: deterministic
+  // (a sequential sum by one thread was a ~50 us serial chain at n = 4096)
+  __shared__ T part[256];
   const int64_t b = blockIdx.x;
   T acc = T(0);
-  for (int64_t c0 = 0; c0 < n; c0 += 1024) {
-    const int64_t cn = min((int64_t)1024, n - c0);
-    for (int64_t i = threadIdx.x; i < cn; i += blockDim.x) logs[i] = Num<T>::log_(*a.at(b, c0 + i, c0 + i));
-    __syncthreads();
-    if (threadIdx.x == 0)
-      for (int64_t i = 0; i < cn; ++i) acc += logs[i];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += Num<T>::log_(*a.at(b, i, i));
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st; st >>= 1) {
+    if ((int)threadIdx.x < st) part[threadIdx.x] += part[threadIdx.x + st];
     __syncthreads();
   }
-  if (threadIdx.x == 0) out[b] = acc;
+  if (threadIdx.x == 0) out[b] = part[0];
 }
 
 template <typename T>
@@ -283,7 +318,7 @@ dla_status ew_scale(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<T> x
 template <typename T>
 dla_status ew_square(const Ctx& c, int64_t batch, int64_t n, MatB<T> x, int op, T alpha, const int32_t* skip) {
   if (batch * n == 0) return DLA_OK;
-  k_square<T><<<blocks_for(batch * n * n, 256), 256, 0, c.stream>>>(batch, n, x, op, alpha, skip);
+  k_square<T><<<row_grid(batch, n), 256, 0, c.stream>>>(batch, n, x, op, alpha, skip);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }
@@ -291,7 +326,7 @@ dla_status ew_square(const Ctx& c, int64_t batch, int64_t n, MatB<T> x, int op, 
 template <typename T>
 dla_status ew_tri_copy(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, bool from_upper) {
   if (batch * n == 0) return DLA_OK;
-  k_tri_copy<T><<<blocks_for(batch * n * n, 256), 256, 0, c.stream>>>(batch, n, src, dst, from_upper);
+  k_tri_copy<T><<<row_grid(batch, n), 256, 0, c.stream>>>(batch, n, src, dst, from_upper);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }
@@ -299,7 +334,9 @@ dla_status ew_tri_copy(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src
 template <typename T>
 dla_status ew_add_transpose(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, T alpha) {
   if (batch * n == 0) return DLA_OK;
-  k_add_transpose<T><<<blocks_for(batch * n * n, 256), 256, 0, c.stream>>>(batch, n, src, dst, alpha);
+  const unsigned tiles = (unsigned)((n + 31) / 32);
+  k_add_transpose<T><<<dim3(tiles, tiles, (unsigned)std::min<int64_t>(batch, 65535)), dim3(32, 8), 0, c.stream>>>(
+      batch, n, src, dst, alpha);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }
@@ -347,7 +384,7 @@ template <typename T>
 dla_status sumlogdiag_fwd(const Ctx& c, int64_t batch, int64_t n, T* out, MatB<const T> a) {
   if (batch == 0) return DLA_OK;
   if (n == 0) return cudaMemsetAsync(out, 0, sizeof(T) * batch, c.stream) == cudaSuccess ? DLA_OK : DLA_ERR_CUDA;
-  k_sumlogdiag<T><<<(unsigned)batch, 128, 0, c.stream>>>(n, out, a);
+  k_sumlogdiag<T><<<(unsigned)batch, n >= 2048 ? 256 : 128, 0, c.stream>>>(n, out, a);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }

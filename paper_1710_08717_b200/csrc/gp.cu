@@ -266,12 +266,14 @@ __global__ void k_rbf_xbar(int64_t rows, int64_t splits, int d, const double* xp
 }
 
 // Fixed-order finalization per slice: grads w.r.t. (log sigma2, log ell2, log lam).
+constexpr int FT = 1024;  // one CTA per slice: wide, so the partial sweep is not a serial chain
 __global__ void k_rbf_finalize(int64_t batch, int64_t n, int64_t splits, const double* part, double sigma2,
                                double ell2, double lam, double two_ell2, double* grads) {
   const int64_t b = blockIdx.x;
-  __shared__ double red[3][RT];
+  __shared__ double red[3][FT];
   double a0 = 0, a1 = 0, a2 = 0;
-  for (int64_t i = threadIdx.x; i < n; i += RT)
+#pragma unroll 4
+  for (int64_t i = threadIdx.x; i < n; i += FT)
     for (int64_t sp = 0; sp < splits; ++sp) {
       const double* pp = part + ((b * n + i) * splits + sp) * 3;
       a0 += pp[0];
@@ -282,7 +284,7 @@ __global__ void k_rbf_finalize(int64_t batch, int64_t n, int64_t splits, const d
   red[1][threadIdx.x] = a1;
   red[2][threadIdx.x] = a2;
   __syncthreads();
-  for (int st = RT / 2; st; st >>= 1) {
+  for (int st = FT / 2; st; st >>= 1) {
     if (threadIdx.x < st)
       for (int k = 0; k < 3; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + st];
     __syncthreads();
@@ -421,14 +423,14 @@ dla_status dla_gp_rbf_bwd_f64(int64_t batch, int64_t n, int64_t d, const double*
   int launches = 2;  // + 1 in DLAB_LAUNCH_CHECK
   if (launch_tiled<false>(d, batch, n, x, sq, sigma2, ell2 * 2.0, lam, nullptr, abar, xbar ? xpart : nullptr, part,
                           s)) {
-    k_rbf_finalize<<<(unsigned)batch, RT, 0, s>>>(batch, n, splits, part, sigma2, ell2, lam, ell2 * 2.0, grads);
+    k_rbf_finalize<<<(unsigned)batch, FT, 0, s>>>(batch, n, splits, part, sigma2, ell2, lam, ell2 * 2.0, grads);
     if (xbar) {
       k_rbf_xbar<<<blocks_for(batch * n * d, 256), 256, 0, s>>>(batch * n, splits, (int)d, xpart, xbar);
       ++launches;
     }
   } else {  // generic d: one CTA per row, partials already per row
     k_rbf_bwd<<<(unsigned)(batch * n), RT, 0, s>>>(n, d, x, sq, sigma2, ell2 * 2.0, abar, xbar, part);
-    k_rbf_finalize<<<(unsigned)batch, RT, 0, s>>>(batch, n, 1, part, sigma2, ell2, lam, ell2 * 2.0, grads);
+    k_rbf_finalize<<<(unsigned)batch, FT, 0, s>>>(batch, n, 1, part, sigma2, ell2, lam, ell2 * 2.0, grads);
   }
   note_launch(launches);
   DLAB_LAUNCH_CHECK();
