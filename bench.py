@@ -487,7 +487,7 @@ def main():
             "step_fp64_tflops": step_tflops,
             "step_frac_of_fp64_peak": step_tflops / fp64_peak,
             "roofline": {"bound": "tensor",
-                         "kernel": "dgemm_dmma<128x128, k-block 32, transposed A> (FP64 DMMA m8n8k4): Z = L^-T W "
+                         "kernel": "dgemm_dmma<128x64 tiles, 2 CTAs/SM, transposed A> (FP64 DMMA m8n8k4): Z = L^-T W "
                                    "inside potrf_bwd, the step's largest launch",
                          "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                          "frac": (achieved / fp64_peak) if achieved else None, "traffic": traffic,
