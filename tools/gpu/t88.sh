@@ -1,0 +1,3 @@
+DLA_LIB_PATH=paper_1710_08717_b200/libdla_prof.so python tools/panel_phases.py 4096 2>&1 | grep -A2 "mean us\|chol phases"
+for i in 1 2; do for L in libdla_alt.so libdla_b200.so; do echo -n "$L "; DLA_LIB_PATH=paper_1710_08717_b200/$L python bench.py --steps 30 --warmup 5 --no-cpu-baseline --no-also 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print(round(d['ms_per_step'],3))"; done; done
+python -m pytest tests -x -q -m gpu -k "potrf or gp or chain" 2>&1 | tail -1
