@@ -594,7 +594,7 @@ dla_status gp_potrf_inv(int64_t batch, int64_t n, T* a, int32_t* info, void* ws,
     cudaEventCreateWithFlags(&fin, cudaEventDisableTiming);
   });
   EarlyInv<T> e{batch, n, a, static_cast<T*>(ws), f.side, mid, false};
-  PotrfHook hook{n / 2, early_inv_first<T>, &e};
+  PotrfHook hook{n / 2, early_inv_first<T>, &e, a, n};
   Ctx hc = cx;
   hc.potrf_hook = &hook;
   DLAB_TRY(potrf_lower<T>(hc, batch, n, pk(a, n, n)));

@@ -50,6 +50,8 @@ struct PotrfHook {
   int64_t col;
   void (*fn)(void* user, cudaStream_t crit);
   void* user;
+  const void* a;  // the factorization it belongs to: fires only in the blocked loop over this
+  int64_t n;      // whole matrix (a recursive schedule's sub-blocks are not final at `col`)
 };
 
 // Launch context: stream + device properties + optional per-slice info.

@@ -907,7 +907,8 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
                                                                                 c.info, arrive.as<int>(), lp, kp);
       DLAB_LAUNCH_CHECK();
     }
-    if (c.potrf_hook && !hook_fired && kbase == 0 && k0 + kb >= c.potrf_hook->col) {
+    if (c.potrf_hook && !hook_fired && kbase == 0 && c.potrf_hook->n == n &&
+        c.potrf_hook->a == static_cast<const void*>(a.p) && k0 + kb >= c.potrf_hook->col) {
       c.potrf_hook->fn(c.potrf_hook->user, cc.stream);  // block columns [0, col) are final from here on
       hook_fired = true;
     }

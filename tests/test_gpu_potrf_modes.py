@@ -36,6 +36,19 @@ try:
     raise SystemExit("no error raised")
 except L.NotPositiveDefiniteError as e:
     assert e.batch_index == 1 and e.step == 200, (e.batch_index, e.step)
+# GP driver: dla_gp_potrf_inv_f64 under this schedule (no blocked hook point
+# in mode 1/3: the early half of L^-1 forms after the factorization) equals
+# potrf + dla_potrf_bwd_begin_f64 bitwise
+from paper_1710_08717_b200 import gp
+xg = torch.from_numpy(r.standard_normal((1, 1024, 8))).cuda()
+yg = torch.from_numpy(r.standard_normal((1, 1024, 1))).cuda()
+outs = []
+for early in (False, True):
+    gp._EARLY = early
+    g = gp.GPNLL(1024, 8, 1, "cuda")
+    outs.append([t.clone() for t in g.step(xg, yg, 1.0, 1.0, 0.1)])
+    g.check()
+assert all(torch.equal(u, v) for u, v in zip(*outs))
 print("ok")
 """
 
