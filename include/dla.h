@@ -219,7 +219,9 @@ size_t dla_potrf_bwd_ws_bytes_f64(int64_t batch, int64_t n);
  * pullback next: the blocked factorization signals once block columns
  * [0, n/2) are final, and L11^-1 and L21 L11^-1 (half of the inverse's
  * flops) form on the side stream during its chain-bound second half; the
- * rest follows the factorization.  Finish with dla_potrf_bwd_end_f64. */
+ * rest follows the factorization.  Finish with dla_potrf_bwd_end_f64; L's
+ * strict upper triangle is zeroed on the side stream and is complete (stream-
+ * ordered) once _end has been enqueued. */
 dla_status dla_gp_potrf_inv_f64(int64_t batch, int64_t n, double* a, int32_t* info, void* ws,
                                 size_t ws_bytes, void* stream);
 dla_status dla_potrf_bwd_begin_f64(int64_t batch, int64_t n, const double* l, int lower, void* ws,

@@ -597,7 +597,7 @@ dla_status gp_potrf_inv(int64_t batch, int64_t n, T* a, int32_t* info, void* ws,
   PotrfHook hook{n / 2, early_inv_first<T>, &e, a, n};
   Ctx hc = cx;
   hc.potrf_hook = &hook;
-  DLAB_TRY(potrf_lower<T>(hc, batch, n, pk(a, n, n)));
+  DLAB_TRY(potrf_lower<T>(hc, batch, n, pk(a, n, n), /*zero_upper*/ false));
   if (!e.fired) early_inv_first<T>(&e, cx.stream);  // a schedule without the hook point (tuning modes)
   const int64_t h = n / 2;
   T* wp = static_cast<T*>(ws);
@@ -613,6 +613,10 @@ dla_status gp_potrf_inv(int64_t batch, int64_t n, T* a, int32_t* info, void* ws,
   DLAB_TRY(gemm<T>(sc, batch, h, h, h, T(-1), MatB<const T>{wi.p + h * n + h, n, n * n}, false,
                    MatB<const T>{tmp, h, h * h}, false, T(0), wi.sub(h, 0), MASK_FULL, nullptr, TRI_LOWER,
                    TRI_NONE));
+  // L's strict upper triangle (the potrf contract) is zeroed here, on the side
+  // stream: no kernel of the step reads it, so it stays off the critical path
+  // and is complete once dla_potrf_bwd_end_f64 has joined `done`
+  DLAB_TRY(ew_square<T>(sc, batch, n, pk(a, n, n), /*tril*/ 0, T(1), info));
   cudaEventRecord(f.done, f.side);
   return DLA_OK;
 }

@@ -1018,7 +1018,7 @@ dla_status trmm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T>
 }
 
 template <typename T>
-dla_status potrf_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
+dla_status potrf_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool zero_upper) {
   if (batch == 0 || n == 0) return DLA_OK;
   static bool once = false;
   if (!once) {
@@ -1045,6 +1045,7 @@ dla_status potrf_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
   if (tiles) {
   } else if (blocked) DLAB_TRY(potrf_blocked<T>(c, batch, n, a, 0));
   else DLAB_TRY(potrf_rec<T>(c, batch, n, 0, a));
+  if (!zero_upper) return DLA_OK;  // the caller zeroes the strict upper triangle itself (off its critical path)
   return ew_square<T>(c, batch, n, a, /*tril*/ 0, T(1), c.info);
 }
 
@@ -1068,7 +1069,7 @@ dla_status potri_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
                               T, bool);                                                                     \
   template dla_status trmm<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<const T>, MatB<T>, bool, bool, bool, \
                               T);                                                                           \
-  template dla_status potrf_lower<T>(const Ctx&, int64_t, int64_t, MatB<T>);                                \
+  template dla_status potrf_lower<T>(const Ctx&, int64_t, int64_t, MatB<T>, bool);                                \
   template dla_status potri_lower<T>(const Ctx&, int64_t, int64_t, MatB<T>);
 INST(double)
 INST(float)

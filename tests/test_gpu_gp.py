@@ -80,6 +80,7 @@ def test_gp_early_inverse_matches_split(monkeypatch, n, batch):
         g = gp.GPNLL(n, 8, batch, "cuda")
         outs.append([t.clone() for t in g.step(x, y, 1.0, 1.0, 0.1)])
         g.check()
+        assert torch.count_nonzero(torch.triu(g.a, 1)) == 0  # potrf contract: L's strict upper is zero
     # same kernels on the same blocks in a different order: bitwise equal
     for a, b in zip(*outs):
         assert torch.equal(a, b)
