@@ -761,6 +761,7 @@ __global__ void __launch_bounds__(256) k_potrf_diag_inv(int nb, int64_t k0, MatB
 // growth happens outside any hot loop).
 struct LookAhead {
   cudaStream_t side = nullptr, crit = nullptr;
+  int prio_hi = 0;
   cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr;
   std::vector<cudaEvent_t> panel, done;
   static LookAhead& get(int64_t steps) {
@@ -774,6 +775,7 @@ struct LookAhead {
       cudaDeviceGetStreamPriorityRange(&lo, &hi);
       cudaStreamCreateWithPriority(&la.side, cudaStreamNonBlocking, lo);
       cudaStreamCreateWithPriority(&la.crit, cudaStreamNonBlocking, hi);
+      la.prio_hi = hi;
       cudaEventCreateWithFlags(&la.fork, cudaEventDisableTiming);
       cudaEventCreateWithFlags(&la.join, cudaEventDisableTiming);
       cudaEventCreateWithFlags(&la.join2, cudaEventDisableTiming);
@@ -902,9 +904,21 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
     } else {
       const int kp = fused(p) ? (int)NBP : 0;
       MatB<const T> lp = C_(p >= 1 ? a.sub(k0, k0 - NBP) : a);
-      k_potrf_panel<T, NBP><<<(unsigned)(batch * chunks), 256, sm, cc.stream>>>((int)kb, rest, kbase + k0,
-                                                                                a.sub(k0, k0), a.sub(k0 + kb, k0),
-                                                                                c.info, arrive.as<int>(), lp, kp);
+      // the chain's priority as a launch attribute too: a CUDA graph captured
+      // from these streams then carries it on the node itself
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3((unsigned)(batch * chunks));
+      cfg.blockDim = dim3(256);
+      cfg.dynamicSmemBytes = sm;
+      cfg.stream = cc.stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributePriority;
+      attr[0].val.priority = la.prio_hi;
+      cfg.attrs = attr;
+      cfg.numAttrs = prio ? 1 : 0;
+      if (cudaLaunchKernelEx(&cfg, k_potrf_panel<T, NBP>, (int)kb, rest, kbase + k0, a.sub(k0, k0),
+                             a.sub(k0 + kb, k0), c.info, arrive.as<int>(), lp, kp) != cudaSuccess)
+        return DLA_ERR_CUDA;
       DLAB_LAUNCH_CHECK();
     }
     if (c.potrf_hook && !hook_fired && kbase == 0 && c.potrf_hook->n == n &&
