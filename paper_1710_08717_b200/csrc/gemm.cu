@@ -23,6 +23,7 @@
 // and the contiguous extent allow, 8/4-byte otherwise, so every shape works.
 // Batch and tiles share a flat grid.x (65536-slice batches exceed gridDim.z).
 #include "common.cuh"
+#include <algorithm>
 
 #ifndef DLAB_GEMM_BKL
 #define DLAB_GEMM_BKL 32  // k-block of the 128 x 128 configuration (3 stages: 212 KB smem)
@@ -585,12 +586,30 @@ bool vec_ok(const MatB<const T>& x, int64_t contiguous_extent) {
   return (p % 16 == 0) && (x.ld % V == 0) && (x.bs % V == 0) && (x.bsi % V == 0) && (contiguous_extent % V == 0);
 }
 
+// Algorithmic flops of one slab: 2 x #{(i, j, k)} with C(i, j) inside the
+// mask and A(i, k), B(k, j) inside their triangles (tri_a lower: k <= i,
+// upper: k >= i; tri_b lower: k >= j, upper: k <= j; mask lower: i >= j).
+// Counted over a strided (i, j) grid, exact k range per point: e.g. upper x
+// lower with a full output is 2n^3/3, lower x lower into a lower mask n^3/3.
+// Only evaluated when DLA profiling is on.
 double useful_flops(int64_t m, int64_t n, int64_t k, int mask, int tri_a, int tri_b) {
-  double f = 2.0 * (double)m * (double)n * (double)k;
-  if (mask != MASK_FULL && m == n) f *= 0.5;
-  if (tri_a != TRI_NONE) f *= 0.5;
-  if (tri_b != TRI_NONE) f *= 0.5;
-  return f;
+  if (mask == MASK_FULL && tri_a == TRI_NONE && tri_b == TRI_NONE) return 2.0 * (double)m * (double)n * (double)k;
+  const int64_t si = (m + 255) / 256, sj = (n + 255) / 256;
+  double cnt = 0.0;
+  for (int64_t i = 0; i < m; i += si) {
+    for (int64_t j = 0; j < n; j += sj) {
+      if (mask == MASK_LOWER && i < j) continue;
+      if (mask == MASK_UPPER && i > j) continue;
+      int64_t lo = 0, hi = k - 1;
+      if (tri_a == TRI_LOWER) hi = std::min(hi, i);
+      if (tri_a == TRI_UPPER) lo = std::max(lo, i);
+      if (tri_b == TRI_LOWER) lo = std::max(lo, j);
+      if (tri_b == TRI_UPPER) hi = std::min(hi, j);
+      if (hi >= lo) cnt += (double)(hi - lo + 1);
+    }
+  }
+  const double pts_i = (double)((m + si - 1) / si), pts_j = (double)((n + sj - 1) / sj);
+  return 2.0 * cnt * ((double)m / pts_i) * ((double)n / pts_j);
 }
 
 }  // namespace

@@ -28,3 +28,22 @@ def test_c5_chain_matches_oracle(port, n):
     got = out.cpu().numpy()
     assert abs(got[0] - want[0]) / abs(want[0]) < 1e-11
     assert abs(got[1] - want[1]) / max(1, abs(want[1])) < 1e-9
+
+
+def test_c5_shards_sum_to_full_batch():
+    # bench.py --gpus N shards the C5 batch into contiguous ranges and all-reduces
+    # [loss, dloss/dtheta]; on one GPU the per-shard results must sum to the
+    # whole-batch result (rtol 1e-12), with the same global inputs per item.
+    from paper_1710_08717_b200.shard import shard_range
+    from tools.bench_configs import c5_inputs
+    total, n, theta = 8192, 128, math.log(0.3)
+    s, y = c5_inputs(torch, 0, total, n)
+    full = MarginalLikelihoods(total, n).step(s, y, theta).clone()
+    for world in (2, 4):
+        acc = torch.zeros(2, dtype=torch.float64, device="cuda")
+        for rank in range(world):
+            lo, hi = shard_range(total, rank, world)
+            ss, yy = c5_inputs(torch, lo, hi, n)
+            assert torch.equal(ss, s[lo:hi]) and torch.equal(yy, y[lo:hi])  # same global items
+            acc += MarginalLikelihoods(hi - lo, n).step(ss, yy, theta)
+        assert torch.allclose(acc, full, rtol=1e-12, atol=0)

@@ -193,46 +193,86 @@ def run(torch, args, rank, world, lib, fp64_peak, hbm):
                                "note": "count-convention flops 10n^3/3 + 6n^3 per matrix; the smem Jacobi does "
                                        "~20x that in FP64 FMA and is bound by its per-round barrier chain"})
     if cfg == "c5":
-        from paper_1710_08717_b200.c5 import MarginalLikelihoods
-        total, n = 65536, 128
-        lo, hi = shard_range(total, rank, world)
-        B = hi - lo
-        r = O.rng(55)
-        s = torch.empty(B, n, n, dtype=torch.float64, device="cuda")
-        chunk = 4096
-        for c0 in range(0, B, chunk):  # per-rank slice of the global synthetic batch
-            cb = min(chunk, B - c0)
-            x = torch.randn(cb, n, n, dtype=torch.float64, device="cuda",
-                            generator=torch.Generator("cuda").manual_seed(lo + c0))
-            s[c0:c0 + cb] = x @ x.transpose(-1, -2) + n * torch.eye(n, dtype=torch.float64, device="cuda")
-        y = torch.randn(B, n, 1, dtype=torch.float64, device="cuda")
-        m = MarginalLikelihoods(B, n)
-        theta = math.log(0.3)
-        ms = bench.timed(torch, lambda: m.step_allreduce(s, y, theta), args.steps, args.warmup, world)
-        m.check()
-        flops = total * 8.33 * n ** 3
+        r = c5_measure(torch, rank, world, args.steps, args.warmup, fp64_peak)
         cpu = None
         if rank == 0 and world == 1 and not getattr(args, "no_cpu_baseline", False):
-            import time as _t
-            port = O.port()
-            sc = s[:1].cpu().numpy()[0]
-            yc = y[:1].cpu().numpy()[0]
-            reps, t0 = 0, _t.perf_counter()
-            while _t.perf_counter() - t0 < 3.0:
-                O.c5_item(port, sc, yc, theta)
-                reps += 1
-            secs = (_t.perf_counter() - t0) / reps
-            cpu = {"value": 1.0 / secs, "unit": "items/s", "cores": 1, "kind": "port",
-                   "sample": f"{reps} C5 items through the oracle port's per-op chain (C restatement of the "
-                             f"reference ops, 1 thread); the reference has no C5 driver"}
-        return _line(args, world, "C5 GP marginal likelihoods items/s", total / (ms / 1e3), "items/s", ms,
-                     "C5: 65536 x 128^2 GP marginal likelihoods (potrf+potri+trmm fwd+bwd), batch sharded over "
-                     f"{world} GPU(s), NCCL all-reduce of (loss, dloss/dtheta)",
-                     step_tflops=flops / (ms / 1e3) / 1e12, loss_grad=m.out.cpu().tolist(),
-                     config_parallelism=f"dp{world} (contiguous batch shards)", cpu_baseline=cpu,
-                     roofline={"bound": "tensor", "achieved": flops / (ms / 1e3) / 1e12 / world, "peak": fp64_peak,
-                               "unit": "TFLOP/s", "frac": flops / (ms / 1e3) / 1e12 / world / fp64_peak,
-                               "traffic": None,
-                               "note": "per GPU, minimal flops 8.33 n^3 per item (SURVEY 8d); the operator "
-                                       "composition executes ~11 n^3 in 128-wide batched DMMA tiles"})
+            cpu = c5_cpu_baseline(r.pop("sample_inputs"), r["theta"])
+        r.pop("sample_inputs", None)
+        return _line(args, world, "C5 GP marginal likelihoods items/s", r["items_per_s"], "items/s", r["ms_per_step"],
+                     r["workload"], cpu_baseline=cpu, **{k: v for k, v in r.items()
+                                                         if k not in ("items_per_s", "ms_per_step", "workload")})
     raise ValueError(cfg)
+
+
+def c5_inputs(torch, lo, hi, n=128):
+    """Per-rank slice [lo, hi) of the GLOBAL synthetic C5 batch: item chunks of
+    4096 are generated on device from a generator seeded by the chunk's global
+    start, so every world size sees the same items (shard bounds are multiples
+    of 4096 for N | 16)."""
+    chunk = 4096
+    B = hi - lo
+    s = torch.empty(B, n, n, dtype=torch.float64, device="cuda")
+    y = torch.empty(B, n, 1, dtype=torch.float64, device="cuda")
+    from paper_1710_08717_b200 import linalg as L
+    from paper_1710_08717_b200._lib import lib
+    import ctypes as C
+    g0 = (lo // chunk) * chunk
+    for c0 in range(g0, hi, chunk):
+        gen = torch.Generator("cuda").manual_seed(c0)
+        x = torch.randn(chunk, n, n, dtype=torch.float64, device="cuda", generator=gen)
+        yy = torch.randn(chunk, n, 1, dtype=torch.float64, device="cuda", generator=gen)
+        a, b = max(c0, lo), min(c0 + chunk, hi)
+        xs = x[a - c0:b - c0].contiguous()
+        # S = X X^T + n I per item through libdla's syrk (batch = grid: the
+        # same bits for an item whatever the shard), then the diagonal shift
+        L.syrk_into(xs, xs.clone(), False, 1.0)
+        st = lib().lib.dla_ml_shift_copy_f64(b - a, n, C.c_void_p(xs.data_ptr()),
+                                            C.c_void_p(s[a - lo:b - lo].data_ptr()), float(n),
+                                            C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        assert st == 0
+        y[a - lo:b - lo] = yy[a - c0:b - c0]
+        del x, yy
+    return s, y
+
+
+def c5_measure(torch, rank, world, steps, warmup, fp64_peak, total=65536, n=128):
+    """C5: `total` independent 128^2 GP marginal likelihoods, contiguous batch
+    shards per rank, one NCCL all-reduce of [loss, dloss/dtheta] per step."""
+    import bench
+    from paper_1710_08717_b200.c5 import MarginalLikelihoods
+    from paper_1710_08717_b200.shard import shard_range
+    lo, hi = shard_range(total, rank, world)
+    s, y = c5_inputs(torch, lo, hi, n)
+    m = MarginalLikelihoods(hi - lo, n)
+    theta = math.log(0.3)
+    ms = bench.timed(torch, lambda: m.step_allreduce(s, y, theta), steps, warmup, world)
+    m.check()
+    flops = total * 8.33 * n ** 3
+    tf = flops / (ms / 1e3) / 1e12
+    out = dict(items_per_s=total / (ms / 1e3), ms_per_step=ms,
+               workload=f"C5: {total} x {n}^2 GP marginal likelihoods (potrf+potri+trmm fwd+bwd), batch sharded "
+                        f"over {world} GPU(s), NCCL all-reduce of (loss, dloss/dtheta)",
+               step_tflops=tf, loss_grad=m.out.cpu().tolist(), theta=theta,
+               config_parallelism=f"dp{world} (contiguous batch shards, one all_reduce of 2 fp64 per step)",
+               roofline={"bound": "tensor", "achieved": tf / world, "peak": fp64_peak, "unit": "TFLOP/s",
+                         "frac": tf / world / fp64_peak, "traffic": None,
+                         "note": "per GPU, minimal flops 8.33 n^3 per item (SURVEY 8d)"},
+               sample_inputs=(s[:1].cpu().numpy()[0], y[:1].cpu().numpy()[0]) if rank == 0 else None)
+    del m, s, y
+    torch.cuda.empty_cache()
+    return out
+
+
+def c5_cpu_baseline(sample, theta):
+    import time as _t
+    from oracle import oracle as O
+    port = O.port()
+    sc, yc = sample
+    reps, t0 = 0, _t.perf_counter()
+    while _t.perf_counter() - t0 < 3.0:
+        O.c5_item(port, sc, yc, theta)
+        reps += 1
+    secs = (_t.perf_counter() - t0) / reps
+    return {"value": 1.0 / secs, "unit": "items/s", "cores": 1, "kind": "port",
+            "sample": f"{reps} C5 items through the oracle port's per-op chain (C restatement of the "
+                      f"reference ops, 1 thread); the reference has no C5 driver"}
