@@ -18,9 +18,22 @@
  *              index, rank row, QL iteration count).  The first failing
  *              slice's info is what the reference would have thrown
  *              (dl/matrix.hpp:232-239); use dla_info_check() to read it.
- *   workspace  caller-owned device scratch sized by dla_workspace_bytes();
- *              no entry point allocates device memory.
+ *   workspace  every operator takes (ws, ws_bytes): caller-owned device
+ *              scratch of at least dla_workspace_bytes() bytes (any
+ *              alignment; NULL/0 when the query returns 0).  ALL internal
+ *              scratch is carved from it -- no entry point allocates device
+ *              memory -- and a too-small workspace returns DLA_ERR_WORKSPACE
+ *              before any launch that would need it.  The workspace must stay
+ *              untouched until the op's work on `stream` has completed
+ *              (stream order: the next call on the same stream may reuse it).
  *   stream     cudaStream_t passed as void*; 0 = legacy default stream.
+ *   threading  no process-global mutable state on the compute path: device
+ *              properties and kernel attributes are per device (the current
+ *              device at the call), fork/join side streams and events are
+ *              per (device, caller stream) and locked for the enqueue, so
+ *              calls from different host threads on different streams or
+ *              devices are independent.  Calls on ONE stream from several
+ *              threads are serialised by the caller (stream order).
  *
  * Host-side validation (shape, aliasing) runs before any launch and
  * returns a status synchronously; numerical failures are per-slice and
@@ -28,8 +41,12 @@
  * (dl/blas.hpp:33-38, :58-59, :146, :197): these return DLA_ERR_ALIAS.
  *
  * Precision: the f64 path computes in IEEE binary64 end to end (FP64 DMMA
- * tensor cores for the blocked contractions); the f32 path computes in
- * binary32 with FFMA (no TF32 rounding), see DESIGN.md "fp32 policy".
+ * tensor cores for the blocked contractions).  The f32 path computes in
+ * binary32: FFMA for small products, and for large products (m, n >= 256,
+ * k >= 128) 3xTF32 on the tcgen05 tensor cores -- each operand split once
+ * into TF32 hi + lo, C += hi*hi + hi*lo + lo*hi with fp32 accumulation,
+ * i.e. binary32-level accuracy (DLA_SGEMM_TC=0
+ * keeps every f32 product on FFMA).
  */
 #ifndef DLA_B200_H_
 #define DLA_B200_H_
@@ -62,21 +79,29 @@ typedef enum dla_status {
 typedef enum dla_op {
   DLA_OP_GEMM = 0, DLA_OP_GEMM2 = 1, DLA_OP_SYRK = 2, DLA_OP_TRMM = 3,
   DLA_OP_TRSM = 4, DLA_OP_POTRF = 5, DLA_OP_POTRI = 6, DLA_OP_SUMLOGDIAG = 7,
-  DLA_OP_GELQF = 8, DLA_OP_SYEVD = 9
+  DLA_OP_GELQF = 8, DLA_OP_SYEVD = 9, DLA_OP_CHOL_CHAIN = 10, DLA_OP_GESVD = 11
 } dla_op;
 
 typedef enum dla_dtype { DLA_F32 = 0, DLA_F64 = 1 } dla_dtype;
 
-/* dla_workspace_bytes flags */
-#define DLA_WS_BACKWARD 1
+/* dla_workspace_bytes phase flags */
+#define DLA_WS_BACKWARD 1  /* the op's pullback (else its forward)          */
+#define DLA_WS_RIGHTSIDE 2 /* trmm / trsm with rightside = 1                */
 
 const char* dla_status_string(dla_status s);
 const char* dla_version(void);
 
-/* Device scratch (bytes) the op needs for the given problem; 0 = none.
- * Budgets mirror dl/adjoints.hpp:1-9: gelqf fwd m per slice (tau), gelqf bwd
- * m*m, syevd fwd/bwd n*n (+ small), everything else 0.  `phase` is 0
- * (forward) or DLA_WS_BACKWARD. */
+/* Device workspace (bytes) one call of the op needs; 0 = none.  Host-only
+ * (no device access), deterministic in its arguments.  Dimensions as the op
+ * takes them: gemm/gemm2 (m, n, k); syrk (n, k); trmm/trsm (m, n) of X plus
+ * DLA_WS_RIGHTSIDE; potrf/potri/sumlogdiag/syevd/chol_chain n; gelqf/gesvd
+ * (m, n).  `phase`: DLA_WS_BACKWARD for the pullback.  The reference's own
+ * budgets (dl/adjoints.hpp:1-9: gelqf tau m, gelqf bwd m*m, syevd n*n + 9n,
+ * syevd bwd n*n; zero for gemm2/syrk/trmm/trsm/potrf/potri pullbacks) are
+ * what the CPU needs; the device schedules here add their own scratch (the
+ * inverse-based pullbacks' n*n factor inverse, the narrow solve's publish
+ * buffer, packed tcgen05 operands for large f32 products) and the query
+ * returns that sum. */
 size_t dla_workspace_bytes(dla_op op, dla_dtype dtype, int64_t batch, int64_t m,
                            int64_t n, int64_t k, int phase);
 
@@ -95,78 +120,80 @@ dla_status dla_info_check(const int32_t* info, int64_t batch, void* stream,
      C must not alias A or B. */                                                    \
   dla_status dla_gemm2_fwd_##S(int64_t batch, int64_t m, int64_t n, int64_t k,      \
                                T* c, const T* a, const T* b, int ta, int tb,        \
-                               T alpha, void* stream);                              \
+                               T alpha, void* ws, size_t ws_bytes, void* stream);                              \
   /* gemm: C = alpha op(A) op(B) + beta C.  beta = 0 / 1 are the reference's        \
      gemm_accum(accumulate = false / true) (dl/blas.hpp:43-110); other beta         \
      scale C first. */                                                              \
   dla_status dla_gemm_fwd_##S(int64_t batch, int64_t m, int64_t n, int64_t k,       \
                               T* c, const T* a, const T* b, int ta, int tb,         \
-                              T alpha, T beta, void* stream);                       \
+                              T alpha, T beta, void* ws, size_t ws_bytes, void* stream);                       \
   /* gemm2 / gemm pullback: dl/adjoints.hpp:36-49 (Abar written before Bbar). */    \
   dla_status dla_gemm2_bwd_##S(int64_t batch, int64_t m, int64_t n, int64_t k,      \
                                T* abar, T* bbar, const T* cbar, const T* a,         \
-                               const T* b, int ta, int tb, T alpha, void* stream);  \
+                               const T* b, int ta, int tb, T alpha, void* ws, size_t ws_bytes, void* stream);  \
   /* gemm pullback: abar/bbar as gemm2; cbar_io <- beta * cbar_io (the C-input     \
      cotangent), after abar/bbar are formed. */                                     \
   dla_status dla_gemm_bwd_##S(int64_t batch, int64_t m, int64_t n, int64_t k,       \
                               T* abar, T* bbar, T* cbar_io, const T* a,             \
                               const T* b, int ta, int tb, T alpha, T beta,          \
-                              void* stream);                                        \
+                              void* ws, size_t ws_bytes, void* stream);                                        \
   /* syrk: B = alpha A A^T (ta=0, A n x k) / alpha A^T A (ta=1, A k x n),           \
      bit-exactly symmetric; dl/blas.hpp:138-169. */                                 \
   dla_status dla_syrk_fwd_##S(int64_t batch, int64_t n, int64_t k, T* b,            \
-                              const T* a, int ta, T alpha, void* stream);           \
+                              const T* a, int ta, T alpha, void* ws, size_t ws_bytes, void* stream);           \
   /* syrk pullback: dl/adjoints.hpp:69-78. */                                       \
   dla_status dla_syrk_bwd_##S(int64_t batch, int64_t n, int64_t k, T* abar,         \
                               const T* bbar, const T* a, int ta, T alpha,           \
-                              void* stream);                                        \
+                              void* ws, size_t ws_bytes, void* stream);                                        \
   /* trmm: X <- alpha op(T) X (right=0) / alpha X op(T) (right=1); X m x n,         \
      T m x m (left) or n x n (right); dl/blas.hpp:202-291. */                       \
   dla_status dla_trmm_fwd_##S(int64_t batch, int64_t m, int64_t n, const T* t,      \
                               T* x, int rightside, int transpose, int lower,        \
-                              T alpha, void* stream);                               \
+                              T alpha, void* ws, size_t ws_bytes, void* stream);                               \
   /* trmm pullback (reads the forward INPUT a); abar may alias bbar;                \
      dl/adjoints.hpp:94-110. */                                                     \
   dla_status dla_trmm_bwd_##S(int64_t batch, int64_t m, int64_t n, T* abar,         \
                               T* tbar, const T* bbar, const T* t, const T* a,       \
                               int rightside, int transpose, int lower, T alpha,     \
-                              void* stream);                                        \
+                              void* ws, size_t ws_bytes, void* stream);                                        \
   /* trsm: X <- alpha op(T)^-1 X / alpha X op(T)^-1; exact zero diagonal =>         \
      SINGULAR(k) in info and the slice is left untouched; dl/blas.hpp:307-395. */   \
   dla_status dla_trsm_fwd_##S(int64_t batch, int64_t m, int64_t n, const T* t,      \
                               T* x, int rightside, int transpose, int lower,        \
-                              T alpha, int32_t* info, void* stream);                \
+                              T alpha, int32_t* info, void* ws, size_t ws_bytes, void* stream);                \
   /* trsm pullback (reads the forward OUTPUT b); abar may alias bbar;               \
      dl/adjoints.hpp:131-153. */                                                    \
   dla_status dla_trsm_bwd_##S(int64_t batch, int64_t m, int64_t n, T* abar,         \
                               T* tbar, const T* bbar, const T* t, const T* b,       \
                               int rightside, int transpose, int lower, T alpha,     \
-                              void* stream);                                        \
+                              void* ws, size_t ws_bytes, void* stream);                                        \
   /* potrf: A = L L^T (lower=1, strict upper zeroed) / A = R^T R (lower=0), in      \
      place.  Asymmetric input => ASYMMETRIC (slice untouched); failed pivot =>      \
      NOT_SPD(step); dl/cholesky.hpp:79-88. */                                       \
   dla_status dla_potrf_fwd_##S(int64_t batch, int64_t n, T* a, int lower,           \
-                               int32_t* info, void* stream);                        \
+                               int32_t* info, void* ws, size_t ws_bytes, void* stream);                        \
   /* potrf pullback: Abar = 1/2 L^-T copyltu(L^T Lbar) L^-1, exactly symmetric;     \
      abar may alias lbar; dl/adjoints.hpp:175-191. */                               \
   dla_status dla_potrf_bwd_##S(int64_t batch, int64_t n, T* abar, const T* lbar,    \
-                               const T* l, int lower, void* stream);                \
+                               const T* l, int lower, void* ws, size_t ws_bytes, void* stream);                \
   /* potri: B = A^-1 from the Cholesky factor, in place, exactly symmetric;         \
      zero diagonal => SINGULAR(j); dl/cholesky.hpp:141-147. */                      \
   dla_status dla_potri_fwd_##S(int64_t batch, int64_t n, T* a, int lower,           \
-                               int32_t* info, void* stream);                        \
+                               int32_t* info, void* ws, size_t ws_bytes, void* stream);                        \
   /* potri pullback: Lbar = -tril((B Bbar + B Bbar^T) L^-T); dl/adjoints.hpp:207. */\
   dla_status dla_potri_bwd_##S(int64_t batch, int64_t n, T* lbar, const T* bbar,    \
-                               const T* l, const T* b, int lower, void* stream);    \
-  /* sumlogdiag: out[b] = sum_i log A_b(i,i), sequential i order (tape chain        \
-     ExtractDiag->Log->Sum, dl/tape.hpp:789-795, :714, :747-755). */                \
+                               const T* l, const T* b, int lower, void* ws, size_t ws_bytes, void* stream);    \
+  /* sumlogdiag: out[b] = sum_i log A_b(i,i) (tape chain ExtractDiag->Log->Sum,   \
+     dl/tape.hpp:789-795, :714, :747-755), summed as per-thread strided partials    \
+     reduced by a fixed-order tree: deterministic, NOT the reference's sequential  \
+     i order (agrees to ~n u). */                                                   \
   dla_status dla_sumlogdiag_fwd_##S(int64_t batch, int64_t n, T* out, const T* a,   \
-                                    void* stream);                                  \
+                                    void* ws, size_t ws_bytes, void* stream);                                  \
   /* sumlogdiag pullback: abar(i,i) = gbar[b] / A(i,i), off-diagonal exactly 0      \
      (accumulate=0) or untouched (accumulate=1: added onto the diagonal). */        \
   dla_status dla_sumlogdiag_bwd_##S(int64_t batch, int64_t n, T* abar,              \
                                     const T* gbar, const T* a, int accumulate,      \
-                                    void* stream);                                  \
+                                    void* ws, size_t ws_bytes, void* stream);                                  \
   /* gelqf: A (m x n, m <= n) = L Q; q: in A, out Q; l: out L (m x m, positive      \
      diagonal); rank deficiency => SINGULAR(row); dl/lq.hpp:24-106.                 \
      workspace: dla_workspace_bytes(DLA_OP_GELQF, ..., 0) (m reals per slice;       \
@@ -211,9 +238,11 @@ long long dla_prof_read_max(double* ms, double* flops);
  * factor's inverse with work that only reads L (the GP driver's solves):
  * _begin forks L^-1 onto an internal side stream; _end joins and produces
  * Abar bitwise identical to dla_potrf_bwd_f64 (dl/adjoints.hpp:175-191).  L
- * must not change in between; one begin/end pair in flight per process.
- * Sizes where the inverse path does not apply (n != 64 * 2^k) make _begin a
- * no-op and _end the plain pullback.  Workspace: dla_potrf_bwd_ws_bytes_f64. */
+ * must not change in between; one begin/end pair in flight per (device,
+ * stream).  Sizes where the inverse path does not apply (n != 64 * 2^k) make
+ * _begin a no-op and _end the plain pullback.  Workspace: one buffer of
+ * dla_potrf_bwd_ws_bytes_f64 bytes, the SAME buffer for every call of a
+ * pair (its head holds L^-1 between the calls). */
 size_t dla_potrf_bwd_ws_bytes_f64(int64_t batch, int64_t n);
 /* dla_potrf_fwd_f64 (lower) fused with _begin for a driver that needs the
  * pullback next: the blocked factorization signals once block columns
@@ -221,13 +250,17 @@ size_t dla_potrf_bwd_ws_bytes_f64(int64_t batch, int64_t n);
  * flops) form on the side stream during its chain-bound second half; the
  * rest follows the factorization.  Finish with dla_potrf_bwd_end_f64; L's
  * strict upper triangle is zeroed on the side stream and is complete (stream-
- * ordered) once _end has been enqueued. */
+ * ordered) once _end -- or, for a caller that does not need the pullback,
+ * dla_potrf_inv_join_f64 -- has been enqueued on `stream`. */
 dla_status dla_gp_potrf_inv_f64(int64_t batch, int64_t n, double* a, int32_t* info, void* ws,
                                 size_t ws_bytes, void* stream);
 dla_status dla_potrf_bwd_begin_f64(int64_t batch, int64_t n, const double* l, int lower, void* ws,
                                    size_t ws_bytes, void* stream);
 dla_status dla_potrf_bwd_end_f64(int64_t batch, int64_t n, double* abar, const double* lbar,
                                  const double* l, int lower, void* ws, size_t ws_bytes, void* stream);
+/* Makes `stream` wait for the side-stream work of the last _begin /
+ * dla_gp_potrf_inv_f64 on it (the join _end performs), without the pullback. */
+dla_status dla_potrf_inv_join_f64(void* stream);
 
 /* ----------------------------------------------- fused C1 likelihood chain */
 /* Gaussian log-likelihood chain over a batch of small SPD matrices
@@ -241,10 +274,10 @@ dla_status dla_potrf_bwd_end_f64(int64_t batch, int64_t n, double* abar, const d
  * outputs of a failed slice are untouched.  No output may overlap an input. */
 dla_status dla_chol_chain_fwdbwd_f64(int64_t batch, int64_t n, const double* a, const double* y,
                                      double* phi, double* abar, double* ybar, int32_t* info,
-                                     void* stream);
+                                     void* ws, size_t ws_bytes, void* stream);
 dla_status dla_chol_chain_fwdbwd_f32(int64_t batch, int64_t n, const float* a, const float* y,
                                      float* phi, float* abar, float* ybar, int32_t* info,
-                                     void* stream);
+                                     void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------ GP driver */
 /* Fused RBF-kernel build and pullback for the Gaussian-process NLL driver
@@ -273,8 +306,10 @@ dla_status dla_gp_nll_assemble_f64(int64_t batch, int64_t n, const double* quad,
 dla_status dla_ml_shift_copy_f64(int64_t batch, int64_t n, const double* s, double* a, double lam,
                                  void* stream);
 dla_status dla_axpy_f64(int64_t count, double alpha, const double* x, double* y, void* stream);
+size_t dla_ml_reduce_ws_bytes(int64_t batch);
 dla_status dla_ml_reduce_f64(int64_t batch, int64_t n, const double* quad, const double* logdet,
-                             const double* abar, double lam, double* out, void* stream);
+                             const double* abar, double lam, double* out, void* ws, size_t ws_bytes,
+                             void* stream);
 
 #ifdef __cplusplus
 }

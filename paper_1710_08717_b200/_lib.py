@@ -20,31 +20,32 @@ DLA_OK = 0
 STATUS_NAMES = {0: "OK", 1: "SHAPE", 2: "NOT_SPD", 3: "SINGULAR", 4: "CONVERGENCE", 5: "ALIAS",
                 6: "ASYMMETRIC", 7: "CUDA", 8: "WORKSPACE", 9: "INVALID"}
 OPS = {"gemm": 0, "gemm2": 1, "syrk": 2, "trmm": 3, "trsm": 4, "potrf": 5, "potri": 6,
-       "sumlogdiag": 7, "gelqf": 8, "syevd": 9}
+       "sumlogdiag": 7, "gelqf": 8, "syevd": 9, "chol_chain": 10, "gesvd": 11}
+WS_BACKWARD, WS_RIGHTSIDE = 1, 2
 
 # argument kinds: P = device pointer, I = int64, F = flag (int), S = scalar (T), Z = size_t
 _SIGS = {
-    "gemm2_fwd": "IIIIPPPFFSP",
-    "gemm_fwd": "IIIIPPPFFSSP",
-    "gemm2_bwd": "IIIIPPPPPFFSP",
-    "gemm_bwd": "IIIIPPPPPFFSSP",
-    "syrk_fwd": "IIIPPFSP",
-    "syrk_bwd": "IIIPPPFSP",
-    "trmm_fwd": "IIIPPFFFSP",
-    "trmm_bwd": "IIIPPPPPFFFSP",
-    "trsm_fwd": "IIIPPFFFSPP",
-    "trsm_bwd": "IIIPPPPPFFFSP",
-    "potrf_fwd": "IIPFPP",
-    "potrf_bwd": "IIPPPFP",
-    "potri_fwd": "IIPFPP",
-    "potri_bwd": "IIPPPPFP",
-    "sumlogdiag_fwd": "IIPPP",
-    "sumlogdiag_bwd": "IIPPPFP",
+    "gemm2_fwd": "IIIIPPPFFSPZP",
+    "gemm_fwd": "IIIIPPPFFSSPZP",
+    "gemm2_bwd": "IIIIPPPPPFFSPZP",
+    "gemm_bwd": "IIIIPPPPPFFSSPZP",
+    "syrk_fwd": "IIIPPFSPZP",
+    "syrk_bwd": "IIIPPPFSPZP",
+    "trmm_fwd": "IIIPPFFFSPZP",
+    "trmm_bwd": "IIIPPPPPFFFSPZP",
+    "trsm_fwd": "IIIPPFFFSPPZP",
+    "trsm_bwd": "IIIPPPPPFFFSPZP",
+    "potrf_fwd": "IIPFPPZP",
+    "potrf_bwd": "IIPPPFPZP",
+    "potri_fwd": "IIPFPPZP",
+    "potri_bwd": "IIPPPPFPZP",
+    "sumlogdiag_fwd": "IIPPPZP",
+    "sumlogdiag_bwd": "IIPPPFPZP",
     "gelqf_fwd": "IIIPPPPZP",
     "gelqf_bwd": "IIIPPPPPPZP",
     "syevd_fwd": "IIPPPPZP",
     "syevd_bwd": "IIPPPPPSPZP",
-    "chol_chain_fwdbwd": "IIPPPPPPP",
+    "chol_chain_fwdbwd": "IIPPPPPPPZP",
 }
 
 
@@ -93,8 +94,12 @@ class _Lib:
         L.dla_ml_shift_copy_f64.restype = _int
         L.dla_axpy_f64.argtypes = [_i64, C.c_double, _vp, _vp, _vp]
         L.dla_axpy_f64.restype = _int
-        L.dla_ml_reduce_f64.argtypes = [_i64, _i64, _vp, _vp, _vp, C.c_double, _vp, _vp]
+        L.dla_ml_reduce_ws_bytes.restype = _sz
+        L.dla_ml_reduce_ws_bytes.argtypes = [_i64]
+        L.dla_ml_reduce_f64.argtypes = [_i64, _i64, _vp, _vp, _vp, C.c_double, _vp, _vp, _sz, _vp]
         L.dla_ml_reduce_f64.restype = _int
+        L.dla_potrf_inv_join_f64.argtypes = [_vp]
+        L.dla_potrf_inv_join_f64.restype = _int
         self.fns = {}
         for name, sig in _SIGS.items():
             for suffix, scal in (("f32", C.c_float), ("f64", C.c_double)):
@@ -123,7 +128,8 @@ def exported_symbols():
     names = ["dla_status_string", "dla_version", "dla_workspace_bytes", "dla_info_check",
              "dla_launch_count", "dla_prof_enable", "dla_prof_read", "dla_prof_read_max", "dla_gp_rbf_ws_bytes",
              "dla_gp_rbf_fwd_f64", "dla_gp_rbf_bwd_f64", "dla_gp_nll_assemble_f64",
-             "dla_ml_shift_copy_f64", "dla_axpy_f64", "dla_ml_reduce_f64", "dla_potrf_bwd_ws_bytes_f64",
+             "dla_ml_shift_copy_f64", "dla_axpy_f64", "dla_ml_reduce_ws_bytes", "dla_ml_reduce_f64",
+             "dla_potrf_bwd_ws_bytes_f64", "dla_potrf_inv_join_f64",
              "dla_potrf_bwd_begin_f64", "dla_potrf_bwd_end_f64", "dla_gp_potrf_inv_f64"]
     for name in _SIGS:
         for s in ("f32", "f64"):

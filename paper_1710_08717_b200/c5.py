@@ -52,6 +52,9 @@ class MarginalLikelihoods:
         self.ones = torch.ones(batch, **f)
         self.info = torch.zeros(batch, dtype=torch.int32, device=device)
         self.out = torch.empty(2, **f)  # [loss, dloss/dtheta] of this shard
+        nb = int(lib().lib.dla_ml_reduce_ws_bytes(batch))
+        self.rws = torch.empty(max(nb, 8), dtype=torch.uint8, device=device)  # reduction partials
+        self.rws_bytes = nb
 
     def _st(self):
         return C.c_void_p(torch.cuda.current_stream(self.l.device).cuda_stream)
@@ -80,7 +83,7 @@ class MarginalLikelihoods:
         L.potrf_backward_into(self.lbar, self.lbar, self.l, True)  # lbar now holds Abar
         # shard reduction: [loss, dloss/dtheta] (fixed order, on device)
         self._ok(lib_.dla_ml_reduce_f64(B, n, P(self.quad), P(self.logdet), P(self.lbar), lam, P(self.out),
-                                        self._st()))
+                                        P(self.rws), self.rws_bytes, self._st()))
         return self.out
 
     @staticmethod

@@ -2,8 +2,21 @@
 // mirrors the reference's ShapeError / alias sites, then stream-ordered
 // launches.  Backward ops follow the reference's closed-form compositions
 // (dl/adjoints.hpp) on the batched device kernels.
+//
+// Boundary contract:
+//   * ownership -- every entry point takes (ws, ws_bytes): the caller's device
+//     workspace, sized by dla_workspace_bytes(); all internal scratch is
+//     carved from it (Arena, common.cuh).  No entry point allocates.
+//   * threading -- no process-global mutable state on the compute path: the
+//     SM count and kernel attributes are per device; the fork/join side
+//     streams and events are per (device, caller stream) and locked for the
+//     enqueue (fork_res).
+#include <algorithm>
 #include <atomic>
+#include <map>
+#include <memory>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -11,22 +24,71 @@
 
 namespace dlab {
 
-Ctx make_ctx(void* stream, int32_t* info) {
-  static int sms = 0;
-  static std::once_flag flag;
-  std::call_once(flag, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
+// ------------------------------------------------------------ device state
+namespace {
+constexpr int kMaxDev = 64;
+std::atomic<int> g_sms[kMaxDev];
+}  // namespace
+
+Ctx make_ctx(void* stream, int32_t* info, Arena* arena) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int sms = (dev >= 0 && dev < kMaxDev) ? g_sms[dev].load(std::memory_order_relaxed) : 0;
+  if (sms == 0) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;  // keep scratch in the pool: no steady-state cudaMalloc
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  });
-  return Ctx{reinterpret_cast<cudaStream_t>(stream), sms, info};
+    if (dev >= 0 && dev < kMaxDev) g_sms[dev].store(sms, std::memory_order_relaxed);
+  }
+  Ctx c{reinterpret_cast<cudaStream_t>(stream), sms, info};
+  c.arena = arena;
+  return c;
 }
 
+void smem_opt_in(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = done[{dev, func}];
+  if (bytes > cur) {
+    cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cur = bytes;
+  }
+}
+
+void ForkRes::grow(int64_t steps) {
+  while ((int64_t)panel.size() < steps) {
+    cudaEvent_t a, b;
+    cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
+    panel.push_back(a);
+    done.push_back(b);
+  }
+}
+
+ForkRes& fork_res(ForkKind kind, cudaStream_t caller) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, cudaStream_t>, std::unique_ptr<ForkRes>> sets;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto& slot = sets[std::make_tuple(dev, (int)kind, caller)];
+  if (!slot) {
+    slot.reset(new ForkRes());
+    ForkRes& f = *slot;
+    // the critical chain gets the highest stream priority so that freed SMs
+    // go to its panel CTAs before the bulk update's next tiles
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&f.side, cudaStreamNonBlocking, lo);
+    cudaStreamCreateWithPriority(&f.crit, cudaStreamNonBlocking, hi);
+    f.prio_hi = hi;
+    for (auto& e : f.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  }
+  return *slot;
+}
+
+// ------------------------------------------------------- instrumentation
 static std::atomic<long long> g_launches{0};
 static std::atomic<bool> g_prof{false};
 static std::mutex g_prof_mu;
@@ -102,15 +164,15 @@ MatB<const T> C_(MatB<T> m) {
   return MatB<const T>{m.p, m.ld, m.bs};
 }
 
+// =================================================================== ops
+// Each op: validation (host, synchronous), then `<op>_run(cx, ...)` on a Ctx
+// whose arena is the caller's workspace; `ws_<op>` is the workspace mirror
+// of the same run (dla_workspace_bytes).
+
 // ------------------------------------------------------------------- gemm
 template <typename T>
-dla_status gemm_fwd(int64_t batch, int64_t m, int64_t n, int64_t k, T* c, const T* a, const T* b, int ta, int tb,
-                    T alpha, T beta, void* stream) {
-  if (batch < 0 || m < 0 || n < 0 || k < 0) return DLA_ERR_SHAPE;
-  if (overlap(c, bytes<T>(batch, m, n), a, bytes<T>(batch, m, k)) ||
-      overlap(c, bytes<T>(batch, m, n), b, bytes<T>(batch, k, n)))
-    return DLA_ERR_ALIAS;
-  Ctx cx = make_ctx(stream, nullptr);
+dla_status gemm_run(const Ctx& cx, int64_t batch, int64_t m, int64_t n, int64_t k, T* c, const T* a, const T* b,
+                    int ta, int tb, T alpha, T beta) {
   if (beta == T(0)) {  // the reference zero-fills C (gemm_accum accumulate=false)
     if (k == 0 || alpha == T(0)) {
       return cudaMemsetAsync(c, 0, bytes<T>(batch, m, n), cx.stream) == cudaSuccess ? DLA_OK : DLA_ERR_CUDA;
@@ -121,20 +183,36 @@ dla_status gemm_fwd(int64_t batch, int64_t m, int64_t n, int64_t k, T* c, const 
 }
 
 template <typename T>
-dla_status gemm_bwd(int64_t batch, int64_t m, int64_t n, int64_t k, T* abar, T* bbar, T* cbar_io, const T* a,
-                    const T* b, int ta, int tb, T alpha, T beta, bool has_c, void* stream) {
+dla_status gemm_fwd(const Ctx& cx, int64_t batch, int64_t m, int64_t n, int64_t k, T* c, const T* a, const T* b,
+                    int ta, int tb, T alpha, T beta) {
+  if (batch < 0 || m < 0 || n < 0 || k < 0) return DLA_ERR_SHAPE;
+  if (overlap(c, bytes<T>(batch, m, n), a, bytes<T>(batch, m, k)) ||
+      overlap(c, bytes<T>(batch, m, n), b, bytes<T>(batch, k, n)))
+    return DLA_ERR_ALIAS;
+  return gemm_run<T>(cx, batch, m, n, k, c, a, b, ta, tb, alpha, beta);
+}
+
+template <typename T>
+size_t ws_gemm_bwd(int64_t batch, int64_t m, int64_t n, int64_t k, int ta, int tb) {
+  size_t w = !ta ? ws_gemm<T>(batch, m, k, n) : ws_gemm<T>(batch, k, m, n);
+  w += !tb ? ws_gemm<T>(batch, k, n, m) : ws_gemm<T>(batch, n, k, m);
+  return w;
+}
+
+template <typename T>
+dla_status gemm_bwd(const Ctx& cx, int64_t batch, int64_t m, int64_t n, int64_t k, T* abar, T* bbar, T* cbar_io,
+                    const T* a, const T* b, int ta, int tb, T alpha, T beta, bool has_c) {
   if (batch < 0 || m < 0 || n < 0 || k < 0) return DLA_ERR_SHAPE;
   const size_t asz = bytes<T>(batch, m, k), bsz = bytes<T>(batch, k, n), csz = bytes<T>(batch, m, n);
   if (overlap(abar, asz, cbar_io, csz) || overlap(abar, asz, b, bsz) || overlap(bbar, bsz, cbar_io, csz) ||
       overlap(bbar, bsz, a, asz) || overlap(abar, asz, bbar, bsz))
     return DLA_ERR_ALIAS;
   // dl/adjoints.hpp:39-48
-  if (!ta) DLAB_TRY(gemm_fwd<T>(batch, m, k, n, abar, cbar_io, b, 0, !tb, alpha, T(0), stream));
-  else DLAB_TRY(gemm_fwd<T>(batch, k, m, n, abar, b, cbar_io, tb, 1, alpha, T(0), stream));
-  if (!tb) DLAB_TRY(gemm_fwd<T>(batch, k, n, m, bbar, a, cbar_io, !ta, 0, alpha, T(0), stream));
-  else DLAB_TRY(gemm_fwd<T>(batch, n, k, m, bbar, cbar_io, a, 1, ta, alpha, T(0), stream));
+  if (!ta) DLAB_TRY(gemm_run<T>(cx, batch, m, k, n, abar, cbar_io, b, 0, !tb, alpha, T(0)));
+  else DLAB_TRY(gemm_run<T>(cx, batch, k, m, n, abar, b, cbar_io, tb, 1, alpha, T(0)));
+  if (!tb) DLAB_TRY(gemm_run<T>(cx, batch, k, n, m, bbar, a, cbar_io, !ta, 0, alpha, T(0)));
+  else DLAB_TRY(gemm_run<T>(cx, batch, n, k, m, bbar, cbar_io, a, 1, ta, alpha, T(0)));
   if (has_c) {
-    Ctx cx = make_ctx(stream, nullptr);
     if (beta == T(0))
       return cudaMemsetAsync(cbar_io, 0, csz, cx.stream) == cudaSuccess ? DLA_OK : DLA_ERR_CUDA;
     return ew_scale<T>(cx, batch, m, n, pk(cbar_io, m, n), beta);
@@ -144,10 +222,14 @@ dla_status gemm_bwd(int64_t batch, int64_t m, int64_t n, int64_t k, T* abar, T* 
 
 // ------------------------------------------------------------------- syrk
 template <typename T>
-dla_status syrk_fwd(int64_t batch, int64_t n, int64_t k, T* bo, const T* a, int ta, T alpha, void* stream) {
+size_t ws_syrk_bwd(int64_t batch, int64_t n, int64_t k, int ta) {
+  return 2 * (!ta ? ws_gemm<T>(batch, n, k, n) : ws_gemm<T>(batch, k, n, n));
+}
+
+template <typename T>
+dla_status syrk_fwd(const Ctx& cx, int64_t batch, int64_t n, int64_t k, T* bo, const T* a, int ta, T alpha) {
   if (batch < 0 || n < 0 || k < 0) return DLA_ERR_SHAPE;
   if (overlap(bo, bytes<T>(batch, n, n), a, bytes<T>(batch, n, k))) return DLA_ERR_ALIAS;
-  Ctx cx = make_ctx(stream, nullptr);
   if (batch * n == 0) return DLA_OK;
   if (k == 0 || alpha == T(0))
     return cudaMemsetAsync(bo, 0, bytes<T>(batch, n, n), cx.stream) == cudaSuccess ? DLA_OK : DLA_ERR_CUDA;
@@ -157,56 +239,58 @@ dla_status syrk_fwd(int64_t batch, int64_t n, int64_t k, T* bo, const T* a, int 
 }
 
 template <typename T>
-dla_status syrk_bwd(int64_t batch, int64_t n, int64_t k, T* abar, const T* bbar, const T* a, int ta, T alpha,
-                    void* stream) {
+dla_status syrk_bwd(const Ctx& cx, int64_t batch, int64_t n, int64_t k, T* abar, const T* bbar, const T* a, int ta,
+                    T alpha) {
   if (batch < 0 || n < 0 || k < 0) return DLA_ERR_SHAPE;
   const size_t asz = bytes<T>(batch, n, k);
   if (overlap(abar, asz, bbar, bytes<T>(batch, n, n)) || overlap(abar, asz, a, asz)) return DLA_ERR_ALIAS;
   // dl/adjoints.hpp:71-77
   if (!ta) {
-    DLAB_TRY(gemm_fwd<T>(batch, n, k, n, abar, bbar, a, 0, 0, alpha, T(0), stream));
-    DLAB_TRY(gemm_fwd<T>(batch, n, k, n, abar, bbar, a, 1, 0, alpha, T(1), stream));
+    DLAB_TRY(gemm_run<T>(cx, batch, n, k, n, abar, bbar, a, 0, 0, alpha, T(0)));
+    DLAB_TRY(gemm_run<T>(cx, batch, n, k, n, abar, bbar, a, 1, 0, alpha, T(1)));
   } else {
-    DLAB_TRY(gemm_fwd<T>(batch, k, n, n, abar, a, bbar, 0, 0, alpha, T(0), stream));
-    DLAB_TRY(gemm_fwd<T>(batch, k, n, n, abar, a, bbar, 0, 1, alpha, T(1), stream));
+    DLAB_TRY(gemm_run<T>(cx, batch, k, n, n, abar, a, bbar, 0, 0, alpha, T(0)));
+    DLAB_TRY(gemm_run<T>(cx, batch, k, n, n, abar, a, bbar, 0, 1, alpha, T(1)));
   }
   return DLA_OK;
 }
 
 // ------------------------------------------------------------ trmm / trsm
 template <typename T>
-dla_status trmm_fwd(int64_t batch, int64_t m, int64_t n, const T* t, T* x, int right, int trans, int lower,
-                    T alpha, void* stream) {
+dla_status trmm_fwd(const Ctx& cx, int64_t batch, int64_t m, int64_t n, const T* t, T* x, int right, int trans,
+                    int lower, T alpha) {
   if (bad_dims(batch, m, n)) return DLA_ERR_SHAPE;
   const int64_t nt = right ? n : m;
   if (overlap(x, bytes<T>(batch, m, n), t, bytes<T>(batch, nt, nt))) return DLA_ERR_ALIAS;
-  Ctx cx = make_ctx(stream, nullptr);
   return trmm<T>(cx, batch, m, n, cpk(t, nt, nt), pk(x, m, n), right, trans, lower, alpha);
 }
 
 template <typename T>
-dla_status trsm_fwd(int64_t batch, int64_t m, int64_t n, const T* t, T* x, int right, int trans, int lower,
-                    T alpha, int32_t* info, void* stream) {
+dla_status trsm_fwd(const Ctx& cx, int64_t batch, int64_t m, int64_t n, const T* t, T* x, int right, int trans,
+                    int lower, T alpha) {
   if (bad_dims(batch, m, n)) return DLA_ERR_SHAPE;
   const int64_t nt = right ? n : m;
   if (overlap(x, bytes<T>(batch, m, n), t, bytes<T>(batch, nt, nt))) return DLA_ERR_ALIAS;
-  Ctx cx = make_ctx(stream, info);
   DLAB_TRY(reset_info(cx, batch));
   return trsm<T>(cx, batch, m, n, cpk(t, nt, nt), pk(x, m, n), right, trans, lower, alpha, /*check_diag*/ true);
 }
 
 template <typename T>
-dla_status trmm_bwd(int64_t batch, int64_t m, int64_t n, T* abar, T* tbar, const T* bbar, const T* t, const T* a,
-                    int right, int trans, int lower, T alpha, void* stream) {
+size_t ws_trmm_bwd(int64_t batch, int64_t m, int64_t n, int right) {
+  return (right ? ws_gemm<T>(batch, n, n, m) : ws_gemm<T>(batch, m, m, n)) + ws_trmm<T>(batch, m, n, right);
+}
+
+template <typename T>
+dla_status trmm_bwd(const Ctx& cx, int64_t batch, int64_t m, int64_t n, T* abar, T* tbar, const T* bbar,
+                    const T* t, const T* a, int right, int trans, int lower, T alpha) {
   if (bad_dims(batch, m, n)) return DLA_ERR_SHAPE;
   const int64_t nt = right ? n : m;
   const size_t xsz = bytes<T>(batch, m, n), tsz = bytes<T>(batch, nt, nt);
   if (overlap(tbar, tsz, bbar, xsz) || overlap(tbar, tsz, a, xsz) || overlap(abar, xsz, t, tsz) ||
       overlap(abar, xsz, tbar, tsz) || (abar != bbar && overlap(abar, xsz, bbar, xsz)))
     return DLA_ERR_ALIAS;
-  Ctx cx = make_ctx(stream, nullptr);
   if (batch * m * n == 0) {
-    if (batch * nt > 0) cudaMemsetAsync(tbar, 0, tsz, cx.stream);
+    if (batch * nt > 0 && cudaMemsetAsync(tbar, 0, tsz, cx.stream) != cudaSuccess) return DLA_ERR_CUDA;
     return DLA_OK;
   }
   MatB<T> tb = pk(tbar, nt, nt);
@@ -223,8 +307,13 @@ dla_status trmm_bwd(int64_t batch, int64_t m, int64_t n, T* abar, T* tbar, const
 }
 
 template <typename T>
-dla_status trsm_bwd(int64_t batch, int64_t m, int64_t n, T* abar, T* tbar, const T* bbar, const T* t, const T* b,
-                    int right, int trans, int lower, T alpha, void* stream) {
+size_t ws_trsm_bwd(int64_t batch, int64_t m, int64_t n, int right) {
+  return ws_trsm<T>(batch, m, n, right) + (right ? ws_gemm<T>(batch, n, n, m) : ws_gemm<T>(batch, m, m, n));
+}
+
+template <typename T>
+dla_status trsm_bwd(const Ctx& cx, int64_t batch, int64_t m, int64_t n, T* abar, T* tbar, const T* bbar,
+                    const T* t, const T* b, int right, int trans, int lower, T alpha) {
   if (bad_dims(batch, m, n)) return DLA_ERR_SHAPE;
   const int64_t nt = right ? n : m;
   const size_t xsz = bytes<T>(batch, m, n), tsz = bytes<T>(batch, nt, nt);
@@ -232,9 +321,8 @@ dla_status trsm_bwd(int64_t batch, int64_t m, int64_t n, T* abar, T* tbar, const
       overlap(abar, xsz, tbar, tsz) || overlap(abar, xsz, b, xsz) ||
       (abar != bbar && overlap(abar, xsz, bbar, xsz)))
     return DLA_ERR_ALIAS;
-  Ctx cx = make_ctx(stream, nullptr);
   if (batch * m * n == 0) {
-    if (batch * nt > 0) cudaMemsetAsync(tbar, 0, tsz, cx.stream);
+    if (batch * nt > 0 && cudaMemsetAsync(tbar, 0, tsz, cx.stream) != cudaSuccess) return DLA_ERR_CUDA;
     return DLA_OK;
   }
   // dl/adjoints.hpp:136-152: S = op(T)^{-T} Bbar in abar, then Tbar, then alpha.
@@ -257,24 +345,34 @@ dla_status trsm_bwd(int64_t batch, int64_t m, int64_t n, T* abar, T* tbar, const
 
 // ------------------------------------------------------------ potrf / potri
 template <typename T>
-dla_status potrf_fwd(int64_t batch, int64_t n, T* a, int lower, int32_t* info, void* stream) {
+size_t ws_potrf_fwd(int64_t batch, int64_t n) {
+  return potrf_small_eligible<T>(n) ? 0 : ws_potrf_lower<T>(batch, n);
+}
+
+template <typename T>
+dla_status potrf_fwd(const Ctx& cx, int64_t batch, int64_t n, T* a, int lower) {
   if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
-  Ctx cx = make_ctx(stream, info);
   DLAB_TRY(reset_info(cx, batch));
   if (batch * n == 0) return DLA_OK;
   if (potrf_small_eligible<T>(n)) return potrf_small<T>(cx, batch, n, pk(a, n, n), lower);
-  DLAB_TRY(check_symmetric<T>(cx, batch, n, cpk(a, n, n), info));
+  DLAB_TRY(check_symmetric<T>(cx, batch, n, cpk(a, n, n), cx.info));
   DLAB_TRY(potrf_lower<T>(cx, batch, n, pk(a, n, n)));
-  if (!lower) DLAB_TRY(ew_square<T>(cx, batch, n, pk(a, n, n), /*transpose*/ 5, T(1), info));
+  if (!lower) DLAB_TRY(ew_square<T>(cx, batch, n, pk(a, n, n), /*transpose*/ 5, T(1), cx.info));
   return DLA_OK;
 }
 
 template <typename T>
-dla_status potrf_bwd(int64_t batch, int64_t n, T* abar, const T* lbar, const T* l, int lower, void* stream) {
+size_t ws_potrf_bwd(int64_t batch, int64_t n) {
+  if (batch * n == 0 || potrf_small_eligible<T>(n)) return 0;
+  if (inv_eligible<T>(n)) return ws_potrf_bwd_inv<T>(batch, n);
+  return ws_trmm<T>(batch, n, n, false) + ws_trsm<T>(batch, n, n, false) + ws_trsm<T>(batch, n, n, true);
+}
+
+template <typename T>
+dla_status potrf_bwd(const Ctx& cx, int64_t batch, int64_t n, T* abar, const T* lbar, const T* l, int lower) {
   if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
   const size_t sz = bytes<T>(batch, n, n);
   if (overlap(abar, sz, l, sz) || (abar != lbar && overlap(abar, sz, lbar, sz))) return DLA_ERR_ALIAS;
-  Ctx cx = make_ctx(stream, nullptr);
   if (batch * n == 0) return DLA_OK;
   if (potrf_small_eligible<T>(n)) return potrf_bwd_small<T>(cx, batch, n, pk(abar, n, n), cpk(lbar, n, n),
                                                             cpk(l, n, n), lower);
@@ -297,32 +395,34 @@ dla_status potrf_bwd(int64_t batch, int64_t n, T* abar, const T* lbar, const T* 
 }
 
 template <typename T>
-dla_status potri_fwd(int64_t batch, int64_t n, T* a, int lower, int32_t* info, void* stream) {
+dla_status potri_fwd(const Ctx& cx, int64_t batch, int64_t n, T* a, int lower) {
   if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
-  Ctx cx = make_ctx(stream, info);
   DLAB_TRY(reset_info(cx, batch));
   if (batch * n == 0) return DLA_OK;
   MatB<T> av = pk(a, n, n);
   if (!lower) DLAB_TRY(ew_square<T>(cx, batch, n, av, /*transpose*/ 5));
-  DLAB_TRY(check_zero_diag<T>(cx, batch, n, C_(av), info));
+  DLAB_TRY(check_zero_diag<T>(cx, batch, n, C_(av), cx.info));
   return potri_lower<T>(cx, batch, n, av);
 }
 
 template <typename T>
-dla_status potri_bwd(int64_t batch, int64_t n, T* lbar, const T* bbar, const T* l, const T* b, int lower,
-                     void* stream) {
+size_t ws_potri_bwd(int64_t batch, int64_t n, int lower) {
+  return carve_bound(bytes<T>(batch, n, n)) + ws_gemm<T>(batch, n, n, n) + ws_trsm<T>(batch, n, n, lower != 0);
+}
+
+template <typename T>
+dla_status potri_bwd(const Ctx& cx, int64_t batch, int64_t n, T* lbar, const T* bbar, const T* l, const T* b,
+                     int lower) {
   if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
   const size_t sz = bytes<T>(batch, n, n);
   if (overlap(lbar, sz, bbar, sz) || overlap(lbar, sz, l, sz) || overlap(lbar, sz, b, sz)) return DLA_ERR_ALIAS;
-  Ctx cx = make_ctx(stream, nullptr);
   if (batch * n == 0) return DLA_OK;
   MatB<T> lb = pk(lbar, n, n);
   MatB<const T> bv = cpk(b, n, n), bb = cpk(bbar, n, n), lv = cpk(l, n, n);
   // The reference forms B Bbar + B Bbar^T as two accumulated products
   // (dl/adjoints.hpp:211-212); here Bbar + Bbar^T is formed once (one n^2
   // pass) and multiplied once: half the O(n^3) work, same value.
-  Scratch ws(bytes<T>(batch, n, n), cx.stream);
-  if (!ws.p) return DLA_ERR_CUDA;
+  DLAB_SCRATCH(ws, cx, bytes<T>(batch, n, n));
   MatB<T> sb = pk(ws.as<T>(), n, n);
   DLAB_TRY(ew_add_transpose<T>(cx, batch, n, bb, sb));
   if (lower) {  // dl/adjoints.hpp:211-215
@@ -338,47 +438,53 @@ dla_status potri_bwd(int64_t batch, int64_t n, T* lbar, const T* bbar, const T* 
 
 // ------------------------------------------------------------- sumlogdiag
 template <typename T>
-dla_status sld_fwd(int64_t batch, int64_t n, T* out, const T* a, void* stream) {
+dla_status sld_fwd(const Ctx& cx, int64_t batch, int64_t n, T* out, const T* a) {
   if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
-  Ctx cx = make_ctx(stream, nullptr);
   return sumlogdiag_fwd<T>(cx, batch, n, out, cpk(a, n, n));
 }
 
 template <typename T>
-dla_status sld_bwd(int64_t batch, int64_t n, T* abar, const T* g, const T* a, int accumulate, void* stream) {
+dla_status sld_bwd(const Ctx& cx, int64_t batch, int64_t n, T* abar, const T* g, const T* a, int accumulate) {
   if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
   const size_t sz = bytes<T>(batch, n, n);
   if (overlap(abar, sz, a, sz)) return DLA_ERR_ALIAS;
-  Ctx cx = make_ctx(stream, nullptr);
   return sumlogdiag_bwd<T>(cx, batch, n, pk(abar, n, n), g, cpk(a, n, n), accumulate != 0);
 }
 
 // --------------------------------------------------------------- gelqf
 template <typename T>
-dla_status gelqf_fwd_abi(int64_t batch, int64_t m, int64_t n, T* q, T* l, int32_t* info, void* ws, size_t wsb,
-                         void* stream) {
-  if (bad_dims(batch, m, n) || m > n) return DLA_ERR_SHAPE;
-  if (overlap(q, bytes<T>(batch, m, n), l, bytes<T>(batch, m, m))) return DLA_ERR_ALIAS;
-  Ctx cx = make_ctx(stream, info);
-  DLAB_TRY(reset_info(cx, batch));
-  if (batch * m == 0) return DLA_OK;
-  if (wsb < gelqf_ws_bytes<T>(batch, m, n, false)) return DLA_ERR_WORKSPACE;
-  return gelqf_fwd<T>(cx, batch, m, n, q, l, ws);
+size_t ws_gelqf_fwd(int64_t batch, int64_t m, int64_t n) {
+  // the panel GEMMs of gelqf_blocked have N or K = 32: never on the carving route
+  return carve_bound(gelqf_ws_bytes<T>(batch, m, n, false));
 }
 
 template <typename T>
-dla_status gelqf_bwd_abi(int64_t batch, int64_t m, int64_t n, T* abar, const T* qbar, const T* lbar, const T* q,
-                         const T* l, void* ws, size_t wsb, void* stream) {
+dla_status gelqf_fwd_abi(const Ctx& cx, int64_t batch, int64_t m, int64_t n, T* q, T* l) {
+  if (bad_dims(batch, m, n) || m > n) return DLA_ERR_SHAPE;
+  if (overlap(q, bytes<T>(batch, m, n), l, bytes<T>(batch, m, m))) return DLA_ERR_ALIAS;
+  DLAB_TRY(reset_info(cx, batch));
+  if (batch * m == 0) return DLA_OK;
+  DLAB_SCRATCH(ws, cx, gelqf_ws_bytes<T>(batch, m, n, false));
+  return gelqf_fwd<T>(cx, batch, m, n, q, l, ws.p);
+}
+
+template <typename T>
+size_t ws_gelqf_bwd(int64_t batch, int64_t m, int64_t n) {
+  return carve_bound(gelqf_ws_bytes<T>(batch, m, n, true)) + ws_trmm<T>(batch, m, m, false) +
+         ws_gemm<T>(batch, m, m, n) + ws_gemm<T>(batch, m, n, m) + ws_trsm<T>(batch, m, n, false);
+}
+
+template <typename T>
+dla_status gelqf_bwd_abi(const Ctx& cx, int64_t batch, int64_t m, int64_t n, T* abar, const T* qbar, const T* lbar,
+                         const T* q, const T* l) {
   if (bad_dims(batch, m, n) || m > n) return DLA_ERR_SHAPE;
   const size_t asz = bytes<T>(batch, m, n);
   if (overlap(abar, asz, q, asz) || overlap(abar, asz, l, bytes<T>(batch, m, m)) ||
       overlap(abar, asz, lbar, bytes<T>(batch, m, m)) || (abar != qbar && overlap(abar, asz, qbar, asz)))
     return DLA_ERR_ALIAS;
-  Ctx cx = make_ctx(stream, nullptr);
   if (batch * m == 0) return DLA_OK;
-  if (wsb < gelqf_ws_bytes<T>(batch, m, n, true) || !ws) return DLA_ERR_WORKSPACE;
-  T* w = static_cast<T*>(ws);
-  MatB<T> wv = pk(w, m, m);
+  DLAB_SCRATCH(ws, cx, gelqf_ws_bytes<T>(batch, m, n, true));
+  MatB<T> wv = pk(ws.as<T>(), m, m);
   MatB<const T> lv = cpk(l, m, m), qv = cpk(q, m, n);
   // dl/adjoints.hpp:243-251
   DLAB_TRY(ew_copy<T>(cx, batch, m, m, cpk(lbar, m, m), wv));
@@ -392,28 +498,30 @@ dla_status gelqf_bwd_abi(int64_t batch, int64_t m, int64_t n, T* abar, const T* 
 
 // --------------------------------------------------------------- syevd
 template <typename T>
-dla_status syevd_fwd_abi(int64_t batch, int64_t n, T* u, T* lambda, int32_t* info, void* ws, size_t wsb,
-                         void* stream) {
+dla_status syevd_fwd_abi(const Ctx& cx, int64_t batch, int64_t n, T* u, T* lambda) {
   if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
   if (overlap(u, bytes<T>(batch, n, n), lambda, bytes<T>(batch, n, 1))) return DLA_ERR_ALIAS;
-  Ctx cx = make_ctx(stream, info);
   DLAB_TRY(reset_info(cx, batch));
   if (batch * n == 0) return DLA_OK;
-  if (wsb < syevd_ws_bytes<T>(batch, n, false)) return DLA_ERR_WORKSPACE;
-  return syevd_fwd<T>(cx, batch, n, u, lambda, ws);
+  DLAB_SCRATCH(ws, cx, syevd_ws_bytes<T>(batch, n, false));
+  return syevd_fwd<T>(cx, batch, n, u, lambda, ws.p);
 }
 
 template <typename T>
-dla_status syevd_bwd_abi(int64_t batch, int64_t n, T* abar, const T* ubar, const T* lambdabar, const T* u,
-                         const T* lambda, T eps_gap, void* ws, size_t wsb, void* stream) {
+size_t ws_syevd_bwd(int64_t batch, int64_t n) {
+  return carve_bound(syevd_ws_bytes<T>(batch, n, true)) + 3 * ws_gemm<T>(batch, n, n, n);
+}
+
+template <typename T>
+dla_status syevd_bwd_abi(const Ctx& cx, int64_t batch, int64_t n, T* abar, const T* ubar, const T* lambdabar,
+                         const T* u, const T* lambda, T eps_gap) {
   if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
   const size_t sz = bytes<T>(batch, n, n);
   if (overlap(abar, sz, ubar, sz) || overlap(abar, sz, u, sz)) return DLA_ERR_ALIAS;
   if (!(eps_gap > T(0))) return DLA_ERR_INVALID;
-  Ctx cx = make_ctx(stream, nullptr);
   if (batch * n == 0) return DLA_OK;
-  if (wsb < syevd_ws_bytes<T>(batch, n, true) || !ws) return DLA_ERR_WORKSPACE;
-  MatB<T> w = pk(static_cast<T*>(ws), n, n);
+  DLAB_SCRATCH(ws, cx, syevd_ws_bytes<T>(batch, n, true));
+  MatB<T> w = pk(ws.as<T>(), n, n);
   MatB<const T> uv = cpk(u, n, n);
   // dl/adjoints.hpp:277-294
   DLAB_TRY(gemm<T>(cx, batch, n, n, n, T(1), cpk(ubar, n, n), false, uv, true, T(0), w));
@@ -423,11 +531,6 @@ dla_status syevd_bwd_abi(int64_t batch, int64_t n, T* abar, const T* ubar, const
   return ew_sym_into<T>(cx, batch, n, C_(w), pk(abar, n, n));
 }
 
-}  // namespace
-}  // namespace dlab
-
-using namespace dlab;
-
 // ------------------------------------------------- fused C1 chain (GP NLL)
 __global__ void k_fill_ones(int64_t n, double* pd, float* pf) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -436,25 +539,31 @@ __global__ void k_fill_ones(int64_t n, double* pd, float* pf) {
   }
 }
 
+template <typename T>
+size_t ws_chol_chain(int64_t batch, int64_t n) {
+  if (n <= 32) return 0;
+  return carve_bound(bytes<T>(batch, n, n) + bytes<T>(batch, n, 1) + bytes<T>(batch, 1, 1)) +
+         ws_potrf_fwd<T>(batch, n) + ws_trsm<T>(batch, n, 1, false) + ws_gemm<T>(batch, 1, 1, n) +
+         ws_trsm_bwd<T>(batch, n, 1, 0) + ws_potrf_bwd<T>(batch, n);
+}
+
 // phi = 1/2 |L^-1 y|^2 + sumlogdiag(L), L = potrf(A); ybar, Abar at phibar = 1.
 // n <= 32: one fused warp-per-matrix launch (small.cu); otherwise the
-// operator chain (the reference's own composition) on stream-ordered scratch.
+// operator chain (the reference's own composition) on workspace scratch.
 template <typename T>
-dla_status chol_chain_abi(int64_t batch, int64_t n, const T* a, const T* y, T* phi, T* abar, T* ybar,
-                          int32_t* info, void* stream) {
+dla_status chol_chain_abi(const Ctx& cx, int64_t batch, int64_t n, const T* a, const T* y, T* phi, T* abar,
+                          T* ybar) {
   if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
   const size_t asz = bytes<T>(batch, n, n), ysz = bytes<T>(batch, n, 1), psz = bytes<T>(batch, 1, 1);
   if (overlap(abar, asz, a, asz) || overlap(abar, asz, y, ysz) || overlap(ybar, ysz, a, asz) ||
       overlap(ybar, ysz, y, ysz) || overlap(phi, psz, a, asz) || overlap(phi, psz, y, ysz) ||
       overlap(abar, asz, ybar, ysz) || overlap(phi, psz, abar, asz) || overlap(phi, psz, ybar, ysz))
     return DLA_ERR_ALIAS;
-  Ctx cx = make_ctx(stream, info);
   DLAB_TRY(reset_info(cx, batch));
   if (batch == 0) return DLA_OK;
   if (n == 0) return cudaMemsetAsync(phi, 0, psz, cx.stream) == cudaSuccess ? DLA_OK : DLA_ERR_CUDA;
   if (n <= 32) return chol_chain_small<T>(cx, batch, n, cpk(a, n, n), y, phi, pk(abar, n, n), ybar);
-  Scratch ws(asz + ysz + psz, cx.stream);
-  if (!ws.p) return DLA_ERR_CUDA;
+  DLAB_SCRATCH(ws, cx, asz + ysz + psz);
   T* l = ws.as<T>();
   T* z = l + batch * n * n;
   T* ones = z + batch * n;
@@ -464,38 +573,29 @@ dla_status chol_chain_abi(int64_t batch, int64_t n, const T* a, const T* y, T* p
   if (cudaMemcpyAsync(l, a, asz, cudaMemcpyDeviceToDevice, cx.stream) != cudaSuccess ||
       cudaMemcpyAsync(z, y, ysz, cudaMemcpyDeviceToDevice, cx.stream) != cudaSuccess)
     return DLA_ERR_CUDA;
-  DLAB_TRY(potrf_fwd<T>(batch, n, l, 1, info, stream));
+  DLAB_TRY(potrf_fwd<T>(cx, batch, n, l, 1));
   // later ops skip failed slices through info (dl/matrix.hpp:232-239 semantics)
   DLAB_TRY(trsm<T>(cx, batch, n, 1, cpk(l, n, n), pk(z, n, 1), false, false, true, T(1)));
   DLAB_TRY(sumlogdiag_fwd<T>(cx, batch, n, phi, cpk(l, n, n)));
   DLAB_TRY(gemm<T>(cx, batch, 1, 1, n, T(0.5), cpk(z, n, 1), true, cpk(z, n, 1), false, T(1), pk(phi, 1, 1)));
-  DLAB_TRY(trsm_bwd<T>(batch, n, 1, ybar, abar, z, l, z, 0, 0, 1, T(1), stream));
-  DLAB_TRY(sumlogdiag_bwd<T>(cx, batch, n, pk(abar, n, n), ones, cpk(l, n, n), true));
-  return potrf_bwd<T>(batch, n, abar, abar, l, 1, stream);
+  Ctx nx = cx;
+  nx.info = nullptr;  // the pullbacks do not report (the reference's backward never throws here)
+  DLAB_TRY(trsm_bwd<T>(nx, batch, n, 1, ybar, abar, z, l, z, 0, 0, 1, T(1)));
+  DLAB_TRY(sumlogdiag_bwd<T>(nx, batch, n, pk(abar, n, n), ones, cpk(l, n, n), true));
+  return potrf_bwd<T>(nx, batch, n, abar, abar, l, 1);
 }
 
 // ------------------------------------------- split potrf pullback (drivers)
 // L^{-1} for the inverse-based potrf pullback computed on a side stream
-// forked from the caller's stream, so a driver can overlap it with work
-// that only needs L (the GP driver's solves).  One begin/end pair in flight
-// per process; both halves are stream-ordered and graph-capturable.
-struct InvFork {
-  cudaStream_t side = nullptr;
-  cudaEvent_t fork = nullptr, done = nullptr;
-  static InvFork& get() {
-    static InvFork f;
-    static std::once_flag once;
-    std::call_once(once, [] {
-      int lo = 0, hi = 0;
-      cudaDeviceGetStreamPriorityRange(&lo, &hi);
-      cudaStreamCreateWithPriority(&f.side, cudaStreamNonBlocking, lo);
-      cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming);
-      cudaEventCreateWithFlags(&f.done, cudaEventDisableTiming);
-    });
-    return f;
-  }
-};
-
+// forked from the caller's stream (fork_res(FORK_INV, stream)), so a driver
+// can overlap it with work that only needs L (the GP driver's solves).  One
+// begin/end pair in flight per (device, caller stream); both halves are
+// stream-ordered and graph-capturable.  Events: ev[0] fork, ev[1] done,
+// ev[2] mid (early-inverse hook), ev[3] fin.
+//
+// Workspace layout (the same in every call of the pair): the explicit
+// inverse region is the FIRST carve of a fresh arena, then the call's own
+// nested scratch.
 template <typename T>
 size_t potrf_inv_ws(int64_t batch, int64_t n) {
   // wi (n^2) | tt (n^2) | tmp (trtri_levels_tmp(n) bytes) | tmp2 (trtri_levels_tmp(n / 2) bytes)
@@ -504,36 +604,51 @@ size_t potrf_inv_ws(int64_t batch, int64_t n) {
 }
 
 template <typename T>
-dla_status potrf_bwd_begin(int64_t batch, int64_t n, const T* l, int lower, void* ws, size_t wsb, void* stream) {
-  if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
-  if (batch * n == 0 || !inv_eligible<T>(n)) return DLA_OK;  // end() takes the direct path
-  if (!ws || wsb < potrf_inv_ws<T>(batch, n)) return DLA_ERR_WORKSPACE;
-  Ctx cx = make_ctx(stream, nullptr);
-  InvFork& f = InvFork::get();
-  Ctx side = cx;
-  side.stream = f.side;
-  cudaEventRecord(f.fork, cx.stream);
-  cudaStreamWaitEvent(f.side, f.fork, 0);
-  T* wp = static_cast<T*>(ws);
-  DLAB_TRY(potrf_inv_prepare<T>(side, batch, n, cpk(l, n, n), lower != 0, pk(wp, n, n), wp + 2 * batch * n * n));
-  cudaEventRecord(f.done, f.side);
-  return DLA_OK;
+size_t ws_potrf_split(int64_t batch, int64_t n) {
+  if (batch * n == 0) return 0;
+  if (!inv_eligible<T>(n)) return std::max(ws_potrf_fwd<T>(batch, n), ws_potrf_bwd<T>(batch, n));
+  const int64_t h = n / 2;
+  const size_t gp = ws_potrf_lower<T>(batch, n) + ws_trtri_levels<T>(batch, h) * 2 + 2 * ws_gemm<T>(batch, h, h, h);
+  const size_t begin = ws_potrf_inv_prepare<T>(batch, n);
+  const size_t end = ws_potrf_bwd_tail<T>(batch, n);
+  return carve_bound(potrf_inv_ws<T>(batch, n)) + std::max(gp, std::max(begin, end));
 }
 
 template <typename T>
-dla_status potrf_bwd_end(int64_t batch, int64_t n, T* abar, const T* lbar, const T* l, int lower, void* ws,
-                         size_t wsb, void* stream) {
+dla_status potrf_bwd_begin(const Ctx& cx, int64_t batch, int64_t n, const T* l, int lower) {
   if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
-  if (batch * n == 0 || !inv_eligible<T>(n)) return potrf_bwd<T>(batch, n, abar, lbar, l, lower, stream);
+  if (batch * n == 0 || !inv_eligible<T>(n)) return DLA_OK;  // end() takes the direct path
+  DLAB_SCRATCH(inv, cx, potrf_inv_ws<T>(batch, n));
+  ForkRes& f = fork_res(FORK_INV, cx.stream);
+  std::lock_guard<std::mutex> lk(f.mu);
+  Ctx side = cx;
+  side.stream = f.side;
+  cudaEventRecord(f.ev[0], cx.stream);
+  cudaStreamWaitEvent(f.side, f.ev[0], 0);
+  T* wp = inv.as<T>();
+  const dla_status st =
+      potrf_inv_prepare<T>(side, batch, n, cpk(l, n, n), lower != 0, pk(wp, n, n), wp + 2 * batch * n * n);
+  cudaEventRecord(f.ev[1], f.side);
+  return st;
+}
+
+template <typename T>
+dla_status potrf_bwd_end(const Ctx& cx, int64_t batch, int64_t n, T* abar, const T* lbar, const T* l, int lower) {
+  if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
+  if (batch * n == 0 || !inv_eligible<T>(n)) return potrf_bwd<T>(cx, batch, n, abar, lbar, l, lower);
   const size_t sz = bytes<T>(batch, n, n);
   if (overlap(abar, sz, l, sz) || (abar != lbar && overlap(abar, sz, lbar, sz))) return DLA_ERR_ALIAS;
-  if (!ws || wsb < potrf_inv_ws<T>(batch, n)) return DLA_ERR_WORKSPACE;
-  Ctx cx = make_ctx(stream, nullptr);
-  T* wp = static_cast<T*>(ws);
+  DLAB_SCRATCH(inv, cx, potrf_inv_ws<T>(batch, n));
+  T* wp = inv.as<T>();
   MatB<T> tt = pk(wp + batch * n * n, n, n);
   // P' needs only L and Lbar: it overlaps the inverse still running on the side stream
-  DLAB_TRY(potrf_bwd_phi<T>(cx, batch, n, cpk(lbar, n, n), cpk(l, n, n), lower != 0, tt));
-  cudaStreamWaitEvent(cx.stream, InvFork::get().done, 0);
+  const dla_status st = potrf_bwd_phi<T>(cx, batch, n, cpk(lbar, n, n), cpk(l, n, n), lower != 0, tt);
+  ForkRes& f = fork_res(FORK_INV, cx.stream);
+  {
+    std::lock_guard<std::mutex> lk(f.mu);
+    cudaStreamWaitEvent(cx.stream, f.ev[1], 0);
+  }
+  if (st != DLA_OK) return st;
   return potrf_bwd_finish<T>(cx, batch, n, pk(abar, n, n), cpk(wp, n, n), tt);
 }
 
@@ -549,9 +664,10 @@ struct EarlyInv {
   int64_t batch, n;
   const T* l;
   T* wp;
-  cudaStream_t side;
+  Ctx side;
   cudaEvent_t ev;
   bool fired;
+  dla_status st;
 };
 
 template <typename T>
@@ -560,68 +676,112 @@ void early_inv_first(void* user, cudaStream_t crit) {
   e.fired = true;
   const int64_t n = e.n, h = n / 2, B = e.batch;
   cudaEventRecord(e.ev, crit);
-  cudaStreamWaitEvent(e.side, e.ev, 0);
-  Ctx sc = make_ctx(e.side, nullptr);
+  cudaStreamWaitEvent(e.side.stream, e.ev, 0);
+  const Ctx& sc = e.side;
   MatB<T> wi{e.wp, n, n * n};
   T* tmp = e.wp + 2 * B * n * n;
   MatB<const T> lv{e.l, n, n * n};
   // W11 = tril(L11), W21 = L21; L11^{-1} in place; T1 = W21 W11^{-1} into tmp
-  if (ew_tri_copy<T>(sc, B, h, lv, wi, false) != DLA_OK) return;
-  if (ew_copy<T>(sc, B, h, h, MatB<const T>{e.l + h * n, n, n * n}, wi.sub(h, 0)) != DLA_OK) return;
+  dla_status st = ew_tri_copy<T>(sc, B, h, lv, wi, false);
+  if (st == DLA_OK) st = ew_copy<T>(sc, B, h, h, MatB<const T>{e.l + h * n, n, n * n}, wi.sub(h, 0));
   T* tmp2 = tmp + B * (trtri_levels_tmp<T>(n) / sizeof(T));
-  if (trtri_levels<T>(sc, B, h, wi, tmp2) != DLA_OK) return;
+  if (st == DLA_OK) st = trtri_levels<T>(sc, B, h, wi, tmp2);
   MatB<T> t1{tmp, h, h * h};
-  gemm<T>(sc, B, h, h, h, T(1), MatB<const T>{wi.p + h * n, n, n * n}, false, MatB<const T>{wi.p, n, n * n}, false,
-          T(0), t1, MASK_FULL, nullptr, TRI_NONE, TRI_LOWER);
+  if (st == DLA_OK)
+    st = gemm<T>(sc, B, h, h, h, T(1), MatB<const T>{wi.p + h * n, n, n * n}, false, MatB<const T>{wi.p, n, n * n},
+                 false, T(0), t1, MASK_FULL, nullptr, TRI_NONE, TRI_LOWER);
+  e.st = st;
 }
 
 template <typename T>
-dla_status gp_potrf_inv(int64_t batch, int64_t n, T* a, int32_t* info, void* ws, size_t wsb, void* stream) {
+dla_status gp_potrf_inv(const Ctx& cx, int64_t batch, int64_t n, T* a) {
   if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
   if (!inv_eligible<T>(n) || batch * n == 0) {  // no early path: factorization, then the plain begin
-    DLAB_TRY(potrf_fwd<T>(batch, n, a, 1, info, stream));
-    return potrf_bwd_begin<T>(batch, n, a, 1, ws, wsb, stream);
+    DLAB_TRY(potrf_fwd<T>(cx, batch, n, a, 1));
+    return potrf_bwd_begin<T>(cx, batch, n, a, 1);
   }
-  if (!ws || wsb < potrf_inv_ws<T>(batch, n)) return DLA_ERR_WORKSPACE;
-  Ctx cx = make_ctx(stream, info);
+  DLAB_SCRATCH(inv, cx, potrf_inv_ws<T>(batch, n));
   DLAB_TRY(reset_info(cx, batch));
-  DLAB_TRY(check_symmetric<T>(cx, batch, n, cpk(a, n, n), info));
-  InvFork& f = InvFork::get();
-  static cudaEvent_t mid = nullptr, fin = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaEventCreateWithFlags(&mid, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&fin, cudaEventDisableTiming);
-  });
-  EarlyInv<T> e{batch, n, a, static_cast<T*>(ws), f.side, mid, false};
+  DLAB_TRY(check_symmetric<T>(cx, batch, n, cpk(a, n, n), cx.info));
+  ForkRes& f = fork_res(FORK_INV, cx.stream);
+  std::lock_guard<std::mutex> lk(f.mu);
+  Ctx sc = cx;
+  sc.stream = f.side;
+  sc.info = nullptr;
+  EarlyInv<T> e{batch, n, a, inv.as<T>(), sc, f.ev[2], false, DLA_OK};
   PotrfHook hook{n / 2, early_inv_first<T>, &e, a, n};
   Ctx hc = cx;
   hc.potrf_hook = &hook;
-  DLAB_TRY(potrf_lower<T>(hc, batch, n, pk(a, n, n), /*zero_upper*/ false));
+  const dla_status sf = potrf_lower<T>(hc, batch, n, pk(a, n, n), /*zero_upper*/ false);
   if (!e.fired) early_inv_first<T>(&e, cx.stream);  // a schedule without the hook point (tuning modes)
   const int64_t h = n / 2;
-  T* wp = static_cast<T*>(ws);
+  T* wp = inv.as<T>();
   MatB<T> wi{wp, n, n * n};
   T* tmp = wp + 2 * batch * n * n;
   T* tmp2 = tmp + batch * (trtri_levels_tmp<T>(n) / sizeof(T));
-  cudaEventRecord(fin, cx.stream);
-  cudaStreamWaitEvent(f.side, fin, 0);
-  Ctx sc = make_ctx(f.side, nullptr);
+  cudaEventRecord(f.ev[3], cx.stream);
+  cudaStreamWaitEvent(f.side, f.ev[3], 0);
+  dla_status st = e.st;
   // W22 = tril(L22); L22^{-1} in place; W21 = -W22^{-1} T1
-  DLAB_TRY(ew_tri_copy<T>(sc, batch, h, MatB<const T>{a + h * n + h, n, n * n}, wi.sub(h, h), false));
-  DLAB_TRY(trtri_levels<T>(sc, batch, h, wi.sub(h, h), tmp2));
-  DLAB_TRY(gemm<T>(sc, batch, h, h, h, T(-1), MatB<const T>{wi.p + h * n + h, n, n * n}, false,
-                   MatB<const T>{tmp, h, h * h}, false, T(0), wi.sub(h, 0), MASK_FULL, nullptr, TRI_LOWER,
-                   TRI_NONE));
+  if (st == DLA_OK)
+    st = ew_tri_copy<T>(sc, batch, h, MatB<const T>{a + h * n + h, n, n * n}, wi.sub(h, h), false);
+  if (st == DLA_OK) st = trtri_levels<T>(sc, batch, h, wi.sub(h, h), tmp2);
+  if (st == DLA_OK)
+    st = gemm<T>(sc, batch, h, h, h, T(-1), MatB<const T>{wi.p + h * n + h, n, n * n}, false,
+                 MatB<const T>{tmp, h, h * h}, false, T(0), wi.sub(h, 0), MASK_FULL, nullptr, TRI_LOWER, TRI_NONE);
   // L's strict upper triangle (the potrf contract) is zeroed here, on the side
-  // stream: no kernel of the step reads it, so it stays off the critical path
-  // and is complete once dla_potrf_bwd_end_f64 has joined `done`
-  DLAB_TRY(ew_square<T>(sc, batch, n, pk(a, n, n), /*tril*/ 0, T(1), info));
-  cudaEventRecord(f.done, f.side);
-  return DLA_OK;
+  // stream: no kernel of the step reads it, so it stays off the critical path.
+  // It is complete once dla_potrf_bwd_end_f64 (or dla_potrf_inv_join_f64)
+  // has been enqueued on the caller's stream.
+  if (st == DLA_OK) {
+    Ctx zc = sc;
+    zc.info = cx.info;
+    st = ew_square<T>(zc, batch, n, pk(a, n, n), /*tril*/ 0, T(1), cx.info);
+  }
+  cudaEventRecord(f.ev[1], f.side);
+  return sf != DLA_OK ? sf : st;
 }
 
+// ------------------------------------------------------ workspace query
+template <typename T>
+size_t ws_query(dla_op op, int64_t batch, int64_t m, int64_t n, int64_t k, int phase) {
+  const bool bwd = (phase & DLA_WS_BACKWARD) != 0, right = (phase & DLA_WS_RIGHTSIDE) != 0;
+  switch (op) {
+    case DLA_OP_GEMM:
+    case DLA_OP_GEMM2: {
+      if (!bwd) return ws_gemm<T>(batch, m, n, k);
+      size_t w = 0;  // the operand transposes are not part of the query: the largest of the four
+      for (int ta = 0; ta < 2; ++ta)
+        for (int tb = 0; tb < 2; ++tb) w = std::max(w, ws_gemm_bwd<T>(batch, m, n, k, ta, tb));
+      return w;
+    }
+    case DLA_OP_SYRK:
+      return !bwd ? ws_gemm<T>(batch, n, n, k) : std::max(ws_syrk_bwd<T>(batch, n, k, 0), ws_syrk_bwd<T>(batch, n, k, 1));
+    case DLA_OP_TRMM:
+      return !bwd ? ws_trmm<T>(batch, m, n, right) : ws_trmm_bwd<T>(batch, m, n, right);
+    case DLA_OP_TRSM:
+      return !bwd ? ws_trsm<T>(batch, m, n, right) : ws_trsm_bwd<T>(batch, m, n, right);
+    case DLA_OP_POTRF:
+      return !bwd ? ws_potrf_fwd<T>(batch, n) : ws_potrf_bwd<T>(batch, n);
+    case DLA_OP_POTRI:
+      return !bwd ? ws_potri_lower<T>(batch, n) : std::max(ws_potri_bwd<T>(batch, n, 1), ws_potri_bwd<T>(batch, n, 0));
+    case DLA_OP_SUMLOGDIAG:
+      return 0;
+    case DLA_OP_GELQF:
+      if (m > n) return 0;  // ShapeError (the op reports it)
+      return !bwd ? ws_gelqf_fwd<T>(batch, m, n) : ws_gelqf_bwd<T>(batch, m, n);
+    case DLA_OP_SYEVD:
+      return !bwd ? carve_bound(syevd_ws_bytes<T>(batch, n, false)) : ws_syevd_bwd<T>(batch, n);
+    case DLA_OP_CHOL_CHAIN:
+      return ws_chol_chain<T>(batch, n);
+  }
+  return 0;
+}
 
+}  // namespace
+}  // namespace dlab
+
+using namespace dlab;
 
 extern "C" {
 
@@ -693,13 +853,8 @@ long long dla_prof_read_max(double* ms, double* flops) {
 }
 
 size_t dla_workspace_bytes(dla_op op, dla_dtype dtype, int64_t batch, int64_t m, int64_t n, int64_t k, int phase) {
-  (void)k;
-  const bool bwd = (phase & DLA_WS_BACKWARD) != 0;
-  if (op == DLA_OP_GELQF)
-    return dtype == DLA_F64 ? gelqf_ws_bytes<double>(batch, m, n, bwd) : gelqf_ws_bytes<float>(batch, m, n, bwd);
-  if (op == DLA_OP_SYEVD)
-    return dtype == DLA_F64 ? syevd_ws_bytes<double>(batch, n, bwd) : syevd_ws_bytes<float>(batch, n, bwd);
-  return 0;
+  if (batch < 0 || m < 0 || n < 0 || k < 0) return 0;
+  return dtype == DLA_F64 ? ws_query<double>(op, batch, m, n, k, phase) : ws_query<float>(op, batch, m, n, k, phase);
 }
 
 dla_status dla_info_check(const int32_t* info, int64_t batch, void* stream, int64_t* first_bad, int64_t* index) {
@@ -720,112 +875,177 @@ dla_status dla_info_check(const int32_t* info, int64_t batch, void* stream, int6
   return DLA_OK;
 }
 
+#define DLA_ARENA(ws, wsb, stream, info) \
+  Arena arena_(ws, wsb);                  \
+  const Ctx cx = make_ctx(stream, info, &arena_)
+
+// A short workspace is refused before any launch (outputs untouched); a
+// negative dimension skips the check so the op reports DLA_ERR_SHAPE.
+#define DLA_NEED(T, op, batch, m, n, k, phase)                                                        \
+  do {                                                                                                \
+    if ((batch) >= 0 && (m) >= 0 && (n) >= 0 && (k) >= 0 &&                                          \
+        (ws == nullptr ? (size_t)0 : wsb) < ws_query<T>(op, batch, m, n, k, phase))                  \
+      return DLA_ERR_WORKSPACE;                                                                       \
+  } while (0)
+
 #define DLA_DEFINE(T, S)                                                                                          \
   dla_status dla_gemm2_fwd_##S(int64_t batch, int64_t m, int64_t n, int64_t k, T* c, const T* a, const T* b,      \
-                               int ta, int tb, T alpha, void* stream) {                                          \
-    return gemm_fwd<T>(batch, m, n, k, c, a, b, ta, tb, alpha, T(0), stream);                                    \
+                               int ta, int tb, T alpha, void* ws, size_t wsb, void* stream) {                    \
+    DLA_NEED(T, DLA_OP_GEMM, batch, m, n, k, 0);                                                                  \
+    DLA_ARENA(ws, wsb, stream, nullptr);                                                                          \
+    return gemm_fwd<T>(cx, batch, m, n, k, c, a, b, ta, tb, alpha, T(0));                                        \
   }                                                                                                               \
   dla_status dla_gemm_fwd_##S(int64_t batch, int64_t m, int64_t n, int64_t k, T* c, const T* a, const T* b,       \
-                              int ta, int tb, T alpha, T beta, void* stream) {                                   \
-    return gemm_fwd<T>(batch, m, n, k, c, a, b, ta, tb, alpha, beta, stream);                                    \
+                              int ta, int tb, T alpha, T beta, void* ws, size_t wsb, void* stream) {             \
+    DLA_NEED(T, DLA_OP_GEMM, batch, m, n, k, 0);                                                                  \
+    DLA_ARENA(ws, wsb, stream, nullptr);                                                                          \
+    return gemm_fwd<T>(cx, batch, m, n, k, c, a, b, ta, tb, alpha, beta);                                        \
   }                                                                                                               \
   dla_status dla_gemm2_bwd_##S(int64_t batch, int64_t m, int64_t n, int64_t k, T* abar, T* bbar, const T* cbar,   \
-                               const T* a, const T* b, int ta, int tb, T alpha, void* stream) {                  \
-    return gemm_bwd<T>(batch, m, n, k, abar, bbar, const_cast<T*>(cbar), a, b, ta, tb, alpha, T(0), false,       \
-                       stream);                                                                                   \
+                               const T* a, const T* b, int ta, int tb, T alpha, void* ws, size_t wsb,            \
+                               void* stream) {                                                                    \
+    DLA_NEED(T, DLA_OP_GEMM, batch, m, n, k, DLA_WS_BACKWARD);                                                    \
+    DLA_ARENA(ws, wsb, stream, nullptr);                                                                          \
+    return gemm_bwd<T>(cx, batch, m, n, k, abar, bbar, const_cast<T*>(cbar), a, b, ta, tb, alpha, T(0), false);  \
   }                                                                                                               \
   dla_status dla_gemm_bwd_##S(int64_t batch, int64_t m, int64_t n, int64_t k, T* abar, T* bbar, T* cbar_io,       \
-                              const T* a, const T* b, int ta, int tb, T alpha, T beta, void* stream) {           \
-    return gemm_bwd<T>(batch, m, n, k, abar, bbar, cbar_io, a, b, ta, tb, alpha, beta, true, stream);            \
-  }                                                                                                               \
-  dla_status dla_syrk_fwd_##S(int64_t batch, int64_t n, int64_t k, T* b, const T* a, int ta, T alpha,             \
+                              const T* a, const T* b, int ta, int tb, T alpha, T beta, void* ws, size_t wsb,     \
                               void* stream) {                                                                     \
-    return syrk_fwd<T>(batch, n, k, b, a, ta, alpha, stream);                                                     \
+    DLA_NEED(T, DLA_OP_GEMM, batch, m, n, k, DLA_WS_BACKWARD);                                                    \
+    DLA_ARENA(ws, wsb, stream, nullptr);                                                                          \
+    return gemm_bwd<T>(cx, batch, m, n, k, abar, bbar, cbar_io, a, b, ta, tb, alpha, beta, true);                \
+  }                                                                                                               \
+  dla_status dla_syrk_fwd_##S(int64_t batch, int64_t n, int64_t k, T* b, const T* a, int ta, T alpha, void* ws,   \
+                              size_t wsb, void* stream) {                                                         \
+    DLA_NEED(T, DLA_OP_SYRK, batch, 0, n, k, 0);                                                                  \
+    DLA_ARENA(ws, wsb, stream, nullptr);                                                                          \
+    return syrk_fwd<T>(cx, batch, n, k, b, a, ta, alpha);                                                         \
   }                                                                                                               \
   dla_status dla_syrk_bwd_##S(int64_t batch, int64_t n, int64_t k, T* abar, const T* bbar, const T* a, int ta,    \
-                              T alpha, void* stream) {                                                            \
-    return syrk_bwd<T>(batch, n, k, abar, bbar, a, ta, alpha, stream);                                            \
+                              T alpha, void* ws, size_t wsb, void* stream) {                                      \
+    DLA_NEED(T, DLA_OP_SYRK, batch, 0, n, k, DLA_WS_BACKWARD);                                                    \
+    DLA_ARENA(ws, wsb, stream, nullptr);                                                                          \
+    return syrk_bwd<T>(cx, batch, n, k, abar, bbar, a, ta, alpha);                                                \
   }                                                                                                               \
   dla_status dla_trmm_fwd_##S(int64_t batch, int64_t m, int64_t n, const T* t, T* x, int r, int tr, int lo,       \
-                              T alpha, void* stream) {                                                            \
-    return trmm_fwd<T>(batch, m, n, t, x, r, tr, lo, alpha, stream);                                              \
+                              T alpha, void* ws, size_t wsb, void* stream) {                                      \
+    DLA_NEED(T, DLA_OP_TRMM, batch, m, n, 0, r ? DLA_WS_RIGHTSIDE : 0);                                           \
+    DLA_ARENA(ws, wsb, stream, nullptr);                                                                          \
+    return trmm_fwd<T>(cx, batch, m, n, t, x, r, tr, lo, alpha);                                                  \
   }                                                                                                               \
   dla_status dla_trmm_bwd_##S(int64_t batch, int64_t m, int64_t n, T* abar, T* tbar, const T* bbar, const T* t,   \
-                              const T* a, int r, int tr, int lo, T alpha, void* stream) {                        \
-    return trmm_bwd<T>(batch, m, n, abar, tbar, bbar, t, a, r, tr, lo, alpha, stream);                            \
+                              const T* a, int r, int tr, int lo, T alpha, void* ws, size_t wsb, void* stream) {  \
+    DLA_NEED(T, DLA_OP_TRMM, batch, m, n, 0, DLA_WS_BACKWARD | (r ? DLA_WS_RIGHTSIDE : 0));                       \
+    DLA_ARENA(ws, wsb, stream, nullptr);                                                                          \
+    return trmm_bwd<T>(cx, batch, m, n, abar, tbar, bbar, t, a, r, tr, lo, alpha);                                \
   }                                                                                                               \
   dla_status dla_trsm_fwd_##S(int64_t batch, int64_t m, int64_t n, const T* t, T* x, int r, int tr, int lo,       \
-                              T alpha, int32_t* info, void* stream) {                                             \
-    return trsm_fwd<T>(batch, m, n, t, x, r, tr, lo, alpha, info, stream);                                        \
+                              T alpha, int32_t* info, void* ws, size_t wsb, void* stream) {                       \
+    DLA_NEED(T, DLA_OP_TRSM, batch, m, n, 0, r ? DLA_WS_RIGHTSIDE : 0);                                           \
+    DLA_ARENA(ws, wsb, stream, info);                                                                             \
+    return trsm_fwd<T>(cx, batch, m, n, t, x, r, tr, lo, alpha);                                                  \
   }                                                                                                               \
   dla_status dla_trsm_bwd_##S(int64_t batch, int64_t m, int64_t n, T* abar, T* tbar, const T* bbar, const T* t,   \
-                              const T* b, int r, int tr, int lo, T alpha, void* stream) {                        \
-    return trsm_bwd<T>(batch, m, n, abar, tbar, bbar, t, b, r, tr, lo, alpha, stream);                            \
+                              const T* b, int r, int tr, int lo, T alpha, void* ws, size_t wsb, void* stream) {  \
+    DLA_NEED(T, DLA_OP_TRSM, batch, m, n, 0, DLA_WS_BACKWARD | (r ? DLA_WS_RIGHTSIDE : 0));                       \
+    DLA_ARENA(ws, wsb, stream, nullptr);                                                                          \
+    return trsm_bwd<T>(cx, batch, m, n, abar, tbar, bbar, t, b, r, tr, lo, alpha);                                \
   }                                                                                                               \
-  dla_status dla_potrf_fwd_##S(int64_t batch, int64_t n, T* a, int lower, int32_t* info, void* stream) {         \
-    return potrf_fwd<T>(batch, n, a, lower, info, stream);                                                        \
+  dla_status dla_potrf_fwd_##S(int64_t batch, int64_t n, T* a, int lower, int32_t* info, void* ws, size_t wsb,    \
+                               void* stream) {                                                                    \
+    DLA_NEED(T, DLA_OP_POTRF, batch, n, n, 0, 0);                                                                 \
+    DLA_ARENA(ws, wsb, stream, info);                                                                             \
+    return potrf_fwd<T>(cx, batch, n, a, lower);                                                                  \
   }                                                                                                               \
   dla_status dla_potrf_bwd_##S(int64_t batch, int64_t n, T* abar, const T* lbar, const T* l, int lower,           \
-                               void* stream) {                                                                    \
-    return potrf_bwd<T>(batch, n, abar, lbar, l, lower, stream);                                                  \
+                               void* ws, size_t wsb, void* stream) {                                              \
+    DLA_NEED(T, DLA_OP_POTRF, batch, n, n, 0, DLA_WS_BACKWARD);                                                   \
+    DLA_ARENA(ws, wsb, stream, nullptr);                                                                          \
+    return potrf_bwd<T>(cx, batch, n, abar, lbar, l, lower);                                                      \
   }                                                                                                               \
-  dla_status dla_potri_fwd_##S(int64_t batch, int64_t n, T* a, int lower, int32_t* info, void* stream) {         \
-    return potri_fwd<T>(batch, n, a, lower, info, stream);                                                        \
+  dla_status dla_potri_fwd_##S(int64_t batch, int64_t n, T* a, int lower, int32_t* info, void* ws, size_t wsb,    \
+                               void* stream) {                                                                    \
+    DLA_NEED(T, DLA_OP_POTRI, batch, n, n, 0, 0);                                                                 \
+    DLA_ARENA(ws, wsb, stream, info);                                                                             \
+    return potri_fwd<T>(cx, batch, n, a, lower);                                                                  \
   }                                                                                                               \
   dla_status dla_potri_bwd_##S(int64_t batch, int64_t n, T* lbar, const T* bbar, const T* l, const T* b,          \
-                               int lower, void* stream) {                                                         \
-    return potri_bwd<T>(batch, n, lbar, bbar, l, b, lower, stream);                                              \
+                               int lower, void* ws, size_t wsb, void* stream) {                                   \
+    DLA_NEED(T, DLA_OP_POTRI, batch, n, n, 0, DLA_WS_BACKWARD);                                                   \
+    DLA_ARENA(ws, wsb, stream, nullptr);                                                                          \
+    return potri_bwd<T>(cx, batch, n, lbar, bbar, l, b, lower);                                                   \
   }                                                                                                               \
-  dla_status dla_sumlogdiag_fwd_##S(int64_t batch, int64_t n, T* out, const T* a, void* stream) {                \
-    return sld_fwd<T>(batch, n, out, a, stream);                                                                  \
+  dla_status dla_sumlogdiag_fwd_##S(int64_t batch, int64_t n, T* out, const T* a, void* ws, size_t wsb,           \
+                                    void* stream) {                                                               \
+    DLA_ARENA(ws, wsb, stream, nullptr);                                                                          \
+    return sld_fwd<T>(cx, batch, n, out, a);                                                                      \
   }                                                                                                               \
   dla_status dla_sumlogdiag_bwd_##S(int64_t batch, int64_t n, T* abar, const T* gbar, const T* a,                 \
-                                    int accumulate, void* stream) {                                               \
-    return sld_bwd<T>(batch, n, abar, gbar, a, accumulate, stream);                                               \
+                                    int accumulate, void* ws, size_t wsb, void* stream) {                         \
+    DLA_ARENA(ws, wsb, stream, nullptr);                                                                          \
+    return sld_bwd<T>(cx, batch, n, abar, gbar, a, accumulate);                                                   \
   }                                                                                                               \
   dla_status dla_gelqf_fwd_##S(int64_t batch, int64_t m, int64_t n, T* q, T* l, int32_t* info, void* ws,         \
-                               size_t ws_bytes, void* stream) {                                                   \
-    return gelqf_fwd_abi<T>(batch, m, n, q, l, info, ws, ws_bytes, stream);                                       \
+                               size_t wsb, void* stream) {                                                        \
+    DLA_NEED(T, DLA_OP_GELQF, batch, m, n, 0, 0);                                                                 \
+    DLA_ARENA(ws, wsb, stream, info);                                                                             \
+    return gelqf_fwd_abi<T>(cx, batch, m, n, q, l);                                                               \
   }                                                                                                               \
   dla_status dla_gelqf_bwd_##S(int64_t batch, int64_t m, int64_t n, T* abar, const T* qbar, const T* lbar,        \
-                               const T* q, const T* l, void* ws, size_t ws_bytes, void* stream) {                \
-    return gelqf_bwd_abi<T>(batch, m, n, abar, qbar, lbar, q, l, ws, ws_bytes, stream);                           \
+                               const T* q, const T* l, void* ws, size_t wsb, void* stream) {                      \
+    DLA_NEED(T, DLA_OP_GELQF, batch, m, n, 0, DLA_WS_BACKWARD);                                                   \
+    DLA_ARENA(ws, wsb, stream, nullptr);                                                                          \
+    return gelqf_bwd_abi<T>(cx, batch, m, n, abar, qbar, lbar, q, l);                                             \
   }                                                                                                               \
   dla_status dla_syevd_fwd_##S(int64_t batch, int64_t n, T* u, T* lambda, int32_t* info, void* ws,               \
-                               size_t ws_bytes, void* stream) {                                                   \
-    return syevd_fwd_abi<T>(batch, n, u, lambda, info, ws, ws_bytes, stream);                                     \
+                               size_t wsb, void* stream) {                                                        \
+    DLA_NEED(T, DLA_OP_SYEVD, batch, n, n, 0, 0);                                                                 \
+    DLA_ARENA(ws, wsb, stream, info);                                                                             \
+    return syevd_fwd_abi<T>(cx, batch, n, u, lambda);                                                             \
   }                                                                                                               \
   dla_status dla_syevd_bwd_##S(int64_t batch, int64_t n, T* abar, const T* ubar, const T* lambdabar, const T* u,  \
-                               const T* lambda, T eps_gap, void* ws, size_t ws_bytes, void* stream) {            \
-    return syevd_bwd_abi<T>(batch, n, abar, ubar, lambdabar, u, lambda, eps_gap, ws, ws_bytes, stream);           \
+                               const T* lambda, T eps_gap, void* ws, size_t wsb, void* stream) {                  \
+    DLA_NEED(T, DLA_OP_SYEVD, batch, n, n, 0, DLA_WS_BACKWARD);                                                   \
+    DLA_ARENA(ws, wsb, stream, nullptr);                                                                          \
+    return syevd_bwd_abi<T>(cx, batch, n, abar, ubar, lambdabar, u, lambda, eps_gap);                             \
+  }                                                                                                               \
+  dla_status dla_chol_chain_fwdbwd_##S(int64_t batch, int64_t n, const T* a, const T* y, T* phi, T* abar,         \
+                                       T* ybar, int32_t* info, void* ws, size_t wsb, void* stream) {              \
+    DLA_NEED(T, DLA_OP_CHOL_CHAIN, batch, n, n, 0, 0);                                                            \
+    DLA_ARENA(ws, wsb, stream, info);                                                                             \
+    return chol_chain_abi<T>(cx, batch, n, a, y, phi, abar, ybar);                                                \
   }
 
 DLA_DEFINE(float, f32)
 DLA_DEFINE(double, f64)
 
 size_t dla_potrf_bwd_ws_bytes_f64(int64_t batch, int64_t n) {
-  return inv_eligible<double>(n) ? potrf_inv_ws<double>(batch, n) : 0;
+  if (batch < 0 || n < 0) return 0;
+  return ws_potrf_split<double>(batch, n);
 }
 dla_status dla_gp_potrf_inv_f64(int64_t batch, int64_t n, double* a, int32_t* info, void* ws, size_t ws_bytes,
                                 void* stream) {
-  return gp_potrf_inv<double>(batch, n, a, info, ws, ws_bytes, stream);
+  if (batch >= 0 && n >= 0 && (ws ? ws_bytes : 0) < ws_potrf_split<double>(batch, n)) return DLA_ERR_WORKSPACE;
+  DLA_ARENA(ws, ws_bytes, stream, info);
+  return gp_potrf_inv<double>(cx, batch, n, a);
 }
 dla_status dla_potrf_bwd_begin_f64(int64_t batch, int64_t n, const double* l, int lower, void* ws, size_t ws_bytes,
                                    void* stream) {
-  return potrf_bwd_begin<double>(batch, n, l, lower, ws, ws_bytes, stream);
+  if (batch >= 0 && n >= 0 && (ws ? ws_bytes : 0) < ws_potrf_split<double>(batch, n)) return DLA_ERR_WORKSPACE;
+  DLA_ARENA(ws, ws_bytes, stream, nullptr);
+  return potrf_bwd_begin<double>(cx, batch, n, l, lower);
 }
 dla_status dla_potrf_bwd_end_f64(int64_t batch, int64_t n, double* abar, const double* lbar, const double* l,
                                  int lower, void* ws, size_t ws_bytes, void* stream) {
-  return potrf_bwd_end<double>(batch, n, abar, lbar, l, lower, ws, ws_bytes, stream);
+  if (batch >= 0 && n >= 0 && (ws ? ws_bytes : 0) < ws_potrf_split<double>(batch, n)) return DLA_ERR_WORKSPACE;
+  DLA_ARENA(ws, ws_bytes, stream, nullptr);
+  return potrf_bwd_end<double>(cx, batch, n, abar, lbar, l, lower);
 }
-
-dla_status dla_chol_chain_fwdbwd_f64(int64_t batch, int64_t n, const double* a, const double* y, double* phi,
-                                     double* abar, double* ybar, int32_t* info, void* stream) {
-  return chol_chain_abi<double>(batch, n, a, y, phi, abar, ybar, info, stream);
-}
-dla_status dla_chol_chain_fwdbwd_f32(int64_t batch, int64_t n, const float* a, const float* y, float* phi,
-                                     float* abar, float* ybar, int32_t* info, void* stream) {
-  return chol_chain_abi<float>(batch, n, a, y, phi, abar, ybar, info, stream);
+dla_status dla_potrf_inv_join_f64(void* stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  ForkRes& f = fork_res(FORK_INV, s);
+  std::lock_guard<std::mutex> lk(f.mu);
+  return cudaStreamWaitEvent(s, f.ev[1], 0) == cudaSuccess ? DLA_OK : DLA_ERR_CUDA;
 }
 
 }  // extern "C"

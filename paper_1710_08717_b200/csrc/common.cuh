@@ -5,6 +5,8 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <mutex>
+#include <vector>
 
 #include "../../include/dla.h"
 
@@ -54,7 +56,37 @@ struct PotrfHook {
   int64_t n;      // whole matrix (a recursive schedule's sub-blocks are not final at `col`)
 };
 
-// Launch context: stream + device properties + optional per-slice info.
+// Caller-owned device workspace (include/dla.h: "no entry point allocates
+// device memory").  One top-level C-ABI call carves it monotonically -- no
+// region is reused within the call, so scratch handed to work on a forked
+// side stream stays valid until the call joins that stream back.  The bytes
+// a call needs are computed host-side by the ws_* mirrors (ws.cu) of the same
+// dispatch; carve_bound() is the per-carve bound they use (size rounded up
+// to the 256-byte carve alignment plus the worst-case alignment skip).
+constexpr size_t kCarveAlign = 256;
+constexpr size_t carve_bound(size_t bytes) {
+  return bytes ? (bytes + kCarveAlign - 1) / kCarveAlign * kCarveAlign + kCarveAlign : 0;
+}
+
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0;
+  size_t off = 0;
+  Arena() = default;
+  Arena(void* p, size_t bytes) : base(static_cast<char*>(p)), cap(p ? bytes : 0) {}
+  void* take(size_t bytes) {
+    if (!bytes) return nullptr;
+    const uintptr_t cur = reinterpret_cast<uintptr_t>(base) + off;
+    const uintptr_t al = (cur + kCarveAlign - 1) / kCarveAlign * kCarveAlign;
+    const size_t need = (size_t)(al - reinterpret_cast<uintptr_t>(base)) + bytes;
+    if (!base || need > cap) return nullptr;
+    off = need;
+    return reinterpret_cast<void*>(al);
+  }
+};
+
+// Launch context: stream + device properties + optional per-slice info +
+// the call's workspace arena.
 struct Ctx {
   cudaStream_t stream;
   int sms;
@@ -62,9 +94,37 @@ struct Ctx {
   int gemm_ctas = 0;   // > 0: DMMA GEMMs run persistent on at most this many CTAs
   int gemm_rowtile = 0;  // 1: (f64, m <= 128) one 128-row tile per column block, so C may alias op(B)
   const PotrfHook* potrf_hook = nullptr;
+  Arena* arena = nullptr;  // the call's workspace (shared by every copy of this Ctx)
 };
 
-Ctx make_ctx(void* stream, int32_t* info);
+// SM count of the CURRENT device (cached per device, read-only after first use).
+Ctx make_ctx(void* stream, int32_t* info, Arena* arena = nullptr);
+
+// Dynamic shared-memory opt-in of a kernel on the current device: thread-safe,
+// set once per (device, kernel) and raised if a larger size is requested.
+void smem_opt_in(const void* func, size_t bytes);
+template <typename K>
+inline void ensure_smem_attr(K* kernel, size_t bytes) {
+  smem_opt_in(reinterpret_cast<const void*>(kernel), bytes);
+}
+
+// Side streams + events for the fork/join schedules, one set per (device,
+// caller stream, user): concurrent calls on different streams (or devices)
+// never share an event, and a caller holds `mu` for its whole enqueue, so
+// two host threads on one stream serialise instead of re-recording each
+// other's events.  Created on first use, owned by the library, read-only
+// thereafter except for the lock.
+enum ForkKind : int { FORK_LOOKAHEAD = 0, FORK_INV = 1, FORK_BWDINV = 2 };
+struct ForkRes {
+  std::mutex mu;
+  cudaStream_t side = nullptr;  // lowest priority
+  cudaStream_t crit = nullptr;  // highest priority (the potrf panel chain)
+  int prio_hi = 0;
+  cudaEvent_t ev[6] = {};
+  std::vector<cudaEvent_t> panel, done;  // per look-ahead step (grown under mu)
+  void grow(int64_t steps);
+};
+ForkRes& fork_res(ForkKind kind, cudaStream_t caller);
 
 // Host-side count of kernels this library launched (bench.py's gpu_launches
 // claim) and optional CUDA-event timing of every GEMM launch (roofline).
@@ -73,17 +133,16 @@ bool gemm_prof_on();
 void gemm_prof_begin(cudaStream_t s);
 void gemm_prof_end(cudaStream_t s, double flops);
 
-// Stream-ordered scratch from the device's default memory pool (release
-// threshold raised in make_ctx, so steady state never reaches cudaMalloc;
-// capturable into CUDA graphs as mem-alloc nodes).
+// Scratch carved from the call's workspace arena; `ok` is false when the
+// caller's workspace is missing or too small (the op returns
+// DLA_ERR_WORKSPACE -- there is no hidden allocation behind it).
 struct Scratch {
   void* p = nullptr;
-  cudaStream_t s;
-  Scratch(size_t bytes, cudaStream_t st) : s(st) {
-    if (bytes && cudaMallocAsync(&p, bytes, s) != cudaSuccess) p = nullptr;
-  }
-  ~Scratch() {
-    if (p) cudaFreeAsync(p, s);
+  bool ok = true;
+  Scratch(const Ctx& c, size_t bytes) {
+    if (!bytes) return;
+    p = c.arena ? c.arena->take(bytes) : nullptr;
+    ok = p != nullptr;
   }
   Scratch(const Scratch&) = delete;
   Scratch& operator=(const Scratch&) = delete;
@@ -92,6 +151,10 @@ struct Scratch {
     return static_cast<T*>(p);
   }
 };
+
+#define DLAB_SCRATCH(name, ctx, bytes) \
+  Scratch name((ctx), (bytes));        \
+  if (!name.ok) return DLA_ERR_WORKSPACE
 
 inline unsigned blocks_for(int64_t work, int threads, int64_t cap = 148 * 32) {
   int64_t b = (work + threads - 1) / threads;
@@ -155,6 +218,17 @@ struct Num<float> {
     note_launch(1);                                          \
   } while (0)
 
+// Status of the kernel launch just issued (counts it on success).
+inline dla_status launch_status() {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "dla_b200: %s\n", cudaGetErrorString(e));
+    return DLA_ERR_CUDA;
+  }
+  note_launch(1);
+  return DLA_OK;
+}
+
 #define DLAB_TRY(expr)              \
   do {                              \
     dla_status s_ = (expr);         \
@@ -186,6 +260,21 @@ bool sgemm_tc(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, floa
 template <typename T>
 bool gemm_skinny(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T alpha, MatB<const T> a, bool ta,
                  MatB<const T> b, bool tb, T beta, MatB<T> cm, int mask, const int32_t* skip, dla_status* st);
+
+// Workspace mirrors: the bytes (carve_bound per carve, summed over the call
+// tree) each routine takes from its Ctx's arena, computed host-side from the
+// same shapes and eligibility tests as the dispatch (no device needed).
+template <typename T>
+size_t ws_gemm(int64_t batch, int64_t m, int64_t n, int64_t k, int64_t inner = 1);
+size_t sgemm_tc_ws_bytes(int64_t batch, int64_t m, int64_t n, int64_t k);
+template <typename T>
+size_t ws_trsm(int64_t batch, int64_t m, int64_t n, bool right);
+template <typename T>
+size_t ws_trmm(int64_t batch, int64_t m, int64_t n, bool right);
+template <typename T>
+size_t ws_potrf_lower(int64_t batch, int64_t n);
+template <typename T>
+size_t ws_potri_lower(int64_t batch, int64_t n);
 
 // elementwise.cu
 template <typename T>

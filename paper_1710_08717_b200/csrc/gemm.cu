@@ -484,11 +484,6 @@ __global__ void __launch_bounds__(256) sgemm_ffma(GemmArgs<float> g) {
     for (int j = 0; j < 4; ++j) store_c<float>(g, tc.C, m0 + ty + 16 * i, n0 + tx + 16 * j, acc[i][j]);
 }
 
-template <typename K>
-void ensure_smem(K k, size_t smem) {
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-}
-
 template <typename T, bool TA, bool TB, int VA, int VB>
 cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large, int max_ctas, bool rowtile) {
   auto grid = [&](int64_t tiles) {
@@ -502,11 +497,7 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large, 
       g.tiles_n = (g.n + C::BN - 1) / C::BN;
       const size_t smem = sizeof(T) * STAGES * (ATile<C::BM, C::BK, TA>::ELEMS + BTile<C::BN, C::BK, TB>::ELEMS);
       auto k = dgemm_dmma<C, TA, TB, VA, VB>;
-      static bool attr = false;
-      if (!attr) {
-        ensure_smem(k, smem);
-        attr = true;
-      }
+      ensure_smem_attr(k, smem);
       const unsigned nb = grid(slabs * g.tiles_m * g.tiles_n);
       k<<<nb, C::NT, smem, s>>>(g);
     } else if (rowtile || (large && (g.k <= DLAB_SHORTK || g.mask != MASK_FULL || g.tri_a != TRI_NONE ||
@@ -516,11 +507,7 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large, 
       g.tiles_n = (g.n + C::BN - 1) / C::BN;
       const size_t smem = sizeof(T) * STAGES * (ATile<C::BM, C::BK, TA>::ELEMS + BTile<C::BN, C::BK, TB>::ELEMS);
       auto k = dgemm_dmma<C, TA, TB, VA, VB>;
-      static bool attr = false;
-      if (!attr) {
-        ensure_smem(k, smem);
-        attr = true;
-      }
+      ensure_smem_attr(k, smem);
       const unsigned nb = grid(slabs * g.tiles_m * g.tiles_n);
       k<<<nb, C::NT, smem, s>>>(g);
     } else if (large) {
@@ -529,11 +516,7 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large, 
       g.tiles_n = (g.n + C::BN - 1) / C::BN;
       const size_t smem = sizeof(T) * STAGES * (ATile<C::BM, C::BK, TA>::ELEMS + BTile<C::BN, C::BK, TB>::ELEMS);
       auto k = dgemm_dmma<C, TA, TB, VA, VB>;
-      static bool attr = false;
-      if (!attr) {
-        ensure_smem(k, smem);
-        attr = true;
-      }
+      ensure_smem_attr(k, smem);
       const unsigned nb = grid(slabs * g.tiles_m * g.tiles_n);
       k<<<nb, C::NT, smem, s>>>(g);
     } else {
@@ -542,11 +525,7 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large, 
       g.tiles_n = (g.n + C::BN - 1) / C::BN;
       const size_t smem = sizeof(T) * STAGES * (ATile<C::BM, C::BK, TA>::ELEMS + BTile<C::BN, C::BK, TB>::ELEMS);
       auto k = dgemm_dmma<C, TA, TB, VA, VB>;
-      static bool attr = false;
-      if (!attr) {
-        ensure_smem(k, smem);
-        attr = true;
-      }
+      ensure_smem_attr(k, smem);
       const unsigned nb = grid(slabs * g.tiles_m * g.tiles_n);
       k<<<nb, C::NT, smem, s>>>(g);
     }
@@ -556,11 +535,7 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large, 
     g.tiles_n = (g.n + 63) / 64;
     const size_t smem = sizeof(T) * STAGES * (ATile<64, 16, TA>::ELEMS + BTile<64, 16, TB>::ELEMS);
     auto k = sgemm_ffma<TA, TB, VA, VB>;
-    static bool attr = false;
-    if (!attr) {
-      ensure_smem(k, smem);
-      attr = true;
-    }
+    ensure_smem_attr(k, smem);
     g.total = slabs * g.tiles_m * g.tiles_n;
     k<<<(unsigned)g.total, 256, smem, s>>>(g);
   }
@@ -614,6 +589,23 @@ double useful_flops(int64_t m, int64_t n, int64_t k, int mask, int tri_a, int tr
 
 }  // namespace
 
+// fp32 products that run on tcgen05 (and carve packed operand tiles)
+bool sgemm_tc_route(int64_t m, int64_t n, int64_t k, int64_t inner) {
+  static const bool tc = [] {
+    const char* e = getenv("DLA_SGEMM_TC");  // tuning switch: 0 keeps every fp32 GEMM on FFMA
+    return e ? atoi(e) != 0 : true;
+  }();
+  return tc && inner == 1 && m >= 256 && n >= 256 && k >= 128;
+}
+
+template <typename T>
+size_t ws_gemm(int64_t batch, int64_t m, int64_t n, int64_t k, int64_t inner) {
+  if (sizeof(T) != 4 || batch <= 0 || !sgemm_tc_route(m, n, k, inner)) return 0;
+  return carve_bound(sgemm_tc_ws_bytes(batch, m, n, k));
+}
+template size_t ws_gemm<double>(int64_t, int64_t, int64_t, int64_t, int64_t);
+template size_t ws_gemm<float>(int64_t, int64_t, int64_t, int64_t, int64_t);
+
 template <typename T>
 dla_status gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T alpha, MatB<const T> a,
                 bool ta, MatB<const T> b, bool tb, T beta, MatB<T> cm, int mask, const int32_t* skip, int tri_a,
@@ -630,11 +622,7 @@ dla_status gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T 
     if (gemm_skinny<T>(c, batch, m, n, k, alpha, a, ta, b, tb, beta, cm, mask, skip, &st)) return st;
   }
   if constexpr (sizeof(T) == 4) {  // large fp32 products: tcgen05 3xTF32 (gemm_tc.cu)
-    static const bool tc = [] {
-      const char* e = getenv("DLA_SGEMM_TC");  // tuning switch: 0 keeps every fp32 GEMM on FFMA
-      return e ? atoi(e) != 0 : true;
-    }();
-    if (tc && inner == 1 && m >= 256 && n >= 256 && k >= 128) {  // big products: the packing pass pays off
+    if (sgemm_tc_route(m, n, k, inner)) {  // big products: the packing pass pays off
       dla_status st;
       const bool prof = gemm_prof_on();
       if (prof) gemm_prof_begin(c.stream);

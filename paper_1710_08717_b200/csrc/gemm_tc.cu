@@ -279,6 +279,12 @@ __global__ void __launch_bounds__(TT, 1) k_sgemm_tc(TcArgs2 g) {
 
 }  // namespace
 
+// Packed hi/lo TF32 operand tiles of one call (the k_tf32_pack output).
+size_t sgemm_tc_ws_bytes(int64_t batch, int64_t m, int64_t n, int64_t k) {
+  const int64_t art = (m + TM - 1) / TM, brt = (n + TN - 1) / TN, kt = (k + TK - 1) / TK;
+  return sizeof(float) * 2 * TILE_F * (size_t)(batch * kt * (art + brt));
+}
+
 // C = alpha op(A) op(B) + beta C on tcgen05 (3xTF32).  Returns false if the
 // problem is outside this kernel's scope (the caller uses the FFMA GEMM).
 bool sgemm_tc(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, float alpha, MatB<const float> a, bool ta,
@@ -287,10 +293,9 @@ bool sgemm_tc(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, floa
   if (inner != 1) return false;
   *st = DLA_OK;
   const int64_t art = (m + TM - 1) / TM, brt = (n + TN - 1) / TN, kt = (k + TK - 1) / TK;
-  const size_t tile_bytes = sizeof(float) * 2 * TILE_F;
-  Scratch ws(tile_bytes * (size_t)(batch * kt * (art + brt)), c.stream);
-  if (!ws.p) {
-    *st = DLA_ERR_CUDA;
+  Scratch ws(c, sgemm_tc_ws_bytes(batch, m, n, k));
+  if (!ws.ok) {
+    *st = DLA_ERR_WORKSPACE;
     return true;
   }
   float* apk = ws.as<float>();
@@ -308,11 +313,7 @@ bool sgemm_tc(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, floa
   const int64_t ctn = (n + TNC - 1) / TNC;
   TcArgs2 g{m, n, alpha, beta, apk, bpk, art, kt, brt, kt, cm, mask, skip, art, ctn, tri_a, tri_b, k};
   const size_t smem = (size_t)TCST * STAGE_BYTES;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_sgemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  ensure_smem_attr(k_sgemm_tc, smem);
   k_sgemm_tc<<<(unsigned)(batch * art * ctn), TT, smem, c.stream>>>(g);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

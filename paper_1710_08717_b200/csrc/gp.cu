@@ -462,18 +462,23 @@ dla_status dla_axpy_f64(int64_t count, double alpha, const double* x, double* y,
   return DLA_OK;
 }
 
+size_t dla_ml_reduce_ws_bytes(int64_t batch) {
+  const int64_t nparts = batch > 0 ? (batch + MLS - 1) / MLS : 0;
+  return sizeof(double) * (size_t)(2 * (nparts > 0 ? nparts : 1));
+}
+
 dla_status dla_ml_reduce_f64(int64_t batch, int64_t n, const double* quad, const double* logdet, const double* abar,
-                             double lam, double* out, void* stream) {
+                             double lam, double* out, void* ws, size_t ws_bytes, void* stream) {
   if (batch < 0 || n < 0) return DLA_ERR_SHAPE;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int64_t nparts = batch > 0 ? (batch + MLS - 1) / MLS : 0;
-  Scratch part(sizeof(double) * (size_t)(2 * (nparts > 0 ? nparts : 1)), s);
-  if (!part.p) return DLA_ERR_CUDA;
+  if (!ws || ws_bytes < dla_ml_reduce_ws_bytes(batch)) return DLA_ERR_WORKSPACE;
+  double* part = static_cast<double*>(ws);  // per-CTA partials of the fixed-order reduction
   if (nparts > 0) {
-    k_ml_partial<<<(unsigned)nparts, MLT, 0, s>>>(batch, n, quad, logdet, abar, part.as<double>());
+    k_ml_partial<<<(unsigned)nparts, MLT, 0, s>>>(batch, n, quad, logdet, abar, part);
     DLAB_LAUNCH_CHECK();
   }
-  k_ml_final<<<1, MLT, 0, s>>>(nparts, batch, n, part.as<double>(), lam, out);
+  k_ml_final<<<1, MLT, 0, s>>>(nparts, batch, n, part, lam, out);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }

@@ -14,7 +14,7 @@
 //                  (dl/adjoints.hpp:175-191) as trtri + three triangular
 //                  GEMMs: 2 n^3 flops, all DMMA, vs the composed 3 n^3 of
 //                  trmm + 2 trsm.
-// Scratch (n^2 per slice) comes from the stream-ordered pool.
+// Scratch (n^2 per slice) is carved from the caller's workspace (ws_* mirrors).
 #include <mutex>
 
 #include "chol64.cuh"
@@ -71,15 +71,67 @@ __global__ void __launch_bounds__(128) k_trtri_blocks(int64_t nblk, MatB<T> w) {
 }  // namespace
 
 template <typename T>
+size_t trtri_levels_tmp(int64_t n) {
+  return sizeof(T) * (size_t)(n / 2) * (size_t)(n / 2);
+}
+
+template <typename T>
 bool inv_eligible(int64_t n) {
   if (n < 2 * IB || n % IB) return false;
   const int64_t q = n / IB;
   return (q & (q - 1)) == 0;
 }
 
+
 template <typename T>
-size_t trtri_levels_tmp(int64_t n) {
-  return sizeof(T) * (size_t)(n / 2) * (size_t)(n / 2);
+size_t trsm_inv_scratch(int64_t batch, int64_t m, int64_t n, int64_t nt) {
+  return sizeof(T) * (size_t)batch * ((size_t)nt * nt + (size_t)m * n) + (size_t)batch * trtri_levels_tmp<T>(nt);
+}
+template <typename T>
+size_t potrf_bwd_inv_scratch(int64_t batch, int64_t n) {
+  return sizeof(T) * (size_t)batch * 2 * (size_t)n * n + (size_t)batch * trtri_levels_tmp<T>(n);
+}
+template <typename T>
+size_t potri_inv_scratch(int64_t batch, int64_t n) {
+  return sizeof(T) * (size_t)batch * (size_t)n * n + (size_t)batch * trtri_levels_tmp<T>(n);
+}
+
+// ---- workspace mirrors (common.cuh): the carves of each routine's call tree
+template <typename T>
+size_t ws_trtri_levels(int64_t batch, int64_t n) {
+  size_t w = 0;
+  for (int64_t s = IB; s < n; s *= 2)
+    if (n / (2 * s) == 1) w += 2 * ws_gemm<T>(batch, s, s, s, 1);  // inner > 1 levels never carve
+  return w;
+}
+template <typename T>
+size_t ws_trsm_inv(int64_t batch, int64_t m, int64_t n, bool right) {
+  const int64_t nt = right ? n : m;
+  return carve_bound(trsm_inv_scratch<T>(batch, m, n, nt)) + ws_trtri_levels<T>(batch, nt) +
+         ws_gemm<T>(batch, m, n, nt);
+}
+template <typename T>
+size_t ws_potrf_inv_prepare(int64_t batch, int64_t n) {
+  return ws_trtri_levels<T>(batch, n);
+}
+template <typename T>
+size_t ws_potrf_bwd_tail(int64_t batch, int64_t n) {  // potrf_bwd_phi + potrf_bwd_finish
+  return 3 * ws_gemm<T>(batch, n, n, n);
+}
+template <typename T>
+size_t ws_potrf_bwd_inv(int64_t batch, int64_t n) {
+  return carve_bound(potrf_bwd_inv_scratch<T>(batch, n)) + ws_potrf_inv_prepare<T>(batch, n) +
+         ws_potrf_bwd_tail<T>(batch, n);
+}
+template <typename T>
+size_t ws_trmm_gemm(int64_t batch, int64_t m, int64_t n, bool right) {
+  const int64_t nt = right ? n : m;
+  if (sizeof(T) == 8 && !right && m <= 128) return ws_gemm<T>(batch, m, n, m);
+  return carve_bound(sizeof(T) * (size_t)batch * (size_t)m * n) + ws_gemm<T>(batch, m, n, nt);
+}
+template <typename T>
+size_t ws_potri_inv(int64_t batch, int64_t n) {
+  return carve_bound(potri_inv_scratch<T>(batch, n)) + ws_trtri_levels<T>(batch, n) + ws_gemm<T>(batch, n, n, n);
 }
 
 // W lower triangular (strict upper must be zero on entry; stays zero).
@@ -88,11 +140,7 @@ template <typename T>
 dla_status trtri_levels(const Ctx& c, int64_t batch, int64_t n, MatB<T> w, T* tmp) {
   const int64_t nblk = n / IB;
   const size_t sm = sizeof(T) * (2 * IB * ILD + IB);
-  static bool once = false;
-  if (!once) {
-    cudaFuncSetAttribute(k_trtri_blocks<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    once = true;
-  }
+  ensure_smem_attr(k_trtri_blocks<T>, sm);
   k_trtri_blocks<T><<<(unsigned)(batch * nblk), 128, sm, c.stream>>>(nblk, w);
   DLAB_LAUNCH_CHECK();
   for (int64_t s = IB; s < n; s *= 2) {
@@ -115,9 +163,7 @@ template <typename T>
 dla_status trsm_inv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x, bool right,
                     bool trans, bool lower, T alpha) {
   const int64_t nt = right ? n : m;
-  Scratch ws(sizeof(T) * (size_t)batch * ((size_t)nt * nt + (size_t)m * n) + (size_t)batch * trtri_levels_tmp<T>(nt),
-             c.stream);
-  if (!ws.p) return DLA_ERR_CUDA;
+  DLAB_SCRATCH(ws, c, trsm_inv_scratch<T>(batch, m, n, nt));
   T* wp = ws.as<T>();
   MatB<T> w{wp, nt, nt * nt};
   MatB<T> y{wp + batch * nt * nt, n, m * n};
@@ -181,33 +227,27 @@ dla_status potrf_bwd_from_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> ab
 template <typename T>
 dla_status potrf_bwd_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> lbar, MatB<const T> l,
                          bool lower) {
-  Scratch ws(sizeof(T) * (size_t)batch * 2 * (size_t)n * n + (size_t)batch * trtri_levels_tmp<T>(n), c.stream);
-  if (!ws.p) return DLA_ERR_CUDA;
+  DLAB_SCRATCH(ws, c, potrf_bwd_inv_scratch<T>(batch, n));
   T* wp = ws.as<T>();
   MatB<T> wi{wp, n, n * n};                  // L^{-1} (lower)
   MatB<T> tt{wp + batch * n * n, n, n * n};  // Phi, then the lower half of L^-T Phi L^-1
   T* tmp = wp + 2 * batch * n * n;
   // L^-1 (trtri) and P' = tril(L^T Lbar) are independent: the inverse runs
   // on a side stream (event fork/join: stream-ordered, graph-capturable)
-  // while P' runs on the caller's stream.
-  static cudaStream_t side = nullptr;
-  static cudaEvent_t fork = nullptr, join = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
-    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
-  });
-  static std::mutex mu;  // one fork in flight per process
-  std::lock_guard<std::mutex> lk(mu);
+  // while P' runs on the caller's stream.  The side stream and events belong
+  // to this (device, caller stream); the join runs even when a launch fails.
+  ForkRes& fr = fork_res(FORK_BWDINV, c.stream);
+  std::lock_guard<std::mutex> lk(fr.mu);
   Ctx sc = c;
-  sc.stream = side;
-  cudaEventRecord(fork, c.stream);
-  cudaStreamWaitEvent(side, fork, 0);
-  DLAB_TRY(potrf_inv_prepare<T>(sc, batch, n, l, lower, wi, tmp));
-  cudaEventRecord(join, side);
-  DLAB_TRY(potrf_bwd_phi<T>(c, batch, n, lbar, l, lower, tt));
-  cudaStreamWaitEvent(c.stream, join, 0);
+  sc.stream = fr.side;
+  cudaEventRecord(fr.ev[0], c.stream);
+  cudaStreamWaitEvent(fr.side, fr.ev[0], 0);
+  const dla_status s1 = potrf_inv_prepare<T>(sc, batch, n, l, lower, wi, tmp);
+  cudaEventRecord(fr.ev[1], fr.side);
+  const dla_status s2 = potrf_bwd_phi<T>(c, batch, n, lbar, l, lower, tt);
+  cudaStreamWaitEvent(c.stream, fr.ev[1], 0);
+  if (s1 != DLA_OK) return s1;
+  if (s2 != DLA_OK) return s2;
   return potrf_bwd_finish<T>(c, batch, n, abar, C_(wi), tt);
 }
 
@@ -226,8 +266,7 @@ dla_status trmm_gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<con
     const int tri = (lower != trans) ? TRI_LOWER : TRI_UPPER;
     return gemm<T>(cr, batch, m, n, m, alpha, t, trans, C_(x), false, T(0), x, MASK_FULL, c.info, tri, TRI_NONE);
   }
-  Scratch ws(sizeof(T) * (size_t)batch * (size_t)m * n, c.stream);
-  if (!ws.p) return DLA_ERR_CUDA;
+  DLAB_SCRATCH(ws, c, sizeof(T) * (size_t)batch * (size_t)m * n);
   MatB<T> y{ws.as<T>(), n, m * n};
   const int tri = (lower != trans) ? TRI_LOWER : TRI_UPPER;  // op(T)
   if (!right)
@@ -242,8 +281,7 @@ dla_status trmm_gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<con
 // checked the diagonal for exact zeros.
 template <typename T>
 dla_status potri_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
-  Scratch ws(sizeof(T) * (size_t)batch * (size_t)n * n + (size_t)batch * trtri_levels_tmp<T>(n), c.stream);
-  if (!ws.p) return DLA_ERR_CUDA;
+  DLAB_SCRATCH(ws, c, potri_inv_scratch<T>(batch, n));
   MatB<T> b{ws.as<T>(), n, n * n};
   T* tmp = ws.as<T>() + batch * n * n;
   DLAB_TRY(ew_square<T>(c, batch, n, a, /*tril*/ 0, T(1), c.info));  // the ignored triangle may hold anything
@@ -259,6 +297,13 @@ dla_status potri_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
   template dla_status potri_inv<T>(const Ctx&, int64_t, int64_t, MatB<T>);                                   \
   template bool inv_eligible<T>(int64_t);                                                                    \
   template size_t trtri_levels_tmp<T>(int64_t);                                                              \
+  template size_t ws_trtri_levels<T>(int64_t, int64_t);                                                      \
+  template size_t ws_trsm_inv<T>(int64_t, int64_t, int64_t, bool);                                           \
+  template size_t ws_potrf_inv_prepare<T>(int64_t, int64_t);                                                 \
+  template size_t ws_potrf_bwd_tail<T>(int64_t, int64_t);                                                    \
+  template size_t ws_potrf_bwd_inv<T>(int64_t, int64_t);                                                     \
+  template size_t ws_trmm_gemm<T>(int64_t, int64_t, int64_t, bool);                                          \
+  template size_t ws_potri_inv<T>(int64_t, int64_t);                                                         \
   template dla_status trtri_levels<T>(const Ctx&, int64_t, int64_t, MatB<T>, T*);                            \
   template dla_status trsm_inv<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<const T>, MatB<T>, bool, bool, \
                                   bool, T);                                                                  \

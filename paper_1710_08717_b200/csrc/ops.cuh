@@ -48,10 +48,26 @@ dla_status trmm_gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<con
                      bool trans, bool lower, T alpha);
 template <typename T>
 dla_status potri_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> a);
+template <typename T>
+size_t ws_trtri_levels(int64_t batch, int64_t n);
+template <typename T>
+size_t ws_trsm_inv(int64_t batch, int64_t m, int64_t n, bool right);
+template <typename T>
+size_t ws_potrf_inv_prepare(int64_t batch, int64_t n);
+template <typename T>
+size_t ws_potrf_bwd_tail(int64_t batch, int64_t n);
+template <typename T>
+size_t ws_potrf_bwd_inv(int64_t batch, int64_t n);
+template <typename T>
+size_t ws_trmm_gemm(int64_t batch, int64_t m, int64_t n, bool right);
+template <typename T>
+size_t ws_potri_inv(int64_t batch, int64_t n);
 
 // trsv.cu — one-launch solve for <= 8 right-hand sides (flag-synchronised)
 template <typename T>
 bool trsv_eligible(int64_t nt, int64_t nvec);
+template <typename T>
+size_t ws_trsv(int64_t batch, int64_t m, int64_t n, bool right);
 template <typename T>
 dla_status trsv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x, bool right, bool trans,
                 bool lower, T alpha);
@@ -74,6 +90,7 @@ dla_status gelqf_fwd(const Ctx& c, int64_t batch, int64_t m, int64_t n, T* q, T*
 // strict upper untouched)
 bool potrf_tiles_eligible(int64_t batch, int64_t n, const MatB<double>& a);
 dla_status potrf_tiles(const Ctx& c, int64_t batch, int64_t n, MatB<double> a, int64_t kbase);
+size_t ws_potrf_tiles(int64_t batch, int64_t n);
 
 // syevd.cu
 template <typename T>

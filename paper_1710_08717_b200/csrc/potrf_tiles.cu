@@ -298,11 +298,15 @@ bool potrf_tiles_eligible(int64_t batch, int64_t n, const MatB<double>& a) {
   return n > TB && (p % 16) == 0 && (a.ld % 2) == 0 && (a.bs % 2) == 0 && batch * ((n + TB - 1) / TB) <= 4096;
 }
 
+size_t ws_potrf_tiles(int64_t batch, int64_t n) {
+  const int64_t nt = (n + TB - 1) / TB;
+  return carve_bound(sizeof(int) * (size_t)(batch * nt * nt) + 16);
+}
+
 dla_status potrf_tiles(const Ctx& c, int64_t batch, int64_t n, MatB<double> a, int64_t kbase) {
   const int64_t nt = (n + TB - 1) / TB;
   const size_t flag_bytes = sizeof(int) * (size_t)(batch * nt * nt);
-  Scratch ws(flag_bytes + 16, c.stream);
-  if (!ws.p) return DLA_ERR_CUDA;
+  DLAB_SCRATCH(ws, c, flag_bytes + 16);
   if (cudaMemsetAsync(ws.p, 0, flag_bytes + 16, c.stream) != cudaSuccess) return DLA_ERR_CUDA;
   TileArgs g;
   g.batch = batch;
@@ -316,14 +320,10 @@ dla_status potrf_tiles(const Ctx& c, int64_t batch, int64_t n, MatB<double> a, i
   const size_t sm_update = sizeof(double) * 2 * TSTAGES * TB * TLD;
   const size_t sm_final = sizeof(double) * (2 * TB * TSLD + TB);
   const size_t sm = sm_update > sm_final ? sm_update : sm_final;
-  static bool once = false;
-  static int per_sm = 1;
-  if (!once) {
-    cudaFuncSetAttribute(k_potrf_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_potrf_tiles, TTHREADS, sm);
-    if (per_sm < 1) per_sm = 1;
-    once = true;
-  }
+  ensure_smem_attr(k_potrf_tiles, sm);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_potrf_tiles, TTHREADS, sm);
+  if (per_sm < 1) per_sm = 1;
   static const int cap = [] {
     const char* e = getenv("DLA_TILES_PER_SM");  // tuning switch: resident CTAs per SM
     return e ? atoi(e) : 0;

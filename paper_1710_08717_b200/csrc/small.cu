@@ -491,12 +491,8 @@ dla_status potrf_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool l
       const char* e = getenv("DLA_WARP_MINB");  // tuning switch: 1 = no register cap
       return e ? atoi(e) : 2;
     }();
-    static bool once = false;
-    if (!once) {
-      cudaFuncSetAttribute(k_potrf_warp<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      cudaFuncSetAttribute(k_potrf_warp<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      once = true;
-    }
+    ensure_smem_attr(k_potrf_warp<T, 1>, sm);
+    ensure_smem_attr(k_potrf_warp<T, 2>, sm);
     const unsigned grid = (unsigned)((batch + wpc - 1) / wpc);
     if (minb == 1)
       k_potrf_warp<T, 1><<<grid, wpc * 32, sm, c.stream>>>((int)n, batch, a, lower, c.info);
@@ -516,22 +512,14 @@ dla_status potrf_bwd_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar,
   if (n <= WN) {
     constexpr int wpc = wpc_bwd<T>();
     const size_t sm = sizeof(T) * wpc * (WN * Bc<T>::LLD + WN * WLD + 2 * WN + 4);
-    static bool once = false;
-    if (!once) {
-      cudaFuncSetAttribute(k_potrf_bwd_warp<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      once = true;
-    }
+    ensure_smem_attr(k_potrf_bwd_warp<T>, sm);
     k_potrf_bwd_warp<T><<<(unsigned)((batch + wpc - 1) / wpc), wpc * 32, sm, c.stream>>>((int)n, batch, abar, lbar,
                                                                                         l, lower);
     DLAB_LAUNCH_CHECK();
     return DLA_OK;
   }
   const size_t sm = sizeof(T) * 3 * SN * SLD;
-  static bool once = false;
-  if (!once) {
-    cudaFuncSetAttribute(k_potrf_bwd_small<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    once = true;
-  }
+  ensure_smem_attr(k_potrf_bwd_small<T>, sm);
   k_potrf_bwd_small<T><<<(unsigned)batch, 256, sm, c.stream>>>((int)n, abar, lbar, l, lower);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
@@ -543,11 +531,7 @@ dla_status chol_chain_small(const Ctx& c, int64_t batch, int64_t n, MatB<const T
                             T* ybar) {
   constexpr int wpc = wpc_bwd<T>();
   const size_t sm = sizeof(T) * wpc * (WN * Bc<T>::LLD + WN * WLD + 6 * WN);
-  static bool once = false;
-  if (!once) {
-    cudaFuncSetAttribute(k_chol_chain_warp<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    once = true;
-  }
+  ensure_smem_attr(k_chol_chain_warp<T>, sm);
   k_chol_chain_warp<T><<<(unsigned)((batch + wpc - 1) / wpc), wpc * 32, sm, c.stream>>>((int)n, batch, a, y, phi,
                                                                                        abar, ybar, c.info);
   DLAB_LAUNCH_CHECK();

@@ -526,11 +526,7 @@ dla_status syevd_fwd(const Ctx& c, int64_t batch, int64_t n, T* u, T* lambda, vo
   const bool sm = n <= EN;
   if (sm) {
     const size_t smem = sizeof(T) * (PK + (PK & 1) + EN * (EN + 1));
-    static bool once = false;
-    if (!once) {
-      cudaFuncSetAttribute(k_syevd_small<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      once = true;
-    }
+    ensure_smem_attr(k_syevd_small<T>, smem);
     k_syevd_small<T><<<(unsigned)batch, ET, smem, c.stream>>>((int)n, u, lambda, c.info);
     DLAB_LAUNCH_CHECK();
     return DLA_OK;
@@ -539,11 +535,7 @@ dla_status syevd_fwd(const Ctx& c, int64_t batch, int64_t n, T* u, T* lambda, vo
   const int64_t npairs = (n + 1) / 2;
   const size_t smem = (sm ? sizeof(T) * 2 * EN * (EN + 1) : 0) + npairs * 2 * (sizeof(T) + sizeof(int));
   if (smem > 200 * 1024) return DLA_ERR_SHAPE;  // n > ~8000: out of the supported range
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(k_syevd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
+  ensure_smem_attr(k_syevd<T>, smem);
   k_syevd<T><<<(unsigned)batch, ET, smem, c.stream>>>((int)n, u, lambda, static_cast<T*>(ws), c.info, sm);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;

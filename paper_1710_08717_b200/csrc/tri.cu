@@ -311,11 +311,6 @@ __global__ void __launch_bounds__(256) k_lauum_leaf(int nb, MatB<T> a, const int
   }
 }
 
-template <typename K>
-void set_smem(K kernel, size_t bytes) {
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-}
-
 template <typename T>
 size_t leaf_smem(int vecs) {
   return sizeof(T) * (size_t)(NB * LDS + vecs * LDS);
@@ -335,11 +330,7 @@ dla_status trsm_core(const Ctx& c, int64_t batch, int64_t nt, int64_t nother, Ma
     const bool slower = right ? !op_lower : op_lower;
     const int64_t chunks = (nother + BV - 1) / BV;
     const size_t sm = sizeof(T) * (size_t)(NB * LDS + BV * LDS + NB);
-    static bool once = false;
-    if (!once) {
-      set_smem(k_trsm_leaf_blk<T>, sm);
-      once = true;
-    }
+    ensure_smem_attr(k_trsm_leaf_blk<T>, sm);
     k_trsm_leaf_blk<T><<<(unsigned)(batch * chunks), 128, sm, c.stream>>>((int)nt, nother, t, x, right, s_tt, slower,
                                                                           alpha, check, c.info);
     DLAB_LAUNCH_CHECK();
@@ -391,11 +382,7 @@ dla_status trmm_core(const Ctx& c, int64_t batch, int64_t nt, int64_t nother, Ma
     const bool slower = right ? !op_lower : op_lower;
     const int64_t chunks = (nother + LEAF_VEC - 1) / LEAF_VEC;
     const size_t sm = leaf_smem<T>(LEAF_VEC);
-    static bool once = false;
-    if (!once) {
-      set_smem(k_trmm_leaf<T>, sm);
-      once = true;
-    }
+    ensure_smem_attr(k_trmm_leaf<T>, sm);
     k_trmm_leaf<T><<<(unsigned)(batch * chunks), 256, sm, c.stream>>>((int)nt, nother, t, x, right, s_tt, slower,
                                                                        alpha, c.info);
     DLAB_LAUNCH_CHECK();
@@ -435,6 +422,32 @@ dla_status trmm_core(const Ctx& c, int64_t batch, int64_t nt, int64_t nother, Ma
 
 template <typename T>
 dla_status potrf_blocked(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int64_t kbase);
+
+// L11^{-1} buffer of the blocked Cholesky's throughput path (large batches of
+// multi-chunk panels); sms < 0 gives the bound the workspace query uses.
+template <typename T, int NBP>
+size_t potrf_linv_bytes(int64_t batch, int64_t n, int sms) {
+  if (NBP != 64 || n <= 2 * NBP) return 0;
+  if (sms >= 0 && batch * ((n + 63) / 64) <= sms) return 0;
+  return sizeof(T) * (size_t)batch * 64 * 64;
+}
+
+// DLA_POTRF_MODE (tuning switch): 0 auto (blocked look-ahead), 1 recursive,
+// 2 blocked, 3 persistent tile dataflow (f64)
+int potrf_mode() {
+  static const int mode = [] {
+    const char* e = getenv("DLA_POTRF_MODE");
+    return e ? atoi(e) : 0;
+  }();
+  return mode;
+}
+int potrf_nb() {
+  static const int nbp = [] {
+    const char* e = getenv("DLA_POTRF_NB");  // tuning switch: 128-wide panels
+    return e ? atoi(e) : 0;
+  }();
+  return nbp == 128 ? 128 : 64;
+}
 
 template <typename T>
 dla_status potrf_rec(const Ctx& c, int64_t batch, int64_t n, int64_t k0, MatB<T> a) {
@@ -757,40 +770,6 @@ __global__ void __launch_bounds__(256) k_potrf_diag_inv(int nb, int64_t k0, MatB
   }
 }
 
-// Side stream + event pool for the look-ahead (created once per process;
-// growth happens outside any hot loop).
-struct LookAhead {
-  cudaStream_t side = nullptr, crit = nullptr;
-  int prio_hi = 0;
-  cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr;
-  std::vector<cudaEvent_t> panel, done;
-  static LookAhead& get(int64_t steps) {
-    static LookAhead la;
-    static std::mutex mu;
-    std::lock_guard<std::mutex> lk(mu);
-    if (!la.side) {
-      // the critical chain gets the highest stream priority so that freed
-      // SMs go to its panel CTAs before the bulk update's next tiles
-      int lo = 0, hi = 0;
-      cudaDeviceGetStreamPriorityRange(&lo, &hi);
-      cudaStreamCreateWithPriority(&la.side, cudaStreamNonBlocking, lo);
-      cudaStreamCreateWithPriority(&la.crit, cudaStreamNonBlocking, hi);
-      la.prio_hi = hi;
-      cudaEventCreateWithFlags(&la.fork, cudaEventDisableTiming);
-      cudaEventCreateWithFlags(&la.join, cudaEventDisableTiming);
-      cudaEventCreateWithFlags(&la.join2, cudaEventDisableTiming);
-    }
-    while ((int64_t)la.panel.size() < steps) {
-      cudaEvent_t a, b;
-      cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
-      cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
-      la.panel.push_back(a);
-      la.done.push_back(b);
-    }
-    return la;
-  }
-};
-
 // Right-looking blocked Cholesky (the reference's own loop structure,
 // dl/cholesky.hpp:43-70, with nb = NBP): per block column one warp-panel leaf
 // factorization and blocked DMMA panel solve (one launch, all rows of the
@@ -800,11 +779,7 @@ struct LookAhead {
 template <typename T, int NBP>
 dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int64_t kbase) {
   const size_t sm = sizeof(T) * ((NBP + 64) * (NBP + 1) + NBP + (NBP == 64 ? 2 * 64 * (NBP + 1) : 0));
-  static bool once = false;
-  if (!once) {
-    set_smem(k_potrf_panel<T, NBP>, sm);
-    once = true;
-  }
+  ensure_smem_attr(k_potrf_panel<T, NBP>, sm);
   // Look-ahead on two streams: the main stream runs the critical chain
   // (panel k, then the update of block column k+1 only), the side stream the
   // bulk trailing update of step k, which overlaps panel k+1.  The side
@@ -813,11 +788,14 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
   // side updates <= k-2, already ordered).  Fork/join by events: stream-
   // ordered w.r.t. the caller and capturable into a CUDA graph.
   const int64_t steps = (n + NBP - 1) / NBP;
-  LookAhead& la = LookAhead::get(steps);
-  Scratch arrive(sizeof(int) * (size_t)batch, c.stream);
-  if (!arrive.p) return DLA_ERR_CUDA;
-  Scratch linv(NBP == 64 && batch * ((n + 63) / 64) > c.sms ? sizeof(T) * (size_t)batch * 64 * 64 : 0, c.stream);
+  DLAB_SCRATCH(arrive, c, sizeof(int) * (size_t)batch);
+  DLAB_SCRATCH(linv, c, (potrf_linv_bytes<T, NBP>(batch, n, c.sms)));
   if (cudaMemsetAsync(arrive.p, 0, sizeof(int) * (size_t)batch, c.stream) != cudaSuccess) return DLA_ERR_CUDA;
+  // side / critical streams and events of THIS (device, caller stream),
+  // held for the whole enqueue (include/dla.h: thread-safe across streams)
+  ForkRes& la = fork_res(FORK_LOOKAHEAD, c.stream);
+  std::lock_guard<std::mutex> la_lock(la.mu);
+  la.grow(steps);
   static const bool prio = [] {
     const char* e = getenv("DLA_POTRF_PRIO");  // tuning switch: 0 keeps the chain on the caller's stream
     return e ? atoi(e) != 0 : true;
@@ -839,9 +817,9 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
     if (reserve > 0 && reserve < c.sms) side.gemm_ctas = c.sms - reserve;
   }
   if (prio) cc.stream = la.crit;
-  cudaEventRecord(la.fork, c.stream);
-  cudaStreamWaitEvent(la.side, la.fork, 0);
-  if (prio) cudaStreamWaitEvent(cc.stream, la.fork, 0);
+  cudaEventRecord(la.ev[0], c.stream);
+  cudaStreamWaitEvent(la.side, la.ev[0], 0);
+  if (prio) cudaStreamWaitEvent(cc.stream, la.ev[0], 0);
   // Look-ahead with (optionally) grouped trailing updates.  Panels are taken in
   // groups of G.  After the last panel of group g the side stream applies
   // the whole group to every column >= (g+2) G NBP in ONE masked SYRK with
@@ -872,6 +850,13 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
   auto throughput = [&](int64_t p) { return NBP == 64 && chunks_of(p) > 1 && batch * chunks_of(p) > c.sms; };
   auto fused = [&](int64_t p) { return NBP == 64 && G == 1 && p >= 1 && !throughput(p); };
   bool hook_fired = false;
+  dla_status st = DLA_OK;
+  // every launch failure leaves the loop through the join below: work already
+  // forked onto the side / critical streams is joined back to the caller's
+  // stream before the scratch (carved from the caller's workspace) is released
+#define LA_TRY(expr)          \
+  if ((st = (expr)) != DLA_OK) \
+    break
   for (int64_t p = 0; p < steps; ++p) {
     const int64_t k0 = p * NBP;
     const int64_t kb = min((int64_t)NBP, n - k0);
@@ -881,7 +866,7 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
       if (g >= 2) cudaStreamWaitEvent(cc.stream, la.done[g - 2], 0);
       const int64_t kk0 = std::max<int64_t>(0, (g - 1) * G) * NBP;
       MatB<T> lrows = a.sub(k0, kk0);
-      DLAB_TRY(gemm<T>(cc, batch, n - k0, kb, k0 - kk0, T(-1), C_(lrows), false, C_(lrows), true, T(1), a.sub(k0, k0),
+      LA_TRY(gemm<T>(cc, batch, n - k0, kb, k0 - kk0, T(-1), C_(lrows), false, C_(lrows), true, T(1), a.sub(k0, k0),
                        MASK_LOWER, c.info));
     } else if (p >= 2) {
       cudaStreamWaitEvent(cc.stream, la.done[p - 2], 0);  // the last side update that wrote column p
@@ -890,16 +875,12 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
     if (throughput(p) && rest > 0) {
       // throughput path: one diagonal factorization per slice + a batched GEMM solve
       const size_t smd = sizeof(T) * (2 * 64 * CH_LD + 64);
-      static bool once_d = false;
-      if (!once_d) {
-        set_smem(k_potrf_diag_inv<T>, smd);
-        once_d = true;
-      }
+      ensure_smem_attr(k_potrf_diag_inv<T>, smd);
       k_potrf_diag_inv<T><<<(unsigned)batch, 256, smd, cc.stream>>>((int)kb, kbase + k0, a.sub(k0, k0), linv.as<T>(),
                                                                      c.info);
-      DLAB_LAUNCH_CHECK();
+      LA_TRY(launch_status());
       MatB<T> a21 = a.sub(k0 + kb, k0);
-      DLAB_TRY(gemm<T>(cc, batch, rest, kb, kb, T(1), C_(a21), false, MatB<const T>{linv.as<T>(), 64, 64 * 64}, true,
+      LA_TRY(gemm<T>(cc, batch, rest, kb, kb, T(1), C_(a21), false, MatB<const T>{linv.as<T>(), 64, 64 * 64}, true,
                        T(0), a21, MASK_FULL, c.info, TRI_NONE, TRI_UPPER));
     } else {
       const int kp = fused(p) ? (int)NBP : 0;
@@ -917,9 +898,11 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
       cfg.attrs = attr;
       cfg.numAttrs = prio ? 1 : 0;
       if (cudaLaunchKernelEx(&cfg, k_potrf_panel<T, NBP>, (int)kb, rest, kbase + k0, a.sub(k0, k0),
-                             a.sub(k0 + kb, k0), c.info, arrive.as<int>(), lp, kp) != cudaSuccess)
-        return DLA_ERR_CUDA;
-      DLAB_LAUNCH_CHECK();
+                             a.sub(k0 + kb, k0), c.info, arrive.as<int>(), lp, kp) != cudaSuccess) {
+        st = DLA_ERR_CUDA;
+        break;
+      }
+      LA_TRY(launch_status());
     }
     if (c.potrf_hook && !hook_fired && kbase == 0 && c.potrf_hook->n == n &&
         c.potrf_hook->a == static_cast<const void*>(a.p) && k0 + kb >= c.potrf_hook->col) {
@@ -934,20 +917,21 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
         cudaStreamWaitEvent(la.side, la.panel[g], 0);
         const int64_t gk0 = g * G * NBP;
         MatB<T> p2 = a.sub(c0, gk0);
-        DLAB_TRY(gemm<T>(side, batch, n - c0, n - c0, k0 + kb - gk0, T(-1), C_(p2), false, C_(p2), true, T(1),
+        LA_TRY(gemm<T>(side, batch, n - c0, n - c0, k0 + kb - gk0, T(-1), C_(p2), false, C_(p2), true, T(1),
                          a.sub(c0, c0), MASK_LOWER, c.info));
       }
       cudaEventRecord(la.done[g], la.side);
     }
   }
+#undef LA_TRY
   (void)ngroups;
-  cudaEventRecord(la.join, la.side);
-  cudaStreamWaitEvent(c.stream, la.join, 0);
+  cudaEventRecord(la.ev[1], la.side);
+  cudaStreamWaitEvent(c.stream, la.ev[1], 0);
   if (prio) {
-    cudaEventRecord(la.join2, cc.stream);
-    cudaStreamWaitEvent(c.stream, la.join2, 0);
+    cudaEventRecord(la.ev[2], cc.stream);
+    cudaStreamWaitEvent(c.stream, la.ev[2], 0);
   }
-  return DLA_OK;
+  return st;
 }
 
 // Panel width: 128 halves the serial panel chain of a large matrix (each step
@@ -955,11 +939,7 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
 // CTAs busy for small n.  DLA_POTRF_NB overrides (tuning switch).
 template <typename T>
 dla_status potrf_blocked(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int64_t kbase) {
-  static const int nbp = [] {
-    const char* e = getenv("DLA_POTRF_NB");
-    return e ? atoi(e) : 0;
-  }();
-  const bool wide = nbp == 128;
+  const bool wide = potrf_nb() == 128;
   return wide ? potrf_blocked_nb<T, 128>(c, batch, n, a, kbase) : potrf_blocked_nb<T, 64>(c, batch, n, a, kbase);
 }
 
@@ -967,11 +947,7 @@ template <typename T>
 dla_status trtri_rec(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
   if (n <= NB) {
     const size_t sm = sizeof(T) * 2 * NB * LDS;
-    static bool once = false;
-    if (!once) {
-      set_smem(k_trtri_leaf<T>, sm);
-      once = true;
-    }
+    ensure_smem_attr(k_trtri_leaf<T>, sm);
     k_trtri_leaf<T><<<(unsigned)batch, 128, sm, c.stream>>>((int)n, a, c.info);
     DLAB_LAUNCH_CHECK();
     return DLA_OK;
@@ -1034,16 +1010,9 @@ dla_status trmm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T>
 template <typename T>
 dla_status potrf_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool zero_upper) {
   if (batch == 0 || n == 0) return DLA_OK;
-  static bool once = false;
-  if (!once) {
-    set_smem(k_potrf_leaf<T>, sizeof(T) * NB * LDS);
-    set_smem(k_lauum_leaf<T>, sizeof(T) * NB * LDS);
-    once = true;
-  }
-  static const int mode = [] {
-    const char* e = getenv("DLA_POTRF_MODE");  // tuning switch: 0 auto, 1 recursive, 2 blocked
-    return e ? atoi(e) : 0;
-  }();
+  ensure_smem_attr(k_potrf_leaf<T>, sizeof(T) * NB * CH_LD);
+  ensure_smem_attr(k_lauum_leaf<T>, sizeof(T) * NB * LDS);
+  const int mode = potrf_mode();
   // default: blocked right-looking with look-ahead (measured faster than the
   // recursive split at every n > 64 on B200, and still ~3% ahead of the
   // persistent tile-dataflow kernel at n = 1024 / 4096, whose per-column
@@ -1066,19 +1035,122 @@ dla_status potrf_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool z
 template <typename T>
 dla_status potri_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
   if (batch == 0 || n == 0) return DLA_OK;
-  static bool once = false;
-  if (!once) {
-    set_smem(k_potrf_leaf<T>, sizeof(T) * NB * LDS);
-    set_smem(k_lauum_leaf<T>, sizeof(T) * NB * LDS);
-    once = true;
-  }
+  ensure_smem_attr(k_potrf_leaf<T>, sizeof(T) * NB * CH_LD);
+  ensure_smem_attr(k_lauum_leaf<T>, sizeof(T) * NB * LDS);
   if (inv_eligible<T>(n)) return potri_inv<T>(c, batch, n, a);
   DLAB_TRY(trtri_rec<T>(c, batch, n, a));
   DLAB_TRY(lauum_rec<T>(c, batch, n, a));
   return ew_square<T>(c, batch, n, a, /*copyltu*/ 2, T(1), c.info);
 }
 
+// ------------------------------------------------------- workspace mirrors
+// Each mirrors the dispatch above call for call (same split points, same
+// eligibility tests); gemm carves only on the fp32 tcgen05 route.
+namespace {
+
+template <typename T>
+size_t ws_trsm_core(int64_t batch, int64_t nt, int64_t no, bool right) {
+  if (nt <= NB) return 0;
+  const int64_t n1 = split_point(nt), n2 = nt - n1, big = std::max(n1, n2);
+  const size_t g = right ? ws_gemm<T>(batch, no, big, big) : ws_gemm<T>(batch, big, no, big);
+  return g + ws_trsm_core<T>(batch, n1, no, right) + ws_trsm_core<T>(batch, n2, no, right);
+}
+
+template <typename T>
+size_t ws_trmm_core(int64_t batch, int64_t nt, int64_t no, bool right) {
+  if (nt <= NB) return 0;
+  const int64_t n1 = split_point(nt), n2 = nt - n1, big = std::max(n1, n2);
+  const size_t g = right ? ws_gemm<T>(batch, no, big, big) : ws_gemm<T>(batch, big, no, big);
+  return g + ws_trmm_core<T>(batch, n1, no, right) + ws_trmm_core<T>(batch, n2, no, right);
+}
+
+template <typename T, int NBP>
+size_t ws_potrf_blocked_nb(int64_t batch, int64_t n) {
+  size_t w = carve_bound(sizeof(int) * (size_t)batch) + carve_bound(potrf_linv_bytes<T, NBP>(batch, n, -1));
+  const int64_t steps = (n + NBP - 1) / NBP;
+  for (int64_t p = 0; p < steps; ++p) {  // column update, throughput solve, side update
+    const int64_t k0 = p * NBP, kb = std::min((int64_t)NBP, n - k0), rest = n - k0 - kb;
+    w += ws_gemm<T>(batch, n - k0, kb, std::min<int64_t>(k0, NBP));
+    w += ws_gemm<T>(batch, rest, kb, kb);
+    const int64_t c0 = (p + 2) * NBP;
+    if (c0 < n) w += ws_gemm<T>(batch, n - c0, n - c0, k0 + kb - p * NBP);
+  }
+  return w;
+}
+
+template <typename T>
+size_t ws_potrf_blocked(int64_t batch, int64_t n) {
+  return potrf_nb() == 128 ? ws_potrf_blocked_nb<T, 128>(batch, n) : ws_potrf_blocked_nb<T, 64>(batch, n);
+}
+
+template <typename T>
+size_t ws_potrf_rec(int64_t batch, int64_t n) {
+  if (n > NB && n <= 512 && batch <= 64) return ws_potrf_blocked<T>(batch, n);
+  if (n <= NB) return 0;
+  const int64_t n1 = split_point(n), n2 = n - n1;
+  size_t w = ws_potrf_rec<T>(batch, n1) + ws_potrf_rec<T>(batch, n2) + ws_gemm<T>(batch, n2, n2, n1);
+  if (inv_eligible<T>(n1) && n2 >= 128) w += ws_trsm_inv<T>(batch, n2, n1, true);
+  else w += ws_trsm_core<T>(batch, n1, n2, true);
+  return w;
+}
+
+template <typename T>
+size_t ws_trtri_rec(int64_t batch, int64_t n) {
+  if (n <= NB) return 0;
+  const int64_t n1 = split_point(n), n2 = n - n1;
+  return ws_trtri_rec<T>(batch, n1) + ws_trtri_rec<T>(batch, n2) + ws_trmm_core<T>(batch, n1, n2, true) +
+         ws_trsm_core<T>(batch, n2, n1, false);
+}
+
+template <typename T>
+size_t ws_lauum_rec(int64_t batch, int64_t n) {
+  if (n <= NB) return 0;
+  const int64_t n1 = split_point(n), n2 = n - n1;
+  return ws_lauum_rec<T>(batch, n1) + ws_lauum_rec<T>(batch, n2) + ws_gemm<T>(batch, n1, n1, n2) +
+         ws_trmm_core<T>(batch, n2, n1, false);
+}
+
+}  // namespace
+
+template <typename T>
+size_t ws_trsm(int64_t batch, int64_t m, int64_t n, bool right) {
+  if (batch == 0 || m == 0 || n == 0) return 0;
+  const int64_t nt = right ? n : m, no = right ? m : n;
+  if (nt <= NB) return 0;
+  if (trsv_eligible<T>(nt, no)) return ws_trsv<T>(batch, m, n, right);
+  if (inv_eligible<T>(nt) && no >= 128) return ws_trsm_inv<T>(batch, m, n, right);
+  return ws_trsm_core<T>(batch, nt, no, right);
+}
+
+template <typename T>
+size_t ws_trmm(int64_t batch, int64_t m, int64_t n, bool right) {
+  if (batch == 0 || m == 0 || n == 0) return 0;
+  const int64_t nt = right ? n : m, no = right ? m : n;
+  if (nt >= 128) return ws_trmm_gemm<T>(batch, m, n, right);
+  return ws_trmm_core<T>(batch, nt, no, right);
+}
+
+template <typename T>
+size_t ws_potrf_lower(int64_t batch, int64_t n) {
+  if (batch == 0 || n == 0) return 0;
+  const int mode = potrf_mode();
+  if (sizeof(T) == 8 && mode == 3) return ws_potrf_tiles(batch, n) + ws_potrf_blocked<T>(batch, n);  // either route
+  if (mode != 1 && n > NB) return ws_potrf_blocked<T>(batch, n);
+  return ws_potrf_rec<T>(batch, n);
+}
+
+template <typename T>
+size_t ws_potri_lower(int64_t batch, int64_t n) {
+  if (batch == 0 || n == 0) return 0;
+  if (inv_eligible<T>(n)) return ws_potri_inv<T>(batch, n);
+  return ws_trtri_rec<T>(batch, n) + ws_lauum_rec<T>(batch, n);
+}
+
 #define INST(T)                                                                                             \
+  template size_t ws_trsm<T>(int64_t, int64_t, int64_t, bool);                                              \
+  template size_t ws_trmm<T>(int64_t, int64_t, int64_t, bool);                                              \
+  template size_t ws_potrf_lower<T>(int64_t, int64_t);                                                      \
+  template size_t ws_potri_lower<T>(int64_t, int64_t);                                                      \
   template dla_status trsm<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<const T>, MatB<T>, bool, bool, bool, \
                               T, bool);                                                                     \
   template dla_status trmm<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<const T>, MatB<T>, bool, bool, bool, \

@@ -140,7 +140,7 @@ __device__ __forceinline__ void stage_block(const StageMap& m, const T* tp, int6
 
 template <typename T>
 __global__ void __launch_bounds__(TT, 1) k_trsv(TrsvGeo g, MatB<const T> t, MatB<T> x, T alpha, T* pub,
-                                             const int32_t* skip) {
+                                             const int32_t* skip, unsigned long long* ticket) {
   using SN = Sentinel<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* S = reinterpret_cast<T*>(smem_raw);  // diagonal block, then partial sums P[4][NR][BR]
@@ -149,7 +149,14 @@ __global__ void __launch_bounds__(TT, 1) k_trsv(TrsvGeo g, MatB<const T> t, MatB
   T(*Y)[NR][BR] = reinterpret_cast<T(*)[NR][BR]>(rd + BR);            // [NY][NR][BR]
   T(*R)[BR] = reinterpret_cast<T(*)[BR]>(rd + BR + NY * NR * BR);     // [NR][BR] right-hand side
   T* ring = rd + BR + (NY + 1) * NR * BR;                             // [NS][BR * TLD]
-  const int64_t b = blockIdx.x / g.nblk, i = blockIdx.x % g.nblk;
+  // Logical block = an atomic ticket, not blockIdx: block (b, i) waits only on
+  // blocks (b, j < i), whose tickets were drawn by CTAs that are already
+  // resident, so forward progress never depends on the order in which the
+  // hardware dispatches CTAs (concurrent streams, MPS).
+  __shared__ unsigned long long tk;
+  if (threadIdx.x == 0) tk = atomicAdd(ticket, 1ull);
+  __syncthreads();
+  const int64_t b = (int64_t)(tk / (unsigned long long)g.nblk), i = (int64_t)(tk % (unsigned long long)g.nblk);
   if (slice_failed(skip, b)) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t r0 = i * BR;
@@ -270,6 +277,12 @@ bool trsv_eligible(int64_t nt, int64_t nvec) {
 }
 
 template <typename T>
+size_t ws_trsv(int64_t batch, int64_t m, int64_t n, bool right) {
+  (void)right;
+  return carve_bound(sizeof(T) * (size_t)(batch * m * n)) + carve_bound(sizeof(unsigned long long));
+}
+
+template <typename T>
 dla_status trsv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x, bool right, bool trans,
                 bool lower, T alpha) {
   const bool op_lower = (lower != trans);
@@ -281,22 +294,22 @@ dla_status trsv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T>
   g.s_tt = right ? !trans : trans;
   g.slower = right ? !op_lower : op_lower;
   const size_t pub_bytes = sizeof(T) * (size_t)(batch * g.nvec * g.nt);
-  Scratch pub(pub_bytes, c.stream);
-  if (!pub.p) return DLA_ERR_CUDA;
+  DLAB_SCRATCH(pub, c, pub_bytes);
+  DLAB_SCRATCH(tick, c, sizeof(unsigned long long));
   if (cudaMemsetAsync(pub.p, 0xFF, pub_bytes, c.stream) != cudaSuccess) return DLA_ERR_CUDA;  // sentinel
+  if (cudaMemsetAsync(tick.p, 0, sizeof(unsigned long long), c.stream) != cudaSuccess) return DLA_ERR_CUDA;
   const size_t sm = sizeof(T) * (2 * BR * SLD + BR + (NY + 1) * NR * BR + NS * BR * TLD);
-  static bool once = false;
-  if (!once) {
-    cudaFuncSetAttribute(k_trsv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    once = true;
-  }
-  k_trsv<T><<<(unsigned)(batch * g.nblk), TT, sm, c.stream>>>(g, t, x, alpha, pub.as<T>(), c.info);
+  ensure_smem_attr(k_trsv<T>, sm);
+  k_trsv<T><<<(unsigned)(batch * g.nblk), TT, sm, c.stream>>>(g, t, x, alpha, pub.as<T>(), c.info,
+                                                               tick.as<unsigned long long>());
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }
 
 template bool trsv_eligible<double>(int64_t, int64_t);
 template bool trsv_eligible<float>(int64_t, int64_t);
+template size_t ws_trsv<double>(int64_t, int64_t, int64_t, bool);
+template size_t ws_trsv<float>(int64_t, int64_t, int64_t, bool);
 template dla_status trsv<double>(const Ctx&, int64_t, int64_t, int64_t, MatB<const double>, MatB<double>, bool, bool,
                                  bool, double);
 template dla_status trsv<float>(const Ctx&, int64_t, int64_t, int64_t, MatB<const float>, MatB<float>, bool, bool,

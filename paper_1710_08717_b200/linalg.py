@@ -19,7 +19,7 @@ import math
 
 import torch
 
-from ._lib import OPS, STATUS_NAMES, lib
+from ._lib import OPS, STATUS_NAMES, WS_BACKWARD, WS_RIGHTSIDE, lib
 
 __all__ = [
     "Error", "ShapeError", "NotPositiveDefiniteError", "SingularError", "ConvergenceError",
@@ -156,10 +156,16 @@ def _check(info, batch, t, what):
 
 
 def _ws(op, t, batch, m, n, k=0, phase=0):
+    """Caller-owned workspace for one call (include/dla.h: the library never
+    allocates): dla_workspace_bytes bytes from torch's caching allocator on
+    the current stream -- stream-ordered, so it may be recycled by the next
+    call on the same stream (every internal fork is joined back to the
+    caller's stream before the op returns).  Returns (tensor or None, bytes)."""
     dt = 1 if t.dtype == torch.float64 else 0
-    nbytes = lib().lib.dla_workspace_bytes(OPS[op], dt, batch, m, n, k, phase)
-    ws = torch.empty(max(int(nbytes), 8), dtype=torch.uint8, device=t.device)
-    return ws, int(nbytes)
+    nbytes = int(lib().lib.dla_workspace_bytes(OPS[op], dt, batch, m, n, k, phase))
+    if nbytes == 0:
+        return None, 0
+    return torch.empty(nbytes, dtype=torch.uint8, device=t.device), nbytes
 
 
 def eps_gap_default(dtype) -> float:
@@ -183,7 +189,8 @@ def gemm_into(c, a, b, ta=False, tb=False, alpha=1.0, beta=0.0):
         raise ShapeError(f"gemm2: inner dimensions disagree ({k} vs {kb})")
     if _shape_of(c) != (m, n):
         raise ShapeError(f"gemm2: output is {tuple(_shape_of(c))}, expected {m}x{n}")
-    _call("gemm_fwd", c, batch, m, n, k, _p(c), _p(a), _p(b), int(ta), int(tb), alpha, beta, _stream(c))
+    ws, nb = _ws("gemm", c, batch, m, n, k)
+    _call("gemm_fwd", c, batch, m, n, k, _p(c), _p(a), _p(b), int(ta), int(tb), alpha, beta, _p(ws), nb, _stream(c))
     return c
 
 
@@ -206,7 +213,8 @@ def syrk_into(b, a, ta=False, alpha=1.0):
     n, k = (ac, ar) if ta else (ar, ac)
     if _shape_of(b) != (n, n):
         raise ShapeError(f"syrk: output must be {n}x{n}")
-    _call("syrk_fwd", b, batch, n, k, _p(b), _p(a), int(ta), alpha, _stream(b))
+    ws, nb = _ws("syrk", b, batch, n, n, k)
+    _call("syrk_fwd", b, batch, n, k, _p(b), _p(a), int(ta), alpha, _p(ws), nb, _stream(b))
     return b
 
 
@@ -231,7 +239,9 @@ def trmm_inplace(t, x, rightside=False, transpose=False, lower=True, alpha=1.0):
     """dl/blas.hpp:202-291"""
     batch = _prep("trmm", x, t)
     m, n = _tri_check(t, x, rightside, "trmm")
-    _call("trmm_fwd", x, batch, m, n, _p(t), _p(x), int(rightside), int(transpose), int(lower), alpha, _stream(x))
+    ws, nb = _ws("trmm", x, batch, m, n, 0, WS_RIGHTSIDE if rightside else 0)
+    _call("trmm_fwd", x, batch, m, n, _p(t), _p(x), int(rightside), int(transpose), int(lower), alpha, _p(ws), nb,
+          _stream(x))
     return x
 
 
@@ -244,8 +254,9 @@ def trsm_inplace(t, x, rightside=False, transpose=False, lower=True, alpha=1.0, 
     batch = _prep("trsm", x, t)
     m, n = _tri_check(t, x, rightside, "trsm")
     info = _info(batch, x.device)
+    ws, nb = _ws("trsm", x, batch, m, n, 0, WS_RIGHTSIDE if rightside else 0)
     _call("trsm_fwd", x, batch, m, n, _p(t), _p(x), int(rightside), int(transpose), int(lower), alpha,
-          _p(info), _stream(x))
+          _p(info), _p(ws), nb, _stream(x))
     if check:
         _check(info, batch, x, "trsm")
     return x
@@ -267,7 +278,8 @@ def potrf_inplace(a, lower=True, check=True, info=None):
     batch = _prep("potrf", a)
     n = _square(a, "potrf")
     info = _info(batch, a.device) if info is None else info
-    _call("potrf_fwd", a, batch, n, _p(a), int(lower), _p(info), _stream(a))
+    ws, nb = _ws("potrf", a, batch, n, n)
+    _call("potrf_fwd", a, batch, n, _p(a), int(lower), _p(info), _p(ws), nb, _stream(a))
     if check:
         _check(info, batch, a, "potrf")
     return a
@@ -282,7 +294,8 @@ def potri_inplace(a, lower=True, check=True):
     batch = _prep("potri", a)
     n = _square(a, "potri")
     info = _info(batch, a.device)
-    _call("potri_fwd", a, batch, n, _p(a), int(lower), _p(info), _stream(a))
+    ws, nb = _ws("potri", a, batch, n, n)
+    _call("potri_fwd", a, batch, n, _p(a), int(lower), _p(info), _p(ws), nb, _stream(a))
     if check:
         _check(info, batch, a, "potri")
     return a
@@ -298,7 +311,7 @@ def sumlogdiag(a, out=None):
     n = _square(a, "sumlogdiag")
     if out is None:
         out = torch.empty(a.shape[:-2] if a.dim() == 3 else (1,), dtype=a.dtype, device=a.device)
-    _call("sumlogdiag_fwd", a, batch, n, _p(out), _p(a), _stream(a))
+    _call("sumlogdiag_fwd", a, batch, n, _p(out), _p(a), None, 0, _stream(a))
     return out
 
 
@@ -314,7 +327,9 @@ def chol_chain_fwdbwd(a, y, phi=None, abar=None, ybar=None, check=True, info=Non
     abar = torch.empty_like(a) if abar is None else abar
     ybar = torch.empty_like(y) if ybar is None else ybar
     info = _info(batch, a.device) if info is None else info
-    _call("chol_chain_fwdbwd", a, batch, n, _p(a), _p(y), _p(phi), _p(abar), _p(ybar), _p(info), _stream(a))
+    ws, nb = _ws("chol_chain", a, batch, n, n)
+    _call("chol_chain_fwdbwd", a, batch, n, _p(a), _p(y), _p(phi), _p(abar), _p(ybar), _p(info), _p(ws), nb,
+          _stream(a))
     if check:
         _check(info, batch, a, "chol_chain")
     return phi, abar, ybar
@@ -367,8 +382,9 @@ def gemm2_backward_into(abar, bbar, cbar, a, b, ta, tb, alpha=1.0):
     batch = _prep("gemm2_backward", abar, bbar, cbar, a, b)
     m, n = _shape_of(cbar)
     k = a.shape[-2] if ta else a.shape[-1]
+    ws, nb = _ws("gemm2", a, batch, m, n, k, WS_BACKWARD)
     _call("gemm2_bwd", a, batch, m, n, k, _p(abar), _p(bbar), _p(cbar), _p(a), _p(b), int(ta), int(tb), alpha,
-          _stream(a))
+          _p(ws), nb, _stream(a))
     return abar, bbar
 
 
@@ -381,8 +397,9 @@ def gemm_backward_into(abar, bbar, cbar_io, a, b, ta, tb, alpha=1.0, beta=0.0):
     batch = _prep("gemm_backward", abar, bbar, cbar_io, a, b)
     m, n = _shape_of(cbar_io)
     k = a.shape[-2] if ta else a.shape[-1]
+    ws, nb = _ws("gemm", a, batch, m, n, k, WS_BACKWARD)
     _call("gemm_bwd", a, batch, m, n, k, _p(abar), _p(bbar), _p(cbar_io), _p(a), _p(b), int(ta), int(tb), alpha,
-          beta, _stream(a))
+          beta, _p(ws), nb, _stream(a))
     return abar, bbar, cbar_io
 
 
@@ -391,7 +408,8 @@ def syrk_backward_into(abar, bbar, a, ta, alpha=1.0):
     batch = _prep("syrk_backward", abar, bbar, a)
     ar, ac = _shape_of(a)
     n, k = (ac, ar) if ta else (ar, ac)
-    _call("syrk_bwd", a, batch, n, k, _p(abar), _p(bbar), _p(a), int(ta), alpha, _stream(a))
+    ws, nb = _ws("syrk", a, batch, n, n, k, WS_BACKWARD)
+    _call("syrk_bwd", a, batch, n, k, _p(abar), _p(bbar), _p(a), int(ta), alpha, _p(ws), nb, _stream(a))
     return abar
 
 
@@ -403,8 +421,9 @@ def trmm_backward_into(abar, tbar, bbar, t, a, rightside, transpose, lower, alph
     """dl/adjoints.hpp:94-110; abar may alias bbar."""
     batch = _prep("trmm_backward", abar, tbar, bbar, t, a)
     m, n = _tri_check(t, a, rightside, "trmm_backward")
+    ws, nb = _ws("trmm", a, batch, m, n, 0, WS_BACKWARD | (WS_RIGHTSIDE if rightside else 0))
     _call("trmm_bwd", a, batch, m, n, _p(abar), _p(tbar), _p(bbar), _p(t), _p(a), int(rightside), int(transpose),
-          int(lower), alpha, _stream(a))
+          int(lower), alpha, _p(ws), nb, _stream(a))
     return abar, tbar
 
 
@@ -417,8 +436,9 @@ def trsm_backward_into(abar, tbar, bbar, t, b, rightside, transpose, lower, alph
     """dl/adjoints.hpp:131-153; reads the forward OUTPUT b; abar may alias bbar."""
     batch = _prep("trsm_backward", abar, tbar, bbar, t, b)
     m, n = _tri_check(t, b, rightside, "trsm_backward")
+    ws, nb = _ws("trsm", b, batch, m, n, 0, WS_BACKWARD | (WS_RIGHTSIDE if rightside else 0))
     _call("trsm_bwd", b, batch, m, n, _p(abar), _p(tbar), _p(bbar), _p(t), _p(b), int(rightside), int(transpose),
-          int(lower), alpha, _stream(b))
+          int(lower), alpha, _p(ws), nb, _stream(b))
     return abar, tbar
 
 
@@ -431,7 +451,8 @@ def potrf_backward_into(abar, lbar, l, lower=True):
     """dl/adjoints.hpp:175-191; abar may alias lbar."""
     batch = _prep("potrf_backward", abar, lbar, l)
     n = _square(l, "potrf_backward")
-    _call("potrf_bwd", l, batch, n, _p(abar), _p(lbar), _p(l), int(lower), _stream(l))
+    ws, nb = _ws("potrf", l, batch, n, n, 0, WS_BACKWARD)
+    _call("potrf_bwd", l, batch, n, _p(abar), _p(lbar), _p(l), int(lower), _p(ws), nb, _stream(l))
     return abar
 
 
@@ -443,7 +464,8 @@ def potri_backward_into(lbar_out, bbar, l, b, lower=True):
     """dl/adjoints.hpp:207-223"""
     batch = _prep("potri_backward", lbar_out, bbar, l, b)
     n = _square(l, "potri_backward")
-    _call("potri_bwd", l, batch, n, _p(lbar_out), _p(bbar), _p(l), _p(b), int(lower), _stream(l))
+    ws, nb = _ws("potri", l, batch, n, n, 0, WS_BACKWARD)
+    _call("potri_bwd", l, batch, n, _p(lbar_out), _p(bbar), _p(l), _p(b), int(lower), _p(ws), nb, _stream(l))
     return lbar_out
 
 
@@ -458,7 +480,7 @@ def sumlogdiag_backward_into(abar, gbar, a, accumulate=False):
     gbar = gbar.reshape(-1).contiguous()
     if gbar.numel() != batch:
         raise ShapeError("sumlogdiag_backward: one cotangent per slice")
-    _call("sumlogdiag_bwd", a, batch, n, _p(abar), _p(gbar), _p(a), int(accumulate), _stream(a))
+    _call("sumlogdiag_bwd", a, batch, n, _p(abar), _p(gbar), _p(a), int(accumulate), None, 0, _stream(a))
     return abar
 
 
@@ -466,7 +488,7 @@ def gelqf_backward_into(abar, qbar, lbar, q, l):
     """dl/adjoints.hpp:239-252 (one m x m workspace per slice)."""
     batch = _prep("gelqf_backward", abar, qbar, lbar, q, l)
     m, n = _shape_of(q)
-    ws, nb = _ws("gelqf", q, batch, m, n, 0, 1)
+    ws, nb = _ws("gelqf", q, batch, m, n, 0, WS_BACKWARD)
     _call("gelqf_bwd", q, batch, m, n, _p(abar), _p(qbar), _p(lbar), _p(q), _p(l), _p(ws), nb, _stream(q))
     return abar
 
@@ -481,7 +503,7 @@ def syevd_backward_into(abar, ubar, lambdabar, u, lam, eps_gap=None):
     n = _square(u, "syevd_backward")
     if eps_gap is None:
         eps_gap = eps_gap_default(u.dtype)
-    ws, nb = _ws("syevd", u, batch, n, n, 0, 1)
+    ws, nb = _ws("syevd", u, batch, n, n, 0, WS_BACKWARD)
     lambdabar = lambdabar.contiguous()
     lam = lam.contiguous()
     _call("syevd_bwd", u, batch, n, _p(abar), _p(ubar), _p(lambdabar), _p(u), _p(lam), eps_gap, _p(ws), nb,
