@@ -15,6 +15,7 @@ one dtype.  Numerical failures are reported per slice; with ``check=True``
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import math
 
 import torch
@@ -155,14 +156,19 @@ def _check(info, batch, t, what):
         _raise_info(st, first.value, idx.value, what)
 
 
+@functools.lru_cache(maxsize=4096)
+def _ws_bytes(op, dt, batch, m, n, k, phase):
+    """dla_workspace_bytes is host-only and deterministic: cached per shape."""
+    return int(lib().lib.dla_workspace_bytes(op, dt, batch, m, n, k, phase))
+
+
 def _ws(op, t, batch, m, n, k=0, phase=0):
     """Caller-owned workspace for one call (include/dla.h: the library never
     allocates): dla_workspace_bytes bytes from torch's caching allocator on
     the current stream -- stream-ordered, so it may be recycled by the next
     call on the same stream (every internal fork is joined back to the
     caller's stream before the op returns).  Returns (tensor or None, bytes)."""
-    dt = 1 if t.dtype == torch.float64 else 0
-    nbytes = int(lib().lib.dla_workspace_bytes(OPS[op], dt, batch, m, n, k, phase))
+    nbytes = _ws_bytes(OPS[op], 1 if t.dtype == torch.float64 else 0, batch, m, n, k, phase)
     if nbytes == 0:
         return None, 0
     return torch.empty(nbytes, dtype=torch.uint8, device=t.device), nbytes
