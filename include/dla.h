@@ -219,6 +219,23 @@ dla_status dla_info_check(const int32_t* info, int64_t batch, void* stream,
                                const T* lambdabar, const T* u, const T* lambda,     \
                                T eps_gap, void* ws, size_t ws_bytes, void* stream);
 
+/* gesvd: thin SVD of a wide A (m x n, m <= n), A = U^T diag(lambda) V; ROWS of U
+ * (m x m) / V (m x n) are the singular vectors, lambda ascending >= 0, the sign
+ * rule of dl/eigen_sym.hpp:316-333 on U's rows with V's rows flipped in
+ * lockstep; v: in A, out V (dl/svd.hpp:229-284).  info: CONVERGENCE(sweeps).
+ * Pullback (dl/adjoints.hpp:315-382): abar may alias vbar; every lambda_i must
+ * exceed eps_gap, else SINGULAR(i) in info and the slice is left untouched. */
+#define DLA_DECLARE_GESVD(T, S)                                                                   \
+  dla_status dla_gesvd_fwd_##S(int64_t batch, int64_t m, int64_t n, T* v, T* u, T* lambda,      \
+                               int32_t* info, void* ws, size_t ws_bytes, void* stream);         \
+  dla_status dla_gesvd_bwd_##S(int64_t batch, int64_t m, int64_t n, T* abar, const T* ubar,     \
+                               const T* lambdabar, const T* vbar, const T* u, const T* lambda,  \
+                               const T* v, T eps_gap, int32_t* info, void* ws, size_t ws_bytes, \
+                               void* stream);
+
+DLA_DECLARE_GESVD(float, f32)
+DLA_DECLARE_GESVD(double, f64)
+
 DLA_DECLARE_OPS(float, f32)
 DLA_DECLARE_OPS(double, f64)
 

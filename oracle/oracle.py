@@ -261,6 +261,31 @@ class Port(_Lib):
         self._chk(st)
         return abar
 
+    def gesvd(self, a):
+        """dl/svd.hpp:229-284: (u [m,m], lambda [m] ascending, v [m,n])."""
+        v = np.array(a, copy=True, order="C")
+        m, n = v.shape
+        u = np.zeros((m, m), v.dtype)
+        lam = np.zeros(m, v.dtype)
+        ws = np.zeros(2 * n * m + 2 * m * m + 2 * m + 1, v.dtype)
+        idx = _i64(-1)
+        st = self.fn("gesvd", v.dtype)(_i64(m), _i64(n), _ptr(v), _ptr(u), _ptr(lam), _ptr(ws), C.byref(idx))
+        self._chk(st, idx)
+        return u, lam, v
+
+    def gesvd_bwd(self, ubar, lambdabar, vbar, u, lam, v, eps_gap=None):
+        m, n = v.shape
+        if eps_gap is None:
+            eps_gap = 1e-8 if v.dtype == np.float64 else 1e-4
+        abar = np.zeros_like(v)
+        work = np.zeros(m * m + m + m * n, v.dtype)
+        idx = _i64(-1)
+        a = [np.ascontiguousarray(x) for x in (ubar, lambdabar, vbar, u, lam, v)]
+        st = self.fn("gesvd_bwd", v.dtype)(_i64(m), _i64(n), _ptr(abar), *[_ptr(x) for x in a],
+                                           _ctype(v.dtype)(eps_gap), _ptr(work), C.byref(idx))
+        self._chk(st, idx)
+        return abar
+
     def sumlogdiag(self, a):
         f = self.fn("sumlogdiag", a.dtype)
         f.restype = _ctype(a.dtype)
@@ -332,6 +357,28 @@ class Ref(_Lib):
                                            _ptr(np.ascontiguousarray(lam)),
                                            _ctype(u.dtype)(eps_gap))
         self._chk(st)
+        return abar
+
+    def gesvd(self, a):
+        v = np.array(a, copy=True, order="C")
+        m, n = v.shape
+        u = np.zeros((m, m), v.dtype)
+        lam = np.zeros(m, v.dtype)
+        idx = _i64(-1)
+        st = self.fn("gesvd", v.dtype)(_i64(m), _i64(n), _ptr(v), _ptr(u), _ptr(lam), C.byref(idx))
+        self._chk(st, idx)
+        return u, lam, v
+
+    def gesvd_bwd(self, ubar, lambdabar, vbar, u, lam, v, eps_gap=None):
+        m, n = v.shape
+        if eps_gap is None:
+            eps_gap = 1e-8 if v.dtype == np.float64 else 1e-4
+        abar = np.zeros_like(v)
+        idx = _i64(-1)
+        a = [np.ascontiguousarray(x) for x in (ubar, lambdabar, vbar, u, lam, v)]
+        st = self.fn("gesvd_bwd", v.dtype)(_i64(m), _i64(n), _ptr(abar), *[_ptr(x) for x in a],
+                                           _ctype(v.dtype)(eps_gap), C.byref(idx))
+        self._chk(st, idx)
         return abar
 
     def sumlogdiag(self, a, with_grad=False):

@@ -876,4 +876,302 @@ int FN(o_syevd_bwd)(int64_t n, R* abar, const R* ubar, const R* lambdabar, const
   return DLA_OK;
 }
 
+/* ------------------------------------------------------------------ gesvd */
+
+/* Golub-Kahan-Reinsch on a (rows M >= cols N), dl/svd.hpp:26-223: a becomes
+ * the economy left factor, w the singular values, v (N x N) the right factor.
+ * rv1: N reals.  Returns DLA_ERR_CONVERGENCE (*idx = total iterations) after
+ * 30 sweeps on one singular value. */
+static int FN(svd_gkr)(int64_t m, int64_t n, R* a, R* w, R* v, R* rv1, int64_t* idx) {
+  const R eps = (R)EPS;
+  R g = 0, scale = 0, anorm = 0, s, f, h, c, x, y, z;
+  int64_t l = 0, nm = 0;
+#define A_(i, j) AT(a, n, i, j)
+#define V_(i, j) AT(v, n, i, j)
+  for (int64_t i = 0; i < n; ++i) {
+    l = i + 1;
+    rv1[i] = scale * g;
+    g = scale = 0;
+    if (i < m) {
+      for (int64_t k = i; k < m; ++k) scale += FN(absr)(A_(k, i));
+      if (scale != (R)0) {
+        s = 0;
+        for (int64_t k = i; k < m; ++k) {
+          A_(k, i) /= scale;
+          s += A_(k, i) * A_(k, i);
+        }
+        f = A_(i, i);
+        g = -FN(sign_like)((R)SQRT(s), f);
+        h = f * g - s;
+        A_(i, i) = f - g;
+        for (int64_t j = l; j < n; ++j) {
+          s = 0;
+          for (int64_t k = i; k < m; ++k) s += A_(k, i) * A_(k, j);
+          f = s / h;
+          for (int64_t k = i; k < m; ++k) A_(k, j) += f * A_(k, i);
+        }
+        for (int64_t k = i; k < m; ++k) A_(k, i) *= scale;
+      }
+    }
+    w[i] = scale * g;
+    g = scale = 0;
+    if (i < m && i != n - 1) {
+      for (int64_t k = l; k < n; ++k) scale += FN(absr)(A_(i, k));
+      if (scale != (R)0) {
+        s = 0;
+        for (int64_t k = l; k < n; ++k) {
+          A_(i, k) /= scale;
+          s += A_(i, k) * A_(i, k);
+        }
+        f = A_(i, l);
+        g = -FN(sign_like)((R)SQRT(s), f);
+        h = f * g - s;
+        A_(i, l) = f - g;
+        for (int64_t k = l; k < n; ++k) rv1[k] = A_(i, k) / h;
+        for (int64_t j = l; j < m; ++j) {
+          s = 0;
+          for (int64_t k = l; k < n; ++k) s += A_(j, k) * A_(i, k);
+          for (int64_t k = l; k < n; ++k) A_(j, k) += s * rv1[k];
+        }
+        for (int64_t k = l; k < n; ++k) A_(i, k) *= scale;
+      }
+    }
+    {
+      const R t = FN(absr)(w[i]) + FN(absr)(rv1[i]);
+      if (t > anorm) anorm = t;
+    }
+  }
+  for (int64_t i = n - 1; i >= 0; --i) {
+    if (i < n - 1) {
+      if (g != (R)0) {
+        for (int64_t j = l; j < n; ++j) V_(j, i) = (A_(i, j) / A_(i, l)) / g;
+        for (int64_t j = l; j < n; ++j) {
+          s = 0;
+          for (int64_t k = l; k < n; ++k) s += A_(i, k) * V_(k, j);
+          for (int64_t k = l; k < n; ++k) V_(k, j) += s * V_(k, i);
+        }
+      }
+      for (int64_t j = l; j < n; ++j) V_(i, j) = V_(j, i) = 0;
+    }
+    V_(i, i) = 1;
+    g = rv1[i];
+    l = i;
+  }
+  for (int64_t i = (m < n ? m : n) - 1; i >= 0; --i) {
+    l = i + 1;
+    g = w[i];
+    for (int64_t j = l; j < n; ++j) A_(i, j) = 0;
+    if (g != (R)0) {
+      g = (R)1 / g;
+      for (int64_t j = l; j < n; ++j) {
+        s = 0;
+        for (int64_t k = l; k < m; ++k) s += A_(k, i) * A_(k, j);
+        f = (s / A_(i, i)) * g;
+        for (int64_t k = i; k < m; ++k) A_(k, j) += f * A_(k, i);
+      }
+      for (int64_t j = i; j < m; ++j) A_(j, i) *= g;
+    } else {
+      for (int64_t j = i; j < m; ++j) A_(j, i) = 0;
+    }
+    A_(i, i) += (R)1;
+  }
+  int64_t total_iter = 0;
+  for (int64_t k = n - 1; k >= 0; --k) {
+    for (int64_t its = 1;; ++its) {
+      int flag = 1;
+      for (l = k; l >= 0; --l) {
+        nm = l - 1;
+        if (FN(absr)(rv1[l]) <= eps * anorm) {
+          flag = 0;
+          break;
+        }
+        if (FN(absr)(w[nm]) <= eps * anorm) break;
+      }
+      if (flag) {
+        c = 0;
+        s = 1;
+        for (int64_t i = l; i <= k; ++i) {
+          f = s * rv1[i];
+          rv1[i] = c * rv1[i];
+          if (FN(absr)(f) <= eps * anorm) break;
+          g = w[i];
+          h = FN(pythag)(f, g);
+          w[i] = h;
+          h = (R)1 / h;
+          c = g * h;
+          s = -f * h;
+          for (int64_t j = 0; j < m; ++j) {
+            y = A_(j, nm);
+            z = A_(j, i);
+            A_(j, nm) = y * c + z * s;
+            A_(j, i) = z * c - y * s;
+          }
+        }
+      }
+      z = w[k];
+      if (l == k) {
+        if (z < (R)0) {
+          w[k] = -z;
+          for (int64_t j = 0; j < n; ++j) V_(j, k) = -V_(j, k);
+        }
+        break;
+      }
+      if (its == 30) {
+        if (idx) *idx = total_iter;
+        return DLA_ERR_CONVERGENCE;
+      }
+      ++total_iter;
+      x = w[l];
+      nm = k - 1;
+      y = w[nm];
+      g = rv1[nm];
+      h = rv1[k];
+      f = ((y - z) * (y + z) + (g - h) * (g + h)) / ((R)2 * h * y);
+      g = FN(pythag)(f, (R)1);
+      f = ((x - z) * (x + z) + h * ((y / (f + FN(sign_like)(g, f))) - h)) / x;
+      c = s = 1;
+      for (int64_t j = l; j <= nm; ++j) {
+        const int64_t i = j + 1;
+        g = rv1[i];
+        y = w[i];
+        h = s * g;
+        g = c * g;
+        z = FN(pythag)(f, h);
+        rv1[j] = z;
+        c = f / z;
+        s = h / z;
+        f = x * c + g * s;
+        g = g * c - x * s;
+        h = y * s;
+        y *= c;
+        for (int64_t jj = 0; jj < n; ++jj) {
+          x = V_(jj, j);
+          z = V_(jj, i);
+          V_(jj, j) = x * c + z * s;
+          V_(jj, i) = z * c - x * s;
+        }
+        z = FN(pythag)(f, h);
+        w[j] = z;
+        if (z != (R)0) {
+          z = (R)1 / z;
+          c = f * z;
+          s = h * z;
+        }
+        f = c * g + s * y;
+        x = c * y - s * g;
+        for (int64_t jj = 0; jj < m; ++jj) {
+          y = A_(jj, j);
+          z = A_(jj, i);
+          A_(jj, j) = y * c + z * s;
+          A_(jj, i) = z * c - y * s;
+        }
+      }
+      rv1[l] = 0;
+      rv1[k] = f;
+      w[k] = x;
+    }
+  }
+#undef A_
+#undef V_
+  return DLA_OK;
+}
+
+/* v: in A (m x n, m <= n), out V; u: out U (m x m); lambda ascending (stable
+ * sort), sign rule on U's rows mirrored onto V (dl/svd.hpp:229-284).
+ * ws: n*m + m*m + m*m + m*n + 2m reals. */
+int FN(o_gesvd)(int64_t m, int64_t n, R* v, R* u, R* lambda, R* ws, int64_t* idx) {
+  if (m > n) return DLA_ERR_SHAPE;
+  if (m == 0) return DLA_OK;
+  R* wt = ws;             /* n x m */
+  R* vs = wt + n * m;     /* m x m */
+  R* ut = vs + m * m;     /* m x m */
+  R* vt = ut + m * m;     /* m x n */
+  R* rv1 = vt + m * n;    /* m */
+  R* lt = rv1 + m;        /* m */
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) AT(wt, m, j, i) = AT(v, n, i, j);
+  int st = FN(svd_gkr)(n, m, wt, lambda, vs, rv1, idx);
+  if (st != DLA_OK) return st;
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t k = 0; k < m; ++k) AT(u, m, i, k) = AT(vs, m, k, i);
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) AT(v, n, i, j) = AT(wt, m, j, i);
+  /* stable ascending sort: insertion sort of the permutation (ties keep order) */
+  int64_t* perm = (int64_t*)malloc(sizeof(int64_t) * (size_t)m);
+  for (int64_t i = 0; i < m; ++i) perm[i] = i;
+  for (int64_t i = 1; i < m; ++i) {
+    const int64_t p = perm[i];
+    int64_t j = i - 1;
+    while (j >= 0 && lambda[p] < lambda[perm[j]]) {
+      perm[j + 1] = perm[j];
+      --j;
+    }
+    perm[j + 1] = p;
+  }
+  for (int64_t i = 0; i < m; ++i) {
+    const int64_t sidx = perm[i];
+    lt[i] = lambda[sidx];
+    memcpy(ut + i * m, u + sidx * m, sizeof(R) * (size_t)m);
+    memcpy(vt + i * n, v + sidx * n, sizeof(R) * (size_t)n);
+  }
+  free(perm);
+  memcpy(lambda, lt, sizeof(R) * (size_t)m);
+  memcpy(u, ut, sizeof(R) * (size_t)(m * m));
+  memcpy(v, vt, sizeof(R) * (size_t)(m * n));
+  /* sign rule on U, V's row flipped in lockstep */
+  for (int64_t i = 0; i < m; ++i) {
+    R* row = u + i * m;
+    int64_t kmax = 0;
+    R best = FN(absr)(row[0]);
+    for (int64_t k = 1; k < m; ++k)
+      if (FN(absr)(row[k]) > best) {
+        best = FN(absr)(row[k]);
+        kmax = k;
+      }
+    if (row[kmax] < (R)0) {
+      for (int64_t k = 0; k < m; ++k) row[k] = -row[k];
+      for (int64_t j = 0; j < n; ++j) AT(v, n, i, j) = -AT(v, n, i, j);
+    }
+  }
+  return DLA_OK;
+}
+
+/* dl/adjoints.hpp:315-382; work: m*m + m + m*n reals.  SINGULAR(i) when a
+ * singular value is not above eps_gap. */
+int FN(o_gesvd_bwd)(int64_t m, int64_t n, R* abar, const R* ubar, const R* lambdabar, const R* vbar,
+                    const R* u, const R* lambda, const R* v, R eps_gap, R* work, int64_t* idx) {
+  for (int64_t i = 0; i < m; ++i)
+    if (!(lambda[i] > eps_gap)) {
+      if (idx) *idx = i;
+      return DLA_ERR_SINGULAR;
+    }
+  R* w = work;
+  R* dvec = w + m * m;
+  R* tmp = dvec + m;
+  for (int64_t i = 0; i < m; ++i) {
+    const R inv = (R)1 / lambda[i];
+    for (int64_t j = 0; j < n; ++j) AT(abar, n, i, j) = inv * AT(vbar, n, i, j);
+  }
+  FN(o_gemm)(m, m, n, w, abar, v, 0, 1, (R)1, 0);
+  for (int64_t i = 0; i < m; ++i) dvec[i] = AT(w, m, i, i);
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < m; ++j) AT(w, m, i, j) *= lambda[j];
+  FN(o_gemm)(m, m, m, w, ubar, u, 0, 1, (R)1, 1);
+  for (int64_t i = 0; i < m; ++i) {
+    for (int64_t j = 0; j < i; ++j) {
+      R hd = lambda[i] - lambda[j], hs = lambda[i] + lambda[j];
+      if (hd < eps_gap) hd = eps_gap;
+      if (hs < eps_gap) hs = eps_gap;
+      const R yv = (AT(w, m, i, j) - AT(w, m, j, i)) / (hd * hs);
+      AT(w, m, i, j) = yv * lambda[j];
+      AT(w, m, j, i) = yv * lambda[i];
+    }
+    AT(w, m, i, i) = lambdabar[i] - dvec[i];
+  }
+  FN(o_gemm)(m, n, m, abar, w, v, 0, 0, (R)1, 1);
+  memcpy(tmp, abar, sizeof(R) * (size_t)(m * n));
+  FN(o_gemm)(m, n, m, abar, u, tmp, 1, 0, (R)1, 0);
+  return DLA_OK;
+}
+
 #undef AT

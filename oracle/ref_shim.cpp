@@ -21,6 +21,7 @@
 #include "dlinalg/lq.hpp"
 #include "dlinalg/matrix.hpp"
 #include "dlinalg/models.hpp"
+#include "dlinalg/svd.hpp"
 #include "dlinalg/tape.hpp"
 #include "dlinalg/transforms.hpp"
 
@@ -151,6 +152,19 @@ double now_s() {
       dla::gelqf_backward_into<T>(mv(abar, m, n), cv(qbar, m, n), cv(lbar, m, m), cv(q, m, n),  \
                                   cv(l, m, m));                                                 \
     }, nullptr);                                                                                \
+  }                                                                                             \
+  int ref_gesvd_##S(int64_t m, int64_t n, T* v, T* u, T* lambda, int64_t* idx) {               \
+    return guarded([&] { dla::gesvd_inplace<T>(mv(v, m, n), mv(u, m, m), lambda); }, idx);      \
+  }                                                                                             \
+  int ref_gesvd_bwd_##S(int64_t m, int64_t n, T* abar, const T* ubar, const T* lambdabar,       \
+                        const T* vbar, const T* u, const T* lambda, const T* v, T eps_gap,      \
+                        int64_t* idx) {                                                         \
+    auto cfg = dla::ToleranceConfig<T>::defaults();                                             \
+    cfg.eps_gap = eps_gap;                                                                      \
+    return guarded([&] {                                                                        \
+      dla::gesvd_backward_into<T>(mv(abar, m, n), cv(ubar, m, m), lambdabar, cv(vbar, m, n),    \
+                                  cv(u, m, m), lambda, cv(v, m, n), cfg);                       \
+    }, idx);                                                                                    \
   }                                                                                             \
   int ref_syevd_bwd_##S(int64_t n, T* abar, const T* ubar, const T* lambdabar, const T* u,      \
                         const T* lambda, T eps_gap) {                                           \

@@ -46,6 +46,8 @@ _SIGS = {
     "syevd_fwd": "IIPPPPZP",
     "syevd_bwd": "IIPPPPPSPZP",
     "chol_chain_fwdbwd": "IIPPPPPPPZP",
+    "gesvd_fwd": "IIIPPPPPZP",
+    "gesvd_bwd": "IIIPPPPPPPSPPZP",
 }
 
 

@@ -531,6 +531,31 @@ dla_status syevd_bwd_abi(const Ctx& cx, int64_t batch, int64_t n, T* abar, const
   return ew_sym_into<T>(cx, batch, n, C_(w), pk(abar, n, n));
 }
 
+// --------------------------------------------------------------- gesvd
+template <typename T>
+dla_status gesvd_fwd_abi(const Ctx& cx, int64_t batch, int64_t m, int64_t n, T* v, T* u, T* lambda) {
+  if (bad_dims(batch, m, n) || m > n) return DLA_ERR_SHAPE;
+  const size_t vsz = bytes<T>(batch, m, n), usz = bytes<T>(batch, m, m), lsz = bytes<T>(batch, m, 1);
+  if (overlap(v, vsz, u, usz) || overlap(v, vsz, lambda, lsz) || overlap(u, usz, lambda, lsz)) return DLA_ERR_ALIAS;
+  DLAB_TRY(reset_info(cx, batch));
+  if (batch * m == 0) return DLA_OK;
+  return gesvd_fwd<T>(cx, batch, m, n, v, u, lambda);
+}
+
+template <typename T>
+dla_status gesvd_bwd_abi(const Ctx& cx, int64_t batch, int64_t m, int64_t n, T* abar, const T* ubar,
+                         const T* lambdabar, const T* vbar, const T* u, const T* lambda, const T* v, T eps_gap) {
+  if (bad_dims(batch, m, n) || m > n) return DLA_ERR_SHAPE;
+  const size_t asz = bytes<T>(batch, m, n), usz = bytes<T>(batch, m, m), lsz = bytes<T>(batch, m, 1);
+  if (overlap(abar, asz, ubar, usz) || overlap(abar, asz, lambdabar, lsz) || overlap(abar, asz, u, usz) ||
+      overlap(abar, asz, lambda, lsz) || overlap(abar, asz, v, asz) || (abar != vbar && overlap(abar, asz, vbar, asz)))
+    return DLA_ERR_ALIAS;
+  if (!(eps_gap > T(0))) return DLA_ERR_INVALID;
+  DLAB_TRY(reset_info(cx, batch));
+  if (batch * m == 0) return DLA_OK;
+  return gesvd_bwd<T>(cx, batch, m, n, abar, ubar, lambdabar, vbar, u, lambda, v, eps_gap);
+}
+
 // ------------------------------------------------- fused C1 chain (GP NLL)
 __global__ void k_fill_ones(int64_t n, double* pd, float* pf) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -774,6 +799,9 @@ size_t ws_query(dla_op op, int64_t batch, int64_t m, int64_t n, int64_t k, int p
       return !bwd ? carve_bound(syevd_ws_bytes<T>(batch, n, false)) : ws_syevd_bwd<T>(batch, n);
     case DLA_OP_CHOL_CHAIN:
       return ws_chol_chain<T>(batch, n);
+    case DLA_OP_GESVD:
+      if (m > n) return 0;
+      return !bwd ? ws_gesvd_fwd<T>(batch, m, n) : ws_gesvd_bwd<T>(batch, m, n);
   }
   return 0;
 }
@@ -1008,6 +1036,19 @@ dla_status dla_info_check(const int32_t* info, int64_t batch, void* stream, int6
     DLA_NEED(T, DLA_OP_SYEVD, batch, n, n, 0, DLA_WS_BACKWARD);                                                   \
     DLA_ARENA(ws, wsb, stream, nullptr);                                                                          \
     return syevd_bwd_abi<T>(cx, batch, n, abar, ubar, lambdabar, u, lambda, eps_gap);                             \
+  }                                                                                                               \
+  dla_status dla_gesvd_fwd_##S(int64_t batch, int64_t m, int64_t n, T* v, T* u, T* lambda, int32_t* info,        \
+                               void* ws, size_t wsb, void* stream) {                                              \
+    DLA_NEED(T, DLA_OP_GESVD, batch, m, n, 0, 0);                                                                 \
+    DLA_ARENA(ws, wsb, stream, info);                                                                             \
+    return gesvd_fwd_abi<T>(cx, batch, m, n, v, u, lambda);                                                       \
+  }                                                                                                               \
+  dla_status dla_gesvd_bwd_##S(int64_t batch, int64_t m, int64_t n, T* abar, const T* ubar, const T* lambdabar,   \
+                               const T* vbar, const T* u, const T* lambda, const T* v, T eps_gap, int32_t* info,  \
+                               void* ws, size_t wsb, void* stream) {                                              \
+    DLA_NEED(T, DLA_OP_GESVD, batch, m, n, 0, DLA_WS_BACKWARD);                                                   \
+    DLA_ARENA(ws, wsb, stream, info);                                                                             \
+    return gesvd_bwd_abi<T>(cx, batch, m, n, abar, ubar, lambdabar, vbar, u, lambda, v, eps_gap);                 \
   }                                                                                                               \
   dla_status dla_chol_chain_fwdbwd_##S(int64_t batch, int64_t n, const T* a, const T* y, T* phi, T* abar,         \
                                        T* ybar, int32_t* info, void* ws, size_t wsb, void* stream) {              \

@@ -58,7 +58,8 @@ __device__ void apply_reflector(T* x, int64_t m, int64_t n, int64_t k, const T* 
 }
 
 template <typename T>
-__global__ void __launch_bounds__(GT) k_gelqf(int64_t m, int64_t n, T* qall, T* lall, T* tauall, int32_t* info) {
+__global__ void __launch_bounds__(GT) k_gelqf(int64_t m, int64_t n, T* qall, T* lall, T* tauall, int32_t* info,
+                                              bool rank_check) {
   __shared__ T red[GT / 32];
   __shared__ int fail_row;
   const int64_t b = blockIdx.x;
@@ -69,7 +70,7 @@ __global__ void __launch_bounds__(GT) k_gelqf(int64_t m, int64_t n, T* qall, T* 
   T mx = T(0);
   for (int64_t e = threadIdx.x; e < m * n; e += GT) mx = fmax(mx, fabs(q[e]));
   const T norm_a = block_maxabs(mx, red);
-  if (norm_a == T(0)) {
+  if (norm_a == T(0) && rank_check) {
     if (threadIdx.x == 0) record_failure(info, b, DLA_ERR_SINGULAR, 0);
     return;
   }
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(GT) k_gelqf(int64_t m, int64_t n, T* qall, T* 
     l[e] = j <= i ? q[i * n + j] : T(0);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && rank_check) {
     for (int64_t i = 0; i < m; ++i)
       if (fabs(l[i * m + i]) < rank_tol) {
         fail_row = (int)i;
@@ -155,17 +156,17 @@ size_t gelqf_ws_bytes(int64_t batch, int64_t m, int64_t n, bool backward) {
 }
 
 template <typename T>
-dla_status gelqf_fwd(const Ctx& c, int64_t batch, int64_t m, int64_t n, T* q, T* l, void* ws) {
+dla_status gelqf_fwd(const Ctx& c, int64_t batch, int64_t m, int64_t n, T* q, T* l, void* ws, bool rank_check) {
   if (!ws) return DLA_ERR_WORKSPACE;
-  if (gelqf_blocked_eligible<T>(m, n)) return gelqf_blocked<T>(c, batch, m, n, q, l, ws);
-  k_gelqf<T><<<(unsigned)batch, GT, 0, c.stream>>>(m, n, q, l, static_cast<T*>(ws), c.info);
+  if (gelqf_blocked_eligible<T>(m, n)) return gelqf_blocked<T>(c, batch, m, n, q, l, ws, rank_check);
+  k_gelqf<T><<<(unsigned)batch, GT, 0, c.stream>>>(m, n, q, l, static_cast<T*>(ws), c.info, rank_check);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }
 
 template size_t gelqf_ws_bytes<double>(int64_t, int64_t, int64_t, bool);
 template size_t gelqf_ws_bytes<float>(int64_t, int64_t, int64_t, bool);
-template dla_status gelqf_fwd<double>(const Ctx&, int64_t, int64_t, int64_t, double*, double*, void*);
-template dla_status gelqf_fwd<float>(const Ctx&, int64_t, int64_t, int64_t, float*, float*, void*);
+template dla_status gelqf_fwd<double>(const Ctx&, int64_t, int64_t, int64_t, double*, double*, void*, bool);
+template dla_status gelqf_fwd<float>(const Ctx&, int64_t, int64_t, int64_t, float*, float*, void*, bool);
 
 }  // namespace dlab

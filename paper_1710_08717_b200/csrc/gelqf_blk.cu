@@ -112,7 +112,8 @@ struct LqWs {
 
 // max|A| per slice; all-zero => SINGULAR(0) (dl/lq.hpp:33-36)
 template <typename T>
-__global__ void __launch_bounds__(LT) k_lq_norm(int64_t m, int64_t n, const T* a, T* ws, int32_t* info) {
+__global__ void __launch_bounds__(LT) k_lq_norm(int64_t m, int64_t n, const T* a, T* ws, int32_t* info,
+                                                bool rank_check) {
   __shared__ T red[LT / 32];
   const int64_t b = blockIdx.x;
   const T* ab = a + b * m * n;
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(LT) k_lq_norm(int64_t m, int64_t n, const T* a
   mx = lq_block_max(mx, red);
   if (threadIdx.x == 0) {
     LqWs<T>(ws, m, n, b).nrm[0] = mx;
-    if (mx == T(0)) record_failure(info, b, DLA_ERR_SINGULAR, 0);
+    if (mx == T(0) && rank_check) record_failure(info, b, DLA_ERR_SINGULAR, 0);
   }
 }
 
@@ -227,7 +228,8 @@ __global__ void __launch_bounds__(LT) k_lq_panel(int64_t m, int64_t n, int64_t k
 
 // L = tril(A[:, :m]) and the rank check (dl/lq.hpp:70-77)
 template <typename T>
-__global__ void __launch_bounds__(LT) k_lq_extract(int64_t m, int64_t n, const T* a, T* l, T* ws, int32_t* info) {
+__global__ void __launch_bounds__(LT) k_lq_extract(int64_t m, int64_t n, const T* a, T* l, T* ws, int32_t* info,
+                                                   bool rank_check) {
   const int64_t b = blockIdx.x;
   if (slice_failed(info, b)) return;
   const T* ab = a + b * m * n;
@@ -236,7 +238,7 @@ __global__ void __launch_bounds__(LT) k_lq_extract(int64_t m, int64_t n, const T
     const int64_t i = e / m, j = e % m;
     lb[e] = j <= i ? ab[i * n + j] : T(0);
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && rank_check) {
     const T tol = Num<T>::rank_rtol * LqWs<T>(ws, m, n, b).nrm[0];
     for (int64_t i = 0; i < m; ++i)
       if (fabs(ab[i * n + i]) < tol) {
@@ -342,22 +344,15 @@ size_t gelqf_blocked_ws_bytes(int64_t batch, int64_t m, int64_t n) {
 }
 
 template <typename T>
-dla_status gelqf_blocked(const Ctx& c, int64_t batch, int64_t m, int64_t n, T* q, T* l, void* wsv) {
+dla_status gelqf_blocked(const Ctx& c, int64_t batch, int64_t m, int64_t n, T* q, T* l, void* wsv, bool rank_check) {
   T* ws = static_cast<T*>(wsv);
   const int64_t per = LqWs<T>::per_slice(m, n);
   const size_t sm_panel = panel_smem<T>(n);
   const size_t sm_form = panel_smem<T>(n);
-  static size_t attr_p = 0, attr_f = 0;
-  if (sm_panel > attr_p) {
-    cudaFuncSetAttribute(k_lq_panel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_panel);
-    attr_p = sm_panel;
-  }
-  if (sm_form > attr_f) {
-    cudaFuncSetAttribute(k_lq_form<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_form);
-    attr_f = sm_form;
-  }
+  ensure_smem_attr(k_lq_panel<T>, sm_panel);
+  ensure_smem_attr(k_lq_form<T>, sm_form);
   const unsigned grid = (unsigned)batch;
-  k_lq_norm<T><<<grid, LT, 0, c.stream>>>(m, n, q, ws, c.info);
+  k_lq_norm<T><<<grid, LT, 0, c.stream>>>(m, n, q, ws, c.info, rank_check);
   DLAB_LAUNCH_CHECK();
   // views: A rows / columns from k0; Yc, Z rows k0.. (same geometry); W [m x BP]
   auto av = [&](int64_t r0, int64_t c0) { return MatB<T>{q + r0 * n + c0, n, m * n}; };
@@ -378,7 +373,7 @@ dla_status gelqf_blocked(const Ctx& c, int64_t batch, int64_t m, int64_t n, T* q
     DLAB_TRY(gemm<T>(c, batch, rm, nc, bp, T(-1), MatB<const T>{wm.p, wm.ld, wm.bs}, false,
                      MatB<const T>{w0.z + k0 * n + k0, n, per}, false, T(1), av(k0 + bp, k0), MASK_FULL, c.info));
   }
-  k_lq_extract<T><<<grid, LT, 0, c.stream>>>(m, n, q, l, ws, c.info);
+  k_lq_extract<T><<<grid, LT, 0, c.stream>>>(m, n, q, l, ws, c.info, rank_check);
   DLAB_LAUNCH_CHECK();
   for (int64_t pj = npan - 1; pj >= 0; --pj) {
     const int64_t k0 = pj * BP;
@@ -403,7 +398,7 @@ dla_status gelqf_blocked(const Ctx& c, int64_t batch, int64_t m, int64_t n, T* q
 #define INST(T)                                                                  \
   template bool gelqf_blocked_eligible<T>(int64_t, int64_t);                     \
   template size_t gelqf_blocked_ws_bytes<T>(int64_t, int64_t, int64_t);          \
-  template dla_status gelqf_blocked<T>(const Ctx&, int64_t, int64_t, int64_t, T*, T*, void*);
+  template dla_status gelqf_blocked<T>(const Ctx&, int64_t, int64_t, int64_t, T*, T*, void*, bool);
 INST(double)
 INST(float)
 

@@ -78,19 +78,32 @@ bool gelqf_blocked_eligible(int64_t m, int64_t n);
 template <typename T>
 size_t gelqf_blocked_ws_bytes(int64_t batch, int64_t m, int64_t n);
 template <typename T>
-dla_status gelqf_blocked(const Ctx& c, int64_t batch, int64_t m, int64_t n, T* q, T* l, void* ws);
+dla_status gelqf_blocked(const Ctx& c, int64_t batch, int64_t m, int64_t n, T* q, T* l, void* ws,
+                         bool rank_check = true);
 
 // gelqf.cu
 template <typename T>
 size_t gelqf_ws_bytes(int64_t batch, int64_t m, int64_t n, bool backward);
 template <typename T>
-dla_status gelqf_fwd(const Ctx& c, int64_t batch, int64_t m, int64_t n, T* q, T* l, void* ws);
+dla_status gelqf_fwd(const Ctx& c, int64_t batch, int64_t m, int64_t n, T* q, T* l, void* ws,
+                     bool rank_check = true);
 
 // potrf_tiles.cu: persistent tile-dataflow Cholesky (f64, lower, in place;
 // strict upper untouched)
 bool potrf_tiles_eligible(int64_t batch, int64_t n, const MatB<double>& a);
 dla_status potrf_tiles(const Ctx& c, int64_t batch, int64_t n, MatB<double> a, int64_t kbase);
 size_t ws_potrf_tiles(int64_t batch, int64_t n);
+
+// gesvd.cu: LQ-preconditioned one-sided Jacobi SVD (m <= n) and its pullback
+template <typename T>
+size_t ws_gesvd_fwd(int64_t batch, int64_t m, int64_t n);
+template <typename T>
+size_t ws_gesvd_bwd(int64_t batch, int64_t m, int64_t n);
+template <typename T>
+dla_status gesvd_fwd(const Ctx& c, int64_t batch, int64_t m, int64_t n, T* v, T* u, T* lambda);
+template <typename T>
+dla_status gesvd_bwd(const Ctx& c, int64_t batch, int64_t m, int64_t n, T* abar, const T* ubar, const T* lambdabar,
+                     const T* vbar, const T* u, const T* lambda, const T* v, T eps_gap);
 
 // syevd.cu
 template <typename T>

@@ -31,6 +31,7 @@ __all__ = [
     "trsm_backward_into", "trsm_backward", "potrf_backward_into", "potrf_backward",
     "potri_backward_into", "potri_backward", "sumlogdiag_backward_into", "gelqf_backward_into",
     "gelqf_backward", "syevd_backward_into", "syevd_backward", "eps_gap_default",
+    "gesvd_inplace", "gesvd", "gesvd_backward_into", "gesvd_backward",
 ]
 
 
@@ -382,6 +383,35 @@ def syevd(a, check=True):
     return syevd_inplace(u, lam, check)
 
 
+def gesvd_inplace(v, u, lam, check=True):
+    """dl/svd.hpp:229-284: v in = A (m x n, m <= n), out = V (rows = right
+    singular vectors); u out = U (m x m, rows = left singular vectors); lam
+    out = singular values, ascending.  A = U^T diag(lam) V."""
+    batch = _prep("gesvd", v, u)
+    m, n = _shape_of(v)
+    if m > n:
+        raise ShapeError(f"gesvd: need m <= n, got {m}x{n}")
+    if _shape_of(u) != (m, m):
+        raise ShapeError(f"gesvd: U output must be {m}x{m}")
+    if lam.numel() != batch * m or lam.dtype != v.dtype or not lam.is_contiguous():
+        raise ShapeError("gesvd: lambda output must hold batch x m values of the operand dtype")
+    ws, nb = _ws("gesvd", v, batch, m, n)
+    info = _info(batch, v.device)
+    _call("gesvd_fwd", v, batch, m, n, _p(v), _p(u), _p(lam), _p(info), _p(ws), nb, _stream(v))
+    if check:
+        _check(info, batch, v, "gesvd")
+    return u, lam, v
+
+
+def gesvd(a, check=True):
+    """Returns (U, lambda, V) as the reference's GesvdResult (dl/svd.hpp:286-299)."""
+    v = a.clone()
+    m = a.shape[-2]
+    u = torch.empty(a.shape[:-2] + (m, m), dtype=a.dtype, device=a.device)
+    lam = torch.empty(a.shape[:-2] + (m,), dtype=a.dtype, device=a.device)
+    return gesvd_inplace(v, u, lam, check)
+
+
 # ---------------------------------------------------------------- backward
 def gemm2_backward_into(abar, bbar, cbar, a, b, ta, tb, alpha=1.0):
     """dl/adjoints.hpp:36-49"""
@@ -519,3 +549,25 @@ def syevd_backward_into(abar, ubar, lambdabar, u, lam, eps_gap=None):
 
 def syevd_backward(ubar, lambdabar, u, lam, eps_gap=None):
     return syevd_backward_into(torch.empty_like(u), ubar, lambdabar, u, lam, eps_gap)
+
+
+def gesvd_backward_into(abar, ubar, lambdabar, vbar, u, lam, v, eps_gap=None, check=True):
+    """dl/adjoints.hpp:315-382; abar may alias vbar.  Raises SingularError(i)
+    when lambda_i <= eps_gap (the reference's throw)."""
+    batch = _prep("gesvd_backward", abar, ubar, vbar, u, v)
+    m, n = _shape_of(v)
+    if eps_gap is None:
+        eps_gap = eps_gap_default(v.dtype)
+    ws, nb = _ws("gesvd", v, batch, m, n, 0, WS_BACKWARD)
+    info = _info(batch, v.device)
+    lambdabar = lambdabar.contiguous()
+    lam = lam.contiguous()
+    _call("gesvd_bwd", v, batch, m, n, _p(abar), _p(ubar), _p(lambdabar), _p(vbar), _p(u), _p(lam), _p(v), eps_gap,
+          _p(info), _p(ws), nb, _stream(v))
+    if check:
+        _check(info, batch, v, "gesvd_backward")
+    return abar
+
+
+def gesvd_backward(ubar, lambdabar, vbar, u, lam, v, eps_gap=None):
+    return gesvd_backward_into(torch.empty_like(v), ubar, lambdabar, vbar, u, lam, v, eps_gap)

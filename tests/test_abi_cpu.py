@@ -20,11 +20,11 @@ LIB = os.path.join(ROOT, "paper_1710_08717_b200", "libdla_b200.so")
 def header_symbols():
     src = open(HEADER).read()
     names = set(re.findall(r"\b(dla_[a-z0-9_]+)\s*\(", src))
-    # expand the DLA_DECLARE_OPS(T, S) prototype list for f32 / f64
-    macro = re.search(r"#define DLA_DECLARE_OPS\(T, S\)(.*?)\n\n", src, re.S).group(1)
-    for base in re.findall(r"dla_([a-z0-9_]+)_##S\s*\(", macro):
-        names.add(f"dla_{base}_f32")
-        names.add(f"dla_{base}_f64")
+    # expand every DLA_DECLARE_*(T, S) prototype list for f32 / f64
+    for macro in re.findall(r"#define DLA_DECLARE_[A-Z]+\(T, S\)(.*?)\n\n", src, re.S):
+        for base in re.findall(r"dla_([a-z0-9_]+)_##S\s*\(", macro):
+            names.add(f"dla_{base}_f32")
+            names.add(f"dla_{base}_f64")
     return {n for n in names if not n.endswith("_")}
 
 

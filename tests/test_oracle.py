@@ -241,6 +241,41 @@ def test_port_matches_reference_lq_eig(port, ref, dt):
         assert np.array_equal(port.syevd_bwd(ub, lb, u, lam), ref.syevd_bwd(ub, lb, u, lam))
 
 
+@pytest.mark.parametrize("dt", DTYPES)
+def test_port_matches_reference_gesvd(port, ref, dt):
+    # dl/svd.hpp:26-284 + dl/adjoints.hpp:315-382, bit for bit
+    r = O.rng(43)
+    for m, n in [(1, 1), (2, 6), (5, 5), (8, 13), (16, 19), (24, 80)]:
+        a = r.standard_normal((m, n)).astype(dt)
+        u, lam, v = port.gesvd(a)
+        ru, rlam, rv = ref.gesvd(a)
+        assert np.array_equal(u, ru) and np.array_equal(lam, rlam) and np.array_equal(v, rv)
+        ub = r.standard_normal((m, m)).astype(dt)
+        lb = r.standard_normal(m).astype(dt)
+        vb = r.standard_normal((m, n)).astype(dt)
+        assert np.array_equal(port.gesvd_bwd(ub, lb, vb, u, lam, v), ref.gesvd_bwd(ub, lb, vb, ru, rlam, rv))
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+def test_kat_gesvd(port, dt):
+    # proj/tests/test_svd.cpp:13-20 (hand value), :55-64 (tall rejected, zero matrix)
+    u, lam, v = port.gesvd(np.array([[3.0, 4.0]], dt))
+    assert abs(lam[0] - 5) < 1e-6 and abs(u[0, 0] - 1) < 1e-6
+    assert abs(v[0, 0] - 0.6) < 1e-6 and abs(v[0, 1] - 0.8) < 1e-6
+    with pytest.raises(O.OracleError):
+        port.gesvd(np.zeros((4, 2), dt))
+    u, lam, v = port.gesvd(np.zeros((3, 5), dt))
+    assert np.all(lam == 0) and np.abs(u @ u.T - np.eye(3)).max() < 1e-6
+    # reconstruction / orthonormal rows (test_svd.cpp:22-42)
+    r = O.rng(47)
+    for m, n in [(1, 1), (2, 6), (5, 5), (8, 13), (16, 16)]:
+        a = r.standard_normal((m, n))
+        u, lam, v = port.gesvd(a)
+        assert np.all(np.diff(lam) >= 0) and np.all(lam >= 0)
+        assert np.abs(u @ u.T - np.eye(m)).max() < 1e-13 and np.abs(v @ v.T - np.eye(m)).max() < 1e-13
+        assert np.abs(u.T @ np.diag(lam) @ v - a).max() / np.abs(a).max() < 1e-12
+
+
 def test_port_matches_reference_sumlogdiag(port, ref):
     r = O.rng(41)
     for n in [1, 2, 32, 100]:
