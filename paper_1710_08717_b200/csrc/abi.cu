@@ -234,7 +234,16 @@ dla_status syrk_fwd(const Ctx& cx, int64_t batch, int64_t n, int64_t k, T* bo, c
   if (k == 0 || alpha == T(0))
     return cudaMemsetAsync(bo, 0, bytes<T>(batch, n, n), cx.stream) == cudaSuccess ? DLA_OK : DLA_ERR_CUDA;
   MatB<const T> av = cpk(a, ta ? k : n, ta ? n : k);
-  DLAB_TRY(gemm<T>(cx, batch, n, n, k, alpha, av, ta, av, !ta, T(0), pk(bo, n, n), MASK_LOWER));
+  bool tma = false;
+  if constexpr (sizeof(T) == 8) {  // A A^T (f64): the TMA-fed persistent update kernel (syrk_tma.cu)
+    MatB<const double> ad{reinterpret_cast<const double*>(av.p), av.ld, av.bs};
+    MatB<double> bd{reinterpret_cast<double*>(bo), n, n * n};
+    if (!ta && syrk_tma_eligible(n, k, ad, bd, batch)) {
+      DLAB_TRY(syrk_tma(cx, batch, n, k, (double)alpha, ad, 0.0, bd, 0));
+      tma = true;
+    }
+  }
+  if (!tma) DLAB_TRY(gemm<T>(cx, batch, n, n, k, alpha, av, ta, av, !ta, T(0), pk(bo, n, n), MASK_LOWER));
   return ew_square<T>(cx, batch, n, pk(bo, n, n), /*copyltu*/ 2);
 }
 
@@ -332,6 +341,21 @@ dla_status trsm_bwd(const Ctx& cx, int64_t batch, int64_t m, int64_t n, T* abar,
   const int mask = lower ? MASK_LOWER : MASK_UPPER;
   auto X = [&](const T* p) { return cpk(p, m, n); };
   const T* s = abar;
+  {  // rank <= 8 (narrow solves): Tbar written whole, zeros outside the mask, in one pass
+    dla_status st = DLA_OK;
+    bool done = false;
+    if (!right) {
+      done = !trans ? outer_tri<T>(cx, batch, m, m, n, T(-1), X(s), false, X(b), true, tb, mask, nullptr, &st)
+                    : outer_tri<T>(cx, batch, m, m, n, T(-1), X(b), false, X(s), true, tb, mask, nullptr, &st);
+    } else {
+      done = !trans ? outer_tri<T>(cx, batch, n, n, m, T(-1), X(b), true, X(s), false, tb, mask, nullptr, &st)
+                    : outer_tri<T>(cx, batch, n, n, m, T(-1), X(s), true, X(b), false, tb, mask, nullptr, &st);
+    }
+    if (done) {
+      if (st != DLA_OK) return st;
+      return ew_scale<T>(cx, batch, m, n, pk(abar, m, n), alpha);
+    }
+  }
   if (!right) {
     if (!trans) DLAB_TRY(gemm<T>(cx, batch, m, m, n, T(-1), X(s), false, X(b), true, T(0), tb, mask));
     else DLAB_TRY(gemm<T>(cx, batch, m, m, n, T(-1), X(b), false, X(s), true, T(0), tb, mask));
@@ -747,6 +771,15 @@ dla_status gp_potrf_inv(const Ctx& cx, int64_t batch, int64_t n, T* a) {
   cudaEventRecord(f.ev[3], cx.stream);
   cudaStreamWaitEvent(f.side, f.ev[3], 0);
   dla_status st = e.st;
+  // DLA_GP_SIDE_CTAS (tuning switch, > 0): cap the side stream's GEMM grid
+  // from here on, so critical-path kernels find room on every SM.  Measured:
+  // the capped inverse and the pullback's first product then share the SMs
+  // and both slow down (C2 7.02 vs 6.81 ms), so the default is unbounded.
+  static const int side_ctas = [] {
+    const char* e = getenv("DLA_GP_SIDE_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  sc.gemm_ctas = side_ctas;
   // W22 = tril(L22); L22^{-1} in place; W21 = -W22^{-1} T1
   if (st == DLA_OK)
     st = ew_tri_copy<T>(sc, batch, h, MatB<const T>{a + h * n + h, n, n * n}, wi.sub(h, h), false);

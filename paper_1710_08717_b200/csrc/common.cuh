@@ -261,6 +261,12 @@ template <typename T>
 bool gemm_skinny(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T alpha, MatB<const T> a, bool ta,
                  MatB<const T> b, bool tb, T beta, MatB<T> cm, int mask, const int32_t* skip, dla_status* st);
 
+// C (m x n) = alpha * mask(op(A) op(B)) with exact zeros outside the mask,
+// k <= 8, one pass (false: not applicable).
+template <typename T>
+bool outer_tri(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T alpha, MatB<const T> a, bool ta,
+               MatB<const T> b, bool tb, MatB<T> cm, int mask, const int32_t* skip, dla_status* st);
+
 // Workspace mirrors: the bytes (carve_bound per carve, summed over the call
 // tree) each routine takes from its Ctx's arena, computed host-side from the
 // same shapes and eligibility tests as the dispatch (no device needed).

@@ -315,9 +315,47 @@ dla_status ew_scale(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<T> x
   return DLA_OK;
 }
 
+// tril / triu zeroing (k_square ops 0 / 1): each row visits only its strict
+// upper (lower) part, two columns per thread with 16-byte stores.
+template <typename T, bool UPPER>
+__global__ void k_zero_tri(int64_t batch, int64_t n, MatB<T> x, const int32_t* skip, bool vec) {
+  for (int64_t row = blockIdx.y; row < batch * n; row += gridDim.y) {
+    const int64_t b = row / n, i = row - b * n;
+    if (slice_failed(skip, b)) continue;
+    const int64_t j0 = UPPER ? i + 1 : 0, j1 = UPPER ? n : i;  // zero columns [j0, j1)
+    if (j0 >= j1) continue;
+    T* xr = x.at(b, i, 0);
+    const int64_t p0 = j0 / 2, p1 = (j1 + 1) / 2;
+    for (int64_t p = p0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < p1; p += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t j = 2 * p;
+      if (vec && j >= j0 && j + 1 < j1) {
+        if constexpr (sizeof(T) == 8)
+          *reinterpret_cast<double2*>(xr + j) = make_double2(0.0, 0.0);
+        else
+          *reinterpret_cast<float2*>(xr + j) = make_float2(0.f, 0.f);
+      } else {
+        if (j >= j0 && j < j1) xr[j] = T(0);
+        if (j + 1 >= j0 && j + 1 < j1) xr[j + 1] = T(0);
+      }
+    }
+  }
+}
+
 template <typename T>
 dla_status ew_square(const Ctx& c, int64_t batch, int64_t n, MatB<T> x, int op, T alpha, const int32_t* skip) {
   if (batch * n == 0) return DLA_OK;
+  if (op == 0 || op == 1) {
+    const bool vec = (x.ld % 2 == 0) && (x.bs % 2 == 0) && (reinterpret_cast<uintptr_t>(x.p) % (2 * sizeof(T)) == 0);
+    const int64_t gx = std::max<int64_t>(1, (n / 2 + 255) / 256);
+    int64_t gy = std::max<int64_t>(1, (148 * 16) / gx);
+    gy = std::min<int64_t>(std::min<int64_t>(gy, batch * n), 65535);
+    if (op == 0)
+      k_zero_tri<T, true><<<dim3((unsigned)gx, (unsigned)gy), 256, 0, c.stream>>>(batch, n, x, skip, vec);
+    else
+      k_zero_tri<T, false><<<dim3((unsigned)gx, (unsigned)gy), 256, 0, c.stream>>>(batch, n, x, skip, vec);
+    DLAB_LAUNCH_CHECK();
+    return DLA_OK;
+  }
   k_square<T><<<row_grid(batch, n), 256, 0, c.stream>>>(batch, n, x, op, alpha, skip);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;

@@ -94,6 +94,11 @@ bool potrf_tiles_eligible(int64_t batch, int64_t n, const MatB<double>& a);
 dla_status potrf_tiles(const Ctx& c, int64_t batch, int64_t n, MatB<double> a, int64_t kbase);
 size_t ws_potrf_tiles(int64_t batch, int64_t n);
 
+// syrk_tma.cu: TMA-fed persistent trailing update C[lower] = alpha P P^T + beta C (f64)
+bool syrk_tma_eligible(int64_t m, int64_t k, const MatB<const double>& p, const MatB<double>& c, int64_t batch);
+dla_status syrk_tma(const Ctx& c, int64_t batch, int64_t m, int64_t k, double alpha, MatB<const double> p, double beta,
+                    MatB<double> cm, int max_ctas);
+
 // gesvd.cu: LQ-preconditioned one-sided Jacobi SVD (m <= n) and its pullback
 template <typename T>
 size_t ws_gesvd_fwd(int64_t batch, int64_t m, int64_t n);

@@ -776,6 +776,18 @@ __global__ void __launch_bounds__(256) k_potrf_diag_inv(int nb, int64_t k0, MatB
 // panel in parallel, 64 per CTA) and masked DMMA SYRK updates of the
 // trailing matrix.  Used for large single matrices where the recursive
 // variant's deep chain of tiny GEMMs dominates.
+// Persistent-grid cap of the TMA trailing update (DLA_SYRK_CAP: 0 = leave the
+// concurrent panel its SMs, -1 = every SM, > 0 = that many CTAs; tuning switch).
+inline int syrk_cap(int leave_panel, int sms) {
+  static const int env = [] {
+    const char* e = getenv("DLA_SYRK_CAP");
+    return e ? atoi(e) : 0;
+  }();
+  if (env < 0) return sms;
+  if (env > 0) return env;
+  return leave_panel;
+}
+
 template <typename T, int NBP>
 dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int64_t kbase) {
   const size_t sm = sizeof(T) * ((NBP + 64) * (NBP + 1) + NBP + (NBP == 64 ? 2 * 64 * (NBP + 1) : 0));
@@ -917,7 +929,26 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
         cudaStreamWaitEvent(la.side, la.panel[g], 0);
         const int64_t gk0 = g * G * NBP;
         MatB<T> p2 = a.sub(c0, gk0);
-        LA_TRY(gemm<T>(side, batch, n - c0, n - c0, k0 + kb - gk0, T(-1), C_(p2), false, C_(p2), true, T(1),
+        bool done_tma = false;
+        if constexpr (sizeof(T) == 8) {
+          MatB<const double> pd{reinterpret_cast<const double*>(p2.p), p2.ld, p2.bs};
+          MatB<double> cd{reinterpret_cast<double*>(a.sub(c0, c0).p), a.ld, a.bs};
+          static const bool la_tma = [] {
+            // tuning switch: the TMA update kernel inside the look-ahead (measured
+            // on par with the two-CTA/SM DMMA GEMM there, so off by default)
+            const char* e = getenv("DLA_POTRF_SYRK_TMA");
+            return e && atoi(e) != 0;
+          }();
+          if (la_tma && syrk_tma_eligible(n - c0, k0 + kb - gk0, pd, cd, batch)) {
+            // the panel kernel of step p + 1 runs concurrently: leave it its SMs
+            const int64_t pc = p + 1 < steps ? batch * chunks_of(p + 1) : 0;
+            const int cap = (int)std::max<int64_t>(c.sms / 2, c.sms - pc);
+            LA_TRY(syrk_tma(side, batch, n - c0, k0 + kb - gk0, -1.0, pd, 1.0, cd, syrk_cap(cap, c.sms)));
+            done_tma = true;
+          }
+        }
+        if (!done_tma)
+          LA_TRY(gemm<T>(side, batch, n - c0, n - c0, k0 + kb - gk0, T(-1), C_(p2), false, C_(p2), true, T(1),
                          a.sub(c0, c0), MASK_LOWER, c.info));
       }
       cudaEventRecord(la.done[g], la.side);

@@ -154,6 +154,18 @@ def test_syrk(port, dt):
             assert_close(host(ga), batch_apply(lambda x, y: port.syrk_bwd(x, y, ta, 0.5), bb, a), dt)
 
 
+def test_syrk_tma_path(port):
+    """f64 A A^T at m >= 256 runs the TMA-fed persistent kernel (syrk_tma.cu):
+    clipped last tile rows/columns, k not a multiple of the 16-wide k-chunk,
+    batches; bit-symmetric output equal to the oracle."""
+    r = O.rng(33)
+    for n, k, B in [(256, 64, 1), (300, 40, 2), (513, 130, 1), (1000, 64, 3), (640, 7, 2)]:
+        a = r.standard_normal((B, n, k))
+        got = L.syrk(dev(a), False, -0.5)
+        assert torch.equal(got, got.transpose(-1, -2)), "syrk must be bit-symmetric"
+        assert_close(host(got), batch_apply(lambda x: port.syrk(x, 0, -0.5), a), np.float64)
+
+
 # ------------------------------------------------------------ trmm / trsm
 SHAPES = [(4, 3), (1, 5), (33, 17), (70, 65), (130, 7), (7, 130), (256, 130), (130, 256), (128, 70), (128, 200)]
 

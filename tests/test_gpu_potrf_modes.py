@@ -53,9 +53,12 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("mode", ["1", "3"])
+@pytest.mark.parametrize("mode", ["1", "3", "tma"])
 def test_potrf_schedule(mode):
-    env = dict(os.environ, DLA_POTRF_MODE=mode, PYTHONPATH=ROOT)
+    # "tma": the default look-ahead with its trailing updates on the TMA-fed
+    # update kernel (syrk_tma.cu, DLA_POTRF_SYRK_TMA=1)
+    extra = {"DLA_POTRF_SYRK_TMA": "1"} if mode == "tma" else {"DLA_POTRF_MODE": mode}
+    env = dict(os.environ, PYTHONPATH=ROOT, **extra)
     p = subprocess.run([sys.executable, "-c", SCRIPT], cwd=ROOT, env=env, capture_output=True, text=True,
                        timeout=300)
     assert p.returncode == 0 and "ok" in p.stdout, p.stdout + p.stderr
