@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """bench.py — headline benchmark of the B200-native dlinalg hot path.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|potrf1024|c3|c4|c5]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|potrf1024|c3|c4|c5|kalman]
                     [--impl ours|reference]
 
 Default workload (BASELINE.json configs[1], the config the metric is quoted
@@ -51,7 +51,7 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", default="c2", choices=["c2", "c1", "potrf1024", "c3", "c4", "c5"])
+    p.add_argument("--config", default="c2", choices=["c2", "c1", "potrf1024", "c3", "c4", "c5", "kalman"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-also", action="store_true")
@@ -393,6 +393,10 @@ def also_measurements(torch, args, rank, world, lib, fp64_peak, hbm):
     c5.pop("sample_inputs", None)
     c5["workload"] = c5.pop("workload")
     out.append(c5)
+    from tools.bench_configs import kalman_measure
+    kal = kalman_measure(torch, world, 10, 3)
+    kal.pop("sample_inputs", None)
+    out.append(kal)
     for n, B in ((1024, 8), (32, 65536)):
         ms = run_potrf_batch(torch, n, B, 10 if n > 64 else 20, 3, world)
         flops = B * 5 * n ** 3 / 3

@@ -310,6 +310,38 @@ dla_status dla_gp_rbf_fwd_f64(int64_t batch, int64_t n, int64_t d, const double*
 dla_status dla_gp_rbf_bwd_f64(int64_t batch, int64_t n, int64_t d, const double* x, double sigma2,
                               double ell2, double lam, const double* abar, double* xbar,
                               double* grads, void* ws, size_t ws_bytes, void* stream);
+/* Batched Kalman filter NLL + gradient of every leaf:
+ * the reference's build_kalman_nll graph (dl/models.hpp:285-337, Joseph-form
+ * covariance update, first observation scored against the prior) and
+ * Graph::backward over it, one launch for `batch` sequences.
+ *   a [h,h] transition, b [d,h] emission, sh [h,h] / sv [d,d] process /
+ *   observation noise, mu0 [h,1] / s0 [h,h] prior, obs [batch][T][d]
+ *   (row t = observation t of that sequence).  param_stride 1: every
+ *   parameter carries a leading [batch] dimension; 0: one model shared by
+ *   all sequences.
+ *   nll [batch]; abar bbar shbar svbar mu0bar s0bar: [batch] x the parameter
+ *   shapes (per-sequence gradients; a shared model sums them); obsbar
+ *   (nullable) [batch][T][d].  h, d <= 32 (SHAPE otherwise; T >= 1).
+ *   info[b]: NOT_SPD with index t*d + pivot when step t's innovation
+ *   covariance is not positive definite (that sequence's outputs untouched).
+ *   workspace: dla_kalman_ws_bytes_{f32,f64} (the device tape of the
+ *   intermediates of every step). */
+size_t dla_kalman_ws_bytes_f64(int64_t batch, int64_t h, int64_t d, int64_t T);
+size_t dla_kalman_ws_bytes_f32(int64_t batch, int64_t h, int64_t d, int64_t T);
+dla_status dla_kalman_nll_fwdbwd_f64(int64_t batch, int64_t h, int64_t d, int64_t T, const double* a,
+                                     const double* b, const double* sh, const double* sv,
+                                     const double* mu0, const double* s0, const double* obs,
+                                     int64_t param_stride, double* nll, double* abar, double* bbar,
+                                     double* shbar, double* svbar, double* mu0bar, double* s0bar,
+                                     double* obsbar, int32_t* info, void* ws, size_t ws_bytes,
+                                     void* stream);
+dla_status dla_kalman_nll_fwdbwd_f32(int64_t batch, int64_t h, int64_t d, int64_t T, const float* a,
+                                     const float* b, const float* sh, const float* sv,
+                                     const float* mu0, const float* s0, const float* obs,
+                                     int64_t param_stride, float* nll, float* abar, float* bbar,
+                                     float* shbar, float* svbar, float* mu0bar, float* s0bar,
+                                     float* obsbar, int32_t* info, void* ws, size_t ws_bytes,
+                                     void* stream);
 /* nll[b] = quad[b] + logdet[b] + n/2 log(2 pi)  (dl/models.hpp:100-103). */
 dla_status dla_gp_nll_assemble_f64(int64_t batch, int64_t n, const double* quad,
                                    const double* logdet, double* nll, void* stream);

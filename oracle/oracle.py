@@ -503,3 +503,70 @@ def c5_item(p, s, y, theta):
     lbar = p.potri_bwd(bbar, l, b) + tbar + np.diag(1.0 / np.diag(l))
     abar = p.potrf_bwd(lbar, l)
     return phi, lam * np.trace(abar)
+
+
+def _kalman_call(fn, a, b, sh, sv, mu0, s0, obs, joint=None):
+    """Shared argument marshalling of o_kalman_f64 / ref_kalman_f64."""
+    h, d = a.shape[0], b.shape[0]
+    T = obs.shape[0]
+    arrs = [np.ascontiguousarray(x, dtype=np.float64) for x in (a, b, sh, sv, mu0, s0, obs)]
+    nll = C.c_double()
+    outs = [np.zeros_like(x) for x in arrs]
+    args = [_i64(h), _i64(d), _i64(T)] + [_ptr(x) for x in arrs] + [C.byref(nll)] + [_ptr(x) for x in outs]
+    return nll, outs, args
+
+
+def kalman_port(a, b, sh, sv, mu0, s0, obs):
+    """Oracle restatement (oracle_impl.h o_kalman): (nll, [Abar, Bbar, Shbar, Svbar, mu0bar, S0bar, obsbar])."""
+    lib = port().lib
+    nll, outs, args = _kalman_call(None, a, b, sh, sv, mu0, s0, obs)
+    idx = _i64(-1)
+    st = lib.o_kalman_f64(*args, C.byref(idx))
+    if st != DLA_OK:
+        raise OracleError(st, idx.value)
+    return nll.value, outs
+
+
+def kalman_ref(a, b, sh, sv, mu0, s0, obs):
+    """The reference (make_kalman + Graph::backward): (nll, grads, dense joint-Gaussian NLL)."""
+    lib = ref().lib
+    nll, outs, args = _kalman_call(None, a, b, sh, sv, mu0, s0, obs)
+    joint = C.c_double()
+    st = lib.ref_kalman_f64(*args, C.byref(joint))
+    if st != DLA_OK:
+        raise OracleError(st)
+    return nll.value, outs, joint.value
+
+
+def kalman_ref_batch(a, b, sh, sv, mu0, s0, obs, threads=1):
+    """Reference batch loop over sequences (per-sequence parameters): (nll [B], seconds)."""
+    lib = ref().lib
+    B, h, d, T = a.shape[0], a.shape[1], b.shape[1], obs.shape[1]
+    arrs = [np.ascontiguousarray(x, dtype=np.float64) for x in (a, b, sh, sv, mu0, s0, obs)]
+    nll = np.zeros(B)
+    lib.ref_kalman_batch_f64.restype = C.c_double
+    sec = lib.ref_kalman_batch_f64(_i64(B), _i64(h), _i64(d), _i64(T), *[_ptr(x) for x in arrs], _ptr(nll),
+                                   _int(threads))
+    return nll, sec
+
+
+def random_kalman(r, h, d, T, batch=None):
+    """Stable random linear-Gaussian state-space model as in
+    proj/tests/test_models.cpp:199-217 (A = 0.5 N(0,1) at h = 2; scaled by
+    sqrt(2/h) above so the spectral radius stays ~0.7), SPD covariances,
+    obs ~ N(0, 1)."""
+    sc = 0.5 * min(1.0, (2.0 / h) ** 0.5)
+
+    def one():
+        a = sc * r.standard_normal((h, h))
+        b = r.standard_normal((d, h))
+        sh = random_spd(h, r)
+        sv = random_spd(d, r)
+        mu0 = r.standard_normal((h, 1))
+        s0 = random_spd(h, r)
+        obs = r.standard_normal((T, d))
+        return a, b, sh, sv, mu0, s0, obs
+    if batch is None:
+        return one()
+    items = [one() for _ in range(batch)]
+    return tuple(np.stack([it[k] for it in items]) for k in range(7))

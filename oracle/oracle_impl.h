@@ -1174,4 +1174,188 @@ int FN(o_gesvd_bwd)(int64_t m, int64_t n, R* abar, const R* ubar, const R* lambd
   return DLA_OK;
 }
 
+
+/* ------------------------------------------------------------------------
+ * Batched Kalman filter NLL: the reference's
+ * build_kalman_nll graph (dl/models.hpp:285-337, Joseph-form covariance
+ * update) evaluated forward, and its reverse-mode gradient w.r.t. every leaf
+ * (A, B, S_h, S_v, mu0, S0, the observations) written out op by op — the
+ * pullbacks the tape applies (dl/tape.hpp:841-917: gemm2, potrf, trsm; the
+ * elementwise add / sub / square / log / sum chain, :930-1086).
+ *
+ * Per step t (mu, S = predicted state; v = obs[t]):
+ *   M1 = B S;  Svv = M1 B^T + Sv;  L = chol(Svv);  e = v - B mu;  z = L^-1 e
+ *   phi_t = 1/2 z^T z + sum log L_ii + d/2 log 2 pi
+ *   X = S B^T;  Y = X L^-T;  K = Y L^-1;  mu_f = mu + K e;  I_KB = I - K B
+ *   P1 = I_KB S;  S_f = P1 I_KB^T + (K Sv) K^T
+ *   (t < T-1)  mu' = A mu_f;  S' = (A S_f) A^T + Sh
+ * nll = sum_t phi_t.  Layout: a h x h, b d x h, sh h x h, sv d x d, mu0 h,
+ * s0 h x h, obs T x d (row t = observation t); gradients in the same shapes.
+ * The tape (intermediates of every step) is malloc'ed here. */
+int FN(o_kalman)(int64_t h, int64_t d, int64_t T, const R* a, const R* b, const R* sh, const R* sv,
+                 const R* mu0, const R* s0, const R* obs, R* nll, R* abar, R* bbar, R* shbar, R* svbar,
+                 R* mu0bar, R* s0bar, R* obsbar, int64_t* idx) {
+  if (h < 1 || d < 1 || T < 1) return DLA_ERR_SHAPE;
+  const int64_t hh = h * h, hd = h * d, dd = d * d;
+  /* tape per step: S mu M1 L e z X Y K IKB P1 Q1 Sf muf */
+  const int64_t step = hh + h + hd + dd + d + d + hd + hd + hd + hh + hh + hd + hh + h;
+  R* tape = (R*)calloc((size_t)(step * T), sizeof(R));
+  R* w = (R*)calloc((size_t)(16 * (hh + hd + dd + h + d) + 64), sizeof(R));
+  if (!tape || !w) {
+    free(tape);
+    free(w);
+    return DLA_ERR_INVALID;
+  }
+#define TP(t, off) (tape + (t) * step + (off))
+  const int64_t oS = 0, oMu = oS + hh, oM1 = oMu + h, oL = oM1 + hd, oE = oL + dd, oZ = oE + d, oX = oZ + d,
+                oY = oX + hd, oK = oY + hd, oI = oK + hd, oP1 = oI + hh, oQ1 = oP1 + hh, oSf = oQ1 + hd,
+                oMuf = oSf + hh;
+  R* t1 = w;            /* h x h scratch */
+  R* t2 = t1 + hh;      /* h x h */
+  R* t3 = t2 + hh;      /* h x h */
+  R* vd = t3 + hh;      /* d x d */
+  R* vhd = vd + dd;     /* h x d */
+  R* vhd2 = vhd + hd;   /* h x d */
+  R* vh = vhd2 + hd;    /* h */
+  R* vdv = vh + h;      /* d */
+  R* sbar = vdv + d;    /* h x h: adjoint of S_pred (running) */
+  R* mubar = sbar + hh; /* h */
+  R* sbn = mubar + h;   /* h x h: adjoint of the next S_pred */
+  R* mbn = sbn + hh;    /* h */
+  R* lbar = mbn + h;    /* d x d */
+  R* kbar = lbar + dd;  /* h x d */
+  R* ybar = kbar + hd;  /* h x d */
+  R* ebar = ybar + hd;  /* d */
+  R* ibar = ebar + d;   /* h x h */
+  R* p1bar = ibar + hh; /* h x h */
+  R* m1bar = p1bar + hh; /* d x h */
+  int st = DLA_OK;
+  const R log2pi = (R)1.8378770664093454835606594728112353L;
+  R total = (R)0;
+  memcpy(TP(0, oS), s0, sizeof(R) * (size_t)hh);
+  memcpy(TP(0, oMu), mu0, sizeof(R) * (size_t)h);
+  for (int64_t t = 0; t < T && st == DLA_OK; ++t) {
+    R *S = TP(t, oS), *mu = TP(t, oMu), *M1 = TP(t, oM1), *L = TP(t, oL), *e = TP(t, oE), *z = TP(t, oZ);
+    R *X = TP(t, oX), *Y = TP(t, oY), *K = TP(t, oK), *I = TP(t, oI), *P1 = TP(t, oP1), *Q1 = TP(t, oQ1);
+    R *Sf = TP(t, oSf), *muf = TP(t, oMuf);
+    FN(o_gemm)(d, h, h, M1, b, S, 0, 0, (R)1, 0);
+    FN(o_gemm)(d, d, h, L, M1, b, 0, 1, (R)1, 0);
+    for (int64_t q = 0; q < dd; ++q) L[q] += sv[q];
+    if (!FN(symmetric_ok)(d, L, FN(sym_rtol)())) {
+      st = DLA_ERR_ASYMMETRIC;
+      break;
+    }
+    st = FN(potrf_lower)(d, L, idx);
+    if (st) break;
+    FN(o_tril)(d, L);
+    FN(o_gemm)(d, 1, h, vdv, b, mu, 0, 0, (R)1, 0);
+    for (int64_t i = 0; i < d; ++i) e[i] = obs[t * d + i] - vdv[i];
+    memcpy(z, e, sizeof(R) * (size_t)d);
+    FN(o_trsm)(d, 1, L, z, 0, 0, 1, (R)1, NULL);
+    R quad = (R)0, ld = (R)0;
+    for (int64_t i = 0; i < d; ++i) quad += z[i] * z[i];
+    for (int64_t i = 0; i < d; ++i) ld += LOG(AT(L, d, i, i));
+    const R term = ((R)0.5 * quad + ld) + (R)0.5 * (R)d * log2pi;
+    total = t == 0 ? term : total + term;
+    FN(o_gemm)(h, d, h, X, S, b, 0, 1, (R)1, 0);
+    memcpy(Y, X, sizeof(R) * (size_t)hd);
+    FN(o_trsm)(h, d, L, Y, 1, 1, 1, (R)1, NULL);
+    memcpy(K, Y, sizeof(R) * (size_t)hd);
+    FN(o_trsm)(h, d, L, K, 1, 0, 1, (R)1, NULL);
+    FN(o_gemm)(h, 1, d, vh, K, e, 0, 0, (R)1, 0);
+    for (int64_t i = 0; i < h; ++i) muf[i] = mu[i] + vh[i];
+    FN(o_gemm)(h, h, d, t1, K, b, 0, 0, (R)1, 0);
+    for (int64_t i = 0; i < h; ++i)
+      for (int64_t j = 0; j < h; ++j) AT(I, h, i, j) = (i == j ? (R)1 : (R)0) - AT(t1, h, i, j);
+    FN(o_gemm)(h, h, h, P1, I, S, 0, 0, (R)1, 0);
+    FN(o_gemm)(h, h, h, t2, P1, I, 0, 1, (R)1, 0);
+    FN(o_gemm)(h, d, d, Q1, K, sv, 0, 0, (R)1, 0);
+    FN(o_gemm)(h, h, d, t3, Q1, K, 0, 1, (R)1, 0);
+    for (int64_t q = 0; q < hh; ++q) Sf[q] = t2[q] + t3[q];
+    if (t + 1 < T) {
+      FN(o_gemm)(h, 1, h, TP(t + 1, oMu), a, muf, 0, 0, (R)1, 0);
+      FN(o_gemm)(h, h, h, t1, a, Sf, 0, 0, (R)1, 0);
+      FN(o_gemm)(h, h, h, TP(t + 1, oS), t1, a, 0, 1, (R)1, 0);
+      for (int64_t q = 0; q < hh; ++q) TP(t + 1, oS)[q] += sh[q];
+    }
+  }
+  if (st == DLA_OK) {
+    *nll = total;
+    memset(abar, 0, sizeof(R) * (size_t)hh);
+    memset(bbar, 0, sizeof(R) * (size_t)hd);
+    memset(shbar, 0, sizeof(R) * (size_t)hh);
+    memset(svbar, 0, sizeof(R) * (size_t)dd);
+    memset(sbn, 0, sizeof(R) * (size_t)hh);
+    memset(mbn, 0, sizeof(R) * (size_t)h);
+    for (int64_t t = T - 1; t >= 0; --t) {
+      R *S = TP(t, oS), *mu = TP(t, oMu), *M1 = TP(t, oM1), *L = TP(t, oL), *e = TP(t, oE), *z = TP(t, oZ);
+      R *Y = TP(t, oY), *K = TP(t, oK), *I = TP(t, oI), *P1 = TP(t, oP1), *Q1 = TP(t, oQ1);
+      R *Sf = TP(t, oSf), *muf = TP(t, oMuf);
+      R* sfbar = t1; /* h x h */
+      R* mufbar = vh;
+      if (t + 1 < T) { /* S' = (A Sf) A^T + Sh, mu' = A muf */
+        for (int64_t q = 0; q < hh; ++q) shbar[q] += sbn[q];
+        FN(o_gemm)(h, h, h, t2, a, Sf, 0, 0, (R)1, 0);       /* R1 = A Sf */
+        FN(o_gemm)(h, h, h, abar, sbn, t2, 1, 0, (R)1, 1);   /* Abar += S'bar^T R1 */
+        FN(o_gemm)(h, h, h, t3, sbn, a, 0, 0, (R)1, 0);      /* R1bar = S'bar A */
+        FN(o_gemm)(h, h, h, abar, t3, Sf, 0, 1, (R)1, 1);    /* Abar += R1bar Sf^T */
+        FN(o_gemm)(h, h, h, sfbar, a, t3, 1, 0, (R)1, 0);    /* Sfbar = A^T R1bar */
+        FN(o_gemm)(h, h, 1, abar, mbn, muf, 0, 1, (R)1, 1);  /* Abar += mu'bar muf^T */
+        FN(o_gemm)(h, 1, h, mufbar, a, mbn, 1, 0, (R)1, 0);  /* mufbar = A^T mu'bar */
+      } else {
+        memset(sfbar, 0, sizeof(R) * (size_t)hh);
+        memset(mufbar, 0, sizeof(R) * (size_t)h);
+      }
+      /* Q2 = Q1 K^T, Q1 = K Sv */
+      FN(o_gemm)(h, d, h, vhd, sfbar, K, 0, 0, (R)1, 0);     /* Q1bar = Sfbar K */
+      FN(o_gemm)(h, d, h, kbar, sfbar, Q1, 1, 0, (R)1, 0);   /* Kbar = Sfbar^T Q1 */
+      FN(o_gemm)(h, d, d, kbar, vhd, sv, 0, 1, (R)1, 1);     /* Kbar += Q1bar Sv^T */
+      FN(o_gemm)(d, d, h, svbar, K, vhd, 1, 0, (R)1, 1);     /* Svbar += K^T Q1bar */
+      /* P2 = P1 I^T, P1 = I S */
+      FN(o_gemm)(h, h, h, p1bar, sfbar, I, 0, 0, (R)1, 0);   /* P1bar = Sfbar I */
+      FN(o_gemm)(h, h, h, ibar, sfbar, P1, 1, 0, (R)1, 0);   /* Ibar = Sfbar^T P1 */
+      FN(o_gemm)(h, h, h, ibar, p1bar, S, 0, 1, (R)1, 1);    /* Ibar += P1bar S^T */
+      FN(o_gemm)(h, h, h, sbar, I, p1bar, 1, 0, (R)1, 0);    /* Sbar = I^T P1bar */
+      /* I = Id - K B */
+      FN(o_gemm)(h, d, h, kbar, ibar, b, 0, 1, (R)-1, 1);    /* Kbar -= Ibar B^T */
+      FN(o_gemm)(d, h, h, bbar, K, ibar, 1, 0, (R)-1, 1);    /* Bbar -= K^T Ibar */
+      /* muf = mu + K e */
+      memcpy(mubar, mufbar, sizeof(R) * (size_t)h);
+      FN(o_gemm)(h, d, 1, kbar, mufbar, e, 0, 1, (R)1, 1);   /* Kbar += mufbar e^T */
+      FN(o_gemm)(d, 1, h, ebar, K, mufbar, 1, 0, (R)1, 0);   /* ebar = K^T mufbar */
+      /* K = Y L^-1, Y = X L^-T: trsm pullbacks (dl/adjoints.hpp:131-153) */
+      FN(o_trsm_bwd)(h, d, ybar, lbar, kbar, L, K, 1, 0, 1, (R)1, NULL);
+      FN(o_trsm_bwd)(h, d, vhd2, vd, ybar, L, Y, 1, 1, 1, (R)1, NULL);  /* vhd2 = Xbar */
+      for (int64_t q = 0; q < dd; ++q) lbar[q] += vd[q];
+      /* X = S B^T */
+      FN(o_gemm)(h, h, d, sbar, vhd2, b, 0, 0, (R)1, 1);     /* Sbar += Xbar B */
+      FN(o_gemm)(d, h, h, bbar, vhd2, S, 1, 0, (R)1, 1);     /* Bbar += Xbar^T S */
+      /* phi_t: zbar = z, Lbar_ii += 1 / L_ii; z = L^-1 e */
+      FN(o_trsm_bwd)(d, 1, vdv, vd, z, L, z, 0, 0, 1, (R)1, NULL);
+      for (int64_t q = 0; q < dd; ++q) lbar[q] += vd[q];
+      for (int64_t i = 0; i < d; ++i) AT(lbar, d, i, i) += (R)1 / AT(L, d, i, i);
+      for (int64_t i = 0; i < d; ++i) ebar[i] += vdv[i];
+      /* e = v - B mu */
+      for (int64_t i = 0; i < d; ++i) obsbar[t * d + i] = ebar[i];
+      FN(o_gemm)(d, h, 1, bbar, ebar, mu, 0, 1, (R)-1, 1);   /* Bbar -= ebar mu^T */
+      FN(o_gemm)(h, 1, d, mubar, b, ebar, 1, 0, (R)-1, 1);   /* mubar -= B^T ebar */
+      /* L = chol(Svv); Svv = M1 B^T + Sv; M1 = B S */
+      FN(o_potrf_bwd)(d, vd, lbar, L, 1);
+      for (int64_t q = 0; q < dd; ++q) svbar[q] += vd[q];
+      FN(o_gemm)(d, h, d, m1bar, vd, b, 0, 0, (R)1, 0);      /* M1bar = Svvbar B */
+      FN(o_gemm)(d, h, d, bbar, vd, M1, 1, 0, (R)1, 1);      /* Bbar += Svvbar^T M1 */
+      FN(o_gemm)(d, h, h, bbar, m1bar, S, 0, 1, (R)1, 1);    /* Bbar += M1bar S^T */
+      FN(o_gemm)(h, h, d, sbar, b, m1bar, 1, 0, (R)1, 1);    /* Sbar += B^T M1bar */
+      memcpy(sbn, sbar, sizeof(R) * (size_t)hh);
+      memcpy(mbn, mubar, sizeof(R) * (size_t)h);
+    }
+    memcpy(s0bar, sbn, sizeof(R) * (size_t)hh);
+    memcpy(mu0bar, mbn, sizeof(R) * (size_t)h);
+  }
+#undef TP
+  free(tape);
+  free(w);
+  return st;
+}
+
 #undef AT

@@ -26,6 +26,7 @@
 #include "dlinalg/transforms.hpp"
 
 #include "../include/dla.h"
+#include "kalman_oracle.hpp"  // the reference's own dense joint-Gaussian oracle (proj/tests)
 
 using dla::ConstMatrixView;
 using dla::index_t;
@@ -294,5 +295,55 @@ double ref_potrf_fwdbwd_batch_f64(int64_t batch, int64_t n, double* a, double* a
 
 REF_BATCH_LQ_EIG(double, f64)
 REF_BATCH_LQ_EIG(float, f32)
+
+
+// Kalman filter NLL + gradient of every leaf through the reference's
+// make_kalman + Graph::backward (dl/models.hpp:285-369, dl/tape.hpp).
+// obs: T x d (row t = observation t); gradients in the input shapes; the
+// observation gradients land in obsbar.  joint (nullable): the reference
+// test oracle's dense joint-Gaussian NLL (proj/tests/kalman_oracle.hpp:16-79).
+int ref_kalman_f64(int64_t h, int64_t d, int64_t T, const double* a, const double* b, const double* sh,
+                   const double* sv, const double* mu0, const double* s0, const double* obs, double* nll,
+                   double* abar, double* bbar, double* shbar, double* svbar, double* mu0bar, double* s0bar,
+                   double* obsbar, double* joint) {
+  return guarded([&] {
+    auto mat = [](const double* p, int64_t r, int64_t c) {
+      dla::Matrix<double> m(r, c);
+      std::memcpy(m.data(), p, sizeof(double) * r * c);
+      return m;
+    };
+    dla::Matrix<double> am = mat(a, h, h), bm = mat(b, d, h), shm = mat(sh, h, h), svm = mat(sv, d, d),
+                        m0 = mat(mu0, h, 1), s0m = mat(s0, h, h);
+    std::vector<dla::Matrix<double>> ob;
+    for (int64_t t = 0; t < T; ++t) ob.push_back(mat(obs + t * d, d, 1));
+    dla::Graph<double> g;
+    auto m = dla::make_kalman(g, am, bm, shm, svm, m0, s0m, ob);
+    *nll = g.value(m.loss)(0, 0);
+    auto gs = g.backward(m.loss);
+    std::memcpy(abar, gs.at(m.a).data(), sizeof(double) * h * h);
+    std::memcpy(bbar, gs.at(m.b).data(), sizeof(double) * d * h);
+    std::memcpy(shbar, gs.at(m.sh).data(), sizeof(double) * h * h);
+    std::memcpy(svbar, gs.at(m.sv).data(), sizeof(double) * d * d);
+    std::memcpy(mu0bar, gs.at(m.mu0).data(), sizeof(double) * h);
+    std::memcpy(s0bar, gs.at(m.s0).data(), sizeof(double) * h * h);
+    for (int64_t t = 0; t < T; ++t) std::memcpy(obsbar + t * d, gs.at(m.obs[t]).data(), sizeof(double) * d);
+    if (joint) *joint = oracle::lgssm_joint_nll(am, bm, shm, svm, m0, s0m, ob);
+  }, nullptr);
+}
+
+// Batched Kalman NLL + gradients with the reference's own batch loop
+// (timing leg of bench.py): sequence s uses parameters + s * (its size).
+double ref_kalman_batch_f64(int64_t batch, int64_t h, int64_t d, int64_t T, const double* a, const double* b,
+                            const double* sh, const double* sv, const double* mu0, const double* s0,
+                            const double* obs, double* nll, int threads) {
+  const double t0 = now_s();
+  dla::for_each_slice(batch, threads, [&](index_t s) {
+    std::vector<double> ga(h * h), gb(d * h), gsh(h * h), gsv(d * d), gm(h), gs0(h * h), go(T * d);
+    ref_kalman_f64(h, d, T, a + s * h * h, b + s * d * h, sh + s * h * h, sv + s * d * d, mu0 + s * h,
+                   s0 + s * h * h, obs + s * T * d, nll + s, ga.data(), gb.data(), gsh.data(), gsv.data(),
+                   gm.data(), gs0.data(), go.data(), nullptr);
+  });
+  return now_s() - t0;
+}
 
 }  // extern "C"

@@ -102,6 +102,13 @@ class _Lib:
         L.dla_ml_reduce_f64.restype = _int
         L.dla_potrf_inv_join_f64.argtypes = [_vp]
         L.dla_potrf_inv_join_f64.restype = _int
+        for sfx in ("f32", "f64"):
+            wsf = getattr(L, f"dla_kalman_ws_bytes_{sfx}")
+            wsf.restype = _sz
+            wsf.argtypes = [_i64, _i64, _i64, _i64]
+            kf = getattr(L, f"dla_kalman_nll_fwdbwd_{sfx}")
+            kf.argtypes = [_i64, _i64, _i64, _i64] + [_vp] * 7 + [_i64] + [_vp] * 9 + [_vp, _sz, _vp]
+            kf.restype = _int
         self.fns = {}
         for name, sig in _SIGS.items():
             for suffix, scal in (("f32", C.c_float), ("f64", C.c_double)):
@@ -132,7 +139,9 @@ def exported_symbols():
              "dla_gp_rbf_fwd_f64", "dla_gp_rbf_bwd_f64", "dla_gp_nll_assemble_f64",
              "dla_ml_shift_copy_f64", "dla_axpy_f64", "dla_ml_reduce_ws_bytes", "dla_ml_reduce_f64",
              "dla_potrf_bwd_ws_bytes_f64", "dla_potrf_inv_join_f64",
-             "dla_potrf_bwd_begin_f64", "dla_potrf_bwd_end_f64", "dla_gp_potrf_inv_f64"]
+             "dla_potrf_bwd_begin_f64", "dla_potrf_bwd_end_f64", "dla_gp_potrf_inv_f64",
+             "dla_kalman_ws_bytes_f32", "dla_kalman_ws_bytes_f64",
+             "dla_kalman_nll_fwdbwd_f32", "dla_kalman_nll_fwdbwd_f64"]
     for name in _SIGS:
         for s in ("f32", "f64"):
             names.append(f"dla_{name}_{s}")

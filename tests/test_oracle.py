@@ -331,3 +331,74 @@ def test_port_matches_committed_golden(port):
             assert np.array_equal(u, g[name + "/u"]) and np.array_equal(lam, g[name + "/lam"])
         elif op == "gp":
             pass  # checked in test_gp_golden (needs the GP driver)
+
+
+# --------------------------------------------------------------- Kalman NLL
+KGOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "kalman_ref.npz")
+KNAMES = ("a", "b", "sh", "sv", "mu0", "s0", "obs")
+
+
+def _kcase(g, name):
+    return tuple(g[f"{name}/in/{k}"] for k in KNAMES)
+
+
+def test_kat_kalman_random_walk():
+    # proj/tests/test_models.cpp:187-197: hand value of the scalar random walk
+    one, zero = np.ones((1, 1)), np.zeros((1, 1))
+    nll, _ = O.kalman_port(one, one, one, one, zero, one, np.zeros((2, 1)))
+    assert abs(nll - 2.6425960226263948) < 1e-12 * 2.65
+
+
+def test_kalman_port_matches_committed_golden():
+    """The restatement (oracle_impl.h o_kalman) against the reference's own
+    make_kalman + Graph::backward outputs and its dense joint-Gaussian oracle."""
+    g = np.load(KGOLD)
+    for name in g["cases"]:
+        nll, grads = O.kalman_port(*_kcase(g, name))
+        ref_nll = float(g[f"{name}/nll"])
+        assert abs(nll - ref_nll) <= 1e-14 * abs(ref_nll), name
+        # the recursive filter equals the dense joint Gaussian (test_models.cpp:199-217)
+        assert abs(ref_nll - float(g[f"{name}/joint"])) < 1e-8 * max(1.0, abs(ref_nll)), name
+        for k, v in zip(KNAMES, grads):
+            w = g[f"{name}/grad/{k}"]
+            assert np.abs(v - w).max() <= 1e-13 * max(1.0, np.abs(w).max()), (name, k)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built (needs /root/reference)")
+def test_kalman_port_matches_live_reference():
+    r = O.rng(2024)
+    for h, d, T in [(2, 2, 6), (5, 3, 17), (7, 9, 11)]:
+        m = O.random_kalman(r, h, d, T)
+        nll, grads = O.kalman_port(*m)
+        rn, rg, _ = O.kalman_ref(*m)
+        assert abs(nll - rn) <= 1e-14 * abs(rn)
+        for v, w in zip(grads, rg):
+            assert np.abs(v - w).max() <= 1e-13 * max(1.0, np.abs(w).max())
+
+
+def test_kalman_port_fd():
+    """Central finite differences of the restated NLL on every leaf
+    (proj/tests/test_models.cpp:219-241 perturbs A, B, Sh, Sv, mu0, S0, v1)."""
+    r = O.rng(137)
+    m = list(O.random_kalman(r, 2, 2, 4))
+    _, grads = O.kalman_port(*m)
+    eps = 1e-6
+    for li in range(7):
+        x = m[li]
+        it = np.nditer(x, flags=["multi_index"])
+        for _ in it:
+            ix = it.multi_index
+            sym = KNAMES[li] in ("sh", "sv", "s0")  # PerturbMode::Symmetric in the reference test
+            if sym and ix[0] > ix[1]:
+                continue
+            xp, xm = x.copy(), x.copy()
+            tw = (ix[1], ix[0])
+            for y, sgn in ((xp, 1.0), (xm, -1.0)):
+                y[ix] += sgn * eps
+                if sym and tw != ix:
+                    y[tw] += sgn * eps
+            mp, mm_ = list(m), list(m)
+            mp[li], mm_[li] = xp, xm
+            fd = (O.kalman_port(*mp)[0] - O.kalman_port(*mm_)[0]) / (2 * eps)
+            an = grads[li][ix] + (grads[li][tw] if sym and tw != ix else 0.0)
+            assert abs(fd - an) < 1e-6 * max(1.0, abs(fd)), (KNAMES[li], ix)

@@ -192,6 +192,15 @@ def run(torch, args, rank, world, lib, fp64_peak, hbm):
                                "unit": "TFLOP/s", "frac": v * flops / B / 1e12 / fp64_peak, "traffic": None,
                                "note": "count-convention flops 10n^3/3 + 6n^3 per matrix; the smem Jacobi does "
                                        "~20x that in FP64 FMA and is bound by its per-round barrier chain"})
+    if cfg == "kalman":
+        r = kalman_measure(torch, world, args.steps, args.warmup)
+        cpu = None
+        if ref is not None and rank == 0 and not getattr(args, "no_cpu_baseline", False):
+            cpu = kalman_cpu_baseline(r.pop("sample_inputs"))
+        r.pop("sample_inputs", None)
+        return _line(args, world, "Kalman NLL+grad sequences/s", r["sequences_per_s"], "sequences/s",
+                     r["ms_per_step"], r["workload"], cpu_baseline=cpu,
+                     **{k: v for k, v in r.items() if k not in ("sequences_per_s", "ms_per_step", "workload")})
     if cfg == "c5":
         r = c5_measure(torch, rank, world, args.steps, args.warmup, fp64_peak)
         cpu = None
@@ -276,3 +285,42 @@ def c5_cpu_baseline(sample, theta):
     return {"value": 1.0 / secs, "unit": "items/s", "cores": 1, "kind": "port",
             "sample": f"{reps} C5 items through the oracle port's per-op chain (C restatement of the "
                       f"reference ops, 1 thread); the reference has no C5 driver"}
+
+
+# Batched Kalman filter NLL + gradient: one CTA per
+# sequence, per-sequence models, the reference's build_kalman_nll graph.
+KALMAN_B, KALMAN_H, KALMAN_D, KALMAN_T = 4096, 8, 8, 128
+
+
+def kalman_measure(torch, world, steps, warmup, B=KALMAN_B, h=KALMAN_H, d=KALMAN_D, T=KALMAN_T):
+    import bench
+    from oracle import oracle as O
+    from paper_1710_08717_b200 import kalman as K
+
+    r = O.rng(21)
+    m = O.random_kalman(r, h, d, T, batch=B)
+    dev = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in m]
+    km = K.KalmanNLL(h, d, T, B)
+    km.step(*dev, check=True)  # validates the inputs once (no failing sequence)
+    ms = bench.timed(torch, bench.graphed(torch, lambda: km.step(*dev, check=False)), steps, warmup, world)
+    # algorithmic flops per time step (forward products + solves, and the
+    # backward's ~2.5x), counted from the graph at h = d
+    fl_step = 2 * (d * h * h + d * d * h + h * h * d + 2 * h * d * d + h * h * d + 2 * h ** 3 + h * d * d
+                   + h * h * d + 2 * h ** 3) + d ** 3 / 3
+    fl = 3.5 * fl_step * T
+    return {"sequences_per_s": world * B / (ms / 1e3), "ms_per_step": ms,
+            "gflops": world * B * fl / (ms / 1e3) / 1e9, "launches_per_step": 1,
+            "workload": f"Kalman filter NLL + gradient of every leaf (dl/models.hpp:285-337), batch {B} sequences, "
+                        f"h = d = {h}, T = {T}, per-sequence models, fp64 (one launch: csrc/kalman.cu)",
+            "sample_inputs": [x[:16] for x in m]}
+
+
+def kalman_cpu_baseline(sample):
+    from oracle import oracle as O
+
+    th = min(16, _cpu_threads())
+    _, secs = O.kalman_ref_batch(*sample, threads=th)
+    n = sample[0].shape[0]
+    return {"value": n / secs, "unit": "sequences/s", "cores": th, "kind": "reference",
+            "sample": f"reference make_kalman + Graph::backward over {n} of the sequences (for_each_slice, "
+                      f"{th} threads)"}
