@@ -421,19 +421,20 @@ __global__ void __launch_bounds__(ET, 4) k_syevd_small(int n, T* uall, T* lamall
         A[i2] = cb * z1 - sb * w1;
         A[i3] = sb * z1 + cb * w1;
       }
-      // Vt <- J^T Vt (rows p, q of Vt = columns of V): thread -> one pair,
-      // every 8th element of its two rows
+      // Vt <- J^T Vt (rows p, q of Vt = columns of V): a warp per row pair,
+      // lanes along contiguous columns (2 wavefronts per access whatever p,
+      // q are; the previous 4-pairs-per-warp split collided across rows)
       {
-        const int k = tid >> 3, i0 = tid & 7;
-        const T sn = k < half ? cs[2 * k + 1] : T(0);
-        if (sn != T(0)) {
-          const int p = pq[2 * k], q = pq[2 * k + 1];
+        const int wp = tid >> 5, lane = tid & 31;
+        for (int k = wp; k < half; k += ET / 32) {
+          const T sn = cs[2 * k + 1];
+          if (sn == T(0)) continue;
           const T c = cs[2 * k];
-          T* vp = Vt + p * ld;
-          T* vq = Vt + q * ld;
+          T* vp = Vt + pq[2 * k] * ld;
+          T* vq = Vt + pq[2 * k + 1] * ld;
 #pragma unroll
-          for (int v = 0; v < EN / 8; ++v) {
-            const int i = i0 + 8 * v;
+          for (int v = 0; v < EN / 32; ++v) {
+            const int i = lane + 32 * v;
             const T a0 = vp[i], a1 = vq[i];
             vp[i] = c * a0 - sn * a1;
             vq[i] = sn * a0 + c * a1;
