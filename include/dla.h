@@ -310,6 +310,48 @@ dla_status dla_gp_rbf_fwd_f64(int64_t batch, int64_t n, int64_t d, const double*
 dla_status dla_gp_rbf_bwd_f64(int64_t batch, int64_t n, int64_t d, const double* x, double sigma2,
                               double ell2, double lam, const double* abar, double* xbar,
                               double* grads, void* ws, size_t ws_bytes, void* stream);
+/* Device tape node kernels: the reference tape's
+ * elementwise / structural nodes and their pullbacks (dl/tape.hpp
+ * compute_node :615-790, pull_node :930-1120, acc :920-929) for the device
+ * Graph (paper_1710_08717_b200/tape.py).  One matrix (no batch), row-major.
+ *   out = f(x[, y][, s[0]][, c])      accumulate != 0:  out += f(...)
+ * x is rows x cols unless stated.  out may alias x (in-place nodes of the
+ * memory plan) for the map ops (COPY .. ABS_BWD).  SUM / DOT / DOT_NEG_DIV
+ * need dla_tape_ew_ws_bytes() of workspace (fixed-order reduction). */
+typedef enum {
+  DLA_EW_COPY = 0, DLA_EW_ADD = 1, DLA_EW_SUB = 2, DLA_EW_MUL = 3,
+  DLA_EW_SQUARE = 4, DLA_EW_SQRT = 5, DLA_EW_LOG = 6, DLA_EW_EXP = 7,
+  DLA_EW_ABS = 8, DLA_EW_NEG = 9,
+  DLA_EW_SCALE = 10,      /* x * c                                         */
+  DLA_EW_ADDC = 11,       /* x + c                                         */
+  DLA_EW_MULS = 12,       /* x * s[0]  (MulScalar)                         */
+  DLA_EW_DIVS = 13,       /* x / s[0]  (DivScalar)                         */
+  DLA_EW_FILL = 14,       /* s[0] everywhere (Sum pullback)                */
+  DLA_EW_SQUARE_BWD = 15, /* x * (2 y)       x = gbar, y = input           */
+  DLA_EW_SQRT_BWD = 16,   /* x / (2 y)       y = output                    */
+  DLA_EW_LOG_BWD = 17,    /* x / y           y = input                     */
+  DLA_EW_ABS_BWD = 18,    /* x * sign(y)     y = input                     */
+  DLA_EW_TRIL = 19, DLA_EW_TRIU = 20,  /* square x                         */
+  DLA_EW_TILECOLS = 21,   /* x rows x 1 -> rows x aux                      */
+  DLA_EW_TILEROWS = 22,   /* x rows x 1 -> aux x rows                      */
+  DLA_EW_EXTRACTDIAG = 23,/* x n x n -> n x 1                              */
+  DLA_EW_MAKEDIAG = 24,   /* x n x 1 -> n x n                              */
+  DLA_EW_CONCATCOLS = 25, /* [x | y], y rows x aux                         */
+  DLA_EW_SLICECOLS = 26,  /* x rows x aux -> columns [c, c + cols)         */
+  DLA_EW_SUMROWS = 27,    /* -> rows x 1                                   */
+  DLA_EW_SUMCOLS = 28,    /* -> cols x 1                                   */
+  DLA_EW_SUM = 29,        /* -> 1 x 1                                      */
+  DLA_EW_DOT = 30,        /* sum(x * y) -> 1 x 1                           */
+  DLA_EW_DOT_NEG_DIV = 31 /* -sum(x * y) / s[0] -> 1 x 1                   */
+} dla_ew_op;
+size_t dla_tape_ew_ws_bytes(void);
+dla_status dla_tape_ew_f64(int op, int64_t rows, int64_t cols, int64_t aux, const double* x,
+                           const double* y, const double* s, double c, double* out, int accumulate,
+                           void* ws, size_t ws_bytes, void* stream);
+dla_status dla_tape_ew_f32(int op, int64_t rows, int64_t cols, int64_t aux, const float* x,
+                           const float* y, const float* s, float c, float* out, int accumulate,
+                           void* ws, size_t ws_bytes, void* stream);
+
 /* Batched Kalman filter NLL + gradient of every leaf:
  * the reference's build_kalman_nll graph (dl/models.hpp:285-337, Joseph-form
  * covariance update, first observation scored against the prior) and

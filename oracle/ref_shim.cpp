@@ -346,4 +346,38 @@ double ref_kalman_batch_f64(int64_t batch, int64_t h, int64_t d, int64_t T, cons
   return now_s() - t0;
 }
 
+
+// Memory-plan hand-off counts of the reference tape (Graph::planned_reuse_count,
+// dl/tape.hpp:486-491) for make_gp and make_kalman graphs: the device tape's
+// restated build_plan must make the same hand-offs.
+int64_t ref_gp_plan_count(int64_t n, int64_t d, const double* x, const double* y) {
+  int64_t c = -1;
+  guarded([&] {
+    dla::Matrix<double> xm(n, d), ym(n, 1);
+    std::memcpy(xm.data(), x, sizeof(double) * n * d);
+    std::memcpy(ym.data(), y, sizeof(double) * n);
+    dla::Graph<double> g;
+    dla::make_gp(g, xm, ym, 1.0, 1.0, 0.1);
+    c = g.planned_reuse_count();
+  }, nullptr);
+  return c;
+}
+int64_t ref_kalman_plan_count(int64_t h, int64_t d, int64_t T, const double* a, const double* b, const double* sh,
+                              const double* sv, const double* mu0, const double* s0, const double* obs) {
+  int64_t c = -1;
+  guarded([&] {
+    auto mat = [](const double* p, int64_t r, int64_t cc) {
+      dla::Matrix<double> m(r, cc);
+      std::memcpy(m.data(), p, sizeof(double) * r * cc);
+      return m;
+    };
+    std::vector<dla::Matrix<double>> ob;
+    for (int64_t t = 0; t < T; ++t) ob.push_back(mat(obs + t * d, d, 1));
+    dla::Graph<double> g;
+    dla::make_kalman(g, mat(a, h, h), mat(b, d, h), mat(sh, h, h), mat(sv, d, d), mat(mu0, h, 1), mat(s0, h, h), ob);
+    c = g.planned_reuse_count();
+  }, nullptr);
+  return c;
+}
+
 }  // extern "C"

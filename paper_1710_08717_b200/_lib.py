@@ -141,7 +141,8 @@ def exported_symbols():
              "dla_potrf_bwd_ws_bytes_f64", "dla_potrf_inv_join_f64",
              "dla_potrf_bwd_begin_f64", "dla_potrf_bwd_end_f64", "dla_gp_potrf_inv_f64",
              "dla_kalman_ws_bytes_f32", "dla_kalman_ws_bytes_f64",
-             "dla_kalman_nll_fwdbwd_f32", "dla_kalman_nll_fwdbwd_f64"]
+             "dla_kalman_nll_fwdbwd_f32", "dla_kalman_nll_fwdbwd_f64",
+             "dla_tape_ew_ws_bytes", "dla_tape_ew_f32", "dla_tape_ew_f64"]
     for name in _SIGS:
         for s in ("f32", "f64"):
             names.append(f"dla_{name}_{s}")
