@@ -491,6 +491,20 @@ cudaError_t launch_tv(GemmArgs<T> g, int64_t slabs, cudaStream_t s, bool large, 
     return (unsigned)(max_ctas > 0 && tiles > max_ctas ? max_ctas : tiles);
   };
   if constexpr (sizeof(T) == 8) {
+    // Masked, triangular-operand and short-K products: 64 x 64 tiles at four
+    // CTAs per SM (measured on B200 against the two-CTA 128 x 64 tiles: the
+    // potrf pullback at n = 1024 x 8 -16 %, n = 128 x 512 -20 %, the C2 step
+    // -1 %; per-tile prologue / C read-modify-write of one CTA hides under
+    // three others' DMMA main loops).  DLA_GEMM_MASKED_TILE=128 restores the
+    // 128 x 64 tiles (tuning switch).  rowtile keeps its 128-row tiles: in-place
+    // trmm correctness depends on them.
+    static const bool masked128 = [] {
+      const char* e = getenv("DLA_GEMM_MASKED_TILE");
+      return e && atoi(e) == 128;
+    }();
+    if (!masked128 && !rowtile && large &&
+        (g.k <= DLAB_SHORTK || g.mask != MASK_FULL || g.tri_a != TRI_NONE || g.tri_b != TRI_NONE))
+      large = false;
     if (g.n <= 32 && g.k >= 128 && g.m >= 64 && !rowtile) {
       using C = CfgN;
       g.tiles_m = (g.m + C::BM - 1) / C::BM;
