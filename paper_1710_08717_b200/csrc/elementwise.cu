@@ -5,6 +5,8 @@
 // ExtractDiag -> Log -> Sum, dl/tape.hpp:789-795, :714, :747-755, pullbacks
 // :1038-1045, :969-975, :1080-1086).  All HBM-bound; grid-stride loops over
 // (batch x elements) sized to the SM count.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace dlab {
@@ -17,6 +19,24 @@ __global__ void k_copy(int64_t batch, int64_t m, int64_t n, MatB<const T> src, M
     const int64_t b = t / (m * n), r = t % (m * n), i = r / n, j = r % n;
     if (slice_failed(skip, b)) continue;
     *dst.at(b, i, j) = *src.at(b, i, j);
+  }
+}
+
+// Packed (contiguous) copy: 16-byte vectors when both ends are aligned, no
+// per-element index arithmetic (the generic k_copy's four 64-bit div/mods per
+// element made it ALU-bound).
+template <typename T>
+__global__ void k_copy_flat(int64_t count, const T* __restrict__ src, T* __restrict__ dst, bool vec) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x, t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (vec) {
+    constexpr int V = 16 / sizeof(T);
+    using V4 = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+    const int64_t nv = count / V;
+    for (int64_t t = t0; t < nv; t += stride)
+      reinterpret_cast<V4*>(dst)[t] = reinterpret_cast<const V4*>(src)[t];
+    for (int64_t t = nv * V + t0; t < count; t += stride) dst[t] = src[t];
+  } else {
+    for (int64_t t = t0; t < count; t += stride) dst[t] = src[t];
   }
 }
 
@@ -96,6 +116,34 @@ __global__ void k_square(int64_t batch, int64_t n, MatB<T> x, int op, T alpha, c
         break;
     }
   DLAB_ROWS_END
+}
+
+// tril(src) -> dst (full square, zeros above), row-mapped, two columns per
+// thread with 16-byte loads / stores.
+template <typename T>
+__global__ void k_tri_copy_vec(int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst) {
+  using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+  const int64_t pairs = (n + 1) / 2;
+  for (int64_t row = blockIdx.y; row < batch * n; row += gridDim.y) {
+    const int64_t b = row / n, i = row - b * n;
+    const T* sr = src.at(b, i, 0);
+    T* dr = dst.at(b, i, 0);
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < pairs; p += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t j = 2 * p;
+      if (j + 1 < n) {
+        V2 v;
+        if (j + 1 <= i) {
+          v = *reinterpret_cast<const V2*>(sr + j);
+        } else {
+          v.x = j <= i ? sr[j] : T(0);
+          v.y = T(0);
+        }
+        *reinterpret_cast<V2*>(dr + j) = v;
+      } else {
+        dr[j] = j <= i ? sr[j] : T(0);
+      }
+    }
+  }
 }
 
 template <typename T>
@@ -302,6 +350,15 @@ template <typename T>
 dla_status ew_copy(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> src, MatB<T> dst,
                    const int32_t* skip) {
   if (batch * m * n == 0 || src.p == dst.p) return DLA_OK;
+  const bool packed = src.ld == n && dst.ld == n && (batch == 1 || (src.bs == m * n && dst.bs == m * n));
+  if (packed && skip == nullptr) {
+    const int64_t count = batch * m * n;
+    const bool vec = (reinterpret_cast<uintptr_t>(src.p) % 16 == 0) && (reinterpret_cast<uintptr_t>(dst.p) % 16 == 0);
+    k_copy_flat<T><<<blocks_for(count / (vec ? 16 / sizeof(T) : 1), 256, 148 * 16), 256, 0, c.stream>>>(count, src.p,
+                                                                                                        dst.p, vec);
+    DLAB_LAUNCH_CHECK();
+    return DLA_OK;
+  }
   k_copy<T><<<blocks_for(batch * m * n, 256), 256, 0, c.stream>>>(batch, m, n, src, dst, skip);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
@@ -364,6 +421,17 @@ dla_status ew_square(const Ctx& c, int64_t batch, int64_t n, MatB<T> x, int op, 
 template <typename T>
 dla_status ew_tri_copy(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, bool from_upper) {
   if (batch * n == 0) return DLA_OK;
+  const bool vec = !from_upper && src.ld % 2 == 0 && dst.ld % 2 == 0 && (batch == 1 || (src.bs % 2 == 0 && dst.bs % 2 == 0)) &&
+                   reinterpret_cast<uintptr_t>(src.p) % (2 * sizeof(T)) == 0 &&
+                   reinterpret_cast<uintptr_t>(dst.p) % (2 * sizeof(T)) == 0;
+  if (vec) {
+    const int64_t gx = std::max<int64_t>(1, (n / 2 + 255) / 256);
+    int64_t gy = std::max<int64_t>(1, (148 * 16) / gx);
+    gy = std::min<int64_t>(std::min<int64_t>(gy, batch * n), 65535);
+    k_tri_copy_vec<T><<<dim3((unsigned)gx, (unsigned)gy), 256, 0, c.stream>>>(batch, n, src, dst);
+    DLAB_LAUNCH_CHECK();
+    return DLA_OK;
+  }
   k_tri_copy<T><<<row_grid(batch, n), 256, 0, c.stream>>>(batch, n, src, dst, from_upper);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
