@@ -384,6 +384,18 @@ dla_status dla_kalman_nll_fwdbwd_f32(int64_t batch, int64_t h, int64_t d, int64_
                                      float* shbar, float* svbar, float* mu0bar, float* s0bar,
                                      float* obsbar, int32_t* info, void* ws, size_t ws_bytes,
                                      void* stream);
+/* The GP step's pullback tail fused (dl/models.hpp:115-135 backward from
+ * Lbar): potrf_backward_into (dl/adjoints.hpp:175-191) up to
+ * Z = L^-T P' L^-1 with L^-1 from dla_gp_potrf_inv_f64 / _begin (iws, the
+ * same workspace), then the RBF pullback reading Abar = 1/2 (Z + Z^T) tile
+ * pair by tile pair (Abar is never materialized; lbar is clobbered).  grads
+ * and xbar as dla_gp_rbf_bwd_f64.  rws: dla_gp_pullback_ws_bytes. */
+size_t dla_gp_rbf_bwd_sym_ws_bytes(int64_t batch, int64_t n, int64_t d);
+size_t dla_gp_pullback_ws_bytes(int64_t batch, int64_t n, int64_t d);
+dla_status dla_gp_pullback_f64(int64_t batch, int64_t n, int64_t d, const double* x, double sigma2,
+                               double ell2, double lam, double* lbar, const double* l, double* xbar,
+                               double* grads, void* iws, size_t iws_bytes, void* rws, size_t rws_bytes,
+                               void* stream);
 /* nll[b] = quad[b] + logdet[b] + n/2 log(2 pi)  (dl/models.hpp:100-103). */
 dla_status dla_gp_nll_assemble_f64(int64_t batch, int64_t n, const double* quad,
                                    const double* logdet, double* nll, void* stream);

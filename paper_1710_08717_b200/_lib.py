@@ -100,6 +100,13 @@ class _Lib:
         L.dla_ml_reduce_ws_bytes.argtypes = [_i64]
         L.dla_ml_reduce_f64.argtypes = [_i64, _i64, _vp, _vp, _vp, C.c_double, _vp, _vp, _sz, _vp]
         L.dla_ml_reduce_f64.restype = _int
+        L.dla_gp_pullback_ws_bytes.restype = _sz
+        L.dla_gp_pullback_ws_bytes.argtypes = [_i64, _i64, _i64]
+        L.dla_gp_rbf_bwd_sym_ws_bytes.restype = _sz
+        L.dla_gp_rbf_bwd_sym_ws_bytes.argtypes = [_i64, _i64, _i64]
+        L.dla_gp_pullback_f64.argtypes = [_i64, _i64, _i64, _vp, C.c_double, C.c_double, C.c_double, _vp, _vp, _vp,
+                                          _vp, _vp, _sz, _vp, _sz, _vp]
+        L.dla_gp_pullback_f64.restype = _int
         L.dla_potrf_inv_join_f64.argtypes = [_vp]
         L.dla_potrf_inv_join_f64.restype = _int
         for sfx in ("f32", "f64"):
@@ -142,7 +149,8 @@ def exported_symbols():
              "dla_potrf_bwd_begin_f64", "dla_potrf_bwd_end_f64", "dla_gp_potrf_inv_f64",
              "dla_kalman_ws_bytes_f32", "dla_kalman_ws_bytes_f64",
              "dla_kalman_nll_fwdbwd_f32", "dla_kalman_nll_fwdbwd_f64",
-             "dla_tape_ew_ws_bytes", "dla_tape_ew_f32", "dla_tape_ew_f64"]
+             "dla_tape_ew_ws_bytes", "dla_tape_ew_f32", "dla_tape_ew_f64",
+             "dla_gp_rbf_bwd_sym_ws_bytes", "dla_gp_pullback_ws_bytes", "dla_gp_pullback_f64"]
     for name in _SIGS:
         for s in ("f32", "f64"):
             names.append(f"dla_{name}_{s}")

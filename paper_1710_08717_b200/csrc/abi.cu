@@ -701,6 +701,34 @@ dla_status potrf_bwd_end(const Ctx& cx, int64_t batch, int64_t n, T* abar, const
   return potrf_bwd_finish<T>(cx, batch, n, pk(abar, n, n), cpk(wp, n, n), tt);
 }
 
+// The GP step's pullback tail in one call: potrf_bwd_end up to Z (no Abar
+// pass) and the symmetric RBF pullback reading Z directly (gp.cu
+// k_rbf_bwd_sym).  lbar is clobbered (W scratch).  Falls back to
+// potrf_bwd_end + the row-wise RBF pullback where the inverse path or the
+// feature count does not apply.
+dla_status gp_pullback(const Ctx& cx, int64_t batch, int64_t n, int64_t d, const double* x, double sigma2,
+                       double ell2, double lam, double* lbar, const double* l, double* xbar, double* grads, void* rws,
+                       size_t rws_bytes) {
+  if (bad_dims(batch, n) || d < 1) return DLA_ERR_SHAPE;
+  if (batch * n == 0) return DLA_OK;
+  if (!inv_eligible<double>(n) || !gp_rbf_sym_ok(d)) {
+    DLAB_TRY(potrf_bwd_end<double>(cx, batch, n, lbar, lbar, l, 1));
+    return dla_gp_rbf_bwd_f64(batch, n, d, x, sigma2, ell2, lam, lbar, xbar, grads, rws, rws_bytes, cx.stream);
+  }
+  DLAB_SCRATCH(inv, cx, potrf_inv_ws<double>(batch, n));
+  double* wp = inv.as<double>();
+  MatB<double> tt = pk(wp + batch * n * n, n, n);
+  const dla_status st = potrf_bwd_phi<double>(cx, batch, n, cpk(lbar, n, n), cpk(l, n, n), true, tt);
+  ForkRes& f = fork_res(FORK_INV, cx.stream);
+  {
+    std::lock_guard<std::mutex> lk(f.mu);
+    cudaStreamWaitEvent(cx.stream, f.ev[1], 0);
+  }
+  if (st != DLA_OK) return st;
+  DLAB_TRY(potrf_bwd_finish_z<double>(cx, batch, n, pk(lbar, n, n), cpk(wp, n, n), tt));
+  return gp_rbf_bwd_sym(batch, n, d, x, sigma2, ell2, lam, tt.p, xbar, grads, rws, rws_bytes, cx.stream);
+}
+
 // Factorization + early inverse for drivers (the GP step): the blocked
 // Cholesky signals once block columns [0, n/2) are final; from then on the
 // side stream forms L11^{-1} and T1 = L21 L11^{-1} (half of the inverse's
@@ -1114,6 +1142,19 @@ dla_status dla_potrf_bwd_end_f64(int64_t batch, int64_t n, double* abar, const d
   if (batch >= 0 && n >= 0 && (ws ? ws_bytes : 0) < ws_potrf_split<double>(batch, n)) return DLA_ERR_WORKSPACE;
   DLA_ARENA(ws, ws_bytes, stream, nullptr);
   return potrf_bwd_end<double>(cx, batch, n, abar, lbar, l, lower);
+}
+size_t dla_gp_pullback_ws_bytes(int64_t batch, int64_t n, int64_t d) {
+  if (batch < 0 || n < 0 || d < 0) return 0;
+  return std::max(dla_gp_rbf_ws_bytes(batch, n, d), dla_gp_rbf_bwd_sym_ws_bytes(batch, n, d));
+}
+dla_status dla_gp_pullback_f64(int64_t batch, int64_t n, int64_t d, const double* x, double sigma2, double ell2,
+                               double lam, double* lbar, const double* l, double* xbar, double* grads, void* iws,
+                               size_t iws_bytes, void* rws, size_t rws_bytes, void* stream) {
+  if (batch >= 0 && n >= 0 && (iws ? iws_bytes : 0) < ws_potrf_split<double>(batch, n)) return DLA_ERR_WORKSPACE;
+  if (batch >= 0 && n >= 0 && d >= 0 && (rws ? rws_bytes : 0) < dla_gp_pullback_ws_bytes(batch, n, d))
+    return DLA_ERR_WORKSPACE;
+  DLA_ARENA(iws, iws_bytes, stream, nullptr);
+  return gp_pullback(cx, batch, n, d, x, sigma2, ell2, lam, lbar, l, xbar, grads, rws, rws_bytes);
 }
 dla_status dla_potrf_inv_join_f64(void* stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -299,6 +299,142 @@ __global__ void k_rbf_finalize(int64_t batch, int64_t n, int64_t splits, const d
   }
 }
 
+// ---- symmetric pullback straight from Z (the GP step's fused tail) ----
+// potrf_backward's last two products leave Z = L^-T P' L^-1 and the operator
+// would materialize Abar = 1/2 (Z + Z^T) (one more 3 n^2 HBM pass) before the
+// RBF pullback reads Abar back.  Here one CTA takes a 64 x 64 tile PAIR
+// (I, J), I >= J, of the symmetric problem: it reads Z(I,J) and Z(J,I),
+// forms Abar_ij = 0.5 (Z_ij + Z_ji) exactly as that add-transpose pass does
+// (same bits), evaluates the RBF entry ONCE for (i,j) and (j,i) (they are the
+// same bits: the distance formula commutes), and contributes the pullback of
+// both: scalar sums twice, xbar rows of I (sum over j) and of J (sum over i).
+// Half the exp work of the row-wise kernel, no Abar pass.  Per-(row, tile)
+// xbar partials and per-pair scalar partials are reduced in a fixed order
+// afterwards: deterministic.
+constexpr int SBT = 64;  // tile
+constexpr size_t SYM_SMEM = sizeof(double) * SBT * (SBT + 1);
+template <int D>
+__global__ void __launch_bounds__(256) k_rbf_bwd_sym(int64_t n, int64_t tiles, int64_t npairs, const double* x,
+                                                    const double* s, double sigma2, double two_ell2,
+                                                    const double* z, double* xpart, double* part) {
+  extern __shared__ double sym_smem[];
+  double(*zr)[SBT + 1] = reinterpret_cast<double(*)[SBT + 1]>(sym_smem);  // Z(I,J) -> Abar(I,J) -> W(I,J)
+  __shared__ double xI[SBT][D + 1], xJ[SBT][D + 1];
+  __shared__ double sI[SBT], sJ[SBT];
+  __shared__ double red[3][8];
+  const int64_t b = blockIdx.x / npairs, pr = blockIdx.x % npairs;
+  int64_t I = (int64_t)((sqrt(8.0 * (double)pr + 1.0) - 1.0) * 0.5);
+  while (I * (I + 1) / 2 > pr) --I;
+  while ((I + 1) * (I + 2) / 2 <= pr) ++I;
+  const int64_t J = pr - I * (I + 1) / 2;
+  const bool diag = I == J;
+  const int64_t i0 = I * SBT, j0 = J * SBT;
+  const double* xb = x + b * n * D;
+  const double* sb = s + b * n;
+  const double* zb = z + b * n * n;
+  const int t = threadIdx.x;
+  for (int e = t; e < SBT * D; e += 256) {
+    const int r = e / D, f = e % D;
+    xI[r][f] = i0 + r < n ? xb[(i0 + r) * D + f] : 0.0;
+    xJ[r][f] = j0 + r < n ? xb[(j0 + r) * D + f] : 0.0;
+  }
+  if (t < SBT) {
+    sI[t] = i0 + t < n ? sb[i0 + t] : 0.0;
+    sJ[t] = j0 + t < n ? sb[j0 + t] : 0.0;
+  }
+  for (int e = t; e < SBT * SBT; e += 256) {
+    const int r = e >> 6, c = e & 63;
+    zr[r][c] = (i0 + r < n && j0 + c < n) ? zb[(i0 + r) * n + j0 + c] : 0.0;
+  }
+  __syncthreads();
+  // Abar_ij = 0.5 (Z_ij + Z_ji) (k_add_transpose's bits): Z(J,I) read by
+  // coalesced rows and folded in transposed; every element has one owner
+  for (int e = t; e < SBT * SBT; e += 256) {
+    const int r = e >> 6, c = e & 63;  // Z(J,I)[r][c] = Z_{i0+c, j0+r}^T partner of (c, r)
+    const double zji = (j0 + r < n && i0 + c < n) ? zb[(j0 + r) * n + i0 + c] : 0.0;
+    zr[c][r] = 0.5 * (zr[c][r] + zji);
+  }
+  __syncthreads();
+  const double inv2l = 1.0 / two_ell2;
+  double ps = 0.0, pe = 0.0, pl = 0.0;
+  const int jl = t & 63;
+  for (int rr = 0; rr < 16; ++rr) {
+    const int il = (t >> 6) + 4 * rr;
+    const int64_t gi = i0 + il, gj = j0 + jl;
+    double w = 0.0;
+    if (gi < n && gj < n) {
+      double g = 0.0;
+#pragma unroll
+      for (int f = 0; f < D; ++f) g += xI[il][f] * xJ[jl][f];
+      const double dist = (sI[il] + sJ[jl]) - 2.0 * g;
+      const double Dv = dist * inv2l;
+      const double E = exp(-Dv);
+      const double kb = zr[il][jl];  // Abar_ij
+      ps += kb * E;
+      const double nb = kb * sigma2 * E;
+      pe += nb * Dv;
+      if (gi == gj) pl += kb;
+      w = -nb * inv2l;
+    }
+    zr[il][jl] = w;  // owned by this thread
+  }
+  // scalar partials: the off-diagonal pair stands for (i,j) and (j,i)
+  const double mult = diag ? 1.0 : 2.0;
+  ps *= mult;
+  pe *= mult;
+  const int warp = t >> 5, lane = t & 31;
+  for (int o = 16; o; o >>= 1) {
+    ps += __shfl_xor_sync(0xffffffffu, ps, o);
+    pe += __shfl_xor_sync(0xffffffffu, pe, o);
+    pl += __shfl_xor_sync(0xffffffffu, pl, o);
+  }
+  if (lane == 0) {
+    red[0][warp] = ps;
+    red[1][warp] = pl;
+    red[2][warp] = pe;
+  }
+  __syncthreads();
+  if (t < 3) {
+    double a = 0.0;
+    for (int w8 = 0; w8 < 8; ++w8) a += red[t][w8];
+    part[(b * npairs + pr) * 3 + t] = a;
+  }
+  // xbar partials: row side (I rows, sum over j) and, off the diagonal, the
+  // column side (J rows, sum over i): x_r sum w - sum w x_other, split over
+  // two threads per line (halves of the tile) and combined by one shuffle
+  const int side = t >> 7, line = (t >> 1) & 63, half = t & 1;
+  if (side == 1 && diag) return;  // (warp-uniform: warps 4..7)
+  double sw = 0.0, acc[D];
+#pragma unroll
+  for (int f = 0; f < D; ++f) acc[f] = 0.0;
+  for (int k = half * 32; k < half * 32 + 32; ++k) {
+    const double w = side == 0 ? zr[line][k] : zr[k][line];
+    sw += w;
+#pragma unroll
+    for (int f = 0; f < D; ++f) acc[f] += w * (side == 0 ? xJ[k][f] : xI[k][f]);
+  }
+  sw += __shfl_xor_sync(0xffffffffu, sw, 1);
+#pragma unroll
+  for (int f = 0; f < D; ++f) acc[f] += __shfl_xor_sync(0xffffffffu, acc[f], 1);
+  const int64_t row = (side == 0 ? i0 : j0) + line;
+  const int64_t other = side == 0 ? J : I;
+  if (half == 0 && row < n) {
+    double* xp = xpart + ((b * n + row) * tiles + other) * D;
+#pragma unroll
+    for (int f = 0; f < D; ++f) xp[f] = (side == 0 ? xI[line][f] : xJ[line][f]) * sw - acc[f];
+  }
+}
+
+// fixed-order finalization of the tile-pair partials
+__global__ void k_rbf_sym_xbar(int64_t rows, int64_t tiles, int d, const double* xpart, double* xbar) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows * d; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / d, f = t % d;
+    double acc = 0.0;
+    for (int64_t q = 0; q < tiles; ++q) acc += xpart[(r * tiles + q) * d + f];
+    xbar[t] = 4.0 * acc;
+  }
+}
+
 __global__ void k_nll(int64_t batch, int64_t n, const double* quad, const double* logdet, double* nll) {
   const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (b < batch) nll[b] = (quad[b] + logdet[b]) + 0.5 * (double)n * 1.8378770664093454835606594728112353;
@@ -382,6 +518,46 @@ __global__ void __launch_bounds__(MLT) k_ml_final(int64_t nparts, int64_t batch,
 }
 
 }  // namespace
+
+// Symmetric RBF pullback from Z (the fused GP tail): workspace = row norms +
+// per-(row, tile) xbar partials + per-pair scalar partials.
+extern "C" size_t dla_gp_rbf_bwd_sym_ws_bytes(int64_t batch, int64_t n, int64_t d) {
+  const int64_t tiles = (n + SBT - 1) / SBT, npairs = tiles * (tiles + 1) / 2;
+  return sizeof(double) * (size_t)(batch * n + batch * n * tiles * d + batch * npairs * 3);
+}
+
+dla_status gp_rbf_bwd_sym(int64_t batch, int64_t n, int64_t d, const double* x, double sigma2, double ell2, double lam,
+                          const double* z, double* xbar, double* grads, void* ws, size_t ws_bytes, cudaStream_t s) {
+  const int64_t tiles = (n + SBT - 1) / SBT, npairs = tiles * (tiles + 1) / 2;
+  if (!ws || ws_bytes < dla_gp_rbf_bwd_sym_ws_bytes(batch, n, d)) return DLA_ERR_WORKSPACE;
+  double* sq = static_cast<double*>(ws);
+  double* xpart = sq + batch * n;
+  double* part = xpart + batch * n * tiles * d;
+  k_rowsq<<<blocks_for(batch * n, 256), 256, 0, s>>>(batch, n, d, x, sq);
+  const unsigned grid = (unsigned)(batch * npairs);
+  switch (d) {
+#define DLAB_SYM_CASE(DD)                                                                                  \
+  case DD:                                                                                                 \
+    ensure_smem_attr(k_rbf_bwd_sym<DD>, SYM_SMEM);                                                        \
+    k_rbf_bwd_sym<DD><<<grid, 256, SYM_SMEM, s>>>(n, tiles, npairs, x, sq, sigma2, ell2 * 2.0, z, xpart, part); \
+    break;
+    DLAB_SYM_CASE(1)
+    DLAB_SYM_CASE(2)
+    DLAB_SYM_CASE(3)
+    DLAB_SYM_CASE(4)
+    DLAB_SYM_CASE(8)
+    DLAB_SYM_CASE(16)
+#undef DLAB_SYM_CASE
+    default:
+      return DLA_ERR_SHAPE;
+  }
+  k_rbf_finalize<<<(unsigned)batch, FT, 0, s>>>(batch, npairs, 1, part, sigma2, ell2, lam, ell2 * 2.0, grads);
+  if (xbar) k_rbf_sym_xbar<<<blocks_for(batch * n * d, 256), 256, 0, s>>>(batch * n, tiles, (int)d, xpart, xbar);
+  note_launch(xbar ? 3 : 2);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+bool gp_rbf_sym_ok(int64_t d) { return d == 1 || d == 2 || d == 3 || d == 4 || d == 8 || d == 16; }
 }  // namespace dlab
 
 using namespace dlab;

@@ -217,6 +217,17 @@ dla_status potrf_bwd_finish(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar
   return ew_add_transpose<T>(c, batch, n, C_(tt), abar, T(0.5));
 }
 
+// potrf_bwd_finish without the final symmetrization: Z = L^-T P' L^-1 stays
+// in tt (Abar = 1/2 (Z + Z^T) is formed by the caller's consumer; abar is
+// clobbered as scratch for W).
+template <typename T>
+dla_status potrf_bwd_finish_z(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> wi, MatB<T> tt) {
+  DLAB_TRY(gemm<T>(c, batch, n, n, n, T(1), C_(tt), false, wi, false, T(0), abar, MASK_LOWER, nullptr, TRI_LOWER,
+                   TRI_LOWER));
+  return gemm<T>(c, batch, n, n, n, T(1), wi, true, C_(abar), false, T(0), tt, MASK_FULL, nullptr, TRI_UPPER,
+                 TRI_LOWER);
+}
+
 template <typename T>
 dla_status potrf_bwd_from_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> lbar, MatB<const T> l,
                               bool lower, MatB<const T> wi, MatB<T> tt) {
@@ -312,7 +323,8 @@ dla_status potri_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
   template dla_status potrf_bwd_from_inv<T>(const Ctx&, int64_t, int64_t, MatB<T>, MatB<const T>, MatB<const T>, \
                                             bool, MatB<const T>, MatB<T>);                                         \
   template dla_status potrf_bwd_phi<T>(const Ctx&, int64_t, int64_t, MatB<const T>, MatB<const T>, bool, MatB<T>); \
-  template dla_status potrf_bwd_finish<T>(const Ctx&, int64_t, int64_t, MatB<T>, MatB<const T>, MatB<T>);
+  template dla_status potrf_bwd_finish<T>(const Ctx&, int64_t, int64_t, MatB<T>, MatB<const T>, MatB<T>);        \
+  template dla_status potrf_bwd_finish_z<T>(const Ctx&, int64_t, int64_t, MatB<T>, MatB<const T>, MatB<T>);
 INST(double)
 INST(float)
 

@@ -44,6 +44,13 @@ dla_status potrf_bwd_phi(const Ctx& c, int64_t batch, int64_t n, MatB<const T> l
 template <typename T>
 dla_status potrf_bwd_finish(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> wi, MatB<T> tt);
 template <typename T>
+dla_status potrf_bwd_finish_z(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> wi, MatB<T> tt);
+
+// gp.cu: the symmetric RBF pullback straight from potrf_bwd's Z (fused GP tail)
+bool gp_rbf_sym_ok(int64_t d);
+dla_status gp_rbf_bwd_sym(int64_t batch, int64_t n, int64_t d, const double* x, double sigma2, double ell2, double lam,
+                          const double* z, double* xbar, double* grads, void* ws, size_t ws_bytes, cudaStream_t s);
+template <typename T>
 dla_status trmm_gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x, bool right,
                      bool trans, bool lower, T alpha);
 template <typename T>

@@ -11,10 +11,13 @@ of independent GP problems:
   backward, phibar = 1:
     zbar = z;  (ybar, Lbar) = trsm_backward(zbar, L, z)   (C-ABI op)
     Lbar += diag(1 / L_ii)                                (sumlogdiag_backward)
-    Abar = potrf_backward(Lbar, L)  (in place)            (C-ABI op, split:
+    Abar = potrf_backward(Lbar, L)                        (C-ABI op, split:
            L^-1 forms on a side stream from right after potrf, overlapping
            the solves; dla_potrf_bwd_{begin,end}_f64, bitwise = the op)
     (d/dlog sigma2, d/dlog ell2, d/dlog lam, xbar) = RBF pullback(Abar)
+  by default the last two are one call (dla_gp_pullback_f64): Abar's
+  symmetrization is folded into a tile-pair RBF pullback that reads
+  Z = L^-T P' L^-1 directly (half the exp work, no Abar pass).
 
 Every step is a libdla_b200.so call on torch's current stream; the driver
 allocates all buffers once so a step can be captured in a CUDA graph.
@@ -31,6 +34,8 @@ from ._lib import lib
 
 LOG_2PI = 1.8378770664093454835606594728112353
 _EARLY = __import__("os").environ.get("DLA_GP_EARLY", "1") != "0"
+# the pullback tail fused (dla_gp_pullback_f64: Z -> symmetric RBF pullback, no Abar pass)
+_FUSED_TAIL = __import__("os").environ.get("DLA_GP_FUSED_TAIL", "1") != "0"
 
 
 class GPNLL:
@@ -51,7 +56,7 @@ class GPNLL:
         self.xbar = torch.empty(batch, n, d, **f) if want_xbar else None
         self.nll = torch.empty(batch, **f)
         self.info = torch.zeros(batch, dtype=torch.int32, device=self.device)
-        nb = int(lib().lib.dla_gp_rbf_ws_bytes(batch, n, d))
+        nb = int(lib().lib.dla_gp_pullback_ws_bytes(batch, n, d))
         self.ws = torch.empty(max(nb, 8), dtype=torch.uint8, device=self.device)
         self.ws_bytes = nb
         # split potrf pullback: L^-1 is formed on a side stream while the
@@ -101,14 +106,25 @@ class GPNLL:
         # backward (phibar = 1): zbar = z
         L.trsm_backward_into(self.ybar, self.lbar, self.z, self.a, self.z, False, False, True, 1.0)
         L.sumlogdiag_backward_into(self.lbar, self.ones, self.a, accumulate=True)
+        xb = C.c_void_p(self.xbar.data_ptr()) if self.xbar is not None else None
+        if _FUSED_TAIL:
+            # Abar = potrf_backward(Lbar) is consumed tile pair by tile pair by the
+            # RBF pullback straight from Z = L^-T P' L^-1 (never materialized)
+            st = lib_.dla_gp_pullback_f64(B, n, d, C.c_void_p(x.data_ptr()), sigma2, ell2, lam,
+                                          C.c_void_p(self.lbar.data_ptr()), C.c_void_p(self.a.data_ptr()), xb,
+                                          C.c_void_p(self.grads.data_ptr()), C.c_void_p(self.iws.data_ptr()),
+                                          self.iws_bytes, C.c_void_p(self.ws.data_ptr()), self.ws_bytes,
+                                          self._stream())
+            if st:
+                L._raise_status(st, "gp_pullback")
+            return self.nll, self.grads, self.xbar, self.ybar
         st = lib_.dla_potrf_bwd_end_f64(B, n, C.c_void_p(self.lbar.data_ptr()), C.c_void_p(self.lbar.data_ptr()),
                                         C.c_void_p(self.a.data_ptr()), 1, C.c_void_p(self.iws.data_ptr()),
                                         self.iws_bytes, self._stream())
         if st:
             L._raise_status(st, "potrf_bwd_end")
         st = lib().lib.dla_gp_rbf_bwd_f64(B, n, d, C.c_void_p(x.data_ptr()), sigma2, ell2, lam,
-                                          C.c_void_p(self.lbar.data_ptr()),
-                                          C.c_void_p(self.xbar.data_ptr()) if self.xbar is not None else None,
+                                          C.c_void_p(self.lbar.data_ptr()), xb,
                                           C.c_void_p(self.grads.data_ptr()), C.c_void_p(self.ws.data_ptr()),
                                           self.ws_bytes, self._stream())
         if st:
