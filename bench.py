@@ -43,7 +43,7 @@ METRIC = "GP NLL+grad evals/s"
 BASELINE_METRIC = "batched potrf fwd+bwd matrices/s & GFLOP/s vs FP64 peak; GP NLL+grad evals/s"
 PEAKS_FILE = os.path.join(ROOT, "profiles", "peaks_fp64_fp32_r01.json")
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
-TRAFFIC_FILE = os.path.join(ROOT, "profiles", "gemm_traffic_r01.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "gemm_traffic_r02.json")
 
 
 def parse():
@@ -570,7 +570,7 @@ def main():
             "step_fp64_tflops": step_tflops,
             "step_frac_of_fp64_peak": step_tflops / fp64_peak,
             "roofline": {"bound": "tensor",
-                         "kernel": "dgemm_dmma<128x64 tiles, 2 CTAs/SM, transposed A> (FP64 DMMA m8n8k4): Z = L^-T W "
+                         "kernel": "dgemm_dmma<64x64 tiles, 4 CTAs/SM, transposed A> (FP64 DMMA m8n8k4): Z = L^-T W "
                                    "inside potrf_bwd, the step's largest launch",
                          "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                          "frac": (achieved / fp64_peak) if achieved else None, "traffic": traffic,
