@@ -243,7 +243,7 @@ __device__ __forceinline__ void warp_ltinv_col(const T* Ls, T (&x)[WN], int n) {
 // Abar = 1/2 sym(L^-T copyltu(L^T Lbar) L^-1) to o (dl/adjoints.hpp:175-191).
 template <typename T>
 __device__ __forceinline__ void warp_potrf_bwd_core(int n, int lane, const T* L, T* W, const T* dg, const T* rd, T* o,
-                                                    int ldo) {
+                                                    int ldo, bool store = true) {
   constexpr int VN = Bc<T>::N, LLD = Bc<T>::LLD;
   // Phi = copyltu(L^T Lbar), lower part of column `lane`: Phi_ij = sum_{k>=i} L_ki Lbar_kj
   // (i >= j = lane) = L_ii (Lbar_ij + sum_{k>i} Ls_ki Lbar_kj), accumulated row by row of Ls
@@ -300,7 +300,7 @@ __device__ __forceinline__ void warp_potrf_bwd_core(int n, int lane, const T* L,
   for (int i = 0; i < WN; ++i)
     if (i < n && lane < n) {
       const T hi = x[i] * T(0.5), hj = W[lane * WLD + i] * T(0.5);
-      o[i * ldo + lane] = (i == lane) ? hi : (hi + hj) * T(0.5);  // == (hi + hj) / 2 exactly
+      if (store) o[i * ldo + lane] = (i == lane) ? hi : (hi + hj) * T(0.5);  // == (hi + hj) / 2 exactly
     }
 }
 
@@ -376,8 +376,15 @@ __global__ void __launch_bounds__(wpc_bwd<T>() * 32) k_chol_chain_warp(int n, in
   constexpr int per_warp = WN * LLD + WN * WLD + 6 * WN;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t b = (int64_t)blockIdx.x * wpc_bwd<T>() + warp;
-  if (b >= batch) return;
+  // The warps of a CTA walk the chain's phases in lockstep (a barrier between
+  // phases), so the SM fetches one code region at a time for all of them: the
+  // chain is ~14 k straight-line instructions and independent warps each
+  // streamed their own region through the instruction cache (ncu: stall
+  // no_instruction).  Inactive / failed warps keep computing on a clamped
+  // slice and only suppress their stores.
+  const int64_t bw = (int64_t)blockIdx.x * wpc_bwd<T>() + warp;
+  bool ok = bw < batch;
+  const int64_t b = ok ? bw : batch - 1;
   T* L = reinterpret_cast<T*>(smem_raw) + warp * per_warp;  // unit-diagonal L D^-1 (LLD rows)
   T* W = L + WN * LLD;                                       // A, then L (rows), then Lbar (columns)
   T* buf = W + WN * WLD;
@@ -411,19 +418,20 @@ __global__ void __launch_bounds__(wpc_bwd<T>() * 32) k_chol_chain_warp(int n, in
   mabs = warp_max(mabs);
   masym = warp_max(masym);
   if (masym > Num<T>::sym_rtol * (mabs > T(0) ? mabs : T(1))) {
-    if (lane == 0) record_failure(info, b, DLA_ERR_ASYMMETRIC, 0);
-    return;
+    if (lane == 0 && ok) record_failure(info, b, DLA_ERR_ASYMMETRIC, 0);
+    ok = false;
   }
+  __syncthreads();
   T r[WN];
 #pragma unroll
   for (int c = 0; c < WN; ++c) r[c] = (lane < n && c <= lane) ? W[lane * WLD + c] : (c == lane ? T(1) : T(0));
   int failed = -1;
   wchol_col<T, 0>(r, lane, n, buf, failed, r[0]);
   if (failed >= 0) {
-    if (lane == 0) record_failure(info, b, DLA_ERR_NOT_SPD, failed);
-    return;
+    if (lane == 0 && ok) record_failure(info, b, DLA_ERR_NOT_SPD, failed);
+    ok = false;
   }
-  __syncwarp();
+  __syncthreads();
 #pragma unroll
   for (int c = 0; c < WN; ++c)
     if (c < n && lane < n) W[lane * WLD + c] = c <= lane ? r[c] : T(0);
@@ -448,7 +456,7 @@ __global__ void __launch_bounds__(wpc_bwd<T>() * 32) k_chol_chain_warp(int n, in
   sv[lane] = lane < n ? z : T(0);
   lg[lane] = lane < n ? Num<T>::log_(d) : T(0);
   __syncwarp();
-  if (lane == 0) {  // sequential i order, as the tape's Sum node
+  if (lane == 0 && ok) {  // sequential i order, as the tape's Sum node
     T q = T(0), ldt = T(0);
     for (int i = 0; i < n; ++i) q += sv[i] * sv[i];
     for (int i = 0; i < n; ++i) ldt += lg[i];
@@ -464,16 +472,16 @@ __global__ void __launch_bounds__(wpc_bwd<T>() * 32) k_chol_chain_warp(int n, in
       if (lane < k) zb -= W[k * WLD + lane] * sk;
     }
   }
-  if (lane < n) ybar[b * n + lane] = s_own;
-  __syncwarp();
+  if (lane < n && ok) ybar[b * n + lane] = s_own;
+  __syncthreads();
   sv[lane] = lane < n ? s_own : T(0);
   __syncwarp();
   // Lbar, column `lane`: -s_i z_lane (i >= lane) + 1 / L_ii on the diagonal
 #pragma unroll
   for (int i = 0; i < WN; ++i)
     if (i < n) W[i * WLD + lane] = (i >= lane && lane < n) ? -sv[i] * z + (i == lane ? rinv : T(0)) : T(0);
-  __syncwarp();
-  warp_potrf_bwd_core<T>(n, lane, L, W, dg, rd, abar.at(b, 0, 0), (int)abar.ld);
+  __syncthreads();
+  warp_potrf_bwd_core<T>(n, lane, L, W, dg, rd, abar.at(b, 0, 0), (int)abar.ld, ok);
 }
 }  // namespace
 
