@@ -478,6 +478,7 @@ dla_status sld_bwd(const Ctx& cx, int64_t batch, int64_t n, T* abar, const T* g,
 // --------------------------------------------------------------- gelqf
 template <typename T>
 size_t ws_gelqf_fwd(int64_t batch, int64_t m, int64_t n) {
+  if (sizeof(T) == 8 && gelqf_cqr_eligible(m, n)) return ws_gelqf_cqr(batch, m, n);
   // the panel GEMMs of gelqf_blocked have N or K = 32: never on the carving route
   return carve_bound(gelqf_ws_bytes<T>(batch, m, n, false));
 }
@@ -488,6 +489,10 @@ dla_status gelqf_fwd_abi(const Ctx& cx, int64_t batch, int64_t m, int64_t n, T* 
   if (overlap(q, bytes<T>(batch, m, n), l, bytes<T>(batch, m, m))) return DLA_ERR_ALIAS;
   DLAB_TRY(reset_info(cx, batch));
   if (batch * m == 0) return DLA_OK;
+  if constexpr (sizeof(T) == 8) {
+    if (gelqf_cqr_eligible(m, n))
+      return gelqf_cqr(cx, batch, m, n, reinterpret_cast<double*>(q), reinterpret_cast<double*>(l));
+  }
   DLAB_SCRATCH(ws, cx, gelqf_ws_bytes<T>(batch, m, n, false));
   return gelqf_fwd<T>(cx, batch, m, n, q, l, ws.p);
 }

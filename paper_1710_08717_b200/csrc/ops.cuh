@@ -88,6 +88,11 @@ template <typename T>
 dla_status gelqf_blocked(const Ctx& c, int64_t batch, int64_t m, int64_t n, T* q, T* l, void* ws,
                          bool rank_check = true);
 
+// gelqf_cqr.cu: CholeskyQR2 LQ (f64) with a per-slice Householder fallback
+bool gelqf_cqr_eligible(int64_t m, int64_t n);
+size_t ws_gelqf_cqr(int64_t batch, int64_t m, int64_t n);
+dla_status gelqf_cqr(const Ctx& c, int64_t batch, int64_t m, int64_t n, double* q, double* l);
+
 // gelqf.cu
 template <typename T>
 size_t gelqf_ws_bytes(int64_t batch, int64_t m, int64_t n, bool backward);

@@ -64,7 +64,11 @@ def test_host_only_entry_points(lib):
     # the blocked compact-WY path (m >= 64) also keeps Yc, Z (m x n each),
     # T and W (m x 32 each) and the norm; backward: m*m (dl/adjoints.hpp:1-9)
     assert ws(8, 1, 256, 32, 512, 0, 0) == carve(256 * 32 * 8)
-    assert ws(8, 1, 256, 128, 512, 0, 0) == carve(256 * (2 * 128 * 512 + 2 * 128 * 32 + 128 + 1) * 8)
+    # f64, 64 <= m <= 512: CholeskyQR2 (A copy + two m x m factors + flags) with the
+    # Householder workspace kept for its per-slice fallback
+    hh = carve(256 * (2 * 128 * 512 + 2 * 128 * 32 + 128 + 1) * 8)
+    assert ws(8, 1, 256, 128, 512, 0, 0) >= carve(256 * 128 * 512 * 8) + 2 * carve(256 * 128 * 128 * 8) + hh
+    assert ws(8, 0, 256, 128, 512, 0, 0) == carve(256 * (2 * 128 * 512 + 2 * 128 * 32 + 128 + 1) * 4)  # f32: Householder
     assert ws(8, 0, 256, 128, 512, 0, 1) >= carve(256 * 128 * 128 * 4)
     assert ws(9, 1, 1024, 64, 64, 0, 1) == carve(1024 * 64 * 64 * 8)  # syevd bwd: n*n
     assert ws(5, 1, 1, 64, 64, 0, 0) == 0                              # small potrf: registers / smem only

@@ -437,6 +437,36 @@ def test_sumlogdiag(port, dt):
 
 
 # ------------------------------------------------------------------ gelqf
+def test_gelqf_cholesky_qr2_fallback(port):
+    """f64 64 <= m <= 512 runs CholeskyQR2 (csrc/gelqf_cqr.cu); slices it cannot
+    serve fall back to the Householder path per slice: an ill-conditioned
+    slice (row scales 1e0 .. 1e-9, kappa ~ 1e9) must still match the oracle,
+    and a rank-deficient slice must raise the reference's SingularError with
+    the reference's index while its neighbours complete."""
+    r = O.rng(23)
+    m, n, B = 128, 300, 4
+    a = r.standard_normal((B, m, n))
+    a[1] *= np.logspace(0, -9, m)[:, None]        # ill-conditioned: fallback, still full rank
+    q, l = L.gelqf(dev(a))
+    q, l = host(q), host(l)
+    wq, wl = batch_apply(port.gelqf, a)
+    assert_close(q, wq, np.float64, 10)
+    for b in range(B):  # L row scales span 1e9: compare per row
+        assert np.abs(l[b] - wl[b]).max(axis=1).max() <= 1e-9 * np.abs(wl[b]).max() + 1e-300
+        np.testing.assert_allclose(l[b], wl[b], rtol=1e-6, atol=1e-13 * np.abs(wl[b]).max())
+    # orthonormal rows on every path
+    for b in range(B):
+        assert np.abs(q[b] @ q[b].T - np.eye(m)).max() < 1e-13
+    a2 = r.standard_normal((B, m, n))
+    a2[2, 70] = a2[2, 3] + 2.0 * a2[2, 40]         # rank deficient at row 70
+    with pytest.raises(L.SingularError) as e:
+        L.gelqf(dev(a2))
+    assert e.value.batch_index == 2
+    with pytest.raises(O.OracleError) as eo:
+        port.gelqf(a2[2])
+    assert e.value.index == eo.value.index
+
+
 @pytest.mark.parametrize("dt", DTYPES)
 def test_gelqf(port, dt):
     r = O.rng(11)
