@@ -40,6 +40,24 @@ __global__ void k_copy_flat(int64_t count, const T* __restrict__ src, T* __restr
   }
 }
 
+// packed per-slice copy honouring the skip array (grid.y = slice)
+template <typename T>
+__global__ void k_copy_slices(int64_t per, const T* __restrict__ src, T* __restrict__ dst, const int32_t* skip,
+                              bool vec) {
+  const int64_t b = blockIdx.y;
+  if (slice_failed(skip, b)) return;
+  const T* s = src + b * per;
+  T* d = dst + b * per;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x, t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (vec) {
+    using V4 = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+    const int64_t nv = per / (16 / sizeof(T));
+    for (int64_t t = t0; t < nv; t += stride) reinterpret_cast<V4*>(d)[t] = reinterpret_cast<const V4*>(s)[t];
+  } else {
+    for (int64_t t = t0; t < per; t += stride) d[t] = s[t];
+  }
+}
+
 template <typename T>
 __global__ void k_scale(int64_t batch, int64_t m, int64_t n, MatB<T> x, T alpha, const int32_t* skip) {
   const int64_t total = batch * m * n;
@@ -351,6 +369,15 @@ dla_status ew_copy(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const
                    const int32_t* skip) {
   if (batch * m * n == 0 || src.p == dst.p) return DLA_OK;
   const bool packed = src.ld == n && dst.ld == n && (batch == 1 || (src.bs == m * n && dst.bs == m * n));
+  if (packed && skip != nullptr && batch <= 65535) {  // per-slice skip: one slice per grid row
+    const bool vec = (reinterpret_cast<uintptr_t>(src.p) % 16 == 0) && (reinterpret_cast<uintptr_t>(dst.p) % 16 == 0) &&
+                     (m * n) % (16 / sizeof(T)) == 0;
+    const int64_t per = m * n;
+    const unsigned gx = blocks_for(per / (vec ? 16 / sizeof(T) : 1), 256, std::max<int64_t>(1, 148 * 16 / batch));
+    k_copy_slices<T><<<dim3(gx, (unsigned)batch), 256, 0, c.stream>>>(per, src.p, dst.p, skip, vec);
+    DLAB_LAUNCH_CHECK();
+    return DLA_OK;
+  }
   if (packed && skip == nullptr) {
     const int64_t count = batch * m * n;
     const bool vec = (reinterpret_cast<uintptr_t>(src.p) % 16 == 0) && (reinterpret_cast<uintptr_t>(dst.p) % 16 == 0);

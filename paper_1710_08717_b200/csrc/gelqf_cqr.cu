@@ -36,28 +36,45 @@ inline MatB<const double> C_(MatB<double> m) { return MatB<const double>{m.p, m.
 
 // per slice: fb[b] = 1 when the CholeskyQR2 result must be replaced; the
 // Householder pass's skip mask hinfo[b] = 0 (run) / 1 (skip)
-__global__ void k_cqr_flags(int64_t batch, int64_t m, int64_t n, const double* a, const double* r1, const double* l,
-                            const int32_t* cinfo, int32_t* fb, int32_t* hinfo) {
-  __shared__ double red[32];
+__global__ void __launch_bounds__(256) k_cqr_flags(int64_t batch, int64_t m, int64_t n, const double* a,
+                                                   const double* r1, const double* l, const int32_t* cinfo,
+                                                   int32_t* fb, int32_t* hinfo) {
+  __shared__ double red[3][8];
   const int64_t b = blockIdx.x;
   const double* ab = a + b * m * n;
-  double mx = 0.0;
-  for (int64_t e = threadIdx.x; e < m * n; e += blockDim.x) mx = fmax(mx, fabs(ab[e]));
-  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  double mx = 0.0, dmin = INFINITY, dmax = 0.0, lmin = INFINITY;
+  for (int64_t e = t; e < m * n; e += 256) mx = fmax(mx, fabs(ab[e]));
+  for (int64_t i = t; i < m; i += 256) {
+    const double d = fabs(r1[b * m * m + i * m + i]);
+    dmin = fmin(dmin, d);
+    dmax = fmax(dmax, d);
+    lmin = fmin(lmin, fabs(l[b * m * m + i * m + i]));
+  }
+  for (int o = 16; o; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+    lmin = fmin(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
+  }
+  __shared__ double red2[8];
+  if (lane == 0) {
+    red[0][w] = mx;
+    red[1][w] = dmax;
+    red[2][w] = dmin;
+    red2[w] = lmin;
+  }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double amax = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) amax = fmax(amax, red[w]);
-    bool bad = cinfo[b] != 0;
-    double dmin = INFINITY, dmax = 0.0;
-    for (int64_t i = 0; i < m && !bad; ++i) {
-      const double d = fabs(r1[b * m * m + i * m + i]);
-      dmin = fmin(dmin, d);
-      dmax = fmax(dmax, d);
-      if (!(fabs(l[b * m * m + i * m + i]) >= Num<double>::rank_rtol * amax)) bad = true;
+  if (t == 0) {
+    double amax = 0.0, dx = 0.0, dn = INFINITY, ln = INFINITY;
+    for (int k = 0; k < 8; ++k) {
+      amax = fmax(amax, red[0][k]);
+      dx = fmax(dx, red[1][k]);
+      dn = fmin(dn, red[2][k]);
+      ln = fmin(ln, red2[k]);
     }
-    if (!bad && !(dmax <= KAPPA_MAX * dmin)) bad = true;
+    // NaN-safe: a breakdown anywhere leaves a NaN / non-positive pivot
+    const bool bad = cinfo[b] != 0 || !(ln >= Num<double>::rank_rtol * amax) || !(dx <= KAPPA_MAX * dn);
     fb[b] = bad ? 1 : 0;
     hinfo[b] = bad ? 0 : 1;
   }

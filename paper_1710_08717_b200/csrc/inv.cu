@@ -173,6 +173,13 @@ dla_status trsm_inv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<cons
   DLAB_TRY(trtri_levels<T>(c, batch, nt, w, tmp));
   const bool eff = (lower != trans);  // op(T)^{-1} = eff ? W : W^T
   const int tri = eff ? TRI_LOWER : TRI_UPPER;
+  if (sizeof(T) == 8 && !right && m <= 128) {
+    // X <- op(T)^{-1} X in place: one 128-row tile per column block reads all
+    // of its X columns (the K range) before writing them (as trmm_gemm)
+    Ctx cr = c;
+    cr.gemm_rowtile = 1;
+    return gemm<T>(cr, batch, m, n, m, alpha, C_(w), !eff, C_(x), false, T(0), x, MASK_FULL, c.info, tri, TRI_NONE);
+  }
   if (!right)
     DLAB_TRY(gemm<T>(c, batch, m, n, m, alpha, C_(w), !eff, C_(x), false, T(0), y, MASK_FULL, c.info, tri, TRI_NONE));
   else
