@@ -370,7 +370,7 @@ dla_status trsm_bwd(const Ctx& cx, int64_t batch, int64_t m, int64_t n, T* abar,
 // ------------------------------------------------------------ potrf / potri
 template <typename T>
 size_t ws_potrf_fwd(int64_t batch, int64_t n) {
-  return potrf_small_eligible<T>(n) ? 0 : ws_potrf_lower<T>(batch, n);
+  return potrf_small_eligible<T>(n) ? 0 : ws_check_symmetric(batch) + ws_potrf_lower<T>(batch, n);
 }
 
 template <typename T>
@@ -662,7 +662,8 @@ size_t ws_potrf_split(int64_t batch, int64_t n) {
   if (batch * n == 0) return 0;
   if (!inv_eligible<T>(n)) return std::max(ws_potrf_fwd<T>(batch, n), ws_potrf_bwd<T>(batch, n));
   const int64_t h = n / 2;
-  const size_t gp = ws_potrf_lower<T>(batch, n) + ws_trtri_levels<T>(batch, h) * 2 + 2 * ws_gemm<T>(batch, h, h, h);
+  const size_t gp = ws_check_symmetric(batch) + ws_potrf_lower<T>(batch, n) + ws_trtri_levels<T>(batch, h) * 2 +
+                    2 * ws_gemm<T>(batch, h, h, h);
   const size_t begin = ws_potrf_inv_prepare<T>(batch, n);
   const size_t end = ws_potrf_bwd_tail<T>(batch, n);
   return carve_bound(potrf_inv_ws<T>(batch, n)) + std::max(gp, std::max(begin, end));

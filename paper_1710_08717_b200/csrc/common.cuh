@@ -308,6 +308,8 @@ template <typename T>
 dla_status ew_scale_diag(const Ctx& c, int64_t batch, int64_t n, MatB<T> x, T alpha);
 template <typename T>
 dla_status check_symmetric(const Ctx& c, int64_t batch, int64_t n, MatB<const T> a, int32_t* info);
+// its (max |a_ij - a_ji|, max |a_ij|) reduction slots, carved from the workspace
+inline size_t ws_check_symmetric(int64_t batch) { return carve_bound(2 * sizeof(unsigned long long) * (size_t)batch); }
 template <typename T>
 dla_status check_zero_diag(const Ctx& c, int64_t batch, int64_t n, MatB<const T> t, int32_t* info);
 template <typename T>

@@ -140,9 +140,12 @@ __global__ void k_square(int64_t batch, int64_t n, MatB<T> x, int op, T alpha, c
 // thread with 16-byte loads / stores.
 template <typename T>
 __global__ void k_tri_copy_vec(int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst) {
+  // block (tx, ty): ty rows at a time, tx lanes over a row's column pairs
+  // (a 128-wide row is 64 pairs: four rows per 256-thread block, no idle lanes)
   using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
   const int64_t pairs = (n + 1) / 2;
-  for (int64_t row = blockIdx.y; row < batch * n; row += gridDim.y) {
+  for (int64_t row = blockIdx.y * (int64_t)blockDim.y + threadIdx.y; row < batch * n;
+       row += (int64_t)gridDim.y * blockDim.y) {
     const int64_t b = row / n, i = row - b * n;
     const T* sr = src.at(b, i, 0);
     T* dr = dst.at(b, i, 0);
@@ -403,7 +406,8 @@ dla_status ew_scale(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<T> x
 // upper (lower) part, two columns per thread with 16-byte stores.
 template <typename T, bool UPPER>
 __global__ void k_zero_tri(int64_t batch, int64_t n, MatB<T> x, const int32_t* skip, bool vec) {
-  for (int64_t row = blockIdx.y; row < batch * n; row += gridDim.y) {
+  for (int64_t row = blockIdx.y * (int64_t)blockDim.y + threadIdx.y; row < batch * n;
+       row += (int64_t)gridDim.y * blockDim.y) {
     const int64_t b = row / n, i = row - b * n;
     if (slice_failed(skip, b)) continue;
     const int64_t j0 = UPPER ? i + 1 : 0, j1 = UPPER ? n : i;  // zero columns [j0, j1)
@@ -425,18 +429,30 @@ __global__ void k_zero_tri(int64_t batch, int64_t n, MatB<T> x, const int32_t* s
   }
 }
 
+// Launch shape of the row-pair kernels: 256-thread blocks of (tx lanes over a
+// row's column pairs) x (ty rows), 16 resident blocks per SM's worth of grid.
+inline void row_pair_grid(int64_t batch, int64_t n, dim3& grid, dim3& block) {
+  const int64_t pairs = std::max<int64_t>(1, (n + 1) / 2);
+  const int tx = (int)std::min<int64_t>(256, (pairs + 31) / 32 * 32);
+  const int ty = 256 / tx;
+  const int64_t gx = (pairs + tx - 1) / tx;
+  int64_t gy = std::max<int64_t>(1, (148 * 16) / gx);
+  gy = std::min<int64_t>(std::min<int64_t>(gy, (batch * n + ty - 1) / ty), 65535);
+  grid = dim3((unsigned)gx, (unsigned)gy);
+  block = dim3((unsigned)tx, (unsigned)ty);
+}
+
 template <typename T>
 dla_status ew_square(const Ctx& c, int64_t batch, int64_t n, MatB<T> x, int op, T alpha, const int32_t* skip) {
   if (batch * n == 0) return DLA_OK;
   if (op == 0 || op == 1) {
     const bool vec = (x.ld % 2 == 0) && (x.bs % 2 == 0) && (reinterpret_cast<uintptr_t>(x.p) % (2 * sizeof(T)) == 0);
-    const int64_t gx = std::max<int64_t>(1, (n / 2 + 255) / 256);
-    int64_t gy = std::max<int64_t>(1, (148 * 16) / gx);
-    gy = std::min<int64_t>(std::min<int64_t>(gy, batch * n), 65535);
+    dim3 grid, block;
+    row_pair_grid(batch, n, grid, block);
     if (op == 0)
-      k_zero_tri<T, true><<<dim3((unsigned)gx, (unsigned)gy), 256, 0, c.stream>>>(batch, n, x, skip, vec);
+      k_zero_tri<T, true><<<grid, block, 0, c.stream>>>(batch, n, x, skip, vec);
     else
-      k_zero_tri<T, false><<<dim3((unsigned)gx, (unsigned)gy), 256, 0, c.stream>>>(batch, n, x, skip, vec);
+      k_zero_tri<T, false><<<grid, block, 0, c.stream>>>(batch, n, x, skip, vec);
     DLAB_LAUNCH_CHECK();
     return DLA_OK;
   }
@@ -452,10 +468,9 @@ dla_status ew_tri_copy(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src
                    reinterpret_cast<uintptr_t>(src.p) % (2 * sizeof(T)) == 0 &&
                    reinterpret_cast<uintptr_t>(dst.p) % (2 * sizeof(T)) == 0;
   if (vec) {
-    const int64_t gx = std::max<int64_t>(1, (n / 2 + 255) / 256);
-    int64_t gy = std::max<int64_t>(1, (148 * 16) / gx);
-    gy = std::min<int64_t>(std::min<int64_t>(gy, batch * n), 65535);
-    k_tri_copy_vec<T><<<dim3((unsigned)gx, (unsigned)gy), 256, 0, c.stream>>>(batch, n, src, dst);
+    dim3 grid, block;
+    row_pair_grid(batch, n, grid, block);
+    k_tri_copy_vec<T><<<grid, block, 0, c.stream>>>(batch, n, src, dst);
     DLAB_LAUNCH_CHECK();
     return DLA_OK;
   }
@@ -493,13 +508,12 @@ dla_status ew_sym_lower_into(const Ctx& c, int64_t batch, int64_t n, MatB<const 
 template <typename T>
 dla_status check_symmetric(const Ctx& c, int64_t batch, int64_t n, MatB<const T> a, int32_t* info) {
   if (info == nullptr || batch * n == 0) return DLA_OK;
-  unsigned long long* red = nullptr;
-  if (cudaMallocAsync(&red, sizeof(unsigned long long) * 2 * batch, c.stream) != cudaSuccess) return DLA_ERR_CUDA;
-  cudaMemsetAsync(red, 0, sizeof(unsigned long long) * 2 * batch, c.stream);
+  DLAB_SCRATCH(red_s, c, ws_check_symmetric(batch));  // from the caller's workspace (no hidden allocation)
+  unsigned long long* red = red_s.as<unsigned long long>();
+  if (cudaMemsetAsync(red, 0, sizeof(unsigned long long) * 2 * batch, c.stream) != cudaSuccess) return DLA_ERR_CUDA;
   const int64_t nt = (n + 31) / 32;
   k_symcheck_reduce<T><<<(unsigned)(batch * (nt * (nt + 1) / 2)), 256, 0, c.stream>>>(batch, n, a, red);
   k_symcheck_decide<T><<<blocks_for(batch, 256), 256, 0, c.stream>>>(batch, red, info);
-  cudaFreeAsync(red, c.stream);
   note_launch(1);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;

@@ -68,6 +68,98 @@ __global__ void __launch_bounds__(128) k_trtri_blocks(int64_t nblk, MatB<T> w) {
   }
 }
 
+// fp64: the same inverse by level doubling inside shared memory.  The eight
+// 8x8 diagonal blocks are inverted by 64 threads (one column each, a serial
+// chain of 8), then for s = 8, 16, 32 every pair [A 0; B C] of the level is
+// finished with two triangular DMMA products, B <- -C^{-1} (B A^{-1}) — the
+// in-smem analogue of trtri_levels' launches.  ~86k MACs per block on DMMA
+// instead of 64 substitution phases: the kernel is bound by its HBM pass.
+constexpr int TLD8 = 33;  // T1 scratch row stride (32 x 32 at most)
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(128) k_trtri64_dmma(int64_t nblk, MatB<double> w) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* S = reinterpret_cast<double*>(smem_raw);  // [64][ILD]
+  double* Tt = S + IB * ILD;                         // [32][TLD8]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, fr = lane >> 2, fc = lane & 3;
+  const int64_t b = blockIdx.x / nblk, k = blockIdx.x % nblk;
+  double* base = w.p + b * w.bs + k * IB * (w.ld + 1);
+  {
+    double v[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int e = tid + u * 128, i = e >> 6, j = e & 63;
+      v[u] = j <= i ? base[i * w.ld + j] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int e = tid + u * 128, i = e >> 6, j = e & 63;
+      S[i * ILD + j] = v[u];
+    }
+  }
+  __syncthreads();
+  // 8x8 diagonal blocks: thread (d, c) solves L_d x = e_c
+  {
+    const int o = ((tid >> 3) & 7) * 8, c = tid & 7;
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      double acc = i == c ? 1.0 : 0.0;
+#pragma unroll
+      for (int q = 0; q < i; ++q)
+        if (q >= c) acc -= S[(o + i) * ILD + o + q] * x[q];
+      x[i] = i >= c ? acc / S[(o + i) * ILD + o + i] : 0.0;
+    }
+    __syncthreads();
+    if (tid < 64) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i >= c) S[(o + i) * ILD + o + c] = x[i];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 8; s < IB; s *= 2) {
+    const int pairs = IB / (2 * s), tps = (s / 8) * (s / 8), tiles = pairs * tps;
+    // T1 = B A^{-1}: tile (rt, nt) of pair p, k >= nt (A^{-1} lower)
+    for (int t = warp; t < tiles; t += 4) {
+      const int p = t / tps, r = t % tps, rt = (r / (s / 8)) * 8, nt = (r % (s / 8)) * 8, o = 2 * s * p;
+      double d0 = 0.0, d1 = 0.0;
+      for (int kk = nt; kk < s; kk += 4) {
+        const double af = S[(o + s + rt + fr) * ILD + o + kk + fc];
+        const double bf = S[(o + kk + fc) * ILD + o + nt + fr];
+        dmma884(d0, d1, af, bf);
+      }
+      Tt[(p * s + rt + fr) * TLD8 + nt + 2 * fc] = d0;
+      Tt[(p * s + rt + fr) * TLD8 + nt + 2 * fc + 1] = d1;
+    }
+    __syncthreads();
+    // B = -C^{-1} T1: k <= rt + 7 (C^{-1} lower)
+    for (int t = warp; t < tiles; t += 4) {
+      const int p = t / tps, r = t % tps, rt = (r / (s / 8)) * 8, nt = (r % (s / 8)) * 8, o = 2 * s * p;
+      double d0 = 0.0, d1 = 0.0;
+      for (int kk = 0; kk < rt + 8; kk += 4) {
+        const double af = S[(o + s + rt + fr) * ILD + o + s + kk + fc];
+        const double bf = Tt[(p * s + kk + fc) * TLD8 + nt + fr];
+        dmma884(d0, d1, af, bf);
+      }
+      S[(o + s + rt + fr) * ILD + o + nt + 2 * fc] = -d0;
+      S[(o + s + rt + fr) * ILD + o + nt + 2 * fc + 1] = -d1;
+    }
+    __syncthreads();
+  }
+#pragma unroll 8
+  for (int u = 0; u < 32; ++u) {
+    const int e = tid + u * 128, i = e >> 6, j = e & 63;
+    base[i * w.ld + j] = j <= i ? S[i * ILD + j] : 0.0;
+  }
+}
+
 }  // namespace
 
 template <typename T>
@@ -139,9 +231,16 @@ size_t ws_potri_inv(int64_t batch, int64_t n) {
 template <typename T>
 dla_status trtri_levels(const Ctx& c, int64_t batch, int64_t n, MatB<T> w, T* tmp) {
   const int64_t nblk = n / IB;
-  const size_t sm = sizeof(T) * (2 * IB * ILD + IB);
-  ensure_smem_attr(k_trtri_blocks<T>, sm);
-  k_trtri_blocks<T><<<(unsigned)(batch * nblk), 128, sm, c.stream>>>(nblk, w);
+  if constexpr (sizeof(T) == 8) {
+    const size_t sm = sizeof(double) * (IB * ILD + 32 * TLD8);
+    ensure_smem_attr(k_trtri64_dmma, sm);
+    MatB<double> wd{reinterpret_cast<double*>(w.p), w.ld, w.bs, w.bsi};
+    k_trtri64_dmma<<<(unsigned)(batch * nblk), 128, sm, c.stream>>>(nblk, wd);
+  } else {
+    const size_t sm = sizeof(T) * (2 * IB * ILD + IB);
+    ensure_smem_attr(k_trtri_blocks<T>, sm);
+    k_trtri_blocks<T><<<(unsigned)(batch * nblk), 128, sm, c.stream>>>(nblk, w);
+  }
   DLAB_LAUNCH_CHECK();
   for (int64_t s = IB; s < n; s *= 2) {
     const int64_t pairs = n / (2 * s);
