@@ -370,7 +370,7 @@ dla_status trsm_bwd(const Ctx& cx, int64_t batch, int64_t m, int64_t n, T* abar,
 // ------------------------------------------------------------ potrf / potri
 template <typename T>
 size_t ws_potrf_fwd(int64_t batch, int64_t n) {
-  return potrf_small_eligible<T>(n) ? 0 : ws_check_symmetric(batch) + ws_potrf_lower<T>(batch, n);
+  return potrf_fwd_small_eligible<T>(n) ? 0 : ws_check_symmetric(batch) + ws_potrf_lower<T>(batch, n);
 }
 
 template <typename T>
@@ -378,7 +378,7 @@ dla_status potrf_fwd(const Ctx& cx, int64_t batch, int64_t n, T* a, int lower) {
   if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
   DLAB_TRY(reset_info(cx, batch));
   if (batch * n == 0) return DLA_OK;
-  if (potrf_small_eligible<T>(n)) return potrf_small<T>(cx, batch, n, pk(a, n, n), lower);
+  if (potrf_fwd_small_eligible<T>(n)) return potrf_small<T>(cx, batch, n, pk(a, n, n), lower);
   DLAB_TRY(check_symmetric<T>(cx, batch, n, cpk(a, n, n), cx.info));
   DLAB_TRY(potrf_lower<T>(cx, batch, n, pk(a, n, n)));
   if (!lower) DLAB_TRY(ew_square<T>(cx, batch, n, pk(a, n, n), /*transpose*/ 5, T(1), cx.info));

@@ -144,9 +144,14 @@ __global__ void k_tri_copy_vec(int64_t batch, int64_t n, MatB<const T> src, MatB
   // (a 128-wide row is 64 pairs: four rows per 256-thread block, no idle lanes)
   using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
   const int64_t pairs = (n + 1) / 2;
-  for (int64_t row = blockIdx.y * (int64_t)blockDim.y + threadIdx.y; row < batch * n;
-       row += (int64_t)gridDim.y * blockDim.y) {
-    const int64_t b = row / n, i = row - b * n;
+  const int64_t r0 = blockIdx.y * (int64_t)blockDim.y + threadIdx.y, rs = (int64_t)gridDim.y * blockDim.y;
+  const int64_t db = rs / n, di = rs - db * n;  // (slice, row) advance incrementally: no division per row
+  int64_t b = r0 / n, i = r0 - b * n;
+  for (int64_t row = r0; row < batch * n; row += rs, b += db, i += di) {
+    if (i >= n) {
+      i -= n;
+      ++b;
+    }
     const T* sr = src.at(b, i, 0);
     T* dr = dst.at(b, i, 0);
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < pairs; p += (int64_t)gridDim.x * blockDim.x) {
@@ -176,18 +181,27 @@ __global__ void k_tri_copy(int64_t batch, int64_t n, MatB<const T> src, MatB<T> 
   DLAB_ROWS_END
 }
 
+// Lower-triangle tile pair p -> (I, J), I >= J (p = I (I + 1) / 2 + J).
+__device__ __forceinline__ void tile_pair(int64_t p, int64_t& I, int64_t& J) {
+  I = (int64_t)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5);
+  while (I * (I + 1) / 2 > p) --I;
+  while ((I + 1) * (I + 2) / 2 <= p) ++I;
+  J = p - I * (I + 1) / 2;
+}
+
 // dst = alpha (src + src^T) by 32 x 32 tile PAIRS: the block of tile (I, J),
 // I >= J, reads tiles (I, J) and (J, I) with coalesced rows, writes both
 // (in-place safe: no other block touches them).  IEEE addition commutes, so
-// the two mirrored sums are the same bits: bit-symmetric output.
+// the two mirrored sums are the same bits: bit-symmetric output.  grid.x
+// enumerates only the T (T + 1) / 2 lower pairs; grid.y strides the batch.
 template <typename T>
 __global__ void __launch_bounds__(256) k_add_transpose(int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst,
                                                        T alpha) {
   __shared__ T ta[32][33], tb[32][33];
-  const int64_t I = blockIdx.x, J = blockIdx.y;
-  if (J > I) return;
+  int64_t I, J;
+  tile_pair(blockIdx.x, I, J);
   const int tx = threadIdx.x, ty = threadIdx.y;
-  for (int64_t b = blockIdx.z; b < batch; b += gridDim.z) {
+  for (int64_t b = blockIdx.y; b < batch; b += gridDim.y) {
 #pragma unroll
     for (int r = ty; r < 32; r += 8) {
       const int64_t i = I * 32 + r, j = J * 32 + tx, i2 = J * 32 + r, j2 = I * 32 + tx;
@@ -205,19 +219,46 @@ __global__ void __launch_bounds__(256) k_add_transpose(int64_t batch, int64_t n,
   }
 }
 
+// dst(i, j) = dst(j, i) = alpha src(max(i, j), min(i, j)): tile pairs again,
+// only the lower tiles of src are read.
+template <typename T>
+__global__ void __launch_bounds__(256) k_sym_lower_tiles(int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst,
+                                                         T alpha) {
+  __shared__ T ta[32][33];
+  int64_t I, J;
+  tile_pair(blockIdx.x, I, J);
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int64_t b = blockIdx.y; b < batch; b += gridDim.y) {
+#pragma unroll
+    for (int r = ty; r < 32; r += 8) {
+      const int64_t i = I * 32 + r, j = J * 32 + tx;
+      ta[r][tx] = (i < n && j < n && (I != J || tx <= r)) ? *src.at(b, i, j) : T(0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = ty; r < 32; r += 8) {
+      const int64_t i = I * 32 + r, j = J * 32 + tx, i2 = J * 32 + r, j2 = I * 32 + tx;
+      if (I != J) {
+        if (i < n && j < n) *dst.at(b, i, j) = alpha * ta[r][tx];
+        if (i2 < n && j2 < n) *dst.at(b, i2, j2) = alpha * ta[tx][r];
+      } else if (i < n && j < n) {
+        *dst.at(b, i, j) = alpha * (tx <= r ? ta[r][tx] : ta[tx][r]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+inline dim3 pair_grid(int64_t batch, int64_t n) {
+  const int64_t t = (n + 31) / 32, pairs = t * (t + 1) / 2;
+  const int64_t gy = std::min<int64_t>(std::max<int64_t>(1, batch), std::max<int64_t>(1, (148 * 8) / pairs));
+  return dim3((unsigned)pairs, (unsigned)std::min<int64_t>(gy, 65535));
+}
+
 template <typename T>
 __global__ void k_scale_diag(int64_t batch, int64_t n, MatB<T> x, T alpha) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < batch * n; t += (int64_t)gridDim.x * blockDim.x)
     *x.at(t / n, t % n, t % n) *= alpha;
-}
-
-template <typename T>
-__global__ void k_sym_lower_into(int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, T alpha) {
-  const int64_t total = batch * n * n;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = t / (n * n), r = t % (n * n), i = r / n, j = r % n;
-    *dst.at(b, i, j) = alpha * *src.at(b, i > j ? i : j, i > j ? j : i);
-  }
 }
 
 // Symmetry precheck, pass 1: per-slice max|a| and max|a_ij - a_ji| as
@@ -406,9 +447,14 @@ dla_status ew_scale(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<T> x
 // upper (lower) part, two columns per thread with 16-byte stores.
 template <typename T, bool UPPER>
 __global__ void k_zero_tri(int64_t batch, int64_t n, MatB<T> x, const int32_t* skip, bool vec) {
-  for (int64_t row = blockIdx.y * (int64_t)blockDim.y + threadIdx.y; row < batch * n;
-       row += (int64_t)gridDim.y * blockDim.y) {
-    const int64_t b = row / n, i = row - b * n;
+  const int64_t r0 = blockIdx.y * (int64_t)blockDim.y + threadIdx.y, rs = (int64_t)gridDim.y * blockDim.y;
+  const int64_t db = rs / n, di = rs - db * n;  // (slice, row) advance incrementally: no division per row
+  int64_t b = r0 / n, i = r0 - b * n;
+  for (int64_t row = r0; row < batch * n; row += rs, b += db, i += di) {
+    if (i >= n) {
+      i -= n;
+      ++b;
+    }
     if (slice_failed(skip, b)) continue;
     const int64_t j0 = UPPER ? i + 1 : 0, j1 = UPPER ? n : i;  // zero columns [j0, j1)
     if (j0 >= j1) continue;
@@ -482,9 +528,7 @@ dla_status ew_tri_copy(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src
 template <typename T>
 dla_status ew_add_transpose(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, T alpha) {
   if (batch * n == 0) return DLA_OK;
-  const unsigned tiles = (unsigned)((n + 31) / 32);
-  k_add_transpose<T><<<dim3(tiles, tiles, (unsigned)std::min<int64_t>(batch, 65535)), dim3(32, 8), 0, c.stream>>>(
-      batch, n, src, dst, alpha);
+  k_add_transpose<T><<<pair_grid(batch, n), dim3(32, 8), 0, c.stream>>>(batch, n, src, dst, alpha);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }
@@ -500,7 +544,9 @@ dla_status ew_scale_diag(const Ctx& c, int64_t batch, int64_t n, MatB<T> x, T al
 template <typename T>
 dla_status ew_sym_lower_into(const Ctx& c, int64_t batch, int64_t n, MatB<const T> src, MatB<T> dst, T alpha) {
   if (batch * n == 0) return DLA_OK;
-  k_sym_lower_into<T><<<blocks_for(batch * n * n, 256), 256, 0, c.stream>>>(batch, n, src, dst, alpha);
+  // in-place safe: a block reads only its own lower tile (I, J) before it
+  // writes (I, J) and the upper tile (J, I), which no block reads
+  k_sym_lower_tiles<T><<<pair_grid(batch, n), dim3(32, 8), 0, c.stream>>>(batch, n, src, dst, alpha);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }

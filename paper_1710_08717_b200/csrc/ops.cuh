@@ -9,6 +9,8 @@ namespace dlab {
 template <typename T>
 bool potrf_small_eligible(int64_t n);
 template <typename T>
+bool potrf_fwd_small_eligible(int64_t n);
+template <typename T>
 dla_status potrf_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool lower);
 template <typename T>
 dla_status potrf_bwd_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> lbar,

@@ -217,6 +217,164 @@ __global__ void __launch_bounds__(256) k_outer_tri(SkinnyArgs<T> g, int64_t batc
   }
 }
 
+// ---- single-vector fast paths (n == 1, 16-byte aligned, contiguous vector):
+// the GP / marginal-likelihood chains' v = G y, G^T v and v y^T at batch x
+// 128 shapes.  Every thread keeps several 16-byte loads or stores in flight
+// and walks (slice, row) with incremental counters (no per-element 64-bit
+// division): these shapes are HBM streams, not tiles.
+//
+// y = alpha A x (+ beta y): a warp per 4 rows, lanes over double2 columns.
+template <typename T>
+__global__ void __launch_bounds__(256) k_matvec_rows(int64_t batch, int64_t m, int64_t k, T alpha, T beta,
+                                                     MatB<const T> a, MatB<const T> x, MatB<T> y,
+                                                     const int32_t* skip) {
+  using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+  constexpr int R = 4;
+  const int lane = threadIdx.x & 31;
+  const int64_t groups_per = (m + R - 1) / R, total = batch * groups_per;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t b = w0 / groups_per, gi = w0 - b * groups_per;
+  const int64_t db = ws / groups_per, dg = ws - db * groups_per;
+  for (int64_t t = w0; t < total; t += ws) {
+    if (!slice_failed(skip, b)) {
+      const T* A = a.p + b * a.bs + gi * R * a.ld;
+      const T* X = x.p + b * x.bs;
+      T acc[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = T(0);
+      for (int64_t c = 2 * lane; c < k; c += 64) {
+        const V2 xv = *reinterpret_cast<const V2*>(X + c);
+        V2 av[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (gi * R + r < m) av[r] = *reinterpret_cast<const V2*>(A + r * a.ld + c);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (gi * R + r < m) acc[r] += av[r].x * xv.x + av[r].y * xv.y;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+      }
+      if (lane < R && gi * R + lane < m) {
+        T v = acc[0];
+#pragma unroll
+        for (int r = 1; r < R; ++r)
+          if (lane == r) v = acc[r];
+        T* py = y.p + b * y.bs + (gi * R + lane) * y.ld;
+        T o = alpha * v;
+        if (beta != T(0)) o += beta * *py;
+        *py = o;
+      }
+    }
+    gi += dg;
+    b += db;
+    if (gi >= groups_per) {
+      gi -= groups_per;
+      ++b;
+    }
+  }
+}
+
+// y = alpha A^T x (+ beta y), m = columns of A (<= 256 per CTA): a CTA per
+// (slice, 256-column block), 64 column-pair lanes x 4 k-groups, shared-memory
+// reduction across the k-groups.
+template <typename T>
+__global__ void __launch_bounds__(256) k_matvec_cols(int64_t batch, int64_t m, int64_t k, T alpha, T beta,
+                                                     MatB<const T> a, MatB<const T> x, MatB<T> y,
+                                                     const int32_t* skip, int64_t cblocks) {
+  using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+  __shared__ T red[4][2 * 64 * 2];
+  const int64_t b = blockIdx.x / cblocks, cb = blockIdx.x % cblocks;
+  if (slice_failed(skip, b)) return;
+  const int cp = threadIdx.x & 63, kg = threadIdx.x >> 6;
+  const T* A = a.p + b * a.bs;
+  const T* X = x.p + b * x.bs;
+  T acc[2][2] = {{T(0), T(0)}, {T(0), T(0)}};  // two column pairs per lane: cols c0, c0 + 128
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t c0 = cb * 256 + h * 128 + 2 * cp;
+    if (c0 < m) {
+#pragma unroll 8
+      for (int64_t r = kg; r < k; r += 4) {
+        const V2 av = *reinterpret_cast<const V2*>(A + r * a.ld + c0);
+        const T xv = X[r * x.ld];
+        acc[h][0] += av.x * xv;
+        acc[h][1] += av.y * xv;
+      }
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    red[kg][h * 128 + 2 * cp] = acc[h][0];
+    red[kg][h * 128 + 2 * cp + 1] = acc[h][1];
+  }
+  __syncthreads();
+  const int64_t col = cb * 256 + threadIdx.x;
+  if (col < m) {
+    const T v = ((red[0][threadIdx.x] + red[1][threadIdx.x]) + red[2][threadIdx.x]) + red[3][threadIdx.x];
+    T* py = y.p + b * y.bs + col * y.ld;
+    T o = alpha * v;
+    if (beta != T(0)) o += beta * *py;
+    *py = o;
+  }
+}
+
+// C(i, j) = alpha a_i b_j (+ beta C), rank-1 outer product into a row-major C
+// with even columns; mask: entries outside are left untouched.  Thread per
+// column pair, rows walked with incremental counters.
+template <typename T>
+__global__ void __launch_bounds__(256) k_outer1(int64_t batch, int64_t m, int64_t n, T alpha, T beta,
+                                                MatB<const T> a, int64_t sa, MatB<const T> bv, int64_t sb,
+                                                MatB<T> c, int mask, const int32_t* skip) {
+  using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+  const int64_t pairs = n / 2, rows = batch * m;
+  const int64_t ty = blockDim.x / 64 > 0 ? blockDim.x / 64 : 1;
+  const int p = threadIdx.x % 64;
+  const int64_t r0 = blockIdx.x * ty + threadIdx.x / 64, rs = (int64_t)gridDim.x * ty;
+  int64_t b = r0 / m, i = r0 - b * m;
+  const int64_t db = rs / m, di = rs - db * m;
+  for (int64_t r = r0; r < rows; r += rs) {
+    if (!slice_failed(skip, b)) {
+      const T ai = a.p[b * a.bs + i * sa];
+      const T* B = bv.p + b * bv.bs;
+      T* C = c.p + b * c.bs + i * c.ld;
+      for (int64_t q = p; q < pairs; q += 64) {
+        const int64_t j = 2 * q;
+        V2 o;  // alpha (a_i b_j): gemm()'s rounding order
+        o.x = alpha * (ai * B[j * sb]);
+        o.y = alpha * (ai * B[(j + 1) * sb]);
+        const bool in0 = mask == MASK_LOWER ? j <= i : (mask == MASK_UPPER ? j >= i : true);
+        const bool in1 = mask == MASK_LOWER ? j + 1 <= i : (mask == MASK_UPPER ? j + 1 >= i : true);
+        if (in0 && in1) {
+          if (beta != T(0)) {
+            const V2 old = *reinterpret_cast<const V2*>(C + j);
+            o.x += beta * old.x;
+            o.y += beta * old.y;
+          }
+          *reinterpret_cast<V2*>(C + j) = o;
+        } else {
+          if (in0) C[j] = beta != T(0) ? o.x + beta * C[j] : o.x;
+          if (in1) C[j + 1] = beta != T(0) ? o.y + beta * C[j + 1] : o.y;
+        }
+      }
+    }
+    i += di;
+    b += db;
+    if (i >= m) {
+      i -= m;
+      ++b;
+    }
+  }
+}
+
+template <typename T>
+bool aligned2(const T* p, int64_t ld, int64_t bs) {
+  return reinterpret_cast<uintptr_t>(p) % (2 * sizeof(T)) == 0 && ld % 2 == 0 && bs % 2 == 0;
+}
+
 }  // namespace
 
 // C (m x n, full) = alpha * mask(op(A) op(B)) with zeros outside the mask, k <= 8.
@@ -247,7 +405,13 @@ bool gemm_skinny(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T
                  MatB<const T> b, bool tb, T beta, MatB<T> cm, int mask, const int32_t* skip, dla_status* st) {
   SkinnyArgs<T> g{m, n, k, alpha, beta, a, b, cm, ta, tb, false, mask, skip};
   *st = DLA_OK;
-  if (k <= SK_NMAX) {
+  if (k == 1 && n >= 2 && n % 2 == 0 && aligned2<T>(cm.p, cm.ld, cm.bs)) {
+    // rank-1 outer product: column of op(A) times row of op(B)
+    const int64_t sa = ta ? 1 : a.ld;  // op(A)(i, 0)
+    const int64_t sb = tb ? b.ld : 1;  // op(B)(0, j)
+    const unsigned grid = blocks_for(batch * m, 4, 148 * 16);
+    k_outer1<T><<<grid, 256, 0, c.stream>>>(batch, m, n, alpha, beta, a, sa, b, sb, cm, mask, skip);
+  } else if (k <= SK_NMAX) {
     k_kskinny<T><<<blocks_for(batch * m, 1, 148 * 64), 128, 0, c.stream>>>(g, batch);
   } else if (mask != MASK_FULL) {
     return false;
@@ -261,7 +425,20 @@ bool gemm_skinny(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T
       g.tb = !ta;
       g.tc = true;
     }
-    if (!g.ta) {
+    // single vector, contiguous, 16-byte aligned rows: the streaming matvecs
+    const bool vec1 = g.n == 1 && !g.tc && g.k % 2 == 0 && aligned2<T>(g.a.p, g.a.ld, g.a.bs);
+    const bool xcontig = g.tb ? true : g.b.ld == 1;
+    if (vec1 && !g.ta && xcontig && reinterpret_cast<uintptr_t>(g.b.p) % (2 * sizeof(T)) == 0 &&
+        (batch == 1 || g.b.bs % 2 == 0)) {
+      const unsigned grid = blocks_for(batch * ((g.m + 3) / 4), 8, 148 * 8);
+      MatB<const T> xv{g.b.p, 1, g.b.bs};
+      k_matvec_rows<T><<<grid, 256, 0, c.stream>>>(batch, g.m, g.k, g.alpha, g.beta, g.a, xv, g.c, skip);
+    } else if (vec1 && g.ta && g.m % 2 == 0) {
+      const int64_t cbk = (g.m + 255) / 256;
+      MatB<const T> xv{g.b.p, g.tb ? 1 : g.b.ld, g.b.bs};
+      k_matvec_cols<T><<<(unsigned)(batch * cbk), 256, 0, c.stream>>>(batch, g.m, g.k, g.alpha, g.beta, g.a, xv,
+                                                                        g.c, skip, cbk);
+    } else if (!g.ta) {
       const int64_t rb = (g.m + 7) / 8;
       k_nskinny_rows<T><<<(unsigned)(batch * rb), 256, 0, c.stream>>>(g, rb);
     } else if (g.m >= 64) {

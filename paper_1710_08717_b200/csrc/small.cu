@@ -483,11 +483,126 @@ __global__ void __launch_bounds__(wpc_bwd<T>() * 32) k_chol_chain_warp(int n, in
   __syncthreads();
   warp_potrf_bwd_core<T>(n, lane, L, W, dg, rd, abar.at(b, 0, 0), (int)abar.ld, ok);
 }
+// ------------------------------------------- 64 < n <= 128 (fp64): CTA per matrix
+// The whole factorization of one matrix in ONE launch with its lower
+// triangle in shared memory as three 64 x 64 blocks (A11, A21, A22: 100 KB,
+// two CTAs per SM): symmetry precheck from the same read, A11 factored with
+// the A21 solve interleaved (chol_tall64, the blocked panel kernel's leaf),
+// A22 -= L21 L21^T on DMMA, A22 factored (chol_smem), L written once with its
+// zero triangle.  Replaces check_symmetric's pass, two panel launches and
+// the zeroing pass of the blocked path at these sizes.
+constexpr int P2 = 128;
+constexpr int P2LD = 65;
+__device__ __forceinline__ int kcol16(int s, int fc) { return ((s & ~3) << 2) + 4 * fc + (s & 3); }
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_potrf128(int n, MatB<double> a, bool lower, int32_t* info) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* S11 = reinterpret_cast<double*>(smem_raw);
+  double* V = S11 + 64 * P2LD;
+  double* S22 = V + 64 * P2LD;
+  __shared__ double red[8];
+  __shared__ int flag;
+  const int64_t b = blockIdx.x;
+  const int tid = threadIdx.x, nv = n - 64;
+  double* g = a.at(b, 0, 0);
+  const int64_t ld = a.ld;
+  auto sm = [&](int i, int j) -> double* {
+    return i < 64 ? S11 + i * P2LD + j : (j < 64 ? V + (i - 64) * P2LD + j : S22 + (i - 64) * P2LD + (j - 64));
+  };
+  // One read of A, bottom row pairs first, 16 loads in flight per thread:
+  // the lower triangle goes to shared memory and each chunk's upper entries
+  // are checked against their mirrors, which sit in rows already stored (the
+  // symmetry precheck of dl/cholesky.hpp:19-25, as k_potrf_small).
+  double mabs = 0.0, masym = 0.0;
+  const int j = tid & 127;
+  for (int c = P2 * P2 / 256 / 16 - 1; c >= 0; --c) {
+    double v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int i = 2 * (16 * c + q) + (tid >> 7);
+      v[q] = (i < n && j < n) ? g[i * ld + j] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int i = 2 * (16 * c + q) + (tid >> 7);
+      if (j <= i) *sm(i, j) = v[q];
+      if (fabs(v[q]) > mabs) mabs = fabs(v[q]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int i = 2 * (16 * c + q) + (tid >> 7);
+      if (j > i && j < n) {
+        const double d = fabs(v[q] - *sm(j, i));
+        if (d > masym) masym = d;
+      }
+    }
+  }
+  mabs = block_max(mabs, red);
+  masym = block_max(masym, red);
+  if (masym > Num<double>::sym_rtol * (mabs > 0.0 ? mabs : 1.0)) {
+    if (tid == 0) record_failure(info, b, DLA_ERR_ASYMMETRIC, 0);
+    return;
+  }
+  // L11 and L21
+  int failed = chol_tall64<P2LD>(S11, V, 64, nv, &flag, [](int) {});
+  if (failed >= 0) {
+    if (tid == 0) record_failure(info, b, DLA_ERR_NOT_SPD, failed);
+    return;
+  }
+  // A22 -= L21 L21^T (lower 8 x 8 tiles, K = 64 on DMMA)
+  {
+    const int warp = tid >> 5, lane = tid & 31, fr = lane >> 2, fc = lane & 3;
+    const int mt = (nv + 7) / 8, ntiles = mt * (mt + 1) / 2;
+    for (int tile = warp; tile < ntiles; tile += 8) {
+      int ta = 0;
+      while ((ta + 1) * (ta + 2) / 2 <= tile) ++ta;
+      const int tb = tile - ta * (ta + 1) / 2;
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int kc = kcol16(q, fc);
+        const double af = V[(8 * ta + fr) * P2LD + kc];
+        const double bf = V[(8 * tb + fr) * P2LD + kc];
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c0), "+d"(c1)
+                     : "d"(af), "d"(bf));
+      }
+      double* crow = S22 + (8 * ta + fr) * P2LD + 8 * tb + 2 * fc;  // above-diagonal entries are scratch
+      crow[0] -= c0;
+      crow[1] -= c1;
+    }
+  }
+  __syncthreads();
+  failed = chol_smem<double, 64>(S22, nv, &flag);
+  if (failed >= 0) {
+    if (tid == 0) record_failure(info, b, DLA_ERR_NOT_SPD, 64 + failed);
+    return;
+  }
+  // L (or R = L^T) with its zero triangle, coalesced rows
+  if (j < n) {
+#pragma unroll 8
+    for (int u = 0; u < P2 * P2 / 256; ++u) {
+      const int i = 2 * u + (tid >> 7);
+      if (i < n) {
+        double v;
+        if (lower) v = j <= i ? *sm(i, j) : 0.0;
+        else v = i <= j ? *sm(j, i) : 0.0;
+        g[i * ld + j] = v;
+      }
+    }
+  }
+}
 }  // namespace
 
 template <typename T>
 bool potrf_small_eligible(int64_t n) {
   return n >= 1 && n <= SN;
+}
+// the forward alone also has the one-launch fp64 kernel up to n = 128
+template <typename T>
+bool potrf_fwd_small_eligible(int64_t n) {
+  return n >= 1 && (n <= SN || (sizeof(T) == 8 && n <= P2));
 }
 
 template <typename T>
@@ -507,6 +622,25 @@ dla_status potrf_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool l
     else
       k_potrf_warp<T, 2><<<grid, wpc * 32, sm, c.stream>>>((int)n, batch, a, lower, c.info);
     DLAB_LAUNCH_CHECK();
+    return DLA_OK;
+  }
+  if (n > SN) {
+    if constexpr (sizeof(T) == 8) {
+      const size_t sm = sizeof(double) * 3 * 64 * P2LD;
+      static const int minb = [] {
+        const char* e = getenv("DLA_P128_MINB");  // tuning switch: 1 = no register cap (one CTA per SM)
+        return e ? atoi(e) : 2;
+      }();
+      MatB<double> ad{reinterpret_cast<double*>(a.p), a.ld, a.bs, a.bsi};
+      if (minb == 1) {
+        ensure_smem_attr(k_potrf128<1>, sm);
+        k_potrf128<1><<<(unsigned)batch, 256, sm, c.stream>>>((int)n, ad, lower, c.info);
+      } else {
+        ensure_smem_attr(k_potrf128<2>, sm);
+        k_potrf128<2><<<(unsigned)batch, 256, sm, c.stream>>>((int)n, ad, lower, c.info);
+      }
+      DLAB_LAUNCH_CHECK();
+    }
     return DLA_OK;
   }
   k_potrf_small<T><<<(unsigned)batch, 256, 0, c.stream>>>((int)n, a, lower, c.info);
@@ -548,6 +682,7 @@ dla_status chol_chain_small(const Ctx& c, int64_t batch, int64_t n, MatB<const T
 
 #define INST(T)                                                                                     \
   template bool potrf_small_eligible<T>(int64_t);                                                   \
+  template bool potrf_fwd_small_eligible<T>(int64_t);                                               \
   template dla_status potrf_small<T>(const Ctx&, int64_t, int64_t, MatB<T>, bool);                  \
   template dla_status potrf_bwd_small<T>(const Ctx&, int64_t, int64_t, MatB<T>, MatB<const T>, MatB<const T>, bool); \
   template dla_status chol_chain_small<T>(const Ctx&, int64_t, int64_t, MatB<const T>, const T*, T*, MatB<T>, T*);

@@ -242,7 +242,7 @@ def test_trsm_singular_reports_index_and_leaves_slice():
 
 
 # ----------------------------------------------------------- potrf / potri
-POTRF_N = [1, 2, 5, 17, 32, 63, 64, 65, 70, 129, 200, 256, 512]  # 256/512: inverse-based DMMA paths
+POTRF_N = [1, 2, 5, 17, 32, 63, 64, 65, 70, 96, 128, 129, 200, 256, 512]  # 65-128 f64: one-launch kernel; 256/512: inverse-based DMMA paths
 
 
 def test_potrf_throughput_panel_path():
@@ -348,6 +348,24 @@ def test_potrf_errors():
         L.potrf_inplace(x)
     assert e.value.batch_index == 2 and e.value.step == 5
     np.testing.assert_allclose(host(x)[0], np.linalg.cholesky(ab[0]), rtol=1e-10, atol=1e-12)
+    # one-launch path (64 < n <= 128, f64): failures in A11, in A22, asymmetry, per slice
+    for n, k in ((100, 30), (100, 90), (128, 127), (65, 64)):
+        a = O.random_spd(n, r, batch=3)
+        a[1, k, k] = -1e6
+        x = dev(a)
+        with pytest.raises(L.NotPositiveDefiniteError) as e:
+            L.potrf_inplace(x)
+        assert e.value.batch_index == 1 and e.value.step == k
+        for b in (0, 2):
+            np.testing.assert_allclose(host(x)[b], np.linalg.cholesky(a[b]), rtol=1e-10, atol=1e-12)
+    asym = O.random_spd(128, r)
+    asym[3, 100] += 1.0
+    with pytest.raises(L.ShapeError):
+        L.potrf(dev(asym))
+    asym = O.random_spd(100, r)
+    asym[70, 90] += 1.0  # inside the A22 block
+    with pytest.raises(L.ShapeError):
+        L.potrf(dev(asym))
     # tile-dataflow path (n >= 256): failure deep inside one slice, the other factored
     a2 = O.random_spd(300, r, batch=2)
     a2[1, 200, 200] = -1e6
