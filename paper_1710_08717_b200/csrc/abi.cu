@@ -388,7 +388,7 @@ dla_status potrf_fwd(const Ctx& cx, int64_t batch, int64_t n, T* a, int lower) {
 template <typename T>
 size_t ws_potrf_bwd(int64_t batch, int64_t n) {
   if (batch * n == 0 || potrf_small_eligible<T>(n)) return 0;
-  if (inv_eligible<T>(n)) return ws_potrf_bwd_inv<T>(batch, n);
+  if (inv_pad<T>(n)) return ws_potrf_bwd_inv<T>(batch, n);
   return ws_trmm<T>(batch, n, n, false) + ws_trsm<T>(batch, n, n, false) + ws_trsm<T>(batch, n, n, true);
 }
 
@@ -400,7 +400,7 @@ dla_status potrf_bwd(const Ctx& cx, int64_t batch, int64_t n, T* abar, const T* 
   if (batch * n == 0) return DLA_OK;
   if (potrf_small_eligible<T>(n)) return potrf_bwd_small<T>(cx, batch, n, pk(abar, n, n), cpk(lbar, n, n),
                                                             cpk(l, n, n), lower);
-  if (inv_eligible<T>(n)) return potrf_bwd_inv<T>(cx, batch, n, pk(abar, n, n), cpk(lbar, n, n), cpk(l, n, n), lower);
+  if (inv_pad<T>(n)) return potrf_bwd_inv<T>(cx, batch, n, pk(abar, n, n), cpk(lbar, n, n), cpk(l, n, n), lower);
   MatB<T> ab = pk(abar, n, n);
   MatB<const T> lv = cpk(l, n, n);
   DLAB_TRY(ew_copy<T>(cx, batch, n, n, cpk(lbar, n, n), ab));

@@ -160,6 +160,19 @@ __global__ void __launch_bounds__(128) k_trtri64_dmma(int64_t nblk, MatB<double>
   }
 }
 
+// The padding of the inverse's operand (see inv_pad): rows < n get zeros in
+// columns [n, N), rows >= n the identity row.
+template <typename T>
+__global__ void k_pad_eye(int64_t batch, int64_t n, int64_t N, MatB<T> w) {
+  for (int64_t row = blockIdx.y; row < batch * N; row += gridDim.y) {
+    const int64_t b = row / N, i = row - b * N;
+    T* wr = w.p + b * w.bs + i * w.ld;
+    const int64_t j0 = i < n ? n : 0;
+    for (int64_t j = j0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x)
+      wr[j] = (i == j) ? T(1) : T(0);
+  }
+}
+
 }  // namespace
 
 template <typename T>
@@ -174,6 +187,20 @@ bool inv_eligible(int64_t n) {
   return (q & (q - 1)) == 0;
 }
 
+// Order of the padded inverse for the potrf pullback at other n: L^{-1} is
+// the leading n x n block of inv([L 0; 0 I]) at the next N = 64 * 2^k (block
+// algebra: the zero off-diagonal block stays exactly zero), so the inverse
+// runs level-batched at N while the three products stay at n.  Taken while the
+// N^3 / 3 inverse is at most ~1.1 n^3 (N <= 1.5 n) or N <= 256; 0 = not used.
+template <typename T>
+int64_t inv_pad(int64_t n) {
+  if (inv_eligible<T>(n)) return n;
+  if (n <= IB) return 0;
+  int64_t N = 2 * IB;
+  while (N < n) N *= 2;
+  return (N <= 4 * IB || 2 * N <= 3 * n) ? N : 0;
+}
+
 
 template <typename T>
 size_t trsm_inv_scratch(int64_t batch, int64_t m, int64_t n, int64_t nt) {
@@ -181,7 +208,8 @@ size_t trsm_inv_scratch(int64_t batch, int64_t m, int64_t n, int64_t nt) {
 }
 template <typename T>
 size_t potrf_bwd_inv_scratch(int64_t batch, int64_t n) {
-  return sizeof(T) * (size_t)batch * 2 * (size_t)n * n + (size_t)batch * trtri_levels_tmp<T>(n);
+  const int64_t N = inv_pad<T>(n);
+  return sizeof(T) * (size_t)batch * ((size_t)N * N + (size_t)n * n) + (size_t)batch * trtri_levels_tmp<T>(N);
 }
 template <typename T>
 size_t potri_inv_scratch(int64_t batch, int64_t n) {
@@ -212,7 +240,7 @@ size_t ws_potrf_bwd_tail(int64_t batch, int64_t n) {  // potrf_bwd_phi + potrf_b
 }
 template <typename T>
 size_t ws_potrf_bwd_inv(int64_t batch, int64_t n) {
-  return carve_bound(potrf_bwd_inv_scratch<T>(batch, n)) + ws_potrf_inv_prepare<T>(batch, n) +
+  return carve_bound(potrf_bwd_inv_scratch<T>(batch, n)) + ws_potrf_inv_prepare<T>(batch, inv_pad<T>(n)) +
          ws_potrf_bwd_tail<T>(batch, n);
 }
 template <typename T>
@@ -344,11 +372,12 @@ dla_status potrf_bwd_from_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> ab
 template <typename T>
 dla_status potrf_bwd_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> lbar, MatB<const T> l,
                          bool lower) {
+  const int64_t N = inv_pad<T>(n);  // == n unless the inverse is padded
   DLAB_SCRATCH(ws, c, potrf_bwd_inv_scratch<T>(batch, n));
   T* wp = ws.as<T>();
-  MatB<T> wi{wp, n, n * n};                  // L^{-1} (lower)
-  MatB<T> tt{wp + batch * n * n, n, n * n};  // Phi, then the lower half of L^-T Phi L^-1
-  T* tmp = wp + 2 * batch * n * n;
+  MatB<T> wi{wp, N, N * N};                  // L^{-1} (lower; the leading n x n block when padded)
+  MatB<T> tt{wp + batch * N * N, n, n * n};  // Phi, then the lower half of L^-T Phi L^-1
+  T* tmp = wp + batch * (N * N + n * n);
   // L^-1 (trtri) and P' = tril(L^T Lbar) are independent: the inverse runs
   // on a side stream (event fork/join: stream-ordered, graph-capturable)
   // while P' runs on the caller's stream.  The side stream and events belong
@@ -359,7 +388,19 @@ dla_status potrf_bwd_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, M
   sc.stream = fr.side;
   cudaEventRecord(fr.ev[0], c.stream);
   cudaStreamWaitEvent(fr.side, fr.ev[0], 0);
-  const dla_status s1 = potrf_inv_prepare<T>(sc, batch, n, l, lower, wi, tmp);
+  dla_status s1;
+  if (N == n) {
+    s1 = potrf_inv_prepare<T>(sc, batch, n, l, lower, wi, tmp);
+  } else {
+    s1 = ew_tri_copy<T>(sc, batch, n, l, wi, !lower);
+    if (s1 == DLA_OK) {
+      const unsigned gx = (unsigned)((N + 255) / 256);
+      const unsigned gy = (unsigned)std::min<int64_t>(std::max<int64_t>(1, (148 * 16) / gx), batch * N);
+      k_pad_eye<T><<<dim3(gx, gy), 256, 0, sc.stream>>>(batch, n, N, wi);
+      s1 = cudaGetLastError() == cudaSuccess ? DLA_OK : DLA_ERR_CUDA;
+    }
+    if (s1 == DLA_OK) s1 = trtri_levels<T>(sc, batch, N, wi, tmp);
+  }
   cudaEventRecord(fr.ev[1], fr.side);
   const dla_status s2 = potrf_bwd_phi<T>(c, batch, n, lbar, l, lower, tt);
   cudaStreamWaitEvent(c.stream, fr.ev[1], 0);
@@ -413,6 +454,7 @@ dla_status potri_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
                                    bool, T);                                                                 \
   template dla_status potri_inv<T>(const Ctx&, int64_t, int64_t, MatB<T>);                                   \
   template bool inv_eligible<T>(int64_t);                                                                    \
+  template int64_t inv_pad<T>(int64_t);                                                                      \
   template size_t trtri_levels_tmp<T>(int64_t);                                                              \
   template size_t ws_trtri_levels<T>(int64_t, int64_t);                                                      \
   template size_t ws_trsm_inv<T>(int64_t, int64_t, int64_t, bool);                                           \
