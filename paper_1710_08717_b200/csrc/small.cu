@@ -149,9 +149,12 @@ __device__ __forceinline__ T warp_max(T v) {
   return v;
 }
 
-template <typename T, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_potrf_warp(int n, int64_t batch, MatB<T> a, bool lower,
+// NFIX = 32: n is the compile-time constant 32 (every `i < n` guard of the
+// unrolled register code folds away: ~1/3 fewer instructions); 0: runtime n.
+template <typename T, int MINB, int NFIX>
+__global__ void __launch_bounds__(256, MINB) k_potrf_warp(int n_, int64_t batch, MatB<T> a, bool lower,
                                                           int32_t* info) {
+  const int n = NFIX > 0 ? NFIX : n_;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b = (int64_t)blockIdx.x * wpc_fwd<T>() + warp;
@@ -304,11 +307,12 @@ __device__ __forceinline__ void warp_potrf_bwd_core(int n, int lane, const T* L,
     }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(wpc_bwd<T>() * 32, sizeof(T) == 8 ? 3 : 2) k_potrf_bwd_warp(int n, int64_t batch,
+template <typename T, int NFIX>
+__global__ void __launch_bounds__(wpc_bwd<T>() * 32, sizeof(T) == 8 ? 3 : 2) k_potrf_bwd_warp(int n_, int64_t batch,
                                                                                       MatB<T> abar,
                                                                                       MatB<const T> lbar,
                                                                                       MatB<const T> l, bool lower) {
+  const int n = NFIX > 0 ? NFIX : n_;
   constexpr int VN = Bc<T>::N, LLD = Bc<T>::LLD;
   constexpr int per_warp = WN * LLD + WN * WLD + 2 * WN + 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -368,10 +372,11 @@ __global__ void __launch_bounds__(wpc_bwd<T>() * 32, sizeof(T) == 8 ? 3 : 2) k_p
 // Lbar = -tril(S z^T) + diag(1 / L_ii) (dl/adjoints.hpp:136-152,
 // dl/tape.hpp:1038-1045); Abar = potrf pullback (warp_potrf_bwd_core).
 // A and y are read once, Abar / ybar / phi written once.
-template <typename T>
-__global__ void __launch_bounds__(wpc_bwd<T>() * 32) k_chol_chain_warp(int n, int64_t batch, MatB<const T> a,
+template <typename T, int NFIX>
+__global__ void __launch_bounds__(wpc_bwd<T>() * 32) k_chol_chain_warp(int n_, int64_t batch, MatB<const T> a,
                                                                        const T* y, T* phi, MatB<T> abar, T* ybar,
                                                                        int32_t* info) {
+  const int n = NFIX > 0 ? NFIX : n_;
   constexpr int LLD = Bc<T>::LLD;
   constexpr int per_warp = WN * LLD + WN * WLD + 6 * WN;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -614,13 +619,15 @@ dla_status potrf_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool l
       const char* e = getenv("DLA_WARP_MINB");  // tuning switch: 1 = no register cap
       return e ? atoi(e) : 2;
     }();
-    ensure_smem_attr(k_potrf_warp<T, 1>, sm);
-    ensure_smem_attr(k_potrf_warp<T, 2>, sm);
     const unsigned grid = (unsigned)((batch + wpc - 1) / wpc);
-    if (minb == 1)
-      k_potrf_warp<T, 1><<<grid, wpc * 32, sm, c.stream>>>((int)n, batch, a, lower, c.info);
+    auto go = [&](auto kern) {
+      ensure_smem_attr(kern, sm);
+      kern<<<grid, wpc * 32, sm, c.stream>>>((int)n, batch, a, lower, c.info);
+    };
+    if (n == WN)
+      minb == 1 ? go(k_potrf_warp<T, 1, WN>) : go(k_potrf_warp<T, 2, WN>);
     else
-      k_potrf_warp<T, 2><<<grid, wpc * 32, sm, c.stream>>>((int)n, batch, a, lower, c.info);
+      minb == 1 ? go(k_potrf_warp<T, 1, 0>) : go(k_potrf_warp<T, 2, 0>);
     DLAB_LAUNCH_CHECK();
     return DLA_OK;
   }
@@ -654,9 +661,11 @@ dla_status potrf_bwd_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar,
   if (n <= WN) {
     constexpr int wpc = wpc_bwd<T>();
     const size_t sm = sizeof(T) * wpc * (WN * Bc<T>::LLD + WN * WLD + 2 * WN + 4);
-    ensure_smem_attr(k_potrf_bwd_warp<T>, sm);
-    k_potrf_bwd_warp<T><<<(unsigned)((batch + wpc - 1) / wpc), wpc * 32, sm, c.stream>>>((int)n, batch, abar, lbar,
-                                                                                        l, lower);
+    auto go = [&](auto kern) {
+      ensure_smem_attr(kern, sm);
+      kern<<<(unsigned)((batch + wpc - 1) / wpc), wpc * 32, sm, c.stream>>>((int)n, batch, abar, lbar, l, lower);
+    };
+    n == WN ? go(k_potrf_bwd_warp<T, WN>) : go(k_potrf_bwd_warp<T, 0>);
     DLAB_LAUNCH_CHECK();
     return DLA_OK;
   }
@@ -673,9 +682,12 @@ dla_status chol_chain_small(const Ctx& c, int64_t batch, int64_t n, MatB<const T
                             T* ybar) {
   constexpr int wpc = wpc_bwd<T>();
   const size_t sm = sizeof(T) * wpc * (WN * Bc<T>::LLD + WN * WLD + 6 * WN);
-  ensure_smem_attr(k_chol_chain_warp<T>, sm);
-  k_chol_chain_warp<T><<<(unsigned)((batch + wpc - 1) / wpc), wpc * 32, sm, c.stream>>>((int)n, batch, a, y, phi,
-                                                                                       abar, ybar, c.info);
+  auto go = [&](auto kern) {
+    ensure_smem_attr(kern, sm);
+    kern<<<(unsigned)((batch + wpc - 1) / wpc), wpc * 32, sm, c.stream>>>((int)n, batch, a, y, phi, abar, ybar,
+                                                                         c.info);
+  };
+  n == WN ? go(k_chol_chain_warp<T, WN>) : go(k_chol_chain_warp<T, 0>);
   DLAB_LAUNCH_CHECK();
   return DLA_OK;
 }
