@@ -67,8 +67,11 @@ def test_gemm_gemm2(port, dt):
     r = O.rng(1)
     B = 3
     # skinny shapes too: vector (n or m <= 8, k > 8) and outer-product (k <= 8) kernels
+    # + the streaming single-vector kernels: matvec rows / columns (n = 1, even k),
+    # rank-1 outer products (k = 1, even n), ragged (odd) fallbacks
     for m, n, k in [(3, 5, 4), (1, 1, 1), (17, 9, 33), (64, 70, 65), (130, 129, 66), (1, 1, 300), (130, 3, 200),
-                    (5, 130, 70), (70, 1, 130), (40, 2, 50), (66, 90, 3)]:
+                    (5, 130, 70), (70, 1, 130), (40, 2, 50), (66, 90, 3), (128, 1, 128), (1, 128, 128),
+                    (129, 1, 64), (64, 128, 1), (5, 6, 1), (300, 1, 258)]:
         for ta, tb in itertools.product([0, 1], repeat=2):
             a = r.standard_normal((B,) + ((k, m) if ta else (m, k))).astype(dt)
             b = r.standard_normal((B,) + ((n, k) if tb else (k, n))).astype(dt)
@@ -86,9 +89,11 @@ def test_gemm_gemm2(port, dt):
 
 
 @pytest.mark.parametrize("dt", DTYPES)
-def test_gemm_backward(port, dt):
+@pytest.mark.parametrize("mnk", [(7, 9, 5), (128, 1, 128), (64, 128, 1), (130, 70, 200), (257, 3, 300),
+                                 (300, 260, 150)])
+def test_gemm_backward(port, dt, mnk):
     r = O.rng(2)
-    B, m, n, k = 2, 7, 9, 5
+    B, (m, n, k) = 2, mnk
     for ta, tb in itertools.product([0, 1], repeat=2):
         a = r.standard_normal((B,) + ((k, m) if ta else (m, k))).astype(dt)
         b = r.standard_normal((B,) + ((n, k) if tb else (k, n))).astype(dt)
@@ -143,7 +148,7 @@ def test_gemm_rejects_alias_and_shape():
 def test_syrk(port, dt):
     r = O.rng(3)
     B = 2
-    for n, k in [(4, 6), (1, 3), (65, 17), (100, 130)]:
+    for n, k in [(4, 6), (1, 3), (65, 17), (100, 130), (64, 1), (6, 1), (7, 1)]:  # k = 1: masked rank-1 kernel
         for ta in (0, 1):
             a = r.standard_normal((B,) + ((k, n) if ta else (n, k))).astype(dt)
             got = L.syrk(dev(a), ta, 0.75)

@@ -22,8 +22,15 @@ g = gp.GPNLL(n, d, 1, "cuda")
 for _ in range(3):
     g.step(x, y, 1.0, 1.0, 0.1)
 torch.cuda.synchronize()
+step = lambda: g.step(x, y, 1.0, 1.0, 0.1)  # noqa: E731
+if os.environ.get("GRAPH", "1") != "0":  # as bench.py times it: CUDA graph replay
+    import bench  # noqa: E402
+
+    step = bench.graphed(torch, step)
+    step()
+    torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
-    g.step(x, y, 1.0, 1.0, 0.1)
+    step()
     torch.cuda.synchronize()
 prof.export_chrome_trace(out)
 ev = [e for e in json.load(open(out))["traceEvents"] if e.get("cat") in ("kernel", "gpu_memset", "gpu_memcpy")]
@@ -63,3 +70,8 @@ for t, dur, st, key in marks:
     p[3] += 1
 for (key, st), (a, b, tot, cnt) in sorted(phase.items(), key=lambda kv: kv[1][0]):
     print(f"{key:30s} stream {st}: [{a:8.1f}, {b:8.1f}] us  busy {tot:8.1f} us  n={cnt}")
+
+if os.environ.get("DUMP"):
+    for e in ev:
+        print(f"{e['ts'] - t0:9.1f} +{e['dur']:7.1f} s{e['args'].get('stream')} "
+              f"{e['name'].replace('dlab::(anonymous namespace)::', '')[:90]}")
