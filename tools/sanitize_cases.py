@@ -12,7 +12,7 @@ from paper_1710_08717_b200 import linalg as L  # noqa: E402
 
 r = O.rng(1)
 f = dict(dtype=torch.float64, device="cuda")
-for n, B in ((16, 3), (40, 2), (200, 2), (256, 1)):
+for n, B in ((16, 3), (32, 5), (40, 2), (100, 3), (128, 2), (200, 2), (256, 1)):
     a = torch.from_numpy(O.random_spd(n, r, batch=B)).cuda()
     l = L.potrf(a)
     L.potrf_backward(torch.tril(torch.randn_like(l)), l)
@@ -27,5 +27,16 @@ q = torch.randn(2, 80, 120, **f)
 L.gelqf(q)
 L.gemm2(torch.randn(2, 130, 70, **f), torch.randn(2, 70, 90, **f))
 gp.gp_nll_grad(torch.randn(256, 8, **f), torch.randn(256, 1, **f), 1.0, 1.0, 0.1)
+gp.gp_nll_grad(torch.randn(512, 8, **f), torch.randn(512, 1, **f), 1.0, 1.0, 0.1)  # early inverse + fused tail
+# single-vector / rank-1 streaming kernels, syrk (TMA at m >= 256), LQ (CholeskyQR2 at m >= 64), SVD
+g = torch.randn(4, 128, 128, **f)
+v = torch.randn(4, 128, 1, **f)
+L.gemm2(g, v)
+L.gemm2(g, v, True, False)
+L.gemm2(v, v, False, True)
+L.syrk(torch.randn(2, 300, 40, **f))
+L.gelqf(torch.randn(2, 128, 512, **f))
+L.gesvd(torch.randn(2, 40, 60, **f))
+torch.cuda.synchronize()
 torch.cuda.synchronize()
 print("sanitize cases done")
