@@ -401,9 +401,13 @@ def also_measurements(torch, args, rank, world, lib, fp64_peak, hbm):
         ms = run_potrf_batch(torch, n, B, 10 if n > 64 else 20, 3, world)
         flops = B * 5 * n ** 3 / 3
         gf = world * flops / (ms / 1e3) / 1e9
+        # HBM bytes per step: input copy (r + w), potrf (r A, w L), potrf_bwd (r L, r Lbar, w Abar)
+        hbm_b = B * 7 * n * n * 8
         out.append({"workload": f"potrf fwd+bwd, batch {B} x {n}^2 fp64 (incl. input copy)",
                     "matrices_per_s": world * B / (ms / 1e3), "ms_per_step": ms, "gflops": gf,
-                    "frac_of_fp64_peak": gf / 1e3 / fp64_peak / world})
+                    "frac_of_fp64_peak": gf / 1e3 / fp64_peak / world,
+                    "hbm_gb_per_s": hbm_b / (ms / 1e3) / 1e9, "frac_of_hbm": hbm_b / (ms / 1e3) / 1e9 / hbm,
+                    "bound": "hbm" if n <= 64 else "tensor"})
     return out
 
 

@@ -364,6 +364,230 @@ __global__ void __launch_bounds__(wpc_bwd<T>() * 32, sizeof(T) == 8 ? 3 : 2) k_p
 }
 
 
+// ---------------------------------------------- n <= 32, fp64, on FP64 DMMA
+// The same pullback as warp_potrf_bwd_core, Abar = 1/2 sym(L^-T Phi L^-1),
+// Phi = copyltu(L^T Lbar) (dl/adjoints.hpp:175-191), with every product a
+// warp-level m8n8k4 DMMA over 8 x 8 tiles and L^-1 formed explicitly (8 x 8
+// diagonal inverses, one column per lane, then two doubling levels):
+//   P = tril(L^T Lbar) (10 lower tiles), Phi -> G;  Linv -> Lm (in place);
+//   X = Linv^T Phi;  Y = X Linv -> G;  Abar = 1/2 sym(Y).
+// ~240 DMMAs replace ~3000 FMA / broadcast-load instructions of the
+// substitution form: the batched n = 32 pullback is issue-bound, not
+// FP64-bound.  Row stride DLD = 36 (= 4 mod 16): both fragment orientations
+// (k along rows and k along columns) load conflict-free.
+constexpr int DLD = 36;
+constexpr int DBUF = WN * DLD;  // one 32 x 32 buffer
+
+__device__ __forceinline__ void dmma8(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Lm: L (lower, strict upper zero, identity beyond n); G: tril(Lbar) (zero
+// beyond n); X: scratch.  Writes Abar's n x n block to o (row stride ldo).
+__device__ __forceinline__ void warp_potrf_bwd_dmma(int n, int lane, double* Lm, double* G, double* X, double* o,
+                                                    int ldo, bool store) {
+  const int fr = lane >> 2, fc = lane & 3;
+  // (1) P = tril(L^T Lbar): tile (I, J), I >= J, k >= 8 I
+  {
+    double p[10][2];
+#pragma unroll
+    for (int t = 0; t < 10; ++t) p[t][0] = p[t][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      double bf[4];
+#pragma unroll
+      for (int J = 0; J < 4; ++J) bf[J] = G[(4 * s + fc) * DLD + 8 * J + fr];
+#pragma unroll
+      for (int I = 0; I < 4; ++I) {
+        if (2 * I > s) continue;  // k = 4 s .. 4 s + 3 >= 8 I
+        const double af = Lm[(4 * s + fc) * DLD + 8 * I + fr];  // (L^T)(8I + fr, k) = L(k, 8I + fr)
+#pragma unroll
+        for (int J = 0; J <= I; ++J) dmma8(p[I * (I + 1) / 2 + J][0], p[I * (I + 1) / 2 + J][1], af, bf[J]);
+      }
+    }
+    __syncwarp();
+    // Phi = copyltu(P) into G (mirrored)
+#pragma unroll
+    for (int I = 0; I < 4; ++I)
+#pragma unroll
+      for (int J = 0; J <= I; ++J)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = 8 * I + fr, j = 8 * J + 2 * fc + e;
+          if (i >= j) {
+            G[i * DLD + j] = p[I * (I + 1) / 2 + J][e];
+            G[j * DLD + i] = p[I * (I + 1) / 2 + J][e];
+          }
+        }
+  }
+  // (2) Linv in place of L: 8 x 8 diagonal blocks (lane = block, column) ...
+  {
+    const int o8 = (lane >> 3) * 8, c = lane & 7;
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      double acc = i == c ? 1.0 : 0.0;
+#pragma unroll
+      for (int q = 0; q < i; ++q)
+        if (q >= c) acc -= Lm[(o8 + i) * DLD + o8 + q] * x[q];
+      x[i] = i >= c ? acc / Lm[(o8 + i) * DLD + o8 + i] : 0.0;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i >= c) Lm[(o8 + i) * DLD + o8 + c] = x[i];
+    __syncwarp();
+  }
+  // ... then [A 0; B C] -> B = -C^{-1} (B A^{-1}) for s = 8 (two pairs), 16
+#pragma unroll
+  for (int s = 8; s < WN; s *= 2) {
+    const int pairs = WN / (2 * s), tps = (s / 8) * (s / 8);
+    double t1[4][2];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) t1[t][0] = t1[t][1] = 0.0;
+#pragma unroll
+    for (int t = 0; t < pairs * tps; ++t) {  // T1 = B A^{-1}: k >= nt
+      const int pr = t / tps, r = t % tps, rt = (r / (s / 8)) * 8, nt = (r % (s / 8)) * 8, o = 2 * s * pr;
+#pragma unroll
+      for (int kk = 0; kk < s; kk += 4) {
+        if (kk < nt) continue;
+        dmma8(t1[t][0], t1[t][1], Lm[(o + s + rt + fr) * DLD + o + kk + fc], Lm[(o + kk + fc) * DLD + o + nt + fr]);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < pairs * tps; ++t) {
+      const int pr = t / tps, r = t % tps, rt = (r / (s / 8)) * 8, nt = (r % (s / 8)) * 8;
+      X[(pr * s + rt + fr) * DLD + nt + 2 * fc] = t1[t][0];
+      X[(pr * s + rt + fr) * DLD + nt + 2 * fc + 1] = t1[t][1];
+    }
+    __syncwarp();
+    double bn[4][2];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) bn[t][0] = bn[t][1] = 0.0;
+#pragma unroll
+    for (int t = 0; t < pairs * tps; ++t) {  // B = -C^{-1} T1: k <= rt + 7
+      const int pr = t / tps, r = t % tps, rt = (r / (s / 8)) * 8, nt = (r % (s / 8)) * 8, o = 2 * s * pr;
+#pragma unroll
+      for (int kk = 0; kk < s; kk += 4) {
+        if (kk >= rt + 8) continue;
+        dmma8(bn[t][0], bn[t][1], Lm[(o + s + rt + fr) * DLD + o + s + kk + fc], X[(pr * s + kk + fc) * DLD + nt + fr]);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < pairs * tps; ++t) {
+      const int pr = t / tps, r = t % tps, rt = (r / (s / 8)) * 8, nt = (r % (s / 8)) * 8, o = 2 * s * pr;
+      Lm[(o + s + rt + fr) * DLD + o + nt + 2 * fc] = -bn[t][0];
+      Lm[(o + s + rt + fr) * DLD + o + nt + 2 * fc + 1] = -bn[t][1];
+    }
+    __syncwarp();
+  }
+  // (3) X = Linv^T Phi: k >= 8 I
+  {
+    double x[16][2];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) x[t][0] = x[t][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      double bf[4];
+#pragma unroll
+      for (int J = 0; J < 4; ++J) bf[J] = G[(4 * s + fc) * DLD + 8 * J + fr];
+#pragma unroll
+      for (int I = 0; I < 4; ++I) {
+        if (2 * I > s) continue;
+        const double af = Lm[(4 * s + fc) * DLD + 8 * I + fr];  // Linv(k, 8I + fr)
+#pragma unroll
+        for (int J = 0; J < 4; ++J) dmma8(x[4 * I + J][0], x[4 * I + J][1], af, bf[J]);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int i = 8 * (t / 4) + fr, j = 8 * (t % 4) + 2 * fc;
+      X[i * DLD + j] = x[t][0];
+      X[i * DLD + j + 1] = x[t][1];
+    }
+  }
+  __syncwarp();
+  // (4) Y = X Linv: k >= 8 J; Y -> G
+  {
+    double y[16][2];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) y[t][0] = y[t][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      double af[4];
+#pragma unroll
+      for (int I = 0; I < 4; ++I) af[I] = X[(8 * I + fr) * DLD + 4 * s + fc];
+#pragma unroll
+      for (int J = 0; J < 4; ++J) {
+        if (2 * J > s) continue;
+        const double bf = Lm[(4 * s + fc) * DLD + 8 * J + fr];
+#pragma unroll
+        for (int I = 0; I < 4; ++I) dmma8(y[4 * I + J][0], y[4 * I + J][1], af[I], bf);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int i = 8 * (t / 4) + fr, j = 8 * (t % 4) + 2 * fc;
+      G[i * DLD + j] = y[t][0];
+      G[i * DLD + j + 1] = y[t][1];
+    }
+  }
+  __syncwarp();
+  // (5) Abar = 1/2 sym(Y), exactly symmetric; column `lane`, coalesced rows
+  if (store && lane < n) {
+#pragma unroll 8
+    for (int i = 0; i < WN; ++i) {
+      if (i < n) {
+        const double hi = G[i * DLD + lane] * 0.5, hj = G[lane * DLD + i] * 0.5;
+        o[i * ldo + lane] = (i == lane) ? hi : (hi + hj) * 0.5;
+      }
+    }
+  }
+}
+
+// Warp per matrix (4 per CTA), fp64 n <= 32: loads L and tril(Lbar) (lower
+// views of the upper variant), pads to 32, runs warp_potrf_bwd_dmma.
+__global__ void __launch_bounds__(128) k_potrf_bwd_dmma(int n, int64_t batch, MatB<double> abar,
+                                                        MatB<const double> lbar, MatB<const double> l, bool lower) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b = (int64_t)blockIdx.x * 4 + warp;
+  if (b >= batch) return;
+  double* Lm = reinterpret_cast<double*>(smem_raw) + warp * 3 * DBUF;
+  double* G = Lm + DBUF;
+  double* X = G + DBUF;
+  const double* gl = l.at(b, 0, 0);
+  const double* gg = lbar.at(b, 0, 0);
+  const int ldl = (int)l.ld, ldg = (int)lbar.ld;
+#pragma unroll
+  for (int i0 = 0; i0 < WN; i0 += 16) {
+    double lv[16], gv[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int i = i0 + u;
+      lv[u] = (i < n && lane < n) ? gl[i * ldl + lane] : 0.0;
+      gv[u] = (i < n && lane < n) ? gg[i * ldg + lane] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int i = i0 + u;
+      if (lower) {  // element (i, lane)
+        Lm[i * DLD + lane] = lane <= i ? (i < n ? lv[u] : (lane == i ? 1.0 : 0.0)) : 0.0;
+        G[i * DLD + lane] = lane <= i ? gv[u] : 0.0;
+      } else {      // R(i, lane) = L(lane, i), Rbar(i, lane) = Lbar(lane, i)
+        Lm[lane * DLD + i] = i <= lane ? (lane < n ? lv[u] : (lane == i ? 1.0 : 0.0)) : 0.0;
+        G[lane * DLD + i] = i <= lane ? gv[u] : 0.0;
+      }
+    }
+  }
+  __syncwarp();
+  warp_potrf_bwd_dmma(n, lane, Lm, G, X, abar.at(b, 0, 0), (int)abar.ld, true);
+}
+
 // Fused Gaussian log-likelihood chain, one warp per matrix (n <= 32), the
 // whole of BASELINE config C1 in one launch (dl/models.hpp:99-103 given A):
 //   L = potrf(A) (dl/cholesky.hpp:35-72), z = L^-1 y (dl/blas.hpp:307-395),
@@ -659,6 +883,22 @@ template <typename T>
 dla_status potrf_bwd_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> lbar,
                            MatB<const T> l, bool lower) {
   if (n <= WN) {
+    if constexpr (sizeof(T) == 8) {
+      static const bool dmma = [] {
+        const char* e = getenv("DLA_SMALL_BWD_DMMA");  // tuning switch: 0 = the substitution kernel
+        return e ? atoi(e) != 0 : true;
+      }();
+      if (dmma) {
+        const size_t sm = sizeof(double) * 4 * 3 * DBUF;
+        ensure_smem_attr(k_potrf_bwd_dmma, sm);
+        MatB<double> ab{reinterpret_cast<double*>(abar.p), abar.ld, abar.bs, abar.bsi};
+        MatB<const double> lb{reinterpret_cast<const double*>(lbar.p), lbar.ld, lbar.bs, lbar.bsi};
+        MatB<const double> lv{reinterpret_cast<const double*>(l.p), l.ld, l.bs, l.bsi};
+        k_potrf_bwd_dmma<<<(unsigned)((batch + 3) / 4), 128, sm, c.stream>>>((int)n, batch, ab, lb, lv, lower);
+        DLAB_LAUNCH_CHECK();
+        return DLA_OK;
+      }
+    }
     constexpr int wpc = wpc_bwd<T>();
     const size_t sm = sizeof(T) * wpc * (WN * Bc<T>::LLD + WN * WLD + 2 * WN + 4);
     auto go = [&](auto kern) {
