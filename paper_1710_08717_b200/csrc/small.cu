@@ -550,9 +550,14 @@ __device__ __forceinline__ void warp_potrf_bwd_dmma(int n, int lane, double* Lm,
 }
 
 // Warp per matrix (4 per CTA), fp64 n <= 32: loads L and tril(Lbar) (lower
-// views of the upper variant), pads to 32, runs warp_potrf_bwd_dmma.
-__global__ void __launch_bounds__(128) k_potrf_bwd_dmma(int n, int64_t batch, MatB<double> abar,
-                                                        MatB<const double> lbar, MatB<const double> l, bool lower) {
+// views of the upper variant), pads to 32, runs warp_potrf_bwd_dmma.  (A
+// persistent variant prefetching the next matrix into registers measured
+// slower: 234 registers, and the kernel is not HBM-latency bound.)
+template <bool LOWER, int NFIX>
+__global__ void __launch_bounds__(128) k_potrf_bwd_dmma(int n_, int64_t batch, MatB<double> abar,
+                                                        MatB<const double> lbar, MatB<const double> l) {
+  constexpr bool lower = LOWER;
+  const int n = NFIX > 0 ? NFIX : n_;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b = (int64_t)blockIdx.x * 4 + warp;
@@ -890,11 +895,17 @@ dla_status potrf_bwd_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar,
       }();
       if (dmma) {
         const size_t sm = sizeof(double) * 4 * 3 * DBUF;
-        ensure_smem_attr(k_potrf_bwd_dmma, sm);
         MatB<double> ab{reinterpret_cast<double*>(abar.p), abar.ld, abar.bs, abar.bsi};
         MatB<const double> lb{reinterpret_cast<const double*>(lbar.p), lbar.ld, lbar.bs, lbar.bsi};
         MatB<const double> lv{reinterpret_cast<const double*>(l.p), l.ld, l.bs, l.bsi};
-        k_potrf_bwd_dmma<<<(unsigned)((batch + 3) / 4), 128, sm, c.stream>>>((int)n, batch, ab, lb, lv, lower);
+        auto go = [&](auto kern) {
+          ensure_smem_attr(kern, sm);
+          kern<<<(unsigned)((batch + 3) / 4), 128, sm, c.stream>>>((int)n, batch, ab, lb, lv);
+        };
+        if (lower)
+          n == WN ? go(k_potrf_bwd_dmma<true, WN>) : go(k_potrf_bwd_dmma<true, 0>);
+        else
+          n == WN ? go(k_potrf_bwd_dmma<false, WN>) : go(k_potrf_bwd_dmma<false, 0>);
         DLAB_LAUNCH_CHECK();
         return DLA_OK;
       }
