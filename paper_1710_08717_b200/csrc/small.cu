@@ -377,6 +377,8 @@ __global__ void __launch_bounds__(wpc_bwd<T>() * 32, sizeof(T) == 8 ? 3 : 2) k_p
 // (k along rows and k along columns) load conflict-free.
 constexpr int DLD = 36;
 constexpr int DBUF = WN * DLD;  // one 32 x 32 buffer
+constexpr int TLD = 20;         // the doubling levels' T1 scratch (16 x 16 at most; = 4 mod 16)
+constexpr int TBUF = 16 * TLD;
 
 __device__ __forceinline__ void dmma8(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -385,7 +387,8 @@ __device__ __forceinline__ void dmma8(double& c0, double& c1, double a, double b
 }
 
 // Lm: L (lower, strict upper zero, identity beyond n); G: tril(Lbar) (zero
-// beyond n); X: scratch.  Writes Abar's n x n block to o (row stride ldo).
+// beyond n), reused for Phi, X and Y; X: TBUF scratch for the doubling
+// levels.  Writes Abar's n x n block to o (row stride ldo).
 __device__ __forceinline__ void warp_potrf_bwd_dmma(int n, int lane, double* Lm, double* G, double* X, double* o,
                                                     int ldo, bool store) {
   const int fr = lane >> 2, fc = lane & 3;
@@ -459,8 +462,8 @@ __device__ __forceinline__ void warp_potrf_bwd_dmma(int n, int lane, double* Lm,
 #pragma unroll
     for (int t = 0; t < pairs * tps; ++t) {
       const int pr = t / tps, r = t % tps, rt = (r / (s / 8)) * 8, nt = (r % (s / 8)) * 8;
-      X[(pr * s + rt + fr) * DLD + nt + 2 * fc] = t1[t][0];
-      X[(pr * s + rt + fr) * DLD + nt + 2 * fc + 1] = t1[t][1];
+      X[(pr * s + rt + fr) * TLD + nt + 2 * fc] = t1[t][0];
+      X[(pr * s + rt + fr) * TLD + nt + 2 * fc + 1] = t1[t][1];
     }
     __syncwarp();
     double bn[4][2];
@@ -472,7 +475,7 @@ __device__ __forceinline__ void warp_potrf_bwd_dmma(int n, int lane, double* Lm,
 #pragma unroll
       for (int kk = 0; kk < s; kk += 4) {
         if (kk >= rt + 8) continue;
-        dmma8(bn[t][0], bn[t][1], Lm[(o + s + rt + fr) * DLD + o + s + kk + fc], X[(pr * s + kk + fc) * DLD + nt + fr]);
+        dmma8(bn[t][0], bn[t][1], Lm[(o + s + rt + fr) * DLD + o + s + kk + fc], X[(pr * s + kk + fc) * TLD + nt + fr]);
       }
     }
     __syncwarp();
@@ -502,15 +505,16 @@ __device__ __forceinline__ void warp_potrf_bwd_dmma(int n, int lane, double* Lm,
         for (int J = 0; J < 4; ++J) dmma8(x[4 * I + J][0], x[4 * I + J][1], af, bf[J]);
       }
     }
+    __syncwarp();  // Phi is dead: X replaces it in G
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
       const int i = 8 * (t / 4) + fr, j = 8 * (t % 4) + 2 * fc;
-      X[i * DLD + j] = x[t][0];
-      X[i * DLD + j + 1] = x[t][1];
+      G[i * DLD + j] = x[t][0];
+      G[i * DLD + j + 1] = x[t][1];
     }
   }
   __syncwarp();
-  // (4) Y = X Linv: k >= 8 J; Y -> G
+  // (4) Y = X Linv: k >= 8 J; Y replaces X in G
   {
     double y[16][2];
 #pragma unroll
@@ -519,7 +523,7 @@ __device__ __forceinline__ void warp_potrf_bwd_dmma(int n, int lane, double* Lm,
     for (int s = 0; s < 8; ++s) {
       double af[4];
 #pragma unroll
-      for (int I = 0; I < 4; ++I) af[I] = X[(8 * I + fr) * DLD + 4 * s + fc];
+      for (int I = 0; I < 4; ++I) af[I] = G[(8 * I + fr) * DLD + 4 * s + fc];
 #pragma unroll
       for (int J = 0; J < 4; ++J) {
         if (2 * J > s) continue;
@@ -549,20 +553,21 @@ __device__ __forceinline__ void warp_potrf_bwd_dmma(int n, int lane, double* Lm,
   }
 }
 
-// Warp per matrix (4 per CTA), fp64 n <= 32: loads L and tril(Lbar) (lower
+// Warp per matrix (BDW per CTA), fp64 n <= 32: loads L and tril(Lbar) (lower
 // views of the upper variant), pads to 32, runs warp_potrf_bwd_dmma.  (A
 // persistent variant prefetching the next matrix into registers measured
 // slower: 234 registers, and the kernel is not HBM-latency bound.)
+constexpr int BDW = 2;  // warps per CTA (42 KB): five CTAs per SM
 template <bool LOWER, int NFIX>
-__global__ void __launch_bounds__(128) k_potrf_bwd_dmma(int n_, int64_t batch, MatB<double> abar,
+__global__ void __launch_bounds__(BDW * 32) k_potrf_bwd_dmma(int n_, int64_t batch, MatB<double> abar,
                                                         MatB<const double> lbar, MatB<const double> l) {
   constexpr bool lower = LOWER;
   const int n = NFIX > 0 ? NFIX : n_;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t b = (int64_t)blockIdx.x * 4 + warp;
+  const int64_t b = (int64_t)blockIdx.x * BDW + warp;
   if (b >= batch) return;
-  double* Lm = reinterpret_cast<double*>(smem_raw) + warp * 3 * DBUF;
+  double* Lm = reinterpret_cast<double*>(smem_raw) + warp * (2 * DBUF + TBUF);
   double* G = Lm + DBUF;
   double* X = G + DBUF;
   const double* gl = l.at(b, 0, 0);
@@ -717,6 +722,119 @@ __global__ void __launch_bounds__(wpc_bwd<T>() * 32) k_chol_chain_warp(int n_, i
   __syncthreads();
   warp_potrf_bwd_core<T>(n, lane, L, W, dg, rd, abar.at(b, 0, 0), (int)abar.ld, ok);
 }
+// fp64 C1 chain with the pullback on DMMA (warp_potrf_bwd_dmma): the
+// forward (symmetry check, register Cholesky, z = L^-1 y, phi) and the
+// vector pullbacks (S = L^-T z, Lbar = -tril(S z^T) + diag(1 / L_ii)) as in
+// k_chol_chain_warp; then the potrf pullback on 8 x 8 DMMA tiles.  Two warps
+// per CTA (2 x 9 KB buffers + 2.5 KB per warp), phases in lockstep as there.
+constexpr int CDW = 2;  // warps per CTA
+template <int NFIX>
+__global__ void __launch_bounds__(CDW * 32) k_chol_chain_dmma(int n_, int64_t batch, MatB<const double> a,
+                                                             const double* y, double* phi, MatB<double> abar,
+                                                             double* ybar, int32_t* info) {
+  using T = double;
+  const int n = NFIX > 0 ? NFIX : n_;
+  constexpr int per_warp = 2 * DBUF + TBUF + 6 * WN;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t bw = (int64_t)blockIdx.x * CDW + warp;
+  bool ok = bw < batch;
+  const int64_t b = ok ? bw : batch - 1;
+  T* Lm = reinterpret_cast<T*>(smem_raw) + warp * per_warp;  // L (true), then L^-1
+  T* G = Lm + DBUF;                                          // A, then Lbar / Phi / Y
+  T* X = G + DBUF;
+  T* buf = X + TBUF;
+  T* rd = buf + 2 * WN;
+  T* sv = rd + WN;
+  T* lg = sv + WN;
+  const T* ga = a.at(b, 0, 0);
+  const int ld = (int)a.ld;
+  {
+    T v[WN];
+#pragma unroll
+    for (int i = 0; i < WN; ++i) v[i] = (i < n && lane < n) ? ga[i * ld + lane] : T(0);
+#pragma unroll
+    for (int i = 0; i < WN; ++i)
+      if (i < n) G[i * DLD + lane] = v[i];
+  }
+  T yv = lane < n ? y[b * n + lane] : T(0);
+  __syncwarp();
+  // symmetry precheck (dl/cholesky.hpp:19-25), as k_potrf_warp
+  T mabs = T(0), masym = T(0);
+  if (lane < n)
+    for (int j = 0; j < n; ++j) {
+      const T v = G[lane * DLD + j];
+      if (fabs(v) > mabs) mabs = fabs(v);
+      if (j > lane) {
+        const T d = fabs(v - G[j * DLD + lane]);
+        if (d > masym) masym = d;
+      }
+    }
+  mabs = warp_max(mabs);
+  masym = warp_max(masym);
+  if (masym > Num<T>::sym_rtol * (mabs > T(0) ? mabs : T(1))) {
+    if (lane == 0 && ok) record_failure(info, b, DLA_ERR_ASYMMETRIC, 0);
+    ok = false;
+  }
+  __syncthreads();
+  T r[WN];
+#pragma unroll
+  for (int c = 0; c < WN; ++c) r[c] = (lane < n && c <= lane) ? G[lane * DLD + c] : (c == lane ? T(1) : T(0));
+  int failed = -1;
+  wchol_col<T, 0>(r, lane, n, buf, failed, r[0]);
+  if (failed >= 0) {
+    if (lane == 0 && ok) record_failure(info, b, DLA_ERR_NOT_SPD, failed);
+    ok = false;
+  }
+  __syncthreads();
+  // L (true, zero strict upper, identity beyond n) into Lm, row `lane`
+#pragma unroll
+  for (int c = 0; c < WN; ++c) Lm[lane * DLD + c] = c <= lane ? (lane < n ? r[c] : (c == lane ? T(1) : T(0))) : T(0);
+  __syncwarp();
+  const T d = Lm[lane * DLD + lane];  // (1 beyond n)
+  const T rinv = T(1) / d;
+  rd[lane] = rinv;
+  // z = L^-1 y, column-oriented: z_j = y_j / L_jj moves by one shuffle
+  T z = T(0);
+#pragma unroll
+  for (int j = 0; j < WN; ++j) {
+    if (j < n) {
+      const T zj = __shfl_sync(0xffffffffu, yv * rinv, j);
+      if (lane == j) z = zj;
+      if (lane > j) yv -= r[j] * zj;
+    }
+  }
+  sv[lane] = lane < n ? z : T(0);
+  lg[lane] = lane < n ? Num<T>::log_(d) : T(0);
+  __syncwarp();
+  if (lane == 0 && ok) {  // sequential i order, as the tape's Sum node
+    T q = T(0), ldt = T(0);
+    for (int i = 0; i < n; ++i) q += sv[i] * sv[i];
+    for (int i = 0; i < n; ++i) ldt += lg[i];
+    phi[b] = T(0.5) * q + ldt;
+  }
+  // S = L^-T z (zbar = z), row k of L from Lm
+  T zb = z, s_own = T(0);
+#pragma unroll
+  for (int k = WN - 1; k >= 0; --k) {
+    if (k < n) {
+      const T sk = __shfl_sync(0xffffffffu, zb * rinv, k);
+      if (lane == k) s_own = sk;
+      if (lane < k) zb -= Lm[k * DLD + lane] * sk;
+    }
+  }
+  if (lane < n && ok) ybar[b * n + lane] = s_own;
+  __syncthreads();
+  sv[lane] = lane < n ? s_own : T(0);
+  __syncwarp();
+  // Lbar, column `lane`: -s_i z_lane (i >= lane) + 1 / L_ii on the diagonal; zero beyond n
+#pragma unroll
+  for (int i = 0; i < WN; ++i)
+    G[i * DLD + lane] = (i < n && i >= lane && lane < n) ? -sv[i] * z + (i == lane ? rinv : T(0)) : T(0);
+  __syncthreads();
+  warp_potrf_bwd_dmma(n, lane, Lm, G, X, abar.at(b, 0, 0), (int)abar.ld, ok);
+}
+
 // ------------------------------------------- 64 < n <= 128 (fp64): CTA per matrix
 // The whole factorization of one matrix in ONE launch with its lower
 // triangle in shared memory as three 64 x 64 blocks (A11, A21, A22: 100 KB,
@@ -894,13 +1012,13 @@ dla_status potrf_bwd_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar,
         return e ? atoi(e) != 0 : true;
       }();
       if (dmma) {
-        const size_t sm = sizeof(double) * 4 * 3 * DBUF;
+        const size_t sm = sizeof(double) * BDW * (2 * DBUF + TBUF);
         MatB<double> ab{reinterpret_cast<double*>(abar.p), abar.ld, abar.bs, abar.bsi};
         MatB<const double> lb{reinterpret_cast<const double*>(lbar.p), lbar.ld, lbar.bs, lbar.bsi};
         MatB<const double> lv{reinterpret_cast<const double*>(l.p), l.ld, l.bs, l.bsi};
         auto go = [&](auto kern) {
           ensure_smem_attr(kern, sm);
-          kern<<<(unsigned)((batch + 3) / 4), 128, sm, c.stream>>>((int)n, batch, ab, lb, lv);
+          kern<<<(unsigned)((batch + BDW - 1) / BDW), BDW * 32, sm, c.stream>>>((int)n, batch, ab, lb, lv);
         };
         if (lower)
           n == WN ? go(k_potrf_bwd_dmma<true, WN>) : go(k_potrf_bwd_dmma<true, 0>);
@@ -931,6 +1049,26 @@ dla_status potrf_bwd_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar,
 template <typename T>
 dla_status chol_chain_small(const Ctx& c, int64_t batch, int64_t n, MatB<const T> a, const T* y, T* phi, MatB<T> abar,
                             T* ybar) {
+  if constexpr (sizeof(T) == 8) {
+    static const bool dmma = [] {
+      const char* e = getenv("DLA_SMALL_BWD_DMMA");  // tuning switch: 0 = the substitution pullback
+      return e ? atoi(e) != 0 : true;
+    }();
+    if (dmma) {
+      const size_t sm = sizeof(double) * CDW * (2 * DBUF + TBUF + 6 * WN);
+      MatB<const double> ad{reinterpret_cast<const double*>(a.p), a.ld, a.bs, a.bsi};
+      MatB<double> abd{reinterpret_cast<double*>(abar.p), abar.ld, abar.bs, abar.bsi};
+      auto go = [&](auto kern) {
+        ensure_smem_attr(kern, sm);
+        kern<<<(unsigned)((batch + CDW - 1) / CDW), CDW * 32, sm, c.stream>>>(
+            (int)n, batch, ad, reinterpret_cast<const double*>(y), reinterpret_cast<double*>(phi), abd,
+            reinterpret_cast<double*>(ybar), c.info);
+      };
+      n == WN ? go(k_chol_chain_dmma<WN>) : go(k_chol_chain_dmma<0>);
+      DLAB_LAUNCH_CHECK();
+      return DLA_OK;
+    }
+  }
   constexpr int wpc = wpc_bwd<T>();
   const size_t sm = sizeof(T) * wpc * (WN * Bc<T>::LLD + WN * WLD + 6 * WN);
   auto go = [&](auto kern) {
