@@ -92,7 +92,7 @@ def run(torch, args, rank, world, lib, fp64_peak, hbm):
                      operator_chain={"ms_per_step": ms_ops, "matrices_per_s": world * B / (ms_ops / 1e3),
                                      "note": "same chain via 7 per-operator C-ABI calls (graph-replayed)"},
                      batch_sweep=sweep,
-                     roofline={"bound": "hbm", "kernel": "k_chol_chain_warp",
+                     roofline={"bound": "hbm", "kernel": "k_chol_chain_dmma (fp64)",
                                "achieved": big["gb_per_s"] if big else None, "peak": hbm, "unit": "GB/s",
                                "frac": big["frac_of_hbm"] if big else None, "traffic": None,
                                "note": f"at batch {big['batch'] if big else '-'} (batch 64 = 1 MiB per step is "
@@ -157,8 +157,9 @@ def run(torch, args, rank, world, lib, fp64_peak, hbm):
                      "rejects 512x128, dl/lq.hpp:26-29)", per_dtype=res, cpu_baseline=cpu,
                      roofline={"bound": "tensor", "achieved": res[0]["tflops"], "peak": fp64_peak, "unit": "TFLOP/s",
                                "frac": res[0]["tflops"] / fp64_peak, "traffic": None,
-                               "note": "fp64 step: blocked compact-WY LQ (panel kernels latency-bound, trailing "
-                                       "updates on FP64 DMMA) + backward GEMMs; algorithmic flops "
+                               "note": "fp64 step: CholeskyQR2 LQ on FP64 DMMA (G = A A^T, chol, inverse-GEMM "
+                                       "solve, twice; per-slice Householder fallback) + backward GEMMs; "
+                                       "algorithmic flops (Householder count, not the CholeskyQR2 work) "
                                        "4m^2n - 4m^3/3 + m^3/3 + 5m^2n per matrix (SURVEY 8d)"})
     if cfg == "c4":
         B, n = 1024, 64
