@@ -361,6 +361,36 @@ def run_potrf_batch(torch, n, B, steps, warmup, world):
     return ms
 
 
+def run_potrf_batch_split(torch, n, B, steps, warmup, world):
+    """The same potrf + potrf_backward through the C-ABI's fused split entry
+    points (dla_gp_potrf_inv_f64 + dla_potrf_bwd_end_f64, include/dla.h):
+    half of L^-1 forms during the factorization's chain-bound second half.
+    Outputs are bitwise those of the two operators (tests/test_gpu_gp.py)."""
+    import ctypes as C
+    from paper_1710_08717_b200._lib import lib as _lib
+    from oracle import oracle as O
+    lib = _lib().lib
+    r = O.rng(11)
+    a0 = torch.from_numpy(O.random_spd(n, r, batch=B)).cuda()
+    lb0 = torch.from_numpy(np.tril(r.standard_normal((B, n, n)))).cuda()
+    a = torch.empty_like(a0)
+    ab = torch.empty_like(a0)
+    info = torch.zeros(B, dtype=torch.int32, device="cuda")
+    nb = int(lib.dla_potrf_bwd_ws_bytes_f64(B, n))
+    ws = torch.empty(max(nb, 8), dtype=torch.uint8, device="cuda")
+    P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+
+    def step():
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        a.copy_(a0)
+        e1 = lib.dla_gp_potrf_inv_f64(B, n, P(a), P(info), P(ws), nb, st)
+        e2 = lib.dla_potrf_bwd_end_f64(B, n, P(ab), P(lb0), P(a), 1, P(ws), nb, st)
+        if e1 or e2:
+            raise RuntimeError(f"split potrf status {e1} {e2}")
+
+    return timed(torch, graphed(torch, step), steps, warmup, world)
+
+
 def also_measurements(torch, args, rank, world, lib, fp64_peak, hbm):
     out = []
     # C1 chain, batch 64 x 32^2 (latency regime) and a large-batch point:
@@ -403,11 +433,16 @@ def also_measurements(torch, args, rank, world, lib, fp64_peak, hbm):
         gf = world * flops / (ms / 1e3) / 1e9
         # HBM bytes per step: input copy (r + w), potrf (r A, w L), potrf_bwd (r L, r Lbar, w Abar)
         hbm_b = B * 7 * n * n * 8
-        out.append({"workload": f"potrf fwd+bwd, batch {B} x {n}^2 fp64 (incl. input copy)",
-                    "matrices_per_s": world * B / (ms / 1e3), "ms_per_step": ms, "gflops": gf,
-                    "frac_of_fp64_peak": gf / 1e3 / fp64_peak / world,
-                    "hbm_gb_per_s": hbm_b / (ms / 1e3) / 1e9, "frac_of_hbm": hbm_b / (ms / 1e3) / 1e9 / hbm,
-                    "bound": "hbm" if n <= 64 else "tensor"})
+        line = {"workload": f"potrf fwd+bwd, batch {B} x {n}^2 fp64 (incl. input copy)",
+                "matrices_per_s": world * B / (ms / 1e3), "ms_per_step": ms, "gflops": gf,
+                "frac_of_fp64_peak": gf / 1e3 / fp64_peak / world,
+                "hbm_gb_per_s": hbm_b / (ms / 1e3) / 1e9, "frac_of_hbm": hbm_b / (ms / 1e3) / 1e9 / hbm,
+                "bound": "hbm" if n <= 64 else "tensor"}
+        if n == 1024:  # the fused split entry points (same outputs): see bench_configs potrf1024
+            ms_s = run_potrf_batch_split(torch, n, B, 10, 3, world)
+            line["split_api"] = {"ms_per_step": ms_s, "matrices_per_s": world * B / (ms_s / 1e3),
+                                 "frac_of_fp64_peak": world * flops / (ms_s / 1e3) / 1e12 / fp64_peak / world}
+        out.append(line)
     return out
 
 

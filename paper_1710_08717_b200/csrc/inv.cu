@@ -384,10 +384,18 @@ dla_status potrf_bwd_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, M
   // to this (device, caller stream); the join runs even when a launch fails.
   ForkRes& fr = fork_res(FORK_BWDINV, c.stream);
   std::lock_guard<std::mutex> lk(fr.mu);
+  // the inverse is the longer, latency-bound branch (a chain of level
+  // launches) and gates W: its stream gets the high priority so P' fills in
+  // around it (DLA_BWDINV_PRIO=0: the low-priority side stream)
+  static const bool hi = [] {
+    const char* e = getenv("DLA_BWDINV_PRIO");
+    return e ? atoi(e) != 0 : true;
+  }();
+  cudaStream_t inv_stream = hi ? fr.crit : fr.side;
   Ctx sc = c;
-  sc.stream = fr.side;
+  sc.stream = inv_stream;
   cudaEventRecord(fr.ev[0], c.stream);
-  cudaStreamWaitEvent(fr.side, fr.ev[0], 0);
+  cudaStreamWaitEvent(inv_stream, fr.ev[0], 0);
   dla_status s1;
   if (N == n) {
     s1 = potrf_inv_prepare<T>(sc, batch, n, l, lower, wi, tmp);
@@ -401,7 +409,7 @@ dla_status potrf_bwd_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, M
     }
     if (s1 == DLA_OK) s1 = trtri_levels<T>(sc, batch, N, wi, tmp);
   }
-  cudaEventRecord(fr.ev[1], fr.side);
+  cudaEventRecord(fr.ev[1], inv_stream);
   const dla_status s2 = potrf_bwd_phi<T>(c, batch, n, lbar, l, lower, tt);
   cudaStreamWaitEvent(c.stream, fr.ev[1], 0);
   if (s1 != DLA_OK) return s1;
