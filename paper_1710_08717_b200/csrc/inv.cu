@@ -160,6 +160,183 @@ __global__ void __launch_bounds__(128) k_trtri64_dmma(int64_t nblk, MatB<double>
   }
 }
 
+// ---------------------------------------------------- n <= 128, fp64, fused
+// W = inv([L 0; 0 I]) of one matrix per CTA in ONE launch (256 threads, two
+// CTAs per SM): L's lower triangle as three 64 x 64 shared blocks
+// (A11, A21, A22; row stride 68 = 4 mod 16, so DMMA fragments load
+// conflict-free in both orientations); the 16 diagonal 8 x 8 inverses (one
+// column per thread), the s = 8, 16, 32 doubling levels of both diagonal
+// blocks together (T1 scratch in each block's unused upper-right quadrant),
+// then the top level A21 <- -A22^{-1} (A21 A11^{-1}) by row strips.  Replaces
+// tri_copy + k_trtri64_dmma + two level GEMMs (three HBM passes, three
+// launches) wherever a 128-wide level-batched inverse was formed.
+// LAUUM: instead of W, write B = W^T W (potri, dl/cholesky.hpp:141-147):
+// its lower tiles on DMMA, each value stored at (i, j) and (j, i) (exactly
+// symmetric).  FROM_UPPER: L(i, j) = src(j, i) (upper-stored factors).
+constexpr int TLD = 68;
+constexpr int TBLK = 64 * TLD;
+
+__device__ __forceinline__ double* t128(double* S, int i, int j) {
+  return i < 64 ? S + i * TLD + j : (j < 64 ? S + TBLK + (i - 64) * TLD + j : S + 2 * TBLK + (i - 64) * TLD + (j - 64));
+}
+
+template <bool FROM_UPPER, bool LAUUM>
+__global__ void __launch_bounds__(256, 2) k_trtri128(int n, int nout, MatB<const double> src, MatB<double> dst) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* S = reinterpret_cast<double*>(smem_raw);
+  double* S1 = S + TBLK;
+  double* S2 = S + 2 * TBLK;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, fr = lane >> 2, fc = lane & 3;
+  const int64_t b = blockIdx.x;
+  const double* g = src.p + b * src.bs;
+  const int64_t lds = src.ld;
+  // (1) load: row pairs, one column per thread; identity beyond n; the strict
+  // upper of the diagonal blocks zeroed (diagonal DMMA tiles read it)
+  {
+    const int j = tid & 127;
+#pragma unroll 4
+    for (int u0 = 0; u0 < 64; u0 += 16) {
+      double v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int i = 2 * (u0 + q) + (tid >> 7);
+        const bool in = i < n && j < n && (FROM_UPPER ? j >= i : j <= i);
+        v[q] = in ? g[i * lds + j] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int i = 2 * (u0 + q) + (tid >> 7);
+        const double pad = (i == j && i >= n) ? 1.0 : 0.0;
+        if (FROM_UPPER) {
+          if (j >= i) *t128(S, j, i) = (i < n && j < n) ? v[q] : pad;  // L(j, i) = src(i, j)
+          if (j > i && (i < 64) == (j < 64)) *t128(S, i, j) = 0.0;
+        } else {
+          if (j <= i) *t128(S, i, j) = (i < n && j < n) ? v[q] : pad;
+          else if ((i < 64) == (j < 64)) *t128(S, i, j) = 0.0;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // (2) 8 x 8 diagonal inverses: thread (block, column)
+  {
+    const int o8 = (tid >> 3) * 8, c = tid & 7;  // tid < 128
+    double x[8];
+    if (tid < 128) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        double acc = i == c ? 1.0 : 0.0;
+#pragma unroll
+        for (int q = 0; q < i; ++q)
+          if (q >= c) acc -= *t128(S, o8 + i, o8 + q) * x[q];
+        x[i] = i >= c ? acc / *t128(S, o8 + i, o8 + i) : 0.0;
+      }
+    }
+    __syncthreads();
+    if (tid < 128) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i >= c) *t128(S, o8 + i, o8 + c) = x[i];
+    }
+  }
+  __syncthreads();
+  // (3) doubling levels inside both diagonal blocks
+#pragma unroll
+  for (int s = 8; s < 64; s *= 2) {
+    const int pairs = 64 / (2 * s), tps = (s / 8) * (s / 8), per = pairs * tps;
+    for (int t = warp; t < 2 * per; t += 8) {  // T1 = B A^{-1}: k >= nt
+      double* blk = t < per ? S : S2;
+      const int tt = t % per, pr = tt / tps, r = tt % tps, rt = (r / (s / 8)) * 8, nt = (r % (s / 8)) * 8;
+      const int o = 2 * s * pr;
+      double d0 = 0.0, d1 = 0.0;
+      for (int kk = nt; kk < s; kk += 4)
+        dmma884(d0, d1, blk[(o + s + rt + fr) * TLD + o + kk + fc], blk[(o + kk + fc) * TLD + o + nt + fr]);
+      double* t1 = blk + (pr * s + rt + fr) * TLD + 32 + pr * s + nt + 2 * fc;
+      t1[0] = d0;
+      t1[1] = d1;
+    }
+    __syncthreads();
+    for (int t = warp; t < 2 * per; t += 8) {  // B = -C^{-1} T1: k <= rt + 7
+      double* blk = t < per ? S : S2;
+      const int tt = t % per, pr = tt / tps, r = tt % tps, rt = (r / (s / 8)) * 8, nt = (r % (s / 8)) * 8;
+      const int o = 2 * s * pr;
+      double d0 = 0.0, d1 = 0.0;
+      for (int kk = 0; kk < rt + 8; kk += 4)
+        dmma884(d0, d1, blk[(o + s + rt + fr) * TLD + o + s + kk + fc],
+                blk[(pr * s + kk + fc) * TLD + 32 + pr * s + nt + fr]);
+      double* bo = blk + (o + s + rt + fr) * TLD + o + nt + 2 * fc;
+      bo[0] = -d0;
+      bo[1] = -d1;
+    }
+    __syncthreads();
+  }
+  // (4) top level: A21 <- -A22^{-1} (A21 A11^{-1}); row strip 8 warp .. + 7 per warp
+  {
+    double acc[8][2];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = 0.0;
+#pragma unroll 4
+    for (int kk = 0; kk < 64; kk += 4) {  // T1 = A21 A11^{-1}: column tile nt needs k >= nt
+      const double af = S1[(8 * warp + fr) * TLD + kk + fc];
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        if (8 * t <= kk) dmma884(acc[t][0], acc[t][1], af, S[(kk + fc) * TLD + 8 * t + fr]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {  // in place: this strip of A21 is read by this warp only
+      S1[(8 * warp + fr) * TLD + 8 * t + 2 * fc] = acc[t][0];
+      S1[(8 * warp + fr) * TLD + 8 * t + 2 * fc + 1] = acc[t][1];
+      acc[t][0] = acc[t][1] = 0.0;
+    }
+    __syncthreads();
+    for (int kk = 0; kk < 8 * warp + 8; kk += 4) {  // -A22^{-1} T1: k <= row
+      const double af = S2[(8 * warp + fr) * TLD + kk + fc];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) dmma884(acc[t][0], acc[t][1], af, S1[(kk + fc) * TLD + 8 * t + fr]);
+    }
+    __syncthreads();  // every strip of T1 has been read
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      S1[(8 * warp + fr) * TLD + 8 * t + 2 * fc] = -acc[t][0];
+      S1[(8 * warp + fr) * TLD + 8 * t + 2 * fc + 1] = -acc[t][1];
+    }
+  }
+  __syncthreads();
+  double* o = dst.p + b * dst.bs;
+  const int64_t ldo = dst.ld;
+  if constexpr (!LAUUM) {
+    const int j = tid & 127;
+    if (j < nout) {
+#pragma unroll 8
+      for (int u = 0; u < 64; ++u) {
+        const int i = 2 * u + (tid >> 7);
+        if (i < nout) o[i * ldo + j] = j <= i ? *t128(S, i, j) : 0.0;
+      }
+    }
+  } else {
+    // (5) B = W^T W: lower 8 x 8 tiles (I >= J), k >= 8 I; stored mirrored
+    for (int t = warp; t < 136; t += 8) {
+      int I = 0;
+      while ((I + 1) * (I + 2) / 2 <= t) ++I;
+      const int J = t - I * (I + 1) / 2;
+      double d0 = 0.0, d1 = 0.0;
+      for (int kk = 8 * I; kk < 128; kk += 4)
+        dmma884(d0, d1, *t128(S, kk + fc, 8 * I + fr), *t128(S, kk + fc, 8 * J + fr));
+      const int i = 8 * I + fr;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = 8 * J + 2 * fc + e;
+        const double v = e ? d1 : d0;
+        if (i >= j && i < nout && j < nout) {
+          o[i * ldo + j] = v;
+          o[j * ldo + i] = v;
+        }
+      }
+    }
+  }
+}
+
 // The padding of the inverse's operand (see inv_pad): rows < n get zeros in
 // columns [n, N), rows >= n the identity row.
 template <typename T>
@@ -286,6 +463,41 @@ dla_status trtri_levels(const Ctx& c, int64_t batch, int64_t n, MatB<T> w, T* tm
   return DLA_OK;
 }
 
+// fp64 128-wide inverse (or potri) in one launch: dst = lower-form
+// inv([L 0; 0 I]) over nout x nout, L read from src's lower (or, from_upper,
+// transposed upper) triangle, n <= 128.
+template <typename T>
+MatB<const double> as_d(MatB<const T> m) {
+  return MatB<const double>{reinterpret_cast<const double*>(m.p), m.ld, m.bs, m.bsi};
+}
+template <typename T>
+MatB<double> as_d(MatB<T> m) {
+  return MatB<double>{reinterpret_cast<double*>(m.p), m.ld, m.bs, m.bsi};
+}
+inline dla_status trtri128(const Ctx& c, int64_t batch, int n, int nout, MatB<const double> src, bool from_upper,
+                           MatB<double> dst, bool lauum) {
+  const size_t sm = sizeof(double) * 3 * TBLK;
+  auto go = [&](auto kern) {
+    ensure_smem_attr(kern, sm);
+    kern<<<(unsigned)batch, 256, sm, c.stream>>>(n, nout, src, dst);
+  };
+  if (lauum)
+    from_upper ? go(k_trtri128<true, true>) : go(k_trtri128<false, true>);
+  else
+    from_upper ? go(k_trtri128<true, false>) : go(k_trtri128<false, false>);
+  DLAB_LAUNCH_CHECK();
+  return DLA_OK;
+}
+// The 128 fused path applies (fp64, batched slices of 128 x 128).
+template <typename T>
+bool use_trtri128(int64_t n) {
+  static const bool on = [] {
+    const char* e = getenv("DLA_TRTRI128");  // tuning switch: 0 = tri_copy + level-batched launches
+    return e ? atoi(e) != 0 : true;
+  }();
+  return sizeof(T) == 8 && n == 128 && on;
+}
+
 template <typename T>
 dla_status trsm_inv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x, bool right,
                     bool trans, bool lower, T alpha) {
@@ -296,8 +508,12 @@ dla_status trsm_inv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<cons
   MatB<T> y{wp + batch * nt * nt, n, m * n};
   T* tmp = wp + batch * (nt * nt + m * n);
   // lower-form W: inv(T) for lower T, inv(T^T) = T^{-T} for upper T
-  DLAB_TRY(ew_tri_copy<T>(c, batch, nt, t, w, !lower));
-  DLAB_TRY(trtri_levels<T>(c, batch, nt, w, tmp));
+  if (use_trtri128<T>(nt)) {
+    DLAB_TRY(trtri128(c, batch, 128, 128, as_d(t), !lower, as_d(w), false));
+  } else {
+    DLAB_TRY(ew_tri_copy<T>(c, batch, nt, t, w, !lower));
+    DLAB_TRY(trtri_levels<T>(c, batch, nt, w, tmp));
+  }
   const bool eff = (lower != trans);  // op(T)^{-1} = eff ? W : W^T
   const int tri = eff ? TRI_LOWER : TRI_UPPER;
   if (sizeof(T) == 8 && !right && m <= 128) {
@@ -318,6 +534,7 @@ dla_status trsm_inv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<cons
 // per slice: the first half of potrf_bwd_inv, callable ahead of time.
 template <typename T>
 dla_status potrf_inv_prepare(const Ctx& c, int64_t batch, int64_t n, MatB<const T> l, bool lower, MatB<T> wi, T* tmp) {
+  if (use_trtri128<T>(n)) return trtri128(c, batch, 128, 128, as_d(l), !lower, as_d(wi), false);
   DLAB_TRY(ew_tri_copy<T>(c, batch, n, l, wi, !lower));
   return trtri_levels<T>(c, batch, n, wi, tmp);
 }
@@ -399,6 +616,8 @@ dla_status potrf_bwd_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, M
   dla_status s1;
   if (N == n) {
     s1 = potrf_inv_prepare<T>(sc, batch, n, l, lower, wi, tmp);
+  } else if (use_trtri128<T>(N)) {  // 64 < n < 128: the padded inverse in one launch
+    s1 = trtri128(sc, batch, (int)n, 128, as_d(l), !lower, as_d(wi), false);
   } else {
     s1 = ew_tri_copy<T>(sc, batch, n, l, wi, !lower);
     if (s1 == DLA_OK) {
@@ -442,11 +661,19 @@ dla_status trmm_gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<con
   return ew_copy<T>(c, batch, m, n, C_(y), x, c.info);
 }
 
+// potri of 64 < n <= 128 (fp64) as one fused launch (k_trtri128<., LAUUM>)
+template <typename T>
+bool potri_fused_eligible(int64_t n) {
+  return n > 64 && n <= 128 && use_trtri128<T>(128);
+}
+
 // potri (lower) via the level-batched inverse: W = L^{-1}, B = W^T W on the
 // lower triangle, mirrored exactly (dl/cholesky.hpp:141-147).  The caller has
 // checked the diagonal for exact zeros.
 template <typename T>
 dla_status potri_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
+  if (potri_fused_eligible<T>(n))  // one launch, in place
+    return trtri128(c, batch, (int)n, (int)n, as_d(MatB<const T>{a.p, a.ld, a.bs, a.bsi}), false, as_d(a), true);
   DLAB_SCRATCH(ws, c, potri_inv_scratch<T>(batch, n));
   MatB<T> b{ws.as<T>(), n, n * n};
   T* tmp = ws.as<T>() + batch * n * n;
@@ -461,6 +688,7 @@ dla_status potri_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
   template dla_status trmm_gemm<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<const T>, MatB<T>, bool, bool, \
                                    bool, T);                                                                 \
   template dla_status potri_inv<T>(const Ctx&, int64_t, int64_t, MatB<T>);                                   \
+  template bool potri_fused_eligible<T>(int64_t);                                                            \
   template bool inv_eligible<T>(int64_t);                                                                    \
   template int64_t inv_pad<T>(int64_t);                                                                      \
   template size_t trtri_levels_tmp<T>(int64_t);                                                              \

@@ -1068,7 +1068,7 @@ dla_status potri_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
   if (batch == 0 || n == 0) return DLA_OK;
   ensure_smem_attr(k_potrf_leaf<T>, sizeof(T) * NB * CH_LD);
   ensure_smem_attr(k_lauum_leaf<T>, sizeof(T) * NB * LDS);
-  if (inv_eligible<T>(n)) return potri_inv<T>(c, batch, n, a);
+  if (inv_eligible<T>(n) || potri_fused_eligible<T>(n)) return potri_inv<T>(c, batch, n, a);
   DLAB_TRY(trtri_rec<T>(c, batch, n, a));
   DLAB_TRY(lauum_rec<T>(c, batch, n, a));
   return ew_square<T>(c, batch, n, a, /*copyltu*/ 2, T(1), c.info);
@@ -1174,6 +1174,7 @@ template <typename T>
 size_t ws_potri_lower(int64_t batch, int64_t n) {
   if (batch == 0 || n == 0) return 0;
   if (inv_eligible<T>(n)) return ws_potri_inv<T>(batch, n);
+  if (potri_fused_eligible<T>(n)) return 0;  // the fused one-launch potri (inv.cu)
   return ws_trtri_rec<T>(batch, n) + ws_lauum_rec<T>(batch, n);
 }
 

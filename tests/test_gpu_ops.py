@@ -417,7 +417,7 @@ def test_potrf_warp_batches(port, dt):
 def test_potri(port, dt):
     r = O.rng(9)
     B = 2
-    for n in [1, 2, 3, 8, 20, 64, 65, 100, 129]:
+    for n in [1, 2, 3, 8, 20, 64, 65, 96, 100, 128, 129]:  # 65-128 f64: one fused launch
         a = O.random_spd(n, r, dt, batch=B)
         for lower in (1, 0):
             l = batch_apply(lambda x: port.potrf(x, lower), a)
