@@ -311,6 +311,16 @@ dla_status trmm_bwd(const Ctx& cx, int64_t batch, int64_t m, int64_t n, T* abar,
   else if (right && !trans) DLAB_TRY(gemm<T>(cx, batch, n, n, m, alpha, X(a), true, X(bbar), false, T(0), tb, mask));
   else DLAB_TRY(gemm<T>(cx, batch, n, n, m, alpha, X(bbar), true, X(a), false, T(0), tb, mask));
   DLAB_TRY(ew_square<T>(cx, batch, nt, tb, lower ? 0 : 1));
+  if (abar != bbar && nt >= 128) {
+    // Abar = alpha op(T)^T Bbar (or Bbar op(T)^T) as ONE triangular GEMM from
+    // Bbar into Abar: no copy pass, no in-place tile constraint
+    const int tri = (lower != !trans) ? TRI_LOWER : TRI_UPPER;  // of op(T) with trans flipped
+    if (!right)
+      return gemm<T>(cx, batch, m, n, m, alpha, cpk(t, nt, nt), !trans, X(bbar), false, T(0), pk(abar, m, n),
+                     MASK_FULL, cx.info, tri, TRI_NONE);
+    return gemm<T>(cx, batch, m, n, n, alpha, X(bbar), false, cpk(t, nt, nt), !trans, T(0), pk(abar, m, n), MASK_FULL,
+                   cx.info, TRI_NONE, tri);
+  }
   DLAB_TRY(ew_copy<T>(cx, batch, m, n, cpk(bbar, m, n), pk(abar, m, n)));
   return trmm<T>(cx, batch, m, n, cpk(t, nt, nt), pk(abar, m, n), right, !trans, lower, alpha);
 }
@@ -431,6 +441,8 @@ dla_status potri_fwd(const Ctx& cx, int64_t batch, int64_t n, T* a, int lower) {
 
 template <typename T>
 size_t ws_potri_bwd(int64_t batch, int64_t n, int lower) {
+  if (lower && inv_eligible<T>(n))
+    return 2 * carve_bound(bytes<T>(batch, n, n)) + ws_gemm<T>(batch, n, n, n) + ws_trsm_inv_from<T>(batch, n, n, true);
   return carve_bound(bytes<T>(batch, n, n)) + ws_gemm<T>(batch, n, n, n) + ws_trsm<T>(batch, n, n, lower != 0);
 }
 
@@ -449,6 +461,15 @@ dla_status potri_bwd(const Ctx& cx, int64_t batch, int64_t n, T* lbar, const T* 
   DLAB_SCRATCH(ws, cx, bytes<T>(batch, n, n));
   MatB<T> sb = pk(ws.as<T>(), n, n);
   DLAB_TRY(ew_add_transpose<T>(cx, batch, n, bb, sb));
+  if (lower && inv_eligible<T>(n)) {
+    // the right solve by the explicit inverse straight from P = B (Bbar +
+    // Bbar^T) into Lbar: P in scratch, one GEMM, no copy back
+    DLAB_SCRATCH(ps, cx, bytes<T>(batch, n, n));
+    MatB<T> pb = pk(ps.as<T>(), n, n);
+    DLAB_TRY(gemm<T>(cx, batch, n, n, n, T(1), bv, false, C_(sb), false, T(0), pb));
+    DLAB_TRY(trsm_inv_from<T>(cx, batch, n, n, lv, C_(pb), lb, true, true, true, T(-1)));
+    return ew_square<T>(cx, batch, n, lb, /*tril*/ 0);
+  }
   if (lower) {  // dl/adjoints.hpp:211-215
     DLAB_TRY(gemm<T>(cx, batch, n, n, n, T(1), bv, false, C_(sb), false, T(0), lb));
     DLAB_TRY(trsm<T>(cx, batch, n, n, lv, lb, true, true, true, T(-1)));

@@ -530,6 +530,36 @@ dla_status trsm_inv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<cons
   return ew_copy<T>(c, batch, m, n, C_(y), x, c.info);
 }
 
+// Out-of-place trsm_inv: X = alpha op(T)^{-1} S (left) or alpha S op(T)^{-1}
+// (right) as one triangular GEMM from S into X (S != X): no y scratch, no
+// copy back.
+template <typename T>
+size_t ws_trsm_inv_from(int64_t batch, int64_t m, int64_t n, bool right) {
+  const int64_t nt = right ? n : m;
+  return carve_bound(sizeof(T) * (size_t)batch * (size_t)nt * nt + (size_t)batch * trtri_levels_tmp<T>(nt)) +
+         ws_trtri_levels<T>(batch, nt) + ws_gemm<T>(batch, m, n, nt);
+}
+template <typename T>
+dla_status trsm_inv_from(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<const T> src,
+                         MatB<T> x, bool right, bool trans, bool lower, T alpha) {
+  const int64_t nt = right ? n : m;
+  DLAB_SCRATCH(ws, c, sizeof(T) * (size_t)batch * (size_t)nt * nt + (size_t)batch * trtri_levels_tmp<T>(nt));
+  T* wp = ws.as<T>();
+  MatB<T> w{wp, nt, nt * nt};
+  T* tmp = wp + batch * nt * nt;
+  if (use_trtri128<T>(nt)) {
+    DLAB_TRY(trtri128(c, batch, 128, 128, as_d(t), !lower, as_d(w), false));
+  } else {
+    DLAB_TRY(ew_tri_copy<T>(c, batch, nt, t, w, !lower));
+    DLAB_TRY(trtri_levels<T>(c, batch, nt, w, tmp));
+  }
+  const bool eff = (lower != trans);
+  const int tri = eff ? TRI_LOWER : TRI_UPPER;
+  if (!right)
+    return gemm<T>(c, batch, m, n, m, alpha, C_(w), !eff, src, false, T(0), x, MASK_FULL, c.info, tri, TRI_NONE);
+  return gemm<T>(c, batch, m, n, n, alpha, src, false, C_(w), !eff, T(0), x, MASK_FULL, c.info, TRI_NONE, tri);
+}
+
 // L^{-1} (lower form) of the factor into wi, with tmp >= trtri_levels_tmp(n)
 // per slice: the first half of potrf_bwd_inv, callable ahead of time.
 template <typename T>
@@ -688,6 +718,9 @@ dla_status potri_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
   template dla_status trmm_gemm<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<const T>, MatB<T>, bool, bool, \
                                    bool, T);                                                                 \
   template dla_status potri_inv<T>(const Ctx&, int64_t, int64_t, MatB<T>);                                   \
+  template size_t ws_trsm_inv_from<T>(int64_t, int64_t, int64_t, bool);                                      \
+  template dla_status trsm_inv_from<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<const T>, MatB<const T>,  \
+                                       MatB<T>, bool, bool, bool, T);                                        \
   template bool potri_fused_eligible<T>(int64_t);                                                            \
   template bool inv_eligible<T>(int64_t);                                                                    \
   template int64_t inv_pad<T>(int64_t);                                                                      \

@@ -28,6 +28,11 @@ bool inv_eligible(int64_t n);
 template <typename T>
 int64_t inv_pad(int64_t n);
 template <typename T>
+dla_status trsm_inv_from(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<const T> src,
+                         MatB<T> x, bool right, bool trans, bool lower, T alpha);
+template <typename T>
+size_t ws_trsm_inv_from(int64_t batch, int64_t m, int64_t n, bool right);
+template <typename T>
 bool potri_fused_eligible(int64_t n);
 template <typename T>
 dla_status trsm_inv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x, bool right,
