@@ -533,11 +533,15 @@ __device__ __forceinline__ void warp_potrf_bwd_dmma(int n, int lane, double* Lm,
       }
     }
     __syncwarp();
+    // Y into G and Y^T into Lm (L^-1 is dead): the symmetrisation below then
+    // reads rows of both (a column read of Y would be a 4-way bank conflict)
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
       const int i = 8 * (t / 4) + fr, j = 8 * (t % 4) + 2 * fc;
       G[i * DLD + j] = y[t][0];
       G[i * DLD + j + 1] = y[t][1];
+      Lm[j * DLD + i] = y[t][0];
+      Lm[(j + 1) * DLD + i] = y[t][1];
     }
   }
   __syncwarp();
@@ -546,7 +550,7 @@ __device__ __forceinline__ void warp_potrf_bwd_dmma(int n, int lane, double* Lm,
 #pragma unroll 8
     for (int i = 0; i < WN; ++i) {
       if (i < n) {
-        const double hi = G[i * DLD + lane] * 0.5, hj = G[lane * DLD + i] * 0.5;
+        const double hi = G[i * DLD + lane] * 0.5, hj = Lm[i * DLD + lane] * 0.5;
         o[i * ldo + lane] = (i == lane) ? hi : (hi + hj) * 0.5;
       }
     }
