@@ -120,6 +120,13 @@ void gemm_prof_begin(cudaStream_t s) {
   cudaEventRecord(t_pending, s);
 }
 
+void gemm_prof_cancel() {  // a begin whose launch did not happen
+  if (!t_pending) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_event_pool.push_back(t_pending);
+  t_pending = nullptr;
+}
+
 void gemm_prof_end(cudaStream_t s, double flops) {
   cudaEvent_t e = take_event();
   cudaEventRecord(e, s);

@@ -132,6 +132,7 @@ void note_launch(int k = 1);
 bool gemm_prof_on();
 void gemm_prof_begin(cudaStream_t s);
 void gemm_prof_end(cudaStream_t s, double flops);
+void gemm_prof_cancel();
 
 // Scratch carved from the call's workspace arena; `ok` is false when the
 // caller's workspace is missing or too small (the op returns

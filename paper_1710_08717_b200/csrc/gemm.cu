@@ -23,6 +23,7 @@
 // and the contiguous extent allow, 8/4-byte otherwise, so every shape works.
 // Batch and tiles share a flat grid.x (65536-slice batches exceed gridDim.z).
 #include "common.cuh"
+#include "ops.cuh"
 #include <algorithm>
 
 #ifndef DLAB_GEMM_BKL
@@ -644,6 +645,18 @@ dla_status gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T 
         if (prof) gemm_prof_end(c.stream, useful_flops(m, n, k, mask, tri_a, tri_b) * (double)batch);
         return st;
       }
+    }
+  }
+  if constexpr (sizeof(T) == 8) {  // large products: the TMA-fed persistent kernel (gemm_tma.cu)
+    if (!rowtile && c.gemm_ctas <= 0) {
+      dla_status st;
+      const bool prof = gemm_prof_on();
+      if (prof) gemm_prof_begin(c.stream);
+      if (gemm_tma(c, batch, m, n, k, alpha, a, ta, b, tb, beta, cm, mask, skip, tri_a, tri_b, inner, &st)) {
+        if (prof) gemm_prof_end(c.stream, useful_flops(m, n, k, mask, tri_a, tri_b) * (double)batch);
+        return st;
+      }
+      if (prof) gemm_prof_cancel();
     }
   }
   GemmArgs<T> g{m, n, k, alpha, beta, a, b, cm, mask, skip, 0, 0, tri_a, tri_b, inner, 0};

@@ -117,6 +117,10 @@ bool potrf_tiles_eligible(int64_t batch, int64_t n, const MatB<double>& a);
 dla_status potrf_tiles(const Ctx& c, int64_t batch, int64_t n, MatB<double> a, int64_t kbase);
 size_t ws_potrf_tiles(int64_t batch, int64_t n);
 
+// gemm_tma.cu: TMA-fed persistent fp64 GEMM for large products (false = not taken)
+bool gemm_tma(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, double alpha, MatB<const double> a,
+              bool ta, MatB<const double> b, bool tb, double beta, MatB<double> cm, int mask, const int32_t* skip,
+              int tri_a, int tri_b, int64_t inner, dla_status* st);
 // syrk_tma.cu: TMA-fed persistent trailing update C[lower] = alpha P P^T + beta C (f64)
 bool syrk_tma_eligible(int64_t m, int64_t k, const MatB<const double>& p, const MatB<double>& c, int64_t batch);
 dla_status syrk_tma(const Ctx& c, int64_t batch, int64_t m, int64_t k, double alpha, MatB<const double> p, double beta,
