@@ -11,7 +11,10 @@ bool potrf_small_eligible(int64_t n);
 template <typename T>
 bool potrf_fwd_small_eligible(int64_t n);
 template <typename T>
-dla_status potrf_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool lower);
+// check_sym: the public op's symmetry precheck (dl/cholesky.hpp:19-25); internal
+// callers that factor a lower triangle (strict upper unspecified) pass false
+// (honoured by the 64 < n <= 128 kernel; the smaller ones are public-op only).
+dla_status potrf_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool lower, bool check_sym = true);
 template <typename T>
 dla_status potrf_bwd_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, MatB<const T> lbar,
                            MatB<const T> l, bool lower);

@@ -851,7 +851,8 @@ constexpr int P2 = 128;
 constexpr int P2LD = 65;
 __device__ __forceinline__ int kcol16(int s, int fc) { return ((s & ~3) << 2) + 4 * fc + (s & 3); }
 template <int MINB>
-__global__ void __launch_bounds__(256, MINB) k_potrf128(int n, MatB<double> a, bool lower, int32_t* info) {
+__global__ void __launch_bounds__(256, MINB) k_potrf128(int n, MatB<double> a, bool lower, int32_t* info,
+                                                        bool check_sym) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* S11 = reinterpret_cast<double*>(smem_raw);
   double* V = S11 + 64 * P2LD;
@@ -876,7 +877,7 @@ __global__ void __launch_bounds__(256, MINB) k_potrf128(int n, MatB<double> a, b
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       const int i = 2 * (16 * c + q) + (tid >> 7);
-      v[q] = (i < n && j < n) ? g[i * ld + j] : 0.0;
+      v[q] = (i < n && j < n && (check_sym || j <= i)) ? g[i * ld + j] : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
@@ -888,7 +889,7 @@ __global__ void __launch_bounds__(256, MINB) k_potrf128(int n, MatB<double> a, b
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       const int i = 2 * (16 * c + q) + (tid >> 7);
-      if (j > i && j < n) {
+      if (check_sym && j > i && j < n) {
         const double d = fabs(v[q] - *sm(j, i));
         if (d > masym) masym = d;
       }
@@ -962,7 +963,7 @@ bool potrf_fwd_small_eligible(int64_t n) {
 }
 
 template <typename T>
-dla_status potrf_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool lower) {
+dla_status potrf_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool lower, bool check_sym) {
   if (n <= WN) {
     constexpr int wpc = wpc_fwd<T>();
     const size_t sm = sizeof(T) * wpc * (WN * WLD + 2 * WN + 4);
@@ -992,10 +993,10 @@ dla_status potrf_small(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool l
       MatB<double> ad{reinterpret_cast<double*>(a.p), a.ld, a.bs, a.bsi};
       if (minb == 1) {
         ensure_smem_attr(k_potrf128<1>, sm);
-        k_potrf128<1><<<(unsigned)batch, 256, sm, c.stream>>>((int)n, ad, lower, c.info);
+        k_potrf128<1><<<(unsigned)batch, 256, sm, c.stream>>>((int)n, ad, lower, c.info, check_sym);
       } else {
         ensure_smem_attr(k_potrf128<2>, sm);
-        k_potrf128<2><<<(unsigned)batch, 256, sm, c.stream>>>((int)n, ad, lower, c.info);
+        k_potrf128<2><<<(unsigned)batch, 256, sm, c.stream>>>((int)n, ad, lower, c.info, check_sym);
       }
       DLAB_LAUNCH_CHECK();
     }
@@ -1088,7 +1089,7 @@ dla_status chol_chain_small(const Ctx& c, int64_t batch, int64_t n, MatB<const T
 #define INST(T)                                                                                     \
   template bool potrf_small_eligible<T>(int64_t);                                                   \
   template bool potrf_fwd_small_eligible<T>(int64_t);                                               \
-  template dla_status potrf_small<T>(const Ctx&, int64_t, int64_t, MatB<T>, bool);                  \
+  template dla_status potrf_small<T>(const Ctx&, int64_t, int64_t, MatB<T>, bool, bool);            \
   template dla_status potrf_bwd_small<T>(const Ctx&, int64_t, int64_t, MatB<T>, MatB<const T>, MatB<const T>, bool); \
   template dla_status chol_chain_small<T>(const Ctx&, int64_t, int64_t, MatB<const T>, const T*, T*, MatB<T>, T*);
 INST(double)

@@ -1044,6 +1044,9 @@ dla_status potrf_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool z
   ensure_smem_attr(k_potrf_leaf<T>, sizeof(T) * NB * CH_LD);
   ensure_smem_attr(k_lauum_leaf<T>, sizeof(T) * NB * LDS);
   const int mode = potrf_mode();
+  if constexpr (sizeof(T) == 8) {  // 64 < n <= 128: the one-launch CTA-per-matrix kernel (small.cu)
+    if (mode == 0 && n > 64 && n <= 128 && potrf_fwd_small_eligible<T>(n)) return potrf_small<T>(c, batch, n, a, true, /*check_sym*/ false);
+  }
   // default: blocked right-looking with look-ahead (measured faster than the
   // recursive split at every n > 64 on B200, and still ~3% ahead of the
   // persistent tile-dataflow kernel at n = 1024 / 4096, whose per-column
