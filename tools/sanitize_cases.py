@@ -37,6 +37,9 @@ L.gemm2(v, v, False, True)
 L.syrk(torch.randn(2, 300, 40, **f))
 L.gelqf(torch.randn(2, 128, 512, **f))
 L.gesvd(torch.randn(2, 40, 60, **f))
+# a plain product with >= 2 waves of 128 x 128 tiles: the TMA-fed GEMM (run the
+# whole script with DLA_GEMM_TMA=2 to put every product >= 256 on it)
+L.gemm2(torch.randn(1, 2560, 300, **f), torch.randn(1, 300, 2560, **f))
 torch.cuda.synchronize()
 torch.cuda.synchronize()
 print("sanitize cases done")
