@@ -191,7 +191,11 @@ def graphed(torch, fn):
     torch.cuda.current_stream().wait_stream(s)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
+    # capture on a high-priority stream (DLA_BENCH_PRIO=0: default priority) -- the step's own
+    # chain then outranks the library's low-priority side streams)
+    prio = os.environ.get("DLA_BENCH_PRIO", "1") != "0"
+    cap = torch.cuda.Stream(priority=-1) if prio else None
+    with torch.cuda.graph(g, stream=cap):
         fn()
     torch.cuda.synchronize()
     return g.replay

@@ -194,6 +194,15 @@ struct Num<double> {
     e = fma(-x, y * y, 1.0);
     return fma(0.5 * y, e, y);
   }
+  // Branch-free 1/x: MUFU.RCP64H seed + two Newton steps (finite nonzero x)
+  __device__ static double rcp_(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+  }
   static constexpr double sym_rtol = 1e-10;
   static constexpr double rank_rtol = 1e-12;
 };
@@ -205,6 +214,7 @@ struct Num<float> {
     const float y = rsqrtf(x);
     return fmaf(0.5f * y, fmaf(-x, y * y, 1.0f), y);
   }
+  __device__ static float rcp_(float x) { return 1.0f / x; }
   static constexpr float sym_rtol = 1e-4f;
   static constexpr float rank_rtol = 1e-5f;
 };

@@ -379,11 +379,18 @@ __global__ void __launch_bounds__(ET, 4) k_syevd_small(int n, T* uall, T* lamall
         if (q < n) {
           const T apq = A[pidx(p, q)];
           if (apq != T(0)) {
-            const T theta = (A[pidx(q, q)] - A[pidx(p, p)]) / (T(2) * apq);
+            // the rotation on the round's serial chain with MUFU-seeded
+            // reciprocal / reciprocal-sqrt (two Newton steps each, ~1 ulp)
+            // instead of IEEE divide / sqrt sequences
+            const T theta = (A[pidx(q, q)] - A[pidx(p, p)]) * Num<T>::rcp_(T(2) * apq);
             T t;
-            if (fabs(theta) > (sizeof(T) == 8 ? T(1e150) : T(1e15))) t = T(0.5) / theta;
-            else t = (theta >= T(0) ? T(1) : T(-1)) / (fabs(theta) + sqrt(theta * theta + T(1)));
-            c = T(1) / sqrt(t * t + T(1));
+            if (fabs(theta) > (sizeof(T) == 8 ? T(1e150) : T(1e15))) {
+              t = T(0.5) * Num<T>::rcp_(theta);
+            } else {
+              const T r2 = theta * theta + T(1);
+              t = (theta >= T(0) ? T(1) : T(-1)) * Num<T>::rcp_(fabs(theta) + r2 * Num<T>::rsqrt_(r2));
+            }
+            c = Num<T>::rsqrt_(t * t + T(1));
             sn = t * c;
           }
         }
