@@ -150,6 +150,11 @@ dla_status dla_info_check(const int32_t* info, int64_t batch, void* stream,
   dla_status dla_trmm_fwd_##S(int64_t batch, int64_t m, int64_t n, const T* t,      \
                               T* x, int rightside, int transpose, int lower,        \
                               T alpha, void* ws, size_t ws_bytes, void* stream);                               \
+  /* trmm out of place: y = alpha op(T) x / alpha x op(T); x, t unchanged, y may  \
+     alias neither; same workspace as dla_trmm_fwd. */                              \
+  dla_status dla_trmm_into_##S(int64_t batch, int64_t m, int64_t n, const T* t,     \
+                               const T* x, T* y, int rightside, int transpose,      \
+                               int lower, T alpha, void* ws, size_t ws_bytes, void* stream);                   \
   /* trmm pullback (reads the forward INPUT a); abar may alias bbar;                \
      dl/adjoints.hpp:94-110. */                                                     \
   dla_status dla_trmm_bwd_##S(int64_t batch, int64_t m, int64_t n, T* abar,         \
@@ -180,6 +185,10 @@ dla_status dla_info_check(const int32_t* info, int64_t batch, void* stream,
      zero diagonal => SINGULAR(j); dl/cholesky.hpp:141-147. */                      \
   dla_status dla_potri_fwd_##S(int64_t batch, int64_t n, T* a, int lower,           \
                                int32_t* info, void* ws, size_t ws_bytes, void* stream);                        \
+  /* potri out of place: b = inv(L L^T) from the factor l (unchanged); same info  \
+     and workspace as the in-place potri; fp64 64 < n <= 128: one fused launch */ \
+  dla_status dla_potri_into_##S(int64_t batch, int64_t n, const T* l, T* b,         \
+                                int lower, int32_t* info, void* ws, size_t ws_bytes, void* stream);            \
   /* potri pullback: Lbar = -tril((B Bbar + B Bbar^T) L^-T); dl/adjoints.hpp:207. */\
   dla_status dla_potri_bwd_##S(int64_t batch, int64_t n, T* lbar, const T* bbar,    \
                                const T* l, const T* b, int lower, void* ws, size_t ws_bytes, void* stream);    \

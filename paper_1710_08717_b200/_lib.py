@@ -32,12 +32,14 @@ _SIGS = {
     "syrk_fwd": "IIIPPFSPZP",
     "syrk_bwd": "IIIPPPFSPZP",
     "trmm_fwd": "IIIPPFFFSPZP",
+    "trmm_into": "IIIPPPFFFSPZP",
     "trmm_bwd": "IIIPPPPPFFFSPZP",
     "trsm_fwd": "IIIPPFFFSPPZP",
     "trsm_bwd": "IIIPPPPPFFFSPZP",
     "potrf_fwd": "IIPFPPZP",
     "potrf_bwd": "IIPPPFPZP",
     "potri_fwd": "IIPFPPZP",
+    "potri_into": "IIPPFPPZP",
     "potri_bwd": "IIPPPPFPZP",
     "sumlogdiag_fwd": "IIPPPZP",
     "sumlogdiag_bwd": "IIPPPFPZP",

@@ -67,10 +67,8 @@ class MarginalLikelihoods:
         # forward: every kernel below is libdla_b200's (copies included)
         self._ok(lib_.dla_ml_shift_copy_f64(B, n, P(s), P(self.l), lam, self._st()))  # A = S + lam I
         L.potrf_inplace(self.l, True, check=False, info=self.info)
-        self._ok(lib_.dla_ml_shift_copy_f64(B, n, P(self.l), P(self.b), 0.0, self._st()))
-        L.potri_inplace(self.b, True, check=False)
-        self._ok(lib_.dla_ml_shift_copy_f64(B, n, P(self.b), P(self.g), 0.0, self._st()))
-        L.trmm_inplace(self.l, self.g, False, True, True)
+        L.potri_into(self.b, self.l, True, check=False)   # out of place: no copy of L
+        L.trmm_into(self.g, self.l, self.b, False, True, True)  # G = L^T B, out of place
         L.gemm2_into(self.v, self.g, y)
         L.gemm2_into(self.quad, self.v, self.v, True, False, 0.5)
         L.sumlogdiag(self.l, out=self.logdet)

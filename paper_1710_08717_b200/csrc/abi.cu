@@ -281,6 +281,30 @@ dla_status trmm_fwd(const Ctx& cx, int64_t batch, int64_t m, int64_t n, const T*
   return trmm<T>(cx, batch, m, n, cpk(t, nt, nt), pk(x, m, n), right, trans, lower, alpha);
 }
 
+// Out-of-place trmm: y = alpha op(T) x / alpha x op(T), x and t unchanged (the
+// reference's functional trmm, dl/blas.hpp:202-291).  For nt >= 128 one
+// triangular GEMM from x into y (no copy, no in-place tile constraint);
+// otherwise a copy and the in-place operator.
+template <typename T>
+dla_status trmm_into(const Ctx& cx, int64_t batch, int64_t m, int64_t n, const T* t, const T* x, T* y, int right,
+                     int trans, int lower, T alpha) {
+  if (bad_dims(batch, m, n)) return DLA_ERR_SHAPE;
+  const int64_t nt = right ? n : m;
+  const size_t ysz = bytes<T>(batch, m, n);
+  if (overlap(y, ysz, t, bytes<T>(batch, nt, nt)) || overlap(y, ysz, x, ysz)) return DLA_ERR_ALIAS;
+  if (batch * m * n == 0) return DLA_OK;
+  if (nt >= 128) {
+    const int tri = (lower != trans) ? TRI_LOWER : TRI_UPPER;  // of op(T)
+    if (!right)
+      return gemm<T>(cx, batch, m, n, m, alpha, cpk(t, nt, nt), trans != 0, cpk(x, m, n), false, T(0), pk(y, m, n),
+                     MASK_FULL, nullptr, tri, TRI_NONE);
+    return gemm<T>(cx, batch, m, n, n, alpha, cpk(x, m, n), false, cpk(t, nt, nt), trans != 0, T(0), pk(y, m, n),
+                   MASK_FULL, nullptr, TRI_NONE, tri);
+  }
+  DLAB_TRY(ew_copy<T>(cx, batch, m, n, cpk(x, m, n), pk(y, m, n)));
+  return trmm<T>(cx, batch, m, n, cpk(t, nt, nt), pk(y, m, n), right, trans, lower, alpha);
+}
+
 template <typename T>
 dla_status trsm_fwd(const Ctx& cx, int64_t batch, int64_t m, int64_t n, const T* t, T* x, int right, int trans,
                     int lower, T alpha) {
@@ -444,6 +468,27 @@ dla_status potri_fwd(const Ctx& cx, int64_t batch, int64_t n, T* a, int lower) {
   if (!lower) DLAB_TRY(ew_square<T>(cx, batch, n, av, /*transpose*/ 5));
   DLAB_TRY(check_zero_diag<T>(cx, batch, n, C_(av), cx.info));
   return potri_lower<T>(cx, batch, n, av);
+}
+
+// Out-of-place potri: b = (L L^T)^{-1} from the factor l (unchanged), the
+// reference's functional potri (dl/cholesky.hpp:141-147).  fp64
+// 64 < n <= 128: one fused launch reading l and writing b (k_trtri128);
+// otherwise a copy and the in-place operator.
+template <typename T>
+dla_status potri_into(const Ctx& cx, int64_t batch, int64_t n, const T* l, T* b, int lower) {
+  if (bad_dims(batch, n)) return DLA_ERR_SHAPE;
+  const size_t sz = bytes<T>(batch, n, n);
+  if (overlap(l, sz, b, sz)) return DLA_ERR_ALIAS;
+  if constexpr (sizeof(T) == 8) {
+    if (potri_fused_eligible<T>(n)) {
+      DLAB_TRY(reset_info(cx, batch));
+      if (batch * n == 0) return DLA_OK;
+      DLAB_TRY(check_zero_diag<T>(cx, batch, n, cpk(l, n, n), cx.info));
+      return potri128_into(cx, batch, n, cpk(l, n, n), lower == 0, pk(b, n, n));
+    }
+  }
+  if (batch * n > 0) DLAB_TRY(ew_copy<T>(cx, batch, n, n, cpk(l, n, n), pk(b, n, n)));
+  return potri_fwd<T>(cx, batch, n, b, lower);
 }
 
 template <typename T>
@@ -1056,6 +1101,12 @@ dla_status dla_info_check(const int32_t* info, int64_t batch, void* stream, int6
     DLA_ARENA(ws, wsb, stream, nullptr);                                                                          \
     return trmm_fwd<T>(cx, batch, m, n, t, x, r, tr, lo, alpha);                                                  \
   }                                                                                                               \
+  dla_status dla_trmm_into_##S(int64_t batch, int64_t m, int64_t n, const T* t, const T* x, T* y, int r, int tr,   \
+                               int lo, T alpha, void* ws, size_t wsb, void* stream) {                            \
+    DLA_NEED(T, DLA_OP_TRMM, batch, m, n, 0, r ? DLA_WS_RIGHTSIDE : 0);                                           \
+    DLA_ARENA(ws, wsb, stream, nullptr);                                                                          \
+    return trmm_into<T>(cx, batch, m, n, t, x, y, r, tr, lo, alpha);                                              \
+  }                                                                                                               \
   dla_status dla_trmm_bwd_##S(int64_t batch, int64_t m, int64_t n, T* abar, T* tbar, const T* bbar, const T* t,   \
                               const T* a, int r, int tr, int lo, T alpha, void* ws, size_t wsb, void* stream) {  \
     DLA_NEED(T, DLA_OP_TRMM, batch, m, n, 0, DLA_WS_BACKWARD | (r ? DLA_WS_RIGHTSIDE : 0));                       \
@@ -1091,6 +1142,12 @@ dla_status dla_info_check(const int32_t* info, int64_t batch, void* stream, int6
     DLA_NEED(T, DLA_OP_POTRI, batch, n, n, 0, 0);                                                                 \
     DLA_ARENA(ws, wsb, stream, info);                                                                             \
     return potri_fwd<T>(cx, batch, n, a, lower);                                                                  \
+  }                                                                                                               \
+  dla_status dla_potri_into_##S(int64_t batch, int64_t n, const T* l, T* b, int lower, int32_t* info, void* ws,  \
+                                size_t wsb, void* stream) {                                                       \
+    DLA_NEED(T, DLA_OP_POTRI, batch, n, n, 0, 0);                                                                 \
+    DLA_ARENA(ws, wsb, stream, info);                                                                             \
+    return potri_into<T>(cx, batch, n, l, b, lower);                                                              \
   }                                                                                                               \
   dla_status dla_potri_bwd_##S(int64_t batch, int64_t n, T* lbar, const T* bbar, const T* l, const T* b,          \
                                int lower, void* ws, size_t wsb, void* stream) {                                   \

@@ -691,6 +691,12 @@ dla_status trmm_gemm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<con
   return ew_copy<T>(c, batch, m, n, C_(y), x, c.info);
 }
 
+// out-of-place fused potri (64 < n <= 128, fp64): b = inv(L L^T) from l
+dla_status potri128_into(const Ctx& c, int64_t batch, int64_t n, MatB<const double> l, bool from_upper,
+                         MatB<double> b) {
+  return trtri128(c, batch, (int)n, (int)n, l, from_upper, b, true);
+}
+
 // potri of 64 < n <= 128 (fp64) as one fused launch (k_trtri128<., LAUUM>)
 template <typename T>
 bool potri_fused_eligible(int64_t n) {

@@ -37,6 +37,8 @@ template <typename T>
 size_t ws_trsm_inv_from(int64_t batch, int64_t m, int64_t n, bool right);
 template <typename T>
 bool potri_fused_eligible(int64_t n);
+dla_status potri128_into(const Ctx& c, int64_t batch, int64_t n, MatB<const double> l, bool from_upper,
+                         MatB<double> b);
 template <typename T>
 dla_status trsm_inv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x, bool right,
                     bool trans, bool lower, T alpha);

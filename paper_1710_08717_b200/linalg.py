@@ -25,7 +25,7 @@ from ._lib import OPS, STATUS_NAMES, WS_BACKWARD, WS_RIGHTSIDE, lib
 __all__ = [
     "Error", "ShapeError", "NotPositiveDefiniteError", "SingularError", "ConvergenceError",
     "gemm2_into", "gemm2", "gemm_into", "syrk_into", "syrk", "trmm_inplace", "trmm", "trsm_inplace",
-    "trsm", "potrf_inplace", "potrf", "potri_inplace", "potri", "sumlogdiag", "gelqf_inplace",
+    "trsm", "potrf_inplace", "potrf", "potri_inplace", "potri", "potri_into", "trmm_into", "sumlogdiag", "gelqf_inplace",
     "gelqf", "syevd_inplace", "syevd", "gemm2_backward_into", "gemm2_backward", "gemm_backward_into",
     "syrk_backward_into", "syrk_backward", "trmm_backward_into", "trmm_backward",
     "trsm_backward_into", "trsm_backward", "potrf_backward_into", "potrf_backward",
@@ -252,8 +252,21 @@ def trmm_inplace(t, x, rightside=False, transpose=False, lower=True, alpha=1.0):
     return x
 
 
+def trmm_into(y, t, x, rightside=False, transpose=False, lower=True, alpha=1.0):
+    """y = alpha op(T) x / alpha x op(T), x and t unchanged (dl/blas.hpp:202-291,
+    out of place: one triangular GEMM from x into y for n_t >= 128)."""
+    batch = _prep("trmm", y, x, t)
+    m, n = _tri_check(t, x, rightside, "trmm")
+    if y.shape != x.shape:
+        raise ShapeError(f"trmm_into: output {tuple(y.shape)} vs operand {tuple(x.shape)}")
+    ws, nb = _ws("trmm", x, batch, m, n, 0, WS_RIGHTSIDE if rightside else 0)
+    _call("trmm_into", x, batch, m, n, _p(t), _p(x), _p(y), int(rightside), int(transpose), int(lower), alpha,
+          _p(ws), nb, _stream(x))
+    return y
+
+
 def trmm(t, x, rightside=False, transpose=False, lower=True, alpha=1.0):
-    return trmm_inplace(t, x.clone(), rightside, transpose, lower, alpha)
+    return trmm_into(torch.empty_like(x), t, x, rightside, transpose, lower, alpha)
 
 
 def trsm_inplace(t, x, rightside=False, transpose=False, lower=True, alpha=1.0, check=True):
@@ -308,8 +321,24 @@ def potri_inplace(a, lower=True, check=True):
     return a
 
 
+def potri_into(b, l, lower=True, check=True, info=None):
+    """b = inv(L L^T) from the factor l, l unchanged (dl/cholesky.hpp:141-147,
+    out of place: one fused launch for fp64 64 < n <= 128)."""
+    batch = _prep("potri", b, l)
+    n = _square(l, "potri")
+    if b.shape != l.shape:
+        raise ShapeError(f"potri_into: output {tuple(b.shape)} vs factor {tuple(l.shape)}")
+    own = info is None
+    info = _info(batch, l.device) if own else info
+    ws, nb = _ws("potri", l, batch, n, n)
+    _call("potri_into", l, batch, n, _p(l), _p(b), int(lower), _p(info), _p(ws), nb, _stream(l))
+    if check:
+        _check(info, batch, b, "potri")
+    return b
+
+
 def potri(a, lower=True, check=True):
-    return potri_inplace(a.clone(), lower, check)
+    return potri_into(torch.empty_like(a), a, lower, check)
 
 
 def sumlogdiag(a, out=None):

@@ -192,6 +192,35 @@ def test_trmm_trsm_forward(port, dt):
 
 
 @pytest.mark.parametrize("dt", DTYPES)
+def test_into_variants_match_inplace(port, dt):
+    """Out-of-place trmm / potri (the reference's functional forms): equal to the
+    in-place operators (bitwise) and to the oracle; inputs unchanged."""
+    r = O.rng(19)
+    B = 2
+    for (m, n), (right, tr, lo) in itertools.product([(128, 70), (70, 128), (33, 17), (256, 130)], FLAGS):
+        nt = n if right else m
+        t = dev(tri_factor(r, nt, lo, dt, B))
+        x = dev(r.standard_normal((B, m, n)).astype(dt))
+        x0, t0 = x.clone(), t.clone()
+        y = L.trmm_into(torch.empty_like(x), t, x, right, tr, lo, 1.5)
+        assert torch.equal(x, x0) and torch.equal(t, t0)
+        assert torch.equal(y, L.trmm_inplace(t, x.clone(), right, tr, lo, 1.5))
+        assert_close(host(y), batch_apply(lambda tt, xx: port.trmm(tt, xx, right, tr, lo, 1.5), host(t), host(x)), dt)
+    for n in (20, 65, 100, 128, 200):
+        a = O.random_spd(n, r, dt, batch=B)
+        for lower in (1, 0):
+            l = dev(batch_apply(lambda x: port.potrf(x, lower), a))
+            l0 = l.clone()
+            b = L.potri_into(torch.empty_like(l), l, lower)
+            assert torch.equal(l, l0)
+            assert torch.equal(b, L.potri_inplace(l.clone(), lower))
+            assert torch.equal(b, b.transpose(-1, -2))
+            assert_close(host(b), batch_apply(lambda x: port.potri(x, lower), host(l)), dt, 10)
+    with pytest.raises(L.ShapeError):
+        L.potri_into(torch.empty(B, 5, 5, dtype=torch.float64, device="cuda"), dev(np.eye(6)[None].repeat(B, 0)))
+
+
+@pytest.mark.parametrize("dt", DTYPES)
 def test_trmm_trsm_backward(port, dt):
     r = O.rng(5)
     B = 2
