@@ -99,6 +99,12 @@ __device__ __forceinline__ bool decode_lower(const SyrkArgs& g, int64_t t, int64
 }
 
 
+// Fragment row fr -> box row: rows r and r ^ 1 of a [rows][16] 128B-swizzled
+// box share their XOR'd chunk pair, so 8 consecutive rows at 4 consecutive k
+// take each bank segment twice; half-warp h takes rows {0, 2, 4, 6} + h of
+// the 8-row group instead (four disjoint 32-byte segments: conflict-free).
+__device__ __forceinline__ int fperm(int fr) { return 2 * (fr & 3) + (fr >> 2); }
+
 // byte offset of element (row, k) in a [rows][16 doubles] 128B-swizzled box
 __device__ __forceinline__ uint32_t swz(int row, int k) {
   return (uint32_t)(row * 128 + ((((k >> 1) ^ (row & 7))) << 4) + ((k & 1) << 3));
@@ -198,9 +204,11 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
       for (int kk = 0; kk < SKC; kk += 4) {
         double af[MI], bf[NI];
 #pragma unroll
-        for (int i = 0; i < MI; ++i) af[i] = *reinterpret_cast<const double*>(sa + swz(wm + i * 8 + fr, kk + fc));
+        for (int i = 0; i < MI; ++i)
+          af[i] = *reinterpret_cast<const double*>(sa + swz(wm + i * 8 + fperm(fr), kk + fc));
 #pragma unroll
-        for (int j = 0; j < NI; ++j) bf[j] = *reinterpret_cast<const double*>(sb + swz(wn + j * 8 + fr, kk + fc));
+        for (int j = 0; j < NI; ++j)
+          bf[j] = *reinterpret_cast<const double*>(sb + swz(wn + j * 8 + fperm(fr), kk + fc));
 #pragma unroll
         for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -223,22 +231,24 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
     else asm volatile("bar.sync 1, %0;\n" ::"n"(SCONS * 32) : "memory");  // buffer q's last store has been read out
 #pragma unroll
     for (int i = 0; i < MI; ++i) {
-      const int64_t gi = m0 + wm + i * 8 + fr;
+      const int rl = wm + i * 8 + fperm(fr);  // tile row of this lane's accumulator row
+      const int64_t gi = m0 + rl;
 #pragma unroll
       for (int j = 0; j < NI; ++j) {
-        const int cl = wn + j * 8 + 2 * fc;  // column within the tile
-        const int64_t gj = n0 + cl;
-        double2* cp = reinterpret_cast<double2*>(cb + (cl >> 4) * BOX + swz(wm + i * 8 + fr, cl & 15));
-        double2 v;
-        if (use_c) {
-          const double2 cv = *cp;
-          v.x = gj <= gi ? g.alpha * acc[i][j][0] + g.beta * cv.x : cv.x;
-          v.y = gj + 1 <= gi ? g.alpha * acc[i][j][1] + g.beta * cv.y : cv.y;
-        } else {
-          v.x = g.alpha * acc[i][j][0];
-          v.y = g.alpha * acc[i][j][1];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int cl = wn + j * 8 + fperm(2 * fc + e);  // accumulator column -> tile column
+          const int64_t gj = n0 + cl;
+          double* cp = reinterpret_cast<double*>(cb + (cl >> 4) * BOX + swz(rl, cl & 15));
+          double v;
+          if (use_c) {
+            const double cv = *cp;
+            v = gj <= gi ? g.alpha * acc[i][j][e] + g.beta * cv : cv;
+          } else {
+            v = g.alpha * acc[i][j][e];
+          }
+          *cp = v;
         }
-        *cp = v;
       }
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
