@@ -868,7 +868,8 @@ dla_status gp_potrf_inv(const Ctx& cx, int64_t batch, int64_t n, T* a) {
   PotrfHook hook{n / 2, early_inv_first<T>, &e, a, n};
   Ctx hc = cx;
   hc.potrf_hook = &hook;
-  const dla_status sf = potrf_lower<T>(hc, batch, n, pk(a, n, n), /*zero_upper*/ false);
+  bool zeroed = false;  // the blocked factorization zeroes the strict upper triangle as it goes
+  const dla_status sf = potrf_lower<T>(hc, batch, n, pk(a, n, n), /*zero_upper*/ false, &zeroed);
   if (!e.fired) early_inv_first<T>(&e, cx.stream);  // a schedule without the hook point (tuning modes)
   const int64_t h = n / 2;
   T* wp = inv.as<T>();
@@ -898,7 +899,7 @@ dla_status gp_potrf_inv(const Ctx& cx, int64_t batch, int64_t n, T* a) {
   // stream: no kernel of the step reads it, so it stays off the critical path.
   // It is complete once dla_potrf_bwd_end_f64 (or dla_potrf_inv_join_f64)
   // has been enqueued on the caller's stream.
-  if (st == DLA_OK) {
+  if (st == DLA_OK && !zeroed) {
     Ctx zc = sc;
     zc.info = cx.info;
     st = ew_square<T>(zc, batch, n, pk(a, n, n), /*tril*/ 0, T(1), cx.info);

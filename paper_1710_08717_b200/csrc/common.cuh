@@ -337,7 +337,8 @@ template <typename T>
 dla_status trmm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T> t, MatB<T> x,
                 bool right, bool trans, bool lower, T alpha);
 template <typename T>
-dla_status potrf_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool zero_upper = true);
+dla_status potrf_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool zero_upper = true,
+                       bool* upper_zeroed = nullptr);
 template <typename T>
 dla_status potri_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a);
 

@@ -421,7 +421,7 @@ dla_status trmm_core(const Ctx& c, int64_t batch, int64_t nt, int64_t nother, Ma
 }
 
 template <typename T>
-dla_status potrf_blocked(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int64_t kbase);
+dla_status potrf_blocked(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int64_t kbase, bool* upper_zeroed = nullptr);
 
 // L11^{-1} buffer of the blocked Cholesky's throughput path (large batches of
 // multi-chunk panels); sms < 0 gives the bound the workspace query uses.
@@ -788,8 +788,12 @@ inline int syrk_cap(int leave_panel, int sms) {
   return leave_panel;
 }
 
+// *upper_zeroed (optional): when given, the strict upper triangle is zeroed
+// here too, on the side stream once the bulk updates have slack (no kernel of
+// the factorization reads it), instead of after the last panel.
 template <typename T, int NBP>
-dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int64_t kbase) {
+dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int64_t kbase,
+                            bool* upper_zeroed = nullptr) {
   const size_t sm = sizeof(T) * ((NBP + 64) * (NBP + 1) + NBP + (NBP == 64 ? 2 * 64 * (NBP + 1) : 0));
   ensure_smem_attr(k_potrf_panel<T, NBP>, sm);
   // Look-ahead on two streams: the main stream runs the critical chain
@@ -862,6 +866,7 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
   auto throughput = [&](int64_t p) { return NBP == 64 && chunks_of(p) > 1 && batch * chunks_of(p) > c.sms; };
   auto fused = [&](int64_t p) { return NBP == 64 && G == 1 && p >= 1 && !throughput(p); };
   bool hook_fired = false;
+  bool zeroed = false;
   dla_status st = DLA_OK;
   // every launch failure leaves the loop through the join below: work already
   // forked onto the side / critical streams is joined back to the caller's
@@ -953,9 +958,21 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
       }
       cudaEventRecord(la.done[g], la.side);
     }
+    // late in the factorization the side stream's updates are shorter than
+    // the panel chain: the strict upper triangle is zeroed in that slack
+    // (DLA_POTRF_ZERO_AT: the step, in % of the steps; tuning switch)
+    static const int zero_at = [] {
+      const char* e = getenv("DLA_POTRF_ZERO_AT");
+      return e ? atoi(e) : 75;
+    }();
+    if (upper_zeroed && !zeroed && 100 * (p + 1) >= zero_at * steps) {
+      LA_TRY(ew_square<T>(side, batch, n, a, /*tril*/ 0, T(1), c.info));
+      zeroed = true;
+    }
   }
 #undef LA_TRY
   (void)ngroups;
+  if (upper_zeroed) *upper_zeroed = zeroed && st == DLA_OK;
   cudaEventRecord(la.ev[1], la.side);
   cudaStreamWaitEvent(c.stream, la.ev[1], 0);
   if (prio) {
@@ -969,9 +986,10 @@ dla_status potrf_blocked_nb(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, i
 // costs one launch + one column update regardless of width); 64 keeps more
 // CTAs busy for small n.  DLA_POTRF_NB overrides (tuning switch).
 template <typename T>
-dla_status potrf_blocked(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int64_t kbase) {
+dla_status potrf_blocked(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, int64_t kbase, bool* upper_zeroed) {
   const bool wide = potrf_nb() == 128;
-  return wide ? potrf_blocked_nb<T, 128>(c, batch, n, a, kbase) : potrf_blocked_nb<T, 64>(c, batch, n, a, kbase);
+  return wide ? potrf_blocked_nb<T, 128>(c, batch, n, a, kbase, upper_zeroed)
+              : potrf_blocked_nb<T, 64>(c, batch, n, a, kbase, upper_zeroed);
 }
 
 template <typename T>
@@ -1039,7 +1057,8 @@ dla_status trmm(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<const T>
 }
 
 template <typename T>
-dla_status potrf_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool zero_upper) {
+dla_status potrf_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool zero_upper, bool* upper_zeroed) {
+  if (upper_zeroed) *upper_zeroed = false;
   if (batch == 0 || n == 0) return DLA_OK;
   ensure_smem_attr(k_potrf_leaf<T>, sizeof(T) * NB * CH_LD);
   ensure_smem_attr(k_lauum_leaf<T>, sizeof(T) * NB * LDS);
@@ -1059,10 +1078,12 @@ dla_status potrf_lower(const Ctx& c, int64_t batch, int64_t n, MatB<T> a, bool z
     if (tiles) DLAB_TRY(potrf_tiles(c, batch, n, ad, 0));
   }
   const bool blocked = mode != 1 && n > NB;
+  bool zeroed = false;  // the blocked schedule zeroes the strict upper triangle as it goes
   if (tiles) {
-  } else if (blocked) DLAB_TRY(potrf_blocked<T>(c, batch, n, a, 0));
+  } else if (blocked) DLAB_TRY(potrf_blocked<T>(c, batch, n, a, 0, &zeroed));
   else DLAB_TRY(potrf_rec<T>(c, batch, n, 0, a));
-  if (!zero_upper) return DLA_OK;  // the caller zeroes the strict upper triangle itself (off its critical path)
+  if (upper_zeroed) *upper_zeroed = zeroed;
+  if (!zero_upper || zeroed) return DLA_OK;  // else the caller zeroes it itself (off its critical path)
   return ew_square<T>(c, batch, n, a, /*tril*/ 0, T(1), c.info);
 }
 
@@ -1190,7 +1211,7 @@ size_t ws_potri_lower(int64_t batch, int64_t n) {
                               T, bool);                                                                     \
   template dla_status trmm<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<const T>, MatB<T>, bool, bool, bool, \
                               T);                                                                           \
-  template dla_status potrf_lower<T>(const Ctx&, int64_t, int64_t, MatB<T>, bool);                                \
+  template dla_status potrf_lower<T>(const Ctx&, int64_t, int64_t, MatB<T>, bool, bool*);                                \
   template dla_status potri_lower<T>(const Ctx&, int64_t, int64_t, MatB<T>);
 INST(double)
 INST(float)

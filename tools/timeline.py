@@ -1,7 +1,7 @@
 """Kernel timeline of one potrf n=4096 (torch.profiler / CUPTI): per-kernel
 start/end on every stream, summarised as the critical-chain gaps.
 
-    python tools/timeline.py [n] [out.json]
+    python tools/timeline.py [n] [out.json] [batch]
 """
 import json
 import os
@@ -15,12 +15,13 @@ from paper_1710_08717_b200 import linalg as L  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 out = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/timeline.json"
+B = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 torch.manual_seed(0)
-xx = torch.randn(1, n, n, dtype=torch.float64, device="cuda")
+xx = torch.randn(B, n, n, dtype=torch.float64, device="cuda")
 spd = xx @ xx.transpose(-1, -2)
 spd = 0.5 * (spd + spd.transpose(-1, -2)) + n * torch.eye(n, dtype=torch.float64, device="cuda")
 a = spd.clone()
-info = torch.zeros(1, dtype=torch.int32, device="cuda")
+info = torch.zeros(B, dtype=torch.int32, device="cuda")
 for _ in range(3):
     a.copy_(spd)
     L.potrf_inplace(a, check=False, info=info)
