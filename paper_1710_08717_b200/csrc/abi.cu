@@ -837,14 +837,13 @@ void early_inv_first(void* user, cudaStream_t crit) {
   MatB<T> wi{e.wp, n, n * n};
   T* tmp = e.wp + 2 * B * n * n;
   MatB<const T> lv{e.l, n, n * n};
-  // W11 = tril(L11), W21 = L21; L11^{-1} in place; T1 = W21 W11^{-1} into tmp
-  dla_status st = ew_tri_copy<T>(sc, B, h, lv, wi, false);
-  if (st == DLA_OK) st = ew_copy<T>(sc, B, h, h, MatB<const T>{e.l + h * n, n, n * n}, wi.sub(h, 0));
+  // W11 = L11^{-1} read straight from the factor (no copy pass); T1 = L21 W11
+  // into tmp, L21 again read from the factor
   T* tmp2 = tmp + B * (trtri_levels_tmp<T>(n) / sizeof(T));
-  if (st == DLA_OK) st = trtri_levels<T>(sc, B, h, wi, tmp2);
+  dla_status st = trtri_levels<T>(sc, B, h, wi, tmp2, &lv, false);
   MatB<T> t1{tmp, h, h * h};
   if (st == DLA_OK)
-    st = gemm<T>(sc, B, h, h, h, T(1), MatB<const T>{wi.p + h * n, n, n * n}, false, MatB<const T>{wi.p, n, n * n},
+    st = gemm<T>(sc, B, h, h, h, T(1), MatB<const T>{e.l + h * n, n, n * n}, false, MatB<const T>{wi.p, n, n * n},
                  false, T(0), t1, MASK_FULL, nullptr, TRI_NONE, TRI_LOWER);
   e.st = st;
 }
@@ -888,10 +887,9 @@ dla_status gp_potrf_inv(const Ctx& cx, int64_t batch, int64_t n, T* a) {
     return e ? atoi(e) : 0;
   }();
   sc.gemm_ctas = side_ctas;
-  // W22 = tril(L22); L22^{-1} in place; W21 = -W22^{-1} T1
-  if (st == DLA_OK)
-    st = ew_tri_copy<T>(sc, batch, h, MatB<const T>{a + h * n + h, n, n * n}, wi.sub(h, h), false);
-  if (st == DLA_OK) st = trtri_levels<T>(sc, batch, h, wi.sub(h, h), tmp2);
+  // W22 = L22^{-1} (read straight from the factor); W21 = -W22 T1
+  const MatB<const T> l22{a + h * n + h, n, n * n};
+  if (st == DLA_OK) st = trtri_levels<T>(sc, batch, h, wi.sub(h, h), tmp2, &l22, false);
   if (st == DLA_OK)
     st = gemm<T>(sc, batch, h, h, h, T(-1), MatB<const T>{wi.p + h * n + h, n, n * n}, false,
                  MatB<const T>{tmp, h, h * h}, false, T(0), wi.sub(h, 0), MASK_FULL, nullptr, TRI_LOWER, TRI_NONE);

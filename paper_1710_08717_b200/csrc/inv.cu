@@ -82,19 +82,23 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(128) k_trtri64_dmma(int64_t nblk, MatB<double> w) {
+// src: the factor (its lower triangle, or with from_upper its upper triangle
+// transposed); the inverted diagonal blocks go to w (may be src itself).
+__global__ void __launch_bounds__(128) k_trtri64_dmma(int64_t nblk, MatB<const double> src, bool from_upper,
+                                                      MatB<double> w) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* S = reinterpret_cast<double*>(smem_raw);  // [64][ILD]
   double* Tt = S + IB * ILD;                         // [32][TLD8]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, fr = lane >> 2, fc = lane & 3;
   const int64_t b = blockIdx.x / nblk, k = blockIdx.x % nblk;
   double* base = w.p + b * w.bs + k * IB * (w.ld + 1);
+  const double* sb = src.p + b * src.bs + k * IB * (src.ld + 1);
   {
     double v[32];
 #pragma unroll
     for (int u = 0; u < 32; ++u) {
       const int e = tid + u * 128, i = e >> 6, j = e & 63;
-      v[u] = j <= i ? base[i * w.ld + j] : 0.0;
+      v[u] = j <= i ? (from_upper ? sb[j * src.ld + i] : sb[i * src.ld + j]) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < 32; ++u) {
@@ -431,17 +435,38 @@ size_t ws_potri_inv(int64_t batch, int64_t n) {
   return carve_bound(potri_inv_scratch<T>(batch, n)) + ws_trtri_levels<T>(batch, n) + ws_gemm<T>(batch, n, n, n);
 }
 
-// W lower triangular (strict upper must be zero on entry; stays zero).
+template <typename T>
+MatB<const double> as_d(MatB<const T> m) {
+  return MatB<const double>{reinterpret_cast<const double*>(m.p), m.ld, m.bs, m.bsi};
+}
+template <typename T>
+MatB<double> as_d(MatB<T> m) {
+  return MatB<double>{reinterpret_cast<double*>(m.p), m.ld, m.bs, m.bsi};
+}
+
+// Level-batched inverse W = L^{-1}.  src == nullptr: in place, W lower
+// triangular on entry (strict upper zero; stays zero).  Otherwise (fp64) L is
+// read straight from src's lower triangle (from_upper: its upper triangle,
+// transposed) -- the diagonal blocks by the block-inverse kernel, the
+// off-diagonal blocks by each level's first product -- so no tri_copy pass
+// precedes it; W's strict upper BLOCKS are then left unwritten, and every
+// consumer reads W through a triangular operand flag (masked by the GEMM).
 // tmp: >= trtri_levels_tmp(n) elements... bytes per slice, batch slices.
 template <typename T>
-dla_status trtri_levels(const Ctx& c, int64_t batch, int64_t n, MatB<T> w, T* tmp) {
+dla_status trtri_levels(const Ctx& c, int64_t batch, int64_t n, MatB<T> w, T* tmp, const MatB<const T>* src,
+                        bool from_upper) {
   const int64_t nblk = n / IB;
   if constexpr (sizeof(T) == 8) {
     const size_t sm = sizeof(double) * (IB * ILD + 32 * TLD8);
     ensure_smem_attr(k_trtri64_dmma, sm);
     MatB<double> wd{reinterpret_cast<double*>(w.p), w.ld, w.bs, w.bsi};
-    k_trtri64_dmma<<<(unsigned)(batch * nblk), 128, sm, c.stream>>>(nblk, wd);
+    const MatB<const double> sd = src ? as_d(*src) : MatB<const double>{wd.p, wd.ld, wd.bs, wd.bsi};
+    k_trtri64_dmma<<<(unsigned)(batch * nblk), 128, sm, c.stream>>>(nblk, sd, src && from_upper, wd);
   } else {
+    if (src) {  // fp32: the copy, then in place
+      DLAB_TRY(ew_tri_copy<T>(c, batch, n, *src, w, from_upper));
+      return trtri_levels<T>(c, batch, n, w, tmp);
+    }
     const size_t sm = sizeof(T) * (2 * IB * ILD + IB);
     ensure_smem_attr(k_trtri_blocks<T>, sm);
     k_trtri_blocks<T><<<(unsigned)(batch * nblk), 128, sm, c.stream>>>(nblk, w);
@@ -453,9 +478,17 @@ dla_status trtri_levels(const Ctx& c, int64_t batch, int64_t n, MatB<T> w, T* tm
     MatB<T> wa{w.p, w.ld, w.bs, stride};
     MatB<T> wb = wa.sub(s, 0), wc = wa.sub(s, s);
     MatB<T> t1{tmp, s, pairs * s * s, s * s};
-    // T1 = B A^{-1}   (A^{-1} lower)
-    DLAB_TRY(gemm<T>(c, batch, s, s, s, T(1), C_(wb), false, C_(wa), false, T(0), t1, MASK_FULL, nullptr, TRI_NONE,
-                     TRI_LOWER, pairs));
+    // T1 = B A^{-1}   (A^{-1} lower; B = L's block, from src when given)
+    if (src && sizeof(T) == 8) {
+      const int64_t sstride = 2 * s * (src->ld + 1);
+      const MatB<const T> sa{src->p, src->ld, src->bs, sstride};
+      const MatB<const T> bsrc = from_upper ? sa.sub(0, s) : sa.sub(s, 0);  // upper: B = (src block)^T
+      DLAB_TRY(gemm<T>(c, batch, s, s, s, T(1), bsrc, from_upper, C_(wa), false, T(0), t1, MASK_FULL, nullptr,
+                       TRI_NONE, TRI_LOWER, pairs));
+    } else {
+      DLAB_TRY(gemm<T>(c, batch, s, s, s, T(1), C_(wb), false, C_(wa), false, T(0), t1, MASK_FULL, nullptr, TRI_NONE,
+                       TRI_LOWER, pairs));
+    }
     // B = -C^{-1} T1  (C^{-1} lower)
     DLAB_TRY(gemm<T>(c, batch, s, s, s, T(-1), C_(wc), false, C_(t1), false, T(0), wb, MASK_FULL, nullptr,
                      TRI_LOWER, TRI_NONE, pairs));
@@ -466,14 +499,6 @@ dla_status trtri_levels(const Ctx& c, int64_t batch, int64_t n, MatB<T> w, T* tm
 // fp64 128-wide inverse (or potri) in one launch: dst = lower-form
 // inv([L 0; 0 I]) over nout x nout, L read from src's lower (or, from_upper,
 // transposed upper) triangle, n <= 128.
-template <typename T>
-MatB<const double> as_d(MatB<const T> m) {
-  return MatB<const double>{reinterpret_cast<const double*>(m.p), m.ld, m.bs, m.bsi};
-}
-template <typename T>
-MatB<double> as_d(MatB<T> m) {
-  return MatB<double>{reinterpret_cast<double*>(m.p), m.ld, m.bs, m.bsi};
-}
 inline dla_status trtri128(const Ctx& c, int64_t batch, int n, int nout, MatB<const double> src, bool from_upper,
                            MatB<double> dst, bool lauum) {
   const size_t sm = sizeof(double) * 3 * TBLK;
@@ -511,8 +536,7 @@ dla_status trsm_inv(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB<cons
   if (use_trtri128<T>(nt)) {
     DLAB_TRY(trtri128(c, batch, 128, 128, as_d(t), !lower, as_d(w), false));
   } else {
-    DLAB_TRY(ew_tri_copy<T>(c, batch, nt, t, w, !lower));
-    DLAB_TRY(trtri_levels<T>(c, batch, nt, w, tmp));
+    DLAB_TRY(trtri_levels<T>(c, batch, nt, w, tmp, &t, !lower));
   }
   const bool eff = (lower != trans);  // op(T)^{-1} = eff ? W : W^T
   const int tri = eff ? TRI_LOWER : TRI_UPPER;
@@ -550,8 +574,7 @@ dla_status trsm_inv_from(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB
   if (use_trtri128<T>(nt)) {
     DLAB_TRY(trtri128(c, batch, 128, 128, as_d(t), !lower, as_d(w), false));
   } else {
-    DLAB_TRY(ew_tri_copy<T>(c, batch, nt, t, w, !lower));
-    DLAB_TRY(trtri_levels<T>(c, batch, nt, w, tmp));
+    DLAB_TRY(trtri_levels<T>(c, batch, nt, w, tmp, &t, !lower));
   }
   const bool eff = (lower != trans);
   const int tri = eff ? TRI_LOWER : TRI_UPPER;
@@ -565,8 +588,7 @@ dla_status trsm_inv_from(const Ctx& c, int64_t batch, int64_t m, int64_t n, MatB
 template <typename T>
 dla_status potrf_inv_prepare(const Ctx& c, int64_t batch, int64_t n, MatB<const T> l, bool lower, MatB<T> wi, T* tmp) {
   if (use_trtri128<T>(n)) return trtri128(c, batch, 128, 128, as_d(l), !lower, as_d(wi), false);
-  DLAB_TRY(ew_tri_copy<T>(c, batch, n, l, wi, !lower));
-  return trtri_levels<T>(c, batch, n, wi, tmp);
+  return trtri_levels<T>(c, batch, n, wi, tmp, &l, !lower);
 }
 
 // The second half: Abar from Lbar, L and the prepared wi = L^{-1}; tt is n^2
@@ -738,7 +760,7 @@ dla_status potri_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> a) {
   template size_t ws_potrf_bwd_inv<T>(int64_t, int64_t);                                                     \
   template size_t ws_trmm_gemm<T>(int64_t, int64_t, int64_t, bool);                                          \
   template size_t ws_potri_inv<T>(int64_t, int64_t);                                                         \
-  template dla_status trtri_levels<T>(const Ctx&, int64_t, int64_t, MatB<T>, T*);                            \
+  template dla_status trtri_levels<T>(const Ctx&, int64_t, int64_t, MatB<T>, T*, const MatB<const T>*, bool);                            \
   template dla_status trsm_inv<T>(const Ctx&, int64_t, int64_t, int64_t, MatB<const T>, MatB<T>, bool, bool, \
                                   bool, T);                                                                  \
   template dla_status potrf_bwd_inv<T>(const Ctx&, int64_t, int64_t, MatB<T>, MatB<const T>, MatB<const T>, bool); \

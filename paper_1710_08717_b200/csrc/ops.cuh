@@ -48,7 +48,8 @@ dla_status potrf_bwd_inv(const Ctx& c, int64_t batch, int64_t n, MatB<T> abar, M
 template <typename T>
 size_t trtri_levels_tmp(int64_t n);
 template <typename T>
-dla_status trtri_levels(const Ctx& c, int64_t batch, int64_t n, MatB<T> w, T* tmp);
+dla_status trtri_levels(const Ctx& c, int64_t batch, int64_t n, MatB<T> w, T* tmp,
+                        const MatB<const T>* src = nullptr, bool from_upper = false);
 template <typename T>
 dla_status potrf_inv_prepare(const Ctx& c, int64_t batch, int64_t n, MatB<const T> l, bool lower, MatB<T> wi, T* tmp);
 template <typename T>
