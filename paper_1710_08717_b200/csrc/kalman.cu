@@ -65,12 +65,17 @@ inline KDims kdims(int64_t h, int64_t d, int64_t T) {
 
 // C (m x n) = alpha op(A) op(B) (+ C if acc); A: ta ? k x m : m x k;
 // B: tb ? n x k : k x n; sequential k (no barrier inside).
-template <typename T>
+// NT: threads per sequence (compile time); with the block sizes compile-time
+// constants too (the specialised kernels) every loop below unrolls into
+// straight-line FMAs on constant shared-memory offsets.
+template <int NT, typename T>
 __device__ __forceinline__ void mm(T* C, const T* A, const T* B, int m, int n, int k, bool ta, bool tb, T alpha,
                                    bool acc) {
-  for (int idx = threadIdx.x; idx < m * n; idx += (int)blockDim.x) {
+#pragma unroll
+  for (int idx = threadIdx.x; idx < m * n; idx += NT) {
     const int i = idx / n, j = idx - i * n;
     T s = T(0);
+#pragma unroll
     for (int p = 0; p < k; ++p) {
       const T av = ta ? A[p * m + i] : A[i * k + p];
       const T bv = tb ? B[j * k + p] : B[p * n + j];
@@ -80,16 +85,17 @@ __device__ __forceinline__ void mm(T* C, const T* A, const T* B, int m, int n, i
   }
 }
 
-template <typename T>
-__device__ __forceinline__ void cpy(T* dst, const T* src, int64_t n) {
-  for (int64_t i = threadIdx.x; i < n; i += (int)blockDim.x) dst[i] = src[i];
+template <int NT, typename T>
+__device__ __forceinline__ void cpy(T* dst, const T* src, int n) {
+#pragma unroll
+  for (int i = threadIdx.x; i < n; i += NT) dst[i] = src[i];
 }
 
 // Cholesky of the d x d block S (lower, in place, strict upper zeroed) by
 // warp 0: right-looking, lane = row.  Returns the failing step or -1
 // (uniform after the caller's barrier through *fail).
 template <typename T>
-__device__ void chol_warp(T* S, int d, int* fail) {
+__device__ __forceinline__ void chol_warp(T* S, int d, int* fail) {
   if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
   for (int j = 0; j < d; ++j) {
@@ -117,10 +123,14 @@ __device__ void chol_warp(T* S, int d, int* fail) {
 // (rows x d) operand X, in place:
 //   mode 0: x <- x L^-T  (L x'^T = x^T: forward substitution)
 //   mode 1: x <- x L^-1  (L^T x'^T = x^T: back substitution)
-template <typename T>
-__device__ __forceinline__ void rows_solve(T* X, int rows, const T* L, int d, int mode) {
-  for (int i = threadIdx.x; i < rows; i += (int)blockDim.x) {
-    T* x = X + i * d;
+// `extra` (optional): one more row vector solved the same way, by the lane
+// after the last row (in the same instruction stream as the rows).
+template <int NT, typename T>
+__device__ __forceinline__ void rows_solve(T* X, int rows, const T* L, int d, int mode, T* extra = nullptr) {
+  const int nr = extra ? rows + 1 : rows;
+#pragma unroll
+  for (int i = threadIdx.x; i < nr; i += NT) {
+    T* x = i < rows ? X + i * d : extra;
     if (mode == 0) {
       for (int j = 0; j < d; ++j) {
         T s = x[j];
@@ -150,13 +160,16 @@ struct KArgs {
 // NT threads per sequence: 128 (8 CTAs/SM by registers), 64 (16) or 32 (32):
 // the per-step chain is latency-bound on 8 x 8 blocks, so smaller CTAs keep
 // more sequences in flight per SM.
-template <typename T, int NT>
+// H, D > 0: the state / observation sizes as compile-time constants (the
+// common small models; same operation order as the runtime-size kernel, so
+// the results are bitwise identical); 0 = read from the arguments.
+template <typename T, int NT, int H = 0, int D = 0>
 __global__ void __launch_bounds__(NT, (NT == 128 ? 8 : NT == 64 ? 16 : 32)) k_kalman(KArgs<T> g) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
   const KDims& K = g.k;
-  const int h = K.h, d = K.d, nT = K.T;
-  const int64_t hh = K.hh, hd = K.hd, dd = K.dd;
+  const int h = H > 0 ? H : K.h, d = D > 0 ? D : K.d, nT = K.T;
+  const int hh = h * h, hd = h * d, dd = d * d;
   const int64_t seq = blockIdx.x;
   if (slice_failed(g.info, seq)) return;
   __shared__ int fail;
@@ -168,10 +181,10 @@ __global__ void __launch_bounds__(NT, (NT == 128 ? 8 : NT == 64 ? 16 : 32)) k_ka
   T* Sh = B + hd;
   T* Sv = Sh + hh;
   T* W = Sv + dd;  // work slots of KMAX^2 / general sizes below
-  cpy(A, g.a + ps * seq * hh, hh);
-  cpy(B, g.b + ps * seq * hd, hd);
-  cpy(Sh, g.sh + ps * seq * hh, hh);
-  cpy(Sv, g.sv + ps * seq * dd, dd);
+  cpy<NT>(A, g.a + ps * seq * hh, hh);
+  cpy<NT>(B, g.b + ps * seq * hd, hd);
+  cpy<NT>(Sh, g.sh + ps * seq * hh, hh);
+  cpy<NT>(Sv, g.sv + ps * seq * dd, dd);
   const int64_t mx = h > d ? h : d;
   const int64_t slot = (mx * mx + 1) & ~int64_t(1), vslot = (mx + 1) & ~int64_t(1);
   auto S_ = [&](int i) { return W + i * slot; };                                  // matrix slots
@@ -182,8 +195,8 @@ __global__ void __launch_bounds__(NT, (NT == 128 ? 8 : NT == 64 ? 16 : 32)) k_ka
   // ------------------------------------------------------------ forward
   {
     T* S = tape + K.oS;  // step 0's predicted state comes from the prior
-    cpy(S, g.s0 + ps * seq * hh, hh);
-    cpy(tape + K.oMu, g.mu0 + ps * seq * h, h);
+    cpy<NT>(S, g.s0 + ps * seq * hh, hh);
+    cpy<NT>(tape + K.oMu, g.mu0 + ps * seq * h, h);
   }
   T total = T(0);
   __syncthreads();
@@ -191,18 +204,18 @@ __global__ void __launch_bounds__(NT, (NT == 128 ? 8 : NT == 64 ? 16 : 32)) k_ka
     T* tp = tape + t * K.step;
     T *S = S_(0), *M1 = S_(1), *L = S_(2), *Y = S_(3), *Kg = S_(4), *I = S_(5), *P1 = S_(6), *Q1 = S_(7);
     T *Sf = S_(8), *t1 = S_(9), *t2 = S_(10);
-    T *mu = V_(0), *e = V_(1), *z = V_(2), *muf = V_(3);
-    cpy(S, tp + K.oS, hh);
-    cpy(mu, tp + K.oMu, h);
+    T *mu = V_(0), *e = V_(1), *z = V_(2), *muf = V_(3), *lg = V_(4);  // (V_(4): the backward's mbn)
+    cpy<NT>(S, tp + K.oS, hh);
+    cpy<NT>(mu, tp + K.oMu, h);
     __syncthreads();
-    mm(M1, B, S, d, h, h, false, false, T(1), false);        // M1 = B S
-    mm(Y, S, B, h, d, h, false, true, T(1), false);          // X = S B^T (into Y)
-    mm(e, B, mu, d, 1, h, false, false, T(-1), false);       // e = -B mu
+    mm<NT>(M1, B, S, d, h, h, false, false, T(1), false);        // M1 = B S
+    mm<NT>(Y, S, B, h, d, h, false, true, T(1), false);          // X = S B^T (into Y)
+    mm<NT>(e, B, mu, d, 1, h, false, false, T(-1), false);       // e = -B mu
     __syncthreads();
-    mm(L, M1, B, d, d, h, false, true, T(1), false);         // Svv = M1 B^T
-    for (int i = threadIdx.x; i < d; i += (int)blockDim.x) e[i] += obs[t * d + i];
+    mm<NT>(L, M1, B, d, d, h, false, true, T(1), false);         // Svv = M1 B^T
+    for (int i = threadIdx.x; i < d; i += NT) e[i] += obs[t * d + i];
     __syncthreads();
-    for (int64_t i = threadIdx.x; i < dd; i += (int)blockDim.x) L[i] += Sv[i];
+    for (int i = threadIdx.x; i < dd; i += NT) L[i] += Sv[i];
     __syncthreads();
     chol_warp(L, d, &fail);
     __syncthreads();
@@ -210,60 +223,58 @@ __global__ void __launch_bounds__(NT, (NT == 128 ? 8 : NT == 64 ? 16 : 32)) k_ka
       if (threadIdx.x == 0) record_failure(g.info, seq, DLA_ERR_NOT_SPD, (int64_t)t * d + fail);
       return;
     }
-    for (int i = threadIdx.x; i < d; i += (int)blockDim.x) z[i] = e[i];
+    for (int i = threadIdx.x; i < d; i += NT) {
+      z[i] = e[i];
+      lg[i] = Num<T>::log_(L[i * d + i]);  // the d logs in parallel; summed in order below
+    }
     __syncthreads();
-    if (threadIdx.x == 0) {  // z = L^-1 e; phi_t (sequential sums as the tape's Sum)
-      for (int j = 0; j < d; ++j) {
-        T s = z[j];
-        for (int k = 0; k < j; ++k) s -= L[j * d + k] * z[k];
-        z[j] = s / L[j * d + j];
-      }
+    rows_solve<NT>(Y, h, L, d, 0, z);                             // Y = X L^-T;  z = L^-1 e (one more row)
+    __syncthreads();
+    if (threadIdx.x == 0) {  // phi_t (sequential sums as the tape's Sum)
       T quad = T(0), ld = T(0);
       for (int i = 0; i < d; ++i) quad += z[i] * z[i];
-      for (int i = 0; i < d; ++i) ld += Num<T>::log_(L[i * d + i]);
+      for (int i = 0; i < d; ++i) ld += lg[i];
       const T term = (T(0.5) * quad + ld) + T(0.5) * T(d) * log2pi;
       total = t == 0 ? term : total + term;
     }
-    rows_solve(Y, h, L, d, 0);                                // Y = X L^-T
+    cpy<NT>(Kg, Y, hd);
     __syncthreads();
-    cpy(Kg, Y, hd);
+    rows_solve<NT>(Kg, h, L, d, 1);                               // K = Y L^-1
     __syncthreads();
-    rows_solve(Kg, h, L, d, 1);                               // K = Y L^-1
+    mm<NT>(muf, Kg, e, h, 1, d, false, false, T(1), false);      // K e
+    mm<NT>(I, Kg, B, h, h, d, false, false, T(-1), false);       // -K B
+    mm<NT>(Q1, Kg, Sv, h, d, d, false, false, T(1), false);      // Q1 = K Sv
     __syncthreads();
-    mm(muf, Kg, e, h, 1, d, false, false, T(1), false);      // K e
-    mm(I, Kg, B, h, h, d, false, false, T(-1), false);       // -K B
-    mm(Q1, Kg, Sv, h, d, d, false, false, T(1), false);      // Q1 = K Sv
+    for (int i = threadIdx.x; i < h; i += NT) muf[i] += mu[i];
+    for (int i = threadIdx.x; i < h; i += NT) I[i * h + i] += T(1);
     __syncthreads();
-    for (int i = threadIdx.x; i < h; i += (int)blockDim.x) muf[i] += mu[i];
-    for (int i = threadIdx.x; i < h; i += (int)blockDim.x) I[i * h + i] += T(1);
+    mm<NT>(P1, I, S, h, h, h, false, false, T(1), false);        // P1 = I_KB S
+    mm<NT>(t1, Q1, Kg, h, h, d, false, true, T(1), false);       // Q2 = Q1 K^T
     __syncthreads();
-    mm(P1, I, S, h, h, h, false, false, T(1), false);        // P1 = I_KB S
-    mm(t1, Q1, Kg, h, h, d, false, true, T(1), false);       // Q2 = Q1 K^T
+    mm<NT>(Sf, P1, I, h, h, h, false, true, T(1), false);        // P2 = P1 I_KB^T
     __syncthreads();
-    mm(Sf, P1, I, h, h, h, false, true, T(1), false);        // P2 = P1 I_KB^T
-    __syncthreads();
-    for (int64_t i = threadIdx.x; i < hh; i += (int)blockDim.x) Sf[i] += t1[i];
+    for (int i = threadIdx.x; i < hh; i += NT) Sf[i] += t1[i];
     __syncthreads();
     // tape of this step
-    cpy(tp + K.oM1, M1, hd);
-    cpy(tp + K.oL, L, dd);
-    cpy(tp + K.oE, e, d);
-    cpy(tp + K.oZ, z, d);
-    cpy(tp + K.oY, Y, hd);
-    cpy(tp + K.oK, Kg, hd);
-    cpy(tp + K.oI, I, hh);
-    cpy(tp + K.oP1, P1, hh);
-    cpy(tp + K.oQ1, Q1, hd);
-    cpy(tp + K.oSf, Sf, hh);
-    cpy(tp + K.oMuf, muf, h);
+    cpy<NT>(tp + K.oM1, M1, hd);
+    cpy<NT>(tp + K.oL, L, dd);
+    cpy<NT>(tp + K.oE, e, d);
+    cpy<NT>(tp + K.oZ, z, d);
+    cpy<NT>(tp + K.oY, Y, hd);
+    cpy<NT>(tp + K.oK, Kg, hd);
+    cpy<NT>(tp + K.oI, I, hh);
+    cpy<NT>(tp + K.oP1, P1, hh);
+    cpy<NT>(tp + K.oQ1, Q1, hd);
+    cpy<NT>(tp + K.oSf, Sf, hh);
+    cpy<NT>(tp + K.oMuf, muf, h);
     if (t + 1 < nT) {
       T* tn = tp + K.step;
-      mm(tn + K.oMu, A, muf, h, 1, h, false, false, T(1), false);  // mu' = A mu_f
-      mm(t2, A, Sf, h, h, h, false, false, T(1), false);           // A S_f
+      mm<NT>(tn + K.oMu, A, muf, h, 1, h, false, false, T(1), false);  // mu' = A mu_f
+      mm<NT>(t2, A, Sf, h, h, h, false, false, T(1), false);           // A S_f
       __syncthreads();
-      mm(tn + K.oS, t2, A, h, h, h, false, true, T(1), false);     // (A S_f) A^T
+      mm<NT>(tn + K.oS, t2, A, h, h, h, false, true, T(1), false);     // (A S_f) A^T
       __syncthreads();
-      for (int64_t i = threadIdx.x; i < hh; i += (int)blockDim.x) tn[K.oS + i] += Sh[i];
+      for (int i = threadIdx.x; i < hh; i += NT) tn[K.oS + i] += Sh[i];
     }
     __syncthreads();
   }
@@ -274,10 +285,10 @@ __global__ void __launch_bounds__(NT, (NT == 128 ? 8 : NT == 64 ? 16 : 32)) k_ka
   T* gSh = g.shbar + seq * hh;
   T* gSv = g.svbar + seq * dd;
   T *aA = S_(11), *aB = S_(12), *aSh = S_(13), *aSv = S_(14), *sbn = S_(15), *mbn = V_(4);
-  for (int64_t i = threadIdx.x; i < hh; i += (int)blockDim.x) aA[i] = aSh[i] = sbn[i] = T(0);
-  for (int64_t i = threadIdx.x; i < hd; i += (int)blockDim.x) aB[i] = T(0);
-  for (int64_t i = threadIdx.x; i < dd; i += (int)blockDim.x) aSv[i] = T(0);
-  for (int i = threadIdx.x; i < h; i += (int)blockDim.x) mbn[i] = T(0);
+  for (int i = threadIdx.x; i < hh; i += NT) aA[i] = aSh[i] = sbn[i] = T(0);
+  for (int i = threadIdx.x; i < hd; i += NT) aB[i] = T(0);
+  for (int i = threadIdx.x; i < dd; i += NT) aSv[i] = T(0);
+  for (int i = threadIdx.x; i < h; i += NT) mbn[i] = T(0);
   __syncthreads();
   for (int t = nT - 1; t >= 0; --t) {
     const T* tp = tape + t * K.step;
@@ -289,86 +300,79 @@ __global__ void __launch_bounds__(NT, (NT == 128 ? 8 : NT == 64 ? 16 : 32)) k_ka
     T *sfb = S_(16), *q1b = S_(17), *kb = S_(18), *p1b = S_(19), *ib = S_(20), *sb = S_(21);
     T *yb = p1b, *xb = q1b, *lb = ib, *m1b = sfb;
     T *mufb = V_(5), *mub = V_(6), *eb = V_(7), *sv_ = V_(8);
-    cpy(S, tp + K.oS, hh);
-    cpy(mu, tp + K.oMu, h);
-    cpy(M1, tp + K.oM1, hd);
-    cpy(L, tp + K.oL, dd);
-    cpy(e, tp + K.oE, d);
-    cpy(z, tp + K.oZ, d);
-    cpy(Y, tp + K.oY, hd);
-    cpy(Kg, tp + K.oK, hd);
-    cpy(I, tp + K.oI, hh);
-    cpy(P1, tp + K.oP1, hh);
-    cpy(Q1, tp + K.oQ1, hd);
-    cpy(Sf, tp + K.oSf, hh);
-    cpy(muf, tp + K.oMuf, h);
+    cpy<NT>(S, tp + K.oS, hh);
+    cpy<NT>(mu, tp + K.oMu, h);
+    cpy<NT>(M1, tp + K.oM1, hd);
+    cpy<NT>(L, tp + K.oL, dd);
+    cpy<NT>(e, tp + K.oE, d);
+    cpy<NT>(z, tp + K.oZ, d);
+    cpy<NT>(Y, tp + K.oY, hd);
+    cpy<NT>(Kg, tp + K.oK, hd);
+    cpy<NT>(I, tp + K.oI, hh);
+    cpy<NT>(P1, tp + K.oP1, hh);
+    cpy<NT>(Q1, tp + K.oQ1, hd);
+    cpy<NT>(Sf, tp + K.oSf, hh);
+    cpy<NT>(muf, tp + K.oMuf, h);
     __syncthreads();
     if (t + 1 < nT) {  // S' = (A S_f) A^T + Sh,  mu' = A mu_f
-      for (int64_t i = threadIdx.x; i < hh; i += (int)blockDim.x) aSh[i] += sbn[i];
-      mm(t1, A, Sf, h, h, h, false, false, T(1), false);     // R1 = A S_f
-      mm(t2, sbn, A, h, h, h, false, false, T(1), false);    // R1bar = S'bar A
-      mm(mufb, A, mbn, h, 1, h, true, false, T(1), false);   // mu_f bar = A^T mu'bar
+      for (int i = threadIdx.x; i < hh; i += NT) aSh[i] += sbn[i];
+      mm<NT>(t1, A, Sf, h, h, h, false, false, T(1), false);     // R1 = A S_f
+      mm<NT>(t2, sbn, A, h, h, h, false, false, T(1), false);    // R1bar = S'bar A
+      mm<NT>(mufb, A, mbn, h, 1, h, true, false, T(1), false);   // mu_f bar = A^T mu'bar
       __syncthreads();
-      mm(aA, sbn, t1, h, h, h, true, false, T(1), true);     // Abar += S'bar^T R1
-      mm(sfb, A, t2, h, h, h, true, false, T(1), false);     // S_f bar = A^T R1bar
+      mm<NT>(aA, sbn, t1, h, h, h, true, false, T(1), true);     // Abar += S'bar^T R1
+      mm<NT>(sfb, A, t2, h, h, h, true, false, T(1), false);     // S_f bar = A^T R1bar
       __syncthreads();
-      mm(aA, t2, Sf, h, h, h, false, true, T(1), true);      // Abar += R1bar S_f^T
+      mm<NT>(aA, t2, Sf, h, h, h, false, true, T(1), true);      // Abar += R1bar S_f^T
       __syncthreads();
-      mm(aA, mbn, muf, h, h, 1, false, true, T(1), true);    // Abar += mu'bar mu_f^T
+      mm<NT>(aA, mbn, muf, h, h, 1, false, true, T(1), true);    // Abar += mu'bar mu_f^T
     } else {
-      for (int64_t i = threadIdx.x; i < hh; i += (int)blockDim.x) sfb[i] = T(0);
-      for (int i = threadIdx.x; i < h; i += (int)blockDim.x) mufb[i] = T(0);
+      for (int i = threadIdx.x; i < hh; i += NT) sfb[i] = T(0);
+      for (int i = threadIdx.x; i < h; i += NT) mufb[i] = T(0);
     }
     __syncthreads();
     // S_f = P1 I^T + (K Sv) K^T
-    mm(q1b, sfb, Kg, h, d, h, false, false, T(1), false);   // Q1bar = S_f bar K
-    mm(kb, sfb, Q1, h, d, h, true, false, T(1), false);     // Kbar = S_f bar^T Q1
-    mm(p1b, sfb, I, h, h, h, false, false, T(1), false);    // P1bar = S_f bar I
-    mm(ib, sfb, P1, h, h, h, true, false, T(1), false);     // Ibar = S_f bar^T P1
+    mm<NT>(q1b, sfb, Kg, h, d, h, false, false, T(1), false);   // Q1bar = S_f bar K
+    mm<NT>(kb, sfb, Q1, h, d, h, true, false, T(1), false);     // Kbar = S_f bar^T Q1
+    mm<NT>(p1b, sfb, I, h, h, h, false, false, T(1), false);    // P1bar = S_f bar I
+    mm<NT>(ib, sfb, P1, h, h, h, true, false, T(1), false);     // Ibar = S_f bar^T P1
     __syncthreads();
-    mm(kb, q1b, Sv, h, d, d, false, true, T(1), true);      // Kbar += Q1bar Sv^T
-    mm(aSv, Kg, q1b, d, d, h, true, false, T(1), true);     // Svbar += K^T Q1bar
-    mm(ib, p1b, S, h, h, h, false, true, T(1), true);       // Ibar += P1bar S^T
-    mm(sb, I, p1b, h, h, h, true, false, T(1), false);      // Sbar = I^T P1bar
+    mm<NT>(kb, q1b, Sv, h, d, d, false, true, T(1), true);      // Kbar += Q1bar Sv^T
+    mm<NT>(aSv, Kg, q1b, d, d, h, true, false, T(1), true);     // Svbar += K^T Q1bar
+    mm<NT>(ib, p1b, S, h, h, h, false, true, T(1), true);       // Ibar += P1bar S^T
+    mm<NT>(sb, I, p1b, h, h, h, true, false, T(1), false);      // Sbar = I^T P1bar
     __syncthreads();
     // I = Id - K B;  mu_f = mu + K e
-    mm(kb, ib, B, h, d, h, false, true, T(-1), true);       // Kbar -= Ibar B^T
-    mm(aB, Kg, ib, d, h, h, true, false, T(-1), true);      // Bbar -= K^T Ibar
-    cpy(mub, mufb, h);
-    mm(eb, Kg, mufb, d, 1, h, true, false, T(1), false);    // ebar = K^T mu_f bar
+    mm<NT>(kb, ib, B, h, d, h, false, true, T(-1), true);       // Kbar -= Ibar B^T
+    mm<NT>(aB, Kg, ib, d, h, h, true, false, T(-1), true);      // Bbar -= K^T Ibar
+    cpy<NT>(mub, mufb, h);
+    mm<NT>(eb, Kg, mufb, d, 1, h, true, false, T(1), false);    // ebar = K^T mu_f bar
     __syncthreads();
-    mm(kb, mufb, e, h, d, 1, false, true, T(1), true);      // Kbar += mu_f bar e^T
+    mm<NT>(kb, mufb, e, h, d, 1, false, true, T(1), true);      // Kbar += mu_f bar e^T
     __syncthreads();
     // K = Y L^-1: Ybar = Kbar L^-T, Lbar = -tril(K^T Ybar)
-    cpy(yb, kb, hd);
+    cpy<NT>(yb, kb, hd);
     __syncthreads();
-    rows_solve(yb, h, L, d, 0);
+    rows_solve<NT>(yb, h, L, d, 0);
     __syncthreads();
-    mm(lb, Kg, yb, d, d, h, true, false, T(-1), false);
+    mm<NT>(lb, Kg, yb, d, d, h, true, false, T(-1), false);
     // Y = X L^-T: Xbar = Ybar L^-1, Lbar += -tril(Xbar^T Y)
-    cpy(xb, yb, hd);
+    cpy<NT>(xb, yb, hd);
+    cpy<NT>(sv_, z, d);
     __syncthreads();
-    rows_solve(xb, h, L, d, 1);
+    // phi_t: zbar = z;  z = L^-1 e:  s = L^-T zbar (one more row of the solve)
+    rows_solve<NT>(xb, h, L, d, 1, sv_);
     __syncthreads();
-    mm(lb, xb, Y, d, d, h, true, false, T(-1), true);
+    mm<NT>(lb, xb, Y, d, d, h, true, false, T(-1), true);
     // X = S B^T
-    mm(sb, xb, B, h, h, d, false, false, T(1), true);       // Sbar += Xbar B
-    mm(aB, xb, S, d, h, h, true, false, T(1), true);        // Bbar += Xbar^T S
+    mm<NT>(sb, xb, B, h, h, d, false, false, T(1), true);       // Sbar += Xbar B
+    mm<NT>(aB, xb, S, d, h, h, true, false, T(1), true);        // Bbar += Xbar^T S
     __syncthreads();
-    if (threadIdx.x == 0) {
-      // phi_t: zbar = z;  z = L^-1 e:  s = L^-T zbar, ebar += s,
-      // Lbar += -tril(s z^T);  Lbar_ii += 1 / L_ii
-      T* s = sv_;
-      for (int j = d - 1; j >= 0; --j) {
-        T acc = z[j];
-        for (int k = j + 1; k < d; ++k) acc -= L[k * d + j] * s[k];
-        s[j] = acc / L[j * d + j];
-      }
-      for (int i = 0; i < d; ++i) eb[i] += s[i];
-    }
+    // ebar += s;  Lbar += -tril(s z^T);  Lbar_ii += 1 / L_ii
+    for (int i = threadIdx.x; i < d; i += NT) eb[i] += sv_[i];
     __syncthreads();
-    for (int64_t idx = threadIdx.x; idx < dd; idx += (int)blockDim.x) {
-      const int i = (int)(idx / d), j = (int)(idx - (int64_t)i * d);
+    for (int idx = threadIdx.x; idx < dd; idx += NT) {
+      const int i = idx / d, j = idx - i * d;
       if (j <= i) {
         T v = lb[idx] - sv_[i] * z[j];
         if (i == j) v += T(1) / L[i * d + i];
@@ -379,19 +383,19 @@ __global__ void __launch_bounds__(NT, (NT == 128 ? 8 : NT == 64 ? 16 : 32)) k_ka
     }
     // e = v - B mu
     if (g.obsbar)
-      for (int i = threadIdx.x; i < d; i += (int)blockDim.x) g.obsbar[(seq * nT + t) * (int64_t)d + i] = eb[i];
+      for (int i = threadIdx.x; i < d; i += NT) g.obsbar[(seq * nT + t) * (int64_t)d + i] = eb[i];
     __syncthreads();
-    mm(aB, eb, mu, d, h, 1, false, true, T(-1), true);      // Bbar -= ebar mu^T
-    mm(mub, B, eb, h, 1, d, true, false, T(-1), true);      // mubar -= B^T ebar
+    mm<NT>(aB, eb, mu, d, h, 1, false, true, T(-1), true);      // Bbar -= ebar mu^T
+    mm<NT>(mub, B, eb, h, 1, d, true, false, T(-1), true);      // mubar -= B^T ebar
     // L = chol(Svv):  Svvbar = 1/2 sym(L^-T copyltu(L^T Lbar) L^-1)  (dl/adjoints.hpp:175-191)
-    mm(t1, L, lb, d, d, d, true, false, T(1), false);       // L^T Lbar
+    mm<NT>(t1, L, lb, d, d, d, true, false, T(1), false);       // L^T Lbar
     __syncthreads();
-    for (int64_t idx = threadIdx.x; idx < dd; idx += (int)blockDim.x) {  // copyltu
-      const int i = (int)(idx / d), j = (int)(idx - (int64_t)i * d);
+    for (int idx = threadIdx.x; idx < dd; idx += NT) {  // copyltu
+      const int i = idx / d, j = idx - i * d;
       t2[idx] = j > i ? t1[j * d + i] : t1[idx];
     }
     __syncthreads();
-    for (int j = threadIdx.x; j < d; j += (int)blockDim.x) {  // column j: t2(:, j) <- L^-T t2(:, j)
+    for (int j = threadIdx.x; j < d; j += NT) {  // column j: t2(:, j) <- L^-T t2(:, j)
       for (int r = d - 1; r >= 0; --r) {
         T acc = t2[r * d + j];
         for (int k = r + 1; k < d; ++k) acc -= L[k * d + r] * t2[k * d + j];
@@ -399,30 +403,30 @@ __global__ void __launch_bounds__(NT, (NT == 128 ? 8 : NT == 64 ? 16 : 32)) k_ka
       }
     }
     __syncthreads();
-    rows_solve(t2, d, L, d, 1);                             // (.) L^-1
+    rows_solve<NT>(t2, d, L, d, 1);                             // (.) L^-1
     __syncthreads();
-    for (int64_t idx = threadIdx.x; idx < dd; idx += (int)blockDim.x) {  // 1/2, then exact symmetrization
-      const int i = (int)(idx / d), j = (int)(idx - (int64_t)i * d);
+    for (int idx = threadIdx.x; idx < dd; idx += NT) {  // 1/2, then exact symmetrization
+      const int i = idx / d, j = idx - i * d;
       t1[idx] = (T(0.5) * t2[idx] + T(0.5) * t2[j * d + i]) / T(2);
     }
     __syncthreads();
-    for (int64_t i = threadIdx.x; i < dd; i += (int)blockDim.x) aSv[i] += t1[i];
-    mm(m1b, t1, B, d, h, d, false, false, T(1), false);     // M1bar = Svvbar B
-    mm(aB, t1, M1, d, h, d, true, false, T(1), true);       // Bbar += Svvbar^T M1
+    for (int i = threadIdx.x; i < dd; i += NT) aSv[i] += t1[i];
+    mm<NT>(m1b, t1, B, d, h, d, false, false, T(1), false);     // M1bar = Svvbar B
+    mm<NT>(aB, t1, M1, d, h, d, true, false, T(1), true);       // Bbar += Svvbar^T M1
     __syncthreads();
-    mm(aB, m1b, S, d, h, h, false, true, T(1), true);       // Bbar += M1bar S^T
-    mm(sb, B, m1b, h, h, d, true, false, T(1), true);       // Sbar += B^T M1bar
+    mm<NT>(aB, m1b, S, d, h, h, false, true, T(1), true);       // Bbar += M1bar S^T
+    mm<NT>(sb, B, m1b, h, h, d, true, false, T(1), true);       // Sbar += B^T M1bar
     __syncthreads();
-    cpy(sbn, sb, hh);
-    cpy(mbn, mub, h);
+    cpy<NT>(sbn, sb, hh);
+    cpy<NT>(mbn, mub, h);
     __syncthreads();
   }
-  cpy(gA, aA, hh);
-  cpy(gB, aB, hd);
-  cpy(gSh, aSh, hh);
-  cpy(gSv, aSv, dd);
-  cpy(g.s0bar + seq * hh, sbn, hh);
-  cpy(g.mu0bar + seq * h, mbn, h);
+  cpy<NT>(gA, aA, hh);
+  cpy<NT>(gB, aB, hd);
+  cpy<NT>(gSh, aSh, hh);
+  cpy<NT>(gSv, aSv, dd);
+  cpy<NT>(g.s0bar + seq * hh, sbn, hh);
+  cpy<NT>(g.mu0bar + seq * h, mbn, h);
 }
 
 template <typename T>
@@ -477,7 +481,14 @@ dla_status kalman_fwdbwd(const Ctx& c, int64_t batch, int64_t h, int64_t d, int6
     ensure_smem_attr(kern, sm);
     kern<<<(unsigned)batch, threads, sm, c.stream>>>(g);
   };
-  if (nt == 32) go(k_kalman<T, 32>, 32);
+  static const bool spec = [] {
+    const char* e = getenv("DLA_KALMAN_SPECIALISE");  // tuning switch: 0 = runtime-size kernel only
+    return e ? atoi(e) != 0 : true;
+  }();
+  if (nt == 32 && spec && h == 8 && d == 8) go(k_kalman<T, 32, 8, 8>, 32);
+  else if (nt == 32 && spec && h == 4 && d == 4) go(k_kalman<T, 32, 4, 4>, 32);
+  else if (nt == 32 && spec && h == 8 && d == 4) go(k_kalman<T, 32, 8, 4>, 32);
+  else if (nt == 32) go(k_kalman<T, 32>, 32);
   else if (nt == 128) go(k_kalman<T, 128>, 128);
   else go(k_kalman<T, 64>, 64);
   DLAB_LAUNCH_CHECK();

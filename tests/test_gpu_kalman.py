@@ -115,3 +115,36 @@ def test_kalman_not_spd_and_shapes():
     with pytest.raises(L.ShapeError):  # blocks beyond the kernel's 32 x 32 design
         K.KalmanNLL(33, 2, 4).step(*[dev(x) for x in O.random_kalman(r, 33, 2, 4)[:6]],
                                     dev(np.zeros((1, 4, 2))))
+
+
+_GENERIC = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from oracle import oracle as O
+from paper_1710_08717_b200 import kalman as K
+h, d, T, B = (int(v) for v in sys.argv[2:6])
+m = O.random_kalman(O.rng(5), h, d, T, batch=B)
+dev = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in m]
+nll, grads, obsbar = K.KalmanNLL(h, d, T, B).step(*dev)
+np.savez(sys.argv[6], nll=nll.cpu().numpy(), obsbar=obsbar.cpu().numpy(),
+         **{k: v.cpu().numpy() for k, v in grads.items()})
+"""
+
+
+@pytest.mark.parametrize("h,d", [(8, 8), (4, 4), (8, 4)])
+def test_kalman_specialised_bitwise_equals_runtime_size_kernel(tmp_path, h, d):
+    # the compile-time-size kernels (k_kalman<T, 32, H, D>) keep the runtime-size
+    # kernel's operation order: results are bitwise identical
+    import subprocess
+    import sys
+    T, B = 30, 40
+    root = os.path.dirname(HERE)
+    outs = {}
+    for spec in ("0", "1"):
+        f = str(tmp_path / f"k{spec}.npz")
+        env = dict(os.environ, DLA_KALMAN_SPECIALISE=spec)
+        subprocess.run([sys.executable, "-c", _GENERIC, root, str(h), str(d), str(T), str(B), f], check=True,
+                       env=env, timeout=300)
+        outs[spec] = np.load(f)
+    for k in outs["0"].files:
+        assert np.array_equal(outs["0"][k], outs["1"][k]), k
