@@ -842,8 +842,19 @@ void early_inv_first(void* user, cudaStream_t crit) {
   T* tmp2 = tmp + B * (trtri_levels_tmp<T>(n) / sizeof(T));
   dla_status st = trtri_levels<T>(sc, B, h, wi, tmp2, &lv, false);
   MatB<T> t1{tmp, h, h * h};
+  // T1 runs beside the factorization's chain-bound second half: a grid of
+  // long-K tiles on every SM keeps the look-ahead updates and panel launches
+  // waiting for SMs (measured: a 100 us stall of the chain when T1 filled the
+  // GPU).  DLA_GP_EARLY_CTAS (tuning switch; 0 = unbounded) caps its
+  // persistent grid; the per-tile arithmetic is unchanged (bitwise the same).
+  static const int early_ctas = [] {
+    const char* v = getenv("DLA_GP_EARLY_CTAS");
+    return v ? atoi(v) : 0;
+  }();
+  Ctx tc = sc;
+  tc.gemm_ctas = early_ctas;
   if (st == DLA_OK)
-    st = gemm<T>(sc, B, h, h, h, T(1), MatB<const T>{e.l + h * n, n, n * n}, false, MatB<const T>{wi.p, n, n * n},
+    st = gemm<T>(tc, B, h, h, h, T(1), MatB<const T>{e.l + h * n, n, n * n}, false, MatB<const T>{wi.p, n, n * n},
                  false, T(0), t1, MASK_FULL, nullptr, TRI_NONE, TRI_LOWER);
   e.st = st;
 }
