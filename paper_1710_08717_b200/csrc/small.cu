@@ -200,6 +200,9 @@ __global__ void __launch_bounds__(256, MINB) k_potrf_warp(int n_, int64_t batch,
     return;
   }
   T* o = a.at(b, 0, 0);
+  // opaque copy of the slice base: otherwise the compiler keeps the 32 row
+  // addresses of the initial load sweep alive (spilled) for these stores
+  asm volatile("mov.b64 %0, %0;" : "+l"(o));
   if (!lower) {  // R(i, lane) = L(lane, i): straight from this lane's registers
 #pragma unroll
     for (int i = 0; i < WN; ++i)
