@@ -372,8 +372,13 @@ struct Bc<float> {
 // Column J of the row-per-lane Cholesky (dl/cholesky.hpp:35-72): the pivot
 // moves by one shuffle, the column's multipliers through a double-buffered
 // shared vector (one __syncwarp per column).
+// sink != nullptr: each finished multiplier r[J] is also stored to sink[J]
+// (the caller's shared-memory row) as its column completes, so callers that
+// only store L afterwards let the register die instead of carrying (and
+// spilling) the finished part of the row through the rest of the chain.
 template <typename T, int J>
-__device__ __forceinline__ void wchol_col(T (&r)[WCH], int lane, int n, T* buf, int& failed, T dcur) {
+__device__ __forceinline__ void wchol_col(T (&r)[WCH], int lane, int n, T* buf, int& failed, T dcur,
+                                          T* sink = nullptr) {
   if constexpr (J < WCH) {
     // dcur: pivot candidate formed from this lane's own multiplier at column
     // J-1 (see panel_cols): the serial chain is shuffle -> rsqrt -> mul -> FMA.
@@ -383,6 +388,7 @@ __device__ __forceinline__ void wchol_col(T (&r)[WCH], int lane, int n, T* buf, 
     const T rt = d * inv;
     const T l = (lane > J) ? r[J] * inv : (lane == J ? rt : r[J]);
     r[J] = l;
+    if (sink) sink[J] = l;
     T dnext = T(0);
     if constexpr (J + 1 < WCH) {
       dnext = r[J + 1] - l * l;
@@ -399,7 +405,7 @@ __device__ __forceinline__ void wchol_col(T (&r)[WCH], int lane, int n, T* buf, 
           if (k0 + u > J) r[k0 + u] -= l * v[u];
       }
     }
-    wchol_col<T, J + 1>(r, lane, n, buf, failed, dnext);
+    wchol_col<T, J + 1>(r, lane, n, buf, failed, dnext, sink);
   }
 }
 

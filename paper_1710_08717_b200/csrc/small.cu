@@ -194,28 +194,30 @@ __global__ void __launch_bounds__(256, MINB) k_potrf_warp(int n_, int64_t batch,
 #pragma unroll
   for (int c = 0; c < WN; ++c) r[c] = (lane < n && c <= lane) ? S[lane * WLD + c] : (c == lane ? T(1) : T(0));
   int failed = -1;
-  wchol_col<T, 0>(r, lane, n, buf, failed, r[0]);
+  // L's row `lane` lands in S's row `lane` column by column (no other lane
+  // reads S until the __syncwarp below)
+  wchol_col<T, 0>(r, lane, n, buf, failed, r[0], S + lane * WLD);
   if (failed >= 0) {
     if (lane == 0) record_failure(info, b, DLA_ERR_NOT_SPD, failed);
     return;
   }
   T* o = a.at(b, 0, 0);
-  // opaque copy of the slice base: otherwise the compiler keeps the 32 row
-  // addresses of the initial load sweep alive (spilled) for these stores
+  // opaque copies of the slice base and row stride: otherwise the compiler
+  // keeps the 32 row offsets of the initial load sweep alive (spilled) for
+  // these stores
   asm volatile("mov.b64 %0, %0;" : "+l"(o));
-  if (!lower) {  // R(i, lane) = L(lane, i): straight from this lane's registers
+  int ldo = ld;
+  asm volatile("mov.b32 %0, %0;" : "+r"(ldo));
+  if (!lower) {  // R(i, lane) = L(lane, i): this lane's own row of S
 #pragma unroll
     for (int i = 0; i < WN; ++i)
-      if (i < n && lane < n) o[i * ld + lane] = i <= lane ? r[i] : T(0);
+      if (i < n && lane < n) o[i * ldo + lane] = i <= lane ? S[lane * WLD + i] : T(0);
     return;
   }
-#pragma unroll
-  for (int c = 0; c < WN; ++c)
-    if (c < n && lane < n) S[lane * WLD + c] = r[c];
   __syncwarp();
 #pragma unroll
   for (int i = 0; i < WN; ++i)
-    if (i < n && lane < n) o[i * ld + lane] = lane <= i ? S[i * WLD + lane] : T(0);
+    if (i < n && lane < n) o[i * ldo + lane] = lane <= i ? S[i * WLD + lane] : T(0);
 }
 
 // Column `lane` of L^{-T} M held in registers, in unit-diagonal form: the
