@@ -40,6 +40,12 @@ L.gesvd(torch.randn(2, 40, 60, **f))
 # a plain product with >= 2 waves of 128 x 128 tiles: the TMA-fed GEMM (run the
 # whole script with DLA_GEMM_TMA=2 to put every product >= 256 on it)
 L.gemm2(torch.randn(1, 2560, 300, **f), torch.randn(1, 300, 2560, **f))
-torch.cuda.synchronize()
+# batched Kalman NLL + gradient: the compile-time-size kernels (h = d = 8, 4, 8 x 4) and the runtime-size one
+from paper_1710_08717_b200 import kalman as K  # noqa: E402
+for h, d, T, B in ((8, 8, 6, 3), (4, 4, 5, 2), (8, 4, 4, 2), (5, 3, 4, 2)):
+    m = O.random_kalman(O.rng(3), h, d, T, batch=B)
+    K.KalmanNLL(h, d, T, B).step(*[torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in m])
+# n = 32 forward, upper output (R = L^T from the lane's shared-memory row)
+L.potrf(torch.from_numpy(O.random_spd(32, r, batch=9)).cuda(), False)
 torch.cuda.synchronize()
 print("sanitize cases done")
