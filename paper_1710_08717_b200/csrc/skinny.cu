@@ -180,39 +180,49 @@ __global__ void __launch_bounds__(128) k_kskinny(SkinnyArgs<T> g, int64_t batch)
 // Full-square rank-k outer product with a triangle mask and beta == 0:
 // C = alpha P inside the mask, exact zeros outside (trsm pullback's
 // Tbar = -mask(S B^T), dl/adjoints.hpp:138-151, written in ONE pass instead of
-// a masked product + a zeroing sweep).  Thread per pair of columns, 16-byte
-// stores when rows are 16-byte aligned.
+// a masked product + a zeroing sweep).  A warp per row (slice and row from one
+// division per row, not per element), lanes over column pairs with 16-byte
+// stores when rows are 16-byte aligned; the row's k multipliers are loaded once.
 template <typename T, int K>
 __global__ void __launch_bounds__(256) k_outer_tri(SkinnyArgs<T> g, int64_t batch, bool vec) {
-  const int64_t pairs = (g.n + 1) / 2, per = g.m * pairs;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < batch * per; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = t / per, r = t - b * per;
-    const int64_t i = r / pairs, j = 2 * (r - i * pairs);
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = batch * g.m, pairs = (g.n + 1) / 2;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t row = w0; row < rows; row += ws) {
+    const int64_t b = row / g.m, i = row - b * g.m;
     if (slice_failed(g.skip, b)) continue;
     const T* A = g.a.p + b * g.a.bs;
     const T* B = g.b.p + b * g.b.bs;
-    T* C = g.c.p + b * g.c.bs + i * g.c.ld + j;
-    T v[2];
+    T* Crow = g.c.p + b * g.c.bs + i * g.c.ld;
+    T av[K];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int64_t jj = j + u;
-      const bool in = g.mask == MASK_LOWER ? jj <= i : (g.mask == MASK_UPPER ? jj >= i : true);
-      T acc = T(0);
-      if (in && jj < g.n) {
+    for (int k = 0; k < K; ++k) av[k] = k < g.k ? opa(g, A, i, k) : T(0);
+    for (int64_t p = lane; p < pairs; p += 32) {
+      const int64_t j = 2 * p;
+      T v[2];
 #pragma unroll
-        for (int k = 0; k < K; ++k)
-          if (k < g.k) acc += opa(g, A, i, k) * opb(g, B, k, jj);
+      for (int u = 0; u < 2; ++u) {
+        const int64_t jj = j + u;
+        const bool in = g.mask == MASK_LOWER ? jj <= i : (g.mask == MASK_UPPER ? jj >= i : true);
+        T acc = T(0);
+        if (in && jj < g.n) {
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+            if (k < g.k) acc += av[k] * opb(g, B, k, jj);
+        }
+        v[u] = in ? g.alpha * acc : T(0);
       }
-      v[u] = in ? g.alpha * acc : T(0);
-    }
-    if (vec && j + 1 < g.n) {
-      if constexpr (sizeof(T) == 8)
-        *reinterpret_cast<double2*>(C) = make_double2(v[0], v[1]);
-      else
-        *reinterpret_cast<float2*>(C) = make_float2(v[0], v[1]);
-    } else {
-      C[0] = v[0];
-      if (j + 1 < g.n) C[1] = v[1];
+      T* C = Crow + j;
+      if (vec && j + 1 < g.n) {
+        if constexpr (sizeof(T) == 8)
+          *reinterpret_cast<double2*>(C) = make_double2(v[0], v[1]);
+        else
+          *reinterpret_cast<float2*>(C) = make_float2(v[0], v[1]);
+      } else {
+        C[0] = v[0];
+        if (j + 1 < g.n) C[1] = v[1];
+      }
     }
   }
 }
@@ -384,7 +394,7 @@ bool outer_tri(const Ctx& c, int64_t batch, int64_t m, int64_t n, int64_t k, T a
   if (k > SK_NMAX || k < 1) return false;
   SkinnyArgs<T> g{m, n, k, alpha, T(0), a, b, cm, ta, tb, false, mask, skip};
   const bool vec = (cm.ld % 2 == 0) && (cm.bs % 2 == 0) && (reinterpret_cast<uintptr_t>(cm.p) % (2 * sizeof(T)) == 0);
-  const unsigned grid = blocks_for(batch * m * ((n + 1) / 2), 256, 148 * 16);
+  const unsigned grid = blocks_for(batch * m * 32, 256, 148 * 16);  // a warp per row
   if (k == 1)
     k_outer_tri<T, 1><<<grid, 256, 0, c.stream>>>(g, batch, vec);
   else
